@@ -1,0 +1,150 @@
+/* pk.h — C ABI of the B200-native ParallelKittens hot path (libpk.so).
+ *
+ * Plain pointers, sizes and opaque handles only (no torch types). Every call
+ * returns a pk_status; on failure pk_last_error() returns a thread-local
+ * message. Device work is enqueued on the caller's cudaStream_t (passed as
+ * void*) and is asynchronous; inputs are borrowed for the stream-ordered call.
+ *
+ * Reference interfaces replaced (all paths into /root/reference):
+ *   pk_comm_init / pk_comm_init_local  <- the simulated "devices" of one engine
+ *                                         (overlapsim/engine.py:169-197) and the
+ *                                         IPC/VMM/multicast setup FSMs
+ *                                         (overlapsim/memsim.py:205-341,
+ *                                         PAPER.md:796-859)
+ *   pk_pgl_alloc / pk_pgl_ptrs         <- allocate_pgl + attach_multicast
+ *                                         (memsim.py:145-149, 333-341)
+ *   pk_gemm                            <- the consumer role of LcscKernelSpec
+ *                                         (lcsc.py:45-86) at n = 1
+ *   pk_ag_gemm                         <- AgGemmPlan (workloads.py:553-609)
+ *   pk_gemm_rs                         <- GemmRsPlan (workloads.py:343-408)
+ *   pk_all_reduce                      <- primitives.all_reduce (primitives.py:237-261)
+ *                                         and GemmArPlan's communicator
+ *                                         (workloads.py:517-546)
+ *   pk_ring_attn_fwd                   <- RingAttentionPlan (workloads.py:616-716)
+ *   pk_moe_dispatch / pk_moe_combine   <- MoePlan (workloads.py:786-868); combine is new
+ *
+ * Status codes map onto the reference's exception classes in the Python
+ * layer: PK_ERR_INVALID -> WorkloadError (workloads.py:62),
+ * PK_ERR_CAPABILITY -> PrimitiveError (primitives.py:31),
+ * PK_ERR_PROTOCOL -> ProtocolViolation (memsim.py:26),
+ * PK_ERR_TIMEOUT -> DeadlockError (engine.py:35).
+ */
+#ifndef PK_H_
+#define PK_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PK_API __attribute__((visibility("default")))
+
+typedef enum {
+  PK_OK = 0,
+  PK_ERR_INVALID = 1,     /* shape / divisibility / argument error          */
+  PK_ERR_CAPABILITY = 2,  /* missing multicast / unsupported dtype / arch    */
+  PK_ERR_PROTOCOL = 3,    /* setup step out of order                         */
+  PK_ERR_TIMEOUT = 4,     /* a device-side wait() timed out (deadlock)       */
+  PK_ERR_CUDA = 5,        /* CUDA runtime / driver failure                   */
+  PK_ERR_NOMEM = 6
+} pk_status;
+
+typedef enum { PK_BF16 = 0, PK_F32 = 1, PK_F16 = 2, PK_I32 = 3, PK_I64 = 4, PK_U8 = 5 } pk_dtype;
+
+/* Schedule modes, as overlapsim.lcsc.ScheduleMode (lcsc.py:27-30). */
+typedef enum { PK_SCHED_AUTO = -1, PK_INTRA_SM = 0, PK_INTER_SM = 1, PK_HYBRID = 2 } pk_mode;
+
+typedef enum { PK_OP_SUM = 0, PK_OP_MAX = 1, PK_OP_MIN = 2 } pk_reduce_op;
+
+/* A strided device (or host, where stated) tensor view. */
+typedef struct {
+  void* ptr;
+  int32_t dtype;         /* pk_dtype */
+  int32_t ndim;          /* <= 4 */
+  int64_t shape[4];
+  int64_t strides[4];    /* in elements */
+} pk_tensor;
+
+/* Per-call schedule; NULL = automatic selection (LcscKernelSpec fields). */
+typedef struct {
+  int32_t mode;           /* pk_mode */
+  int32_t num_comm_sms;   /* communicator SMs when mode == PK_INTER_SM */
+  int32_t stages;         /* pipeline stages (informational; compiled per config) */
+  int32_t num_sms;        /* SMs the kernel may occupy (0 = all) */
+} pk_sched;
+
+typedef struct pk_comm pk_comm;   /* one rank's communicator */
+typedef struct pk_pgl pk_pgl;     /* one parallel global layout (symmetric buffer) */
+
+#define PK_PGL_MULTICAST 1u
+
+PK_API const char* pk_last_error(void);
+PK_API int pk_version(void);
+PK_API int pk_num_sms(int device, int* out);
+
+/* ---- communicators ------------------------------------------------------ */
+/* Multi-process: one process per GPU (torchrun). `uid` names the rendezvous
+ * (identical on all ranks); handles are exchanged as POSIX FDs over abstract
+ * Unix-domain sockets (SCM_RIGHTS). */
+PK_API int pk_comm_init(int rank, int world, int device, const char* uid, pk_comm** out);
+/* Single-process group: `world` ranks that share `device` (emulated peers:
+ * every rank's buffers live on the same GPU). comms_out has `world` slots. */
+PK_API int pk_comm_init_local(int world, int device, pk_comm** comms_out);
+PK_API int pk_comm_destroy(pk_comm* comm);
+PK_API int pk_comm_rank(const pk_comm* comm, int* rank, int* world);
+PK_API int pk_comm_has_multicast(const pk_comm* comm, int* out);
+/* Device-side timeout of every wait() in ns (default 10 s). */
+PK_API int pk_comm_set_timeout(pk_comm* comm, uint64_t ns);
+/* Read (and clear) the sticky device error flag: 1 = a wait() timed out. */
+PK_API int pk_comm_check(pk_comm* comm, int* timed_out);
+
+/* ---- parallel global layouts --------------------------------------------- */
+PK_API int pk_pgl_alloc(pk_comm* comm, size_t bytes, uint32_t flags, pk_pgl** out);
+/* local = this rank's buffer; peers[world] = every rank's buffer as seen by
+ * this rank (peers[rank] == local); mc = multicast VA or NULL. */
+PK_API int pk_pgl_ptrs(const pk_pgl* pgl, void** local, void** peers, void** mc);
+PK_API int pk_pgl_free(pk_pgl* pgl);
+
+/* ---- compute + communication ops --------------------------------------- */
+/* C[M,N] = A[M,K] . B[N,K]^T ; bf16 in, f32 accumulate, bf16 out. */
+PK_API int pk_gemm(const pk_tensor* a, const pk_tensor* b, pk_tensor* c,
+                   const pk_sched* sched, void* stream);
+
+/* AG-GEMM: C_r[M, N/n] = AllGather_rows(A_r[M/n, K]) . B_r[N/n, K]^T.
+ * a_gathered (nullable): if given, receives the rank-major gathered A[M,K]
+ * (the reference's `ag` layout, workloads.py:603-609). */
+PK_API int pk_ag_gemm(pk_comm* comm, const pk_tensor* a_shard, const pk_tensor* b,
+                      pk_tensor* c, pk_tensor* a_gathered, const pk_sched* sched, void* stream);
+
+/* GEMM-RS: out_r[M/n, N] = sum_d (A_d[M, K/n] . B_d[N, K/n]^T)[rows of r]. */
+PK_API int pk_gemm_rs(pk_comm* comm, const pk_tensor* a, const pk_tensor* b,
+                      pk_tensor* out, const pk_sched* sched, void* stream);
+
+/* In-place all-reduce of x (bf16 or f32, contiguous) over all ranks. */
+PK_API int pk_all_reduce(pk_comm* comm, pk_tensor* x, int op, const pk_sched* sched, void* stream);
+
+/* Ring attention forward (non-causal): q,k,v,o [B, S/n, H, D] bf16 local
+ * shards; lse [B, H, S/n] f32. KV rotates d -> d+1 (workloads.py:666-681). */
+PK_API int pk_ring_attn_fwd(pk_comm* comm, const pk_tensor* q, const pk_tensor* k,
+                            const pk_tensor* v, pk_tensor* o, pk_tensor* lse, float softmax_scale,
+                            const pk_sched* sched, void* stream);
+
+/* Expert-parallel dispatch: x [T, H] bf16, topk_idx [T, k] int32 (expert ids);
+ * expert e lives on rank e % n (workloads.py:802). Tokens are placed on their
+ * owner in slots sorted by (src_rank, token, k) (workloads.py:821-832).
+ * recv [cap, H] bf16 receives rows; recv_src [cap] int32 (src*T*k + tok*k + j)
+ * and *recv_count (device int32) describe them. */
+PK_API int pk_moe_dispatch(pk_comm* comm, const pk_tensor* x, const pk_tensor* topk_idx,
+                           int num_experts, pk_tensor* recv, pk_tensor* recv_src,
+                           pk_tensor* recv_count, void* stream);
+/* Combine: y [cap, H] rows produced by the owner for its received slots are
+ * sent back and summed with weights w [T, k] f32 into out [T, H] bf16. */
+PK_API int pk_moe_combine(pk_comm* comm, const pk_tensor* y, const pk_tensor* topk_idx,
+                          const pk_tensor* w, int num_experts, pk_tensor* out, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PK_H_ */

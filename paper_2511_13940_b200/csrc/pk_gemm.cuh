@@ -1,0 +1,398 @@
+// pk_gemm.cuh — the LCSC (load / compute / store / communicate) kernel template
+// for sm_100a: a persistent, warp-specialised tcgen05 GEMM whose loader can
+// pull A tiles from peer GPUs and whose storer can push (or reduce-add) C
+// tiles into peer GPUs, with optional dedicated communicator CTAs.
+//
+// Reference mapping:
+//   * LCSC roles loader/storer/consumer/communicator — PAPER.md:685-732,
+//     overlapsim/lcsc.py:16-76 (ROLES, LcscKernelSpec: num_comm_sms, stages,
+//     tile 128x128x64 there; 256x256x64 per CTA pair here).
+//   * AG-GEMM tile sources (rank-major gathered rows) — workloads.py:562-609.
+//   * GEMM-RS owner = row_block // (M/n), store_add_async of each tile into
+//     the owner — workloads.py:374-395.
+//   * signal / wait on per-rank counters — primitives.py:264-306.
+//
+// Roles (one CTA per SM, persistent; CTA pairs when CG == 2):
+//   warp 0        loader  : TMA A/B tiles into a STAGES-deep smem ring
+//   warp 1        consumer: one elected thread issues tcgen05.mma into TMEM
+//   warp 2        TMEM allocator
+//   warp 3        (idle)  : reserved
+//   warps 4..7    storer  : TMEM -> regs -> bf16 -> swizzled smem -> TMA
+//                           store / TMA reduce-add (local or peer VA)
+//   comm CTAs     communicator: bulk-copy peer A shards into the local
+//                           gathered buffer and publish per-block flags
+#pragma once
+#include "pk_ptx.cuh"
+
+namespace pk {
+
+constexpr int kMaxRanksDev = 8;
+constexpr int BLOCK_K = 64;                 // 64 bf16 = one 128 B swizzle atom
+constexpr int UMMA_K = 16;
+constexpr int EPI_COLS = 64;                // epilogue chunk = 64 cols = 128 B rows
+constexpr int kNumThreads = 256;
+constexpr int kEpiWarp0 = 4;
+
+enum EpiMode : int { EPI_STORE = 0, EPI_REDUCE_ADD = 1 };
+
+// Cross-rank sync state for one fused call (all pointers are device VAs).
+struct SyncArgs {
+  uint32_t* ready_local;                  // [n]: ready_local[s] bumped by rank s when its inputs are ready
+  uint32_t* ready_peer[kMaxRanksDev];        // ready_local of every rank (peer VAs)
+  uint32_t* done_local;                   // [n]: done_local[s] bumped by rank s CTAs when they finished touching my buffers
+  uint32_t* done_peer[kMaxRanksDev];
+  uint32_t* flags;                        // [num_m_tiles] local per-m-tile "rows landed" flags (inter-SM AG)
+  uint32_t* err;                          // timeout flag
+  uint32_t epoch;                         // this call's epoch (>= 1): value published in flags
+  uint32_t ready_expect;                  // cumulative ready count expected from every rank
+  uint32_t done_expect;                   // cumulative done count expected from every rank
+  uint64_t timeout_ns;
+};
+
+struct GemmArgs {
+  CUtensorMap tmap_a[kMaxRanksDev];          // A row sources
+  CUtensorMap tmap_b;                     // B^T [N, K] (K-major)
+  CUtensorMap tmap_c[kMaxRanksDev];          // C destinations
+  int M, N, K;
+  int rank, world;
+  int a_rows_per_src;                     // rows of the global M covered by each A source
+  int a_nsrc;                             // number of A sources (1 = plain)
+  int a_base[kMaxRanksDev];                  // row offset inside source map s
+  int a_wait_flag[kMaxRanksDev];             // 1: wait flags[m_tile] before loading rows of source s
+  int c_rows_per_dst;                     // rows of global M per C destination
+  int c_ndst;
+  int m_rot;                              // tile-order rotation along M (in M tiles)
+  int num_compute_clusters;               // clusters that run GEMM tiles
+  int sync_ready_before_load;             // AG intra-SM: wait ready[s] before loading peer rows
+  int sync_ready_before_store;            // RS: wait ready[owner] before the first reduce-add
+  int sync_done_signal;                   // signal done to peers at the end (RS / AG intra)
+  // communicator (inter-SM all-gather): copy peer shards into a_gathered
+  uint8_t* comm_src[kMaxRanksDev];           // shard base of every rank (peer VAs)
+  uint8_t* comm_dst;                      // local gathered buffer [M, K]
+  long long comm_shard_bytes;             // bytes per shard (= rows_per_src * K * 2)
+  int comm_copy_local;                    // also copy the local shard into the gathered buffer
+  SyncArgs sync;
+};
+
+template <int CG, int BN>
+struct GemmCfg {
+  static constexpr int BM = 128;                       // rows per CTA
+  static constexpr int UMMA_M = BM * CG;               // 128 or 256
+  static constexpr int UMMA_N = BN;
+  static constexpr int TILE_M = BM * CG;               // rows per cluster tile
+  static constexpr int B_ROWS = BN / CG;               // B rows loaded per CTA
+  static constexpr int A_BYTES = BM * BLOCK_K * 2;
+  static constexpr int B_BYTES = B_ROWS * BLOCK_K * 2;
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int STAGES = (CG == 2) ? 6 : 4;
+  static constexpr int EPI_BUF_BYTES = 32 * EPI_COLS * 2;          // per warp per buffer: 4 KB
+  static constexpr int EPI_BYTES = 4 * 2 * EPI_BUF_BYTES;           // 4 warps, double buffered
+  static constexpr int TMEM_COLS = 2 * BN;                          // double-buffered accumulator
+  static constexpr int BAR_BYTES = 256;
+  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + EPI_BYTES + BAR_BYTES + 1024;  // +1024 align slack
+  static_assert(TMEM_COLS <= 512, "TMEM overflow");
+  static_assert(SMEM_BYTES <= 232448, "smem overflow");
+};
+
+// Tile order: grouped raster along M (GROUP tiles) for L2 reuse of B, then
+// rotated along M so rank r starts on its own / its neighbour's rows.
+PK_DEV void tile_coords(int t, int num_m, int num_n, int m_rot, int& mt, int& nt) {
+  constexpr int GROUP = 8;
+  const int per_group = GROUP * num_n;
+  const int g = t / per_group;
+  const int first_m = g * GROUP;
+  const int gsize = min(num_m - first_m, GROUP);
+  const int r = t - g * per_group;
+  mt = first_m + r % gsize;
+  nt = r / gsize;
+  mt = (mt + m_rot) % num_m;
+}
+
+template <int CG, int BN, int EPI>
+__global__ void __launch_bounds__(kNumThreads, 1)
+lcsc_gemm_kernel(const __grid_constant__ GemmArgs args) {
+  using Cfg = GemmCfg<CG, BN>;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smem_a = smem;
+  uint8_t* smem_b = smem + Cfg::STAGES * Cfg::A_BYTES;
+  uint8_t* smem_epi = smem + Cfg::STAGES * Cfg::STAGE_BYTES;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem_epi + Cfg::EPI_BYTES);
+  uint64_t* full_bar = bars;                         // [STAGES]
+  uint64_t* empty_bar = bars + Cfg::STAGES;          // [STAGES]
+  uint64_t* tfull_bar = bars + 2 * Cfg::STAGES;      // [2]
+  uint64_t* tempty_bar = bars + 2 * Cfg::STAGES + 2; // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * Cfg::STAGES + 4);
+
+  const uint32_t warp = warp_id_sync();
+  const uint32_t lane = lane_id();
+  const uint32_t cta_rank = (CG == 2) ? cluster_ctarank() : 0;
+  const bool leader = (cta_rank == 0);
+  const int cluster = (CG == 2) ? (int)cluster_id_x() : (int)blockIdx.x;
+  const bool is_comm = cluster >= args.num_compute_clusters;
+
+  const int num_m = args.M / Cfg::TILE_M;
+  const int num_n = args.N / BN;
+  const int num_tiles = num_m * num_n;
+  const int num_kb = args.K / BLOCK_K;
+
+  // ------------------------------------------------------------ one-time setup
+  if (warp == 0 && lane == 0) {
+    for (int s = 0; s < Cfg::STAGES; ++s) {
+      mbar_init(&full_bar[s], 1);
+      mbar_init(&empty_bar[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull_bar[a], 1);
+      mbar_init(&tempty_bar[a], 4 * CG);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 2 && !is_comm) tmem_alloc<Cfg::TMEM_COLS, CG>(tmem_slot);
+  if (warp == 1 && lane == 0) {
+    prefetch_tmap(&args.tmap_b);
+    for (int s = 0; s < args.a_nsrc; ++s) prefetch_tmap(&args.tmap_a[s]);
+  }
+  // Inputs-ready announcement: one thread of the first CTA bumps ready[rank] on
+  // every rank (signal(), primitives.py:264-272); the stream order guarantees
+  // this rank's inputs/zeroed outputs are in place when the kernel runs.
+  if (args.sync.ready_local != nullptr && blockIdx.x == 0 && threadIdx.x == 0) {
+    __threadfence_system();
+    for (int d = 0; d < args.world; ++d) signal_add(args.sync.ready_peer[d] + args.rank, 1u);
+  }
+  tc_fence_before();
+  if constexpr (CG == 2) cluster_sync(); else __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (is_comm) {
+    // ========================================================= communicator
+    // Inter-SM all-gather: copy every shard (peer VA -> smem ring -> local
+    // gathered buffer) in TILE_M-row chunks and publish flags[m_tile] per
+    // chunk. One elected thread per CTA drives the bulk-copy engine (TMA
+    // needs ~15 SMs to saturate NVLink).
+    if (warp == 0) {
+      const int ncomm = (int)(gridDim.x / CG) - args.num_compute_clusters;
+      const int cidx = cluster - args.num_compute_clusters;
+      const int comm_ctas = ncomm * CG;
+      const int me = cidx * CG + (int)cta_rank;
+      const long long chunk_bytes = (long long)Cfg::TILE_M * args.K * 2;
+      const int chunks_per_shard = args.a_rows_per_src / Cfg::TILE_M;
+      const int total_chunks = args.world * chunks_per_shard;
+      constexpr int PIECE = 32768;
+      constexpr int NBUF = (Cfg::STAGES * Cfg::STAGE_BYTES) / PIECE < Cfg::STAGES
+                               ? (Cfg::STAGES * Cfg::STAGE_BYTES) / PIECE : Cfg::STAGES;
+      uint32_t phase_bits = 0;
+      int buf = 0;
+      bool failed = false;
+      for (int i = 0; i < total_chunks && !failed; ++i) {
+        const int sidx = i / chunks_per_shard;                  // right neighbour first, local last
+        const int src = (args.rank + 1 + sidx) % args.world;
+        const int j = i % chunks_per_shard;
+        const int mt = (src * args.a_rows_per_src) / Cfg::TILE_M + j;
+        if ((mt % comm_ctas) != me) continue;
+        if (src == args.rank && !args.comm_copy_local) continue;
+        if (src != args.rank && args.sync.ready_local != nullptr) {
+          if (!wait_geq(args.sync.ready_local + src, args.sync.ready_expect, args.sync.err, args.sync.timeout_ns)) {
+            failed = true;
+            break;
+          }
+        }
+        const uint8_t* s = args.comm_src[src] + (long long)j * chunk_bytes;
+        uint8_t* d = args.comm_dst + (long long)mt * chunk_bytes;
+        for (long long off = 0; off < chunk_bytes; off += PIECE) {
+          const uint32_t bytes = (uint32_t)min((long long)PIECE, chunk_bytes - off);
+          uint8_t* sb = smem + buf * PIECE;
+          uint64_t* bar = &full_bar[buf];
+          if (lane == 0) {
+            bulk_wait_read<NBUF - 1>();        // the store issued NBUF pieces ago has drained this buffer
+            mbar_arrive_expect_tx(bar, bytes);
+            bulk_g2s(sb, s + off, bytes, bar);
+          }
+          __syncwarp();
+          mbar_wait(bar, (phase_bits >> buf) & 1);
+          phase_bits ^= 1u << buf;
+          if (lane == 0) {
+            bulk_s2g(d + off, sb, bytes);
+            bulk_commit();
+          }
+          __syncwarp();
+          buf = (buf + 1 == NBUF) ? 0 : buf + 1;
+        }
+        if (lane == 0) {
+          bulk_wait<0>();
+          fence_async_global();
+          __threadfence();
+          asm volatile("st.release.gpu.global.u32 [%0], %1;" :: "l"(args.sync.flags + mt), "r"(args.sync.epoch) : "memory");
+        }
+        __syncwarp();
+      }
+      if (lane == 0) bulk_wait<0>();
+      __syncwarp();
+    }
+  } else if (warp == 0) {
+    // ========================================================= loader
+    int stage = 0;
+    uint32_t phase = 0;
+    uint32_t peers_ready = 0;
+    for (int t = cluster; t < num_tiles; t += args.num_compute_clusters) {
+      int mt, nt;
+      tile_coords(t, num_m, num_n, args.m_rot, mt, nt);
+      const int m_row = mt * Cfg::TILE_M + (int)cta_rank * Cfg::BM;
+      const int src = (args.a_nsrc > 1) ? (mt * Cfg::TILE_M) / args.a_rows_per_src : 0;
+      const int a_row = args.a_base[src] + m_row - src * args.a_rows_per_src;
+      const int b_row = nt * BN + (int)cta_rank * Cfg::B_ROWS;
+      if (args.a_wait_flag[src]) {
+        wait_geq(args.sync.flags + mt, args.sync.epoch, args.sync.err, args.sync.timeout_ns);
+        fence_async_global();
+      }
+      if (args.sync_ready_before_load && !((peers_ready >> src) & 1)) {
+        wait_geq(args.sync.ready_local + src, args.sync.ready_expect, args.sync.err, args.sync.timeout_ns);
+        fence_async_global();
+        peers_ready |= 1u << src;
+      }
+      for (int kb = 0; kb < num_kb; ++kb) {
+        mbar_wait(&empty_bar[stage], phase ^ 1);
+        uint8_t* sa = smem_a + stage * Cfg::A_BYTES;
+        uint8_t* sb = smem_b + stage * Cfg::B_BYTES;
+        if (elect_one()) {
+          if constexpr (CG == 1) {
+            mbar_arrive_expect_tx(&full_bar[stage], Cfg::STAGE_BYTES);
+            tma_load_2d(&args.tmap_a[src], &full_bar[stage], sa, kb * BLOCK_K, a_row);
+            tma_load_2d(&args.tmap_b, &full_bar[stage], sb, kb * BLOCK_K, b_row);
+          } else {
+            if (leader) mbar_arrive_expect_tx(&full_bar[stage], 2 * Cfg::STAGE_BYTES);
+            tma_load_2d_2sm(&args.tmap_a[src], &full_bar[stage], sa, kb * BLOCK_K, a_row);
+            tma_load_2d_2sm(&args.tmap_b, &full_bar[stage], sb, kb * BLOCK_K, b_row);
+          }
+        }
+        __syncwarp();
+        if (++stage == Cfg::STAGES) { stage = 0; phase ^= 1; }
+      }
+    }
+  } else if (warp == 1) {
+    // ========================================================= consumer (MMA)
+    if (leader) {
+      constexpr uint32_t idesc = idesc_bf16_f32(Cfg::UMMA_M, Cfg::UMMA_N);
+      int stage = 0;
+      uint32_t phase = 0;
+      int it = 0;
+      for (int t = cluster; t < num_tiles; t += args.num_compute_clusters, ++it) {
+        const int acc = it & 1;
+        const uint32_t acc_phase = (it >> 1) & 1;
+        mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * BN;
+        for (int kb = 0; kb < num_kb; ++kb) {
+          mbar_wait(&full_bar[stage], phase);
+          tc_fence_after();
+          if (elect_one()) {
+            const uint32_t a_addr = smem_u32(smem_a + stage * Cfg::A_BYTES);
+            const uint32_t b_addr = smem_u32(smem_b + stage * Cfg::B_BYTES);
+            const uint64_t a_desc = sdesc_kmajor_sw128(a_addr);
+            const uint64_t b_desc = sdesc_kmajor_sw128(b_addr);
+#pragma unroll
+            for (int k = 0; k < BLOCK_K / UMMA_K; ++k) {
+              // advance 16 elements = 32 B along K inside the swizzle atom
+              umma_f16<CG>(d_tmem, a_desc + (uint64_t)(k * 2), b_desc + (uint64_t)(k * 2), idesc,
+                           (kb | k) != 0 ? 1u : 0u);
+            }
+            umma_commit<CG>(&empty_bar[stage]);
+            if (kb == num_kb - 1) umma_commit<CG>(&tfull_bar[acc]);
+          }
+          __syncwarp();
+          if (++stage == Cfg::STAGES) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp >= kEpiWarp0) {
+    // ========================================================= storer (epilogue)
+    const int q = (int)warp - kEpiWarp0;             // TMEM lane quarter
+    uint8_t* ebuf = smem_epi + q * 2 * Cfg::EPI_BUF_BYTES;
+    int it = 0;
+    int ebuf_idx = 0;
+    uint32_t owners_ready = 0;
+    for (int t = cluster; t < num_tiles; t += args.num_compute_clusters, ++it) {
+      int mt, nt;
+      tile_coords(t, num_m, num_n, args.m_rot, mt, nt);
+      const int acc = it & 1;
+      const uint32_t acc_phase = (it >> 1) & 1;
+      const int row0 = mt * Cfg::TILE_M + (int)cta_rank * Cfg::BM + q * 32;   // global M row of lane 0
+      const int dst = (args.c_ndst > 1) ? row0 / args.c_rows_per_dst : 0;
+      const int c_row = row0 - dst * args.c_rows_per_dst;
+      if (EPI == EPI_REDUCE_ADD && args.sync_ready_before_store && !((owners_ready >> dst) & 1)) {
+        if (lane == 0) wait_geq(args.sync.ready_local + dst, args.sync.ready_expect, args.sync.err, args.sync.timeout_ns);
+        __syncwarp();
+        owners_ready |= 1u << dst;
+      }
+      mbar_wait(&tfull_bar[acc], acc_phase);
+      tc_fence_after();
+      const uint32_t t_lane = (uint32_t)(q * 32) << 16;
+#pragma unroll 1
+      for (int c = 0; c < BN / EPI_COLS; ++c) {
+        uint32_t v0[32], v1[32];
+        const uint32_t taddr = tmem_base + t_lane + (uint32_t)(acc * BN + c * EPI_COLS);
+        tmem_ld_32x32b_x32(taddr, v0);
+        tmem_ld_32x32b_x32(taddr + 32, v1);
+        tmem_ld_wait();
+        if (c == BN / EPI_COLS - 1) {
+          // all TMEM columns of this accumulator are in registers: release it
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) {
+            if constexpr (CG == 1) mbar_arrive(&tempty_bar[acc]);
+            else mbar_arrive_cluster(&tempty_bar[acc], 0);
+          }
+        }
+        // buffer reuse guard: the store issued two chunks ago must have read smem
+        if (lane == 0) bulk_wait_read<1>();
+        __syncwarp();
+        uint8_t* buf = ebuf + ebuf_idx * Cfg::EPI_BUF_BYTES;
+        const uint32_t row_addr = smem_u32(buf) + lane * 128;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const uint32_t* src = (j < 4) ? &v0[j * 8] : &v1[(j - 4) * 8];
+          const uint32_t p0 = pack_bf16x2(__uint_as_float(src[0]), __uint_as_float(src[1]));
+          const uint32_t p1 = pack_bf16x2(__uint_as_float(src[2]), __uint_as_float(src[3]));
+          const uint32_t p2 = pack_bf16x2(__uint_as_float(src[4]), __uint_as_float(src[5]));
+          const uint32_t p3 = pack_bf16x2(__uint_as_float(src[6]), __uint_as_float(src[7]));
+          st_shared_v4(row_addr + ((j ^ (lane & 7)) << 4), p0, p1, p2, p3);
+        }
+        fence_async_shared();
+        __syncwarp();
+        if (lane == 0) {
+          const int col = nt * BN + c * EPI_COLS;
+          if constexpr (EPI == EPI_STORE) tma_store_2d(&args.tmap_c[dst], buf, col, c_row);
+          else tma_reduce_add_2d(&args.tmap_c[dst], buf, col, c_row);
+          bulk_commit();
+        }
+        ebuf_idx ^= 1;
+      }
+    }
+    if (lane == 0) bulk_wait<0>();
+    __syncwarp();
+    // Done announcement: after this CTA's last reduce-add landed, bump
+    // done[rank] on every peer (one per epilogue warp).
+    if (args.sync_done_signal && lane == 0) {
+      fence_async_global();
+      __threadfence_system();
+      for (int d = 0; d < args.world; ++d) signal_add(args.sync.done_peer[d] + args.rank, 1u);
+    }
+  }
+
+  // ------------------------------------------------------------ teardown
+  tc_fence_before();
+  if constexpr (CG == 2) cluster_sync(); else __syncthreads();
+  if (warp == 2 && !is_comm) {
+    tc_fence_after();
+    tmem_dealloc<Cfg::TMEM_COLS, CG>(tmem_base);
+  }
+  // Completion wait: block 0 waits until every rank has finished touching this
+  // rank's buffers, so the caller may reuse them once the kernel returns.
+  if (args.sync_done_signal && blockIdx.x == 0 && threadIdx.x == 0) {
+    for (int s = 0; s < args.world; ++s)
+      wait_geq(args.sync.done_local + s, args.sync.done_expect, args.sync.err, args.sync.timeout_ns);
+  }
+}
+
+}  // namespace pk

@@ -1,0 +1,120 @@
+// pk_host.cu — errors, runtime-resolved driver API, tensor-map encoding.
+#include "pk_host.h"
+#include <cstdarg>
+#include <mutex>
+
+namespace pk {
+
+static thread_local std::string g_last_error;
+
+void set_error(const char* fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_last_error = buf;
+}
+
+int fail(int code, const char* fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_last_error = buf;
+  return code;
+}
+
+template <typename F>
+static bool resolve(const char* name, F* fn) {
+  void* p = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  if (cudaGetDriverEntryPoint(name, &p, cudaEnableDefault, &q) != cudaSuccess || q != cudaDriverEntryPointSuccess || !p) {
+    *fn = nullptr;
+    return false;
+  }
+  *fn = reinterpret_cast<F>(p);
+  return true;
+}
+
+int driver(const Driver** out) {
+  static Driver d;
+  static std::once_flag once;
+  static bool okay = false;
+  std::call_once(once, [] {
+    bool ok = true;
+    ok &= resolve("cuTensorMapEncodeTiled", &d.tensorMapEncodeTiled);
+    ok &= resolve("cuMemCreate", &d.memCreate);
+    ok &= resolve("cuMemRelease", &d.memRelease);
+    ok &= resolve("cuMemAddressReserve", &d.memAddressReserve);
+    ok &= resolve("cuMemAddressFree", &d.memAddressFree);
+    ok &= resolve("cuMemMap", &d.memMap);
+    ok &= resolve("cuMemUnmap", &d.memUnmap);
+    ok &= resolve("cuMemSetAccess", &d.memSetAccess);
+    ok &= resolve("cuMemGetAllocationGranularity", &d.memGetAllocationGranularity);
+    ok &= resolve("cuMemExportToShareableHandle", &d.memExportToShareableHandle);
+    ok &= resolve("cuMemImportFromShareableHandle", &d.memImportFromShareableHandle);
+    ok &= resolve("cuDeviceGetAttribute", &d.deviceGetAttribute);
+    ok &= resolve("cuDeviceGet", &d.deviceGet);
+    // multicast entry points are optional (absent -> no NVLS)
+    resolve("cuMulticastCreate", &d.multicastCreate);
+    resolve("cuMulticastAddDevice", &d.multicastAddDevice);
+    resolve("cuMulticastBindMem", &d.multicastBindMem);
+    resolve("cuMulticastUnbind", &d.multicastUnbind);
+    resolve("cuMulticastGetGranularity", &d.multicastGetGranularity);
+    d.ok = ok;
+    okay = ok;
+  });
+  if (!okay) return fail(PK_ERR_CUDA, "CUDA driver entry points unavailable (no GPU driver?)");
+  *out = &d;
+  return PK_OK;
+}
+
+int check_matrix(const pk_tensor* t, const char* name, int dtype, int64_t* rows, int64_t* cols, int64_t* ld) {
+  if (t == nullptr || t->ptr == nullptr) return fail(PK_ERR_INVALID, "%s: null tensor", name);
+  if (t->dtype != dtype) return fail(PK_ERR_INVALID, "%s: dtype %d, expected %d", name, t->dtype, dtype);
+  if (t->ndim != 2) return fail(PK_ERR_INVALID, "%s: expected 2-D, got %d-D", name, t->ndim);
+  if (t->strides[1] != 1) return fail(PK_ERR_INVALID, "%s: inner dimension must be contiguous", name);
+  *rows = t->shape[0];
+  *cols = t->shape[1];
+  *ld = t->strides[0];
+  if (*ld < *cols) return fail(PK_ERR_INVALID, "%s: row stride %lld < cols %lld", name, (long long)*ld, (long long)*cols);
+  const int eb = dtype_bytes(dtype);
+  if (((*ld) * eb) % 16 != 0 || (reinterpret_cast<uintptr_t>(t->ptr) % 16) != 0)
+    return fail(PK_ERR_INVALID, "%s: rows must be 16-byte aligned", name);
+  return PK_OK;
+}
+
+int make_tmap_2d(CUtensorMap* map, const void* ptr, CUtensorMapDataType dt, int elem_bytes,
+                 int64_t rows, int64_t cols, int64_t ld, int box_rows, int box_cols,
+                 CUtensorMapSwizzle swz) {
+  const Driver* d;
+  PK_TRY(driver(&d));
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)(ld * elem_bytes)};
+  cuuint32_t box[2] = {(cuuint32_t)box_cols, (cuuint32_t)box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = d->tensorMapEncodeTiled(map, dt, 2, const_cast<void*>(ptr), dims, strides, box, estr,
+                                       CU_TENSOR_MAP_INTERLEAVE_NONE, swz,
+                                       CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    return fail(PK_ERR_INVALID, "cuTensorMapEncodeTiled failed (%d): rows=%lld cols=%lld ld=%lld box=%dx%d",
+                (int)r, (long long)rows, (long long)cols, (long long)ld, box_rows, box_cols);
+  return PK_OK;
+}
+
+}  // namespace pk
+
+extern "C" {
+
+PK_API const char* pk_last_error(void) { return pk::g_last_error.c_str(); }
+PK_API int pk_version(void) { return 100; }
+PK_API int pk_num_sms(int device, int* out) {
+  int v = 0;
+  PK_CUDA(cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, device));
+  *out = v;
+  return PK_OK;
+}
+
+}  // extern "C"

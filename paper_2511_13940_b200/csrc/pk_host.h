@@ -1,0 +1,140 @@
+// pk_host.h — host-side internals shared by the libpk translation units:
+// error reporting, driver entry points (resolved at runtime through cudart so
+// the library loads on machines without libcuda), tensor-map encoding, and
+// the communicator / PGL structs.
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cstdint>
+#include <cstdio>
+#include <string>
+#include <vector>
+#include "../../include/pk.h"
+
+namespace pk {
+
+void set_error(const char* fmt, ...);
+int fail(int code, const char* fmt, ...);
+
+#define PK_CUDA(expr)                                                               \
+  do {                                                                              \
+    cudaError_t _e = (expr);                                                        \
+    if (_e != cudaSuccess)                                                          \
+      return ::pk::fail(PK_ERR_CUDA, "%s failed: %s (%s:%d)", #expr,                \
+                        cudaGetErrorString(_e), __FILE__, __LINE__);                \
+  } while (0)
+
+#define PK_CU(expr)                                                                 \
+  do {                                                                              \
+    CUresult _r = (expr);                                                           \
+    if (_r != CUDA_SUCCESS)                                                         \
+      return ::pk::fail(PK_ERR_CUDA, "%s failed: CUresult %d (%s:%d)", #expr,       \
+                        (int)_r, __FILE__, __LINE__);                               \
+  } while (0)
+
+#define PK_TRY(expr)                 \
+  do {                               \
+    int _s = (expr);                 \
+    if (_s != PK_OK) return _s;      \
+  } while (0)
+
+// Driver API, resolved lazily through cudaGetDriverEntryPoint.
+struct Driver {
+  decltype(&cuTensorMapEncodeTiled) tensorMapEncodeTiled = nullptr;
+  decltype(&cuMemCreate) memCreate = nullptr;
+  decltype(&cuMemRelease) memRelease = nullptr;
+  decltype(&cuMemAddressReserve) memAddressReserve = nullptr;
+  decltype(&cuMemAddressFree) memAddressFree = nullptr;
+  decltype(&cuMemMap) memMap = nullptr;
+  decltype(&cuMemUnmap) memUnmap = nullptr;
+  decltype(&cuMemSetAccess) memSetAccess = nullptr;
+  decltype(&cuMemGetAllocationGranularity) memGetAllocationGranularity = nullptr;
+  decltype(&cuMemExportToShareableHandle) memExportToShareableHandle = nullptr;
+  decltype(&cuMemImportFromShareableHandle) memImportFromShareableHandle = nullptr;
+  decltype(&cuMulticastCreate) multicastCreate = nullptr;
+  decltype(&cuMulticastAddDevice) multicastAddDevice = nullptr;
+  decltype(&cuMulticastBindMem) multicastBindMem = nullptr;
+  decltype(&cuMulticastUnbind) multicastUnbind = nullptr;
+  decltype(&cuMulticastGetGranularity) multicastGetGranularity = nullptr;
+  decltype(&cuDeviceGetAttribute) deviceGetAttribute = nullptr;
+  decltype(&cuDeviceGet) deviceGet = nullptr;
+  bool ok = false;
+};
+int driver(const Driver** out);
+
+enum { kMaxRanks = 8 };
+
+// Element size of a pk_dtype.
+inline int dtype_bytes(int dt) {
+  switch (dt) {
+    case PK_BF16: case PK_F16: return 2;
+    case PK_F32: case PK_I32: return 4;
+    case PK_I64: return 8;
+    case PK_U8: return 1;
+  }
+  return 0;
+}
+
+// 2-D row-major bf16 view checks: returns rows/cols/row stride (elements).
+int check_matrix(const pk_tensor* t, const char* name, int dtype, int64_t* rows, int64_t* cols, int64_t* ld);
+
+// Encode a 2-D tensor map over a row-major [rows, cols] matrix (ld in
+// elements), box = [box_rows, box_cols], 128 B swizzle.
+int make_tmap_2d(CUtensorMap* map, const void* ptr, CUtensorMapDataType dt, int elem_bytes,
+                 int64_t rows, int64_t cols, int64_t ld, int box_rows, int box_cols,
+                 CUtensorMapSwizzle swz);
+
+// ---------------------------------------------------------------- communicator
+struct Comm;
+
+struct Pgl {
+  Comm* comm = nullptr;
+  size_t bytes = 0;            // requested
+  size_t mapped = 0;           // rounded to granularity
+  void* local = nullptr;
+  void* peers[kMaxRanks] = {};
+  void* mc = nullptr;
+  // VMM bookkeeping (multi-process mode)
+  CUmemGenericAllocationHandle handle = 0;
+  CUmemGenericAllocationHandle peer_handles[kMaxRanks] = {};
+  CUmemGenericAllocationHandle mc_handle = 0;
+  bool vmm = false;
+  bool owns_cudamalloc = false;   // local-group mode: rank's own cudaMalloc
+};
+
+struct LocalGroup;
+
+struct Comm {
+  int rank = 0, world = 1, device = 0;
+  bool local_group = false;          // single-process emulated peers
+  LocalGroup* group = nullptr;
+  std::string uid;
+  int num_sms = 148;
+  bool multicast_supported = false;
+  uint64_t timeout_ns = 10ull * 1000 * 1000 * 1000;
+  // sync PGL: [0,n) ready counters, [n,2n) done counters, [2n, 2n+1) err,
+  // then per-m-tile flags.
+  Pgl* sync = nullptr;
+  uint32_t epoch = 0;
+  uint32_t ready_count = 0;          // cumulative ready signals expected per src
+  uint32_t done_count = 0;           // cumulative done signals expected per src
+  int max_flags = 0;
+  // scratch (symmetric) buffers, grown on demand
+  Pgl* scratch[4] = {};
+  // rendezvous socket (multi-process)
+  int listen_fd = -1;
+};
+
+// Exchange `len` bytes from every rank (allgather) — multi-process through
+// the Unix-socket rendezvous; local groups copy in-process.
+int comm_allgather(Comm* c, const void* mine, void* all, size_t len);
+int comm_barrier(Comm* c);
+int pgl_alloc(Comm* c, size_t bytes, uint32_t flags, Pgl** out);
+int pgl_free(Pgl* p);
+// Ensure scratch slot `slot` holds >= bytes (collective: all ranks call).
+int comm_scratch(Comm* c, int slot, size_t bytes, Pgl** out);
+
+}  // namespace pk
+
+struct pk_comm : pk::Comm {};
+struct pk_pgl : pk::Pgl {};
