@@ -7,6 +7,7 @@ lives in `compat`.
 """
 from .errors import (DeadlockError, LcscError, MemSimError, MulticastReadError,  # noqa: F401
                      PkCudaError, PkError, PrimitiveError, ProtocolViolation, WorkloadError)
-from .ops import gemm  # noqa: F401
+from .comm import Comm, Pgl, local_group  # noqa: F401
+from .ops import all_gather_gemm, gemm, gemm_reduce_scatter  # noqa: F401
 
 __version__ = "0.1.0"

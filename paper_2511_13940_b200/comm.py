@@ -1,0 +1,152 @@
+"""Communicators and symmetric (PGL) tensors.
+
+`Comm` wraps one rank's `pk_comm` (include/pk.h). Two ways to get one:
+
+* `Comm.init(rank, world, device, uid)` — one process per GPU (torchrun);
+  VMM handles are exchanged between the processes as POSIX fds over abstract
+  Unix sockets named by `uid` (identical on all ranks). `init_from_env()`
+  derives rank/world/device from torchrun's environment and agrees on `uid`
+  through torch.distributed.
+* `local_group(world, device)` — `world` ranks inside this process sharing
+  one GPU; peers are separate allocations on that GPU. This is how the fused
+  kernels' real peer-memory code runs on a single B200.
+
+`comm.empty(shape, dtype)` returns a torch tensor over a parallel global
+layout (ParallelGlobalLayout, overlapsim/memsim.py:89-149): one identically
+sized buffer per rank, with `comm.peer_ptrs(t)` giving every rank's copy and
+an optional multicast alias (attach_multicast, memsim.py:333-341).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import uuid
+
+import torch
+
+from . import _lib
+from .errors import DeadlockError, check
+
+PK_PGL_MULTICAST = 1
+
+
+class _CudaArray:
+    """Minimal __cuda_array_interface__ exporter over a raw device pointer."""
+
+    def __init__(self, ptr: int, nbytes: int, owner):
+        self.__cuda_array_interface__ = {
+            "shape": (nbytes,), "typestr": "|u1", "data": (ptr, False), "version": 3, "strides": None,
+        }
+        self._owner = owner
+
+
+class Pgl:
+    """One parallel global layout (symmetric buffer) of a communicator."""
+
+    def __init__(self, comm: "Comm", nbytes: int, multicast: bool = False):
+        self.comm = comm
+        self.nbytes = nbytes
+        h = ctypes.c_void_p()
+        lib = _lib.load()
+        check(lib.pk_pgl_alloc(comm._h, ctypes.c_size_t(nbytes), ctypes.c_uint32(PK_PGL_MULTICAST if multicast else 0),
+                               ctypes.byref(h)), "pgl_alloc")
+        self._h = h
+        local = ctypes.c_void_p()
+        peers = (ctypes.c_void_p * 8)()
+        mc = ctypes.c_void_p()
+        check(lib.pk_pgl_ptrs(h, ctypes.byref(local), peers, ctypes.byref(mc)), "pgl_ptrs")
+        self.local = local.value
+        self.peers = [peers[i] for i in range(comm.world)]
+        self.multicast = mc.value
+
+    def tensor(self, shape, dtype) -> torch.Tensor:
+        numel = 1
+        for s in shape:
+            numel *= s
+        nbytes = numel * torch.empty((), dtype=dtype).element_size()
+        if nbytes > self.nbytes:
+            raise ValueError("tensor larger than the PGL")
+        raw = torch.as_tensor(_CudaArray(self.local, nbytes, self), device=f"cuda:{self.comm.device}")
+        t = raw.view(dtype).view(*shape)
+        t._pk_pgl = self        # keep the allocation alive with the tensor
+        return t
+
+    def free(self):
+        if self._h:
+            _lib.load().pk_pgl_free(self._h)
+            self._h = None
+
+
+class Comm:
+    def __init__(self, handle: ctypes.c_void_p, device: int, keepalive=None):
+        self._h = handle
+        lib = _lib.load()
+        r, w = ctypes.c_int(), ctypes.c_int()
+        check(lib.pk_comm_rank(handle, ctypes.byref(r), ctypes.byref(w)), "comm_rank")
+        self.rank, self.world, self.device = r.value, w.value, device
+        mc = ctypes.c_int()
+        check(lib.pk_comm_has_multicast(handle, ctypes.byref(mc)), "comm_has_multicast")
+        self.has_multicast = bool(mc.value)
+        self._pgls: list[Pgl] = []
+        self._keep = keepalive
+
+    # ------------------------------------------------------------------ construction
+    @classmethod
+    def init(cls, rank: int, world: int, device: int, uid: str) -> "Comm":
+        lib = _lib.load()
+        h = ctypes.c_void_p()
+        check(lib.pk_comm_init(rank, world, device, uid.encode(), ctypes.byref(h)), "comm_init")
+        return cls(h, device)
+
+    @classmethod
+    def init_from_env(cls) -> "Comm":
+        """torchrun: RANK / WORLD_SIZE / LOCAL_RANK; uid agreed via torch.distributed."""
+        import torch.distributed as dist
+        rank = int(os.environ.get("RANK", "0"))
+        world = int(os.environ.get("WORLD_SIZE", "1"))
+        device = int(os.environ.get("LOCAL_RANK", "0"))
+        uid = [uuid.uuid4().hex[:16] if rank == 0 else None]
+        if world > 1 and dist.is_initialized():
+            dist.broadcast_object_list(uid, src=0)
+        return cls.init(rank, world, device, uid[0])
+
+    # ------------------------------------------------------------------ memory
+    def pgl(self, nbytes: int, multicast: bool = False) -> Pgl:
+        p = Pgl(self, nbytes, multicast)
+        self._pgls.append(p)
+        return p
+
+    def empty(self, shape, dtype=torch.bfloat16, multicast: bool = False) -> torch.Tensor:
+        numel = 1
+        for s in shape:
+            numel *= s
+        nbytes = max(16, numel * torch.empty((), dtype=dtype).element_size())
+        return self.pgl(nbytes, multicast).tensor(shape, dtype)
+
+    # ------------------------------------------------------------------ misc
+    def set_timeout(self, seconds: float):
+        check(_lib.load().pk_comm_set_timeout(self._h, ctypes.c_uint64(int(seconds * 1e9))), "set_timeout")
+
+    def check(self):
+        """Raise DeadlockError if a device-side wait() timed out since the last check."""
+        t = ctypes.c_int()
+        check(_lib.load().pk_comm_check(self._h, ctypes.byref(t)), "comm_check")
+        if t.value:
+            raise DeadlockError(f"rank {self.rank}: a device-side wait() timed out (some rank never signalled)")
+
+    def destroy(self):
+        if self._h:
+            torch.cuda.synchronize(self.device)
+            for p in self._pgls:
+                p.free()
+            self._pgls.clear()
+            _lib.load().pk_comm_destroy(self._h)
+            self._h = None
+
+
+def local_group(world: int, device: int = 0) -> list[Comm]:
+    """`world` communicator ranks sharing one GPU inside this process."""
+    lib = _lib.load()
+    arr = (ctypes.c_void_p * world)()
+    check(lib.pk_comm_init_local(world, device, arr), "comm_init_local")
+    return [Comm(ctypes.c_void_p(arr[i]), device) for i in range(world)]

@@ -123,7 +123,18 @@ struct Comm {
   Pgl* scratch[4] = {};
   // rendezvous socket (multi-process)
   int listen_fd = -1;
+  uint32_t seq = 0;                  // collective sequence number (message tag)
+  struct Pending { int src; uint32_t tag; std::vector<char> payload; int fd; };
+  std::vector<Pending> pending;      // messages that arrived for a later collective
+  std::vector<Pgl*> user_pgls;       // PGLs handed out through pk_pgl_alloc (zero-copy lookup)
 };
+
+// If [ptr, ptr+bytes) lies inside one of c's user PGLs, fill peers[] with the
+// same offset in every rank's buffer and return true.
+bool find_symmetric(Comm* c, const void* ptr, size_t bytes, void** peers);
+
+// Word offsets inside the per-comm sync PGL.
+enum { kSyncReady = 0, kSyncDone = 8, kSyncErr = 16, kSyncFlags = 32, kSyncBytes = 1 << 20 };
 
 // Exchange `len` bytes from every rank (allgather) — multi-process through
 // the Unix-socket rendezvous; local groups copy in-process.

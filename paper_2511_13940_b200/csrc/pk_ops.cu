@@ -103,6 +103,183 @@ int gemm_local(const pk_tensor* A, const pk_tensor* B, pk_tensor* C, const pk_sc
   return launch_gemm_variant(cg, EPI_STORE, args, clusters * cg, st);
 }
 
+// Fill the cross-rank sync block of one fused call.
+static void fill_sync(Comm* c, SyncArgs& sy) {
+  uint32_t* local = static_cast<uint32_t*>(c->sync->local);
+  sy.ready_local = local + kSyncReady;
+  sy.done_local = local + kSyncDone;
+  sy.err = local + kSyncErr;
+  sy.flags = local + kSyncFlags;
+  for (int r = 0; r < c->world; ++r) {
+    uint32_t* peer = static_cast<uint32_t*>(c->sync->peers[r]);
+    sy.ready_peer[r] = peer + kSyncReady;
+    sy.done_peer[r] = peer + kSyncDone;
+  }
+  sy.epoch = c->epoch;
+  sy.ready_expect = c->ready_count;
+  sy.done_expect = c->done_count;
+  sy.timeout_ns = c->timeout_ns;
+}
+
+static int contiguous_rows(const pk_tensor* t) { return t->strides[0] == t->shape[1]; }
+
+int ag_gemm(Comm* c, const pk_tensor* A, const pk_tensor* B, pk_tensor* C, pk_tensor* AG,
+            const pk_sched* sched, cudaStream_t st) {
+  int64_t m_loc, K, ldA, n_loc, Kb, ldB, Mc, Nc, ldC;
+  PK_TRY(check_matrix(A, "a_shard", PK_BF16, &m_loc, &K, &ldA));
+  PK_TRY(check_matrix(B, "b", PK_BF16, &n_loc, &Kb, &ldB));
+  PK_TRY(check_matrix(C, "c", PK_BF16, &Mc, &Nc, &ldC));
+  const int n = c->world;
+  const int64_t M = m_loc * n;
+  if (Kb != K) return fail(PK_ERR_INVALID, "ag_gemm: K mismatch (a %lld, b %lld)", (long long)K, (long long)Kb);
+  if (Mc != M || Nc != n_loc)
+    return fail(PK_ERR_INVALID, "ag_gemm: c must be [%lld, %lld]", (long long)M, (long long)n_loc);
+  if (AG) {
+    int64_t r, k2, ld;
+    PK_TRY(check_matrix(AG, "a_gathered", PK_BF16, &r, &k2, &ld));
+    if (r != M || k2 != K || ld != K) return fail(PK_ERR_INVALID, "ag_gemm: a_gathered must be contiguous [%lld, %lld]", (long long)M, (long long)K);
+  }
+  if (m_loc % 128 || n_loc % 256 || K % BLOCK_K || K == 0)
+    return fail(PK_ERR_INVALID, "ag_gemm: need (M/n) %% 128 == 0, N_local %% 256 == 0, K %% 64 == 0 (got %lld, %lld, %lld)",
+                (long long)m_loc, (long long)n_loc, (long long)K);
+  if (n == 1) {
+    PK_TRY(gemm_local(A, B, C, sched, st, c->device));
+    if (AG) PK_CUDA(cudaMemcpy2DAsync(AG->ptr, K * 2, A->ptr, ldA * 2, K * 2, m_loc, cudaMemcpyDeviceToDevice, st));
+    return PK_OK;
+  }
+  const int cg = pick_cg(m_loc);
+  const int tile_m = 128 * cg;
+  const int num_n = (int)(n_loc / 256);
+  int mode = sched ? sched->mode : PK_SCHED_AUTO;
+  if (mode == PK_SCHED_AUTO) mode = (num_n == 1 && !AG) ? PK_INTRA_SM : PK_INTER_SM;
+  if (mode == PK_HYBRID) mode = PK_INTER_SM;   // HYBRID behaves like INTER_SM
+
+  // Shard of every rank: zero-copy if the caller's tensor is symmetric.
+  void* shard[kMaxRanks];
+  const size_t shard_bytes = (size_t)m_loc * K * 2;
+  if (!(contiguous_rows(A) && find_symmetric(c, A->ptr, shard_bytes, shard))) {
+    Pgl* s0;
+    PK_TRY(comm_scratch(c, 0, shard_bytes, &s0));
+    PK_CUDA(cudaMemcpy2DAsync(s0->local, K * 2, A->ptr, ldA * 2, K * 2, m_loc, cudaMemcpyDeviceToDevice, st));
+    for (int r = 0; r < n; ++r) shard[r] = s0->peers[r];
+  }
+
+  GemmArgs args;
+  init_args(args);
+  args.M = (int)M; args.N = (int)n_loc; args.K = (int)K;
+  args.rank = c->rank; args.world = n;
+  args.a_rows_per_src = (int)m_loc;
+  args.a_nsrc = n;
+  args.c_rows_per_dst = (int)M;
+  args.m_rot = (int)(c->rank * (m_loc / tile_m));
+  PK_TRY(tmap_b(&args.tmap_b, B->ptr, n_loc, K, ldB, cg));
+  PK_TRY(tmap_c(&args.tmap_c[0], C->ptr, M, n_loc, ldC));
+  const int tiles = (int)((M / tile_m) * num_n);
+  const int clusters_total = std::max(1, (sched && sched->num_sms > 0 ? std::min(sched->num_sms, c->num_sms) : c->num_sms) / cg);
+  int comm_clusters = 0;
+  if (mode == PK_INTRA_SM) {
+    for (int r = 0; r < n; ++r) PK_TRY(tmap_a(&args.tmap_a[r], shard[r], m_loc, K, K));
+    args.sync_ready_before_load = 1;
+  } else {
+    const int comm_sms = (sched && sched->num_comm_sms > 0) ? sched->num_comm_sms : std::max(2, std::min(16, c->num_sms / 8));
+    comm_clusters = std::max(1, comm_sms / cg);
+    if (comm_clusters >= clusters_total) return fail(PK_ERR_INVALID, "ag_gemm: num_comm_sms leaves no compute SMs");
+    void* gathered;
+    if (AG) {
+      gathered = AG->ptr;
+    } else {
+      Pgl* s1;
+      PK_TRY(comm_scratch(c, 1, (size_t)M * K * 2, &s1));
+      gathered = s1->local;
+    }
+    if (M / tile_m > c->max_flags) return fail(PK_ERR_INVALID, "ag_gemm: too many row tiles for the flag array");
+    for (int r = 0; r < n; ++r) {
+      if (r == c->rank) {
+        PK_TRY(tmap_a(&args.tmap_a[r], shard[r], m_loc, K, K));
+        args.a_base[r] = 0;
+      } else {
+        PK_TRY(tmap_a(&args.tmap_a[r], gathered, M, K, K));
+        args.a_base[r] = (int)(r * m_loc);
+        args.a_wait_flag[r] = 1;
+      }
+      args.comm_src[r] = static_cast<uint8_t*>(shard[r]);
+    }
+    args.comm_dst = static_cast<uint8_t*>(gathered);
+    args.comm_shard_bytes = (long long)shard_bytes;
+    args.comm_copy_local = AG ? 1 : 0;
+  }
+  int compute_clusters = std::min(tiles, clusters_total - comm_clusters);
+  args.num_compute_clusters = compute_clusters;
+  args.sync_done_signal = 1;
+  c->epoch += 1;
+  c->ready_count += 1;
+  c->done_count += (uint32_t)(compute_clusters * cg * 4);
+  fill_sync(c, args.sync);
+  PK_TRY(launch_gemm_variant(cg, EPI_STORE, args, (compute_clusters + comm_clusters) * cg, st));
+  if (AG && mode == PK_INTRA_SM) {
+    // intra-SM never materialises the gathered rows; copy them on demand
+    for (int r = 0; r < n; ++r)
+      PK_CUDA(cudaMemcpyAsync(static_cast<char*>(AG->ptr) + (size_t)r * shard_bytes, shard[r], shard_bytes,
+                              cudaMemcpyDeviceToDevice, st));
+  }
+  return PK_OK;
+}
+
+int gemm_rs(Comm* c, const pk_tensor* A, const pk_tensor* B, pk_tensor* O, const pk_sched* sched, cudaStream_t st) {
+  int64_t M, k_loc, ldA, N, Kb, ldB, Mo, No, ldO;
+  PK_TRY(check_matrix(A, "a", PK_BF16, &M, &k_loc, &ldA));
+  PK_TRY(check_matrix(B, "b", PK_BF16, &N, &Kb, &ldB));
+  PK_TRY(check_matrix(O, "out", PK_BF16, &Mo, &No, &ldO));
+  const int n = c->world;
+  if (Kb != k_loc) return fail(PK_ERR_INVALID, "gemm_rs: K mismatch (a %lld, b %lld)", (long long)k_loc, (long long)Kb);
+  if (M % n) return fail(PK_ERR_INVALID, "gemm_rs: M=%lld must divide across %d ranks", (long long)M, n);
+  const int64_t m_own = M / n;
+  if (Mo != m_own || No != N)
+    return fail(PK_ERR_INVALID, "gemm_rs: out must be [%lld, %lld]", (long long)m_own, (long long)N);
+  if (m_own % 128 || N % 256 || k_loc % BLOCK_K || k_loc == 0)
+    return fail(PK_ERR_INVALID, "gemm_rs: need (M/n) %% 128 == 0, N %% 256 == 0, K %% 64 == 0 (got %lld, %lld, %lld)",
+                (long long)m_own, (long long)N, (long long)k_loc);
+  if (n == 1) return gemm_local(A, B, O, sched, st, c->device);
+  const int cg = pick_cg(m_own);
+  const int tile_m = 128 * cg;
+  // Destination of every rank (zero-copy when `out` is symmetric).
+  void* dst[kMaxRanks];
+  const size_t out_bytes = (size_t)m_own * N * 2;
+  bool staged = false;
+  if (!(contiguous_rows(O) && find_symmetric(c, O->ptr, out_bytes, dst))) {
+    Pgl* s2;
+    PK_TRY(comm_scratch(c, 2, out_bytes, &s2));
+    for (int r = 0; r < n; ++r) dst[r] = s2->peers[r];
+    staged = true;
+  }
+  PK_CUDA(cudaMemsetAsync(dst[c->rank], 0, out_bytes, st));
+  GemmArgs args;
+  init_args(args);
+  args.M = (int)M; args.N = (int)N; args.K = (int)k_loc;
+  args.rank = c->rank; args.world = n;
+  args.a_rows_per_src = (int)M;
+  PK_TRY(tmap_a(&args.tmap_a[0], A->ptr, M, k_loc, ldA));
+  PK_TRY(tmap_b(&args.tmap_b, B->ptr, N, k_loc, ldB, cg));
+  for (int r = 0; r < n; ++r) PK_TRY(tmap_c(&args.tmap_c[r], dst[r], m_own, N, N));
+  args.c_rows_per_dst = (int)m_own;
+  args.c_ndst = n;
+  args.m_rot = (int)(((c->rank + 1) % n) * (m_own / tile_m));   // right neighbour's rows first, own last
+  const int tiles = (int)((M / tile_m) * (N / 256));
+  const int clusters_total = std::max(1, (sched && sched->num_sms > 0 ? std::min(sched->num_sms, c->num_sms) : c->num_sms) / cg);
+  const int compute_clusters = std::min(tiles, clusters_total);
+  args.num_compute_clusters = compute_clusters;
+  args.sync_ready_before_store = 1;
+  args.sync_done_signal = 1;
+  c->epoch += 1;
+  c->ready_count += 1;
+  c->done_count += (uint32_t)(compute_clusters * cg * 4);
+  fill_sync(c, args.sync);
+  PK_TRY(launch_gemm_variant(cg, EPI_REDUCE_ADD, args, compute_clusters * cg, st));
+  if (staged)
+    PK_CUDA(cudaMemcpy2DAsync(O->ptr, ldO * 2, dst[c->rank], N * 2, N * 2, m_own, cudaMemcpyDeviceToDevice, st));
+  return PK_OK;
+}
+
 }  // namespace pk
 
 extern "C" {
@@ -111,6 +288,18 @@ PK_API int pk_gemm(const pk_tensor* a, const pk_tensor* b, pk_tensor* c, const p
   int dev = 0;
   PK_CUDA(cudaGetDevice(&dev));
   return pk::gemm_local(a, b, c, sched, (cudaStream_t)stream, dev);
+}
+
+PK_API int pk_ag_gemm(pk_comm* comm, const pk_tensor* a_shard, const pk_tensor* b, pk_tensor* c,
+                      pk_tensor* a_gathered, const pk_sched* sched, void* stream) {
+  if (!comm) return pk::fail(PK_ERR_INVALID, "null comm");
+  return pk::ag_gemm(comm, a_shard, b, c, a_gathered, sched, (cudaStream_t)stream);
+}
+
+PK_API int pk_gemm_rs(pk_comm* comm, const pk_tensor* a, const pk_tensor* b, pk_tensor* out,
+                      const pk_sched* sched, void* stream) {
+  if (!comm) return pk::fail(PK_ERR_INVALID, "null comm");
+  return pk::gemm_rs(comm, a, b, out, sched, (cudaStream_t)stream);
 }
 
 }  // extern "C"

@@ -34,7 +34,7 @@ def gemm(a: torch.Tensor, b: torch.Tensor, out: torch.Tensor | None = None,
         out = torch.empty((a.shape[0], b.shape[0]), dtype=torch.bfloat16, device=a.device)
     lib = _lib.load()
     da, db, dc = _lib.tensor_desc(a), _lib.tensor_desc(b), _lib.tensor_desc(out)
-    sc = _lib.sched_desc(schedule)
+    sc = _sched(schedule)
     check(lib.pk_gemm(_lib.ref(da), _lib.ref(db), _lib.ref(dc), _lib.ref(sc),
                       ctypes_stream(_stream())), "gemm")
     return out
@@ -43,3 +43,54 @@ def gemm(a: torch.Tensor, b: torch.Tensor, out: torch.Tensor | None = None,
 def ctypes_stream(s: int):
     import ctypes
     return ctypes.c_void_p(s)
+
+
+_MODES = {None: -1, "auto": -1, "intra_sm": 0, "inter_sm": 1, "hybrid": 2}
+
+
+def _sched(schedule):
+    if schedule is None:
+        return None
+    sc = dict(schedule)
+    mode = sc.get("mode")
+    if isinstance(mode, str) or mode is None:
+        sc["mode"] = _MODES[mode]
+    elif hasattr(mode, "value"):          # ScheduleMode enum
+        sc["mode"] = _MODES[mode.value]
+    return _lib.sched_desc(sc)
+
+
+def all_gather_gemm(comm, a_shard: torch.Tensor, b: torch.Tensor, out: torch.Tensor | None = None,
+                    a_gathered: torch.Tensor | None = None, schedule: dict | None = None,
+                    stream=None) -> torch.Tensor:
+    """C_r[M, N/n] = AllGather_rows(A)[M, K] @ B_r[N/n, K]^T (AgGemmPlan, workloads.py:553-609).
+
+    a_shard is this rank's rows [M/n, K]; rows are gathered rank-major
+    (workloads.py:603-609). If `a_gathered` [M, K] is given it receives the
+    gathered rows (the reference's `ag` layout).
+    """
+    _require_cuda(a_shard, b)
+    m = a_shard.shape[0] * comm.world
+    if out is None:
+        out = torch.empty((m, b.shape[0]), dtype=torch.bfloat16, device=a_shard.device)
+    lib = _lib.load()
+    da, db, dc = _lib.tensor_desc(a_shard), _lib.tensor_desc(b), _lib.tensor_desc(out)
+    dg = _lib.tensor_desc(a_gathered) if a_gathered is not None else None
+    sc = _sched(schedule)
+    check(lib.pk_ag_gemm(comm._h, _lib.ref(da), _lib.ref(db), _lib.ref(dc), _lib.ref(dg), _lib.ref(sc),
+                         ctypes_stream(_stream(stream))), "all_gather_gemm")
+    return out
+
+
+def gemm_reduce_scatter(comm, a: torch.Tensor, b: torch.Tensor, out: torch.Tensor | None = None,
+                        schedule: dict | None = None, stream=None) -> torch.Tensor:
+    """out_r[M/n, N] = sum_d (A_d[M, K/n] @ B_d[N, K/n]^T)[rows owned by r] (GemmRsPlan, workloads.py:343-408)."""
+    _require_cuda(a, b)
+    if out is None:
+        out = torch.empty((a.shape[0] // comm.world, b.shape[0]), dtype=torch.bfloat16, device=a.device)
+    lib = _lib.load()
+    da, db, do = _lib.tensor_desc(a), _lib.tensor_desc(b), _lib.tensor_desc(out)
+    sc = _sched(schedule)
+    check(lib.pk_gemm_rs(comm._h, _lib.ref(da), _lib.ref(db), _lib.ref(do), _lib.ref(sc),
+                         ctypes_stream(_stream(stream))), "gemm_reduce_scatter")
+    return out
