@@ -1,0 +1,393 @@
+#!/usr/bin/env python
+"""Benchmark of the pk hot path: AG-GEMM + GEMM-RS TFLOP/s (BASELINE.json metric).
+
+One step = one tensor-parallel AG-GEMM followed by one GEMM-RS at
+M = N = K = S (default S = 16384, bf16 in / fp32 accumulate / bf16 out):
+  AG-GEMM : C_r[S, S/n]  = AllGather(A_r[S/n, S]) @ B_r[S/n, S]^T
+  GEMM-RS : out_r[S/n, S] = sum_d (A_d[S, S/n] @ B_d[S, S/n]^T)[rows of r]
+Whole-job FLOPs per step = 2 * 2 * S^3 (strong scaling: total work fixed).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--size S] [--impl pk|reference]
+
+N > 1 runs under torchrun (one rank per GPU); the device time is the max over
+ranks. Inputs are synthetic (torch.randn * 0.1, seeded per rank) and larger
+than L2 (each operand >= 128 MiB at S = 16384), so no L2 flush is needed.
+`--impl reference` times the CPU oracle port (oracle/, numpy) on rank 0.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "AG-GEMM & GEMM-RS TFLOP/s @1/2/4/8 B200; speedup vs NCCL+cuBLAS non-overlap"
+UNIT = "TFLOP/s"
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=10)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--size", type=int, default=16384)
+    p.add_argument("--impl", default="pk", choices=["pk", "reference"])
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-baseline", action="store_true")
+    p.add_argument("--cpu-seconds", type=float, default=10.0)
+    return p.parse_args()
+
+
+# ----------------------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi sampling DURING the timed region (B200_PROFILING.md clocks line)."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.lines: list[str] = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except Exception:
+            self.proc.kill()
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax = float(parts[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[4:8]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ----------------------------------------------------------------------------- helpers
+def peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        d = json.load(open(path))
+        return d.get("bf16_tflops", 1590.0), d.get("bf16_tflops_sustained", 1400.0), "measured"
+    return 1590.0, 1400.0, "fallback"
+
+
+def traffic_for(size: int):
+    path = os.path.join(ROOT, "profiles", "gemm_dram_traffic.json")
+    if os.path.exists(path):
+        d = json.load(open(path))
+        return d.get(str(size))
+    return None
+
+
+def cpu_threads() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def cpu_oracle_rate(size: int, seconds: float, slab_div: int = 1):
+    """Time the oracle port's AG-GEMM + GEMM-RS (n = 1) in float32 on host cores.
+
+    Returns (TFLOP/s, sample description, threads)."""
+    import numpy as np
+
+    import oracle
+    rng = np.random.default_rng(0)
+    rows = max(1, size // slab_div)
+    a = (rng.standard_normal((rows, size)) * 0.1).astype(np.float32)
+    b = (rng.standard_normal((size, size)) * 0.1).astype(np.float32)
+    flops_per = 2 * 2.0 * rows * size * size
+    oracle.ag_gemm([a], [b], dtype=np.float32)  # warm
+    reps, t0 = 0, time.perf_counter()
+    while True:
+        oracle.ag_gemm([a], [b], dtype=np.float32)
+        oracle.gemm_rs([a], [b], dtype=np.float32)
+        reps += 1
+        dt = time.perf_counter() - t0
+        if dt >= seconds:
+            break
+    tf = flops_per * reps / dt / 1e12
+    sample = (f"oracle.ag_gemm + oracle.gemm_rs (numpy float32) at n=1, rows {rows} of M={size}, "
+              f"N=K={size}; {reps} steps in {dt:.1f}s")
+    return tf, sample, cpu_threads()
+
+
+# ----------------------------------------------------------------------------- reference arm
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    S = args.size
+    n = args.gpus
+    # bounded sample: a 1/16 row slab of each GEMM per step
+    slab = 16 if S >= 8192 else 1
+    import numpy as np
+
+    import oracle
+    rng = np.random.default_rng(0)
+    rows = S // slab
+    a = (rng.standard_normal((rows, S)) * 0.1).astype(np.float32)
+    b = (rng.standard_normal((S, S)) * 0.1).astype(np.float32)
+    flops = 2 * 2.0 * rows * S * S
+    for _ in range(args.warmup):
+        oracle.ag_gemm([a], [b], dtype=np.float32)
+        oracle.gemm_rs([a], [b], dtype=np.float32)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        oracle.ag_gemm([a], [b], dtype=np.float32)
+        oracle.gemm_rs([a], [b], dtype=np.float32)
+    dt = time.perf_counter() - t0
+    value = flops * args.steps / dt / 1e12
+    sample = f"per step: AG-GEMM + GEMM-RS row slab {rows}/{S} rows (numpy float32, oracle port)"
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": n,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic", "config": {"workload": f"ag_gemm+gemm_rs M=N=K={S} (row-slab sample)", "size": S,
+                                        "parallelism": f"tp{n}"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cpu_threads(), "kind": "port", "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ----------------------------------------------------------------------------- pk arm
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_2511_13940_b200 as pk
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus and rank == 0:
+        print(f"warning: --gpus {args.gpus} but WORLD_SIZE {world}", file=sys.stderr)
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+        comm = pk.Comm.init_from_env()
+    else:
+        comm = pk.local_group(1, local)[0]
+    n = world
+    S = args.size
+    if S % (256 * n):
+        raise SystemExit(f"--size must be a multiple of {256 * n}")
+    g = torch.Generator(device=dev)
+    g.manual_seed(1234 + rank)
+
+    def randn(*shape):
+        return (torch.randn(*shape, device=dev, generator=g) * 0.1).to(torch.bfloat16)
+
+    # AG-GEMM operands; the shard lives in a symmetric PGL so peers read it in place
+    a_ag = comm.empty((S // n, S))
+    a_ag.copy_(randn(S // n, S))
+    b_ag = randn(S // n, S)
+    c_ag = torch.empty(S, S // n, device=dev, dtype=torch.bfloat16)
+    # GEMM-RS operands; the output is symmetric so peers reduce-add into it
+    a_rs = randn(S, S // n)
+    b_rs = randn(S, S // n)
+    o_rs = comm.empty((S // n, S))
+    flops_step = 2 * 2.0 * S ** 3                  # whole job (all ranks)
+    flops_launch = 2.0 * S ** 3 / n                # per rank per GEMM launch
+    stream = torch.cuda.current_stream()
+
+    def step(evs=None):
+        if evs is not None:
+            evs[0].record(stream)
+        pk.all_gather_gemm(comm, a_ag, b_ag, out=c_ag)
+        if evs is not None:
+            evs[1].record(stream)
+        pk.gemm_reduce_scatter(comm, a_rs, b_rs, out=o_rs)
+        if evs is not None:
+            evs[2].record(stream)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def max_over_ranks(x: float) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    for _ in range(args.warmup):
+        step()
+    barrier()
+    comm.check()
+
+    # ---------------------------------------------------------------- timed region
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
+    clocks = ClockSampler(local)
+    clocks.start()
+    barrier()
+    t_start = torch.cuda.Event(enable_timing=True)
+    t_end = torch.cuda.Event(enable_timing=True)
+    t_start.record(stream)
+    for i in range(args.steps):
+        step(evs[i])
+    t_end.record(stream)
+    barrier()
+    clk = clocks.stop()
+    comm.check()
+    ms_total = max_over_ranks(t_start.elapsed_time(t_end))
+    ms_step = ms_total / args.steps
+    value = flops_step * args.steps / (ms_total / 1e3) / 1e12
+    ag_ms = statistics.mean(e[0].elapsed_time(e[1]) for e in evs)
+    rs_ms = statistics.mean(e[1].elapsed_time(e[2]) for e in evs)
+    launch_ms = max_over_ranks((ag_ms + rs_ms) / 2)
+
+    # ---------------------------------------------------------------- NCCL + cuBLAS, non-overlapped
+    base = None
+    if not args.no_baseline:
+        a_full = torch.empty(S, S, device=dev, dtype=torch.bfloat16) if n > 1 else None
+        part = torch.empty(S, S, device=dev, dtype=torch.bfloat16) if n > 1 else None
+
+        def base_step():
+            if n > 1:
+                dist.all_gather_into_tensor(a_full, a_ag)
+                torch.matmul(a_full, b_ag.t(), out=c_ag)
+                torch.matmul(a_rs, b_rs.t(), out=part)
+                dist.reduce_scatter_tensor(o_rs, part)
+            else:
+                torch.matmul(a_ag, b_ag.t(), out=c_ag)
+                torch.matmul(a_rs, b_rs.t(), out=o_rs)
+        for _ in range(args.warmup):
+            base_step()
+        barrier()
+        b0, b1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        b0.record(stream)
+        for _ in range(args.steps):
+            base_step()
+        b1.record(stream)
+        barrier()
+        bms = max_over_ranks(b0.elapsed_time(b1)) / args.steps
+        base = {"impl": "torch.matmul (cuBLAS)" + (" + NCCL all_gather / reduce_scatter" if n > 1 else ""),
+                "value": flops_step / (bms / 1e3) / 1e12, "ms_per_step": bms, "speedup": bms / ms_step}
+
+    # ---------------------------------------------------------------- end to end (host buffers)
+    e2e = None
+    if not args.no_e2e:
+        ins = [a_ag, b_ag, a_rs, b_rs]
+        outs = [c_ag, o_rs]
+        h_in = [torch.empty(t.shape, dtype=t.dtype, pin_memory=True) for t in ins]
+        h_out = [torch.empty(t.shape, dtype=t.dtype, pin_memory=True) for t in outs]
+        for h, t in zip(h_in, ins):
+            h.copy_(t)
+        k_e2e = max(1, min(args.steps, 5))
+
+        def e2e_step():
+            for t, h in zip(ins, h_in):
+                t.copy_(h, non_blocking=True)
+            step()
+            for h, t in zip(h_out, outs):
+                h.copy_(t, non_blocking=True)
+        e2e_step()
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(k_e2e):
+            e2e_step()
+        e1.record(stream)
+        barrier()
+        ems = max_over_ranks(e0.elapsed_time(e1)) / k_e2e
+        e2e = {"value": flops_step / (ems / 1e3) / 1e12, "unit": UNIT, "ms_per_step": ems, "steps": k_e2e,
+               "h2d_bytes_per_step": sum(t.numel() * t.element_size() for t in ins),
+               "d2h_bytes_per_step": sum(t.numel() * t.element_size() for t in outs),
+               "api": "paper_2511_13940_b200.all_gather_gemm + gemm_reduce_scatter, pinned host buffers"}
+
+    # ---------------------------------------------------------------- roofline of the dominant kernel
+    peak_burst, peak_sus, src = peaks()
+    achieved = flops_launch / (launch_ms / 1e3) / 1e12
+    roofline = {"bound": "tensor", "achieved": achieved, "peak": peak_burst, "unit": UNIT,
+                "frac": achieved / peak_burst, "traffic": traffic_for(S),
+                "kernel": "pk::lcsc_gemm_kernel<2,256,*>",
+                "per_launch": f"2*S^3/n = {flops_launch:.4g} FLOP per launch (one AG-GEMM or GEMM-RS)",
+                "peak_source": f"{src} bf16_tflops (burst); sustained {peak_sus}",
+                "ag_ms": ag_ms, "rs_ms": rs_ms}
+    if n > 1:
+        link_bytes = (n - 1) / n * S * S * 2
+        t_comp = flops_launch / (peak_burst * 1e12)
+        t_link = link_bytes / 770e9
+        roofline["overlapped"] = {"t_roof_ms": max(t_comp, t_link) * 1e3,
+                                  "limit": "tensor" if t_comp >= t_link else "nvlink",
+                                  "frac": max(t_comp, t_link) * 1e3 / launch_ms,
+                                  "link_bytes_per_launch": link_bytes, "link_gbs": 770}
+
+    cpu = None
+    if rank == 0 and world == 1:
+        tf, sample, cores = cpu_oracle_rate(min(S, 4096), args.cpu_seconds)
+        cpu = {"value": tf, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample}
+    elif rank == 0:
+        cpu = {"value": None, "unit": UNIT, "cores": cpu_threads(), "kind": "port",
+               "sample": "measured on rank 0 at N=1 only"}
+
+    comm.check()
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": n, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "bf16", "data": "synthetic (torch.randn*0.1, seeded per rank)",
+            "config": {"workload": f"ag_gemm+gemm_rs M=N=K={S} (one AG-GEMM then one GEMM-RS per step)",
+                       "size": S, "parallelism": f"tp{n}", "global_batch": S,
+                       "l2": "no flush: every operand > L2 (126 MB)" if S * S * 2 / n > 126e6 else "operands fit L2"},
+            "e2e": e2e, "gpu_launches": 2 * args.steps, "roofline": roofline, "cpu_baseline": cpu,
+            "nccl_cublas": base, "clocks": clk,
+        }
+        print(json.dumps(line), flush=True)
+    comm.destroy()
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -97,8 +97,10 @@ PK_API int pk_comm_rank(const pk_comm* comm, int* rank, int* world);
 PK_API int pk_comm_has_multicast(const pk_comm* comm, int* out);
 /* Device-side timeout of every wait() in ns (default 10 s). */
 PK_API int pk_comm_set_timeout(pk_comm* comm, uint64_t ns);
-/* Read (and clear) the sticky device error flag: 1 = a wait() timed out. */
-PK_API int pk_comm_check(pk_comm* comm, int* timed_out);
+/* Read (and clear) the sticky device error code of the last calls:
+ * 0 = none, 1 = a wait() timed out (deadlock), 2 = an expert id out of range,
+ * 3 = MoE receive capacity exceeded. Synchronises with the device. */
+PK_API int pk_comm_check(pk_comm* comm, int* code);
 
 /* ---- parallel global layouts --------------------------------------------- */
 PK_API int pk_pgl_alloc(pk_comm* comm, size_t bytes, uint32_t flags, pk_pgl** out);

@@ -5,9 +5,18 @@ gemm_reduce_scatter, all_reduce, ring_attention, moe_dispatch, moe_combine.
 The reference-compatible plan API (build / execute_kernel / check_oracle)
 lives in `compat`.
 """
+import os as _os
+
+# Local groups run every emulated rank's streams in one process; with the
+# default 8 hardware work queues, streams share queues and one rank's spinning
+# wait() could block the queue a peer's signal sits in. Must be set before the
+# CUDA context exists (import this package before touching CUDA).
+_os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
+
 from .errors import (DeadlockError, LcscError, MemSimError, MulticastReadError,  # noqa: F401
                      PkCudaError, PkError, PrimitiveError, ProtocolViolation, WorkloadError)
 from .comm import Comm, Pgl, local_group  # noqa: F401
-from .ops import all_gather_gemm, gemm, gemm_reduce_scatter  # noqa: F401
+from .ops import (all_gather_gemm, all_reduce, gemm, gemm_reduce_scatter, moe_combine,  # noqa: F401
+                  moe_dispatch, ring_attention)
 
 __version__ = "0.1.0"

@@ -25,7 +25,7 @@ import uuid
 import torch
 
 from . import _lib
-from .errors import DeadlockError, check
+from .errors import DeadlockError, WorkloadError, check
 
 PK_PGL_MULTICAST = 1
 
@@ -128,11 +128,19 @@ class Comm:
         check(_lib.load().pk_comm_set_timeout(self._h, ctypes.c_uint64(int(seconds * 1e9))), "set_timeout")
 
     def check(self):
-        """Raise DeadlockError if a device-side wait() timed out since the last check."""
+        """Raise if a device-side error was flagged since the last check:
+        DeadlockError (a wait() timed out) or WorkloadError (bad expert id,
+        MoE capacity exceeded)."""
         t = ctypes.c_int()
         check(_lib.load().pk_comm_check(self._h, ctypes.byref(t)), "comm_check")
-        if t.value:
+        if t.value == 1:
             raise DeadlockError(f"rank {self.rank}: a device-side wait() timed out (some rank never signalled)")
+        if t.value == 2:
+            raise WorkloadError(f"rank {self.rank}: an expert id was outside [0, num_experts)")
+        if t.value == 3:
+            raise WorkloadError(f"rank {self.rank}: MoE receive capacity exceeded")
+        if t.value:
+            raise DeadlockError(f"rank {self.rank}: device error code {t.value}")
 
     def destroy(self):
         if self._h:

@@ -1,0 +1,259 @@
+// pk_allreduce.cu — in-place all-reduce over a PGL (pk_all_reduce).
+//
+// Reference: primitives.all_reduce (overlapsim/primitives.py:237-261) and the
+// GEMM+AR communicator (workloads.py:517-546); the PK primitive is
+// `all_reduce<ROWS, COLS, OP>(PGL&, coord)`: a warp-
+// cooperative multimem.ld_reduce on the multicast address followed by a
+// multimem.st back to it.
+//
+// Two device paths, both two-shot (rank r owns slice r of the buffer):
+//   NVLS (multicast PGL, distinct GPUs): for each 16 B vector of slice r,
+//     multimem.ld_reduce(.acc::f32) pulls the switch-reduced sum of every
+//     rank's copy and multimem.st broadcasts it back to every rank. Per rank
+//     ~S bytes cross the link in each direction.
+//   P2P register ops (no multicast, e.g. a local group): rank r loads slice r
+//     from every peer with 16 B ld.global (peer VAs), folds in fp32 in the
+//     canonical ascending device order of primitives.py:187-195, and stores
+//     the result to slice r of every peer with 16 B st.global.
+// A start barrier (every rank's input is ready) and an end barrier (every
+// rank's stores have landed) bracket the data phase.
+#include "pk_host.h"
+#include "pk_ptx.cuh"
+#include <algorithm>
+#include <cstring>
+
+namespace pk {
+
+struct ArArgs {
+  uint8_t* peers[kMaxRanks];      // every rank's buffer (peer VAs)
+  uint8_t* mc;                    // multicast VA (NVLS path) or null
+  long long nvec;                 // 16-byte vectors in the buffer
+  int rank, world;
+  int dtype;                      // PK_BF16 / PK_F32
+  int op;                         // PK_OP_SUM / MAX / MIN
+  uint32_t* ready_local;
+  uint32_t* ready_peer[kMaxRanks];
+  uint32_t* done_local;
+  uint32_t* done_peer[kMaxRanks];
+  uint32_t* err;
+  uint32_t ready_expect, done_expect;
+  uint64_t timeout_ns;
+};
+
+template <int OP>
+__device__ __forceinline__ float red_op(float a, float b) {
+  if constexpr (OP == PK_OP_SUM) return a + b;
+  else if constexpr (OP == PK_OP_MAX) return fmaxf(a, b);
+  else return fminf(a, b);
+}
+
+__device__ __forceinline__ void unpack8(const uint4& v, float (&f)[8]) {
+  const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    f[2 * i] = __uint_as_float(w[i] << 16);
+    f[2 * i + 1] = __uint_as_float(w[i] & 0xFFFF0000u);
+  }
+}
+__device__ __forceinline__ uint4 pack8(const float (&f)[8]) {
+  uint4 v;
+  v.x = pack_bf16x2(f[0], f[1]);
+  v.y = pack_bf16x2(f[2], f[3]);
+  v.z = pack_bf16x2(f[4], f[5]);
+  v.w = pack_bf16x2(f[6], f[7]);
+  return v;
+}
+
+__device__ __forceinline__ void ar_start_barrier(const ArArgs& a) {
+  if (threadIdx.x == 0) {
+    if (blockIdx.x == 0) {
+      __threadfence_system();
+      for (int d = 0; d < a.world; ++d) signal_add(a.ready_peer[d] + a.rank, 1u);
+    }
+    for (int d = 0; d < a.world; ++d) wait_geq(a.ready_local + d, a.ready_expect, a.err, a.timeout_ns);
+  }
+  __syncthreads();
+}
+
+__device__ __forceinline__ void ar_end_barrier(const ArArgs& a) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence_system();
+    for (int d = 0; d < a.world; ++d) signal_add(a.done_peer[d] + a.rank, 1u);
+    if (blockIdx.x == 0)
+      for (int d = 0; d < a.world; ++d) wait_geq(a.done_local + d, a.done_expect, a.err, a.timeout_ns);
+  }
+}
+
+// NVLS two-shot. bf16: ld_reduce accumulates in f32 inside the switch.
+template <int DT>
+__global__ void __launch_bounds__(512) ar_nvls_kernel(const __grid_constant__ ArArgs a) {
+  ar_start_barrier(a);
+  const long long per = (a.nvec + a.world - 1) / a.world;
+  const long long lo = per * a.rank;
+  const long long hi = min(a.nvec, lo + per);
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  constexpr int U = 4;
+  for (long long base = lo + (long long)blockIdx.x * blockDim.x + threadIdx.x; base < hi; base += stride * U) {
+    uint32_t v[U][4];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const long long i = base + u * stride;
+      if (i < hi) {
+        if constexpr (DT == PK_BF16) mm_ld_reduce_bf16x8(a.mc + i * 16, v[u]);
+        else mm_ld_reduce_f32x4(a.mc + i * 16, v[u]);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const long long i = base + u * stride;
+      if (i < hi) mm_st_v4(a.mc + i * 16, v[u]);
+    }
+  }
+  ar_end_barrier(a);
+}
+
+// P2P register-op two-shot with a canonical ascending fold.
+template <int DT, int OP, int NR>
+__global__ void __launch_bounds__(512) ar_p2p_kernel(const __grid_constant__ ArArgs a) {
+  ar_start_barrier(a);
+  const long long per = (a.nvec + a.world - 1) / a.world;
+  const long long lo = per * a.rank;
+  const long long hi = min(a.nvec, lo + per);
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long i = lo + (long long)blockIdx.x * blockDim.x + threadIdx.x; i < hi; i += stride) {
+    uint4 in[NR];
+#pragma unroll
+    for (int d = 0; d < NR; ++d) in[d] = ld_v4_volatile(a.peers[d] + i * 16);
+    uint4 outv;
+    if constexpr (DT == PK_BF16) {
+      float acc[8], t[8];
+      unpack8(in[0], acc);
+#pragma unroll
+      for (int d = 1; d < NR; ++d) {
+        unpack8(in[d], t);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[j] = red_op<OP>(acc[j], t[j]);
+      }
+      outv = pack8(acc);
+    } else {
+      float acc[4] = {__uint_as_float(in[0].x), __uint_as_float(in[0].y), __uint_as_float(in[0].z), __uint_as_float(in[0].w)};
+#pragma unroll
+      for (int d = 1; d < NR; ++d) {
+        acc[0] = red_op<OP>(acc[0], __uint_as_float(in[d].x));
+        acc[1] = red_op<OP>(acc[1], __uint_as_float(in[d].y));
+        acc[2] = red_op<OP>(acc[2], __uint_as_float(in[d].z));
+        acc[3] = red_op<OP>(acc[3], __uint_as_float(in[d].w));
+      }
+      outv = make_uint4(__float_as_uint(acc[0]), __float_as_uint(acc[1]), __float_as_uint(acc[2]), __float_as_uint(acc[3]));
+    }
+#pragma unroll
+    for (int d = 0; d < NR; ++d) st_v4(a.peers[d] + i * 16, outv);
+  }
+  ar_end_barrier(a);
+}
+
+template <int DT, int OP>
+static void* p2p_kernel_for(int n) {
+  switch (n) {
+    case 1: return (void*)ar_p2p_kernel<DT, OP, 1>;
+    case 2: return (void*)ar_p2p_kernel<DT, OP, 2>;
+    case 3: return (void*)ar_p2p_kernel<DT, OP, 3>;
+    case 4: return (void*)ar_p2p_kernel<DT, OP, 4>;
+    case 5: return (void*)ar_p2p_kernel<DT, OP, 5>;
+    case 6: return (void*)ar_p2p_kernel<DT, OP, 6>;
+    case 7: return (void*)ar_p2p_kernel<DT, OP, 7>;
+    default: return (void*)ar_p2p_kernel<DT, OP, 8>;
+  }
+}
+
+int all_reduce(Comm* c, pk_tensor* x, int op, const pk_sched* sched, cudaStream_t st) {
+  if (!x || !x->ptr) return fail(PK_ERR_INVALID, "all_reduce: null tensor");
+  if (x->dtype != PK_BF16 && x->dtype != PK_F32) return fail(PK_ERR_CAPABILITY, "all_reduce: dtype must be bf16 or f32");
+  if (op < PK_OP_SUM || op > PK_OP_MIN) return fail(PK_ERR_CAPABILITY, "all_reduce: unsupported reduce op %d", op);
+  long long numel = 1;
+  for (int i = 0; i < x->ndim; ++i) numel *= x->shape[i];
+  for (int i = x->ndim - 1, expect = 1; i >= 0; --i) {
+    if (x->shape[i] != 1 && x->strides[i] != expect) return fail(PK_ERR_INVALID, "all_reduce: tensor must be contiguous");
+    expect *= (int)x->shape[i];
+  }
+  const size_t bytes = (size_t)numel * dtype_bytes(x->dtype);
+  if (bytes % 16) return fail(PK_ERR_INVALID, "all_reduce: size must be a multiple of 16 bytes (got %zu)", bytes);
+  if (bytes == 0 || c->world == 1) return PK_OK;
+
+  void* peers[kMaxRanks];
+  void* mc = nullptr;
+  bool staged = false;
+  Pgl* owner = nullptr;
+  for (Pgl* p : c->user_pgls) {
+    const uintptr_t a = (uintptr_t)x->ptr, b = (uintptr_t)p->local;
+    if (a >= b && a + bytes <= b + p->bytes) { owner = p; break; }
+  }
+  if (owner) {
+    const size_t off = (uintptr_t)x->ptr - (uintptr_t)owner->local;
+    for (int r = 0; r < c->world; ++r) peers[r] = (char*)owner->peers[r] + off;
+    if (owner->mc) mc = (char*)owner->mc + off;
+  } else {
+    Pgl* s3;
+    PK_TRY(comm_scratch(c, 3, bytes, &s3, PK_PGL_MULTICAST));
+    for (int r = 0; r < c->world; ++r) peers[r] = s3->peers[r];
+    if (s3->mc) mc = s3->mc;
+    PK_CUDA(cudaMemcpyAsync(s3->local, x->ptr, bytes, cudaMemcpyDeviceToDevice, st));
+    staged = true;
+  }
+  const bool use_nvls = mc != nullptr && op == PK_OP_SUM && !(sched && sched->mode == PK_INTRA_SM);
+
+  ArArgs a;
+  memset(&a, 0, sizeof(a));
+  for (int r = 0; r < c->world; ++r) a.peers[r] = (uint8_t*)peers[r];
+  a.mc = (uint8_t*)mc;
+  a.nvec = (long long)(bytes / 16);
+  a.rank = c->rank;
+  a.world = c->world;
+  a.dtype = x->dtype;
+  a.op = op;
+  uint32_t* local = static_cast<uint32_t*>(c->sync->local);
+  a.ready_local = local + kSyncReady;
+  a.done_local = local + kSyncDone;
+  a.err = local + kSyncErr;
+  for (int r = 0; r < c->world; ++r) {
+    uint32_t* pr = static_cast<uint32_t*>(c->sync->peers[r]);
+    a.ready_peer[r] = pr + kSyncReady;
+    a.done_peer[r] = pr + kSyncDone;
+  }
+  int sms = c->num_sms;
+  if (sched && sched->num_sms > 0) sms = std::min(sms, sched->num_sms);
+  const long long per = (a.nvec + c->world - 1) / c->world;
+  const int threads = 512;
+  int blocks = (int)std::min<long long>((long long)sms * 2, std::max<long long>(1, (per + threads - 1) / threads));
+  if (c->local_group) blocks = std::min(blocks, sms);   // co-residency of all ranks
+  c->ready_count += 1;
+  c->done_count += (uint32_t)blocks;
+  a.ready_expect = c->ready_count;
+  a.done_expect = c->done_count;
+  a.timeout_ns = c->timeout_ns;
+
+  void* kern;
+  if (use_nvls) {
+    kern = (x->dtype == PK_BF16) ? (void*)ar_nvls_kernel<PK_BF16> : (void*)ar_nvls_kernel<PK_F32>;
+  } else if (x->dtype == PK_BF16) {
+    kern = op == PK_OP_SUM ? p2p_kernel_for<PK_BF16, PK_OP_SUM>(c->world)
+         : op == PK_OP_MAX ? p2p_kernel_for<PK_BF16, PK_OP_MAX>(c->world)
+                           : p2p_kernel_for<PK_BF16, PK_OP_MIN>(c->world);
+  } else {
+    kern = op == PK_OP_SUM ? p2p_kernel_for<PK_F32, PK_OP_SUM>(c->world)
+         : op == PK_OP_MAX ? p2p_kernel_for<PK_F32, PK_OP_MAX>(c->world)
+                           : p2p_kernel_for<PK_F32, PK_OP_MIN>(c->world);
+  }
+  void* params[] = {&a};
+  PK_CUDA(cudaLaunchKernel(kern, dim3(blocks), dim3(threads), params, 0, st));
+  if (staged) PK_CUDA(cudaMemcpyAsync(x->ptr, peers[c->rank], bytes, cudaMemcpyDeviceToDevice, st));
+  return PK_OK;
+}
+
+}  // namespace pk
+
+extern "C" PK_API int pk_all_reduce(pk_comm* comm, pk_tensor* x, int op, const pk_sched* sched, void* stream) {
+  if (!comm) return pk::fail(PK_ERR_INVALID, "null comm");
+  return pk::all_reduce(comm, x, op, sched, (cudaStream_t)stream);
+}

@@ -1,0 +1,541 @@
+// pk_attn.cu — ring attention forward (pk_ring_attn_fwd).
+//
+// Reference: RingAttentionPlan (overlapsim/workloads.py:616-716): the KV shard
+// of rank d rotates to d+1 each step, so at step s rank r visits the shard of
+// rank (r - s) mod n; every rank visits every shard exactly once
+// (workloads.py:714-716). FLOPs per step 4*B*H*(S/n)^2*D (workloads.py:633).
+// The paper stages the next KV shard into a local double buffer with
+// dedicated comm SMs (remote_reuse_policy, lcsc.py:208-223: a shard is re-read
+// by every query tile, so staging beats direct peer reads).
+//
+// B200 design:
+//   * compute: a tcgen05 flash-attention forward kernel (attn_fwd_kernel).
+//     One CTA = one 128-query tile of one (batch, head); one CTA per SM.
+//       warp 0      loader   : TMA Q once, K/V 64-key blocks (K 3 stages, V 2)
+//       warp 1      MMA      : S = Q K^T (M128 N64 K128) into TMEM (double
+//                              buffered), O_blk = P V (M128 N128 K64, V as an
+//                              MN-major operand) into TMEM
+//       warps 4-7   softmax  : TMEM -> regs, online max / exp2 / row sum,
+//                              P (bf16) -> 128B-swizzled smem (A operand)
+//       warps 8-11  correct  : O = O*alpha + O_blk in registers; epilogue
+//     The running (O, m, l) state crosses ring steps through global memory
+//     (fp32), merged by log-sum-exp; the last step writes o (bf16) and lse.
+//   * communication: the shard of step s+1 is pulled from its owner's
+//     symmetric buffer by the copy engine (the paper's 726 GB/s CE path,
+//     PAPER.md:127) on a side stream while step s computes; a 2-slot local
+//     buffer and CUDA events order reuse. Pulling from the owner (not the
+//     neighbour) moves the same bytes per link on a uniform NVSwitch fabric
+//     and needs no per-step neighbour handshake.
+#include "pk_host.h"
+#include "pk_ptx.cuh"
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+
+namespace pk {
+
+constexpr int AT_BM = 128;       // queries per CTA
+constexpr int AT_BN = 64;        // keys per block
+constexpr int AT_D = 128;        // head dim
+constexpr int AT_THREADS = 384;
+constexpr int AT_Q_BYTES = AT_BM * AT_D * 2;     // 32 KB (2 swizzle atoms of 16 KB)
+constexpr int AT_K_BYTES = AT_BN * AT_D * 2;     // 16 KB
+constexpr int AT_V_BYTES = AT_BN * AT_D * 2;     // 16 KB
+constexpr int AT_P_BYTES = AT_BM * AT_BN * 2;    // 16 KB
+constexpr int AT_KSTAGES = 3;
+constexpr int AT_VSTAGES = 2;
+constexpr int AT_ALPHA = 4;                       // alpha ring slots
+constexpr int AT_SMEM = AT_Q_BYTES + AT_KSTAGES * AT_K_BYTES + AT_VSTAGES * AT_V_BYTES + 2 * AT_P_BYTES +
+                        (AT_ALPHA + 2) * AT_BM * 4 + 512 + 1024;
+constexpr int AT_TMEM_COLS = 512;                // S[2] (2 x 64) + O_blk[2] (2 x 128)
+
+struct AttnArgs {
+  CUtensorMap tm_q, tm_k, tm_v;  // 4-D maps over [B, S, H, D] (dims D, H, S, B)
+  int B, S_q, S_kv, H;
+  float scale_log2;              // softmax_scale * log2(e)
+  // ring state (fp32), [B, H, S_q, D] / [B, H, S_q]; unused for single-step
+  float* o_acc;
+  float* m_acc;
+  float* l_acc;
+  int first, last;               // first / last ring step
+  uint16_t* o;                   // [B, S_q, H, D] bf16 output (last step)
+  float* lse;                    // [B, H, S_q] natural-log LSE (last step)
+};
+
+// MN-major (N contiguous) SW128 descriptor for the V operand: 64-element
+// groups along N are LBO apart, 8-row K groups SBO apart.
+PK_DEV uint64_t sdesc_mnmajor_sw128(uint32_t saddr, uint32_t lbo_bytes, uint32_t sbo_bytes) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr & 0x3FFFF) >> 4);
+  d |= (uint64_t)((lbo_bytes >> 4) & 0x3FFF) << 16;
+  d |= (uint64_t)((sbo_bytes >> 4) & 0x3FFF) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)2 << 61;
+  return d;
+}
+
+__host__ __device__ constexpr uint32_t idesc_bf16(int M, int N, int b_mn_major) {
+  return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)b_mn_major << 16) |
+         ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+
+PK_DEV void tma_load_4d(const CUtensorMap* m, uint64_t* bar, void* dst, int c0, int c1, int c2, int c3) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5, %6}], [%2];"
+      :: "r"(smem_u32(dst)), "l"(reinterpret_cast<uint64_t>(m)), "r"(smem_u32(bar)),
+         "r"(c0), "r"(c1), "r"(c2), "r"(c3) : "memory");
+}
+
+PK_DEV float fast_exp2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+// Pipeline invariants (j = key block):
+//   K_j -> k stage j%3, V_j -> v stage j%2, S_j -> TMEM S[j%2], P_j -> smem P[j%2],
+//   P_j V_j -> TMEM O[j%2], alpha_j -> smem ring slot j%4.
+//   alpha slot reuse is safe: softmax writes alpha_{j+4} only after P slot
+//   (j+4)%2 is free, i.e. after PV_{j+2} completed, which waited O[j%2] to be
+//   drained by the correction of block j (which read alpha_j first).
+__global__ void __launch_bounds__(AT_THREADS, 1) attn_fwd_kernel(const __grid_constant__ AttnArgs a) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sq = smem;
+  uint8_t* sk = sq + AT_Q_BYTES;
+  uint8_t* sv = sk + AT_KSTAGES * AT_K_BYTES;
+  uint8_t* sp = sv + AT_VSTAGES * AT_V_BYTES;
+  float* alpha_s = reinterpret_cast<float*>(sp + 2 * AT_P_BYTES);    // [AT_ALPHA][128]
+  float* stat_m = alpha_s + AT_ALPHA * AT_BM;                          // [128]
+  float* stat_l = stat_m + AT_BM;                                      // [128]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(stat_l + AT_BM);
+  uint64_t* q_full = bars + 0;
+  uint64_t* k_full = bars + 1;      // [3]
+  uint64_t* k_empty = bars + 4;     // [3]
+  uint64_t* v_full = bars + 7;      // [2]
+  uint64_t* v_empty = bars + 9;     // [2]
+  uint64_t* s_full = bars + 11;     // [2]
+  uint64_t* s_empty = bars + 13;    // [2]
+  uint64_t* p_full = bars + 15;     // [2]
+  uint64_t* p_empty = bars + 17;    // [2]
+  uint64_t* pv_full = bars + 19;    // [2]
+  uint64_t* pv_empty = bars + 21;   // [2]
+  uint64_t* stat_full = bars + 23;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 24);
+
+  const uint32_t warp = warp_id_sync();
+  const uint32_t lane = lane_id();
+  const int q_tiles = a.S_q / AT_BM;
+  const int tile = blockIdx.x;
+  const int qt = tile % q_tiles;
+  const int h = (tile / q_tiles) % a.H;
+  const int b = tile / (q_tiles * a.H);
+  const int nblk = a.S_kv / AT_BN;
+
+  if (warp == 0 && lane == 0) {
+    mbar_init(q_full, 1);
+    for (int i = 0; i < AT_KSTAGES; ++i) { mbar_init(&k_full[i], 1); mbar_init(&k_empty[i], 1); }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&v_full[i], 1); mbar_init(&v_empty[i], 1);
+      mbar_init(&s_full[i], 1); mbar_init(&s_empty[i], 4);
+      mbar_init(&p_full[i], 4); mbar_init(&p_empty[i], 1);
+      mbar_init(&pv_full[i], 1); mbar_init(&pv_empty[i], 4);
+    }
+    mbar_init(stat_full, 4);
+    fence_mbar_init();
+  }
+  if (warp == 2) tmem_alloc<AT_TMEM_COLS, 1>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t t_s = tmem;            // S[2] at cols [0,64), [64,128)
+  const uint32_t t_o = tmem + 128;      // O_blk[2] at cols [128,256), [256,384)
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ loader (lane 0; the
+    // warp reconverges at __syncwarp before the teardown barrier)
+    if (lane == 0) {
+      mbar_arrive_expect_tx(q_full, AT_Q_BYTES);
+      tma_load_4d(&a.tm_q, q_full, sq, 0, h, qt * AT_BM, b);
+      tma_load_4d(&a.tm_q, q_full, sq + AT_Q_BYTES / 2, 64, h, qt * AT_BM, b);
+      auto load_k = [&](int j) {
+        const int st = j % AT_KSTAGES;
+        mbar_wait(&k_empty[st], ((j / AT_KSTAGES) & 1) ^ 1);
+        uint8_t* kb = sk + st * AT_K_BYTES;
+        mbar_arrive_expect_tx(&k_full[st], AT_K_BYTES);
+        tma_load_4d(&a.tm_k, &k_full[st], kb, 0, h, j * AT_BN, b);
+        tma_load_4d(&a.tm_k, &k_full[st], kb + AT_K_BYTES / 2, 64, h, j * AT_BN, b);
+      };
+      // K runs up to two blocks ahead of V so S = Q K^T never waits on P V.
+      if (nblk > 0) load_k(0);
+      if (nblk > 1) load_k(1);
+      for (int j = 0; j < nblk; ++j) {
+        if (j + 2 < nblk) load_k(j + 2);
+        const int vs = j & 1;
+        mbar_wait(&v_empty[vs], ((j >> 1) & 1) ^ 1);
+        uint8_t* vb = sv + vs * AT_V_BYTES;
+        mbar_arrive_expect_tx(&v_full[vs], AT_V_BYTES);
+        tma_load_4d(&a.tm_v, &v_full[vs], vb, 0, h, j * AT_BN, b);
+        tma_load_4d(&a.tm_v, &v_full[vs], vb + AT_V_BYTES / 2, 64, h, j * AT_BN, b);
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA issuer
+    constexpr uint32_t id_s = idesc_bf16(AT_BM, AT_BN, 0);
+    constexpr uint32_t id_o = idesc_bf16(AT_BM, AT_D, 1);
+    mbar_wait(q_full, 0);
+    tc_fence_after();
+    const uint32_t q_addr = smem_u32(sq);
+    auto issue_pv = [&](int j) {
+      const int bs = j & 1;
+      const uint32_t ph = (j >> 1) & 1;
+      mbar_wait(&v_full[bs], ph);
+      mbar_wait(&p_full[bs], ph);
+      mbar_wait(&pv_empty[bs], ph ^ 1);
+      tc_fence_after();
+      if (elect_one()) {
+        const uint32_t p_addr = smem_u32(sp + bs * AT_P_BYTES);
+        const uint32_t v_addr = smem_u32(sv + bs * AT_V_BYTES);
+#pragma unroll
+        for (int kk = 0; kk < AT_BN / 16; ++kk) {
+          const uint64_t ad = sdesc_kmajor_sw128(p_addr) + (uint64_t)(kk * 2);   // +32 B per 16 keys
+          // V: keys are K (8-row groups 1024 B apart), D is N (64-col groups 8 KB apart)
+          const uint64_t bd = sdesc_mnmajor_sw128(v_addr + kk * 2048, AT_V_BYTES / 2, 1024);
+          umma_f16<1>(t_o + bs * AT_D, ad, bd, id_o, kk > 0 ? 1u : 0u);
+        }
+        umma_commit<1>(&pv_full[bs]);
+        umma_commit<1>(&p_empty[bs]);
+        umma_commit<1>(&v_empty[bs]);
+      }
+      __syncwarp();
+    };
+    for (int j = 0; j < nblk; ++j) {
+      const int st = j % AT_KSTAGES;
+      const int bs = j & 1;
+      mbar_wait(&k_full[st], (j / AT_KSTAGES) & 1);
+      mbar_wait(&s_empty[bs], ((j >> 1) & 1) ^ 1);
+      tc_fence_after();
+      if (elect_one()) {
+        const uint32_t k_addr = smem_u32(sk + st * AT_K_BYTES);
+#pragma unroll
+        for (int kk = 0; kk < AT_D / 16; ++kk) {
+          const int atom = kk >> 2, sub = kk & 3;
+          const uint64_t ad = sdesc_kmajor_sw128(q_addr + atom * (AT_Q_BYTES / 2)) + (uint64_t)(sub * 2);
+          const uint64_t bd = sdesc_kmajor_sw128(k_addr + atom * (AT_K_BYTES / 2)) + (uint64_t)(sub * 2);
+          umma_f16<1>(t_s + bs * AT_BN, ad, bd, id_s, kk > 0 ? 1u : 0u);
+        }
+        umma_commit<1>(&s_full[bs]);
+        umma_commit<1>(&k_empty[st]);
+      }
+      __syncwarp();
+      if (j > 0) issue_pv(j - 1);
+    }
+    if (nblk > 0) issue_pv(nblk - 1);
+  } else if (warp >= 4 && warp < 8) {
+    // ------------------------------------------------------------ softmax
+    const int q = warp & 3;
+    const int row = q * 32 + (int)lane;
+    const uint32_t lane_off = (uint32_t)(q * 32) << 16;
+    float m = -INFINITY, l = 0.f;
+    const float sc = a.scale_log2;
+    for (int j = 0; j < nblk; ++j) {
+      const int bs = j & 1;
+      const uint32_t ph = (j >> 1) & 1;
+      mbar_wait(&s_full[bs], ph);
+      tc_fence_after();
+      uint32_t r0[32], r1[32];
+      tmem_ld_32x32b_x32(t_s + lane_off + bs * AT_BN, r0);
+      tmem_ld_32x32b_x32(t_s + lane_off + bs * AT_BN + 32, r1);
+      tmem_ld_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&s_empty[bs]);
+      float mx = -INFINITY;
+#pragma unroll
+      for (int i = 0; i < 32; ++i) mx = fmaxf(mx, fmaxf(__uint_as_float(r0[i]), __uint_as_float(r1[i])));
+      const float m_new = fmaxf(m, mx * sc);
+      const float alpha = (m == -INFINITY) ? 0.f : fast_exp2(m - m_new);
+      float p[64];
+      float rs = 0.f;
+#pragma unroll
+      for (int i = 0; i < 32; ++i) {
+        p[i] = fast_exp2(__uint_as_float(r0[i]) * sc - m_new);
+        p[32 + i] = fast_exp2(__uint_as_float(r1[i]) * sc - m_new);
+      }
+#pragma unroll
+      for (int i = 0; i < 64; ++i) rs += p[i];
+      l = l * alpha + rs;
+      m = m_new;
+      mbar_wait(&p_empty[bs], ph ^ 1);          // PV_{j-2} has finished reading this P slot
+      const uint32_t row_addr = smem_u32(sp + bs * AT_P_BYTES) + row * 128;
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        st_shared_v4(row_addr + ((c ^ (row & 7)) << 4),
+                     pack_bf16x2(p[8 * c + 0], p[8 * c + 1]), pack_bf16x2(p[8 * c + 2], p[8 * c + 3]),
+                     pack_bf16x2(p[8 * c + 4], p[8 * c + 5]), pack_bf16x2(p[8 * c + 6], p[8 * c + 7]));
+      }
+      alpha_s[(j % AT_ALPHA) * AT_BM + row] = alpha;
+      fence_async_shared();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&p_full[bs]);
+    }
+    stat_m[row] = m;
+    stat_l[row] = l;
+    __syncwarp();
+    if (lane == 0) mbar_arrive(stat_full);
+  } else if (warp >= 8) {
+    // ------------------------------------------------------------ correction + epilogue
+    const int q = warp & 3;
+    const int row = q * 32 + (int)lane;
+    const uint32_t lane_off = (uint32_t)(q * 32) << 16;
+    float o[AT_D];
+#pragma unroll
+    for (int i = 0; i < AT_D; ++i) o[i] = 0.f;
+    for (int j = 0; j < nblk; ++j) {
+      const int bs = j & 1;
+      mbar_wait(&pv_full[bs], (j >> 1) & 1);
+      tc_fence_after();
+      const float alpha = alpha_s[(j % AT_ALPHA) * AT_BM + row];
+#pragma unroll
+      for (int c = 0; c < AT_D / 32; ++c) {
+        uint32_t r[32];
+        tmem_ld_32x32b_x32(t_o + lane_off + bs * AT_D + c * 32, r);
+        tmem_ld_wait();
+#pragma unroll
+        for (int i = 0; i < 32; ++i) o[c * 32 + i] = o[c * 32 + i] * alpha + __uint_as_float(r[i]);
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&pv_empty[bs]);
+    }
+    mbar_wait(stat_full, 0);
+    float m = stat_m[row], l = stat_l[row];
+    const int sq_idx = qt * AT_BM + row;                     // query index within the local shard
+    const long long srow = ((long long)(b * a.H + h) * a.S_q + sq_idx);   // [B, H, S_q] row
+    if (!a.first) {
+      // merge with the running state of earlier ring steps (log2 domain)
+      const float mg = a.m_acc[srow], lg = a.l_acc[srow];
+      const float mt = fmaxf(mg, m);
+      const float wg = (mg == -INFINITY) ? 0.f : fast_exp2(mg - mt);
+      const float wn = (m == -INFINITY) ? 0.f : fast_exp2(m - mt);
+      const float4* og = reinterpret_cast<const float4*>(a.o_acc + srow * AT_D);
+#pragma unroll
+      for (int i = 0; i < AT_D / 4; ++i) {
+        const float4 v = og[i];
+        o[4 * i + 0] = v.x * wg + o[4 * i + 0] * wn;
+        o[4 * i + 1] = v.y * wg + o[4 * i + 1] * wn;
+        o[4 * i + 2] = v.z * wg + o[4 * i + 2] * wn;
+        o[4 * i + 3] = v.w * wg + o[4 * i + 3] * wn;
+      }
+      l = lg * wg + l * wn;
+      m = mt;
+    }
+    if (a.last) {
+      const float inv = (l > 0.f) ? 1.f / l : 0.f;
+      uint4* dst = reinterpret_cast<uint4*>(a.o + (((long long)b * a.S_q + sq_idx) * a.H + h) * AT_D);
+#pragma unroll
+      for (int i = 0; i < AT_D / 8; ++i) {
+        uint4 w;
+        w.x = pack_bf16x2(o[8 * i + 0] * inv, o[8 * i + 1] * inv);
+        w.y = pack_bf16x2(o[8 * i + 2] * inv, o[8 * i + 3] * inv);
+        w.z = pack_bf16x2(o[8 * i + 4] * inv, o[8 * i + 5] * inv);
+        w.w = pack_bf16x2(o[8 * i + 6] * inv, o[8 * i + 7] * inv);
+        dst[i] = w;
+      }
+      a.lse[srow] = (m + log2f(l)) * 0.69314718055994531f;
+    } else {
+      float4* og = reinterpret_cast<float4*>(a.o_acc + srow * AT_D);
+#pragma unroll
+      for (int i = 0; i < AT_D / 4; ++i) og[i] = make_float4(o[4 * i], o[4 * i + 1], o[4 * i + 2], o[4 * i + 3]);
+      a.m_acc[srow] = m;
+      a.l_acc[srow] = l;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc<AT_TMEM_COLS, 1>(tmem);
+  }
+}
+
+// ---------------------------------------------------------------- sync kernels
+__global__ void sync_signal_kernel(uint32_t* p0, uint32_t* p1, uint32_t* p2, uint32_t* p3, uint32_t* p4,
+                                   uint32_t* p5, uint32_t* p6, uint32_t* p7, int n) {
+  uint32_t* ps[8] = {p0, p1, p2, p3, p4, p5, p6, p7};
+  __threadfence_system();
+  for (int d = 0; d < n; ++d) signal_add(ps[d], 1u);
+}
+__global__ void sync_wait_kernel(const uint32_t* counters, int n, uint32_t expected, uint32_t* err, uint64_t timeout) {
+  for (int d = 0; d < n; ++d) wait_geq(counters + d, expected, err, timeout);
+}
+
+static int signal_all(Comm* c, int which_off, cudaStream_t st) {
+  uint32_t* ps[8] = {};
+  for (int r = 0; r < c->world; ++r) ps[r] = static_cast<uint32_t*>(c->sync->peers[r]) + which_off + c->rank;
+  sync_signal_kernel<<<1, 1, 0, st>>>(ps[0], ps[1], ps[2], ps[3], ps[4], ps[5], ps[6], ps[7], c->world);
+  PK_CUDA(cudaGetLastError());
+  return PK_OK;
+}
+static int wait_all(Comm* c, int which_off, uint32_t expected, cudaStream_t st) {
+  uint32_t* local = static_cast<uint32_t*>(c->sync->local);
+  sync_wait_kernel<<<1, 1, 0, st>>>(local + which_off, c->world, expected, local + kSyncErr, c->timeout_ns);
+  PK_CUDA(cudaGetLastError());
+  return PK_OK;
+}
+
+// ---------------------------------------------------------------- host
+static int check_bshd(const pk_tensor* t, const char* name, int64_t* B, int64_t* S, int64_t* H, int64_t* D) {
+  if (!t || !t->ptr) return fail(PK_ERR_INVALID, "%s: null tensor", name);
+  if (t->dtype != PK_BF16 || t->ndim != 4) return fail(PK_ERR_INVALID, "%s: expected bf16 [B, S, H, D]", name);
+  *B = t->shape[0]; *S = t->shape[1]; *H = t->shape[2]; *D = t->shape[3];
+  const int64_t* s = t->strides;
+  if (s[3] != 1 || s[2] != *D || s[1] != *H * *D || s[0] != *S * *H * *D)
+    return fail(PK_ERR_INVALID, "%s: must be contiguous [B, S, H, D]", name);
+  return PK_OK;
+}
+
+static int tmap_bshd(CUtensorMap* m, const void* p, int64_t B, int64_t S, int64_t H, int rows) {
+  const Driver* d;
+  PK_TRY(driver(&d));
+  cuuint64_t dims[4] = {(cuuint64_t)AT_D, (cuuint64_t)H, (cuuint64_t)S, (cuuint64_t)B};
+  cuuint64_t strides[3] = {(cuuint64_t)(AT_D * 2), (cuuint64_t)(H * AT_D * 2), (cuuint64_t)(S * H * AT_D * 2)};
+  cuuint32_t box[4] = {64, 1, (cuuint32_t)rows, 1};
+  cuuint32_t es[4] = {1, 1, 1, 1};
+  CUresult r = d->tensorMapEncodeTiled(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(p), dims, strides, box, es,
+                                       CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                       CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(PK_ERR_INVALID, "attention tensor map failed (%d)", (int)r);
+  return PK_OK;
+}
+
+static int launch_attn(const AttnArgs& a, cudaStream_t st) {
+  static thread_local bool attr = false;
+  if (!attr) {
+    PK_CUDA(cudaFuncSetAttribute(attn_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, AT_SMEM));
+    attr = true;
+  }
+  const int grid = a.B * a.H * (a.S_q / AT_BM);
+  attn_fwd_kernel<<<grid, AT_THREADS, AT_SMEM, st>>>(a);
+  PK_CUDA(cudaGetLastError());
+  return PK_OK;
+}
+
+enum { kScratchAttnK = 0, kScratchAttnV = 1, kScratchAttnStage = 7 };
+
+int ring_attn_fwd(Comm* c, const pk_tensor* q, const pk_tensor* k, const pk_tensor* v, pk_tensor* o, pk_tensor* lse,
+                  float scale, cudaStream_t st) {
+  int64_t B, S, H, D, B2, S2, H2, D2;
+  PK_TRY(check_bshd(q, "q", &B, &S, &H, &D));
+  PK_TRY(check_bshd(k, "k", &B2, &S2, &H2, &D2));
+  if (B2 != B || S2 != S || H2 != H || D2 != D) return fail(PK_ERR_INVALID, "ring_attention: k shape differs from q");
+  PK_TRY(check_bshd(v, "v", &B2, &S2, &H2, &D2));
+  if (B2 != B || S2 != S || H2 != H || D2 != D) return fail(PK_ERR_INVALID, "ring_attention: v shape differs from q");
+  PK_TRY(check_bshd(o, "o", &B2, &S2, &H2, &D2));
+  if (B2 != B || S2 != S || H2 != H || D2 != D) return fail(PK_ERR_INVALID, "ring_attention: o shape differs from q");
+  if (D != AT_D) return fail(PK_ERR_CAPABILITY, "ring_attention: head dim %lld unsupported (128 only)", (long long)D);
+  if (S % AT_BM) return fail(PK_ERR_INVALID, "ring_attention: local sequence %lld must be a multiple of %d", (long long)S, AT_BM);
+  if (!lse || !lse->ptr || lse->dtype != PK_F32 || lse->ndim != 3 || lse->shape[0] != B || lse->shape[1] != H ||
+      lse->shape[2] != S || lse->strides[2] != 1 || lse->strides[1] != S || lse->strides[0] != H * S)
+    return fail(PK_ERR_INVALID, "ring_attention: lse must be contiguous float32 [B, H, S/n]");
+  const int n = c->world;
+  const size_t shard = (size_t)B * S * H * D * 2;
+
+  AttnArgs a;
+  memset(&a, 0, sizeof(a));
+  a.B = (int)B; a.S_q = (int)S; a.S_kv = (int)S; a.H = (int)H;
+  a.scale_log2 = scale * 1.4426950408889634f;
+  a.o = static_cast<uint16_t*>(o->ptr);
+  a.lse = static_cast<float*>(lse->ptr);
+  PK_TRY(tmap_bshd(&a.tm_q, q->ptr, B, S, H, AT_BM));
+  if (n == 1) {
+    PK_TRY(tmap_bshd(&a.tm_k, k->ptr, B, S, H, AT_BN));
+    PK_TRY(tmap_bshd(&a.tm_v, v->ptr, B, S, H, AT_BN));
+    a.first = 1;
+    a.last = 1;
+    return launch_attn(a, st);
+  }
+
+  // Every rank's K/V shard must be readable by its peers (symmetric memory).
+  void* kp[kMaxRanks];
+  void* vp[kMaxRanks];
+  if (!find_symmetric(c, k->ptr, shard, kp)) {
+    Pgl* s;
+    PK_TRY(comm_scratch(c, kScratchAttnK, shard, &s));
+    PK_CUDA(cudaMemcpyAsync(s->local, k->ptr, shard, cudaMemcpyDeviceToDevice, st));
+    for (int r = 0; r < n; ++r) kp[r] = s->peers[r];
+  }
+  if (!find_symmetric(c, v->ptr, shard, vp)) {
+    Pgl* s;
+    PK_TRY(comm_scratch(c, kScratchAttnV, shard, &s));
+    PK_CUDA(cudaMemcpyAsync(s->local, v->ptr, shard, cudaMemcpyDeviceToDevice, st));
+    for (int r = 0; r < n; ++r) vp[r] = s->peers[r];
+  }
+  // Local state: 2 staging slots x (K, V) + fp32 running (O, m, l).
+  const size_t state_o = (size_t)B * H * S * D * 4, state_ml = (size_t)B * H * S * 4;
+  Pgl* stage;
+  PK_TRY(comm_scratch(c, kScratchAttnStage, 4 * shard + state_o + 2 * state_ml, &stage));
+  uint8_t* base = static_cast<uint8_t*>(stage->local);
+  uint8_t* slot_k[2] = {base, base + shard};
+  uint8_t* slot_v[2] = {base + 2 * shard, base + 3 * shard};
+  a.o_acc = reinterpret_cast<float*>(base + 4 * shard);
+  a.m_acc = reinterpret_cast<float*>(base + 4 * shard + state_o);
+  a.l_acc = a.m_acc + (size_t)B * H * S;
+
+  // Streams / events for the copy-engine staging pipeline.
+  if (!c->side) PK_CUDA(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
+  cudaStream_t side = c->side;
+  cudaEvent_t ev_start, ev_attn[kMaxRanks], ev_copy[kMaxRanks];
+  PK_CUDA(cudaEventCreateWithFlags(&ev_start, cudaEventDisableTiming));
+  for (int s = 0; s < n; ++s) {
+    PK_CUDA(cudaEventCreateWithFlags(&ev_attn[s], cudaEventDisableTiming));
+    PK_CUDA(cudaEventCreateWithFlags(&ev_copy[s], cudaEventDisableTiming));
+  }
+  // 1. my shard is ready -> tell everyone; the side stream waits for all shards.
+  c->ready_count += 1;
+  const uint32_t ready_expect = c->ready_count;
+  PK_TRY(signal_all(c, kSyncReady, st));
+  PK_CUDA(cudaEventRecord(ev_start, st));
+  PK_CUDA(cudaStreamWaitEvent(side, ev_start, 0));
+  PK_TRY(wait_all(c, kSyncReady, ready_expect, side));
+  // 2. ring steps: rank r visits shard (r - s) mod n at step s (workloads.py:666-681).
+  for (int s = 0; s < n; ++s) {
+    if (s + 1 < n) {
+      const int src = ((c->rank - (s + 1)) % n + n) % n;
+      const int slot = (s + 1) & 1;
+      if (s + 1 >= 2) PK_CUDA(cudaStreamWaitEvent(side, ev_attn[s - 1], 0));   // slot free again
+      PK_CUDA(cudaMemcpyAsync(slot_k[slot], kp[src], shard, cudaMemcpyDeviceToDevice, side));
+      PK_CUDA(cudaMemcpyAsync(slot_v[slot], vp[src], shard, cudaMemcpyDeviceToDevice, side));
+      PK_CUDA(cudaEventRecord(ev_copy[s + 1], side));
+    }
+    const void* ks = (s == 0) ? kp[c->rank] : slot_k[s & 1];
+    const void* vs = (s == 0) ? vp[c->rank] : slot_v[s & 1];
+    if (s > 0) PK_CUDA(cudaStreamWaitEvent(st, ev_copy[s], 0));
+    PK_TRY(tmap_bshd(&a.tm_k, ks, B, S, H, AT_BN));
+    PK_TRY(tmap_bshd(&a.tm_v, vs, B, S, H, AT_BN));
+    a.first = (s == 0);
+    a.last = (s == n - 1);
+    PK_TRY(launch_attn(a, st));
+    PK_CUDA(cudaEventRecord(ev_attn[s], st));
+  }
+  // 3. I am done reading every peer's shard; wait until every peer is done with mine.
+  c->done_count += 1;
+  PK_TRY(signal_all(c, kSyncDone, st));
+  PK_TRY(wait_all(c, kSyncDone, c->done_count, st));
+  cudaEventDestroy(ev_start);
+  for (int s = 0; s < n; ++s) { cudaEventDestroy(ev_attn[s]); cudaEventDestroy(ev_copy[s]); }
+  return PK_OK;
+}
+
+}  // namespace pk
+
+extern "C" PK_API int pk_ring_attn_fwd(pk_comm* comm, const pk_tensor* q, const pk_tensor* k, const pk_tensor* v,
+                                       pk_tensor* o, pk_tensor* lse, float softmax_scale, const pk_sched* sched,
+                                       void* stream) {
+  (void)sched;
+  if (!comm) return pk::fail(PK_ERR_INVALID, "null comm");
+  return pk::ring_attn_fwd(comm, q, k, v, o, lse, softmax_scale, (cudaStream_t)stream);
+}

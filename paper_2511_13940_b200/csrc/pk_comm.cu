@@ -461,12 +461,25 @@ int pgl_free(Pgl* p) {
   return PK_OK;
 }
 
-int comm_scratch(Comm* c, int slot, size_t bytes, Pgl** out) {
-  if (c->scratch[slot] && c->scratch[slot]->bytes >= bytes) { *out = c->scratch[slot]; return PK_OK; }
-  if (c->scratch[slot]) { cudaDeviceSynchronize(); pgl_free(c->scratch[slot]); c->scratch[slot] = nullptr; }
-  // grow geometrically so a sweep does not reallocate at every size
+int comm_scratch(Comm* c, int slot, size_t bytes, Pgl** out, uint32_t flags) {
+  if (slot < 0 || slot >= 8) return fail(PK_ERR_INVALID, "scratch slot %d", slot);
+  if ((flags & PK_PGL_MULTICAST) && !c->multicast_supported) flags &= ~PK_PGL_MULTICAST;
+  Pgl* cur = c->scratch[slot];
+  if (cur && cur->bytes >= bytes && (!(flags & PK_PGL_MULTICAST) || cur->mc)) { *out = cur; return PK_OK; }
   size_t want = std::max(bytes, (size_t)2 << 20);
-  PK_TRY(pgl_alloc(c, want, 0, &c->scratch[slot]));
+  if (cur) {
+    want = std::max(want, cur->bytes * 2);   // grow geometrically: a size sweep reallocates O(log) times
+    if (c->local_group) {
+      // Another rank of this process may have a kernel in flight that waits
+      // for ours: a device-wide sync here would deadlock. Retire instead.
+      c->retired.push_back(cur);
+    } else {
+      cudaDeviceSynchronize();
+      pgl_free(cur);
+    }
+    c->scratch[slot] = nullptr;
+  }
+  PK_TRY(pgl_alloc(c, want, flags, &c->scratch[slot]));
   *out = c->scratch[slot];
   return PK_OK;
 }
@@ -573,9 +586,12 @@ PK_API int pk_comm_destroy(pk_comm* c) {
   if (!c) return PK_OK;
   cudaDeviceSynchronize();
   for (auto& s : c->scratch) { if (s) pgl_free(s); s = nullptr; }
+  for (Pgl* p : c->retired) pgl_free(p);
+  c->retired.clear();
   if (c->sync) pgl_free(c->sync);
   c->sync = nullptr;
   if (c->listen_fd >= 0) ::close(c->listen_fd);
+  if (c->side) cudaStreamDestroy(c->side);
   for (auto& m : c->pending) if (m.fd >= 0) ::close(m.fd);
   LocalGroup* g = c->group;
   delete c;
@@ -606,13 +622,13 @@ PK_API int pk_comm_set_timeout(pk_comm* c, uint64_t ns) {
   return PK_OK;
 }
 
-PK_API int pk_comm_check(pk_comm* c, int* timed_out) {
+PK_API int pk_comm_check(pk_comm* c, int* code) {
   if (!c) return fail(PK_ERR_INVALID, "null comm");
   uint32_t v = 0;
   uint32_t* err = static_cast<uint32_t*>(c->sync->local) + kSyncErr;
   PK_CUDA(cudaMemcpy(&v, err, sizeof(v), cudaMemcpyDeviceToHost));
   if (v) PK_CUDA(cudaMemset(err, 0, sizeof(uint32_t)));
-  *timed_out = v ? 1 : 0;
+  *code = (int)v;
   return PK_OK;
 }
 

@@ -74,24 +74,33 @@ struct GemmArgs {
   SyncArgs sync;
 };
 
-template <int CG, int BN>
+// CG: CTAs per MMA (cta_group::1 / ::2). AM: 128-row A blocks per CTA (1 or 2).
+// Per CTA tile = (128*AM) x BN; per cluster tile = (128*AM*CG) x BN.
+template <int CG, int BN, int AM>
 struct GemmCfg {
-  static constexpr int BM = 128;                       // rows per CTA
-  static constexpr int UMMA_M = BM * CG;               // 128 or 256
+  static constexpr int BM = 128 * AM;                  // rows per CTA
+  static constexpr int UMMA_M = 128 * CG;              // 128 or 256 (pair)
   static constexpr int UMMA_N = BN;
   static constexpr int TILE_M = BM * CG;               // rows per cluster tile
   static constexpr int B_ROWS = BN / CG;               // B rows loaded per CTA
   static constexpr int A_BYTES = BM * BLOCK_K * 2;
   static constexpr int B_BYTES = B_ROWS * BLOCK_K * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int STAGES = (CG == 2) ? 6 : 4;
-  static constexpr int EPI_BUF_BYTES = 32 * EPI_COLS * 2;          // per warp per buffer: 4 KB
-  static constexpr int EPI_BYTES = 4 * 2 * EPI_BUF_BYTES;           // 4 warps, double buffered
-  static constexpr int TMEM_COLS = 2 * BN;                          // double-buffered accumulator
+  static constexpr int EPI_WARPS = 4 * AM;
+  static constexpr int NUM_THREADS = 128 + 32 * EPI_WARPS;
+  static constexpr int EPI_BUF_BYTES = 32 * EPI_COLS * 2;                  // per warp per buffer: 4 KB
+  static constexpr int EPI_NBUF = (AM == 2) ? 1 : 2;                       // staging buffers per warp
+  static constexpr int EPI_BYTES = EPI_WARPS * EPI_NBUF * EPI_BUF_BYTES;
+  static constexpr int ACC_COLS = AM * BN;                                 // TMEM columns per accumulator stage
+  static constexpr int ACC_STAGES = (2 * ACC_COLS <= 512) ? 2 : 1;         // overlap epilogue with next tile?
+  static constexpr int TMEM_COLS = ACC_STAGES * ACC_COLS;
   static constexpr int BAR_BYTES = 256;
+  static constexpr int STAGES = (232448 - 1024 - BAR_BYTES - EPI_BYTES) / STAGE_BYTES > 8
+                                    ? 8 : (232448 - 1024 - BAR_BYTES - EPI_BYTES) / STAGE_BYTES;
   static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + EPI_BYTES + BAR_BYTES + 1024;  // +1024 align slack
   static_assert(TMEM_COLS <= 512, "TMEM overflow");
   static_assert(SMEM_BYTES <= 232448, "smem overflow");
+  static_assert(STAGES >= 2, "need >= 2 pipeline stages");
 };
 
 // Tile order: grouped raster along M (GROUP tiles) for L2 reuse of B, then
@@ -108,10 +117,10 @@ PK_DEV void tile_coords(int t, int num_m, int num_n, int m_rot, int& mt, int& nt
   mt = (mt + m_rot) % num_m;
 }
 
-template <int CG, int BN, int EPI>
-__global__ void __launch_bounds__(kNumThreads, 1)
+template <int CG, int BN, int AM, int EPI>
+__global__ void __launch_bounds__(GemmCfg<CG, BN, AM>::NUM_THREADS, 1)
 lcsc_gemm_kernel(const __grid_constant__ GemmArgs args) {
-  using Cfg = GemmCfg<CG, BN>;
+  using Cfg = GemmCfg<CG, BN, AM>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* smem_a = smem;
@@ -120,8 +129,8 @@ lcsc_gemm_kernel(const __grid_constant__ GemmArgs args) {
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem_epi + Cfg::EPI_BYTES);
   uint64_t* full_bar = bars;                         // [STAGES]
   uint64_t* empty_bar = bars + Cfg::STAGES;          // [STAGES]
-  uint64_t* tfull_bar = bars + 2 * Cfg::STAGES;      // [2]
-  uint64_t* tempty_bar = bars + 2 * Cfg::STAGES + 2; // [2]
+  uint64_t* tfull_bar = bars + 2 * Cfg::STAGES;      // [ACC_STAGES]
+  uint64_t* tempty_bar = bars + 2 * Cfg::STAGES + 2; // [ACC_STAGES]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * Cfg::STAGES + 4);
 
   const uint32_t warp = warp_id_sync();
@@ -142,9 +151,9 @@ lcsc_gemm_kernel(const __grid_constant__ GemmArgs args) {
       mbar_init(&full_bar[s], 1);
       mbar_init(&empty_bar[s], 1);
     }
-    for (int a = 0; a < 2; ++a) {
+    for (int a = 0; a < Cfg::ACC_STAGES; ++a) {
       mbar_init(&tfull_bar[a], 1);
-      mbar_init(&tempty_bar[a], 4 * CG);
+      mbar_init(&tempty_bar[a], Cfg::EPI_WARPS * CG);
     }
     fence_mbar_init();
   }
@@ -278,24 +287,28 @@ lcsc_gemm_kernel(const __grid_constant__ GemmArgs args) {
       uint32_t phase = 0;
       int it = 0;
       for (int t = cluster; t < num_tiles; t += args.num_compute_clusters, ++it) {
-        const int acc = it & 1;
-        const uint32_t acc_phase = (it >> 1) & 1;
+        const int acc = (Cfg::ACC_STAGES == 2) ? (it & 1) : 0;
+        const uint32_t acc_phase = (Cfg::ACC_STAGES == 2) ? ((it >> 1) & 1) : (it & 1);
         mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
         tc_fence_after();
-        const uint32_t d_tmem = tmem_base + acc * BN;
+        const uint32_t d_tmem = tmem_base + acc * Cfg::ACC_COLS;
         for (int kb = 0; kb < num_kb; ++kb) {
           mbar_wait(&full_bar[stage], phase);
           tc_fence_after();
           if (elect_one()) {
             const uint32_t a_addr = smem_u32(smem_a + stage * Cfg::A_BYTES);
             const uint32_t b_addr = smem_u32(smem_b + stage * Cfg::B_BYTES);
-            const uint64_t a_desc = sdesc_kmajor_sw128(a_addr);
             const uint64_t b_desc = sdesc_kmajor_sw128(b_addr);
 #pragma unroll
-            for (int k = 0; k < BLOCK_K / UMMA_K; ++k) {
-              // advance 16 elements = 32 B along K inside the swizzle atom
-              umma_f16<CG>(d_tmem, a_desc + (uint64_t)(k * 2), b_desc + (uint64_t)(k * 2), idesc,
-                           (kb | k) != 0 ? 1u : 0u);
+            for (int am = 0; am < AM; ++am) {
+              // A row block am: 128 rows x 128 B = 16 KB further into the stage
+              const uint64_t a_desc = sdesc_kmajor_sw128(a_addr + am * 128 * 128);
+#pragma unroll
+              for (int k = 0; k < BLOCK_K / UMMA_K; ++k) {
+                // advance 16 elements = 32 B along K inside the swizzle atom
+                umma_f16<CG>(d_tmem + am * BN, a_desc + (uint64_t)(k * 2), b_desc + (uint64_t)(k * 2), idesc,
+                             (kb | k) != 0 ? 1u : 0u);
+              }
             }
             umma_commit<CG>(&empty_bar[stage]);
             if (kb == num_kb - 1) umma_commit<CG>(&tfull_bar[acc]);
@@ -305,19 +318,21 @@ lcsc_gemm_kernel(const __grid_constant__ GemmArgs args) {
         }
       }
     }
-  } else if (warp >= kEpiWarp0) {
+  } else if (warp >= kEpiWarp0 && warp < kEpiWarp0 + Cfg::EPI_WARPS) {
     // ========================================================= storer (epilogue)
-    const int q = (int)warp - kEpiWarp0;             // TMEM lane quarter
-    uint8_t* ebuf = smem_epi + q * 2 * Cfg::EPI_BUF_BYTES;
+    const int ew = (int)warp - kEpiWarp0;            // epilogue warp index
+    const int q = (int)warp & 3;                     // TMEM lane quarter this warp may access
+    const int am = ew >> 2;                          // which 128-row accumulator
+    uint8_t* ebuf = smem_epi + ew * Cfg::EPI_NBUF * Cfg::EPI_BUF_BYTES;
     int it = 0;
     int ebuf_idx = 0;
     uint32_t owners_ready = 0;
     for (int t = cluster; t < num_tiles; t += args.num_compute_clusters, ++it) {
       int mt, nt;
       tile_coords(t, num_m, num_n, args.m_rot, mt, nt);
-      const int acc = it & 1;
-      const uint32_t acc_phase = (it >> 1) & 1;
-      const int row0 = mt * Cfg::TILE_M + (int)cta_rank * Cfg::BM + q * 32;   // global M row of lane 0
+      const int acc = (Cfg::ACC_STAGES == 2) ? (it & 1) : 0;
+      const uint32_t acc_phase = (Cfg::ACC_STAGES == 2) ? ((it >> 1) & 1) : (it & 1);
+      const int row0 = mt * Cfg::TILE_M + (int)cta_rank * Cfg::BM + am * 128 + q * 32;   // global M row of lane 0
       const int dst = (args.c_ndst > 1) ? row0 / args.c_rows_per_dst : 0;
       const int c_row = row0 - dst * args.c_rows_per_dst;
       if (EPI == EPI_REDUCE_ADD && args.sync_ready_before_store && !((owners_ready >> dst) & 1)) {
@@ -331,7 +346,7 @@ lcsc_gemm_kernel(const __grid_constant__ GemmArgs args) {
 #pragma unroll 1
       for (int c = 0; c < BN / EPI_COLS; ++c) {
         uint32_t v0[32], v1[32];
-        const uint32_t taddr = tmem_base + t_lane + (uint32_t)(acc * BN + c * EPI_COLS);
+        const uint32_t taddr = tmem_base + t_lane + (uint32_t)(acc * Cfg::ACC_COLS + am * BN + c * EPI_COLS);
         tmem_ld_32x32b_x32(taddr, v0);
         tmem_ld_32x32b_x32(taddr + 32, v1);
         tmem_ld_wait();
@@ -344,8 +359,10 @@ lcsc_gemm_kernel(const __grid_constant__ GemmArgs args) {
             else mbar_arrive_cluster(&tempty_bar[acc], 0);
           }
         }
-        // buffer reuse guard: the store issued two chunks ago must have read smem
-        if (lane == 0) bulk_wait_read<1>();
+        // buffer reuse guard: the store that last used this buffer must have read smem
+        if (lane == 0) {
+          if constexpr (Cfg::EPI_NBUF == 2) bulk_wait_read<1>(); else bulk_wait_read<0>();
+        }
         __syncwarp();
         uint8_t* buf = ebuf + ebuf_idx * Cfg::EPI_BUF_BYTES;
         const uint32_t row_addr = smem_u32(buf) + lane * 128;
@@ -366,7 +383,7 @@ lcsc_gemm_kernel(const __grid_constant__ GemmArgs args) {
           else tma_reduce_add_2d(&args.tmap_c[dst], buf, col, c_row);
           bulk_commit();
         }
-        ebuf_idx ^= 1;
+        if constexpr (Cfg::EPI_NBUF == 2) ebuf_idx ^= 1;
       }
     }
     if (lane == 0) bulk_wait<0>();

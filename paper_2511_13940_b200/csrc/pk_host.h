@@ -120,13 +120,15 @@ struct Comm {
   uint32_t done_count = 0;           // cumulative done signals expected per src
   int max_flags = 0;
   // scratch (symmetric) buffers, grown on demand
-  Pgl* scratch[4] = {};
+  Pgl* scratch[8] = {};
   // rendezvous socket (multi-process)
   int listen_fd = -1;
   uint32_t seq = 0;                  // collective sequence number (message tag)
   struct Pending { int src; uint32_t tag; std::vector<char> payload; int fd; };
   std::vector<Pending> pending;      // messages that arrived for a later collective
   std::vector<Pgl*> user_pgls;       // PGLs handed out through pk_pgl_alloc (zero-copy lookup)
+  std::vector<Pgl*> retired;         // outgrown scratch PGLs (local groups free them at destroy)
+  cudaStream_t side = nullptr;       // side stream for copy-engine staging (ring attention)
 };
 
 // If [ptr, ptr+bytes) lies inside one of c's user PGLs, fill peers[] with the
@@ -143,7 +145,7 @@ int comm_barrier(Comm* c);
 int pgl_alloc(Comm* c, size_t bytes, uint32_t flags, Pgl** out);
 int pgl_free(Pgl* p);
 // Ensure scratch slot `slot` holds >= bytes (collective: all ranks call).
-int comm_scratch(Comm* c, int slot, size_t bytes, Pgl** out);
+int comm_scratch(Comm* c, int slot, size_t bytes, Pgl** out, uint32_t flags = 0);
 
 }  // namespace pk
 

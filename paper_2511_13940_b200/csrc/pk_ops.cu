@@ -10,10 +10,10 @@
 
 namespace pk {
 
-template <int CG, int BN, int EPI>
+template <int CG, int BN, int AM, int EPI>
 static int launch_lcsc(const GemmArgs& args, int grid_ctas, cudaStream_t st) {
-  using Cfg = GemmCfg<CG, BN>;
-  auto kern = lcsc_gemm_kernel<CG, BN, EPI>;
+  using Cfg = GemmCfg<CG, BN, AM>;
+  auto kern = lcsc_gemm_kernel<CG, BN, AM, EPI>;
   static thread_local bool attr_done = false;
   if (!attr_done) {
     PK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES));
@@ -21,7 +21,7 @@ static int launch_lcsc(const GemmArgs& args, int grid_ctas, cudaStream_t st) {
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid_ctas, 1, 1);
-  cfg.blockDim = dim3(kNumThreads, 1, 1);
+  cfg.blockDim = dim3(Cfg::NUM_THREADS, 1, 1);
   cfg.dynamicSmemBytes = Cfg::SMEM_BYTES;
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
@@ -35,18 +35,30 @@ static int launch_lcsc(const GemmArgs& args, int grid_ctas, cudaStream_t st) {
   return PK_OK;
 }
 
-int launch_gemm_variant(int cg, int epi, const GemmArgs& args, int grid_ctas, cudaStream_t st) {
-  if (cg == 2 && epi == EPI_STORE) return launch_lcsc<2, 256, EPI_STORE>(args, grid_ctas, st);
-  if (cg == 2 && epi == EPI_REDUCE_ADD) return launch_lcsc<2, 256, EPI_REDUCE_ADD>(args, grid_ctas, st);
-  if (cg == 1 && epi == EPI_STORE) return launch_lcsc<1, 256, EPI_STORE>(args, grid_ctas, st);
-  if (cg == 1 && epi == EPI_REDUCE_ADD) return launch_lcsc<1, 256, EPI_REDUCE_ADD>(args, grid_ctas, st);
-  return fail(PK_ERR_INVALID, "no GEMM variant for cta_group=%d epi=%d", cg, epi);
+// Kernel variants: (cta_group, A row blocks per CTA) x epilogue.
+struct Variant { int cg, am; };
+
+int launch_gemm_variant(Variant v, int epi, const GemmArgs& args, int grid_ctas, cudaStream_t st) {
+#define PK_V(CG, AM, E) if (v.cg == CG && v.am == AM && epi == E) return launch_lcsc<CG, 256, AM, E>(args, grid_ctas, st);
+  PK_V(2, 2, EPI_STORE) PK_V(2, 2, EPI_REDUCE_ADD)
+  PK_V(2, 1, EPI_STORE) PK_V(2, 1, EPI_REDUCE_ADD)
+  PK_V(1, 1, EPI_STORE) PK_V(1, 1, EPI_REDUCE_ADD)
+#undef PK_V
+  return fail(PK_ERR_INVALID, "no GEMM variant for cta_group=%d am=%d epi=%d", v.cg, v.am, epi);
 }
 
-int gemm_smem_bytes(int cg) { return cg == 2 ? GemmCfg<2, 256>::SMEM_BYTES : GemmCfg<1, 256>::SMEM_BYTES; }
-
-// Pick the CTA-group size: pairs (256-row tiles) when the row partition allows.
-static int pick_cg(int64_t rows_per_part) { return (rows_per_part % 256 == 0) ? 2 : 1; }
+// Pick the tile shape for a row partition of `rows_per_part` rows:
+//   512-row pair tiles (256 x 256 per CTA, one TMEM accumulator stage) cut
+//   L2->SM traffic by 25% vs 256-row pair tiles; the latter double-buffer
+//   TMEM so the epilogue overlaps the next tile, which wins at small K.
+static Variant pick_variant(int64_t rows_per_part, int64_t K, const pk_sched* sched) {
+  int force_am = 0;
+  if (const char* e = getenv("PK_GEMM_AM")) force_am = atoi(e);
+  if (sched && sched->stages < 0) force_am = -sched->stages;     // test hook: stages = -am
+  if (rows_per_part % 512 == 0 && force_am == 2) return {2, 2};   // opt-in until it measures faster
+  if (rows_per_part % 256 == 0) return {2, 1};
+  return {1, 1};
+}
 
 static int default_sms(int device, const pk_sched* sched) {
   int n = 148;
@@ -55,8 +67,8 @@ static int default_sms(int device, const pk_sched* sched) {
   return n;
 }
 
-static int tmap_a(CUtensorMap* m, const void* p, int64_t rows, int64_t k, int64_t ld) {
-  return make_tmap_2d(m, p, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, rows, k, ld, 128, BLOCK_K,
+static int tmap_a(CUtensorMap* m, const void* p, int64_t rows, int64_t k, int64_t ld, int am) {
+  return make_tmap_2d(m, p, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, rows, k, ld, 128 * am, BLOCK_K,
                       CU_TENSOR_MAP_SWIZZLE_128B);
 }
 static int tmap_b(CUtensorMap* m, const void* p, int64_t rows, int64_t k, int64_t ld, int cg) {
@@ -85,22 +97,23 @@ int gemm_local(const pk_tensor* A, const pk_tensor* B, pk_tensor* C, const pk_sc
   if (M % 128 || N % 256 || K % BLOCK_K || K == 0)
     return fail(PK_ERR_INVALID, "gemm: need M %% 128 == 0, N %% 256 == 0, K %% 64 == 0 (got %lld, %lld, %lld)",
                 (long long)M, (long long)N, (long long)K);
-  const int cg = pick_cg(M);
+  const Variant v = pick_variant(M, K, sched);
+  const int cg = v.cg;
   GemmArgs args;
   init_args(args);
-  PK_TRY(tmap_a(&args.tmap_a[0], A->ptr, M, K, ldA));
+  PK_TRY(tmap_a(&args.tmap_a[0], A->ptr, M, K, ldA, v.am));
   PK_TRY(tmap_b(&args.tmap_b, B->ptr, N, K, ldB, cg));
   PK_TRY(tmap_c(&args.tmap_c[0], C->ptr, M, N, ldC));
   args.M = (int)M; args.N = (int)N; args.K = (int)K;
   args.rank = 0; args.world = 1;
   args.a_rows_per_src = (int)M;
   args.c_rows_per_dst = (int)M;
-  const int tiles = (int)((M / (128 * cg)) * (N / 256));
+  const int tiles = (int)((M / (128 * v.am * cg)) * (N / 256));
   const int sms = default_sms(device, sched);
   int clusters = std::min(tiles, sms / cg);
   if (clusters < 1) clusters = 1;
   args.num_compute_clusters = clusters;
-  return launch_gemm_variant(cg, EPI_STORE, args, clusters * cg, st);
+  return launch_gemm_variant(v, EPI_STORE, args, clusters * cg, st);
 }
 
 // Fill the cross-rank sync block of one fused call.
@@ -147,8 +160,9 @@ int ag_gemm(Comm* c, const pk_tensor* A, const pk_tensor* B, pk_tensor* C, pk_te
     if (AG) PK_CUDA(cudaMemcpy2DAsync(AG->ptr, K * 2, A->ptr, ldA * 2, K * 2, m_loc, cudaMemcpyDeviceToDevice, st));
     return PK_OK;
   }
-  const int cg = pick_cg(m_loc);
-  const int tile_m = 128 * cg;
+  const Variant v = pick_variant(m_loc, K, sched);
+  const int cg = v.cg;
+  const int tile_m = 128 * v.am * cg;
   const int num_n = (int)(n_loc / 256);
   int mode = sched ? sched->mode : PK_SCHED_AUTO;
   if (mode == PK_SCHED_AUTO) mode = (num_n == 1 && !AG) ? PK_INTRA_SM : PK_INTER_SM;
@@ -178,7 +192,7 @@ int ag_gemm(Comm* c, const pk_tensor* A, const pk_tensor* B, pk_tensor* C, pk_te
   const int clusters_total = std::max(1, (sched && sched->num_sms > 0 ? std::min(sched->num_sms, c->num_sms) : c->num_sms) / cg);
   int comm_clusters = 0;
   if (mode == PK_INTRA_SM) {
-    for (int r = 0; r < n; ++r) PK_TRY(tmap_a(&args.tmap_a[r], shard[r], m_loc, K, K));
+    for (int r = 0; r < n; ++r) PK_TRY(tmap_a(&args.tmap_a[r], shard[r], m_loc, K, K, v.am));
     args.sync_ready_before_load = 1;
   } else {
     const int comm_sms = (sched && sched->num_comm_sms > 0) ? sched->num_comm_sms : std::max(2, std::min(16, c->num_sms / 8));
@@ -195,10 +209,10 @@ int ag_gemm(Comm* c, const pk_tensor* A, const pk_tensor* B, pk_tensor* C, pk_te
     if (M / tile_m > c->max_flags) return fail(PK_ERR_INVALID, "ag_gemm: too many row tiles for the flag array");
     for (int r = 0; r < n; ++r) {
       if (r == c->rank) {
-        PK_TRY(tmap_a(&args.tmap_a[r], shard[r], m_loc, K, K));
+        PK_TRY(tmap_a(&args.tmap_a[r], shard[r], m_loc, K, K, v.am));
         args.a_base[r] = 0;
       } else {
-        PK_TRY(tmap_a(&args.tmap_a[r], gathered, M, K, K));
+        PK_TRY(tmap_a(&args.tmap_a[r], gathered, M, K, K, v.am));
         args.a_base[r] = (int)(r * m_loc);
         args.a_wait_flag[r] = 1;
       }
@@ -213,9 +227,9 @@ int ag_gemm(Comm* c, const pk_tensor* A, const pk_tensor* B, pk_tensor* C, pk_te
   args.sync_done_signal = 1;
   c->epoch += 1;
   c->ready_count += 1;
-  c->done_count += (uint32_t)(compute_clusters * cg * 4);
+  c->done_count += (uint32_t)(compute_clusters * cg * 4 * v.am);
   fill_sync(c, args.sync);
-  PK_TRY(launch_gemm_variant(cg, EPI_STORE, args, (compute_clusters + comm_clusters) * cg, st));
+  PK_TRY(launch_gemm_variant(v, EPI_STORE, args, (compute_clusters + comm_clusters) * cg, st));
   if (AG && mode == PK_INTRA_SM) {
     // intra-SM never materialises the gathered rows; copy them on demand
     for (int r = 0; r < n; ++r)
@@ -240,8 +254,9 @@ int gemm_rs(Comm* c, const pk_tensor* A, const pk_tensor* B, pk_tensor* O, const
     return fail(PK_ERR_INVALID, "gemm_rs: need (M/n) %% 128 == 0, N %% 256 == 0, K %% 64 == 0 (got %lld, %lld, %lld)",
                 (long long)m_own, (long long)N, (long long)k_loc);
   if (n == 1) return gemm_local(A, B, O, sched, st, c->device);
-  const int cg = pick_cg(m_own);
-  const int tile_m = 128 * cg;
+  const Variant v = pick_variant(m_own, k_loc, sched);
+  const int cg = v.cg;
+  const int tile_m = 128 * v.am * cg;
   // Destination of every rank (zero-copy when `out` is symmetric).
   void* dst[kMaxRanks];
   const size_t out_bytes = (size_t)m_own * N * 2;
@@ -258,7 +273,7 @@ int gemm_rs(Comm* c, const pk_tensor* A, const pk_tensor* B, pk_tensor* O, const
   args.M = (int)M; args.N = (int)N; args.K = (int)k_loc;
   args.rank = c->rank; args.world = n;
   args.a_rows_per_src = (int)M;
-  PK_TRY(tmap_a(&args.tmap_a[0], A->ptr, M, k_loc, ldA));
+  PK_TRY(tmap_a(&args.tmap_a[0], A->ptr, M, k_loc, ldA, v.am));
   PK_TRY(tmap_b(&args.tmap_b, B->ptr, N, k_loc, ldB, cg));
   for (int r = 0; r < n; ++r) PK_TRY(tmap_c(&args.tmap_c[r], dst[r], m_own, N, N));
   args.c_rows_per_dst = (int)m_own;
@@ -272,9 +287,9 @@ int gemm_rs(Comm* c, const pk_tensor* A, const pk_tensor* B, pk_tensor* O, const
   args.sync_done_signal = 1;
   c->epoch += 1;
   c->ready_count += 1;
-  c->done_count += (uint32_t)(compute_clusters * cg * 4);
+  c->done_count += (uint32_t)(compute_clusters * cg * 4 * v.am);
   fill_sync(c, args.sync);
-  PK_TRY(launch_gemm_variant(cg, EPI_REDUCE_ADD, args, compute_clusters * cg, st));
+  PK_TRY(launch_gemm_variant(v, EPI_REDUCE_ADD, args, compute_clusters * cg, st));
   if (staged)
     PK_CUDA(cudaMemcpy2DAsync(O->ptr, ldO * 2, dst[c->rank], N * 2, N * 2, m_own, cudaMemcpyDeviceToDevice, st));
   return PK_OK;

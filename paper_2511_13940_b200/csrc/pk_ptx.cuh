@@ -67,9 +67,9 @@ PK_DEV bool mbar_try_wait(uint32_t addr, uint32_t parity) {
   uint32_t ok;
   asm volatile(
       "{\n\t.reg .pred P1;\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2, %3;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
       "selp.b32 %0, 1, 0, P1;\n\t}"
-      : "=r"(ok) : "r"(addr), "r"(parity), "r"(0x989680) : "memory");
+      : "=r"(ok) : "r"(addr), "r"(parity) : "memory");
   return ok != 0;
 }
 PK_DEV void mbar_wait(uint64_t* bar, uint32_t parity) {
@@ -246,6 +246,11 @@ PK_DEV void mm_signal_add(uint32_t* mc_counter, uint32_t v) {
 PK_DEV uint32_t ld_acquire_sys(const uint32_t* p) {
   uint32_t v;
   asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+PK_DEV int32_t ld_volatile_s32(const int32_t* p) {
+  int32_t v;
+  asm volatile("ld.volatile.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
 PK_DEV uint32_t ld_relaxed_sys(const uint32_t* p) {

@@ -94,3 +94,97 @@ def gemm_reduce_scatter(comm, a: torch.Tensor, b: torch.Tensor, out: torch.Tenso
     check(lib.pk_gemm_rs(comm._h, _lib.ref(da), _lib.ref(db), _lib.ref(do), _lib.ref(sc),
                          ctypes_stream(_stream(stream))), "gemm_reduce_scatter")
     return out
+
+
+_REDUCE_OPS = {"sum": 0, "max": 1, "min": 2}   # primitives.py:24-28
+
+
+def all_reduce(comm, x: torch.Tensor, op: str = "sum", schedule: dict | None = None, stream=None) -> torch.Tensor:
+    """In-place all-reduce of x over all ranks (primitives.all_reduce, primitives.py:237-261).
+
+    NVLS two-shot (multimem.ld_reduce + multimem.st) when x lives in a
+    multicast PGL on distinct GPUs; otherwise P2P register ops with the
+    canonical ascending fold. bf16 or fp32, size a multiple of 16 bytes.
+    """
+    _require_cuda(x)
+    if op not in _REDUCE_OPS:
+        from .errors import PrimitiveError
+        raise PrimitiveError(f"unsupported reduce op {op!r}")
+    lib = _lib.load()
+    dx = _lib.tensor_desc(x)
+    sc = _sched(schedule)
+    check(lib.pk_all_reduce(comm._h, _lib.ref(dx), _REDUCE_OPS[op], _lib.ref(sc),
+                            ctypes_stream(_stream(stream))), "all_reduce")
+    return x
+
+
+def moe_capacity(tokens: int, top_k: int, world: int, hidden: int) -> int:
+    """Default receive capacity: the worst case (every token of every rank routed
+    here) when that fits in 1 GiB, else twice the average load."""
+    worst = tokens * top_k * world
+    return worst if worst * hidden * 2 <= (1 << 30) else 2 * tokens * top_k
+
+
+def moe_dispatch(comm, x: torch.Tensor, topk_idx: torch.Tensor, num_experts: int,
+                 capacity: int | None = None, recv=None, stream=None):
+    """Expert-parallel dispatch (MoePlan, workloads.py:786-868).
+
+    x [T, H] bf16, topk_idx [T, k] int32. Expert e lives on rank e % n. Returns
+    (recv [cap, H] bf16, recv_src [cap] int32, recv_count [1] int32 on device):
+    on the owner, slot s holds the token whose (src_rank, token, k) triple is
+    the s-th in sorted order (workloads.py:821-832); recv_src[s] =
+    (src_rank * T + token) * k + j. recv/recv_src are symmetric (Comm.empty).
+    """
+    _require_cuda(x, topk_idx)
+    T, k = topk_idx.shape
+    if capacity is None:
+        capacity = moe_capacity(T, k, comm.world, x.shape[1])
+    if recv is None:
+        recv = (comm.empty((capacity, x.shape[1]), torch.bfloat16), comm.empty((capacity,), torch.int32))
+    recv_rows, recv_src = recv
+    count = torch.zeros(1, dtype=torch.int32, device=x.device)
+    lib = _lib.load()
+    dx, dt = _lib.tensor_desc(x), _lib.tensor_desc(topk_idx)
+    dr, ds, dc = _lib.tensor_desc(recv_rows), _lib.tensor_desc(recv_src), _lib.tensor_desc(count)
+    check(lib.pk_moe_dispatch(comm._h, _lib.ref(dx), _lib.ref(dt), int(num_experts), _lib.ref(dr), _lib.ref(ds),
+                              _lib.ref(dc), ctypes_stream(_stream(stream))), "moe_dispatch")
+    return recv_rows, recv_src, count
+
+
+def moe_combine(comm, y: torch.Tensor, topk_idx: torch.Tensor, weights: torch.Tensor, num_experts: int,
+                out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+    """Inverse of the last moe_dispatch on this comm (new; absent from the reference):
+    out[t] = sum_j weights[t, j] * y_owner[slot(rank, t, j)], accumulated in fp32."""
+    _require_cuda(y, topk_idx, weights)
+    T = topk_idx.shape[0]
+    if out is None:
+        out = torch.empty((T, y.shape[1]), dtype=torch.bfloat16, device=y.device)
+    lib = _lib.load()
+    dy, dt, dw, do = (_lib.tensor_desc(y), _lib.tensor_desc(topk_idx), _lib.tensor_desc(weights),
+                      _lib.tensor_desc(out))
+    check(lib.pk_moe_combine(comm._h, _lib.ref(dy), _lib.ref(dt), _lib.ref(dw), int(num_experts), _lib.ref(do),
+                             ctypes_stream(_stream(stream))), "moe_combine")
+    return out
+
+
+def ring_attention(comm, q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, softmax_scale: float | None = None,
+                   out: torch.Tensor | None = None, lse: torch.Tensor | None = None, stream=None):
+    """Sequence-parallel ring attention forward, non-causal (RingAttentionPlan,
+    workloads.py:616-716). q, k, v: this rank's [B, S/n, H, D] bf16 shards
+    (D = 128, S/n % 128 == 0). At ring step s rank r attends to the KV shard of
+    rank (r - s) mod n. Returns (o [B, S/n, H, D] bf16, lse [B, H, S/n] fp32,
+    natural log)."""
+    _require_cuda(q, k, v)
+    B, S, H, D = q.shape
+    if softmax_scale is None:
+        softmax_scale = D ** -0.5
+    if out is None:
+        out = torch.empty_like(q)
+    if lse is None:
+        lse = torch.empty((B, H, S), dtype=torch.float32, device=q.device)
+    lib = _lib.load()
+    dq, dk, dv, do, dl = (_lib.tensor_desc(x) for x in (q, k, v, out, lse))
+    import ctypes
+    check(lib.pk_ring_attn_fwd(comm._h, _lib.ref(dq), _lib.ref(dk), _lib.ref(dv), _lib.ref(do), _lib.ref(dl),
+                               ctypes.c_float(softmax_scale), None, ctypes_stream(_stream(stream))), "ring_attention")
+    return out, lse
