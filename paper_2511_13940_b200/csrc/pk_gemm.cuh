@@ -34,6 +34,7 @@ constexpr int kNumThreads = 256;
 constexpr int kEpiWarp0 = 4;
 
 enum EpiMode : int { EPI_STORE = 0, EPI_REDUCE_ADD = 1 };
+constexpr int kTileRing = 4;                // depth of the tile-index broadcast ring
 
 // Cross-rank sync state for one fused call (all pointers are device VAs).
 struct SyncArgs {
@@ -62,6 +63,9 @@ struct GemmArgs {
   int c_rows_per_dst;                     // rows of global M per C destination
   int c_ndst;
   int m_rot;                              // tile-order rotation along M (in M tiles)
+  int raster_group;                       // tiles per raster group (L2 reuse)
+  uint32_t* tile_counter;                 // dynamic tile scheduler (0 at launch; reset by the last fetch)
+  int raster_dir;                         // 0: group along M, 1: group along N
   int num_compute_clusters;               // clusters that run GEMM tiles
   int sync_ready_before_load;             // AG intra-SM: wait ready[s] before loading peer rows
   int sync_ready_before_store;            // RS: wait ready[owner] before the first reduce-add
@@ -94,7 +98,7 @@ struct GemmCfg {
   static constexpr int ACC_COLS = AM * BN;                                 // TMEM columns per accumulator stage
   static constexpr int ACC_STAGES = (2 * ACC_COLS <= 512) ? 2 : 1;         // overlap epilogue with next tile?
   static constexpr int TMEM_COLS = ACC_STAGES * ACC_COLS;
-  static constexpr int BAR_BYTES = 256;
+  static constexpr int BAR_BYTES = 512;
   static constexpr int STAGES = (232448 - 1024 - BAR_BYTES - EPI_BYTES) / STAGE_BYTES > 8
                                     ? 8 : (232448 - 1024 - BAR_BYTES - EPI_BYTES) / STAGE_BYTES;
   static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + EPI_BYTES + BAR_BYTES + 1024;  // +1024 align slack
@@ -105,15 +109,24 @@ struct GemmCfg {
 
 // Tile order: grouped raster along M (GROUP tiles) for L2 reuse of B, then
 // rotated along M so rank r starts on its own / its neighbour's rows.
-PK_DEV void tile_coords(int t, int num_m, int num_n, int m_rot, int& mt, int& nt) {
-  constexpr int GROUP = 8;
-  const int per_group = GROUP * num_n;
-  const int g = t / per_group;
-  const int first_m = g * GROUP;
-  const int gsize = min(num_m - first_m, GROUP);
-  const int r = t - g * per_group;
-  mt = first_m + r % gsize;
-  nt = r / gsize;
+PK_DEV void tile_coords(int t, int num_m, int num_n, int m_rot, int group, int dir, int& mt, int& nt) {
+  if (dir == 0) {
+    const int per_group = group * num_n;
+    const int g = t / per_group;
+    const int first_m = g * group;
+    const int gsize = min(num_m - first_m, group);
+    const int r = t - g * per_group;
+    mt = first_m + r % gsize;
+    nt = r / gsize;
+  } else {
+    const int per_group = group * num_m;
+    const int g = t / per_group;
+    const int first_n = g * group;
+    const int gsize = min(num_n - first_n, group);
+    const int r = t - g * per_group;
+    nt = first_n + r % gsize;
+    mt = r / gsize;
+  }
   mt = (mt + m_rot) % num_m;
 }
 
@@ -131,7 +144,10 @@ lcsc_gemm_kernel(const __grid_constant__ GemmArgs args) {
   uint64_t* empty_bar = bars + Cfg::STAGES;          // [STAGES]
   uint64_t* tfull_bar = bars + 2 * Cfg::STAGES;      // [ACC_STAGES]
   uint64_t* tempty_bar = bars + 2 * Cfg::STAGES + 2; // [ACC_STAGES]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 2 * Cfg::STAGES + 4);
+  uint64_t* tile_full = bars + 2 * Cfg::STAGES + 4;  // [kTileRing]
+  uint64_t* tile_empty = tile_full + kTileRing;       // [kTileRing]
+  int32_t* tile_ring = reinterpret_cast<int32_t*>(tile_empty + kTileRing);   // [kTileRing]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tile_ring + kTileRing);
 
   const uint32_t warp = warp_id_sync();
   const uint32_t lane = lane_id();
@@ -155,6 +171,12 @@ lcsc_gemm_kernel(const __grid_constant__ GemmArgs args) {
       mbar_init(&tfull_bar[a], 1);
       mbar_init(&tempty_bar[a], Cfg::EPI_WARPS * CG);
     }
+    // tile ring consumers: MMA warp (leader) + every epilogue warp of the pair
+    // + the peer CTA's loader
+    for (int i = 0; i < kTileRing; ++i) {
+      mbar_init(&tile_full[i], 1);
+      mbar_init(&tile_empty[i], 1 + Cfg::EPI_WARPS * CG + (CG - 1));
+    }
     fence_mbar_init();
   }
   if (warp == 2 && !is_comm) tmem_alloc<Cfg::TMEM_COLS, CG>(tmem_slot);
@@ -173,6 +195,41 @@ lcsc_gemm_kernel(const __grid_constant__ GemmArgs args) {
   if constexpr (CG == 2) cluster_sync(); else __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+
+  // Dynamic tile scheduler. The leader CTA's loader fetches tile indices from
+  // a global counter (in-order consumption keeps the tiles in flight a
+  // contiguous window of the raster, so A/B panels stay L2-resident; a static
+  // round-robin lets clusters drift apart by whole waves) and broadcasts them
+  // to every role of the pair through a kTileRing-deep smem ring.
+  const int num_clusters = args.num_compute_clusters;
+  auto tile_publish = [&](int it) -> int {      // leader loader, one lane
+    const int slot = it % kTileRing;
+    mbar_wait(&tile_empty[slot], ((it / kTileRing) & 1) ^ 1);
+    const uint32_t t = atomicAdd(args.tile_counter, 1u);
+    if (t == (uint32_t)(num_tiles + num_clusters - 1)) *args.tile_counter = 0;   // last fetch of this launch
+    tile_ring[slot] = (int)t;
+    if constexpr (CG == 2) {
+      asm volatile(
+          "{\n\t.reg .b32 ra;\n\t"
+          "mapa.shared::cluster.u32 ra, %0, 1;\n\t"
+          "st.shared::cluster.u32 [ra], %1;\n\t}"
+          :: "r"(smem_u32(&tile_ring[slot])), "r"(t) : "memory");
+      mbar_arrive_cluster(&tile_full[slot], 1);
+    }
+    mbar_arrive(&tile_full[slot]);
+    return (int)t;
+  };
+  auto tile_consume = [&](int it) -> int {      // any other role; one arrival per warp
+    const int slot = it % kTileRing;
+    mbar_wait(&tile_full[slot], (it / kTileRing) & 1);
+    const int t = tile_ring[slot];
+    __syncwarp();
+    if (lane_id() == 0) {
+      if (CG == 2 && !leader) mbar_arrive_cluster(&tile_empty[slot], 0);
+      else mbar_arrive(&tile_empty[slot]);
+    }
+    return t;
+  };
 
   if (is_comm) {
     // ========================================================= communicator
@@ -244,9 +301,17 @@ lcsc_gemm_kernel(const __grid_constant__ GemmArgs args) {
     int stage = 0;
     uint32_t phase = 0;
     uint32_t peers_ready = 0;
-    for (int t = cluster; t < num_tiles; t += args.num_compute_clusters) {
+    for (int it = 0;; ++it) {
+      int t;
+      if (leader) {
+        if (lane == 0) t = tile_publish(it);
+        t = __shfl_sync(0xffffffffu, t, 0);
+      } else {
+        t = tile_consume(it);
+      }
+      if (t >= num_tiles) break;
       int mt, nt;
-      tile_coords(t, num_m, num_n, args.m_rot, mt, nt);
+      tile_coords(t, num_m, num_n, args.m_rot, args.raster_group, args.raster_dir, mt, nt);
       const int m_row = mt * Cfg::TILE_M + (int)cta_rank * Cfg::BM;
       const int src = (args.a_nsrc > 1) ? (mt * Cfg::TILE_M) / args.a_rows_per_src : 0;
       const int a_row = args.a_base[src] + m_row - src * args.a_rows_per_src;
@@ -285,8 +350,9 @@ lcsc_gemm_kernel(const __grid_constant__ GemmArgs args) {
       constexpr uint32_t idesc = idesc_bf16_f32(Cfg::UMMA_M, Cfg::UMMA_N);
       int stage = 0;
       uint32_t phase = 0;
-      int it = 0;
-      for (int t = cluster; t < num_tiles; t += args.num_compute_clusters, ++it) {
+      for (int it = 0;; ++it) {
+        const int t = tile_consume(it);
+        if (t >= num_tiles) break;
         const int acc = (Cfg::ACC_STAGES == 2) ? (it & 1) : 0;
         const uint32_t acc_phase = (Cfg::ACC_STAGES == 2) ? ((it >> 1) & 1) : (it & 1);
         mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
@@ -327,9 +393,11 @@ lcsc_gemm_kernel(const __grid_constant__ GemmArgs args) {
     int it = 0;
     int ebuf_idx = 0;
     uint32_t owners_ready = 0;
-    for (int t = cluster; t < num_tiles; t += args.num_compute_clusters, ++it) {
+    for (;; ++it) {
+      const int t = tile_consume(it);
+      if (t >= num_tiles) break;
       int mt, nt;
-      tile_coords(t, num_m, num_n, args.m_rot, mt, nt);
+      tile_coords(t, num_m, num_n, args.m_rot, args.raster_group, args.raster_dir, mt, nt);
       const int acc = (Cfg::ACC_STAGES == 2) ? (it & 1) : 0;
       const uint32_t acc_phase = (Cfg::ACC_STAGES == 2) ? ((it >> 1) & 1) : (it & 1);
       const int row0 = mt * Cfg::TILE_M + (int)cta_rank * Cfg::BM + am * 128 + q * 32;   // global M row of lane 0

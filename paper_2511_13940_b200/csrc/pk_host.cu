@@ -95,9 +95,10 @@ int make_tmap_2d(CUtensorMap* map, const void* ptr, CUtensorMapDataType dt, int 
   cuuint64_t strides[1] = {(cuuint64_t)(ld * elem_bytes)};
   cuuint32_t box[2] = {(cuuint32_t)box_cols, (cuuint32_t)box_rows};
   cuuint32_t estr[2] = {1, 1};
+  CUtensorMapL2promotion promo = CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
+  if (const char* e = getenv("PK_L2PROMO")) promo = (CUtensorMapL2promotion)atoi(e);   // tuning hook
   CUresult r = d->tensorMapEncodeTiled(map, dt, 2, const_cast<void*>(ptr), dims, strides, box, estr,
-                                       CU_TENSOR_MAP_INTERLEAVE_NONE, swz,
-                                       CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                                       CU_TENSOR_MAP_INTERLEAVE_NONE, swz, promo, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS)
     return fail(PK_ERR_INVALID, "cuTensorMapEncodeTiled failed (%d): rows=%lld cols=%lld ld=%lld box=%dx%d",
                 (int)r, (long long)rows, (long long)cols, (long long)ld, box_rows, box_cols);

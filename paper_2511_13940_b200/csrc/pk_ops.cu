@@ -6,12 +6,38 @@
 #include "pk_host.h"
 #include "pk_gemm.cuh"
 #include <algorithm>
+#include <atomic>
 #include <cstring>
+#include <mutex>
 
 namespace pk {
 
+// Zero-initialised tile counters for the dynamic scheduler, one per launch in
+// flight (each launch resets its counter to 0 when it finishes fetching).
+constexpr int kCounterSlots = 4096;
+static int tile_counter(uint32_t** out) {
+  static uint32_t* buf[64] = {};
+  static std::atomic<uint32_t> next{0};
+  int dev = 0;
+  PK_CUDA(cudaGetDevice(&dev));
+  if (dev < 0 || dev >= 64) return fail(PK_ERR_INVALID, "device %d", dev);
+  static std::mutex mu;
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    if (!buf[dev]) {
+      PK_CUDA(cudaMalloc(&buf[dev], kCounterSlots * sizeof(uint32_t)));
+      PK_CUDA(cudaMemset(buf[dev], 0, kCounterSlots * sizeof(uint32_t)));
+      PK_CUDA(cudaDeviceSynchronize());
+    }
+  }
+  *out = buf[dev] + (next.fetch_add(1) % kCounterSlots);
+  return PK_OK;
+}
+
 template <int CG, int BN, int AM, int EPI>
-static int launch_lcsc(const GemmArgs& args, int grid_ctas, cudaStream_t st) {
+static int launch_lcsc(const GemmArgs& args_in, int grid_ctas, cudaStream_t st) {
+  GemmArgs args = args_in;
+  PK_TRY(tile_counter(&args.tile_counter));
   using Cfg = GemmCfg<CG, BN, AM>;
   auto kern = lcsc_gemm_kernel<CG, BN, AM, EPI>;
   static thread_local bool attr_done = false;
@@ -84,6 +110,12 @@ static void init_args(GemmArgs& a) {
   memset(&a, 0, sizeof(a));
   a.a_nsrc = 1;
   a.c_ndst = 1;
+  a.raster_group = 8;
+  a.raster_dir = 0;
+  if (const char* e = getenv("PK_RASTER")) {      // "dir,group" (tuning hook)
+    int d = 0, g = 8;
+    if (sscanf(e, "%d,%d", &d, &g) == 2 && g > 0) { a.raster_dir = d; a.raster_group = g; }
+  }
 }
 
 int gemm_local(const pk_tensor* A, const pk_tensor* B, pk_tensor* C, const pk_sched* sched,
