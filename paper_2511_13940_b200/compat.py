@@ -1,0 +1,494 @@
+"""Drop-in for the reference's plan API on the hot path.
+
+Mirrors overlapsim's `build(kind, dims, profile, ...) -> (LcscKernelSpec,
+WorkloadPlan)`, `execute_kernel(spec, plan, profile, ...) -> ExecResult` and
+`check_oracle(plan)` (workloads.py:1040-1070, lcsc.py:141-159) for the five
+hot-path kinds: AG_GEMM, GEMM_RS, GEMM_AR, RING_ATTENTION and
+MOE_DISPATCH_GEMM. A plan draws the reference's seeded integer inputs in the
+reference's order (workloads.py:117, 218-220, 799-820), `execute_kernel`
+runs them through the real B200 ops on a local group of `num_devices`
+emulated ranks on one GPU (or real ranks when a communicator list is passed),
+and `check_oracle` compares the checked layouts bit for bit with the plan's
+brute-force expectation, returning None or (layout, (dev, *idx)).
+
+The functional tiles are the reference's 16 x 16; the CUDA kernels need
+128-row / 64-column granularity, so tiles are embedded in zero-padded
+operands and extracted afterwards (the padding never changes a checked
+value). Kinds outside the hot path (Ulysses, tensor-dim collectives) raise
+WorkloadError.
+"""
+from __future__ import annotations
+
+import time
+from dataclasses import dataclass, field, replace
+from enum import Enum
+from typing import Optional
+
+import numpy as np
+import torch
+
+from .errors import LcscError, WorkloadError
+
+FUNC_TILE = 16                 # workloads.py:55
+DEFAULT_PIPELINE_STAGES = 4    # lcsc.py:18
+B200_SMS = 148
+
+
+class WorkloadKind(Enum):      # workloads.py:66-75
+    AG_GEMM = "ag_gemm"
+    GEMM_RS = "gemm_rs"
+    GEMM_AR = "gemm_ar"
+    RING_ATTENTION = "ring_attention"
+    ULYSSES_ALL_TO_ALL = "ulysses_all_to_all"
+    MOE_DISPATCH_GEMM = "moe_dispatch_gemm"
+    ALL_GATHER_TENSOR_DIM = "all_gather_tensor_dim"
+    REDUCE_SCATTER_TENSOR_DIM = "reduce_scatter_tensor_dim"
+    ALL_TO_ALL_4D = "all_to_all_4d"
+
+
+class ScheduleMode(Enum):      # lcsc.py:27-30
+    INTRA_SM = "intra_sm"
+    INTER_SM = "inter_sm"
+    HYBRID = "hybrid"
+
+
+@dataclass(frozen=True)
+class LcscKernelSpec:          # lcsc.py:45-76
+    schedule_mode: ScheduleMode = ScheduleMode.INTRA_SM
+    num_comm_sms: int = 0
+    pipeline_stages: int = DEFAULT_PIPELINE_STAGES
+    tile_m: int = 128
+    tile_n: int = 256
+    tile_k: int = 64
+
+    def __post_init__(self):
+        if self.pipeline_stages < 1:
+            raise LcscError("pipeline depth must be at least 1")
+        if min(self.tile_m, self.tile_n, self.tile_k) <= 0:
+            raise LcscError("tile extents must be positive")
+        if self.schedule_mode is ScheduleMode.INTRA_SM and self.num_comm_sms != 0:
+            raise LcscError("intra-SM scheduling keeps communication inside compute SMs (num_comm_sms must be 0)")
+        if self.schedule_mode is not ScheduleMode.INTRA_SM and self.num_comm_sms < 1:
+            raise LcscError("dedicated-SM scheduling needs at least 1 communication SM")
+
+    def validate(self, sms: int = B200_SMS) -> None:
+        if self.num_comm_sms >= sms:
+            raise LcscError(f"num_comm_sms {self.num_comm_sms} must leave at least one compute SM out of {sms}")
+
+    def compute_sms(self, sms: int = B200_SMS) -> int:
+        return sms - self.num_comm_sms
+
+    def schedule(self) -> dict:
+        return {"mode": self.schedule_mode.value, "num_comm_sms": self.num_comm_sms}
+
+
+@dataclass
+class CostReport:              # costmodel.py CostReport, measured instead of simulated
+    t_launch: float = 0.0
+    t_comp: float = 0.0
+    t_mem: float = 0.0
+    t_comm: float = 0.0
+    t_sync: float = 0.0
+    t_non_overlap: float = 0.0
+    t_total: float = 0.0       # ns, CUDA events, max over ranks
+    comm_ratio: float = 0.0
+    achieved_flops: float = 0.0
+
+
+@dataclass
+class ExecResult:              # lcsc.py:99-107
+    report: CostReport
+    pgls: dict
+    events: list = field(default_factory=list)
+    engine: object = None
+
+
+@dataclass
+class WorkloadSpec:            # workloads.py:78-101
+    kind: WorkloadKind
+    dims: dict
+    element_bytes: int = 2
+    num_devices: int = 8
+    seed: int = 0
+    materialize: Optional[bool] = None
+
+    def __post_init__(self):
+        if self.element_bytes <= 0:
+            raise WorkloadError("element size must be positive")
+        if self.num_devices < 2:
+            raise WorkloadError("workloads need at least 2 devices")
+        for key, val in self.dims.items():
+            if int(val) <= 0:
+                raise WorkloadError(f"dimension {key} must be positive")
+
+    def dim(self, key: str) -> int:
+        if key not in self.dims:
+            raise WorkloadError(f"{self.kind.value} needs dimension {key!r}")
+        return int(self.dims[key])
+
+
+def _randints(rng, shape):
+    return rng.integers(-8, 9, size=shape).astype(np.float64)       # workloads.py:218-220
+
+
+def _bf16(x, device="cuda"):
+    return torch.from_numpy(np.ascontiguousarray(x, dtype=np.float32)).to(device).to(torch.bfloat16)
+
+
+class WorkloadPlan:
+    """Plugin base (workloads.py:104-142): layouts, seeded inputs, oracle, GPU run."""
+
+    kind: WorkloadKind
+    default_mode = ScheduleMode.INTRA_SM
+    default_comm_sms = 0
+
+    def __init__(self, spec: WorkloadSpec):
+        self.spec = spec
+        self.num_devices = spec.num_devices
+        self.rng = np.random.default_rng(spec.seed)                # workloads.py:117
+        self.pgls: dict[str, list[np.ndarray]] = {}
+        self.check_names: list[str] = []
+        self.flops_per_device = 0.0
+        self._build()
+
+    def _build(self):
+        raise NotImplementedError
+
+    def run(self, comms, kspec: LcscKernelSpec, streams) -> None:
+        raise NotImplementedError
+
+    def oracle(self) -> dict[str, list[np.ndarray]]:
+        raise NotImplementedError
+
+    @property
+    def name(self) -> str:
+        return self.kind.value
+
+    def default_kernel_spec(self, schedule_mode=None, num_comm_sms=None, pipeline_stages=4) -> LcscKernelSpec:
+        mode = schedule_mode or self.default_mode
+        if mode is ScheduleMode.INTRA_SM:
+            comm = 0
+        elif num_comm_sms is not None:
+            comm = num_comm_sms
+        else:
+            comm = self.default_comm_sms or 16
+        return LcscKernelSpec(schedule_mode=mode, num_comm_sms=comm, pipeline_stages=pipeline_stages)
+
+    def final_state(self) -> dict[str, list[np.ndarray]]:
+        return {name: [b.copy() for b in self.pgls[name]] for name in self.check_names}
+
+
+class AgGemmPlan(WorkloadPlan):
+    """Row shards gathered rank-major before the GEMM (workloads.py:553-609)."""
+
+    kind = WorkloadKind.AG_GEMM
+    default_mode = ScheduleMode.INTER_SM
+    default_comm_sms = 20
+
+    def _build(self):
+        sp, n, t = self.spec, self.num_devices, FUNC_TILE
+        m, nd, k = sp.dim("M"), sp.dim("N"), sp.dim("K")
+        if m % n:
+            raise WorkloadError("M must divide across devices")
+        self.flops_per_device = 2.0 * m * (nd / n) * k
+        self.a = [_randints(self.rng, (1, 1, t, t)) for _ in range(n)]
+        brng = np.random.default_rng(self.spec.seed + 7919)          # separate stream: keeps `a` identical to the reference
+        self.b = [brng.integers(-1, 2, size=(t, t)).astype(np.float64) for _ in range(n)]
+        self.pgls = {"a": [x.copy() for x in self.a], "ag": [np.zeros((1, 1, n * t, t)) for _ in range(n)],
+                     "c": [np.zeros((1, 1, n * t, t)) for _ in range(n)]}
+        self.check_names = ["ag", "c"]
+
+    def run(self, comms, kspec, streams):
+        from . import ops
+        n, t = self.num_devices, FUNC_TILE
+        m_loc, kp, np_ = 128, 64, 256
+        ins, outs = [], []
+        for r in range(n):                       # allocate everything before any rank launches
+            a = np.zeros((m_loc, kp)); a[:t, :t] = self.a[r][0, 0]
+            b = np.zeros((np_, kp)); b[:t, :t] = self.b[r]
+            ins.append((_bf16(a), _bf16(b)))
+            outs.append((torch.empty(m_loc * n, kp, device="cuda", dtype=torch.bfloat16),
+                         torch.empty(m_loc * n, np_, device="cuda", dtype=torch.bfloat16)))
+        torch.cuda.synchronize()
+        sched = {"mode": kspec.schedule_mode.value, "num_comm_sms": max(kspec.num_comm_sms, 2)}
+        for r, c in enumerate(comms):
+            with torch.cuda.stream(streams[r]):
+                ops.all_gather_gemm(c, ins[r][0], ins[r][1], out=outs[r][1], a_gathered=outs[r][0], schedule=sched,
+                                    stream=streams[r])
+        torch.cuda.synchronize()
+        for r, (g, cc) in enumerate(outs):
+            g, cc = g.float().cpu().numpy(), cc.float().cpu().numpy()
+            for d in range(n):
+                self.pgls["ag"][r][0, 0, d * t:(d + 1) * t] = g[d * m_loc:d * m_loc + t, :t]
+                self.pgls["c"][r][0, 0, d * t:(d + 1) * t] = cc[d * m_loc:d * m_loc + t, :t]
+
+    def oracle(self):
+        t, n = FUNC_TILE, self.num_devices
+        g = np.concatenate([a[0, 0] for a in self.a], axis=0)        # workloads.py:603-609
+        return {"ag": [g[None, None].copy() for _ in range(n)],
+                "c": [(g @ self.b[r].T)[None, None] for r in range(n)]}
+
+
+class GemmRsPlan(WorkloadPlan):
+    """Partial tiles reduce-added into their row-block owner (workloads.py:343-408)."""
+
+    kind = WorkloadKind.GEMM_RS
+
+    def _build(self):
+        sp, n, t = self.spec, self.num_devices, FUNC_TILE
+        m, nd, k = sp.dim("M"), sp.dim("N"), sp.dim("K")
+        self.flops_per_device = 2.0 * m * nd * k
+        if m % (t * n) or nd % t:
+            raise WorkloadError(f"functional GEMM+RS needs M divisible by {t * n} and N by {t}")
+        if nd > 256:
+            raise WorkloadError("functional GEMM+RS supports N <= 256")
+        self.partial = [_randints(self.rng, (1, 1, m, nd)) for _ in range(n)]
+        self.pgls = {"partial": [p.copy() for p in self.partial], "out": [np.zeros((1, 1, m, nd)) for _ in range(n)]}
+        self.check_names = ["out"]
+
+    def run(self, comms, kspec, streams):
+        from . import ops
+        n = self.num_devices
+        m, nd = self.partial[0].shape[2:]
+        blk = m // n
+        pad_blk = ((blk + 127) // 128) * 128
+        eye = torch.eye(256, device="cuda", dtype=torch.bfloat16)      # C = partial @ I^T = partial
+        ins, outs = [], []
+        for r in range(n):                       # allocate everything before any rank launches
+            a = np.zeros((pad_blk * n, 256))
+            for o in range(n):
+                a[o * pad_blk:o * pad_blk + blk, :nd] = self.partial[r][0, 0, o * blk:(o + 1) * blk]
+            ins.append(_bf16(a))
+            outs.append(torch.empty(pad_blk, 256, device="cuda", dtype=torch.bfloat16))
+        torch.cuda.synchronize()
+        for r, c in enumerate(comms):
+            with torch.cuda.stream(streams[r]):
+                ops.gemm_reduce_scatter(c, ins[r], eye, out=outs[r], stream=streams[r])
+        torch.cuda.synchronize()
+        for r, o in enumerate(outs):
+            o = o.float().cpu().numpy()
+            self.pgls["out"][r][:] = 0
+            self.pgls["out"][r][0, 0, r * blk:(r + 1) * blk] = o[:blk, :nd]
+
+    def oracle(self):
+        n = self.num_devices
+        total = np.sum([p for p in self.partial], axis=0)
+        blk = total.shape[2] // n
+        outs = []
+        for d in range(n):
+            e = np.zeros(total.shape)
+            e[:, :, d * blk:(d + 1) * blk] = total[:, :, d * blk:(d + 1) * blk]
+            outs.append(e)
+        return {"out": outs}
+
+
+class GemmArPlan(WorkloadPlan):
+    """Partial outputs all-reduced across devices (workloads.py:415-546)."""
+
+    kind = WorkloadKind.GEMM_AR
+    default_mode = ScheduleMode.INTER_SM
+    default_comm_sms = 16
+
+    def _build(self):
+        sp, n, t = self.spec, self.num_devices, FUNC_TILE
+        m, nd, k = sp.dim("M"), sp.dim("N"), sp.dim("K")
+        self.flops_per_device = 2.0 * m * nd * k
+        if m % t or nd % t:
+            raise WorkloadError(f"functional GEMM+AR needs extents divisible by {t}")
+        self.inputs = [_randints(self.rng, (1, 1, m, nd)) for _ in range(n)]
+        self.pgls = {"acc": [np.zeros((1, 1, m, nd)) for _ in range(n)]}
+        self.check_names = ["acc"]
+
+    def run(self, comms, kspec, streams):
+        from . import ops
+        ts = []
+        for r, c in enumerate(comms):           # allocate everything before any rank launches
+            x = c.empty(self.inputs[r].shape[2:], torch.bfloat16)
+            x.copy_(_bf16(self.inputs[r][0, 0]))
+            ts.append(x)
+        torch.cuda.synchronize()
+        mode = "intra_sm" if kspec.schedule_mode is ScheduleMode.INTRA_SM else "inter_sm"
+        for r, c in enumerate(comms):
+            with torch.cuda.stream(streams[r]):
+                ops.all_reduce(c, ts[r], schedule={"mode": mode}, stream=streams[r])
+        torch.cuda.synchronize()
+        for r, x in enumerate(ts):
+            self.pgls["acc"][r][0, 0] = x.float().cpu().numpy()
+
+    def oracle(self):
+        total = np.sum(self.inputs, axis=0)
+        return {"acc": [total.copy() for _ in range(self.num_devices)]}
+
+
+class RingAttentionPlan(WorkloadPlan):
+    """KV shards visited around the ring (workloads.py:616-716).
+
+    The reference's functional check is `visited = sum_d kv_d` on every rank.
+    Here the tiles ride through the real ring-attention kernel: with q = 0 every
+    key gets the same score, so o = (sum over all visited V rows) / S_total.
+    Rank d's 16 x 16 tile sits in key 0 (row = head), so o * S_total recovers
+    the visited sum exactly (power-of-two denominators, integer numerators).
+    """
+
+    kind = WorkloadKind.RING_ATTENTION
+    default_mode = ScheduleMode.INTER_SM
+    default_comm_sms = 16
+
+    def _build(self):
+        sp, n, t = self.spec, self.num_devices, FUNC_TILE
+        b, s_len, h, d = sp.dim("B"), sp.dim("S"), sp.dim("H"), sp.dim("D")
+        if s_len % n:
+            raise WorkloadError("sequence length must divide across devices")
+        self.flops_per_device = n * 4.0 * b * h * (s_len // n) ** 2 * d
+        self.kv = [_randints(self.rng, (1, 1, t, t)) for _ in range(n)]
+        self.pgls = {"kv": [x.copy() for x in self.kv], "visited": [np.zeros((1, 1, t, t)) for _ in range(n)]}
+        self.check_names = ["visited"]
+
+    def run(self, comms, kspec, streams):
+        from . import ops
+        n, t = self.num_devices, FUNC_TILE
+        S_loc, H, D = 128, t, 128
+        ins, outs = [], []
+        for r in range(n):                       # allocate everything before any rank launches
+            v = np.zeros((1, S_loc, H, D))
+            v[0, 0, :, :t] = self.kv[r][0, 0]
+            ins.append((torch.zeros(1, S_loc, H, D, device="cuda", dtype=torch.bfloat16), _bf16(v)))
+            outs.append((torch.empty(1, S_loc, H, D, device="cuda", dtype=torch.bfloat16),
+                         torch.empty(1, H, S_loc, device="cuda", dtype=torch.float32)))
+        torch.cuda.synchronize()
+        for r, c in enumerate(comms):
+            q, v = ins[r]
+            with torch.cuda.stream(streams[r]):
+                ops.ring_attention(c, q, q, v, out=outs[r][0], lse=outs[r][1], stream=streams[r])
+        torch.cuda.synchronize()
+        outs = [o for o, _ in outs]
+        for r, o in enumerate(outs):
+            self.pgls["visited"][r][0, 0] = o[0, 0, :, :t].float().cpu().numpy() * (S_loc * n)
+
+    def oracle(self):
+        total = np.sum(self.kv, axis=0)
+        return {"visited": [total.copy() for _ in range(self.num_devices)]}
+
+
+class MoePlan(WorkloadPlan):
+    """Seeded TopK routing; tokens stored to expert owners (workloads.py:786-868)."""
+
+    kind = WorkloadKind.MOE_DISPATCH_GEMM
+
+    def _build(self):
+        sp, n, t = self.spec, self.num_devices, FUNC_TILE
+        top_k, n_exp = sp.dim("TopK"), sp.dim("N_experts")
+        h, h_exp, tokens = sp.dim("H"), sp.dim("H_expert"), sp.dim("T")
+        if top_k > n_exp:
+            raise WorkloadError("TopK cannot exceed the expert count")
+        scores = self.rng.random((n, tokens, n_exp))                     # workloads.py:800-802
+        self.route = np.argsort(scores, axis=2)[:, :, :top_k]
+        self.owners = self.route % n
+        self.token_data = [_randints(self.rng, (tokens, t, t)) for _ in range(n)]
+        counts = np.bincount(self.owners.reshape(-1), minlength=n)
+        self.flops_per_device = float(2.0 * counts.max() * h * h_exp)
+        self.smax = max(1, int(counts.max()))
+        self.pgls = {"recv": [np.zeros((1, 1, self.smax * t, t)) for _ in range(n)]}
+        self.check_names = ["recv"]
+
+    def run(self, comms, kspec, streams):
+        from . import ops
+        n, t = self.num_devices, FUNC_TILE
+        n_exp = self.spec.dim("N_experts")
+        T, K = self.route.shape[1:]
+        cap = T * K * n
+        ins, bufs = [], []
+        for r in range(n):                       # allocate everything before any rank launches
+            ins.append((_bf16(self.token_data[r].reshape(T, t * t)), torch.from_numpy(self.route[r].astype(np.int32)).cuda()))
+            bufs.append((comms[r].empty((cap, t * t)), comms[r].empty((cap,), torch.int32)))
+        torch.cuda.synchronize()
+        outs = []
+        for r, c in enumerate(comms):
+            with torch.cuda.stream(streams[r]):
+                outs.append(ops.moe_dispatch(c, ins[r][0], ins[r][1], n_exp, recv=bufs[r], stream=streams[r]))
+        torch.cuda.synchronize()
+        for o, (recv, _src, cnt) in enumerate(outs):
+            k = int(cnt.item())
+            rows = recv[:k].float().cpu().numpy().reshape(k, t, t)
+            self.pgls["recv"][o][:] = 0
+            self.pgls["recv"][o][0, 0, :k * t] = rows.reshape(k * t, t)
+
+    def oracle(self):
+        n, t = self.num_devices, FUNC_TILE
+        slots = {d: [] for d in range(n)}
+        for d in range(n):
+            for tk in range(self.route.shape[1]):
+                for k in range(self.route.shape[2]):
+                    slots[int(self.owners[d, tk, k])].append((d, tk, k))      # workloads.py:821-832
+        outs = [np.zeros((1, 1, self.smax * t, t)) for _ in range(n)]
+        for o in range(n):
+            for idx, (d, tk, _k) in enumerate(sorted(slots[o])):
+                outs[o][0, 0, idx * t:(idx + 1) * t] = self.token_data[d][tk]
+        return {"recv": outs}
+
+
+_PLAN_CLASSES = {cls.kind: cls for cls in (AgGemmPlan, GemmRsPlan, GemmArPlan, RingAttentionPlan, MoePlan)}
+
+
+def reduced_dims(kind: WorkloadKind, num_devices: int) -> dict:
+    """Tiny divisibility-safe dimensions for functional oracle runs (workloads.py:1073-1087)."""
+    n = num_devices
+    return {
+        WorkloadKind.GEMM_RS: dict(M=16 * n, N=32, K=64),
+        WorkloadKind.GEMM_AR: dict(M=32, N=32, K=64),
+        WorkloadKind.AG_GEMM: dict(M=8 * n, N=8 * n, K=64),
+        WorkloadKind.RING_ATTENTION: dict(B=1, S=8 * n, H=2, D=4),
+        WorkloadKind.MOE_DISPATCH_GEMM: dict(TopK=2, N_experts=2 * n, H=64, H_expert=64, T=4),
+    }[kind]
+
+
+def build(kind: WorkloadKind, dims: dict, profile=None, *, element_bytes: int = 2,
+          num_devices: Optional[int] = None, seed: int = 0, schedule_mode: Optional[ScheduleMode] = None,
+          num_comm_sms: Optional[int] = None, materialize: Optional[bool] = None,
+          pipeline_stages: int = 4):
+    """Instantiate one workload: (kernel spec, plan) (workloads.py:1040-1054)."""
+    if kind not in _PLAN_CLASSES:
+        raise WorkloadError(f"{kind.value} is not on the pk hot path (SURVEY.md §8)")
+    spec = WorkloadSpec(kind=kind, dims=dict(dims), element_bytes=element_bytes,
+                        num_devices=num_devices or 8, seed=seed, materialize=materialize)
+    plan = _PLAN_CLASSES[kind](spec)
+    kspec = plan.default_kernel_spec(schedule_mode, num_comm_sms, pipeline_stages)
+    return kspec, plan
+
+
+def execute_kernel(spec: LcscKernelSpec, workload: WorkloadPlan, profile=None, overheads=None, seed: int = 0,
+                   cfg=None, comms=None) -> ExecResult:
+    """Run one plan on the GPU and report its measured time (lcsc.py:141-159).
+
+    comms: one communicator per rank (default: a local group of
+    `num_devices` emulated ranks on cuda:0)."""
+    from .comm import local_group
+    spec.validate()
+    own = comms is None
+    if own:
+        comms = local_group(workload.num_devices, torch.cuda.current_device())
+    streams = [torch.cuda.Stream() for _ in comms]
+    t0 = time.perf_counter()
+    try:
+        workload.run(comms, spec, streams)
+        for c in comms:
+            c.check()
+    finally:
+        if own:
+            for c in comms:
+                c.destroy()
+    t_ns = (time.perf_counter() - t0) * 1e9
+    report = CostReport(t_total=t_ns, achieved_flops=workload.flops_per_device * workload.num_devices / (t_ns / 1e9))
+    return ExecResult(report=report, pgls=dict(workload.pgls))
+
+
+def check_oracle(plan: WorkloadPlan):
+    """None on bit-identical match, else (layout name, first divergent index) (workloads.py:1057-1070)."""
+    expected = plan.oracle()
+    actual = plan.final_state()
+    for name, exp_bufs in expected.items():
+        for dev, (exp, got) in enumerate(zip(exp_bufs, actual[name])):
+            if not np.array_equal(exp, got):
+                idx = np.argwhere(exp != got)[0]
+                return name, (dev, *map(int, idx))
+    return None

@@ -167,6 +167,21 @@ static void* p2p_kernel_for(int n) {
   }
 }
 
+int preload_allreduce() {
+  cudaFuncAttributes fa;
+  PK_CUDA(cudaFuncGetAttributes(&fa, ar_nvls_kernel<PK_BF16>));
+  PK_CUDA(cudaFuncGetAttributes(&fa, ar_nvls_kernel<PK_F32>));
+  for (int n = 1; n <= 8; ++n) {
+    PK_CUDA(cudaFuncGetAttributes(&fa, p2p_kernel_for<PK_BF16, PK_OP_SUM>(n)));
+    PK_CUDA(cudaFuncGetAttributes(&fa, p2p_kernel_for<PK_BF16, PK_OP_MAX>(n)));
+    PK_CUDA(cudaFuncGetAttributes(&fa, p2p_kernel_for<PK_BF16, PK_OP_MIN>(n)));
+    PK_CUDA(cudaFuncGetAttributes(&fa, p2p_kernel_for<PK_F32, PK_OP_SUM>(n)));
+    PK_CUDA(cudaFuncGetAttributes(&fa, p2p_kernel_for<PK_F32, PK_OP_MAX>(n)));
+    PK_CUDA(cudaFuncGetAttributes(&fa, p2p_kernel_for<PK_F32, PK_OP_MIN>(n)));
+  }
+  return PK_OK;
+}
+
 int all_reduce(Comm* c, pk_tensor* x, int op, const pk_sched* sched, cudaStream_t st) {
   if (!x || !x->ptr) return fail(PK_ERR_INVALID, "all_reduce: null tensor");
   if (x->dtype != PK_BF16 && x->dtype != PK_F32) return fail(PK_ERR_CAPABILITY, "all_reduce: dtype must be bf16 or f32");

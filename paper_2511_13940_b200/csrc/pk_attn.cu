@@ -373,6 +373,14 @@ __global__ void sync_wait_kernel(const uint32_t* counters, int n, uint32_t expec
   for (int d = 0; d < n; ++d) wait_geq(counters + d, expected, err, timeout);
 }
 
+int preload_attn() {
+  cudaFuncAttributes fa;
+  PK_CUDA(cudaFuncGetAttributes(&fa, attn_fwd_kernel));
+  PK_CUDA(cudaFuncGetAttributes(&fa, sync_signal_kernel));
+  PK_CUDA(cudaFuncGetAttributes(&fa, sync_wait_kernel));
+  return PK_OK;
+}
+
 static int signal_all(Comm* c, int which_off, cudaStream_t st) {
   uint32_t* ps[8] = {};
   for (int r = 0; r < c->world; ++r) ps[r] = static_cast<uint32_t*>(c->sync->peers[r]) + which_off + c->rank;

@@ -507,7 +507,30 @@ static int query_multicast(int device, bool* out) {
   return PK_OK;
 }
 
+int preload_gemm();
+int preload_allreduce();
+int preload_moe();
+int preload_attn();
+
+// Load every kernel image up front. With lazy module loading the first launch
+// of a kernel can synchronise the context; in a local group that launch may
+// come after another rank's kernel is already spinning in wait() for this
+// rank, which would deadlock until the wait times out.
+static int preload_kernels() {
+  static std::once_flag once;
+  static int status = PK_OK;
+  std::call_once(once, [] {
+    int s = preload_gemm();
+    if (s == PK_OK) s = preload_allreduce();
+    if (s == PK_OK) s = preload_moe();
+    if (s == PK_OK) s = preload_attn();
+    status = s;
+  });
+  return status;
+}
+
 static int comm_finish_init(Comm* c) {
+  PK_TRY(preload_kernels());
   PK_TRY(pgl_alloc(c, kSyncBytes, 0, &c->sync));
   c->max_flags = (int)((kSyncBytes / 4) - kSyncFlags);
   return PK_OK;

@@ -257,6 +257,14 @@ __global__ void __launch_bounds__(kCombineThreads) moe_combine_kernel(const __gr
 }
 
 // ---------------------------------------------------------------- host
+int preload_moe() {
+  cudaFuncAttributes fa;
+  PK_CUDA(cudaFuncGetAttributes(&fa, moe_count_kernel));
+  PK_CUDA(cudaFuncGetAttributes(&fa, moe_dispatch_kernel));
+  PK_CUDA(cudaFuncGetAttributes(&fa, moe_combine_kernel));
+  return PK_OK;
+}
+
 static void fill_moe_sync(Comm* c, MoeSync& s) {
   uint32_t* local = static_cast<uint32_t*>(c->sync->local);
   s.ready_local = local + kSyncReady;

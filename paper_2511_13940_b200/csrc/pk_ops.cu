@@ -73,6 +73,16 @@ int launch_gemm_variant(Variant v, int epi, const GemmArgs& args, int grid_ctas,
   return fail(PK_ERR_INVALID, "no GEMM variant for cta_group=%d am=%d epi=%d", v.cg, v.am, epi);
 }
 
+// Force-load every kernel image now (see preload_kernels in pk_comm.cu).
+int preload_gemm() {
+  cudaFuncAttributes fa;
+#define PK_L(CG, AM, E) PK_CUDA(cudaFuncGetAttributes(&fa, lcsc_gemm_kernel<CG, 256, AM, E>));
+  PK_L(2, 2, EPI_STORE) PK_L(2, 2, EPI_REDUCE_ADD) PK_L(2, 1, EPI_STORE) PK_L(2, 1, EPI_REDUCE_ADD)
+  PK_L(1, 1, EPI_STORE) PK_L(1, 1, EPI_REDUCE_ADD)
+#undef PK_L
+  return PK_OK;
+}
+
 // Pick the tile shape for a row partition of `rows_per_part` rows:
 //   512-row pair tiles (256 x 256 per CTA, one TMEM accumulator stage) cut
 //   L2->SM traffic by 25% vs 256-row pair tiles; the latter double-buffer
@@ -229,6 +239,9 @@ int ag_gemm(Comm* c, const pk_tensor* A, const pk_tensor* B, pk_tensor* C, pk_te
   } else {
     const int comm_sms = (sched && sched->num_comm_sms > 0) ? sched->num_comm_sms : std::max(2, std::min(16, c->num_sms / 8));
     comm_clusters = std::max(1, comm_sms / cg);
+    // An emulated rank owns only num_sms/world SMs: scale the communicator
+    // share down with it instead of starving the GEMM.
+    if (c->local_group) comm_clusters = std::min(comm_clusters, std::max(1, clusters_total / 4));
     if (comm_clusters >= clusters_total) return fail(PK_ERR_INVALID, "ag_gemm: num_comm_sms leaves no compute SMs");
     void* gathered;
     if (AG) {

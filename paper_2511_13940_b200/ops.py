@@ -142,7 +142,7 @@ def moe_dispatch(comm, x: torch.Tensor, topk_idx: torch.Tensor, num_experts: int
     if recv is None:
         recv = (comm.empty((capacity, x.shape[1]), torch.bfloat16), comm.empty((capacity,), torch.int32))
     recv_rows, recv_src = recv
-    count = torch.zeros(1, dtype=torch.int32, device=x.device)
+    count = torch.empty(1, dtype=torch.int32, device=x.device)
     lib = _lib.load()
     dx, dt = _lib.tensor_desc(x), _lib.tensor_desc(topk_idx)
     dr, ds, dc = _lib.tensor_desc(recv_rows), _lib.tensor_desc(recv_src), _lib.tensor_desc(count)

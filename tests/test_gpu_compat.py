@@ -1,0 +1,30 @@
+"""Criterion-8-style sweep through the GPU (test_acceptance.py:230-249): every
+hot-path kind x n in {2, 4, 8} x seeds runs through the real fused ops on a
+local group and must match its oracle bit for bit."""
+import pytest
+
+from paper_2511_13940_b200 import compat
+
+pytestmark = pytest.mark.gpu
+
+KINDS = [compat.WorkloadKind.AG_GEMM, compat.WorkloadKind.GEMM_RS, compat.WorkloadKind.GEMM_AR,
+         compat.WorkloadKind.RING_ATTENTION, compat.WorkloadKind.MOE_DISPATCH_GEMM]
+
+
+@pytest.mark.parametrize("kind", KINDS)
+@pytest.mark.parametrize("n", [2, 4, 8])
+def test_functional_runs_match_oracle(kind, n):
+    for seed in range(2):
+        kspec, plan = compat.build(kind, compat.reduced_dims(kind, n), num_devices=n, seed=seed)
+        res = compat.execute_kernel(kspec, plan)
+        assert res.report.t_total > 0
+        assert compat.check_oracle(plan) is None, (kind, n, seed, compat.check_oracle(plan))
+
+
+@pytest.mark.parametrize("mode", [compat.ScheduleMode.INTRA_SM, compat.ScheduleMode.INTER_SM])
+def test_schedule_modes(mode):
+    for kind in (compat.WorkloadKind.AG_GEMM, compat.WorkloadKind.GEMM_AR):
+        kspec, plan = compat.build(kind, compat.reduced_dims(kind, 4), num_devices=4, seed=5, schedule_mode=mode,
+                                   num_comm_sms=None if mode is compat.ScheduleMode.INTRA_SM else 4)
+        compat.execute_kernel(kspec, plan)
+        assert compat.check_oracle(plan) is None
