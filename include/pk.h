@@ -102,6 +102,10 @@ PK_API int pk_comm_set_timeout(pk_comm* comm, uint64_t ns);
  * 3 = MoE receive capacity exceeded. Synchronises with the device. */
 PK_API int pk_comm_check(pk_comm* comm, int* code);
 
+/* Diagnostics: host-only self test of the multi-process rendezvous (rank-id
+ * allgather, barrier, SCM_RIGHTS fd exchange). Needs no GPU. */
+PK_API int pk_debug_rendezvous(int rank, int world, const char* uid);
+
 /* ---- parallel global layouts --------------------------------------------- */
 PK_API int pk_pgl_alloc(pk_comm* comm, size_t bytes, uint32_t flags, pk_pgl** out);
 /* local = this rank's buffer; peers[world] = every rank's buffer as seen by

@@ -32,6 +32,7 @@
 #include <mutex>
 #include <thread>
 #include <sys/socket.h>
+#include <sys/mman.h>
 #include <sys/un.h>
 #include <unistd.h>
 
@@ -538,9 +539,75 @@ static int comm_finish_init(Comm* c) {
 
 }  // namespace pk
 
+namespace pk {
+
+static int open_listener(Comm* c) {
+  c->listen_fd = ::socket(AF_UNIX, SOCK_STREAM, 0);
+  sockaddr_un a; socklen_t len;
+  sock_name(c->uid, c->rank, &a, &len);
+  if (c->listen_fd < 0 || ::bind(c->listen_fd, reinterpret_cast<sockaddr*>(&a), len) != 0 ||
+      ::listen(c->listen_fd, 256) != 0) {
+    int e = errno;
+    if (c->listen_fd >= 0) ::close(c->listen_fd);
+    c->listen_fd = -1;
+    return fail(PK_ERR_CUDA, "rendezvous socket for rank %d: %s", c->rank, strerror(e));
+  }
+  return PK_OK;
+}
+
+// Host-only self test of the multi-process rendezvous: allgather of rank ids,
+// a barrier, and an SCM_RIGHTS exchange of memfds whose contents name the
+// sender (the same path VMM handles take in vmm_pgl_alloc).
+static int rendezvous_selftest(int rank, int world, const char* uid) {
+  Comm c;
+  c.rank = rank;
+  c.world = world;
+  c.uid = uid;
+  PK_TRY(open_listener(&c));
+  struct Closer { Comm* c; ~Closer() { if (c->listen_fd >= 0) ::close(c->listen_fd); } } closer{&c};
+  std::vector<int> ids(world, -1);
+  int mine = 1000 + rank;
+  PK_TRY(comm_allgather(&c, &mine, ids.data(), sizeof(int)));
+  for (int r = 0; r < world; ++r)
+    if (ids[r] != 1000 + r) return fail(PK_ERR_PROTOCOL, "allgather: slot %d holds %d", r, ids[r]);
+  PK_TRY(comm_barrier(&c));
+  char name[64];
+  snprintf(name, sizeof(name), "pk-selftest-%d", rank);
+  int fd = ::memfd_create(name, 0);
+  if (fd < 0) return fail(PK_ERR_CUDA, "memfd_create: %s", strerror(errno));
+  char payload[32];
+  const int plen = snprintf(payload, sizeof(payload), "rank-%d", rank);
+  if (::write(fd, payload, plen) != plen) { ::close(fd); return fail(PK_ERR_CUDA, "memfd write"); }
+  int fds[kMaxRanks];
+  uint64_t sizes[kMaxRanks];
+  int st = exchange_fds(&c, fd, (uint64_t)plen, fds, sizes);
+  ::close(fd);
+  if (st != PK_OK) return st;
+  for (int r = 0; r < world; ++r) {
+    if (r == rank) continue;
+    char buf[32] = {};
+    const ssize_t n = ::pread(fds[r], buf, sizeof(buf) - 1, 0);
+    ::close(fds[r]);
+    char want[32];
+    snprintf(want, sizeof(want), "rank-%d", r);
+    if (n <= 0 || strcmp(buf, want) != 0 || sizes[r] != strlen(want))
+      return fail(PK_ERR_PROTOCOL, "fd from rank %d carried '%s'", r, buf);
+  }
+  PK_TRY(comm_barrier(&c));
+  return PK_OK;
+}
+
+}  // namespace pk
+
 using namespace pk;
 
 extern "C" {
+
+PK_API int pk_debug_rendezvous(int rank, int world, const char* uid) {
+  if (world < 2 || world > kMaxRanks || rank < 0 || rank >= world || !uid || !*uid)
+    return fail(PK_ERR_INVALID, "pk_debug_rendezvous: bad rank %d / world %d", rank, world);
+  return rendezvous_selftest(rank, world, uid);
+}
 
 PK_API int pk_comm_init(int rank, int world, int device, const char* uid, pk_comm** out) {
   if (world < 1 || world > kMaxRanks || rank < 0 || rank >= world)
@@ -557,16 +624,8 @@ PK_API int pk_comm_init(int rank, int world, int device, const char* uid, pk_com
   query_multicast(device, &mc);
   c->multicast_supported = mc && world > 1;
   if (world > 1) {
-    c->listen_fd = ::socket(AF_UNIX, SOCK_STREAM, 0);
-    sockaddr_un a; socklen_t len;
-    sock_name(c->uid, rank, &a, &len);
-    if (c->listen_fd < 0 || ::bind(c->listen_fd, reinterpret_cast<sockaddr*>(&a), len) != 0 ||
-        ::listen(c->listen_fd, 256) != 0) {
-      int e = errno;
-      if (c->listen_fd >= 0) ::close(c->listen_fd);
-      delete c;
-      return fail(PK_ERR_CUDA, "rendezvous socket for rank %d: %s", rank, strerror(e));
-    }
+    const int st = open_listener(c);
+    if (st != PK_OK) { delete c; return st; }
   }
   int st = comm_finish_init(c);
   if (st != PK_OK) { if (c->listen_fd >= 0) ::close(c->listen_fd); delete c; return st; }
