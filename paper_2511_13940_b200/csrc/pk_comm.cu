@@ -624,8 +624,19 @@ PK_API int pk_comm_init(int rank, int world, int device, const char* uid, pk_com
   query_multicast(device, &mc);
   c->multicast_supported = mc && world > 1;
   if (world > 1) {
-    const int st = open_listener(c);
+    int st = open_listener(c);
     if (st != PK_OK) { delete c; return st; }
+    // NVLS needs every rank on a distinct GPU (a device joins a multicast
+    // object once); ranks sharing a GPU fall back to P2P register ops.
+    cudaDeviceProp prop;
+    memset(&prop, 0, sizeof(prop));
+    cudaGetDeviceProperties(&prop, device);
+    std::vector<cudaUUID_t> ids(world);
+    st = comm_allgather(c, &prop.uuid, ids.data(), sizeof(cudaUUID_t));
+    if (st != PK_OK) { ::close(c->listen_fd); delete c; return st; }
+    for (int i = 0; i < world; ++i)
+      for (int j = i + 1; j < world; ++j)
+        if (memcmp(&ids[i], &ids[j], sizeof(cudaUUID_t)) == 0) c->multicast_supported = false;
   }
   int st = comm_finish_init(c);
   if (st != PK_OK) { if (c->listen_fd >= 0) ::close(c->listen_fd); delete c; return st; }

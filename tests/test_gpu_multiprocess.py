@@ -1,0 +1,32 @@
+"""The multi-process path (pk_comm_init: VMM + POSIX-fd exchange over Unix
+sockets) under torchrun, world 2. On a single-GPU box both ranks share
+cuda:0 (their kernels time-slice); with >= 2 GPUs each rank gets its own."""
+import os
+import socket
+import subprocess
+import sys
+
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+HERE = os.path.dirname(os.path.abspath(__file__))
+
+
+def _port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def test_torchrun_world2():
+    env = dict(os.environ)
+    if torch.cuda.device_count() < 2:
+        env["PK_TEST_DEVICE"] = "0"
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr", "127.0.0.1", "--master-port", str(_port()), os.path.join(HERE, "mp_worker.py")]
+    r = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    assert r.stdout.count("multiprocess ok") == 2, r.stdout
