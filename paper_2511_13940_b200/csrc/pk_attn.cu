@@ -10,14 +10,16 @@
 //
 // B200 design:
 //   * compute: a tcgen05 flash-attention forward kernel (attn_fwd_kernel).
-//     One CTA = one 128-query tile of one (batch, head); one CTA per SM.
-//       warp 0      loader   : TMA Q once, K/V 64-key blocks (K 3 stages, V 2)
-//       warp 1      MMA      : S = Q K^T (M128 N64 K128) into TMEM (double
-//                              buffered), O_blk = P V (M128 N128 K64, V as an
-//                              MN-major operand) into TMEM
-//       warps 4-7   softmax  : TMEM -> regs, online max / exp2 / row sum,
-//                              P (bf16) -> 128B-swizzled smem (A operand)
-//       warps 8-11  correct  : O = O*alpha + O_blk in registers; epilogue
+//     One CTA = two 128-query tiles of one (batch, head); one CTA per SM.
+//       warp 0      loader   : TMA Q (both tiles) once, K/V 128-key blocks
+//                              shared by the two tiles (2 stages each)
+//       warp 1      MMA      : S_x = Q_x K^T (M128 N128 K128) into TMEM;
+//                              O_x += P_x V (P_x read from TMEM, V as an
+//                              MN-major smem operand) accumulated in TMEM;
+//                              ping-pongs between the two tiles
+//       warps 4-7 / 8-11 softmax of tile 0 / 1: max pass, lazy rescale of O
+//                              in TMEM, exp2, P (bf16x2) back into TMEM;
+//                              final epilogue
 //     The running (O, m, l) state crosses ring steps through global memory
 //     (fp32), merged by log-sum-exp; the last step writes o (bf16) and lse.
 //   * communication: the shard of step s+1 is pulled from its owner's
@@ -34,20 +36,18 @@
 
 namespace pk {
 
-constexpr int AT_BM = 128;       // queries per CTA
-constexpr int AT_BN = 64;        // keys per block
+constexpr int AT_BM = 128;       // queries per tile (two tiles per CTA)
+constexpr int AT_BN = 128;       // keys per block
 constexpr int AT_D = 128;        // head dim
-constexpr int AT_THREADS = 384;
-constexpr int AT_Q_BYTES = AT_BM * AT_D * 2;     // 32 KB (2 swizzle atoms of 16 KB)
-constexpr int AT_K_BYTES = AT_BN * AT_D * 2;     // 16 KB
-constexpr int AT_V_BYTES = AT_BN * AT_D * 2;     // 16 KB
-constexpr int AT_P_BYTES = AT_BM * AT_BN * 2;    // 16 KB
-constexpr int AT_KSTAGES = 3;
+constexpr int AT_THREADS = 384;  // loader, MMA, TMEM alloc, idle, 2 x 4 softmax warps
+constexpr int AT_Q_BYTES = AT_BM * AT_D * 2;     // 32 KB per tile (2 swizzle atoms of 16 KB)
+constexpr int AT_K_BYTES = AT_BN * AT_D * 2;     // 32 KB
+constexpr int AT_V_BYTES = AT_BN * AT_D * 2;     // 32 KB
+constexpr int AT_KSTAGES = 2;
 constexpr int AT_VSTAGES = 2;
-constexpr int AT_ALPHA = 4;                       // alpha ring slots
-constexpr int AT_SMEM = AT_Q_BYTES + AT_KSTAGES * AT_K_BYTES + AT_VSTAGES * AT_V_BYTES + 2 * AT_P_BYTES +
-                        (AT_ALPHA + 2) * AT_BM * 4 + 512 + 1024;
-constexpr int AT_TMEM_COLS = 512;                // S[2] (2 x 64) + O_blk[2] (2 x 128)
+constexpr int AT_SMEM = 2 * AT_Q_BYTES + AT_KSTAGES * AT_K_BYTES + AT_VSTAGES * AT_V_BYTES + 512 + 1024;
+constexpr int AT_TMEM_COLS = 512;                // per tile: S (128, P aliased in its first 64) + O (128)
+constexpr float AT_RESCALE_THRESHOLD = 8.0f;     // log2 units: P stays <= 2^8 between rescales
 
 struct AttnArgs {
   CUtensorMap tm_q, tm_k, tm_v;  // 4-D maps over [B, S, H, D] (dims D, H, S, B)
@@ -93,56 +93,54 @@ PK_DEV float fast_exp2(float x) {
   return y;
 }
 
-// Pipeline invariants (j = key block):
-//   K_j -> k stage j%3, V_j -> v stage j%2, S_j -> TMEM S[j%2], P_j -> smem P[j%2],
-//   P_j V_j -> TMEM O[j%2], alpha_j -> smem ring slot j%4.
-//   alpha slot reuse is safe: softmax writes alpha_{j+4} only after P slot
-//   (j+4)%2 is free, i.e. after PV_{j+2} completed, which waited O[j%2] to be
-//   drained by the correction of block j (which read alpha_j first).
+// Two 128-query tiles (X = 0, 1) share every K/V block; the single MMA warp
+// ping-pongs between them so one tile's softmax overlaps the other tile's
+// tensor-core work (FA4-style).
+// Per tile X and 128-key block j:
+//   S_X = Q_X K_j^T -> TMEM S_X (fp32, 128 cols)
+//   softmax_X: max pass over S_X; lazy rescale of O_X in TMEM when the row max
+//   grows by more than AT_RESCALE_THRESHOLD; P_X = exp2(S_X*scale - m) packed
+//   bf16x2 back into S_X's first 64 columns (each chunk is read before the
+//   packed half that aliases it is written)
+//   O_X += P_X V_j with P_X as a TMEM A operand, V_j MN-major in smem.
+// Ordering: the MMAs of one thread complete in issue order, so s_full_X(j)
+// (committed after QK_X(j), which is issued after PV_X(j-1)) also means PV_X(j-1)
+// has finished reading P_X(j-1) and updating O_X.
 __global__ void __launch_bounds__(AT_THREADS, 1) attn_fwd_kernel(const __grid_constant__ AttnArgs a) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* sq = smem;
-  uint8_t* sk = sq + AT_Q_BYTES;
+  uint8_t* sq = smem;                               // [2][32 KB]
+  uint8_t* sk = sq + 2 * AT_Q_BYTES;
   uint8_t* sv = sk + AT_KSTAGES * AT_K_BYTES;
-  uint8_t* sp = sv + AT_VSTAGES * AT_V_BYTES;
-  float* alpha_s = reinterpret_cast<float*>(sp + 2 * AT_P_BYTES);    // [AT_ALPHA][128]
-  float* stat_m = alpha_s + AT_ALPHA * AT_BM;                          // [128]
-  float* stat_l = stat_m + AT_BM;                                      // [128]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(stat_l + AT_BM);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sv + AT_VSTAGES * AT_V_BYTES);
   uint64_t* q_full = bars + 0;
-  uint64_t* k_full = bars + 1;      // [3]
-  uint64_t* k_empty = bars + 4;     // [3]
-  uint64_t* v_full = bars + 7;      // [2]
-  uint64_t* v_empty = bars + 9;     // [2]
-  uint64_t* s_full = bars + 11;     // [2]
-  uint64_t* s_empty = bars + 13;    // [2]
-  uint64_t* p_full = bars + 15;     // [2]
-  uint64_t* p_empty = bars + 17;    // [2]
-  uint64_t* pv_full = bars + 19;    // [2]
-  uint64_t* pv_empty = bars + 21;   // [2]
-  uint64_t* stat_full = bars + 23;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 24);
+  uint64_t* k_full = bars + 1;      // [2]
+  uint64_t* k_empty = bars + 3;     // [2]
+  uint64_t* v_full = bars + 5;      // [2]
+  uint64_t* v_empty = bars + 7;     // [2]
+  uint64_t* s_full = bars + 9;      // [2] per tile
+  uint64_t* p_full = bars + 11;     // [2] per tile
+  uint64_t* o_full = bars + 13;     // [2] per tile
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 15);
 
   const uint32_t warp = warp_id_sync();
   const uint32_t lane = lane_id();
   const int q_tiles = a.S_q / AT_BM;
+  const int pairs = (q_tiles + 1) / 2;
   const int tile = blockIdx.x;
-  const int qt = tile % q_tiles;
-  const int h = (tile / q_tiles) % a.H;
-  const int b = tile / (q_tiles * a.H);
+  const int qp = tile % pairs;
+  const int h = (tile / pairs) % a.H;
+  const int b = tile / (pairs * a.H);
+  const int ntile = (2 * qp + 1 < q_tiles) ? 2 : 1;   // the last pair may hold one tile
   const int nblk = a.S_kv / AT_BN;
 
   if (warp == 0 && lane == 0) {
     mbar_init(q_full, 1);
-    for (int i = 0; i < AT_KSTAGES; ++i) { mbar_init(&k_full[i], 1); mbar_init(&k_empty[i], 1); }
     for (int i = 0; i < 2; ++i) {
+      mbar_init(&k_full[i], 1); mbar_init(&k_empty[i], 1);
       mbar_init(&v_full[i], 1); mbar_init(&v_empty[i], 1);
-      mbar_init(&s_full[i], 1); mbar_init(&s_empty[i], 4);
-      mbar_init(&p_full[i], 4); mbar_init(&p_empty[i], 1);
-      mbar_init(&pv_full[i], 1); mbar_init(&pv_empty[i], 4);
+      mbar_init(&s_full[i], 1); mbar_init(&p_full[i], 4); mbar_init(&o_full[i], 1);
     }
-    mbar_init(stat_full, 4);
     fence_mbar_init();
   }
   if (warp == 2) tmem_alloc<AT_TMEM_COLS, 1>(tmem_slot);
@@ -150,29 +148,28 @@ __global__ void __launch_bounds__(AT_THREADS, 1) attn_fwd_kernel(const __grid_co
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  const uint32_t t_s = tmem;            // S[2] at cols [0,64), [64,128)
-  const uint32_t t_o = tmem + 128;      // O_blk[2] at cols [128,256), [256,384)
+  // tile X: S at cols [256X, 256X+128) (P packed in its first 64), O at [256X+128, 256X+256)
 
   if (warp == 0) {
-    // ------------------------------------------------------------ loader (lane 0; the
-    // warp reconverges at __syncwarp before the teardown barrier)
+    // ------------------------------------------------------------ loader (lane 0)
     if (lane == 0) {
-      mbar_arrive_expect_tx(q_full, AT_Q_BYTES);
-      tma_load_4d(&a.tm_q, q_full, sq, 0, h, qt * AT_BM, b);
-      tma_load_4d(&a.tm_q, q_full, sq + AT_Q_BYTES / 2, 64, h, qt * AT_BM, b);
+      mbar_arrive_expect_tx(q_full, ntile * AT_Q_BYTES);
+      for (int x = 0; x < ntile; ++x) {
+        const int qrow = (2 * qp + x) * AT_BM;
+        tma_load_4d(&a.tm_q, q_full, sq + x * AT_Q_BYTES, 0, h, qrow, b);
+        tma_load_4d(&a.tm_q, q_full, sq + x * AT_Q_BYTES + AT_Q_BYTES / 2, 64, h, qrow, b);
+      }
       auto load_k = [&](int j) {
-        const int st = j % AT_KSTAGES;
-        mbar_wait(&k_empty[st], ((j / AT_KSTAGES) & 1) ^ 1);
+        const int st = j & 1;
+        mbar_wait(&k_empty[st], ((j >> 1) & 1) ^ 1);
         uint8_t* kb = sk + st * AT_K_BYTES;
         mbar_arrive_expect_tx(&k_full[st], AT_K_BYTES);
         tma_load_4d(&a.tm_k, &k_full[st], kb, 0, h, j * AT_BN, b);
         tma_load_4d(&a.tm_k, &k_full[st], kb + AT_K_BYTES / 2, 64, h, j * AT_BN, b);
       };
-      // K runs up to two blocks ahead of V so S = Q K^T never waits on P V.
       if (nblk > 0) load_k(0);
-      if (nblk > 1) load_k(1);
       for (int j = 0; j < nblk; ++j) {
-        if (j + 2 < nblk) load_k(j + 2);
+        if (j + 1 < nblk) load_k(j + 1);
         const int vs = j & 1;
         mbar_wait(&v_empty[vs], ((j >> 1) & 1) ^ 1);
         uint8_t* vb = sv + vs * AT_V_BYTES;
@@ -188,131 +185,128 @@ __global__ void __launch_bounds__(AT_THREADS, 1) attn_fwd_kernel(const __grid_co
     constexpr uint32_t id_o = idesc_bf16(AT_BM, AT_D, 1);
     mbar_wait(q_full, 0);
     tc_fence_after();
-    const uint32_t q_addr = smem_u32(sq);
-    auto issue_pv = [&](int j) {
-      const int bs = j & 1;
-      const uint32_t ph = (j >> 1) & 1;
-      mbar_wait(&v_full[bs], ph);
-      mbar_wait(&p_full[bs], ph);
-      mbar_wait(&pv_empty[bs], ph ^ 1);
-      tc_fence_after();
-      if (elect_one()) {
-        const uint32_t p_addr = smem_u32(sp + bs * AT_P_BYTES);
-        const uint32_t v_addr = smem_u32(sv + bs * AT_V_BYTES);
+    auto issue_qk = [&](int x, int j) {                 // S_x = Q_x K_j^T
+      const uint32_t q_addr = smem_u32(sq + x * AT_Q_BYTES);
+      const uint32_t k_addr = smem_u32(sk + (j & 1) * AT_K_BYTES);
 #pragma unroll
-        for (int kk = 0; kk < AT_BN / 16; ++kk) {
-          const uint64_t ad = sdesc_kmajor_sw128(p_addr) + (uint64_t)(kk * 2);   // +32 B per 16 keys
-          // V: keys are K (8-row groups 1024 B apart), D is N (64-col groups 8 KB apart)
-          const uint64_t bd = sdesc_mnmajor_sw128(v_addr + kk * 2048, AT_V_BYTES / 2, 1024);
-          umma_f16<1>(t_o + bs * AT_D, ad, bd, id_o, kk > 0 ? 1u : 0u);
-        }
-        umma_commit<1>(&pv_full[bs]);
-        umma_commit<1>(&p_empty[bs]);
-        umma_commit<1>(&v_empty[bs]);
+      for (int kk = 0; kk < AT_D / 16; ++kk) {
+        const int atom = kk >> 2, sub = kk & 3;
+        const uint64_t ad = sdesc_kmajor_sw128(q_addr + atom * (AT_Q_BYTES / 2)) + (uint64_t)(sub * 2);
+        const uint64_t bd = sdesc_kmajor_sw128(k_addr + atom * (AT_K_BYTES / 2)) + (uint64_t)(sub * 2);
+        umma_f16<1>(tmem + 256 * x, ad, bd, id_s, kk > 0 ? 1u : 0u);
       }
-      __syncwarp();
+      umma_commit<1>(&s_full[x]);
     };
-    for (int j = 0; j < nblk; ++j) {
-      const int st = j % AT_KSTAGES;
-      const int bs = j & 1;
-      mbar_wait(&k_full[st], (j / AT_KSTAGES) & 1);
-      mbar_wait(&s_empty[bs], ((j >> 1) & 1) ^ 1);
+    auto issue_pv = [&](int x, int j) {                 // O_x += P_x V_j
+      const uint32_t v_addr = smem_u32(sv + (j & 1) * AT_V_BYTES);
+#pragma unroll
+      for (int kk = 0; kk < AT_BN / 16; ++kk) {
+        const uint64_t bd = sdesc_mnmajor_sw128(v_addr + kk * 2048, AT_V_BYTES / 2, 1024);
+        umma_f16_ts(tmem + 256 * x + 128, tmem + 256 * x + kk * 8, bd, id_o, (j > 0 || kk > 0) ? 1u : 0u);
+      }
+      if (j == nblk - 1) umma_commit<1>(&o_full[x]);
+    };
+    if (nblk > 0) {
+      mbar_wait(&k_full[0], 0);
       tc_fence_after();
       if (elect_one()) {
-        const uint32_t k_addr = smem_u32(sk + st * AT_K_BYTES);
-#pragma unroll
-        for (int kk = 0; kk < AT_D / 16; ++kk) {
-          const int atom = kk >> 2, sub = kk & 3;
-          const uint64_t ad = sdesc_kmajor_sw128(q_addr + atom * (AT_Q_BYTES / 2)) + (uint64_t)(sub * 2);
-          const uint64_t bd = sdesc_kmajor_sw128(k_addr + atom * (AT_K_BYTES / 2)) + (uint64_t)(sub * 2);
-          umma_f16<1>(t_s + bs * AT_BN, ad, bd, id_s, kk > 0 ? 1u : 0u);
-        }
-        umma_commit<1>(&s_full[bs]);
-        umma_commit<1>(&k_empty[st]);
+        for (int x = 0; x < ntile; ++x) issue_qk(x, 0);
+        umma_commit<1>(&k_empty[0]);
       }
       __syncwarp();
-      if (j > 0) issue_pv(j - 1);
     }
-    if (nblk > 0) issue_pv(nblk - 1);
-  } else if (warp >= 4 && warp < 8) {
-    // ------------------------------------------------------------ softmax
+    for (int j = 0; j < nblk; ++j) {
+      mbar_wait(&v_full[j & 1], (j >> 1) & 1);
+      const bool more = j + 1 < nblk;
+      if (more) mbar_wait(&k_full[(j + 1) & 1], ((j + 1) >> 1) & 1);
+      for (int x = 0; x < ntile; ++x) {
+        mbar_wait(&p_full[x], j & 1);
+        tc_fence_after();
+        if (elect_one()) {
+          issue_pv(x, j);
+          if (more) issue_qk(x, j + 1);
+        }
+        __syncwarp();
+      }
+      if (elect_one()) {
+        umma_commit<1>(&v_empty[j & 1]);
+        if (more) umma_commit<1>(&k_empty[(j + 1) & 1]);
+      }
+      __syncwarp();
+    }
+  } else if (warp >= 4 && (int)(warp - 4) / 4 < ntile) {
+    // ------------------------------------------------------------ softmax + epilogue (tile x)
+    const int x = (warp - 4) / 4;
+    const int qt = 2 * qp + x;
     const int q = warp & 3;
     const int row = q * 32 + (int)lane;
     const uint32_t lane_off = (uint32_t)(q * 32) << 16;
-    float m = -INFINITY, l = 0.f;
+    const uint32_t t_s = tmem + 256 * x + lane_off;
+    const uint32_t t_o = t_s + 128;
+    float m = -INFINITY, l = 0.f;     // m: the max the current P values are relative to (log2 units)
     const float sc = a.scale_log2;
     for (int j = 0; j < nblk; ++j) {
-      const int bs = j & 1;
-      const uint32_t ph = (j >> 1) & 1;
-      mbar_wait(&s_full[bs], ph);
+      mbar_wait(&s_full[x], j & 1);
       tc_fence_after();
-      uint32_t r0[32], r1[32];
-      tmem_ld_32x32b_x32(t_s + lane_off + bs * AT_BN, r0);
-      tmem_ld_32x32b_x32(t_s + lane_off + bs * AT_BN + 32, r1);
-      tmem_ld_wait();
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&s_empty[bs]);
       float mx = -INFINITY;
 #pragma unroll
-      for (int i = 0; i < 32; ++i) mx = fmaxf(mx, fmaxf(__uint_as_float(r0[i]), __uint_as_float(r1[i])));
-      const float m_new = fmaxf(m, mx * sc);
-      const float alpha = (m == -INFINITY) ? 0.f : fast_exp2(m - m_new);
-      float p[64];
-      float rs = 0.f;
-#pragma unroll
-      for (int i = 0; i < 32; ++i) {
-        p[i] = fast_exp2(__uint_as_float(r0[i]) * sc - m_new);
-        p[32 + i] = fast_exp2(__uint_as_float(r1[i]) * sc - m_new);
-      }
-#pragma unroll
-      for (int i = 0; i < 64; ++i) rs += p[i];
-      l = l * alpha + rs;
-      m = m_new;
-      mbar_wait(&p_empty[bs], ph ^ 1);          // PV_{j-2} has finished reading this P slot
-      const uint32_t row_addr = smem_u32(sp + bs * AT_P_BYTES) + row * 128;
-#pragma unroll
-      for (int c = 0; c < 8; ++c) {
-        st_shared_v4(row_addr + ((c ^ (row & 7)) << 4),
-                     pack_bf16x2(p[8 * c + 0], p[8 * c + 1]), pack_bf16x2(p[8 * c + 2], p[8 * c + 3]),
-                     pack_bf16x2(p[8 * c + 4], p[8 * c + 5]), pack_bf16x2(p[8 * c + 6], p[8 * c + 7]));
-      }
-      alpha_s[(j % AT_ALPHA) * AT_BM + row] = alpha;
-      fence_async_shared();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&p_full[bs]);
-    }
-    stat_m[row] = m;
-    stat_l[row] = l;
-    __syncwarp();
-    if (lane == 0) mbar_arrive(stat_full);
-  } else if (warp >= 8) {
-    // ------------------------------------------------------------ correction + epilogue
-    const int q = warp & 3;
-    const int row = q * 32 + (int)lane;
-    const uint32_t lane_off = (uint32_t)(q * 32) << 16;
-    float o[AT_D];
-#pragma unroll
-    for (int i = 0; i < AT_D; ++i) o[i] = 0.f;
-    for (int j = 0; j < nblk; ++j) {
-      const int bs = j & 1;
-      mbar_wait(&pv_full[bs], (j >> 1) & 1);
-      tc_fence_after();
-      const float alpha = alpha_s[(j % AT_ALPHA) * AT_BM + row];
-#pragma unroll
-      for (int c = 0; c < AT_D / 32; ++c) {
+      for (int c = 0; c < 4; ++c) {
         uint32_t r[32];
-        tmem_ld_32x32b_x32(t_o + lane_off + bs * AT_D + c * 32, r);
+        tmem_ld_32x32b_x32(t_s + c * 32, r);
         tmem_ld_wait();
 #pragma unroll
-        for (int i = 0; i < 32; ++i) o[c * 32 + i] = o[c * 32 + i] * alpha + __uint_as_float(r[i]);
+        for (int i = 0; i < 32; ++i) mx = fmaxf(mx, __uint_as_float(r[i]));
       }
+      mx *= sc;
+      const bool grow = mx > m + AT_RESCALE_THRESHOLD;
+      if (j > 0 && __any_sync(0xffffffffu, grow)) {
+        const float alpha = grow ? fast_exp2(m - mx) : 1.f;
+#pragma unroll 1
+        for (int c = 0; c < 4; ++c) {
+          uint32_t o[32];
+          tmem_ld_32x32b_x32(t_o + c * 32, o);
+          tmem_ld_wait();
+#pragma unroll
+          for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
+          tmem_st_32x32b_x32(t_o + c * 32, o);
+        }
+        l *= alpha;
+      }
+      if (grow) m = mx;
+      float rs = 0.f;
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        uint32_t r[32];
+        tmem_ld_32x32b_x32(t_s + c * 32, r);
+        tmem_ld_wait();
+        uint32_t pk[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          const float p0 = fast_exp2(__uint_as_float(r[2 * i]) * sc - m);
+          const float p1 = fast_exp2(__uint_as_float(r[2 * i + 1]) * sc - m);
+          rs += p0 + p1;
+          pk[i] = pack_bf16x2(p0, p1);
+        }
+        tmem_st_32x32b_x16(t_s + c * 16, pk);          // columns [16c, 16c+16): already consumed
+      }
+      l += rs;
+      tmem_st_wait();
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&pv_empty[bs]);
+      if (lane == 0) mbar_arrive(&p_full[x]);
     }
-    mbar_wait(stat_full, 0);
-    float m = stat_m[row], l = stat_l[row];
+    // ------------------------------------------------------------ epilogue
+    mbar_wait(&o_full[x], 0);
+    tc_fence_after();
+    float o[AT_D];
+#pragma unroll
+    for (int c = 0; c < AT_D / 32; ++c) {
+      uint32_t t[32];
+      tmem_ld_32x32b_x32(t_o + c * 32, t);
+      tmem_ld_wait();
+#pragma unroll
+      for (int i = 0; i < 32; ++i) o[c * 32 + i] = __uint_as_float(t[i]);
+    }
     const int sq_idx = qt * AT_BM + row;                     // query index within the local shard
     const long long srow = ((long long)(b * a.H + h) * a.S_q + sq_idx);   // [B, H, S_q] row
     if (!a.first) {
@@ -426,7 +420,7 @@ static int launch_attn(const AttnArgs& a, cudaStream_t st) {
     PK_CUDA(cudaFuncSetAttribute(attn_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, AT_SMEM));
     attr = true;
   }
-  const int grid = a.B * a.H * (a.S_q / AT_BM);
+  const int grid = a.B * a.H * ((a.S_q / AT_BM + 1) / 2);
   attn_fwd_kernel<<<grid, AT_THREADS, AT_SMEM, st>>>(a);
   PK_CUDA(cudaGetLastError());
   return PK_OK;
