@@ -12,9 +12,9 @@ import os as _os
 # wait() could block the queue a peer's signal sits in. Must be set before the
 # CUDA context exists (import this package before touching CUDA).
 _os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
-# Kernels are also force-loaded when a communicator is created (pk_comm.cu,
-# preload_kernels): a lazily loaded first launch can synchronise the context.
-_os.environ.setdefault("CUDA_MODULE_LOADING", "EAGER")
+# (libpk's own kernels are force-loaded when a communicator is created,
+# pk_comm.cu preload_kernels: a lazily loaded first launch can synchronise the
+# context while another emulated rank's wait() spins.)
 
 from .errors import (DeadlockError, LcscError, MemSimError, MulticastReadError,  # noqa: F401
                      PkCudaError, PkError, PrimitiveError, ProtocolViolation, WorkloadError)
