@@ -141,7 +141,8 @@ PK_API int pk_ring_attn_fwd(pk_comm* comm, const pk_tensor* q, const pk_tensor* 
  * expert e lives on rank e % n (workloads.py:802). Tokens are placed on their
  * owner in slots sorted by (src_rank, token, k) (workloads.py:821-832).
  * recv [cap, H] bf16 receives rows; recv_src [cap] int32 (src*T*k + tok*k + j)
- * and *recv_count (device int32) describe them. */
+ * — or [cap, 2] to also receive each row's local expert (expert / n) — and
+ * *recv_count (device int32) describe them. */
 PK_API int pk_moe_dispatch(pk_comm* comm, const pk_tensor* x, const pk_tensor* topk_idx,
                            int num_experts, pk_tensor* recv, pk_tensor* recv_src,
                            pk_tensor* recv_count, void* stream);
@@ -149,6 +150,14 @@ PK_API int pk_moe_dispatch(pk_comm* comm, const pk_tensor* x, const pk_tensor* t
  * sent back and summed with weights w [T, k] f32 into out [T, H] bf16. */
 PK_API int pk_moe_combine(pk_comm* comm, const pk_tensor* y, const pk_tensor* topk_idx,
                           const pk_tensor* w, int num_experts, pk_tensor* out, void* stream);
+
+/* Grouped GEMM (MoE expert GEMM1): y[i] = a[i] . w[g_i]^T for i < *num_rows
+ * (device int32, nullable = all rows); a [R, K] bf16, w [G, N, K] bf16,
+ * y [R, N] bf16; group ids int32 [R] or the [R, 2] recv_src of
+ * pk_moe_dispatch (column 1). Rows of one group are gathered into 256-row
+ * tiles on the device; no host synchronisation. */
+PK_API int pk_grouped_gemm(const pk_tensor* a, const pk_tensor* group_ids, const pk_tensor* w, pk_tensor* y,
+                           const pk_tensor* num_rows, const pk_sched* sched, void* stream);
 
 #ifdef __cplusplus
 }

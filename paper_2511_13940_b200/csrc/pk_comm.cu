@@ -512,6 +512,7 @@ int preload_gemm();
 int preload_allreduce();
 int preload_moe();
 int preload_attn();
+int preload_grouped();
 
 // Load every kernel image up front. With lazy module loading the first launch
 // of a kernel can synchronise the context; in a local group that launch may
@@ -525,6 +526,7 @@ static int preload_kernels() {
     if (s == PK_OK) s = preload_allreduce();
     if (s == PK_OK) s = preload_moe();
     if (s == PK_OK) s = preload_attn();
+    if (s == PK_OK) s = preload_grouped();
     status = s;
   });
   return status;

@@ -33,7 +33,7 @@ constexpr int EPI_COLS = 64;                // epilogue chunk = 64 cols = 128 B 
 constexpr int kNumThreads = 256;
 constexpr int kEpiWarp0 = 4;
 
-enum EpiMode : int { EPI_STORE = 0, EPI_REDUCE_ADD = 1 };
+enum EpiMode : int { EPI_STORE = 0, EPI_REDUCE_ADD = 1, EPI_SCATTER = 2 };
 constexpr int kTileRing = 4;                // depth of the tile-index broadcast ring
 
 // Cross-rank sync state for one fused call (all pointers are device VAs).
@@ -64,6 +64,12 @@ struct GemmArgs {
   int c_ndst;
   int m_rot;                              // tile-order rotation along M (in M tiles)
   int raster_group;                       // tiles per raster group (L2 reuse)
+  // grouped GEMM (MoE experts): M tiles come from a device-built plan
+  const int32_t* num_m_tiles_dev;         // if set: number of valid M tiles (device)
+  const int32_t* tile_group;              // [M tiles] group of each M tile (B rows group*N ..)
+  const int32_t* row_perm;                // [M] destination row of each sorted row (-1 = padding)
+  uint8_t* y;                             // EPI_SCATTER destination [rows, N] bf16
+  long long y_ld;                         // bytes between rows of y
   uint32_t* tile_counter;                 // dynamic tile scheduler (0 at launch; reset by the last fetch)
   int raster_dir;                         // 0: group along M, 1: group along N
   int num_compute_clusters;               // clusters that run GEMM tiles
@@ -156,7 +162,7 @@ lcsc_gemm_kernel(const __grid_constant__ GemmArgs args) {
   const int cluster = (CG == 2) ? (int)cluster_id_x() : (int)blockIdx.x;
   const bool is_comm = cluster >= args.num_compute_clusters;
 
-  const int num_m = args.M / Cfg::TILE_M;
+  const int num_m = args.num_m_tiles_dev ? *args.num_m_tiles_dev : args.M / Cfg::TILE_M;
   const int num_n = args.N / BN;
   const int num_tiles = num_m * num_n;
   const int num_kb = args.K / BLOCK_K;
@@ -315,7 +321,7 @@ lcsc_gemm_kernel(const __grid_constant__ GemmArgs args) {
       const int m_row = mt * Cfg::TILE_M + (int)cta_rank * Cfg::BM;
       const int src = (args.a_nsrc > 1) ? (mt * Cfg::TILE_M) / args.a_rows_per_src : 0;
       const int a_row = args.a_base[src] + m_row - src * args.a_rows_per_src;
-      const int b_row = nt * BN + (int)cta_rank * Cfg::B_ROWS;
+      const int b_row = (args.tile_group ? args.tile_group[mt] * args.N : 0) + nt * BN + (int)cta_rank * Cfg::B_ROWS;
       if (args.a_wait_flag[src]) {
         wait_geq(args.sync.flags + mt, args.sync.epoch, args.sync.err, args.sync.timeout_ns);
         fence_async_global();
@@ -426,6 +432,26 @@ lcsc_gemm_kernel(const __grid_constant__ GemmArgs args) {
             if constexpr (CG == 1) mbar_arrive(&tempty_bar[acc]);
             else mbar_arrive_cluster(&tempty_bar[acc], 0);
           }
+        }
+        if constexpr (EPI == EPI_SCATTER) {
+          // each thread owns one output row: write its 64 columns (128 B) straight
+          // to the row's destination (row_perm), skipping padding rows
+          const int dst_row = args.row_perm[row0 + (int)lane];
+          if (dst_row >= 0) {
+            uint4* dstp = reinterpret_cast<uint4*>(args.y + (long long)dst_row * args.y_ld +
+                                                   (long long)(nt * BN + c * EPI_COLS) * 2);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              const uint32_t* src = (j < 4) ? &v0[j * 8] : &v1[(j - 4) * 8];
+              uint4 w;
+              w.x = pack_bf16x2(__uint_as_float(src[0]), __uint_as_float(src[1]));
+              w.y = pack_bf16x2(__uint_as_float(src[2]), __uint_as_float(src[3]));
+              w.z = pack_bf16x2(__uint_as_float(src[4]), __uint_as_float(src[5]));
+              w.w = pack_bf16x2(__uint_as_float(src[6]), __uint_as_float(src[7]));
+              dstp[j] = w;
+            }
+          }
+          continue;
         }
         // buffer reuse guard: the store that last used this buffer must have read smem
         if (lane == 0) {

@@ -47,7 +47,8 @@ struct MoeArgs {
   int32_t* table_local;         // [n * n] count table (row = src)
   int32_t* table_peer[kMaxRanks];
   uint8_t* recv_peer[kMaxRanks];      // owner recv buffers [cap, H]
-  int32_t* recv_src_peer[kMaxRanks];  // owner recv_src [cap]
+  int32_t* recv_src_peer[kMaxRanks];  // owner recv_src [cap] or [cap, 2] (+ local expert)
+  int recv_src_cols;
   int32_t* recv_count;                // local count output (device int32)
   long long cap;
   // combine
@@ -177,7 +178,10 @@ __global__ void __launch_bounds__(kDispatchThreads) moe_dispatch_kernel(const __
           const long long slot = (long long)base[o] + li;
           if (slot >= a.cap) continue;
           bulk_s2g(a.recv_peer[o] + slot * (long long)a.row_bytes + off, sb, bytes);
-          if (off == 0) a.recv_src_peer[o][slot] = (a.rank * a.T + t) * a.k + j;
+          if (off == 0) {
+            a.recv_src_peer[o][slot * a.recv_src_cols] = (a.rank * a.T + t) * a.k + j;
+            if (a.recv_src_cols == 2) a.recv_src_peer[o][slot * 2 + 1] = a.topk[i] / a.n;   // local expert id
+          }
         }
         bulk_commit();
         buf = (buf + 1) % kDispatchBufs;
@@ -320,18 +324,22 @@ int moe_dispatch(Comm* c, const pk_tensor* x, const pk_tensor* topk, int num_exp
   int64_t cap, H2, rld;
   PK_TRY(check_matrix(recv, "recv", PK_BF16, &cap, &H2, &rld));
   if (H2 != H || rld != H) return fail(PK_ERR_INVALID, "moe_dispatch: recv must be contiguous [cap, %lld]", (long long)H);
-  if (!recv_src || recv_src->dtype != PK_I32 || recv_src->shape[0] < cap)
-    return fail(PK_ERR_INVALID, "moe_dispatch: recv_src must be int32 [cap]");
+  if (!recv_src || recv_src->dtype != PK_I32 || recv_src->shape[0] < cap || recv_src->ndim > 2 ||
+      (recv_src->ndim == 2 && (recv_src->shape[1] != 2 || recv_src->strides[0] != 2)))
+    return fail(PK_ERR_INVALID, "moe_dispatch: recv_src must be int32 [cap] or [cap, 2]");
+  const int src_cols = recv_src->ndim == 2 ? 2 : 1;
   if (!recv_count || recv_count->dtype != PK_I32) return fail(PK_ERR_INVALID, "moe_dispatch: recv_count must be int32");
   void* rp[kMaxRanks];
   void* sp[kMaxRanks];
-  if (!find_symmetric(c, recv->ptr, (size_t)cap * H * 2, rp) || !find_symmetric(c, recv_src->ptr, (size_t)cap * 4, sp))
+  if (!find_symmetric(c, recv->ptr, (size_t)cap * H * 2, rp) ||
+      !find_symmetric(c, recv_src->ptr, (size_t)cap * 4 * src_cols, sp))
     return fail(PK_ERR_INVALID, "moe_dispatch: recv and recv_src must be symmetric (Comm.empty) tensors");
   a.x = static_cast<const uint8_t*>(x->ptr);
   a.x_ld = xld * 2;
   a.row_bytes = (int)(H * 2);
   a.cap = cap;
   a.recv_count = static_cast<int32_t*>(recv_count->ptr);
+  a.recv_src_cols = src_cols;
   for (int r = 0; r < c->world; ++r) {
     a.recv_peer[r] = static_cast<uint8_t*>(rp[r]);
     a.recv_src_peer[r] = static_cast<int32_t*>(sp[r]);

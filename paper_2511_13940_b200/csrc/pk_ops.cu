@@ -73,12 +73,16 @@ int launch_gemm_variant(Variant v, int epi, const GemmArgs& args, int grid_ctas,
   return fail(PK_ERR_INVALID, "no GEMM variant for cta_group=%d am=%d epi=%d", v.cg, v.am, epi);
 }
 
+int launch_gemm_grouped(const GemmArgs& args, int grid_ctas, cudaStream_t st) {
+  return launch_lcsc<2, 256, 1, EPI_SCATTER>(args, grid_ctas, st);
+}
+
 // Force-load every kernel image now (see preload_kernels in pk_comm.cu).
 int preload_gemm() {
   cudaFuncAttributes fa;
 #define PK_L(CG, AM, E) PK_CUDA(cudaFuncGetAttributes(&fa, lcsc_gemm_kernel<CG, 256, AM, E>));
   PK_L(2, 2, EPI_STORE) PK_L(2, 2, EPI_REDUCE_ADD) PK_L(2, 1, EPI_STORE) PK_L(2, 1, EPI_REDUCE_ADD)
-  PK_L(1, 1, EPI_STORE) PK_L(1, 1, EPI_REDUCE_ADD)
+  PK_L(1, 1, EPI_STORE) PK_L(1, 1, EPI_REDUCE_ADD) PK_L(2, 1, EPI_SCATTER)
 #undef PK_L
   return PK_OK;
 }

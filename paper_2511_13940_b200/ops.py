@@ -133,14 +133,15 @@ def moe_dispatch(comm, x: torch.Tensor, topk_idx: torch.Tensor, num_experts: int
     (recv [cap, H] bf16, recv_src [cap] int32, recv_count [1] int32 on device):
     on the owner, slot s holds the token whose (src_rank, token, k) triple is
     the s-th in sorted order (workloads.py:821-832); recv_src[s] =
-    (src_rank * T + token) * k + j. recv/recv_src are symmetric (Comm.empty).
+    (src_rank * T + token) * k + j (recv_src [cap, 2]: column 1 = the row's local
+    expert, expert // n). recv/recv_src are symmetric (Comm.empty).
     """
     _require_cuda(x, topk_idx)
     T, k = topk_idx.shape
     if capacity is None:
         capacity = moe_capacity(T, k, comm.world, x.shape[1])
     if recv is None:
-        recv = (comm.empty((capacity, x.shape[1]), torch.bfloat16), comm.empty((capacity,), torch.int32))
+        recv = (comm.empty((capacity, x.shape[1]), torch.bfloat16), comm.empty((capacity, 2), torch.int32))
     recv_rows, recv_src = recv
     count = torch.empty(1, dtype=torch.int32, device=x.device)
     lib = _lib.load()
@@ -188,3 +189,22 @@ def ring_attention(comm, q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, soft
     check(lib.pk_ring_attn_fwd(comm._h, _lib.ref(dq), _lib.ref(dk), _lib.ref(dv), _lib.ref(do), _lib.ref(dl),
                                ctypes.c_float(softmax_scale), None, ctypes_stream(_stream(stream))), "ring_attention")
     return out, lse
+
+
+def grouped_gemm(a: torch.Tensor, group_ids: torch.Tensor, w: torch.Tensor, out: torch.Tensor | None = None,
+                 num_rows: torch.Tensor | None = None, schedule: dict | None = None, stream=None) -> torch.Tensor:
+    """y[i] = a[i] @ w[group_ids[i]]^T for i < num_rows (device int32; default all rows).
+
+    a [R, K] bf16, w [G, N, K] bf16 (K-major per group), group ids int32 [R]
+    or the [R, 2] recv_src of moe_dispatch. The expert GEMM1 of the MoE path
+    (PAPER.md:445): recv, recv_src, count = moe_dispatch(...);
+    y = grouped_gemm(recv, recv_src, w_local, num_rows=count)."""
+    _require_cuda(a, group_ids, w)
+    if out is None:
+        out = torch.empty((a.shape[0], w.shape[1]), dtype=torch.bfloat16, device=a.device)
+    lib = _lib.load()
+    da, dg, dw, dy = (_lib.tensor_desc(x) for x in (a, group_ids, w, out))
+    dn = _lib.tensor_desc(num_rows) if num_rows is not None else None
+    check(lib.pk_grouped_gemm(_lib.ref(da), _lib.ref(dg), _lib.ref(dw), _lib.ref(dy), _lib.ref(dn),
+                              _lib.ref(_sched(schedule)), ctypes_stream(_stream(stream))), "grouped_gemm")
+    return out

@@ -45,7 +45,7 @@ def test_dispatch_matches_reference_routing(world, seed):
         recv, src, cnt = outs[o]
         assert int(cnt.item()) == counts[o]
         assert np.array_equal(recv[:counts[o]].float().cpu().numpy(), exp[o])
-        ids = src[:counts[o]].cpu().numpy()
+        ids = src[:counts[o], 0].cpu().numpy()
         trip = sorted(t for t, _ in slot_of.items() if owners[t] == o)
         assert [((d * T + tk) * K + j) for (d, tk, j) in trip] == ids.tolist()
     for c in comms:
@@ -84,6 +84,8 @@ def test_combine_inverts_dispatch(world):
 def test_bad_expert_id_is_reported():
     pk = _pk()
     comms = pk.local_group(2)
+    for c in comms:
+        c.set_timeout(0.5)     # rank 0 aborts; rank 1 then times out waiting for it
     x = torch.zeros(8, 64, device="cuda", dtype=torch.bfloat16)
     topk = torch.full((8, 2), 99, device="cuda", dtype=torch.int32)
     good = torch.zeros((8, 2), device="cuda", dtype=torch.int32)
