@@ -33,7 +33,7 @@ constexpr int EPI_COLS = 64;                // epilogue chunk = 64 cols = 128 B 
 constexpr int kNumThreads = 256;
 constexpr int kEpiWarp0 = 4;
 
-enum EpiMode : int { EPI_STORE = 0, EPI_REDUCE_ADD = 1, EPI_SCATTER = 2 };
+enum EpiMode : int { EPI_STORE = 0, EPI_REDUCE_ADD = 1, EPI_SCATTER = 2, EPI_DIRECT = 3 };
 constexpr int kTileRing = 4;                // depth of the tile-index broadcast ring
 
 // Cross-rank sync state for one fused call (all pointers are device VAs).
@@ -433,10 +433,10 @@ lcsc_gemm_kernel(const __grid_constant__ GemmArgs args) {
             else mbar_arrive_cluster(&tempty_bar[acc], 0);
           }
         }
-        if constexpr (EPI == EPI_SCATTER) {
+        if constexpr (EPI == EPI_SCATTER || EPI == EPI_DIRECT) {
           // each thread owns one output row: write its 64 columns (128 B) straight
-          // to the row's destination (row_perm), skipping padding rows
-          const int dst_row = args.row_perm[row0 + (int)lane];
+          // to the row's destination (row_perm for SCATTER), skipping padding rows
+          const int dst_row = (EPI == EPI_SCATTER) ? args.row_perm[row0 + (int)lane] : row0 + (int)lane;
           if (dst_row >= 0) {
             uint4* dstp = reinterpret_cast<uint4*>(args.y + (long long)dst_row * args.y_ld +
                                                    (long long)(nt * BN + c * EPI_COLS) * 2);

@@ -66,7 +66,7 @@ struct Variant { int cg, am; };
 
 int launch_gemm_variant(Variant v, int epi, const GemmArgs& args, int grid_ctas, cudaStream_t st) {
 #define PK_V(CG, AM, E) if (v.cg == CG && v.am == AM && epi == E) return launch_lcsc<CG, 256, AM, E>(args, grid_ctas, st);
-  PK_V(2, 2, EPI_STORE) PK_V(2, 2, EPI_REDUCE_ADD)
+  PK_V(2, 2, EPI_STORE) PK_V(2, 1, EPI_DIRECT)
   PK_V(2, 1, EPI_STORE) PK_V(2, 1, EPI_REDUCE_ADD)
   PK_V(1, 1, EPI_STORE) PK_V(1, 1, EPI_REDUCE_ADD)
 #undef PK_V
@@ -81,7 +81,7 @@ int launch_gemm_grouped(const GemmArgs& args, int grid_ctas, cudaStream_t st) {
 int preload_gemm() {
   cudaFuncAttributes fa;
 #define PK_L(CG, AM, E) PK_CUDA(cudaFuncGetAttributes(&fa, lcsc_gemm_kernel<CG, 256, AM, E>));
-  PK_L(2, 2, EPI_STORE) PK_L(2, 2, EPI_REDUCE_ADD) PK_L(2, 1, EPI_STORE) PK_L(2, 1, EPI_REDUCE_ADD)
+  PK_L(2, 2, EPI_STORE) PK_L(2, 1, EPI_DIRECT) PK_L(2, 1, EPI_STORE) PK_L(2, 1, EPI_REDUCE_ADD)
   PK_L(1, 1, EPI_STORE) PK_L(1, 1, EPI_REDUCE_ADD) PK_L(2, 1, EPI_SCATTER)
 #undef PK_L
   return PK_OK;
@@ -91,11 +91,11 @@ int preload_gemm() {
 //   512-row pair tiles (256 x 256 per CTA, one TMEM accumulator stage) cut
 //   L2->SM traffic by 25% vs 256-row pair tiles; the latter double-buffer
 //   TMEM so the epilogue overlaps the next tile, which wins at small K.
-static Variant pick_variant(int64_t rows_per_part, int64_t K, const pk_sched* sched) {
+static Variant pick_variant(int64_t rows_per_part, int64_t K, const pk_sched* sched, bool reduce = false) {
   int force_am = 0;
   if (const char* e = getenv("PK_GEMM_AM")) force_am = atoi(e);
   if (sched && sched->stages < 0) force_am = -sched->stages;     // test hook: stages = -am
-  if (rows_per_part % 512 == 0 && force_am == 2) return {2, 2};   // opt-in until it measures faster
+  if (!reduce && rows_per_part % 512 == 0 && force_am == 2) return {2, 2};   // opt-in until it measures faster
   if (rows_per_part % 256 == 0) return {2, 1};
   return {1, 1};
 }
@@ -159,7 +159,13 @@ int gemm_local(const pk_tensor* A, const pk_tensor* B, pk_tensor* C, const pk_sc
   int clusters = std::min(tiles, sms / cg);
   if (clusters < 1) clusters = 1;
   args.num_compute_clusters = clusters;
-  return launch_gemm_variant(v, EPI_STORE, args, clusters * cg, st);
+  int epi = EPI_STORE;
+  if (getenv("PK_EPI_DIRECT") && v.cg == 2 && v.am == 1) {   // tuning hook: measured slower than TMA stores
+    epi = EPI_DIRECT;
+    args.y = static_cast<uint8_t*>(C->ptr);
+    args.y_ld = ldC * 2;
+  }
+  return launch_gemm_variant(v, epi, args, clusters * cg, st);
 }
 
 // Fill the cross-rank sync block of one fused call.
@@ -303,7 +309,7 @@ int gemm_rs(Comm* c, const pk_tensor* A, const pk_tensor* B, pk_tensor* O, const
     return fail(PK_ERR_INVALID, "gemm_rs: need (M/n) %% 128 == 0, N %% 256 == 0, K %% 64 == 0 (got %lld, %lld, %lld)",
                 (long long)m_own, (long long)N, (long long)k_loc);
   if (n == 1) return gemm_local(A, B, O, sched, st, c->device);
-  const Variant v = pick_variant(m_own, k_loc, sched);
+  const Variant v = pick_variant(m_own, k_loc, sched, /*reduce=*/true);
   const int cg = v.cg;
   const int tile_m = 128 * v.am * cg;
   // Destination of every rank (zero-copy when `out` is symmetric).
