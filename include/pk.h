@@ -128,6 +128,15 @@ PK_API int pk_ag_gemm(pk_comm* comm, const pk_tensor* a_shard, const pk_tensor* 
 PK_API int pk_gemm_rs(pk_comm* comm, const pk_tensor* a, const pk_tensor* b,
                       pk_tensor* out, const pk_sched* sched, void* stream);
 
+/* Fused GEMM + all-reduce: out[M, N] = sum_d A_d[M, K] . B_d[N, K]^T on every
+ * rank (GemmArPlan inter-SM schedule, workloads.py:517-542).
+ * Each rank's partial tile is stored locally and its owner (tile % n)
+ * signalled; the owner's communicator SMs reduce the tile in place on every
+ * rank (NVLS multimem when `out` has a multicast VA, P2P register ops
+ * otherwise; PK_INTRA_SM forces P2P). */
+PK_API int pk_gemm_ar(pk_comm* comm, const pk_tensor* a, const pk_tensor* b, pk_tensor* out,
+                      const pk_sched* sched, void* stream);
+
 /* In-place all-reduce of x (bf16 or f32, contiguous) over all ranks. */
 PK_API int pk_all_reduce(pk_comm* comm, pk_tensor* x, int op, const pk_sched* sched, void* stream);
 

@@ -19,7 +19,8 @@ _os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
 from .errors import (DeadlockError, LcscError, MemSimError, MulticastReadError,  # noqa: F401
                      PkCudaError, PkError, PrimitiveError, ProtocolViolation, WorkloadError)
 from .comm import Comm, Pgl, local_group  # noqa: F401
-from .ops import (all_gather_gemm, all_reduce, gemm, gemm_reduce_scatter, grouped_gemm, moe_combine,  # noqa: F401
+from .ops import (all_gather_gemm, all_reduce, gemm, gemm_all_reduce, gemm_reduce_scatter, grouped_gemm,  # noqa: F401
+                  moe_combine,
                   moe_dispatch, ring_attention)
 
 __version__ = "0.1.0"

@@ -300,20 +300,40 @@ class GemmArPlan(WorkloadPlan):
         self.check_names = ["acc"]
 
     def run(self, comms, kspec, streams):
+        """INTER_SM: the fused GEMM+AR kernel (partial = input @ I^T, tiles reduced
+        by their owner's communicator SMs). INTRA_SM: the stand-alone all-reduce."""
         from . import ops
-        ts = []
+        n = self.num_devices
+        m, nd = self.inputs[0].shape[2:]
+        if kspec.schedule_mode is ScheduleMode.INTRA_SM:
+            ts = []
+            for r, c in enumerate(comms):           # allocate everything before any rank launches
+                x = c.empty((m, nd), torch.bfloat16)
+                x.copy_(_bf16(self.inputs[r][0, 0]))
+                ts.append(x)
+            torch.cuda.synchronize()
+            for r, c in enumerate(comms):
+                with torch.cuda.stream(streams[r]):
+                    ops.all_reduce(c, ts[r], schedule={"mode": "intra_sm"}, stream=streams[r])
+            torch.cuda.synchronize()
+            for r, x in enumerate(ts):
+                self.pgls["acc"][r][0, 0] = x.float().cpu().numpy()
+            return
+        mp, kp = ((m + 255) // 256) * 256, ((nd + 255) // 256) * 256
+        eye = torch.eye(kp, device="cuda", dtype=torch.bfloat16)
+        ins, outs = [], []
         for r, c in enumerate(comms):           # allocate everything before any rank launches
-            x = c.empty(self.inputs[r].shape[2:], torch.bfloat16)
-            x.copy_(_bf16(self.inputs[r][0, 0]))
-            ts.append(x)
+            a = np.zeros((mp, kp)); a[:m, :nd] = self.inputs[r][0, 0]
+            ins.append(_bf16(a))
+            outs.append(c.empty((mp, kp), torch.bfloat16))
         torch.cuda.synchronize()
-        mode = "intra_sm" if kspec.schedule_mode is ScheduleMode.INTRA_SM else "inter_sm"
+        sched = {"mode": "inter_sm", "num_comm_sms": max(kspec.num_comm_sms, 2)}
         for r, c in enumerate(comms):
             with torch.cuda.stream(streams[r]):
-                ops.all_reduce(c, ts[r], schedule={"mode": mode}, stream=streams[r])
+                ops.gemm_all_reduce(c, ins[r], eye, out=outs[r], schedule=sched, stream=streams[r])
         torch.cuda.synchronize()
-        for r, x in enumerate(ts):
-            self.pgls["acc"][r][0, 0] = x.float().cpu().numpy()
+        for r, o in enumerate(outs):
+            self.pgls["acc"][r][0, 0] = o[:m, :nd].float().cpu().numpy()
 
     def oracle(self):
         total = np.sum(self.inputs, axis=0)

@@ -463,7 +463,7 @@ int pgl_free(Pgl* p) {
 }
 
 int comm_scratch(Comm* c, int slot, size_t bytes, Pgl** out, uint32_t flags) {
-  if (slot < 0 || slot >= 8) return fail(PK_ERR_INVALID, "scratch slot %d", slot);
+  if (slot < 0 || slot >= 12) return fail(PK_ERR_INVALID, "scratch slot %d", slot);
   if ((flags & PK_PGL_MULTICAST) && !c->multicast_supported) flags &= ~PK_PGL_MULTICAST;
   Pgl* cur = c->scratch[slot];
   if (cur && cur->bytes >= bytes && (!(flags & PK_PGL_MULTICAST) || cur->mc)) { *out = cur; return PK_OK; }
@@ -535,7 +535,7 @@ static int preload_kernels() {
 static int comm_finish_init(Comm* c) {
   PK_TRY(preload_kernels());
   PK_TRY(pgl_alloc(c, kSyncBytes, 0, &c->sync));
-  c->max_flags = (int)((kSyncBytes / 4) - kSyncFlags);
+  c->max_flags = kSyncArTiles - kSyncFlags;
   return PK_OK;
 }
 

@@ -75,12 +75,21 @@ struct GemmArgs {
   int num_compute_clusters;               // clusters that run GEMM tiles
   int sync_ready_before_load;             // AG intra-SM: wait ready[s] before loading peer rows
   int sync_ready_before_store;            // RS: wait ready[owner] before the first reduce-add
-  int sync_done_signal;                   // signal done to peers at the end (RS / AG intra)
+  int sync_done_signal;                   // epilogue warps signal done to peers at the end (RS / AG)
+  int sync_done_wait;                     // block 0 waits for done from every rank before exiting
   // communicator (inter-SM all-gather): copy peer shards into a_gathered
   uint8_t* comm_src[kMaxRanksDev];           // shard base of every rank (peer VAs)
   uint8_t* comm_dst;                      // local gathered buffer [M, K]
   long long comm_shard_bytes;             // bytes per shard (= rows_per_src * K * 2)
   int comm_copy_local;                    // also copy the local shard into the gathered buffer
+  // fused GEMM + all-reduce (GemmArPlan inter-SM, workloads.py:517-542)
+  int ar_mode;                            // 1: signal each finished tile's owner; comm CTAs all-reduce owned tiles
+  uint32_t* ar_tile_local;                // [tiles] partial-tile arrivals at this rank (as owner)
+  uint32_t* ar_tile_peer[kMaxRanksDev];   // the same array on every rank
+  uint32_t ar_expect;                     // cumulative arrivals per tile once all partials of this call landed
+  uint8_t* ar_buf_peer[kMaxRanksDev];     // every rank's output buffer [M, N] bf16
+  uint8_t* ar_mc;                         // multicast VA of the output (NVLS) or null
+  long long ar_ld;                        // bytes between output rows
   SyncArgs sync;
 };
 
@@ -237,7 +246,64 @@ lcsc_gemm_kernel(const __grid_constant__ GemmArgs args) {
     return t;
   };
 
-  if (is_comm) {
+  if (is_comm && args.ar_mode) {
+    // ========================================================= communicator: all-reduce
+    // Tiles owned by this rank (tile % world == rank) are split across the
+    // comm CTAs; each waits until every rank's partial of the tile landed, then
+    // reduces it in place on every rank: NVLS multimem.ld_reduce + multimem.st
+    // on the multicast VA, or P2P 16 B loads / fp32 fold in ascending rank
+    // order / 16 B stores (primitives.py:187-195, 237-261).
+    const int ncomm = (int)(gridDim.x / CG) - args.num_compute_clusters;
+    const int me = (cluster - args.num_compute_clusters) * CG + (int)cta_rank;
+    const int comm_ctas = ncomm * CG;
+    const int vec_per_row = BN * 2 / 16;                       // 16 B vectors per tile row
+    const int vecs = Cfg::TILE_M * vec_per_row;
+    __shared__ int ok_s;
+    int j = 0;
+    for (int t = args.rank; t < num_m * num_n; t += args.world, ++j) {
+      if (j % comm_ctas != me) continue;
+      if (threadIdx.x == 0) {
+        ok_s = wait_geq(args.ar_tile_local + t, args.ar_expect, args.sync.err, args.sync.timeout_ns) ? 1 : 0;
+        fence_async_global();
+      }
+      __syncthreads();
+      if (!ok_s) break;
+      const long long base = (long long)(t / num_n) * Cfg::TILE_M * args.ar_ld + (long long)(t % num_n) * BN * 2;
+      for (int v = threadIdx.x; v < vecs; v += blockDim.x) {
+        const long long off = base + (long long)(v / vec_per_row) * args.ar_ld + (v % vec_per_row) * 16;
+        if (args.ar_mc != nullptr) {
+          uint32_t r[4];
+          mm_ld_reduce_bf16x8(args.ar_mc + off, r);
+          mm_st_v4(args.ar_mc + off, r);
+        } else {
+          float acc[8];
+#pragma unroll
+          for (int e = 0; e < 8; ++e) acc[e] = 0.f;
+          for (int d = 0; d < args.world; ++d) {
+            const uint4 x = ld_v4_volatile(args.ar_buf_peer[d] + off);
+            const uint32_t w[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              acc[2 * e] += __uint_as_float(w[e] << 16);
+              acc[2 * e + 1] += __uint_as_float(w[e] & 0xFFFF0000u);
+            }
+          }
+          uint4 o;
+          o.x = pack_bf16x2(acc[0], acc[1]);
+          o.y = pack_bf16x2(acc[2], acc[3]);
+          o.z = pack_bf16x2(acc[4], acc[5]);
+          o.w = pack_bf16x2(acc[6], acc[7]);
+          for (int d = 0; d < args.world; ++d) st_v4(args.ar_buf_peer[d] + off, o);
+        }
+      }
+      __syncthreads();
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence_system();
+      for (int d = 0; d < args.world; ++d) signal_add(args.sync.done_peer[d] + args.rank, 1u);
+    }
+  } else if (is_comm) {
     // ========================================================= communicator
     // Inter-SM all-gather: copy every shard (peer VA -> smem ring -> local
     // gathered buffer) in TILE_M-row chunks and publish flags[m_tile] per
@@ -479,6 +545,17 @@ lcsc_gemm_kernel(const __grid_constant__ GemmArgs args) {
         }
         if constexpr (Cfg::EPI_NBUF == 2) ebuf_idx ^= 1;
       }
+      if (args.ar_mode) {
+        // this warp's slice of the partial tile is in HBM: tell the tile's owner
+        if (lane == 0) {
+          bulk_wait<0>();
+          fence_async_global();
+          __threadfence_system();
+          const int tile_id = mt * num_n + nt;
+          signal_add(args.ar_tile_peer[tile_id % args.world] + tile_id, 1u);
+        }
+        __syncwarp();
+      }
     }
     if (lane == 0) bulk_wait<0>();
     __syncwarp();
@@ -500,7 +577,7 @@ lcsc_gemm_kernel(const __grid_constant__ GemmArgs args) {
   }
   // Completion wait: block 0 waits until every rank has finished touching this
   // rank's buffers, so the caller may reuse them once the kernel returns.
-  if (args.sync_done_signal && blockIdx.x == 0 && threadIdx.x == 0) {
+  if (args.sync_done_wait && blockIdx.x == 0 && threadIdx.x == 0) {
     for (int s = 0; s < args.world; ++s)
       wait_geq(args.sync.done_local + s, args.sync.done_expect, args.sync.err, args.sync.timeout_ns);
   }

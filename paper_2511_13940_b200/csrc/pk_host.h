@@ -118,9 +118,10 @@ struct Comm {
   uint32_t epoch = 0;
   uint32_t ready_count = 0;          // cumulative ready signals expected per src
   uint32_t done_count = 0;           // cumulative done signals expected per src
+  uint32_t gemm_ar_calls = 0;        // fused GEMM+AR calls so far (per-tile arrival counters)
   int max_flags = 0;
   // scratch (symmetric) buffers, grown on demand
-  Pgl* scratch[8] = {};
+  Pgl* scratch[12] = {};
   // rendezvous socket (multi-process)
   int listen_fd = -1;
   uint32_t seq = 0;                  // collective sequence number (message tag)
@@ -136,7 +137,7 @@ struct Comm {
 bool find_symmetric(Comm* c, const void* ptr, size_t bytes, void** peers);
 
 // Word offsets inside the per-comm sync PGL.
-enum { kSyncReady = 0, kSyncDone = 8, kSyncErr = 16, kSyncFlags = 32, kSyncBytes = 1 << 20 };
+enum { kSyncReady = 0, kSyncDone = 8, kSyncErr = 16, kSyncFlags = 32, kSyncArTiles = 32 + 65536, kSyncBytes = 1 << 20 };
 
 // Exchange `len` bytes from every rank (allgather) — multi-process through
 // the Unix-socket rendezvous; local groups copy in-process.

@@ -280,6 +280,7 @@ int ag_gemm(Comm* c, const pk_tensor* A, const pk_tensor* B, pk_tensor* C, pk_te
   int compute_clusters = std::min(tiles, clusters_total - comm_clusters);
   args.num_compute_clusters = compute_clusters;
   args.sync_done_signal = 1;
+  args.sync_done_wait = 1;
   c->epoch += 1;
   c->ready_count += 1;
   c->done_count += (uint32_t)(compute_clusters * cg * 4 * v.am);
@@ -340,6 +341,7 @@ int gemm_rs(Comm* c, const pk_tensor* A, const pk_tensor* B, pk_tensor* O, const
   args.num_compute_clusters = compute_clusters;
   args.sync_ready_before_store = 1;
   args.sync_done_signal = 1;
+  args.sync_done_wait = 1;
   c->epoch += 1;
   c->ready_count += 1;
   c->done_count += (uint32_t)(compute_clusters * cg * 4 * v.am);
@@ -350,9 +352,93 @@ int gemm_rs(Comm* c, const pk_tensor* A, const pk_tensor* B, pk_tensor* O, const
   return PK_OK;
 }
 
+int gemm_ar(Comm* c, const pk_tensor* A, const pk_tensor* B, pk_tensor* O, const pk_sched* sched, cudaStream_t st) {
+  int64_t M, K, ldA, N, Kb, ldB, Mo, No, ldO;
+  PK_TRY(check_matrix(A, "a", PK_BF16, &M, &K, &ldA));
+  PK_TRY(check_matrix(B, "b", PK_BF16, &N, &Kb, &ldB));
+  PK_TRY(check_matrix(O, "out", PK_BF16, &Mo, &No, &ldO));
+  const int n = c->world;
+  if (Kb != K) return fail(PK_ERR_INVALID, "gemm_ar: K mismatch (a %lld, b %lld)", (long long)K, (long long)Kb);
+  if (Mo != M || No != N) return fail(PK_ERR_INVALID, "gemm_ar: out must be [%lld, %lld]", (long long)M, (long long)N);
+  if (M % 256 || N % 256 || K % BLOCK_K || K == 0)   // workloads.py:445-447 (extent divisibility)
+    return fail(PK_ERR_INVALID, "gemm_ar: need M %% 256 == 0, N %% 256 == 0, K %% 64 == 0 (got %lld, %lld, %lld)",
+                (long long)M, (long long)N, (long long)K);
+  if (n == 1) return gemm_local(A, B, O, sched, st, c->device);
+  const Variant v{2, 1};
+  const int tile_m = 256;
+  const int tiles = (int)((M / tile_m) * (N / 256));
+  if (tiles > (kSyncBytes / 4) - kSyncArTiles) return fail(PK_ERR_INVALID, "gemm_ar: too many tiles");
+  // Output of every rank (zero-copy when `out` is symmetric; NVLS when it has a multicast VA).
+  void* dst[kMaxRanks];
+  void* mc = nullptr;
+  const size_t out_bytes = (size_t)M * N * 2;
+  bool staged = false;
+  Pgl* owner = nullptr;
+  if (ldO == N) {
+    for (Pgl* p : c->user_pgls) {
+      const uintptr_t a = (uintptr_t)O->ptr, b = (uintptr_t)p->local;
+      if (a >= b && a + out_bytes <= b + p->bytes) { owner = p; break; }
+    }
+  }
+  if (owner) {
+    const size_t off = (uintptr_t)O->ptr - (uintptr_t)owner->local;
+    for (int r = 0; r < n; ++r) dst[r] = (char*)owner->peers[r] + off;
+    if (owner->mc) mc = (char*)owner->mc + off;
+  } else {
+    Pgl* s8;
+    PK_TRY(comm_scratch(c, 8, out_bytes, &s8, PK_PGL_MULTICAST));
+    for (int r = 0; r < n; ++r) dst[r] = s8->peers[r];
+    mc = s8->mc;
+    staged = true;
+  }
+  if (sched && sched->mode == PK_INTRA_SM) mc = nullptr;   // force the P2P register-op path
+  GemmArgs args;
+  init_args(args);
+  args.M = (int)M; args.N = (int)N; args.K = (int)K;
+  args.rank = c->rank; args.world = n;
+  args.a_rows_per_src = (int)M;
+  args.c_rows_per_dst = (int)M;
+  PK_TRY(tmap_a(&args.tmap_a[0], A->ptr, M, K, ldA, 1));
+  PK_TRY(tmap_b(&args.tmap_b, B->ptr, N, K, ldB, 2));
+  PK_TRY(tmap_c(&args.tmap_c[0], dst[c->rank], M, N, N));
+  const int clusters_total = std::max(2, (sched && sched->num_sms > 0 ? std::min(sched->num_sms, c->num_sms) : c->num_sms) / 2);
+  const int comm_sms = (sched && sched->num_comm_sms > 0) ? sched->num_comm_sms : 16;   // GemmArPlan default (workloads.py:425-426)
+  int comm_clusters = std::max(1, comm_sms / 2);
+  if (c->local_group) comm_clusters = std::min(comm_clusters, std::max(1, clusters_total / 4));
+  if (comm_clusters >= clusters_total) return fail(PK_ERR_INVALID, "gemm_ar: num_comm_sms leaves no compute SMs");
+  const int compute_clusters = std::min(tiles, clusters_total - comm_clusters);
+  args.num_compute_clusters = compute_clusters;
+  uint32_t* local = static_cast<uint32_t*>(c->sync->local);
+  args.ar_mode = 1;
+  args.ar_tile_local = local + kSyncArTiles;
+  for (int r = 0; r < n; ++r) {
+    args.ar_tile_peer[r] = static_cast<uint32_t*>(c->sync->peers[r]) + kSyncArTiles;
+    args.ar_buf_peer[r] = static_cast<uint8_t*>(dst[r]);
+  }
+  args.ar_mc = static_cast<uint8_t*>(mc);
+  args.ar_ld = N * 2;
+  c->gemm_ar_calls += 1;
+  args.ar_expect = c->gemm_ar_calls * (uint32_t)(n * 4 * 2);     // every rank's 4 epilogue warps x 2 CTAs per tile
+  args.sync_done_wait = 1;                                         // block 0 waits for every rank's comm CTAs
+  c->epoch += 1;
+  c->done_count += (uint32_t)(comm_clusters * 2);
+  fill_sync(c, args.sync);
+  args.sync.ready_local = nullptr;                                 // no ready handshake: tiles are flagged
+  PK_TRY(launch_gemm_variant(v, EPI_STORE, args, (compute_clusters + comm_clusters) * 2, st));
+  if (staged)
+    PK_CUDA(cudaMemcpy2DAsync(O->ptr, ldO * 2, dst[c->rank], N * 2, N * 2, M, cudaMemcpyDeviceToDevice, st));
+  return PK_OK;
+}
+
 }  // namespace pk
 
 extern "C" {
+
+PK_API int pk_gemm_ar(pk_comm* comm, const pk_tensor* a, const pk_tensor* b, pk_tensor* out,
+                      const pk_sched* sched, void* stream) {
+  if (!comm) return pk::fail(PK_ERR_INVALID, "null comm");
+  return pk::gemm_ar(comm, a, b, out, sched, (cudaStream_t)stream);
+}
 
 PK_API int pk_gemm(const pk_tensor* a, const pk_tensor* b, pk_tensor* c, const pk_sched* sched, void* stream) {
   int dev = 0;

@@ -96,6 +96,22 @@ def gemm_reduce_scatter(comm, a: torch.Tensor, b: torch.Tensor, out: torch.Tenso
     return out
 
 
+def gemm_all_reduce(comm, a: torch.Tensor, b: torch.Tensor, out: torch.Tensor | None = None,
+                    schedule: dict | None = None, stream=None) -> torch.Tensor:
+    """Fused GEMM + all-reduce: out = sum_d A_d @ B_d^T on every rank (GemmArPlan,
+    workloads.py:415-546). Tiles are reduced by the owner's
+    communicator SMs as soon as all partials landed (NVLS when `out` is a
+    multicast symmetric tensor, P2P otherwise)."""
+    _require_cuda(a, b)
+    if out is None:
+        out = comm.empty((a.shape[0], b.shape[0]), torch.bfloat16, multicast=comm.has_multicast)
+    lib = _lib.load()
+    da, db, do = _lib.tensor_desc(a), _lib.tensor_desc(b), _lib.tensor_desc(out)
+    check(lib.pk_gemm_ar(comm._h, _lib.ref(da), _lib.ref(db), _lib.ref(do), _lib.ref(_sched(schedule)),
+                         ctypes_stream(_stream(stream))), "gemm_all_reduce")
+    return out
+
+
 _REDUCE_OPS = {"sum": 0, "max": 1, "min": 2}   # primitives.py:24-28
 
 
