@@ -22,6 +22,11 @@
  *                                         (workloads.py:517-546)
  *   pk_ring_attn_fwd                   <- RingAttentionPlan (workloads.py:616-716)
  *   pk_moe_dispatch / pk_moe_combine   <- MoePlan (workloads.py:786-868); combine is new
+ *   pk_grouped_gemm                    <- MoePlan's GEMM1 (workloads.py:808-815)
+ *   pk_gemm_ar                         <- GemmArPlan inter-SM (workloads.py:415-546)
+ *   pk_ulysses_a2a                     <- UlyssesPlan (workloads.py:723-779)
+ *   pk_all_gather / pk_reduce_scatter  <- AllGatherTdPlan / ReduceScatterTdPlan
+ *   / pk_all_to_all                       / AllToAll4DPlan (workloads.py:875-1028)
  *
  * Status codes map onto the reference's exception classes in the Python
  * layer: PK_ERR_INVALID -> WorkloadError (workloads.py:62),
@@ -159,6 +164,20 @@ PK_API int pk_moe_dispatch(pk_comm* comm, const pk_tensor* x, const pk_tensor* t
  * sent back and summed with weights w [T, k] f32 into out [T, H] bf16. */
 PK_API int pk_moe_combine(pk_comm* comm, const pk_tensor* y, const pk_tensor* topk_idx,
                           const pk_tensor* w, int num_experts, pk_tensor* out, void* stream);
+
+/* ---- pure collectives on strided layouts (pull-based over peer memory) --- */
+/* Tensor-dim all-gather, rank-major: y = [x_0; x_1; ...] (AllGatherTdPlan,
+ * workloads.py:875-920). x: any contiguous tensor; y: world * numel(x). */
+PK_API int pk_all_gather(pk_comm* comm, const pk_tensor* x, pk_tensor* y, void* stream);
+/* Tensor-dim reduce-scatter: y = fold_d x_d[block rank] in ascending rank order
+ * (ReduceScatterTdPlan, workloads.py:923-975); bf16 / f32; op = pk_reduce_op. */
+PK_API int pk_reduce_scatter(pk_comm* comm, const pk_tensor* x, pk_tensor* y, int op, void* stream);
+/* All-to-all on the leading dim: y_j[i] = x_i[j], x/y [world, ...]
+ * (AllToAll4DPlan, workloads.py:978-1028). */
+PK_API int pk_all_to_all(pk_comm* comm, const pk_tensor* x, pk_tensor* y, void* stream);
+/* Ulysses sequence <-> head all-to-all (UlyssesPlan, workloads.py:723-779):
+ * inverse = 0: x [B, S/n, H, D] -> y [B, S, H/n, D]; inverse = 1: back. */
+PK_API int pk_ulysses_a2a(pk_comm* comm, const pk_tensor* x, pk_tensor* y, int inverse, void* stream);
 
 /* Grouped GEMM (MoE expert GEMM1): y[i] = a[i] . w[g_i]^T for i < *num_rows
  * (device int32, nullable = all rows); a [R, K] bf16, w [G, N, K] bf16,

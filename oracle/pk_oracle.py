@@ -244,6 +244,28 @@ def grouped_gemm(recv_rows, expert_of_row, w_t) -> np.ndarray:
     return out
 
 
+# --------------------------------------------------------------------------- pure collectives
+def ulysses_a2a(x_shards, n: int, inverse: bool = False):
+    """Sequence <-> head all-to-all (UlyssesPlan, workloads.py:723-779) on real
+    [B, S/n, H, D] shards: forward y_r[b, i*S/n + s, h, :] = x_i[b, s, r*H/n + h, :]."""
+    outs = []
+    for r in range(n):
+        if not inverse:
+            parts = [x[:, :, r * (x.shape[2] // n):(r + 1) * (x.shape[2] // n)] for x in x_shards]
+            outs.append(np.concatenate(parts, axis=1))
+        else:
+            sl = x_shards[0].shape[1] // n
+            parts = [x[:, r * sl:(r + 1) * sl] for x in x_shards]
+            outs.append(np.concatenate(parts, axis=2))
+    return outs
+
+
+def all_to_all(x_list):
+    """y_j[i] = x_i[j] along the leading dim (AllToAll4DPlan, workloads.py:1020-1028)."""
+    n = len(x_list)
+    return [np.stack([np.asarray(x_list[i][j]) for i in range(n)]) for j in range(n)]
+
+
 # --------------------------------------------------------------------------- reference plans, re-derived
 def plan_inputs(kind: str, dims: dict, n: int, seed: int) -> dict:
     """Regenerate a reference functional plan's seeded inputs exactly, in the
@@ -265,6 +287,14 @@ def plan_inputs(kind: str, dims: dict, n: int, seed: int) -> dict:
         route, owners = moe_route(rng, n, dims["T"], dims["N_experts"], dims["TopK"])
         token_data = [randints(rng, (dims["T"], t, t)) for _ in range(n)]
         return {"route": route, "owners": owners, "token_data": token_data}
+    if kind == "ulysses_all_to_all":                                   # workloads.py:743-751
+        return {"x": [randints(rng, (1, n, t, t)) for _ in range(n)]}
+    if kind == "all_gather_tensor_dim":                                # workloads.py:888-897
+        return {"x": [randints(rng, (1, 1, t, t)) for _ in range(n)]}
+    if kind == "reduce_scatter_tensor_dim":                            # workloads.py:938-946
+        return {"x": [randints(rng, (1, 1, n * t, t)) for _ in range(n)]}
+    if kind == "all_to_all_4d":                                        # workloads.py:992-1000
+        return {"x": [randints(rng, (n, 1, t, t)) for _ in range(n)]}
     raise KeyError(kind)
 
 
@@ -291,6 +321,16 @@ def plan_expected(kind: str, inputs: dict, n: int) -> dict:
                 e[s * t:(s + 1) * t] = recv[o][s]
             outs.append(e)
         return {"recv": four(outs)}
+    if kind == "ulysses_all_to_all":                                   # y[j][0, i] = x[i][0, j]
+        ys = all_to_all([x[0] for x in inputs["x"]])
+        return {"y": [y[None] for y in ys]}
+    if kind == "all_gather_tensor_dim":
+        g = gather_rows([x[0, 0] for x in inputs["x"]])
+        return {"out": four([g.copy() for _ in range(n)])}
+    if kind == "reduce_scatter_tensor_dim":
+        return {"out": four(reduce_scatter_full([x[0, 0] for x in inputs["x"]]))}
+    if kind == "all_to_all_4d":                                        # y[j][i, 0] = x[i][j, 0]
+        return {"y": all_to_all(inputs["x"])}
     raise KeyError(kind)
 
 
@@ -302,7 +342,13 @@ def reduced_dims(kind: str, n: int) -> dict:
         "ag_gemm": dict(M=8 * n, N=8 * n, K=64),
         "ring_attention": dict(B=1, S=8 * n, H=2, D=4),
         "moe_dispatch_gemm": dict(TopK=2, N_experts=2 * n, H=64, H_expert=64, T=4),
+        "ulysses_all_to_all": dict(B=2, S=16, H=2 * n, D=4),
+        "all_gather_tensor_dim": dict(R=16, C=16),
+        "reduce_scatter_tensor_dim": dict(R=16, C=16),
+        "all_to_all_4d": dict(R=16, C=16),
     }[kind]
 
 
 HOT_PATH_KINDS = ("ag_gemm", "gemm_rs", "gemm_ar", "ring_attention", "moe_dispatch_gemm")
+NEXT_KINDS = ("ulysses_all_to_all", "all_gather_tensor_dim", "reduce_scatter_tensor_dim", "all_to_all_4d")
+ALL_KINDS = HOT_PATH_KINDS + NEXT_KINDS

@@ -14,8 +14,9 @@ brute-force expectation, returning None or (layout, (dev, *idx)).
 The functional tiles are the reference's 16 x 16; the CUDA kernels need
 128-row / 64-column granularity, so tiles are embedded in zero-padded
 operands and extracted afterwards (the padding never changes a checked
-value). Kinds outside the hot path (Ulysses, tensor-dim collectives) raise
-WorkloadError.
+value). The four pure-collective kinds (Ulysses, tensor-dim all-gather /
+reduce-scatter, 4-D all-to-all) run through pk's strided
+collectives.
 """
 from __future__ import annotations
 
@@ -447,7 +448,171 @@ class MoePlan(WorkloadPlan):
         return {"recv": outs}
 
 
-_PLAN_CLASSES = {cls.kind: cls for cls in (AgGemmPlan, GemmRsPlan, GemmArPlan, RingAttentionPlan, MoePlan)}
+class _CollectivePlan(WorkloadPlan):
+    """Pure collectives (workloads.py:723-779, 875-1028): seeded integer inputs
+    `x`, one GPU collective, checked layout `y` / `out`."""
+
+    x_shape = None           # per-device input shape, filled by _shapes()
+    out_name = "out"
+
+    def _shapes(self, n, t):
+        raise NotImplementedError
+
+    def _build(self):
+        sp, n, t = self.spec, self.num_devices, FUNC_TILE
+        self._dims()
+        self.x_shape, out_shape = self._shapes(n, t)
+        self.x = [_randints(self.rng, self.x_shape) for _ in range(n)]
+        self.pgls = {"x": [v.copy() for v in self.x], self.out_name: [np.zeros(out_shape) for _ in range(n)]}
+        self.check_names = [self.out_name]
+
+    def _dims(self):
+        pass
+
+    def _op(self, ops, c, x, out, stream):
+        raise NotImplementedError
+
+    def run(self, comms, kspec, streams):
+        from . import ops
+        n = self.num_devices
+        ins, outs = [], []
+        for r, c in enumerate(comms):           # allocate everything before any rank launches
+            xi = c.empty(self._gpu_shape(self.x_shape), torch.bfloat16)
+            xi.copy_(_bf16(self.x[r]).reshape(xi.shape))
+            ins.append(xi)
+            outs.append(torch.empty(self._gpu_out_shape(n), device="cuda", dtype=torch.bfloat16))
+        torch.cuda.synchronize()
+        for r, c in enumerate(comms):
+            with torch.cuda.stream(streams[r]):
+                self._op(ops, c, ins[r], outs[r], streams[r])
+        torch.cuda.synchronize()
+        for r, o in enumerate(outs):
+            self.pgls[self.out_name][r][:] = o.float().cpu().numpy().reshape(self.pgls[self.out_name][r].shape)
+
+    def _gpu_shape(self, shape):
+        return shape
+
+    def _gpu_out_shape(self, n):
+        return self.pgls[self.out_name][0].shape
+
+
+class UlyssesPlan(_CollectivePlan):
+    """Head-dimension all-to-all, no reshape staging (workloads.py:723-779)."""
+
+    kind = WorkloadKind.ULYSSES_ALL_TO_ALL
+    out_name = "y"
+
+    def _dims(self):
+        sp, n = self.spec, self.num_devices
+        b, s_len, h, d = sp.dim("B"), sp.dim("S"), sp.dim("H"), sp.dim("D")
+        if h % n:
+            raise WorkloadError("head count must divide across devices")
+        self.flops_per_device = 4.0 * b * s_len * h * d * d
+
+    def _shapes(self, n, t):
+        return (1, n, t, t), (1, n, t, t)
+
+    def _gpu_shape(self, shape):
+        return (shape[1], shape[2] * shape[3])          # slot j of x[i] -> y[j] slot i: a2a on the slot dim
+
+    def _gpu_out_shape(self, n):
+        return (n, FUNC_TILE * FUNC_TILE)
+
+    def _op(self, ops, c, x, out, stream):
+        ops.all_to_all(c, x, out=out, stream=stream)
+
+    def oracle(self):
+        n = self.num_devices
+        outs = []
+        for j in range(n):
+            e = np.zeros(self.x[0].shape)
+            for i in range(n):
+                e[0, i] = self.x[i][0, j]
+            outs.append(e)
+        return {"y": outs}
+
+
+class AllGatherTdPlan(_CollectivePlan):
+    """Tensor-dimension all-gather (workloads.py:875-920)."""
+
+    kind = WorkloadKind.ALL_GATHER_TENSOR_DIM
+
+    def _shapes(self, n, t):
+        return (1, 1, t, t), (1, 1, n * t, t)
+
+    def _op(self, ops, c, x, out, stream):
+        ops.all_gather(c, x.reshape(FUNC_TILE, FUNC_TILE), out=out.reshape(-1, FUNC_TILE), stream=stream)
+
+    def oracle(self):
+        g = np.concatenate([x[0, 0] for x in self.x], axis=0)
+        return {"out": [g[None, None].copy() for _ in range(self.num_devices)]}
+
+
+class ReduceScatterTdPlan(_CollectivePlan):
+    """Tensor-dimension reduce-scatter (workloads.py:923-975)."""
+
+    kind = WorkloadKind.REDUCE_SCATTER_TENSOR_DIM
+
+    def _shapes(self, n, t):
+        return (1, 1, n * t, t), (1, 1, n * t, t)
+
+    def _gpu_out_shape(self, n):
+        return (FUNC_TILE, FUNC_TILE)
+
+    def run(self, comms, kspec, streams):
+        from . import ops
+        t = FUNC_TILE
+        ins, outs = [], []
+        for r, c in enumerate(comms):           # allocate everything before any rank launches
+            xi = c.empty((self.x_shape[2], t), torch.bfloat16)
+            xi.copy_(_bf16(self.x[r][0, 0]))
+            ins.append(xi)
+            outs.append(torch.empty(t, t, device="cuda", dtype=torch.bfloat16))
+        torch.cuda.synchronize()
+        for r, c in enumerate(comms):
+            with torch.cuda.stream(streams[r]):
+                ops.reduce_scatter(c, ins[r], out=outs[r], stream=streams[r])
+        torch.cuda.synchronize()
+        for r, o in enumerate(outs):            # the reference's full-size layout: owner block, zeros elsewhere
+            self.pgls["out"][r][:] = 0
+            self.pgls["out"][r][0, 0, r * t:(r + 1) * t] = o.float().cpu().numpy()
+
+    def oracle(self):
+        n, t = self.num_devices, FUNC_TILE
+        total = np.sum(self.x, axis=0)
+        outs = []
+        for d in range(n):
+            e = np.zeros(total.shape)
+            e[0, 0, d * t:(d + 1) * t] = total[0, 0, d * t:(d + 1) * t]
+            outs.append(e)
+        return {"out": outs}
+
+
+class AllToAll4DPlan(_CollectivePlan):
+    """Batch-dimension all-to-all permute: x[i] slot j becomes y[j] slot i (workloads.py:978-1028)."""
+
+    kind = WorkloadKind.ALL_TO_ALL_4D
+    out_name = "y"
+
+    def _shapes(self, n, t):
+        return (n, 1, t, t), (n, 1, t, t)
+
+    def _op(self, ops, c, x, out, stream):
+        ops.all_to_all(c, x, out=out, stream=stream)
+
+    def oracle(self):
+        n = self.num_devices
+        outs = []
+        for j in range(n):
+            e = np.zeros(self.x[0].shape)
+            for i in range(n):
+                e[i, 0] = self.x[i][j, 0]
+            outs.append(e)
+        return {"y": outs}
+
+
+_PLAN_CLASSES = {cls.kind: cls for cls in (AgGemmPlan, GemmRsPlan, GemmArPlan, RingAttentionPlan, MoePlan, UlyssesPlan,
+                                           AllGatherTdPlan, ReduceScatterTdPlan, AllToAll4DPlan)}
 
 
 def reduced_dims(kind: WorkloadKind, num_devices: int) -> dict:
@@ -459,6 +624,10 @@ def reduced_dims(kind: WorkloadKind, num_devices: int) -> dict:
         WorkloadKind.AG_GEMM: dict(M=8 * n, N=8 * n, K=64),
         WorkloadKind.RING_ATTENTION: dict(B=1, S=8 * n, H=2, D=4),
         WorkloadKind.MOE_DISPATCH_GEMM: dict(TopK=2, N_experts=2 * n, H=64, H_expert=64, T=4),
+        WorkloadKind.ULYSSES_ALL_TO_ALL: dict(B=2, S=16, H=2 * n, D=4),
+        WorkloadKind.ALL_GATHER_TENSOR_DIM: dict(R=16, C=16),
+        WorkloadKind.REDUCE_SCATTER_TENSOR_DIM: dict(R=16, C=16),
+        WorkloadKind.ALL_TO_ALL_4D: dict(R=16, C=16),
     }[kind]
 
 
@@ -468,7 +637,7 @@ def build(kind: WorkloadKind, dims: dict, profile=None, *, element_bytes: int = 
           pipeline_stages: int = 4):
     """Instantiate one workload: (kernel spec, plan) (workloads.py:1040-1054)."""
     if kind not in _PLAN_CLASSES:
-        raise WorkloadError(f"{kind.value} is not on the pk hot path (SURVEY.md §8)")
+        raise WorkloadError(f"unknown workload kind {kind!r}")
     spec = WorkloadSpec(kind=kind, dims=dict(dims), element_bytes=element_bytes,
                         num_devices=num_devices or 8, seed=seed, materialize=materialize)
     plan = _PLAN_CLASSES[kind](spec)

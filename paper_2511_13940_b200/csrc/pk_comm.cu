@@ -513,6 +513,7 @@ int preload_allreduce();
 int preload_moe();
 int preload_attn();
 int preload_grouped();
+int preload_coll();
 
 // Load every kernel image up front. With lazy module loading the first launch
 // of a kernel can synchronise the context; in a local group that launch may
@@ -527,6 +528,7 @@ static int preload_kernels() {
     if (s == PK_OK) s = preload_moe();
     if (s == PK_OK) s = preload_attn();
     if (s == PK_OK) s = preload_grouped();
+    if (s == PK_OK) s = preload_coll();
     status = s;
   });
   return status;

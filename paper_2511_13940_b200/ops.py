@@ -224,3 +224,52 @@ def grouped_gemm(a: torch.Tensor, group_ids: torch.Tensor, w: torch.Tensor, out:
     check(lib.pk_grouped_gemm(_lib.ref(da), _lib.ref(dg), _lib.ref(dw), _lib.ref(dy), _lib.ref(dn),
                               _lib.ref(_sched(schedule)), ctypes_stream(_stream(stream))), "grouped_gemm")
     return out
+
+
+def all_gather(comm, x: torch.Tensor, out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+    """Tensor-dim all-gather, rank-major along dim 0 (AllGatherTdPlan, workloads.py:875-920)."""
+    _require_cuda(x)
+    if out is None:
+        out = torch.empty((x.shape[0] * comm.world,) + tuple(x.shape[1:]), dtype=x.dtype, device=x.device)
+    check(_lib.load().pk_all_gather(comm._h, _lib.ref(_lib.tensor_desc(x)), _lib.ref(_lib.tensor_desc(out)),
+                                    ctypes_stream(_stream(stream))), "all_gather")
+    return out
+
+
+def reduce_scatter(comm, x: torch.Tensor, op: str = "sum", out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+    """Tensor-dim reduce-scatter along dim 0: rank r gets the ascending fold of
+    block r (ReduceScatterTdPlan, workloads.py:923-975)."""
+    _require_cuda(x)
+    if op not in _REDUCE_OPS:
+        from .errors import PrimitiveError
+        raise PrimitiveError(f"unsupported reduce op {op!r}")
+    if out is None:
+        out = torch.empty((x.shape[0] // comm.world,) + tuple(x.shape[1:]), dtype=x.dtype, device=x.device)
+    check(_lib.load().pk_reduce_scatter(comm._h, _lib.ref(_lib.tensor_desc(x)), _lib.ref(_lib.tensor_desc(out)),
+                                        _REDUCE_OPS[op], ctypes_stream(_stream(stream))), "reduce_scatter")
+    return out
+
+
+def all_to_all(comm, x: torch.Tensor, out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+    """All-to-all on the leading dim: out_j[i] = x_i[j] (AllToAll4DPlan, workloads.py:978-1028)."""
+    _require_cuda(x)
+    if out is None:
+        out = torch.empty_like(x)
+    check(_lib.load().pk_all_to_all(comm._h, _lib.ref(_lib.tensor_desc(x)), _lib.ref(_lib.tensor_desc(out)),
+                                    ctypes_stream(_stream(stream))), "all_to_all")
+    return out
+
+
+def ulysses_all_to_all(comm, x: torch.Tensor, inverse: bool = False, out: torch.Tensor | None = None,
+                       stream=None) -> torch.Tensor:
+    """Ulysses sequence <-> head all-to-all (UlyssesPlan, workloads.py:723-779).
+    forward: [B, S/n, H, D] -> [B, S, H/n, D]; inverse: back."""
+    _require_cuda(x)
+    n = comm.world
+    B, S, H, D = x.shape
+    if out is None:
+        shape = (B, S // n, H * n, D) if inverse else (B, S * n, H // n, D)
+        out = torch.empty(shape, dtype=x.dtype, device=x.device)
+    check(_lib.load().pk_ulysses_a2a(comm._h, _lib.ref(_lib.tensor_desc(x)), _lib.ref(_lib.tensor_desc(out)),
+                                     1 if inverse else 0, ctypes_stream(_stream(stream))), "ulysses_all_to_all")
+    return out

@@ -30,7 +30,8 @@ from overlapsim.primitives import IssueCtx, all_reduce, await_token, reduce, sto
 from overlapsim.workloads import WorkloadKind, build, check_oracle, reduced_dims  # noqa: E402
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-KINDS = ["ag_gemm", "gemm_rs", "gemm_ar", "ring_attention", "moe_dispatch_gemm"]
+KINDS = ["ag_gemm", "gemm_rs", "gemm_ar", "ring_attention", "moe_dispatch_gemm",
+         "ulysses_all_to_all", "all_gather_tensor_dim", "reduce_scatter_tensor_dim", "all_to_all_4d"]
 PROF = get_profile("b200-8")
 
 
@@ -62,6 +63,8 @@ def inputs_of(kind: str, plan) -> dict:
         return {"kv": np.stack(plan.pgls["kv"].buffers)}
     if kind == "moe_dispatch_gemm":
         return {"route": plan.route.astype(np.int16), "token_data": np.stack(plan.token_data)}
+    if kind in ("ulysses_all_to_all", "all_gather_tensor_dim", "reduce_scatter_tensor_dim", "all_to_all_4d"):
+        return {"x": np.stack(plan.pgls["x"].buffers)}
     raise KeyError(kind)
 
 

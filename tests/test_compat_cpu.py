@@ -11,10 +11,10 @@ from paper_2511_13940_b200.errors import LcscError, WorkloadError
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 GOLD = np.load(os.path.join(HERE, "golden", "golden_states.npz"))
-KINDS = [compat.WorkloadKind.AG_GEMM, compat.WorkloadKind.GEMM_RS, compat.WorkloadKind.GEMM_AR,
-         compat.WorkloadKind.RING_ATTENTION, compat.WorkloadKind.MOE_DISPATCH_GEMM]
+KINDS = list(compat.WorkloadKind)
 CHECKED = {"ag_gemm": "ag", "gemm_rs": "out", "gemm_ar": "acc", "ring_attention": "visited",
-           "moe_dispatch_gemm": "recv"}
+           "moe_dispatch_gemm": "recv", "ulysses_all_to_all": "y", "all_gather_tensor_dim": "out",
+           "reduce_scatter_tensor_dim": "out", "all_to_all_4d": "y"}
 
 
 @pytest.mark.parametrize("kind", KINDS)
@@ -31,9 +31,11 @@ def test_plan_inputs_and_oracle_match_reference(kind, n, seed):
         assert np.array_equal(np.stack(plan.inputs), GOLD[f"{key}/in/inputs"])
     elif kind is compat.WorkloadKind.RING_ATTENTION:
         assert np.array_equal(np.stack(plan.kv), GOLD[f"{key}/in/kv"])
-    else:
+    elif kind is compat.WorkloadKind.MOE_DISPATCH_GEMM:
         assert np.array_equal(plan.route, GOLD[f"{key}/in/route"])
         assert np.array_equal(np.stack(plan.token_data), GOLD[f"{key}/in/token_data"])
+    else:
+        assert np.array_equal(np.stack(plan.x), GOLD[f"{key}/in/x"])
     name = CHECKED[kind.value]
     exp = plan.oracle()[name]
     assert np.array_equal(np.stack(exp), GOLD[f"{key}/out/{name}"].astype(np.float64))
@@ -50,7 +52,7 @@ def test_validation_errors():
     with pytest.raises(WorkloadError):
         compat.build(compat.WorkloadKind.AG_GEMM, dict(M=8, N=8, K=64), num_devices=1)          # n >= 2
     with pytest.raises(WorkloadError):
-        compat.build(compat.WorkloadKind.ULYSSES_ALL_TO_ALL, dict(B=1, S=16, H=4, D=4), num_devices=2)
+        compat.build(compat.WorkloadKind.ULYSSES_ALL_TO_ALL, dict(B=1, S=16, H=3, D=4), num_devices=2)   # H % n
     with pytest.raises(LcscError):
         compat.LcscKernelSpec(schedule_mode=compat.ScheduleMode.INTRA_SM, num_comm_sms=4)
     with pytest.raises(LcscError):

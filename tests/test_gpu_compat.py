@@ -1,14 +1,13 @@
-"""Criterion-8-style sweep through the GPU (test_acceptance.py:230-249): every
-hot-path kind x n in {2, 4, 8} x seeds runs through the real fused ops on a
-local group and must match its oracle bit for bit."""
+"""Criterion-8-style sweep through the GPU (test_acceptance.py:230-249): all 9
+reference kinds x n in {2, 4, 8} x seeds run through the real fused ops /
+collectives on a local group and must match their oracle bit for bit."""
 import pytest
 
 from paper_2511_13940_b200 import compat
 
 pytestmark = pytest.mark.gpu
 
-KINDS = [compat.WorkloadKind.AG_GEMM, compat.WorkloadKind.GEMM_RS, compat.WorkloadKind.GEMM_AR,
-         compat.WorkloadKind.RING_ATTENTION, compat.WorkloadKind.MOE_DISPATCH_GEMM]
+KINDS = list(compat.WorkloadKind)
 
 
 @pytest.mark.parametrize("kind", KINDS)
