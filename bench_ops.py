@@ -1,0 +1,183 @@
+#!/usr/bin/env python
+"""Per-op measurements for every SURVEY.md §8 row (the headline metric is
+bench.py). One JSON line per op: device time (CUDA events, after warm-up),
+achieved rate, and the fraction of the bound that limits it on ONE B200:
+
+  * tensor-bound ops (GEMM, grouped GEMM, attention, fused GEMM+comm):
+    TFLOP/s / MEASURED_PEAKS.bf16_tflops (burst)
+  * byte-bound ops (MoE dispatch/combine, collectives): GB/s of HBM traffic /
+    MEASURED_PEAKS.hbm_gbs. On one GPU the multi-rank collectives run as a
+    local group (every rank's buffers in the same HBM), so their bound is HBM,
+    not NVLink: the numbers measure the kernels, not the fabric.
+
+    python bench_ops.py [--quick] [--out profiles/r1/ops.jsonl]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import torch  # noqa: E402
+
+import paper_2511_13940_b200 as pk  # noqa: E402
+
+PEAKS = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
+    os.path.join(ROOT, "MEASURED_PEAKS.json")) else {"bf16_tflops": 1590.0, "hbm_gbs": 6650.0}
+TF, HBM = PEAKS["bf16_tflops"], PEAKS["hbm_gbs"]
+
+
+def timeit(fn, iters=10, warm=3):
+    for _ in range(warm):
+        fn()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(iters):
+        fn()
+    e1.record()
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / iters
+
+
+def ranks(comms, fn):
+    """Launch fn(r, comm, stream) for every local-group rank, joined into the current stream."""
+    cur = torch.cuda.current_stream()
+    streams = ranks.streams.setdefault(len(comms), [torch.cuda.Stream() for _ in comms])
+
+    def run():
+        for r, c in enumerate(comms):
+            streams[r].wait_stream(cur)
+            with torch.cuda.stream(streams[r]):
+                fn(r, c, streams[r])
+        for s in streams:
+            cur.wait_stream(s)
+    return run
+
+
+ranks.streams = {}
+
+
+def emit(out, **kw):
+    line = json.dumps(kw)
+    print(line, flush=True)
+    out.write(line + "\n")
+
+
+def tensor_line(name, flops, ms, **extra):
+    tf = flops / (ms / 1e3) / 1e12
+    return dict(op=name, ms=ms, tflops=tf, bound="tensor", peak=TF, frac=tf / TF, **extra)
+
+
+def bytes_line(name, nbytes, ms, **extra):
+    gbs = nbytes / (ms / 1e3) / 1e9
+    return dict(op=name, ms=ms, gbs=gbs, bound="hbm", peak=HBM, frac=gbs / HBM, bytes=nbytes, **extra)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--quick", action="store_true")
+    ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "r1", "ops.jsonl"))
+    args = ap.parse_args()
+    os.makedirs(os.path.dirname(args.out), exist_ok=True)
+    out = open(args.out, "w")
+    torch.manual_seed(0)
+    dev = "cuda"
+    c1 = pk.local_group(1)[0]
+
+    # ---------------------------------------------------------------- GEMM (n = 1 AG-GEMM / GEMM-RS)
+    for S in ([8192] if args.quick else [8192, 16384]):
+        a = torch.randn(S, S, device=dev).bfloat16()
+        b = torch.randn(S, S, device=dev).bfloat16()
+        c = torch.empty(S, S, device=dev, dtype=torch.bfloat16)
+        ms = timeit(lambda: pk.gemm(a, b, c), iters=10)
+        ms_cb = timeit(lambda: torch.matmul(a, b.t(), out=c), iters=10)
+        emit(out, **tensor_line("gemm", 2 * S ** 3, ms, shape=[S, S, S], cublas_ms=ms_cb, vs_cublas=ms_cb / ms))
+        del a, b, c
+
+    # ---------------------------------------------------------------- ring attention (n = 1)
+    for S in ([4096] if args.quick else [4096, 16384]):
+        B, H, D = 1, 16, 128
+        q = torch.randn(B, S, H, D, device=dev).bfloat16()
+        k, v = torch.randn_like(q), torch.randn_like(q)
+        o, lse = torch.empty_like(q), torch.empty(B, H, S, device=dev)
+        ms = timeit(lambda: pk.ring_attention(c1, q, k, v, out=o, lse=lse))
+        qt, kt, vt = (x.transpose(1, 2).contiguous() for x in (q, k, v))
+        ms_sdpa = timeit(lambda: torch.nn.functional.scaled_dot_product_attention(qt, kt, vt))
+        emit(out, **tensor_line("ring_attention_n1", 4 * B * H * S * S * D, ms, shape=[B, S, H, D],
+                                sdpa_ms=ms_sdpa, vs_sdpa=ms_sdpa / ms))
+
+    # ---------------------------------------------------------------- MoE (n = 1): dispatch, grouped GEMM, combine
+    T, K, E, H, HE = (1024, 8, 64, 7168, 2048) if args.quick else (4096, 8, 64, 7168, 2048)
+    x = torch.randn(T, H, device=dev).bfloat16()
+    topk = torch.stack([torch.randperm(E, device=dev)[:K] for _ in range(T)]).int()
+    recv = (c1.empty((T * K, H)), c1.empty((T * K, 2), torch.int32))
+    ms = timeit(lambda: pk.moe_dispatch(c1, x, topk, E, recv=recv))
+    emit(out, **bytes_line("moe_dispatch_n1", T * H * 2 + T * K * H * 2, ms, T=T, H=H, k=K))
+    cnt = torch.tensor([T * K], dtype=torch.int32, device=dev)
+    w = torch.randn(E, HE, H, device=dev).bfloat16()
+    y = c1.empty((T * K, HE))
+    ms = timeit(lambda: pk.grouped_gemm(recv[0], recv[1], w, out=y, num_rows=cnt))
+    emit(out, **tensor_line("grouped_gemm_n1", 2 * T * K * H * HE, ms, rows=T * K, experts=E, H=H, H_exp=HE))
+    yh = c1.empty((T * K, H))
+    wts = torch.rand(T, K, device=dev)
+    comb = torch.empty(T, H, device=dev, dtype=torch.bfloat16)
+    ms = timeit(lambda: pk.moe_combine(c1, yh, topk, wts, E, out=comb))
+    emit(out, **bytes_line("moe_combine_n1", T * K * H * 2 + T * H * 2, ms, T=T, H=H, k=K))
+    del recv, y, yh, w
+
+    # ---------------------------------------------------------------- local groups (emulated ranks on one GPU)
+    for world in (2, 4):
+        comms = pk.local_group(world)
+        # all-reduce, P2P two-shot: every rank reads and writes S per op -> 2*n*S HBM bytes
+        for mb in ([64] if args.quick else [64, 256]):
+            n_el = mb * (1 << 20) // 2
+            ts = [c.empty((n_el,)) for c in comms]
+            ms = timeit(ranks(comms, lambda r, c, s: pk.all_reduce(c, ts[r], stream=s)))
+            emit(out, **bytes_line(f"all_reduce_local{world}", 2 * world * n_el * 2, ms, mib=mb,
+                                   algbw_gbs=n_el * 2 / (ms / 1e3) / 1e9))
+            del ts
+        # AG-GEMM / GEMM-RS / fused GEMM+AR: TFLOP/s of all emulated ranks together
+        S = 8192
+        ash = [c.empty((S // world, S)) for c in comms]
+        bsh = [torch.randn(S // world, S, device=dev).bfloat16() for _ in comms]
+        cs = [torch.empty(S, S // world, device=dev, dtype=torch.bfloat16) for _ in comms]
+        for t_ in ash:
+            t_.copy_(torch.randn_like(t_, dtype=torch.float32).bfloat16())
+        ms = timeit(ranks(comms, lambda r, c, s: pk.all_gather_gemm(c, ash[r], bsh[r], out=cs[r], stream=s)), iters=5)
+        emit(out, **tensor_line(f"ag_gemm_local{world}", 2 * S ** 3, ms, shape=[S, S, S], mode="inter_sm"))
+        ars = [torch.randn(S, S // world, device=dev).bfloat16() for _ in comms]
+        brs = [torch.randn(S, S // world, device=dev).bfloat16() for _ in comms]
+        ors = [c.empty((S // world, S)) for c in comms]
+        ms = timeit(ranks(comms, lambda r, c, s: pk.gemm_reduce_scatter(c, ars[r], brs[r], out=ors[r], stream=s)), iters=5)
+        emit(out, **tensor_line(f"gemm_rs_local{world}", 2 * S ** 3, ms, shape=[S, S, S]))
+        oar = [c.empty((S, S)) for c in comms]
+        ms = timeit(ranks(comms, lambda r, c, s: pk.gemm_all_reduce(c, ars[r], brs[r], out=oar[r], stream=s)), iters=5)
+        emit(out, **tensor_line(f"gemm_ar_local{world}", 2 * S ** 3, ms, shape=[S, S, S]))
+        # collectives: bytes = output written + input read, summed over ranks
+        rows = 8192
+        xs = [c.empty((rows, 1024)) for c in comms]
+        ag = [torch.empty(rows * world, 1024, device=dev, dtype=torch.bfloat16) for _ in comms]
+        ms = timeit(ranks(comms, lambda r, c, s: pk.all_gather(c, xs[r], out=ag[r], stream=s)))
+        emit(out, **bytes_line(f"all_gather_local{world}", 2 * world * rows * world * 1024 * 2, ms))
+        ul = [c.empty((1, 4096, 16, 128)) for c in comms]
+        uy = [torch.empty(1, 4096 * world, 16 // world, 128, device=dev, dtype=torch.bfloat16) for _ in comms]
+        ms = timeit(ranks(comms, lambda r, c, s: pk.ulysses_all_to_all(c, ul[r], out=uy[r], stream=s)))
+        emit(out, **bytes_line(f"ulysses_local{world}", 2 * world * 4096 * 16 * 128 * 2, ms))
+        qs = [torch.randn(1, 2048, 16, 128, device=dev).bfloat16() for _ in comms]
+        ms = timeit(ranks(comms, lambda r, c, s: pk.ring_attention(c, qs[r], qs[r], qs[r], stream=s)), iters=5)
+        emit(out, **tensor_line(f"ring_attention_local{world}", world * 4 * 16 * 2048 * 2048 * world * 128, ms,
+                                shape=[1, 2048 * world, 16, 128]))
+        for c in comms:
+            c.check()
+            c.destroy()
+    c1.destroy()
+    out.close()
+
+
+if __name__ == "__main__":
+    main()

@@ -121,10 +121,22 @@ __global__ void __launch_bounds__(512) ar_p2p_kernel(const __grid_constant__ ArA
   const long long lo = per * a.rank;
   const long long hi = min(a.nvec, lo + per);
   const long long stride = (long long)gridDim.x * blockDim.x;
-  for (long long i = lo + (long long)blockIdx.x * blockDim.x + threadIdx.x; i < hi; i += stride) {
-    uint4 in[NR];
+  constexpr int U = NR <= 2 ? 4 : (NR <= 4 ? 2 : 1);     // loads in flight per thread ~ 8
+  for (long long i0 = lo + (long long)blockIdx.x * blockDim.x + threadIdx.x; i0 < hi; i0 += stride * U) {
+  uint4 inu[U][NR];
 #pragma unroll
-    for (int d = 0; d < NR; ++d) in[d] = ld_v4_volatile(a.peers[d] + i * 16);
+  for (int u = 0; u < U; ++u) {
+    const long long iu = i0 + u * stride;
+    if (iu < hi) {
+#pragma unroll
+      for (int d = 0; d < NR; ++d) inu[u][d] = ld_v4_volatile(a.peers[d] + iu * 16);
+    }
+  }
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    const long long i = i0 + u * stride;
+    if (i >= hi) break;
+    uint4 (&in)[NR] = inu[u];
     uint4 outv;
     if constexpr (DT == PK_BF16) {
       float acc[8], t[8];
@@ -149,6 +161,7 @@ __global__ void __launch_bounds__(512) ar_p2p_kernel(const __grid_constant__ ArA
     }
 #pragma unroll
     for (int d = 0; d < NR; ++d) st_v4(a.peers[d] + i * 16, outv);
+  }
   }
   ar_end_barrier(a);
 }

@@ -45,7 +45,7 @@ __device__ __forceinline__ float coll_op(int op, float a, float b) {
   return op == 1 ? a + b : (op == 2 ? fmaxf(a, b) : fminf(a, b));
 }
 
-__global__ void __launch_bounds__(256) coll_kernel(const __grid_constant__ CollArgs a) {
+__global__ void __launch_bounds__(1024) coll_kernel(const __grid_constant__ CollArgs a) {
   if (threadIdx.x == 0) {
     if (blockIdx.x == 0) {
       __threadfence_system();
@@ -56,21 +56,34 @@ __global__ void __launch_bounds__(256) coll_kernel(const __grid_constant__ CollA
   __syncthreads();
   const int lane = threadIdx.x & 31;
   const long long warps = (long long)gridDim.x * (blockDim.x / 32);
-  const long long pieces = (a.run + kPiece - 1) / kPiece;
+  // 32-bit index decomposition (the host checks units < 2^31): 64-bit div/mod
+  // would dominate for small runs such as Ulysses' (H/n)*D rows.
+  const uint32_t pieces = (uint32_t)((a.run + kPiece - 1) / kPiece);
+  const uint32_t n1 = (uint32_t)a.n1, n2 = (uint32_t)a.n2;
   const int nsrc = a.reduce ? 1 : a.world;
-  const long long units = (long long)nsrc * a.n1 * a.n2 * pieces;
-  for (long long u = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32; u < units; u += warps) {
-    long long r = u;
-    const long long pc = r % pieces; r /= pieces;
-    const long long o2 = r % a.n2; r /= a.n2;
-    const long long o1 = r % a.n1; r /= a.n1;
+  const uint32_t units = (uint32_t)nsrc * n1 * n2 * pieces;
+  for (uint32_t u = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32; u < units; u += (uint32_t)warps) {
+    uint32_t r = u;
+    const uint32_t pc = r % pieces; r /= pieces;
+    const uint32_t o2 = r % n2; r /= n2;
+    const uint32_t o1 = r % n1; r /= n1;
     const int i = (int)r;
     const long long soff = a.s0 + o1 * a.s1 + o2 * a.s2 + pc * kPiece;
     uint8_t* d = a.dst + i * a.d_i + o1 * a.d1 + o2 * a.d2 + pc * kPiece;
     const long long bytes = min(kPiece, a.run - pc * kPiece);
     if (!a.reduce) {
+      // 4 independent 16 B loads in flight per lane before the stores
       const uint8_t* s = a.src[i] + soff;
-      for (long long v = lane * 16; v < bytes; v += 32 * 16) st_v4(d + v, ld_v4_volatile(s + v));
+      constexpr int U = 4;
+      long long v = lane * 16;
+      for (; v + (U - 1) * 512 < bytes; v += U * 512) {
+        uint4 t[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) t[u] = ld_v4_volatile(s + v + u * 512);
+#pragma unroll
+        for (int u = 0; u < U; ++u) st_v4(d + v + u * 512, t[u]);
+      }
+      for (; v < bytes; v += 512) st_v4(d + v, ld_v4_volatile(s + v));
     } else {
       for (long long v = lane * 16; v < bytes; v += 32 * 16) {
         uint4 acc4 = ld_v4_volatile(a.src[0] + soff + v);
@@ -133,6 +146,9 @@ static bool contiguous(const pk_tensor* t) {
 
 // Common launch: make x readable by peers, fill sync, launch.
 static int run_coll(Comm* c, const pk_tensor* x, CollArgs& a, long long units, cudaStream_t st) {
+  const long long pieces = (a.run + kPiece - 1) / kPiece;
+  if ((long long)c->world * a.n1 * a.n2 * pieces >= (1ll << 31))
+    return fail(PK_ERR_INVALID, "collective too large for one launch (2^31 pieces)");
   const size_t xbytes = (size_t)numel_of(x) * dtype_bytes(x->dtype);
   void* xs[kMaxRanks];
   if (!find_symmetric(c, x->ptr, xbytes, xs)) {
@@ -153,14 +169,14 @@ static int run_coll(Comm* c, const pk_tensor* x, CollArgs& a, long long units, c
     a.ready_peer[r] = pr + kSyncReady;
     a.done_peer[r] = pr + kSyncDone;
   }
-  int blocks = (int)std::min<long long>((long long)c->num_sms * 2, std::max<long long>(1, (units + 7) / 8));
+  int blocks = (int)std::min<long long>((long long)c->num_sms, std::max<long long>(1, (units + 31) / 32));
   if (c->local_group) blocks = std::min(blocks, c->num_sms);   // co-residency of all ranks' kernels
   c->ready_count += 1;
   c->done_count += (uint32_t)blocks;
   a.ready_expect = c->ready_count;
   a.done_expect = c->done_count;
   a.timeout_ns = c->timeout_ns;
-  coll_kernel<<<blocks, 256, 0, st>>>(a);
+  coll_kernel<<<blocks, 1024, 0, st>>>(a);   // 32 warps x 4 loads in flight per lane per SM
   PK_CUDA(cudaGetLastError());
   return PK_OK;
 }

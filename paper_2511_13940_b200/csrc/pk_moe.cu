@@ -156,35 +156,55 @@ __global__ void __launch_bounds__(kDispatchThreads) moe_dispatch_kernel(const __
     if (tot > a.cap) atomicExch(a.sync.err, 3u);
   }
   __syncthreads();
-  // one elected thread drives the bulk-copy engine for this CTA's tokens
+  // One elected thread drives the bulk-copy engine for this CTA's tokens as a
+  // flat sequence of <=16 KB pieces: piece p+3 is loaded (global -> smem)
+  // while piece p is stored to its k destinations (smem -> owner slots).
   if (threadIdx.x == 0) {
+    const int per_row = (a.row_bytes + kPiece - 1) / kPiece;
+    const int my_tokens = (a.T - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x;
+    const int total = my_tokens * per_row;
+    auto piece_src = [&](int p, int* tok, int* off, uint32_t* bytes) {
+      *tok = (int)blockIdx.x + (p / per_row) * (int)gridDim.x;
+      *off = (p % per_row) * kPiece;
+      *bytes = (uint32_t)min(kPiece, a.row_bytes - *off);
+    };
+    auto issue_load = [&](int p) {
+      int t, off;
+      uint32_t bytes;
+      piece_src(p, &t, &off, &bytes);
+      const int buf = p % kDispatchBufs;
+      mbar_arrive_expect_tx(&bars[buf], bytes);
+      bulk_g2s(smem + buf * kPiece, a.x + (long long)t * a.x_ld + off, bytes, &bars[buf]);
+    };
+    constexpr int kAhead = kDispatchBufs - 1;
+    for (int p = 0; p < total && p < kAhead; ++p) issue_load(p);
     uint32_t phase = 0;
-    int buf = 0;
-    for (int t = blockIdx.x; t < a.T; t += gridDim.x) {
-      const uint8_t* src = a.x + (long long)t * a.x_ld;
-      for (int off = 0; off < a.row_bytes; off += kPiece) {
-        const uint32_t bytes = (uint32_t)min(kPiece, a.row_bytes - off);
-        uint8_t* sb = smem + buf * kPiece;
-        bulk_wait_read<kDispatchBufs - 1>();     // the stores that last read this buffer are done reading
-        mbar_arrive_expect_tx(&bars[buf], bytes);
-        bulk_g2s(sb, src + off, bytes, &bars[buf]);
-        mbar_wait(&bars[buf], (phase >> buf) & 1);
-        phase ^= 1u << buf;
-        for (int j = 0; j < a.k; ++j) {
-          const int i = t * a.k + j;
-          const int li = a.local_idx[i];
-          if (li < 0) continue;
-          const int o = a.topk[i] % a.n;
-          const long long slot = (long long)base[o] + li;
-          if (slot >= a.cap) continue;
-          bulk_s2g(a.recv_peer[o] + slot * (long long)a.row_bytes + off, sb, bytes);
-          if (off == 0) {
-            a.recv_src_peer[o][slot * a.recv_src_cols] = (a.rank * a.T + t) * a.k + j;
-            if (a.recv_src_cols == 2) a.recv_src_peer[o][slot * 2 + 1] = a.topk[i] / a.n;   // local expert id
-          }
+    for (int p = 0; p < total; ++p) {
+      const int buf = p % kDispatchBufs;
+      mbar_wait(&bars[buf], (phase >> buf) & 1);
+      phase ^= 1u << buf;
+      int t, off;
+      uint32_t bytes;
+      piece_src(p, &t, &off, &bytes);
+      uint8_t* sb = smem + buf * kPiece;
+      for (int j = 0; j < a.k; ++j) {
+        const int i = t * a.k + j;
+        const int li = a.local_idx[i];
+        if (li < 0) continue;
+        const int o = a.topk[i] % a.n;
+        const long long slot = (long long)base[o] + li;
+        if (slot >= a.cap) continue;
+        bulk_s2g(a.recv_peer[o] + slot * (long long)a.row_bytes + off, sb, bytes);
+        if (off == 0) {
+          a.recv_src_peer[o][slot * a.recv_src_cols] = (a.rank * a.T + t) * a.k + j;
+          if (a.recv_src_cols == 2) a.recv_src_peer[o][slot * 2 + 1] = a.topk[i] / a.n;   // local expert id
         }
-        bulk_commit();
-        buf = (buf + 1) % kDispatchBufs;
+      }
+      bulk_commit();
+      if (p + kAhead < total) {
+        // the buffer of piece p+kAhead was last used by piece p-1: its stores must have read smem
+        bulk_wait_read<1>();
+        issue_load(p + kAhead);
       }
     }
     bulk_wait<0>();
