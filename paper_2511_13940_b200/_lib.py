@@ -12,7 +12,7 @@ import os
 import threading
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libpk.so")
+LIB_PATH = os.environ.get("PK_LIB", os.path.join(HERE, "libpk.so"))   # PK_LIB: A/B an alternative build
 
 PK_OK = 0
 PK_ERR_INVALID = 1

@@ -48,6 +48,9 @@ constexpr int AT_VSTAGES = 2;
 constexpr int AT_SMEM = 2 * AT_Q_BYTES + AT_KSTAGES * AT_K_BYTES + AT_VSTAGES * AT_V_BYTES + 512 + 1024;
 constexpr int AT_TMEM_COLS = 512;                // per tile: S (128, P aliased in its first 64) + O (128)
 constexpr float AT_RESCALE_THRESHOLD = 8.0f;     // log2 units: P stays <= 2^8 between rescales
+#ifndef AT_EXP_EMU
+#define AT_EXP_EMU 0                             // of every 8 exponentials, this many run on the FMA pipe (measured: 0 is fastest, softmax is issue-bound)
+#endif
 
 struct AttnArgs {
   CUtensorMap tm_q, tm_k, tm_v;  // 4-D maps over [B, S, H, D] (dims D, H, S, B)
@@ -91,6 +94,24 @@ PK_DEV float fast_exp2(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
+}
+
+// 2^x on the FMA/ALU pipes (FA4's MUFU offload): Cody-Waite split x = j + f,
+// f in [-0.5, 0.5], degree-5 polynomial for 2^f (rel. error < 2e-4, below
+// bf16's 2^-8 rounding of P), exponent added as integer bits.
+// Valid for x in [-126, 126]; softmax arguments are <= AT_RESCALE_THRESHOLD
+// and underflow to 0 is clamped.
+PK_DEV float poly_exp2(float x) {
+  x = fmaxf(x, -126.f);
+  const float j = rintf(x);
+  const float f = x - j;
+  float p = 1.8775767e-3f;
+  p = fmaf(p, f, 8.9893397e-3f);
+  p = fmaf(p, f, 5.5826318e-2f);
+  p = fmaf(p, f, 2.4015361e-1f);
+  p = fmaf(p, f, 6.9315308e-1f);
+  p = fmaf(p, f, 9.9999994e-1f);
+  return __int_as_float(__float_as_int(p) + (static_cast<int>(j) << 23));
 }
 
 // Two 128-query tiles (X = 0, 1) share every K/V block; the single MMA warp
@@ -255,7 +276,7 @@ __global__ void __launch_bounds__(AT_THREADS, 1) attn_fwd_kernel(const __grid_co
         tmem_ld_32x32b_x32(t_s + c * 32, r);
         tmem_ld_wait();
 #pragma unroll
-        for (int i = 0; i < 32; ++i) mx = fmaxf(mx, __uint_as_float(r[i]));
+        for (int i = 0; i < 16; ++i) mx = fmax3(mx, __uint_as_float(r[2 * i]), __uint_as_float(r[2 * i + 1]));
       }
       mx *= sc;
       const bool grow = mx > m + AT_RESCALE_THRESHOLD;
@@ -273,7 +294,10 @@ __global__ void __launch_bounds__(AT_THREADS, 1) attn_fwd_kernel(const __grid_co
         l *= alpha;
       }
       if (grow) m = mx;
-      float rs = 0.f;
+      // packed fp32 pairs: one FFMA2 computes s*scale - m for two keys, one FADD2
+      // accumulates two probabilities (the softmax warps are issue-bound)
+      const uint64_t sc2 = f2_pack(sc, sc), nm2 = f2_pack(-m, -m);
+      uint64_t rs2 = f2_pack(0.f, 0.f);
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
         uint32_t r[32];
@@ -282,14 +306,19 @@ __global__ void __launch_bounds__(AT_THREADS, 1) attn_fwd_kernel(const __grid_co
         uint32_t pk[16];
 #pragma unroll
         for (int i = 0; i < 16; ++i) {
-          const float p0 = fast_exp2(__uint_as_float(r[2 * i]) * sc - m);
-          const float p1 = fast_exp2(__uint_as_float(r[2 * i + 1]) * sc - m);
-          rs += p0 + p1;
+          float x0, x1;
+          f2_unpack(f2_fma(f2_pack(__uint_as_float(r[2 * i]), __uint_as_float(r[2 * i + 1])), sc2, nm2), x0, x1);
+          // optionally split the exponentials between MUFU (ex2) and the FMA pipe
+          const float p0 = fast_exp2(x0);
+          const float p1 = ((i & 3) < AT_EXP_EMU) ? poly_exp2(x1) : fast_exp2(x1);
+          rs2 = f2_add(rs2, f2_pack(p0, p1));
           pk[i] = pack_bf16x2(p0, p1);
         }
         tmem_st_32x32b_x16(t_s + c * 16, pk);          // columns [16c, 16c+16): already consumed
       }
-      l += rs;
+      float rs_lo, rs_hi;
+      f2_unpack(rs2, rs_lo, rs_hi);
+      l += rs_lo + rs_hi;
       tmem_st_wait();
       tc_fence_before();
       __syncwarp();
