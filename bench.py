@@ -191,6 +191,13 @@ def run_reference(args):
     return 0
 
 
+def _agree_uid(dist, rank: int, world: int) -> str:
+    import uuid
+    uid = [uuid.uuid4().hex[:16] if rank == 0 else None]
+    dist.broadcast_object_list(uid, src=0)
+    return uid[0]
+
+
 # ----------------------------------------------------------------------------- pk arm
 def main():
     args = parse()
@@ -205,13 +212,21 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # test hooks: all ranks on one GPU (gloo plumbing, no NCCL baseline) to exercise the N>1 path
+    if "PK_BENCH_DEVICE" in os.environ:
+        local = int(os.environ["PK_BENCH_DEVICE"])
+    backend = os.environ.get("PK_BENCH_BACKEND", "nccl")
     if world != args.gpus and rank == 0:
         print(f"warning: --gpus {args.gpus} but WORLD_SIZE {world}", file=sys.stderr)
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
-        comm = pk.Comm.init_from_env()
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
+            args.no_baseline = True
+        comm = pk.Comm.init(rank, world, local, _agree_uid(dist, rank, world))
     else:
         comm = pk.local_group(1, local)[0]
     n = world
@@ -255,7 +270,7 @@ def main():
     def max_over_ranks(x: float) -> float:
         if world == 1:
             return x
-        t = torch.tensor([x], device=dev, dtype=torch.float64)
+        t = torch.tensor([x], device=dev if backend == "nccl" else "cpu", dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
