@@ -318,54 +318,89 @@ lcsc_gemm_kernel(const __grid_constant__ GemmArgs args) {
       const int chunks_per_shard = args.a_rows_per_src / Cfg::TILE_M;
       const int total_chunks = args.world * chunks_per_shard;
       constexpr int PIECE = 32768;
-      constexpr int NBUF = (Cfg::STAGES * Cfg::STAGE_BYTES) / PIECE < Cfg::STAGES
-                               ? (Cfg::STAGES * Cfg::STAGE_BYTES) / PIECE : Cfg::STAGES;
-      uint32_t phase_bits = 0;
-      int buf = 0;
-      bool failed = false;
-      for (int i = 0; i < total_chunks && !failed; ++i) {
-        const int sidx = i / chunks_per_shard;                  // right neighbour first, local last
-        const int src = (args.rank + 1 + sidx) % args.world;
-        const int j = i % chunks_per_shard;
-        const int mt = (src * args.a_rows_per_src) / Cfg::TILE_M + j;
+      constexpr int NBUF = (Cfg::STAGES * Cfg::STAGE_BYTES) / PIECE < 8 ? (Cfg::STAGES * Cfg::STAGE_BYTES) / PIECE : 8;
+      static_assert(NBUF >= 3, "communicator needs >= 3 smem pieces");
+      constexpr int kLag = NBUF - 2;                   // stores allowed in flight before flags are published
+      const int pieces_per_chunk = (int)((chunk_bytes + PIECE - 1) / PIECE);
+      // this CTA's chunks in visiting order (right neighbour's shard first, local last)
+      int my_chunks[64];
+      int nmine = 0;
+      for (int i = 0; i < total_chunks && nmine < 64; ++i) {
+        const int src = (args.rank + 1 + i / chunks_per_shard) % args.world;
+        const int mt = (src * args.a_rows_per_src) / Cfg::TILE_M + i % chunks_per_shard;
         if ((mt % comm_ctas) != me) continue;
         if (src == args.rank && !args.comm_copy_local) continue;
-        if (src != args.rank && args.sync.ready_local != nullptr) {
-          if (!wait_geq(args.sync.ready_local + src, args.sync.ready_expect, args.sync.err, args.sync.timeout_ns)) {
-            failed = true;
-            break;
-          }
-        }
-        const uint8_t* s = args.comm_src[src] + (long long)j * chunk_bytes;
-        uint8_t* d = args.comm_dst + (long long)mt * chunk_bytes;
-        for (long long off = 0; off < chunk_bytes; off += PIECE) {
-          const uint32_t bytes = (uint32_t)min((long long)PIECE, chunk_bytes - off);
-          uint8_t* sb = smem + buf * PIECE;
-          uint64_t* bar = &full_bar[buf];
-          if (lane == 0) {
-            bulk_wait_read<NBUF - 1>();        // the store issued NBUF pieces ago has drained this buffer
-            mbar_arrive_expect_tx(bar, bytes);
-            bulk_g2s(sb, s + off, bytes, bar);
-          }
-          __syncwarp();
-          mbar_wait(bar, (phase_bits >> buf) & 1);
-          phase_bits ^= 1u << buf;
-          if (lane == 0) {
-            bulk_s2g(d + off, sb, bytes);
-            bulk_commit();
-          }
-          __syncwarp();
-          buf = (buf + 1 == NBUF) ? 0 : buf + 1;
-        }
-        if (lane == 0) {
-          bulk_wait<0>();
+        my_chunks[nmine++] = i;
+      }
+      const int total = nmine * pieces_per_chunk;
+      auto piece_of = [&](int p, const uint8_t** srcp, uint8_t** dstp, uint32_t* bytes, int* src_rank) {
+        const int i = my_chunks[p / pieces_per_chunk];
+        const int src = (args.rank + 1 + i / chunks_per_shard) % args.world;
+        const int j = i % chunks_per_shard;
+        const int mt = (src * args.a_rows_per_src) / Cfg::TILE_M + j;
+        const long long off = (long long)(p % pieces_per_chunk) * PIECE;
+        *srcp = args.comm_src[src] + (long long)j * chunk_bytes + off;
+        *dstp = args.comm_dst + (long long)mt * chunk_bytes + off;
+        *bytes = (uint32_t)min((long long)PIECE, chunk_bytes - off);
+        *src_rank = src;
+      };
+      bool failed = false;
+      uint32_t ready_mask = 0;
+      // make sure a shard's owner published it before its first piece is read
+      auto ensure_ready = [&](int src) -> bool {
+        if (src == args.rank || args.sync.ready_local == nullptr || ((ready_mask >> src) & 1)) return true;
+        if (!wait_geq(args.sync.ready_local + src, args.sync.ready_expect, args.sync.err, args.sync.timeout_ns)) return false;
+        ready_mask |= 1u << src;
+        return true;
+      };
+      auto issue_load = [&](int p) -> bool {
+        const uint8_t* sp;
+        uint8_t* dp;
+        uint32_t bytes;
+        int src;
+        piece_of(p, &sp, &dp, &bytes, &src);
+        if (!ensure_ready(src)) return false;
+        const int buf = p % NBUF;
+        mbar_arrive_expect_tx(&full_bar[buf], bytes);
+        bulk_g2s(smem + buf * PIECE, sp, bytes, &full_bar[buf]);
+        return true;
+      };
+      int published = 0;                               // chunks whose flag is out
+      auto publish_upto = [&](int done_pieces) {       // pieces [0, done_pieces) fully written
+        while (published < nmine && (published + 1) * pieces_per_chunk <= done_pieces) {
+          const int i = my_chunks[published];
+          const int src = (args.rank + 1 + i / chunks_per_shard) % args.world;
+          const int mt = (src * args.a_rows_per_src) / Cfg::TILE_M + i % chunks_per_shard;
           fence_async_global();
           __threadfence();
           asm volatile("st.release.gpu.global.u32 [%0], %1;" :: "l"(args.sync.flags + mt), "r"(args.sync.epoch) : "memory");
+          ++published;
         }
-        __syncwarp();
+      };
+      if (lane == 0) {
+        for (int p = 0; p < total && p < NBUF - 1 && !failed; ++p) failed = !issue_load(p);
+        uint32_t phase = 0;
+        for (int p = 0; p < total && !failed; ++p) {
+          const int buf = p % NBUF;
+          mbar_wait(&full_bar[buf], (phase >> buf) & 1);
+          phase ^= 1u << buf;
+          const uint8_t* sp;
+          uint8_t* dp;
+          uint32_t bytes;
+          int src;
+          piece_of(p, &sp, &dp, &bytes, &src);
+          bulk_s2g(dp, smem + buf * PIECE, bytes);
+          bulk_commit();
+          if (p + NBUF - 1 < total) {
+            bulk_wait_read<1>();                       // piece p-1 (same buffer as p+NBUF-1) has been read
+            failed = !issue_load(p + NBUF - 1);
+          }
+          bulk_wait<kLag>();                           // pieces <= p - kLag are in HBM
+          publish_upto(p + 1 - kLag);
+        }
+        bulk_wait<0>();
+        if (!failed) publish_upto(total);
       }
-      if (lane == 0) bulk_wait<0>();
       __syncwarp();
     }
   } else if (warp == 0) {
