@@ -61,6 +61,13 @@ struct AttnArgs {
   float* m_acc;
   float* l_acc;
   int first, last;               // first / last ring step
+  // single-launch ring: KV of ring step s lives at batch coordinate s*B + b of
+  // the K/V maps; steps >= 1 are usable once step_flags[s] >= flag_epoch
+  int blocks_per_step;           // 128-key blocks per ring step (S/n / 128)
+  const uint32_t* step_flags;    // null: all KV resident
+  uint32_t flag_epoch;
+  uint32_t* err;
+  uint64_t timeout_ns;
   uint16_t* o;                   // [B, S_q, H, D] bf16 output (last step)
   float* lse;                    // [B, H, S_q] natural-log LSE (last step)
 };
@@ -180,23 +187,36 @@ __global__ void __launch_bounds__(AT_THREADS, 1) attn_fwd_kernel(const __grid_co
         tma_load_4d(&a.tm_q, q_full, sq + x * AT_Q_BYTES, 0, h, qrow, b);
         tma_load_4d(&a.tm_q, q_full, sq + x * AT_Q_BYTES + AT_Q_BYTES / 2, 64, h, qrow, b);
       }
+      // key block j = ring step j / bps, block j % bps of that step's shard
+      const int bps = a.blocks_per_step;
+      int ready_steps = 1;                               // step 0 (own shard) is always resident
+      auto step_ready = [&](int step) {
+        while (a.step_flags != nullptr && ready_steps <= step) {
+          wait_geq(a.step_flags + ready_steps, a.flag_epoch, a.err, a.timeout_ns);
+          fence_async_global();
+          ++ready_steps;
+        }
+      };
       auto load_k = [&](int j) {
         const int st = j & 1;
+        const int step = j / bps, row = (j % bps) * AT_BN;
+        step_ready(step);
         mbar_wait(&k_empty[st], ((j >> 1) & 1) ^ 1);
         uint8_t* kb = sk + st * AT_K_BYTES;
         mbar_arrive_expect_tx(&k_full[st], AT_K_BYTES);
-        tma_load_4d(&a.tm_k, &k_full[st], kb, 0, h, j * AT_BN, b);
-        tma_load_4d(&a.tm_k, &k_full[st], kb + AT_K_BYTES / 2, 64, h, j * AT_BN, b);
+        tma_load_4d(&a.tm_k, &k_full[st], kb, 0, h, row, step * a.B + b);
+        tma_load_4d(&a.tm_k, &k_full[st], kb + AT_K_BYTES / 2, 64, h, row, step * a.B + b);
       };
       if (nblk > 0) load_k(0);
       for (int j = 0; j < nblk; ++j) {
         if (j + 1 < nblk) load_k(j + 1);
         const int vs = j & 1;
+        const int step = j / bps, row = (j % bps) * AT_BN;
         mbar_wait(&v_empty[vs], ((j >> 1) & 1) ^ 1);
         uint8_t* vb = sv + vs * AT_V_BYTES;
         mbar_arrive_expect_tx(&v_full[vs], AT_V_BYTES);
-        tma_load_4d(&a.tm_v, &v_full[vs], vb, 0, h, j * AT_BN, b);
-        tma_load_4d(&a.tm_v, &v_full[vs], vb + AT_V_BYTES / 2, 64, h, j * AT_BN, b);
+        tma_load_4d(&a.tm_v, &v_full[vs], vb, 0, h, row, step * a.B + b);
+        tma_load_4d(&a.tm_v, &v_full[vs], vb + AT_V_BYTES / 2, 64, h, row, step * a.B + b);
       }
     }
     __syncwarp();
@@ -392,6 +412,10 @@ __global__ void sync_signal_kernel(uint32_t* p0, uint32_t* p1, uint32_t* p2, uin
   __threadfence_system();
   for (int d = 0; d < n; ++d) signal_add(ps[d], 1u);
 }
+__global__ void flag_set_kernel(uint32_t* flag, uint32_t value) {
+  __threadfence_system();
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" :: "l"(flag), "r"(value) : "memory");
+}
 __global__ void sync_wait_kernel(const uint32_t* counters, int n, uint32_t expected, uint32_t* err, uint64_t timeout) {
   for (int d = 0; d < n; ++d) wait_geq(counters + d, expected, err, timeout);
 }
@@ -401,6 +425,7 @@ int preload_attn() {
   PK_CUDA(cudaFuncGetAttributes(&fa, attn_fwd_kernel));
   PK_CUDA(cudaFuncGetAttributes(&fa, sync_signal_kernel));
   PK_CUDA(cudaFuncGetAttributes(&fa, sync_wait_kernel));
+  PK_CUDA(cudaFuncGetAttributes(&fa, flag_set_kernel));
   return PK_OK;
 }
 
@@ -487,6 +512,7 @@ int ring_attn_fwd(Comm* c, const pk_tensor* q, const pk_tensor* k, const pk_tens
     PK_TRY(tmap_bshd(&a.tm_v, v->ptr, B, S, H, AT_BN));
     a.first = 1;
     a.last = 1;
+    a.blocks_per_step = (int)(S / AT_BN);
     return launch_attn(a, st);
   }
 
@@ -505,59 +531,71 @@ int ring_attn_fwd(Comm* c, const pk_tensor* q, const pk_tensor* k, const pk_tens
     PK_CUDA(cudaMemcpyAsync(s->local, v->ptr, shard, cudaMemcpyDeviceToDevice, st));
     for (int r = 0; r < n; ++r) vp[r] = s->peers[r];
   }
-  // Local state: 2 staging slots x (K, V) + fp32 running (O, m, l).
-  const size_t state_o = (size_t)B * H * S * D * 4, state_ml = (size_t)B * H * S * 4;
+  // Local staging: K and V of every ring step, step s at batch index s*B + b
+  // ([n*B, S/n, H, D] each); slot 0 is this rank's own shard. B200's HBM holds
+  // all n shards, so the ring's 2-slot rotation (workloads.py:644-681) becomes
+  // a single pass over n*S/n keys in the same visiting order (r, r-1, ...):
+  // one launch, O stays in TMEM across steps, no per-step LSE merge.
   Pgl* stage;
-  PK_TRY(comm_scratch(c, kScratchAttnStage, 4 * shard + state_o + 2 * state_ml, &stage));
-  uint8_t* base = static_cast<uint8_t*>(stage->local);
-  uint8_t* slot_k[2] = {base, base + shard};
-  uint8_t* slot_v[2] = {base + 2 * shard, base + 3 * shard};
-  a.o_acc = reinterpret_cast<float*>(base + 4 * shard);
-  a.m_acc = reinterpret_cast<float*>(base + 4 * shard + state_o);
-  a.l_acc = a.m_acc + (size_t)B * H * S;
-
-  // Streams / events for the copy-engine staging pipeline.
+  PK_TRY(comm_scratch(c, kScratchAttnStage, 2 * (size_t)n * shard, &stage));
+  uint8_t* kst = static_cast<uint8_t*>(stage->local);
+  uint8_t* vst = kst + (size_t)n * shard;
+  PK_CUDA(cudaMemcpyAsync(kst, kp[c->rank], shard, cudaMemcpyDeviceToDevice, st));
+  PK_CUDA(cudaMemcpyAsync(vst, vp[c->rank], shard, cudaMemcpyDeviceToDevice, st));
   if (!c->side) PK_CUDA(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
   cudaStream_t side = c->side;
-  cudaEvent_t ev_start, ev_attn[kMaxRanks], ev_copy[kMaxRanks];
+  cudaEvent_t ev_start, ev_side;
   PK_CUDA(cudaEventCreateWithFlags(&ev_start, cudaEventDisableTiming));
-  for (int s = 0; s < n; ++s) {
-    PK_CUDA(cudaEventCreateWithFlags(&ev_attn[s], cudaEventDisableTiming));
-    PK_CUDA(cudaEventCreateWithFlags(&ev_copy[s], cudaEventDisableTiming));
-  }
-  // 1. my shard is ready -> tell everyone; the side stream waits for all shards.
+  PK_CUDA(cudaEventCreateWithFlags(&ev_side, cudaEventDisableTiming));
+  uint32_t* flags = static_cast<uint32_t*>(c->sync->local) + kSyncFlags;    // per-step "staged" flags
+  c->epoch += 1;
+  // 1. my shard is ready -> tell everyone; the side stream pulls every peer shard
+  //    with the copy engine in ring order and flags each step as it lands.
   c->ready_count += 1;
   const uint32_t ready_expect = c->ready_count;
   PK_TRY(signal_all(c, kSyncReady, st));
   PK_CUDA(cudaEventRecord(ev_start, st));
   PK_CUDA(cudaStreamWaitEvent(side, ev_start, 0));
   PK_TRY(wait_all(c, kSyncReady, ready_expect, side));
-  // 2. ring steps: rank r visits shard (r - s) mod n at step s (workloads.py:666-681).
-  for (int s = 0; s < n; ++s) {
-    if (s + 1 < n) {
-      const int src = ((c->rank - (s + 1)) % n + n) % n;
-      const int slot = (s + 1) & 1;
-      if (s + 1 >= 2) PK_CUDA(cudaStreamWaitEvent(side, ev_attn[s - 1], 0));   // slot free again
-      PK_CUDA(cudaMemcpyAsync(slot_k[slot], kp[src], shard, cudaMemcpyDeviceToDevice, side));
-      PK_CUDA(cudaMemcpyAsync(slot_v[slot], vp[src], shard, cudaMemcpyDeviceToDevice, side));
-      PK_CUDA(cudaEventRecord(ev_copy[s + 1], side));
-    }
-    const void* ks = (s == 0) ? kp[c->rank] : slot_k[s & 1];
-    const void* vs = (s == 0) ? vp[c->rank] : slot_v[s & 1];
-    if (s > 0) PK_CUDA(cudaStreamWaitEvent(st, ev_copy[s], 0));
-    PK_TRY(tmap_bshd(&a.tm_k, ks, B, S, H, AT_BN));
-    PK_TRY(tmap_bshd(&a.tm_v, vs, B, S, H, AT_BN));
-    a.first = (s == 0);
-    a.last = (s == n - 1);
-    PK_TRY(launch_attn(a, st));
-    PK_CUDA(cudaEventRecord(ev_attn[s], st));
+  for (int s = 1; s < n; ++s) {
+    const int src = ((c->rank - s) % n + n) % n;                             // workloads.py:666-681
+    PK_CUDA(cudaMemcpyAsync(kst + (size_t)s * shard, kp[src], shard, cudaMemcpyDeviceToDevice, side));
+    PK_CUDA(cudaMemcpyAsync(vst + (size_t)s * shard, vp[src], shard, cudaMemcpyDeviceToDevice, side));
+    flag_set_kernel<<<1, 1, 0, side>>>(flags + s, c->epoch);
+    PK_CUDA(cudaGetLastError());
   }
-  // 3. I am done reading every peer's shard; wait until every peer is done with mine.
+  cudaEvent_t ev_copies;
+  PK_CUDA(cudaEventCreateWithFlags(&ev_copies, cudaEventDisableTiming));
+  PK_CUDA(cudaEventRecord(ev_copies, side));
+  // 2. done reading every peer's shard (side) -> signal; join the side stream.
   c->done_count += 1;
-  PK_TRY(signal_all(c, kSyncDone, st));
+  PK_TRY(signal_all(c, kSyncDone, side));
+  PK_CUDA(cudaEventRecord(ev_side, side));
+  // 3. one attention launch over all n*S/n keys; the loader waits step flags.
+  PK_TRY(tmap_bshd(&a.tm_k, kst, (int64_t)n * B, S, H, AT_BN));
+  PK_TRY(tmap_bshd(&a.tm_v, vst, (int64_t)n * B, S, H, AT_BN));
+  a.S_kv = (int)(n * S);
+  a.blocks_per_step = (int)(S / AT_BN);
+  a.step_flags = flags;
+  a.flag_epoch = c->epoch;
+  if (c->local_group) {
+    // Emulated ranks share this GPU's SMs: CTAs spinning on a step flag could
+    // hold the SMs the flag's producer chain needs (another rank's previous
+    // kernel). Start the attention after the copies instead of overlapping.
+    PK_CUDA(cudaStreamWaitEvent(st, ev_copies, 0));
+    a.step_flags = nullptr;
+  }
+  a.err = static_cast<uint32_t*>(c->sync->local) + kSyncErr;
+  a.timeout_ns = c->timeout_ns;
+  a.first = 1;
+  a.last = 1;
+  PK_TRY(launch_attn(a, st));
+  // 4. wait until every peer is done with my shard before the caller may reuse it.
+  PK_CUDA(cudaStreamWaitEvent(st, ev_side, 0));
   PK_TRY(wait_all(c, kSyncDone, c->done_count, st));
   cudaEventDestroy(ev_start);
-  for (int s = 0; s < n; ++s) { cudaEventDestroy(ev_attn[s]); cudaEventDestroy(ev_copy[s]); }
+  cudaEventDestroy(ev_side);
+  cudaEventDestroy(ev_copies);
   return PK_OK;
 }
 
