@@ -469,11 +469,7 @@ static int tmap_bshd(CUtensorMap* m, const void* p, int64_t B, int64_t S, int64_
 }
 
 static int launch_attn(const AttnArgs& a, cudaStream_t st) {
-  static thread_local bool attr = false;
-  if (!attr) {
-    PK_CUDA(cudaFuncSetAttribute(attn_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, AT_SMEM));
-    attr = true;
-  }
+  PK_TRY(ensure_smem_attr((const void*)attn_fwd_kernel, AT_SMEM));
   const int grid = a.B * a.H * ((a.S_q / AT_BM + 1) / 2);
   attn_fwd_kernel<<<grid, AT_THREADS, AT_SMEM, st>>>(a);
   PK_CUDA(cudaGetLastError());
@@ -544,9 +540,12 @@ int ring_attn_fwd(Comm* c, const pk_tensor* q, const pk_tensor* k, const pk_tens
   PK_CUDA(cudaMemcpyAsync(vst, vp[c->rank], shard, cudaMemcpyDeviceToDevice, st));
   if (!c->side) PK_CUDA(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
   cudaStream_t side = c->side;
-  cudaEvent_t ev_start, ev_side;
-  PK_CUDA(cudaEventCreateWithFlags(&ev_start, cudaEventDisableTiming));
-  PK_CUDA(cudaEventCreateWithFlags(&ev_side, cudaEventDisableTiming));
+  struct Events {
+    cudaEvent_t e[3] = {nullptr, nullptr, nullptr};
+    ~Events() { for (auto x : e) if (x) cudaEventDestroy(x); }
+  } evs;
+  for (auto& x : evs.e) PK_CUDA(cudaEventCreateWithFlags(&x, cudaEventDisableTiming));
+  cudaEvent_t ev_start = evs.e[0], ev_side = evs.e[1], ev_copies = evs.e[2];
   uint32_t* flags = static_cast<uint32_t*>(c->sync->local) + kSyncFlags;    // per-step "staged" flags
   c->epoch += 1;
   // 1. my shard is ready -> tell everyone; the side stream pulls every peer shard
@@ -564,8 +563,6 @@ int ring_attn_fwd(Comm* c, const pk_tensor* q, const pk_tensor* k, const pk_tens
     flag_set_kernel<<<1, 1, 0, side>>>(flags + s, c->epoch);
     PK_CUDA(cudaGetLastError());
   }
-  cudaEvent_t ev_copies;
-  PK_CUDA(cudaEventCreateWithFlags(&ev_copies, cudaEventDisableTiming));
   PK_CUDA(cudaEventRecord(ev_copies, side));
   // 2. done reading every peer's shard (side) -> signal; join the side stream.
   c->done_count += 1;
@@ -593,9 +590,6 @@ int ring_attn_fwd(Comm* c, const pk_tensor* q, const pk_tensor* k, const pk_tens
   // 4. wait until every peer is done with my shard before the caller may reuse it.
   PK_CUDA(cudaStreamWaitEvent(st, ev_side, 0));
   PK_TRY(wait_all(c, kSyncDone, c->done_count, st));
-  cudaEventDestroy(ev_start);
-  cudaEventDestroy(ev_side);
-  cudaEventDestroy(ev_copies);
   return PK_OK;
 }
 

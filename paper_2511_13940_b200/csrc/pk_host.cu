@@ -105,6 +105,19 @@ int make_tmap_2d(CUtensorMap* map, const void* ptr, CUtensorMapDataType dt, int 
   return PK_OK;
 }
 
+int ensure_smem_attr(const void* kern, int bytes) {
+  static std::mutex mu;
+  static std::vector<std::pair<const void*, int>> done;
+  int dev = 0;
+  PK_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lk(mu);
+  for (auto& e : done)
+    if (e.first == kern && e.second == dev) return PK_OK;
+  PK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+  done.emplace_back(kern, dev);
+  return PK_OK;
+}
+
 }  // namespace pk
 
 extern "C" {

@@ -84,6 +84,10 @@ int make_tmap_2d(CUtensorMap* map, const void* ptr, CUtensorMapDataType dt, int 
                  int64_t rows, int64_t cols, int64_t ld, int box_rows, int box_cols,
                  CUtensorMapSwizzle swz);
 
+// Set cudaFuncAttributeMaxDynamicSharedMemorySize for `kern` on the current
+// device once (the attribute is per device; cached per (kernel, device)).
+int ensure_smem_attr(const void* kern, int bytes);
+
 // ---------------------------------------------------------------- communicator
 struct Comm;
 

@@ -372,12 +372,8 @@ int moe_dispatch(Comm* c, const pk_tensor* x, const pk_tensor* topk, int num_exp
   fill_moe_sync(c, a.sync);
   void* params[] = {&a};
   PK_CUDA(cudaLaunchKernel((void*)moe_count_kernel, dim3(1), dim3(kCountThreads), params, 0, st));
-  static thread_local bool attr = false;
   const int smem = kDispatchBufs * kPiece;
-  if (!attr) {
-    PK_CUDA(cudaFuncSetAttribute(moe_dispatch_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    attr = true;
-  }
+  PK_TRY(ensure_smem_attr((const void*)moe_dispatch_kernel, smem));
   PK_CUDA(cudaLaunchKernel((void*)moe_dispatch_kernel, dim3(blocks), dim3(kDispatchThreads), params, smem, st));
   return PK_OK;
 }

@@ -40,11 +40,7 @@ static int launch_lcsc(const GemmArgs& args_in, int grid_ctas, cudaStream_t st) 
   PK_TRY(tile_counter(&args.tile_counter));
   using Cfg = GemmCfg<CG, BN, AM>;
   auto kern = lcsc_gemm_kernel<CG, BN, AM, EPI>;
-  static thread_local bool attr_done = false;
-  if (!attr_done) {
-    PK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES));
-    attr_done = true;
-  }
+  PK_TRY(ensure_smem_attr((const void*)kern, Cfg::SMEM_BYTES));
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid_ctas, 1, 1);
   cfg.blockDim = dim3(Cfg::NUM_THREADS, 1, 1);
