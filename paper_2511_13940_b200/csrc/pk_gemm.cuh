@@ -86,10 +86,15 @@ struct GemmArgs {
   int ar_mode;                            // 1: signal each finished tile's owner; comm CTAs all-reduce owned tiles
   uint32_t* ar_tile_local;                // [tiles] partial-tile arrivals at this rank (as owner)
   uint32_t* ar_tile_peer[kMaxRanksDev];   // the same array on every rank
-  uint32_t ar_expect;                     // cumulative arrivals per tile once all partials of this call landed
+  uint32_t ar_expect;                     // arrivals per tile in one call (the owner re-arms the counter to 0)
   uint8_t* ar_buf_peer[kMaxRanksDev];     // every rank's output buffer [M, N] bf16
   uint8_t* ar_mc;                         // multicast VA of the output (NVLS) or null
   long long ar_ld;                        // bytes between output rows
+  // inter-SM GEMM-RS (ar_mode 2): the owner of a tile is its row block
+  // (rows / ar_owner_rows); reduced rows go only to the owner's rs_out
+  int ar_owner_rows;
+  uint8_t* rs_out;                        // local output [M / world, N]
+  long long rs_ld;
   SyncArgs sync;
 };
 
@@ -259,22 +264,38 @@ lcsc_gemm_kernel(const __grid_constant__ GemmArgs args) {
     const int vec_per_row = BN * 2 / 16;                       // 16 B vectors per tile row
     const int vecs = Cfg::TILE_M * vec_per_row;
     __shared__ int ok_s;
+    const bool rs = args.ar_mode == 2;
+    // AR: tiles t = rank, rank + world, ...; RS: the tiles of this rank's row block
+    const int t_first = rs ? (args.rank * args.ar_owner_rows / Cfg::TILE_M) * num_n : args.rank;
+    const int t_end = rs ? ((args.rank + 1) * args.ar_owner_rows / Cfg::TILE_M) * num_n : num_m * num_n;
+    const int t_step = rs ? 1 : args.world;
     int j = 0;
-    for (int t = args.rank; t < num_m * num_n; t += args.world, ++j) {
+    for (int t = t_first; t < t_end; t += t_step, ++j) {
       if (j % comm_ctas != me) continue;
       if (threadIdx.x == 0) {
         ok_s = wait_geq(args.ar_tile_local + t, args.ar_expect, args.sync.err, args.sync.timeout_ns) ? 1 : 0;
+        // all arrivals of this call are in: re-arm the counter for the next call
+        // (no rank can start its next call before our done signal, sent later)
+        if (ok_s) args.ar_tile_local[t] = 0;
         fence_async_global();
       }
       __syncthreads();
       if (!ok_s) break;
       const long long base = (long long)(t / num_n) * Cfg::TILE_M * args.ar_ld + (long long)(t % num_n) * BN * 2;
+      // RS: destination row inside the owner's [M / world, N] output
+      const long long rs_base = rs ? ((long long)(t / num_n) * Cfg::TILE_M - (long long)args.rank * args.ar_owner_rows) *
+                                         args.rs_ld + (long long)(t % num_n) * BN * 2 : 0;
       for (int v = threadIdx.x; v < vecs; v += blockDim.x) {
         const long long off = base + (long long)(v / vec_per_row) * args.ar_ld + (v % vec_per_row) * 16;
         if (args.ar_mc != nullptr) {
           uint32_t r[4];
-          mm_ld_reduce_bf16x8(args.ar_mc + off, r);
-          mm_st_v4(args.ar_mc + off, r);
+          mm_ld_reduce_bf16x8(args.ar_mc + off, r);                  // reduce(): one in-fabric reduction load
+          if (rs) {
+            st_v4(args.rs_out + rs_base + (long long)(v / vec_per_row) * args.rs_ld + (v % vec_per_row) * 16,
+                  make_uint4(r[0], r[1], r[2], r[3]));
+          } else {
+            mm_st_v4(args.ar_mc + off, r);                           // all_reduce(): + multicast write-back
+          }
         } else {
           float acc[8];
 #pragma unroll
@@ -293,7 +314,8 @@ lcsc_gemm_kernel(const __grid_constant__ GemmArgs args) {
           o.y = pack_bf16x2(acc[2], acc[3]);
           o.z = pack_bf16x2(acc[4], acc[5]);
           o.w = pack_bf16x2(acc[6], acc[7]);
-          for (int d = 0; d < args.world; ++d) st_v4(args.ar_buf_peer[d] + off, o);
+          if (rs) st_v4(args.rs_out + rs_base + (long long)(v / vec_per_row) * args.rs_ld + (v % vec_per_row) * 16, o);
+          else for (int d = 0; d < args.world; ++d) st_v4(args.ar_buf_peer[d] + off, o);
         }
       }
       __syncthreads();
@@ -587,7 +609,8 @@ lcsc_gemm_kernel(const __grid_constant__ GemmArgs args) {
           fence_async_global();
           __threadfence_system();
           const int tile_id = mt * num_n + nt;
-          signal_add(args.ar_tile_peer[tile_id % args.world] + tile_id, 1u);
+          const int owner = args.ar_mode == 2 ? (mt * Cfg::TILE_M) / args.ar_owner_rows : tile_id % args.world;
+          signal_add(args.ar_tile_peer[owner] + tile_id, 1u);
         }
         __syncwarp();
       }

@@ -122,7 +122,6 @@ struct Comm {
   uint32_t epoch = 0;
   uint32_t ready_count = 0;          // cumulative ready signals expected per src
   uint32_t done_count = 0;           // cumulative done signals expected per src
-  uint32_t gemm_ar_calls = 0;        // fused GEMM+AR calls so far (per-tile arrival counters)
   int max_flags = 0;
   // scratch (symmetric) buffers, grown on demand
   Pgl* scratch[12] = {};

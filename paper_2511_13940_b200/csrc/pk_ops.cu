@@ -293,6 +293,65 @@ int ag_gemm(Comm* c, const pk_tensor* A, const pk_tensor* B, pk_tensor* C, pk_te
   return PK_OK;
 }
 
+// Inter-SM GEMM-RS (the paper's alternative schedule):
+// every rank stores its full partial product into a symmetric scratch and
+// signals the owner of each finished tile (the rank owning its rows); the
+// owner's communicator SMs reduce their rows over every rank's partial —
+// NVLS multimem.ld_reduce (the `reduce` primitive, primitives.py:211-234)
+// when the scratch has a multicast VA, P2P loads with the ascending fold
+// otherwise — and write the result to the local output.
+static int gemm_rs_inter(Comm* c, const pk_tensor* A, const pk_tensor* B, pk_tensor* O, const pk_sched* sched,
+                         cudaStream_t st) {
+  int64_t M, k_loc, ldA, N, Kb, ldB, Mo, No, ldO;
+  PK_TRY(check_matrix(A, "a", PK_BF16, &M, &k_loc, &ldA));
+  PK_TRY(check_matrix(B, "b", PK_BF16, &N, &Kb, &ldB));
+  PK_TRY(check_matrix(O, "out", PK_BF16, &Mo, &No, &ldO));
+  const int n = c->world;
+  const int64_t m_own = M / n;
+  if (m_own % 256) return fail(PK_ERR_INVALID, "gemm_rs (inter-SM): need (M/n) %% 256 == 0");
+  const Variant v{2, 1};
+  const int tiles = (int)((M / 256) * (N / 256));
+  if (tiles > (kSyncBytes / 4) - kSyncArTiles) return fail(PK_ERR_INVALID, "gemm_rs: too many tiles");
+  Pgl* part;
+  PK_TRY(comm_scratch(c, 10, (size_t)M * N * 2, &part, PK_PGL_MULTICAST));
+  GemmArgs args;
+  init_args(args);
+  args.M = (int)M; args.N = (int)N; args.K = (int)k_loc;
+  args.rank = c->rank; args.world = n;
+  args.a_rows_per_src = (int)M;
+  args.c_rows_per_dst = (int)M;
+  PK_TRY(tmap_a(&args.tmap_a[0], A->ptr, M, k_loc, ldA, 1));
+  PK_TRY(tmap_b(&args.tmap_b, B->ptr, N, k_loc, ldB, 2));
+  PK_TRY(tmap_c(&args.tmap_c[0], part->local, M, N, N));
+  // right neighbour's rows first, own rows last (their partials are local)
+  args.m_rot = (int)(((c->rank + 1) % n) * (m_own / 256));
+  const int clusters_total = std::max(2, (sched->num_sms > 0 ? std::min(sched->num_sms, c->num_sms) : c->num_sms) / 2);
+  int comm_clusters = std::max(1, (sched->num_comm_sms > 0 ? sched->num_comm_sms : 16) / 2);
+  if (c->local_group) comm_clusters = std::min(comm_clusters, std::max(1, clusters_total / 4));
+  if (comm_clusters >= clusters_total) return fail(PK_ERR_INVALID, "gemm_rs: num_comm_sms leaves no compute SMs");
+  const int compute_clusters = std::min(tiles, clusters_total - comm_clusters);
+  args.num_compute_clusters = compute_clusters;
+  uint32_t* local = static_cast<uint32_t*>(c->sync->local);
+  args.ar_mode = 2;
+  args.ar_owner_rows = (int)m_own;
+  args.ar_tile_local = local + kSyncArTiles;
+  for (int r = 0; r < n; ++r) {
+    args.ar_tile_peer[r] = static_cast<uint32_t*>(c->sync->peers[r]) + kSyncArTiles;
+    args.ar_buf_peer[r] = static_cast<uint8_t*>(part->peers[r]);
+  }
+  args.ar_mc = (sched->mode == PK_HYBRID) ? nullptr : static_cast<uint8_t*>(part->mc);   // HYBRID: force P2P
+  args.ar_ld = N * 2;
+  args.rs_out = static_cast<uint8_t*>(O->ptr);
+  args.rs_ld = ldO * 2;
+  args.ar_expect = (uint32_t)(n * 4 * 2);                          // every rank's 4 epilogue warps x 2 CTAs
+  args.sync_done_wait = 1;
+  c->epoch += 1;
+  c->done_count += (uint32_t)(comm_clusters * 2);
+  fill_sync(c, args.sync);
+  args.sync.ready_local = nullptr;
+  return launch_gemm_variant(v, EPI_STORE, args, (compute_clusters + comm_clusters) * 2, st);
+}
+
 int gemm_rs(Comm* c, const pk_tensor* A, const pk_tensor* B, pk_tensor* O, const pk_sched* sched, cudaStream_t st) {
   int64_t M, k_loc, ldA, N, Kb, ldB, Mo, No, ldO;
   PK_TRY(check_matrix(A, "a", PK_BF16, &M, &k_loc, &ldA));
@@ -308,6 +367,7 @@ int gemm_rs(Comm* c, const pk_tensor* A, const pk_tensor* B, pk_tensor* O, const
     return fail(PK_ERR_INVALID, "gemm_rs: need (M/n) %% 128 == 0, N %% 256 == 0, K %% 64 == 0 (got %lld, %lld, %lld)",
                 (long long)m_own, (long long)N, (long long)k_loc);
   if (n == 1) return gemm_local(A, B, O, sched, st, c->device);
+  if (sched && (sched->mode == PK_INTER_SM || sched->mode == PK_HYBRID)) return gemm_rs_inter(c, A, B, O, sched, st);
   const Variant v = pick_variant(m_own, k_loc, sched, /*reduce=*/true);
   const int cg = v.cg;
   const int tile_m = 128 * v.am * cg;
@@ -415,8 +475,7 @@ int gemm_ar(Comm* c, const pk_tensor* A, const pk_tensor* B, pk_tensor* O, const
   }
   args.ar_mc = static_cast<uint8_t*>(mc);
   args.ar_ld = N * 2;
-  c->gemm_ar_calls += 1;
-  args.ar_expect = c->gemm_ar_calls * (uint32_t)(n * 4 * 2);     // every rank's 4 epilogue warps x 2 CTAs per tile
+  args.ar_expect = (uint32_t)(n * 4 * 2);                          // every rank's 4 epilogue warps x 2 CTAs per tile
   args.sync_done_wait = 1;                                         // block 0 waits for every rank's comm CTAs
   c->epoch += 1;
   c->done_count += (uint32_t)(comm_clusters * 2);

@@ -75,3 +75,51 @@ def test_gemm_ar_shape_errors():
                            torch.zeros(256, 64, device="cuda", dtype=torch.bfloat16))
     for c in comms:
         c.destroy()
+
+
+def test_gemm_ar_and_rs_inter_sm_shape_changes_share_counters():
+    """Growing / shrinking tile counts and alternating GEMM+AR with inter-SM
+    GEMM-RS on one communicator (per-tile counters are re-armed by the owner)."""
+    pk = _pk()
+    world = 2
+    comms = pk.local_group(world)
+    rng = np.random.default_rng(11)
+    for it, (op, M, N) in enumerate([("ar", 256, 256), ("ar", 1024, 512), ("rs", 1024, 256), ("ar", 512, 256),
+                                     ("rs", 2048, 512), ("ar", 1024, 768)]):
+        K = 64
+        a = [(rng.random((M, K)) < 0.2).astype(np.float32) for _ in range(world)]
+        b = [rng.integers(-1, 2, size=(N, K)).astype(np.float32) for _ in range(world)]
+        da = [torch.from_numpy(x).cuda().bfloat16() for x in a]
+        db = [torch.from_numpy(x).cuda().bfloat16() for x in b]
+        torch.cuda.synchronize()
+        if op == "ar":
+            outs = run_ranks(comms, lambda r, c, s: pk.gemm_all_reduce(c, da[r], db[r], stream=s))
+            exp = [oracle.fold([x.astype(np.float64) @ y.T for x, y in zip(a, b)])] * world
+        else:
+            outs = run_ranks(comms, lambda r, c, s: pk.gemm_reduce_scatter(
+                c, da[r], db[r], schedule={"mode": "inter_sm", "num_comm_sms": 4}, stream=s))
+            exp = oracle.gemm_rs(a, b)
+        for r in range(world):
+            assert np.array_equal(outs[r].float().cpu().numpy(), exp[r]), (it, op, r)
+    for c in comms:
+        c.destroy()
+
+
+@pytest.mark.parametrize("world", [2, 4, 8])
+def test_gemm_rs_inter_sm_matches_oracle(world):
+    pk = _pk()
+    rng = np.random.default_rng(200 + world)
+    M, N, K = 256 * world, 512, 64
+    a = [(rng.random((M, K)) < 0.25).astype(np.float32) for _ in range(world)]
+    b = [rng.integers(-1, 2, size=(N, K)).astype(np.float32) for _ in range(world)]
+    comms = pk.local_group(world)
+    da = [torch.from_numpy(x).cuda().bfloat16() for x in a]
+    db = [torch.from_numpy(x).cuda().bfloat16() for x in b]
+    torch.cuda.synchronize()
+    outs = run_ranks(comms, lambda r, c, s: pk.gemm_reduce_scatter(c, da[r], db[r], schedule={"mode": "inter_sm"},
+                                                                    stream=s))
+    exp = oracle.gemm_rs(a, b)
+    for r in range(world):
+        assert np.array_equal(outs[r].float().cpu().numpy(), exp[r]), r
+    for c in comms:
+        c.destroy()
