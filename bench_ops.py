@@ -82,7 +82,10 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--quick", action="store_true")
     ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "r1", "ops.jsonl"))
+    ap.add_argument("--only", default="", help="comma list of sections: gemm,attn,moe,local")
     args = ap.parse_args()
+    only = set(filter(None, args.only.split(",")))
+    want = lambda sec: not only or sec in only
     os.makedirs(os.path.dirname(args.out), exist_ok=True)
     out = open(args.out, "w")
     torch.manual_seed(0)
@@ -90,7 +93,7 @@ def main():
     c1 = pk.local_group(1)[0]
 
     # ---------------------------------------------------------------- GEMM (n = 1 AG-GEMM / GEMM-RS)
-    for S in ([8192] if args.quick else [8192, 16384]):
+    for S in ([8192] if args.quick else [8192, 16384]) if want("gemm") else []:
         a = torch.randn(S, S, device=dev).bfloat16()
         b = torch.randn(S, S, device=dev).bfloat16()
         c = torch.empty(S, S, device=dev, dtype=torch.bfloat16)
@@ -100,7 +103,7 @@ def main():
         del a, b, c
 
     # ---------------------------------------------------------------- ring attention (n = 1)
-    for S in ([4096] if args.quick else [4096, 16384]):
+    for S in ([4096] if args.quick else [4096, 16384]) if want("attn") else []:
         B, H, D = 1, 16, 128
         q = torch.randn(B, S, H, D, device=dev).bfloat16()
         k, v = torch.randn_like(q), torch.randn_like(q)
@@ -113,6 +116,14 @@ def main():
 
     # ---------------------------------------------------------------- MoE (n = 1): dispatch, grouped GEMM, combine
     T, K, E, H, HE = (1024, 8, 64, 7168, 2048) if args.quick else (4096, 8, 64, 7168, 2048)
+    moe(args, out, c1, T, K, E, H, HE) if want("moe") else None
+    local(args, out) if want("local") else None
+    c1.destroy()
+    out.close()
+
+
+def moe(args, out, c1, T, K, E, H, HE):
+    dev = "cuda"
     x = torch.randn(T, H, device=dev).bfloat16()
     topk = torch.stack([torch.randperm(E, device=dev)[:K] for _ in range(T)]).int()
     recv = (c1.empty((T * K, H)), c1.empty((T * K, 2), torch.int32))
@@ -123,6 +134,13 @@ def main():
     y = c1.empty((T * K, HE))
     ms = timeit(lambda: pk.grouped_gemm(recv[0], recv[1], w, out=y, num_rows=cnt))
     emit(out, **tensor_line("grouped_gemm_n1", 2 * T * K * H * HE, ms, rows=T * K, experts=E, H=H, H_exp=HE))
+    # per-rank view of the 8-GPU deployment: 64 experts / 8 ranks = 8 local experts, T*k rows received
+    g8 = torch.randint(0, 8, (T * K,), device=dev, dtype=torch.int32)
+    w8 = torch.randn(8, HE, H, device=dev).bfloat16()
+    ms = timeit(lambda: pk.grouped_gemm(recv[0], g8, w8, out=y))
+    emit(out, **tensor_line("grouped_gemm_8experts", 2 * T * K * H * HE, ms, rows=T * K, experts=8, H=H, H_exp=HE))
+    ms_g = timeit(lambda: pk.gemm(recv[0], w8[0], out=y))
+    emit(out, **tensor_line("gemm_same_shape", 2 * T * K * H * HE, ms_g, rows=T * K, H=H, H_exp=HE))
     yh = c1.empty((T * K, H))
     wts = torch.rand(T, K, device=dev)
     comb = torch.empty(T, H, device=dev, dtype=torch.bfloat16)
@@ -130,7 +148,10 @@ def main():
     emit(out, **bytes_line("moe_combine_n1", T * K * H * 2 + T * H * 2, ms, T=T, H=H, k=K))
     del recv, y, yh, w
 
+
+def local(args, out):
     # ---------------------------------------------------------------- local groups (emulated ranks on one GPU)
+    dev = "cuda"
     for world in (2, 4):
         comms = pk.local_group(world)
         # all-reduce, P2P two-shot: every rank reads and writes S per op -> 2*n*S HBM bytes
@@ -154,7 +175,10 @@ def main():
         brs = [torch.randn(S, S // world, device=dev).bfloat16() for _ in comms]
         ors = [c.empty((S // world, S)) for c in comms]
         ms = timeit(ranks(comms, lambda r, c, s: pk.gemm_reduce_scatter(c, ars[r], brs[r], out=ors[r], stream=s)), iters=5)
-        emit(out, **tensor_line(f"gemm_rs_local{world}", 2 * S ** 3, ms, shape=[S, S, S]))
+        emit(out, **tensor_line(f"gemm_rs_local{world}", 2 * S ** 3, ms, shape=[S, S, S], mode="intra_sm"))
+        ms = timeit(ranks(comms, lambda r, c, s: pk.gemm_reduce_scatter(c, ars[r], brs[r], out=ors[r],
+                                                                        schedule={"mode": "inter_sm"}, stream=s)), iters=5)
+        emit(out, **tensor_line(f"gemm_rs_inter_local{world}", 2 * S ** 3, ms, shape=[S, S, S], mode="inter_sm"))
         oar = [c.empty((S, S)) for c in comms]
         ms = timeit(ranks(comms, lambda r, c, s: pk.gemm_all_reduce(c, ars[r], brs[r], out=oar[r], stream=s)), iters=5)
         emit(out, **tensor_line(f"gemm_ar_local{world}", 2 * S ** 3, ms, shape=[S, S, S]))
@@ -175,8 +199,6 @@ def main():
         for c in comms:
             c.check()
             c.destroy()
-    c1.destroy()
-    out.close()
 
 
 if __name__ == "__main__":
