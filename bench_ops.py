@@ -183,19 +183,25 @@ def local(args, out):
         ms = timeit(ranks(comms, lambda r, c, s: pk.gemm_all_reduce(c, ars[r], brs[r], out=oar[r], stream=s)), iters=5)
         emit(out, **tensor_line(f"gemm_ar_local{world}", 2 * S ** 3, ms, shape=[S, S, S]))
         # collectives: bytes = output written + input read, summed over ranks
-        rows = 8192
+        # sizes large enough that the device time, not the Python launch of
+        # `world` emulated ranks (~25 us each), is what gets measured
+        rows = 65536
         xs = [c.empty((rows, 1024)) for c in comms]
         ag = [torch.empty(rows * world, 1024, device=dev, dtype=torch.bfloat16) for _ in comms]
         ms = timeit(ranks(comms, lambda r, c, s: pk.all_gather(c, xs[r], out=ag[r], stream=s)))
         emit(out, **bytes_line(f"all_gather_local{world}", 2 * world * rows * world * 1024 * 2, ms))
-        ul = [c.empty((1, 4096, 16, 128)) for c in comms]
-        uy = [torch.empty(1, 4096 * world, 16 // world, 128, device=dev, dtype=torch.bfloat16) for _ in comms]
+        del xs, ag
+        SU = 32768
+        ul = [c.empty((1, SU, 16, 128)) for c in comms]
+        uy = [torch.empty(1, SU * world, 16 // world, 128, device=dev, dtype=torch.bfloat16) for _ in comms]
         ms = timeit(ranks(comms, lambda r, c, s: pk.ulysses_all_to_all(c, ul[r], out=uy[r], stream=s)))
-        emit(out, **bytes_line(f"ulysses_local{world}", 2 * world * 4096 * 16 * 128 * 2, ms))
-        qs = [torch.randn(1, 2048, 16, 128, device=dev).bfloat16() for _ in comms]
+        emit(out, **bytes_line(f"ulysses_local{world}", 2 * world * SU * 16 * 128 * 2, ms, shape=[1, SU, 16, 128]))
+        del ul, uy
+        SL = 8192
+        qs = [torch.randn(1, SL, 16, 128, device=dev).bfloat16() for _ in comms]
         ms = timeit(ranks(comms, lambda r, c, s: pk.ring_attention(c, qs[r], qs[r], qs[r], stream=s)), iters=5)
-        emit(out, **tensor_line(f"ring_attention_local{world}", world * 4 * 16 * 2048 * 2048 * world * 128, ms,
-                                shape=[1, 2048 * world, 16, 128]))
+        emit(out, **tensor_line(f"ring_attention_local{world}", world * 4 * 16 * SL * SL * world * 128, ms,
+                                shape=[1, SL * world, 16, 128]))
         for c in comms:
             c.check()
             c.destroy()

@@ -49,7 +49,7 @@ constexpr int AT_SMEM = 2 * AT_Q_BYTES + AT_KSTAGES * AT_K_BYTES + AT_VSTAGES * 
 constexpr int AT_TMEM_COLS = 512;                // per tile: S (128, P aliased in its first 64) + O (128)
 constexpr float AT_RESCALE_THRESHOLD = 8.0f;     // log2 units: P stays <= 2^8 between rescales
 #ifndef AT_EXP_EMU
-#define AT_EXP_EMU 0                             // of every 8 exponentials, this many run on the FMA pipe (measured: 0 is fastest, softmax is issue-bound)
+#define AT_EXP_EMU 1                             // of every 4 key pairs, this many take 2^x on the FMA pipe (MUFU offload)
 #endif
 
 struct AttnArgs {
@@ -103,22 +103,28 @@ PK_DEV float fast_exp2(float x) {
   return y;
 }
 
-// 2^x on the FMA/ALU pipes (FA4's MUFU offload): Cody-Waite split x = j + f,
-// f in [-0.5, 0.5], degree-5 polynomial for 2^f (rel. error < 2e-4, below
-// bf16's 2^-8 rounding of P), exponent added as integer bits.
-// Valid for x in [-126, 126]; softmax arguments are <= AT_RESCALE_THRESHOLD
-// and underflow to 0 is clamped.
-PK_DEV float poly_exp2(float x) {
-  x = fmaxf(x, -126.f);
-  const float j = rintf(x);
-  const float f = x - j;
-  float p = 1.8775767e-3f;
-  p = fmaf(p, f, 8.9893397e-3f);
-  p = fmaf(p, f, 5.5826318e-2f);
-  p = fmaf(p, f, 2.4015361e-1f);
-  p = fmaf(p, f, 6.9315308e-1f);
-  p = fmaf(p, f, 9.9999994e-1f);
-  return __int_as_float(__float_as_int(p) + (static_cast<int>(j) << 23));
+// 2^x for two arguments on the FMA/ALU pipes (FA4's MUFU offload). At D = 128
+// one tile's 128x128 exponentials keep MUFU (16/clk/SM) busy for as long as
+// its two MMAs keep the tensor core busy, so moving a fraction of them to the
+// FMA pipe shortens the softmax critical path. No XU instruction is used:
+//   t = x + 1.5*2^23         round(x) lands in t's low mantissa bits
+//   f = x - (t - 1.5*2^23)   in [-0.5, 0.5], exact
+//   2^f ~ degree-3 minimax   (rel. error 7.5e-5, far below bf16's 2^-9 for P)
+//   2^x = bits(2^f) + (bits(t) << 23)   (the 1.5*2^23 bias shifts out mod 2^32)
+// x is clamped to -125 so the exponent add cannot underflow.
+PK_DEV void poly_exp2x2(float x0, float x1, float& p0, float& p1) {
+  const uint64_t x2 = f2_pack(fmaxf(x0, -125.f), fmaxf(x1, -125.f));
+  const uint64_t big = f2_pack(12582912.f, 12582912.f);
+  const uint64_t t2 = f2_add(x2, big);
+  const uint64_t f2 = f2_add(x2, f2_fma(t2, f2_pack(-1.f, -1.f), big));
+  uint64_t q = f2_fma(f2_pack(5.5171456e-2f, 5.5171456e-2f), f2, f2_pack(2.4261115e-1f, 2.4261115e-1f));
+  q = f2_fma(q, f2, f2_pack(6.9326103e-1f, 6.9326103e-1f));
+  q = f2_fma(q, f2, f2_pack(9.9992806e-1f, 9.9992806e-1f));
+  float q0, q1, t0, t1;
+  f2_unpack(q, q0, q1);
+  f2_unpack(t2, t0, t1);
+  p0 = __int_as_float(__float_as_int(q0) + (__float_as_int(t0) << 23));
+  p1 = __int_as_float(__float_as_int(q1) + (__float_as_int(t1) << 23));
 }
 
 // Two 128-query tiles (X = 0, 1) share every K/V block; the single MMA warp
@@ -147,9 +153,9 @@ __global__ void __launch_bounds__(AT_THREADS, 1) attn_fwd_kernel(const __grid_co
   uint64_t* v_full = bars + 5;      // [2]
   uint64_t* v_empty = bars + 7;     // [2]
   uint64_t* s_full = bars + 9;      // [2] per tile
-  uint64_t* p_full = bars + 11;     // [2] per tile
-  uint64_t* o_full = bars + 13;     // [2] per tile
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 15);
+  uint64_t* p_full = bars + 11;     // [2 tiles][2 halves]: P of keys [64h, 64h+64) in TMEM
+  uint64_t* o_full = bars + 15;     // [2] per tile
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 17);
 
   const uint32_t warp = warp_id_sync();
   const uint32_t lane = lane_id();
@@ -167,7 +173,8 @@ __global__ void __launch_bounds__(AT_THREADS, 1) attn_fwd_kernel(const __grid_co
     for (int i = 0; i < 2; ++i) {
       mbar_init(&k_full[i], 1); mbar_init(&k_empty[i], 1);
       mbar_init(&v_full[i], 1); mbar_init(&v_empty[i], 1);
-      mbar_init(&s_full[i], 1); mbar_init(&p_full[i], 4); mbar_init(&o_full[i], 1);
+      mbar_init(&s_full[i], 1); mbar_init(&o_full[i], 1);
+      mbar_init(&p_full[2 * i], 4); mbar_init(&p_full[2 * i + 1], 4);
     }
     fence_mbar_init();
   }
@@ -178,6 +185,10 @@ __global__ void __launch_bounds__(AT_THREADS, 1) attn_fwd_kernel(const __grid_co
   const uint32_t tmem = *tmem_slot;
   // tile X: S at cols [256X, 256X+128) (P packed in its first 64), O at [256X+128, 256X+256)
 
+  // registers follow the roles: warpgroup 0 (loader, MMA, allocator, idle)
+  // needs few, the two softmax warpgroups hold a whole 128-key S row each
+  if (warp < 4) {
+  asm volatile("setmaxnreg.dec.sync.aligned.u32 56;\n" ::: "memory");
   if (warp == 0) {
     // ------------------------------------------------------------ loader (lane 0)
     if (lane == 0) {
@@ -238,14 +249,15 @@ __global__ void __launch_bounds__(AT_THREADS, 1) attn_fwd_kernel(const __grid_co
       }
       umma_commit<1>(&s_full[x]);
     };
-    auto issue_pv = [&](int x, int j) {                 // O_x += P_x V_j
+    auto issue_pv = [&](int x, int j, int half) {       // O_x += P_x V_j over keys [64 half, 64 half + 64)
       const uint32_t v_addr = smem_u32(sv + (j & 1) * AT_V_BYTES);
 #pragma unroll
-      for (int kk = 0; kk < AT_BN / 16; ++kk) {
+      for (int k4 = 0; k4 < AT_BN / 32; ++k4) {
+        const int kk = half * (AT_BN / 32) + k4;
         const uint64_t bd = sdesc_mnmajor_sw128(v_addr + kk * 2048, AT_V_BYTES / 2, 1024);
         umma_f16_ts(tmem + 256 * x + 128, tmem + 256 * x + kk * 8, bd, id_o, (j > 0 || kk > 0) ? 1u : 0u);
       }
-      if (j == nblk - 1) umma_commit<1>(&o_full[x]);
+      if (half == 1 && j == nblk - 1) umma_commit<1>(&o_full[x]);
     };
     if (nblk > 0) {
       mbar_wait(&k_full[0], 0);
@@ -261,10 +273,15 @@ __global__ void __launch_bounds__(AT_THREADS, 1) attn_fwd_kernel(const __grid_co
       const bool more = j + 1 < nblk;
       if (more) mbar_wait(&k_full[(j + 1) & 1], ((j + 1) >> 1) & 1);
       for (int x = 0; x < ntile; ++x) {
-        mbar_wait(&p_full[x], j & 1);
+        // the first half of P is consumed while the softmax still works on the second
+        mbar_wait(&p_full[2 * x], j & 1);
+        tc_fence_after();
+        if (elect_one()) issue_pv(x, j, 0);
+        __syncwarp();
+        mbar_wait(&p_full[2 * x + 1], j & 1);
         tc_fence_after();
         if (elect_one()) {
-          issue_pv(x, j);
+          issue_pv(x, j, 1);
           if (more) issue_qk(x, j + 1);
         }
         __syncwarp();
@@ -275,7 +292,10 @@ __global__ void __launch_bounds__(AT_THREADS, 1) attn_fwd_kernel(const __grid_co
       }
       __syncwarp();
     }
-  } else if (warp >= 4 && (int)(warp - 4) / 4 < ntile) {
+  }
+  } else {
+  asm volatile("setmaxnreg.inc.sync.aligned.u32 224;\n" ::: "memory");
+  if ((int)(warp - 4) / 4 < ntile) {
     // ------------------------------------------------------------ softmax + epilogue (tile x)
     const int x = (warp - 4) / 4;
     const int qt = 2 * qp + x;
@@ -289,15 +309,20 @@ __global__ void __launch_bounds__(AT_THREADS, 1) attn_fwd_kernel(const __grid_co
     for (int j = 0; j < nblk; ++j) {
       mbar_wait(&s_full[x], j & 1);
       tc_fence_after();
-      float mx = -INFINITY;
+      // the whole S row (128 fp32) into registers with one TMEM wait; the max
+      // and exp passes both read registers
+      uint32_t r[AT_BN];
 #pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        uint32_t r[32];
-        tmem_ld_32x32b_x32(t_s + c * 32, r);
-        tmem_ld_wait();
+      for (int c = 0; c < 4; ++c) tmem_ld_32x32b_x32(t_s + c * 32, *reinterpret_cast<uint32_t(*)[32]>(r + c * 32));
+      tmem_ld_wait();
+      // row max as 8 independent FMNMX3 chains (a single chain is 64 dependent ops)
+      float m8[8];
 #pragma unroll
-        for (int i = 0; i < 16; ++i) mx = fmax3(mx, __uint_as_float(r[2 * i]), __uint_as_float(r[2 * i + 1]));
-      }
+      for (int t = 0; t < 8; ++t) m8[t] = fmax3(__uint_as_float(r[2 * t]), __uint_as_float(r[2 * t + 1]), -INFINITY);
+#pragma unroll
+      for (int i = 8; i < AT_BN / 2; ++i)
+        m8[i & 7] = fmax3(m8[i & 7], __uint_as_float(r[2 * i]), __uint_as_float(r[2 * i + 1]));
+      float mx = fmax3(fmax3(m8[0], m8[1], m8[2]), fmax3(m8[3], m8[4], m8[5]), fmaxf(m8[6], m8[7]));
       mx *= sc;
       const bool grow = mx > m + AT_RESCALE_THRESHOLD;
       if (j > 0 && __any_sync(0xffffffffu, grow)) {
@@ -317,32 +342,37 @@ __global__ void __launch_bounds__(AT_THREADS, 1) attn_fwd_kernel(const __grid_co
       // packed fp32 pairs: one FFMA2 computes s*scale - m for two keys, one FADD2
       // accumulates two probabilities (the softmax warps are issue-bound)
       const uint64_t sc2 = f2_pack(sc, sc), nm2 = f2_pack(-m, -m);
-      uint64_t rs2 = f2_pack(0.f, 0.f);
+      uint64_t rs2[4];                                    // 4 independent row-sum chains
+#pragma unroll
+      for (int t = 0; t < 4; ++t) rs2[t] = f2_pack(0.f, 0.f);
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
-        uint32_t r[32];
-        tmem_ld_32x32b_x32(t_s + c * 32, r);
-        tmem_ld_wait();
         uint32_t pk[16];
 #pragma unroll
         for (int i = 0; i < 16; ++i) {
-          float x0, x1;
-          f2_unpack(f2_fma(f2_pack(__uint_as_float(r[2 * i]), __uint_as_float(r[2 * i + 1])), sc2, nm2), x0, x1);
-          // optionally split the exponentials between MUFU (ex2) and the FMA pipe
-          const float p0 = fast_exp2(x0);
-          const float p1 = ((i & 3) < AT_EXP_EMU) ? poly_exp2(x1) : fast_exp2(x1);
-          rs2 = f2_add(rs2, f2_pack(p0, p1));
+          float x0, x1, p0, p1;
+          f2_unpack(f2_fma(f2_pack(__uint_as_float(r[32 * c + 2 * i]), __uint_as_float(r[32 * c + 2 * i + 1])), sc2, nm2),
+                    x0, x1);
+          if ((i & 3) < AT_EXP_EMU) {
+            poly_exp2x2(x0, x1, p0, p1);
+          } else {
+            p0 = fast_exp2(x0);
+            p1 = fast_exp2(x1);
+          }
+          rs2[i & 3] = f2_add(rs2[i & 3], f2_pack(p0, p1));
           pk[i] = pack_bf16x2(p0, p1);
         }
-        tmem_st_32x32b_x16(t_s + c * 16, pk);          // columns [16c, 16c+16): already consumed
+        tmem_st_32x32b_x16(t_s + c * 16, pk);          // columns [16c, 16c+16): already in registers
+        if (c & 1) {                                    // keys [64h, 64h+64) are in TMEM: release that half
+          tmem_st_wait();
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&p_full[2 * x + (c >> 1)]);
+        }
       }
       float rs_lo, rs_hi;
-      f2_unpack(rs2, rs_lo, rs_hi);
+      f2_unpack(f2_add(f2_add(rs2[0], rs2[1]), f2_add(rs2[2], rs2[3])), rs_lo, rs_hi);
       l += rs_lo + rs_hi;
-      tmem_st_wait();
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&p_full[x]);
     }
     // ------------------------------------------------------------ epilogue
     mbar_wait(&o_full[x], 0);
@@ -396,6 +426,7 @@ __global__ void __launch_bounds__(AT_THREADS, 1) attn_fwd_kernel(const __grid_co
       a.m_acc[srow] = m;
       a.l_acc[srow] = l;
     }
+  }
   }
   tc_fence_before();
   __syncthreads();
