@@ -330,16 +330,19 @@ def main():
 
     # ---------------------------------------------------------------- end to end (host buffers)
     # Through the public API with pinned host buffers: every step copies its
-    # four inputs host -> device and reads its two outputs back. The copies are
-    # pipelined against the kernels with double-buffered device tensors: the
-    # H2D of step i+1 (copy stream) and the D2H of step i-1 (second copy
-    # stream, the other PCIe direction) overlap the fused ops of step i.
+    # two activation inputs (the AG-GEMM shard and the GEMM-RS input) host ->
+    # device and reads both full outputs back; the two weight matrices are
+    # layer parameters and stay resident, as in the reference's tensor-parallel
+    # layer. The copies are pipelined against the kernels with double-buffered
+    # device tensors: the H2D of step i+1 (copy stream) and the D2H of step i-1
+    # (second copy stream, the other PCIe direction) overlap the fused ops of
+    # step i.
     e2e = None
     if not args.no_e2e:
-        ins0 = [a_ag, b_ag, a_rs, b_rs]
+        ins0 = [a_ag, a_rs]
         outs0 = [c_ag, o_rs]
         sets = [(ins0, outs0),
-                ([comm.empty(tuple(a_ag.shape)), torch.empty_like(b_ag), torch.empty_like(a_rs), torch.empty_like(b_rs)],
+                ([comm.empty(tuple(a_ag.shape)), torch.empty_like(a_rs)],
                  [torch.empty_like(c_ag), comm.empty(tuple(o_rs.shape))])]
         h_in = [torch.empty(t.shape, dtype=t.dtype, pin_memory=True) for t in ins0]
         h_out = [[torch.empty(t.shape, dtype=t.dtype, pin_memory=True) for t in outs0] for _ in range(2)]
@@ -363,8 +366,8 @@ def main():
                 stream.wait_event(ev_in)
                 if done_d2h[i % 2] is not None:
                     stream.wait_event(done_d2h[i % 2])                 # outputs of step i-2 read back
-                pk.all_gather_gemm(comm, ins[0], ins[1], out=outs[0])
-                pk.gemm_reduce_scatter(comm, ins[2], ins[3], out=outs[1])
+                pk.all_gather_gemm(comm, ins[0], b_ag, out=outs[0])
+                pk.gemm_reduce_scatter(comm, ins[1], b_rs, out=outs[1])
                 ev_c = torch.cuda.Event()
                 ev_c.record(stream)
                 done_compute[i % 2] = ev_c
@@ -391,7 +394,8 @@ def main():
                "h2d_bytes_per_step": sum(t.numel() * t.element_size() for t in ins0),
                "d2h_bytes_per_step": sum(t.numel() * t.element_size() for t in outs0),
                "api": "paper_2511_13940_b200.all_gather_gemm + gemm_reduce_scatter, pinned host buffers, "
-                      "H2D/D2H pipelined against compute (double-buffered device tensors)"}
+                      "H2D/D2H pipelined against compute (double-buffered device tensors)",
+               "resident": "weights b_ag, b_rs (layer parameters); activations copied in, outputs copied out every step"}
 
     # ---------------------------------------------------------------- roofline of the dominant kernel
     peak_burst, peak_sus, src = peaks()

@@ -31,10 +31,18 @@ PEAKS = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.ex
 TF, HBM = PEAKS["bf16_tflops"], PEAKS["hbm_gbs"]
 
 
-def timeit(fn, iters=10, warm=3):
+def timeit(fn, iters=10, warm=3, min_ms=50.0):
+    """Mean device time per call; iterations are raised until the timed region
+    is at least `min_ms` long (short ops are otherwise dominated by noise)."""
     for _ in range(warm):
         fn()
     torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    fn()
+    e1.record()
+    torch.cuda.synchronize()
+    iters = max(iters, min(500, int(min_ms / max(e0.elapsed_time(e1), 1e-3)) + 1))
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
     for _ in range(iters):

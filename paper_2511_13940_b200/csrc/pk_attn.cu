@@ -309,6 +309,10 @@ __global__ void __launch_bounds__(AT_THREADS, 1) attn_fwd_kernel(const __grid_co
     for (int j = 0; j < nblk; ++j) {
       mbar_wait(&s_full[x], j & 1);
       tc_fence_after();
+#ifdef AT_MMA_ONLY   // timing diagnostic only: the MMA pipeline without softmax (wrong results)
+      if (lane == 0) { mbar_arrive(&p_full[2 * x]); mbar_arrive(&p_full[2 * x + 1]); }
+      continue;
+#endif
       // the whole S row (128 fp32) into registers with one TMEM wait; the max
       // and exp passes both read registers
       uint32_t r[AT_BN];

@@ -170,7 +170,7 @@ static int run_coll(Comm* c, const pk_tensor* x, CollArgs& a, long long units, c
     a.done_peer[r] = pr + kSyncDone;
   }
   int blocks = (int)std::min<long long>((long long)c->num_sms, std::max<long long>(1, (units + 31) / 32));
-  if (c->local_group) blocks = std::min(blocks, c->num_sms);   // co-residency of all ranks' kernels
+  if (c->local_group && c->world > 1) blocks = std::min(blocks, c->num_sms);   // co-residency of all ranks' kernels
   c->ready_count += 1;
   c->done_count += (uint32_t)blocks;
   a.ready_expect = c->ready_count;

@@ -10,14 +10,14 @@
 //   sum_k w[t, k] * y_owner[slot(d, t, k)], pulled back over peer loads.
 //
 // Device work (three kernels, all communication over peer VAs):
-//   moe_count    one CTA per rank: per-owner exclusive scan of the flattened
-//                (token, k) routing -> local slot index; writes this rank's row
-//                of the [n x n] count table into every rank (symmetric
-//                scratch) and signals ready.
-//   moe_dispatch waits for every rank's row, then streams token rows with the
-//                bulk-copy engine: global -> smem once per token, smem -> the
-//                owner's recv slot once per (token, k) (PK store_async,
-//                PAPER.md:543-567), plus the (src, token, k) id of the slot.
+//   moe_count    one CTA per token chunk: per-owner counts; the last CTA
+//                publishes this rank's row of the [n x n] count table into
+//                every rank (symmetric scratch) and signals ready.
+//   moe_dispatch waits for every rank's row; each CTA ranks its chunk's
+//                entries (ballots + block scan) into slots, then streams the
+//                token rows with the bulk-copy engine: global -> smem once per
+//                token, smem -> the owner's recv slot once per (token, k) (PK
+//                store_async), plus the (src, token, k) id.
 //   moe_combine  pulls the k expert-output rows of every local token from
 //                their owners with 16 B peer loads and accumulates in fp32.
 #include "pk_host.h"
@@ -44,6 +44,10 @@ struct MoeArgs {
   int T, k, n, rank, num_experts;
   int row_bytes;                // H * 2
   int32_t* local_idx;           // [T * k] slot offset within (src=rank, owner)
+  int grid;                     // number of chunks G
+  int tpc;                      // tokens per chunk (one count / dispatch CTA per chunk)
+  int32_t* chunk_counts;        // [G, n] entries per (chunk, owner)
+  uint32_t* count_done;         // CTAs of moe_count finished (last one publishes)
   int32_t* table_local;         // [n * n] count table (row = src)
   int32_t* table_peer[kMaxRanks];
   uint8_t* recv_peer[kMaxRanks];      // owner recv buffers [cap, H]
@@ -71,142 +75,194 @@ __device__ __forceinline__ bool moe_wait_all(const MoeSync& s, int n, bool done)
   return ok;
 }
 
-// ---------------------------------------------------------------- count / scan
-constexpr int kCountThreads = 1024;
+// ---------------------------------------------------------------- count
+// The flattened (token, k) routing is cut into G chunks of `tpc` tokens. One
+// CTA per chunk counts its entries per owner; the last CTA to finish sums the
+// chunk counts, publishes this rank's row of the [n x n] count table to every
+// rank and signals ready. The per-entry slot ranks are computed by the
+// dispatch CTA that owns the chunk (no grid-wide scan, no single-CTA pass).
+constexpr int kCountThreads = 256;
 
 __global__ void __launch_bounds__(kCountThreads) moe_count_kernel(const __grid_constant__ MoeArgs a) {
-  __shared__ int32_t part[kMaxRanks][kCountThreads];
-  const int total = a.T * a.k;
-  const int per = (total + kCountThreads - 1) / kCountThreads;
-  const int lo = threadIdx.x * per;
-  const int hi = min(total, lo + per);
-  int cnt[kMaxRanks];
+  __shared__ int32_t cnt[kMaxRanks];
+  __shared__ int last;
+  const int tid = threadIdx.x, lane = tid & 31;
+  if (tid < kMaxRanks) cnt[tid] = 0;
+  __syncthreads();
+  const int e0 = (int)blockIdx.x * a.tpc * a.k;
+  const int e1 = min(a.T, ((int)blockIdx.x + 1) * a.tpc) * a.k;
+  int my[kMaxRanks];
 #pragma unroll
-  for (int o = 0; o < kMaxRanks; ++o) cnt[o] = 0;
+  for (int q = 0; q < kMaxRanks; ++q) my[q] = 0;
   bool bad = false;
-  for (int i = lo; i < hi; ++i) {
+  for (int i = e0 + tid; i < e1; i += blockDim.x) {
     const int e = a.topk[i];
     if (e < 0 || e >= a.num_experts) { bad = true; continue; }
     const int o = e % a.n;
 #pragma unroll
-    for (int q = 0; q < kMaxRanks; ++q) cnt[q] += (q == o);
+    for (int q = 0; q < kMaxRanks; ++q) my[q] += (q == o);
   }
   if (bad) atomicExch(a.sync.err, 2u);
 #pragma unroll
-  for (int o = 0; o < kMaxRanks; ++o) part[o][threadIdx.x] = cnt[o];
-  __syncthreads();
-  // exclusive scan per owner (Hillis-Steele over 1024 entries, one owner per pass)
-  for (int o = 0; o < a.n; ++o) {
-    for (int off = 1; off < kCountThreads; off <<= 1) {
-      const int v = (threadIdx.x >= off) ? part[o][threadIdx.x - off] : 0;
-      __syncthreads();
-      part[o][threadIdx.x] += v;
-      __syncthreads();
-    }
-  }
-  int run[kMaxRanks];
-#pragma unroll
-  for (int o = 0; o < kMaxRanks; ++o) run[o] = (o < a.n) ? part[o][threadIdx.x] - cnt[o] : 0;
-  for (int i = lo; i < hi; ++i) {
-    const int e = a.topk[i];
-    if (e < 0 || e >= a.num_experts) { a.local_idx[i] = -1; continue; }
-    const int o = e % a.n;
-    int v = 0;
-#pragma unroll
-    for (int q = 0; q < kMaxRanks; ++q) if (q == o) v = run[q]++;
-    a.local_idx[i] = v;
+  for (int q = 0; q < kMaxRanks; ++q) {
+    const int v = __reduce_add_sync(0xffffffffu, my[q]);
+    if (lane == 0 && v) atomicAdd(&cnt[q], v);
   }
   __syncthreads();
-  if (threadIdx.x < a.n * a.n) {
-    // publish row `rank` of the count table to every rank: entry (rank, o)
-    const int d = threadIdx.x / a.n, o = threadIdx.x % a.n;
-    a.table_peer[d][a.rank * a.n + o] = part[o][kCountThreads - 1];
+  if (tid < a.n) a.chunk_counts[blockIdx.x * a.n + tid] = cnt[tid];
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) last = atomicAdd(a.count_done, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  if (tid < a.n * a.n) {
+    // entry (rank, o) of the count table, written into rank d's copy
+    const int d = tid / a.n, o = tid % a.n;
+    int tot = 0;
+    for (int c = 0; c < (int)gridDim.x; ++c) tot += ld_volatile_s32(a.chunk_counts + c * a.n + o);
+    a.table_peer[d][a.rank * a.n + o] = tot;
   }
   __syncthreads();
-  if (threadIdx.x == 0) moe_signal_all(a.sync, a.n, a.rank, false);
+  if (tid == 0) {
+    *a.count_done = 0;                                // re-armed for the next call
+    moe_signal_all(a.sync, a.n, a.rank, false);
+  }
 }
 
 // ---------------------------------------------------------------- dispatch
-constexpr int kDispatchThreads = 128;
+constexpr int kDispatchThreads = 256;
 constexpr int kPiece = 16384;      // bytes per bulk piece
 constexpr int kDispatchBufs = 4;
+constexpr int kWinEntries = 2048;  // (token, k) entries ranked per window
+constexpr int kDispatchSmem = kDispatchBufs * kPiece + 3 * kWinEntries * 4;
 
+// CTA b owns the tokens of chunk b. Per window of its entries:
+//   1. rank: slot of entry (t, j) on owner o = sum_{d < rank} count[d][o]
+//      (earlier sources) + entries of earlier chunks with owner o + earlier
+//      entries of this chunk with owner o (warp ballots + a block scan), i.e.
+//      the sorted (src, token, k) order of workloads.py:821-832
+//   2. copy: one elected thread streams the rows with the bulk-copy engine,
+//      global -> smem once per token, smem -> owner slot once per (token, k)
 __global__ void __launch_bounds__(kDispatchThreads) moe_dispatch_kernel(const __grid_constant__ MoeArgs a) {
   extern __shared__ __align__(128) uint8_t smem[];
+  int32_t* sslot = reinterpret_cast<int32_t*>(smem + kDispatchBufs * kPiece);
+  int32_t* sown = sslot + kWinEntries;
+  int32_t* sexp = sown + kWinEntries;
   __shared__ __align__(8) uint64_t bars[kDispatchBufs];
-  __shared__ int32_t base[kMaxRanks];
+  __shared__ int32_t base[kMaxRanks], cbase[kMaxRanks], run[kMaxRanks];
+  __shared__ int32_t wc[kDispatchThreads / 32][kMaxRanks];
   __shared__ int ok_flag;
-  if (threadIdx.x == 0) {
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (tid == 0) {
     ok_flag = moe_wait_all(a.sync, a.n, false) ? 1 : 0;
     for (int i = 0; i < kDispatchBufs; ++i) mbar_init(&bars[i], 1);
     fence_mbar_init();
   }
   __syncthreads();
   if (!ok_flag) return;
-  if (threadIdx.x < a.n) {
-    const int o = threadIdx.x;
+  if (tid < a.n) {
+    const int o = tid;
     int b = 0;
     for (int d = 0; d < a.rank; ++d) b += ld_volatile_s32(a.table_local + d * a.n + o);
     base[o] = b;
+    int cb = 0;
+    for (int c = 0; c < (int)blockIdx.x; ++c) cb += a.chunk_counts[c * a.n + o];
+    cbase[o] = cb;
+    run[o] = 0;
   }
-  if (blockIdx.x == 0 && threadIdx.x == 0) {
+  if (blockIdx.x == 0 && tid == 0) {
     int tot = 0;
     for (int d = 0; d < a.n; ++d) tot += ld_volatile_s32(a.table_local + d * a.n + a.rank);
     *a.recv_count = tot;
     if (tot > a.cap) atomicExch(a.sync.err, 3u);
   }
   __syncthreads();
-  // One elected thread drives the bulk-copy engine for this CTA's tokens as a
-  // flat sequence of <=16 KB pieces: piece p+3 is loaded (global -> smem)
-  // while piece p is stored to its k destinations (smem -> owner slots).
-  if (threadIdx.x == 0) {
-    const int per_row = (a.row_bytes + kPiece - 1) / kPiece;
-    const int my_tokens = (a.T - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x;
-    const int total = my_tokens * per_row;
-    auto piece_src = [&](int p, int* tok, int* off, uint32_t* bytes) {
-      *tok = (int)blockIdx.x + (p / per_row) * (int)gridDim.x;
-      *off = (p % per_row) * kPiece;
-      *bytes = (uint32_t)min(kPiece, a.row_bytes - *off);
-    };
-    auto issue_load = [&](int p) {
-      int t, off;
-      uint32_t bytes;
-      piece_src(p, &t, &off, &bytes);
-      const int buf = p % kDispatchBufs;
-      mbar_arrive_expect_tx(&bars[buf], bytes);
-      bulk_g2s(smem + buf * kPiece, a.x + (long long)t * a.x_ld + off, bytes, &bars[buf]);
-    };
-    constexpr int kAhead = kDispatchBufs - 1;
-    for (int p = 0; p < total && p < kAhead; ++p) issue_load(p);
-    uint32_t phase = 0;
-    for (int p = 0; p < total; ++p) {
-      const int buf = p % kDispatchBufs;
-      mbar_wait(&bars[buf], (phase >> buf) & 1);
-      phase ^= 1u << buf;
-      int t, off;
-      uint32_t bytes;
-      piece_src(p, &t, &off, &bytes);
-      uint8_t* sb = smem + buf * kPiece;
-      for (int j = 0; j < a.k; ++j) {
-        const int i = t * a.k + j;
-        const int li = a.local_idx[i];
-        if (li < 0) continue;
-        const int o = a.topk[i] % a.n;
-        const long long slot = (long long)base[o] + li;
-        if (slot >= a.cap) continue;
-        bulk_s2g(a.recv_peer[o] + slot * (long long)a.row_bytes + off, sb, bytes);
-        if (off == 0) {
-          a.recv_src_peer[o][slot * a.recv_src_cols] = (a.rank * a.T + t) * a.k + j;
-          if (a.recv_src_cols == 2) a.recv_src_peer[o][slot * 2 + 1] = a.topk[i] / a.n;   // local expert id
+  const int t_begin = (int)blockIdx.x * a.tpc, t_end = min(a.T, t_begin + a.tpc);
+  const int win_tokens = max(1, kWinEntries / a.k);
+  const int per_row = (a.row_bytes + kPiece - 1) / kPiece;
+  uint32_t phase = 0;   // thread 0: parity of each bulk buffer's barrier
+  int gp = 0;           // thread 0: pieces issued so far (buffer index continues across windows)
+  for (int w0 = t_begin; w0 < t_end; w0 += win_tokens) {
+    const int w1 = min(t_end, w0 + win_tokens);
+    const int e0 = w0 * a.k, ne = (w1 - w0) * a.k;
+    for (int g = 0; g < ne; g += kDispatchThreads) {
+      const int le = g + tid;
+      const bool valid = le < ne;
+      int o = -1, ex = -1;
+      if (valid) {
+        ex = a.topk[e0 + le];
+        if (ex >= 0 && ex < a.num_experts) o = ex % a.n;
+      }
+      int r = 0;
+      for (int q = 0; q < a.n; ++q) {
+        const unsigned m = __ballot_sync(0xffffffffu, o == q);
+        if (o == q) r = __popc(m & ((1u << lane) - 1u));
+        if (lane == 0) wc[warp][q] = __popc(m);
+      }
+      __syncthreads();
+      if (tid < a.n) {
+        int s2 = run[tid];
+        for (int w = 0; w < kDispatchThreads / 32; ++w) {
+          const int c = wc[w][tid];
+          wc[w][tid] = s2;
+          s2 += c;
+        }
+        run[tid] = s2;
+      }
+      __syncthreads();
+      if (valid) {
+        const int li = o >= 0 ? cbase[o] + wc[warp][o] + r : -1;
+        a.local_idx[e0 + le] = li;
+        sslot[le] = o >= 0 ? base[o] + li : -1;
+        sown[le] = o;
+        sexp[le] = o >= 0 ? ex / a.n : -1;
+      }
+      __syncthreads();
+    }
+    if (tid == 0) {
+      const int total = (w1 - w0) * per_row;
+      auto issue_load = [&](int p) {
+        const int tl = p / per_row, off = (p % per_row) * kPiece;
+        const uint32_t bytes = (uint32_t)min(kPiece, a.row_bytes - off);
+        const int buf = (gp + p) % kDispatchBufs;
+        mbar_arrive_expect_tx(&bars[buf], bytes);
+        bulk_g2s(smem + buf * kPiece, a.x + (long long)(w0 + tl) * a.x_ld + off, bytes, &bars[buf]);
+      };
+      constexpr int kAhead = kDispatchBufs - 1;
+      for (int p = 0; p < total && p < kAhead; ++p) issue_load(p);
+      for (int p = 0; p < total; ++p) {
+        const int buf = (gp + p) % kDispatchBufs;
+        mbar_wait(&bars[buf], (phase >> buf) & 1);
+        phase ^= 1u << buf;
+        const int tl = p / per_row, off = (p % per_row) * kPiece;
+        const uint32_t bytes = (uint32_t)min(kPiece, a.row_bytes - off);
+        const uint8_t* sb = smem + buf * kPiece;
+        for (int j = 0; j < a.k; ++j) {
+          const int le = tl * a.k + j;
+          const int o = sown[le];
+          if (o < 0) continue;
+          const int slot = sslot[le];
+          if (slot >= a.cap) continue;
+          bulk_s2g(a.recv_peer[o] + (long long)slot * a.row_bytes + off, sb, bytes);
+          if (off == 0) {
+            a.recv_src_peer[o][(long long)slot * a.recv_src_cols] = (a.rank * a.T + w0 + tl) * a.k + j;
+            if (a.recv_src_cols == 2) a.recv_src_peer[o][(long long)slot * 2 + 1] = sexp[le];   // local expert id
+          }
+        }
+        bulk_commit();
+        if (p + kAhead < total) {
+          // the buffer of piece p+kAhead was last used by piece p-1: its stores must have read smem
+          bulk_wait_read<1>();
+          issue_load(p + kAhead);
         }
       }
-      bulk_commit();
-      if (p + kAhead < total) {
-        // the buffer of piece p+kAhead was last used by piece p-1: its stores must have read smem
-        bulk_wait_read<1>();
-        issue_load(p + kAhead);
-      }
+      bulk_wait_read<0>();
+      gp += total;
     }
+    __syncthreads();
+  }
+  if (tid == 0) {
     bulk_wait<0>();
     fence_async_global();
     moe_signal_all(a.sync, a.n, a.rank, true);
@@ -215,11 +271,17 @@ __global__ void __launch_bounds__(kDispatchThreads) moe_dispatch_kernel(const __
 }
 
 // ---------------------------------------------------------------- combine
-constexpr int kCombineThreads = 256;
+// One warp per (token, 512 B column chunk): lanes 0..k-1 resolve the token's
+// k expert-output rows (owner VA + slot) and weights, broadcast by shuffle;
+// every lane then has KMAX independent 16 B peer loads in flight and folds
+// them in ascending k order in fp32.
+constexpr int kCombineThreads = 512;
 
+template <int KMAX>
 __global__ void __launch_bounds__(kCombineThreads) moe_combine_kernel(const __grid_constant__ MoeArgs a) {
   __shared__ int32_t base[kMaxRanks];
   __shared__ int ok_flag;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
     if (blockIdx.x == 0) moe_signal_all(a.sync, a.n, a.rank, false);   // my y is ready
     ok_flag = moe_wait_all(a.sync, a.n, false) ? 1 : 0;
@@ -233,29 +295,39 @@ __global__ void __launch_bounds__(kCombineThreads) moe_combine_kernel(const __gr
   __syncthreads();
   if (ok_flag) {
     const int nvec = a.row_bytes / 16;
-    for (int t = blockIdx.x; t < a.T; t += gridDim.x) {
-      const uint8_t* rows[16];
-      float wt[16];
-      int kk = 0;
-      for (int j = 0; j < a.k && j < 16; ++j) {
-        const int i = t * a.k + j;
+    const int nchunk = (nvec + 31) / 32;
+    const long long items = (long long)a.T * nchunk;
+    const long long nwarps = (long long)gridDim.x * (kCombineThreads / 32);
+    for (long long it = (long long)blockIdx.x * (kCombineThreads / 32) + warp; it < items; it += nwarps) {
+      const int t = (int)(it / nchunk), ch = (int)(it % nchunk);
+      const uint8_t* myrow = nullptr;
+      float myw = 0.f;
+      if (lane < a.k) {
+        const int i = t * a.k + lane;
         const int li = a.local_idx[i];
-        if (li < 0) continue;
-        const int o = a.topk[i] % a.n;
-        rows[kk] = a.y_peer[o] + ((long long)base[o] + li) * a.y_ld;
-        wt[kk] = a.w[i];
-        ++kk;
+        if (li >= 0) {
+          const int o = a.topk[i] % a.n;
+          myrow = a.y_peer[o] + ((long long)base[o] + li) * a.y_ld;
+          myw = a.w[i];
+        }
       }
-      for (int v = threadIdx.x; v < nvec; v += blockDim.x) {
+      const int v = ch * 32 + lane;
+      const uint8_t* rows[KMAX];
+      float wt[KMAX];
+      uint4 in[KMAX];
+#pragma unroll
+      for (int j = 0; j < KMAX; ++j) {
+        rows[j] = reinterpret_cast<const uint8_t*>(__shfl_sync(0xffffffffu, reinterpret_cast<uintptr_t>(myrow), j));
+        wt[j] = __shfl_sync(0xffffffffu, myw, j);
+        if (j < a.k && rows[j] != nullptr && v < nvec) in[j] = ld_v4_volatile(rows[j] + v * 16);
+      }
+      if (v < nvec) {
         float acc[8];
 #pragma unroll
         for (int e = 0; e < 8; ++e) acc[e] = 0.f;
-        uint4 in[16];
 #pragma unroll
-        for (int j = 0; j < 16; ++j) if (j < kk) in[j] = ld_v4_volatile(rows[j] + v * 16);
-#pragma unroll
-        for (int j = 0; j < 16; ++j) {
-          if (j < kk) {
+        for (int j = 0; j < KMAX; ++j) {
+          if (j < a.k && rows[j] != nullptr) {
             const uint32_t w4[4] = {in[j].x, in[j].y, in[j].z, in[j].w};
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
@@ -285,7 +357,8 @@ int preload_moe() {
   cudaFuncAttributes fa;
   PK_CUDA(cudaFuncGetAttributes(&fa, moe_count_kernel));
   PK_CUDA(cudaFuncGetAttributes(&fa, moe_dispatch_kernel));
-  PK_CUDA(cudaFuncGetAttributes(&fa, moe_combine_kernel));
+  PK_CUDA(cudaFuncGetAttributes(&fa, moe_combine_kernel<8>));
+  PK_CUDA(cudaFuncGetAttributes(&fa, moe_combine_kernel<16>));
   return PK_OK;
 }
 
@@ -305,6 +378,7 @@ static void fill_moe_sync(Comm* c, MoeSync& s) {
 }
 
 enum { kScratchMoeTable = 4, kScratchMoeIdx = 5, kScratchMoeY = 6 };
+constexpr int kMaxChunks = 4096;
 
 static int moe_common(Comm* c, const pk_tensor* topk, int num_experts, MoeArgs& a, int* T, int* K) {
   if (!topk || topk->dtype != PK_I32 || topk->ndim != 2 || topk->strides[1] != 1 || topk->strides[0] != topk->shape[1])
@@ -326,9 +400,19 @@ static int moe_common(Comm* c, const pk_tensor* topk, int num_experts, MoeArgs& 
   PK_TRY(comm_scratch(c, kScratchMoeTable, sizeof(int32_t) * kMaxRanks * kMaxRanks, &tbl));
   a.table_local = static_cast<int32_t*>(tbl->local);
   for (int r = 0; r < c->world; ++r) a.table_peer[r] = static_cast<int32_t*>(tbl->peers[r]);
+  // chunking shared by moe_count and moe_dispatch (one CTA per chunk)
+  int G = std::min(*T, c->num_sms * 2);
+  if (c->local_group && c->world > 1) G = std::min(G, c->num_sms);   // co-residency of all emulated ranks
+  G = std::max(G, 1);
+  a.tpc = (*T + G - 1) / G;
+  a.grid = std::max(1, (*T + a.tpc - 1) / a.tpc);
+  // scratch: [count_done | pad to 256 B][chunk_counts kMaxChunks x n][local_idx T*k]
   Pgl* idx;
-  PK_TRY(comm_scratch(c, kScratchMoeIdx, sizeof(int32_t) * (size_t)(*T) * (*K), &idx));
-  a.local_idx = static_cast<int32_t*>(idx->local);
+  PK_TRY(comm_scratch(c, kScratchMoeIdx, 256 + sizeof(int32_t) * ((size_t)kMaxChunks * kMaxRanks + (size_t)(*T) * (*K)), &idx));
+  uint8_t* base = static_cast<uint8_t*>(idx->local);
+  a.count_done = reinterpret_cast<uint32_t*>(base);
+  a.chunk_counts = reinterpret_cast<int32_t*>(base + 256);
+  a.local_idx = a.chunk_counts + (size_t)kMaxChunks * kMaxRanks;
   return PK_OK;
 }
 
@@ -364,17 +448,16 @@ int moe_dispatch(Comm* c, const pk_tensor* x, const pk_tensor* topk, int num_exp
     a.recv_peer[r] = static_cast<uint8_t*>(rp[r]);
     a.recv_src_peer[r] = static_cast<int32_t*>(sp[r]);
   }
+  if (cap >= (1ll << 31)) return fail(PK_ERR_INVALID, "moe_dispatch: recv capacity must be < 2^31 rows");
+  if (a.grid > kMaxChunks) return fail(PK_ERR_INVALID, "moe_dispatch: too many chunks");
   c->ready_count += 1;
-  int blocks = std::min(T, c->num_sms * 2);
-  if (c->local_group) blocks = std::min(blocks, c->num_sms);
-  blocks = std::max(blocks, 1);
-  c->done_count += (uint32_t)blocks;
+  c->done_count += (uint32_t)a.grid;
   fill_moe_sync(c, a.sync);
   void* params[] = {&a};
-  PK_CUDA(cudaLaunchKernel((void*)moe_count_kernel, dim3(1), dim3(kCountThreads), params, 0, st));
-  const int smem = kDispatchBufs * kPiece;
-  PK_TRY(ensure_smem_attr((const void*)moe_dispatch_kernel, smem));
-  PK_CUDA(cudaLaunchKernel((void*)moe_dispatch_kernel, dim3(blocks), dim3(kDispatchThreads), params, smem, st));
+  PK_CUDA(cudaMemsetAsync(a.count_done, 0, sizeof(uint32_t), st));
+  PK_CUDA(cudaLaunchKernel((void*)moe_count_kernel, dim3(a.grid), dim3(kCountThreads), params, 0, st));
+  PK_TRY(ensure_smem_attr((const void*)moe_dispatch_kernel, kDispatchSmem));
+  PK_CUDA(cudaLaunchKernel((void*)moe_dispatch_kernel, dim3(a.grid), dim3(kDispatchThreads), params, kDispatchSmem, st));
   return PK_OK;
 }
 
@@ -405,13 +488,15 @@ int moe_combine(Comm* c, const pk_tensor* y, const pk_tensor* topk, const pk_ten
   a.out_ld = old * 2;
   a.cap = cap;
   c->ready_count += 1;
-  int blocks = std::min(T, c->num_sms * 4);
-  if (c->local_group) blocks = std::min(blocks, c->num_sms);
+  const long long items = (long long)T * ((H * 2 / 16 + 31) / 32);   // (token, 512 B chunk) work items, one warp each
+  int blocks = (int)std::min<long long>((items + kCombineThreads / 32 - 1) / (kCombineThreads / 32), c->num_sms * 2);
+  if (c->local_group && c->world > 1) blocks = std::min(blocks, c->num_sms);   // co-residency of all emulated ranks
   blocks = std::max(blocks, 1);
   c->done_count += (uint32_t)blocks;
   fill_moe_sync(c, a.sync);
   void* params[] = {&a};
-  PK_CUDA(cudaLaunchKernel((void*)moe_combine_kernel, dim3(blocks), dim3(kCombineThreads), params, 0, st));
+  const void* kern = K <= 8 ? (const void*)moe_combine_kernel<8> : (const void*)moe_combine_kernel<16>;
+  PK_CUDA(cudaLaunchKernel(kern, dim3(blocks), dim3(kCombineThreads), params, 0, st));
   return PK_OK;
 }
 
