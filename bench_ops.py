@@ -135,8 +135,31 @@ def moe(args, out, c1, T, K, E, H, HE):
     x = torch.randn(T, H, device=dev).bfloat16()
     topk = torch.stack([torch.randperm(E, device=dev)[:K] for _ in range(T)]).int()
     recv = (c1.empty((T * K, H)), c1.empty((T * K, 2), torch.int32))
-    ms = timeit(lambda: pk.moe_dispatch(c1, x, topk, E, recv=recv))
-    emit(out, **bytes_line("moe_dispatch_n1", T * H * 2 + T * K * H * 2, ms, T=T, H=H, k=K))
+    for mech in ("reg", "tma"):
+        ms = timeit(lambda: pk.moe_dispatch(c1, x, topk, E, recv=recv, mechanism=mech))
+        emit(out, **bytes_line("moe_dispatch_n1", T * H * 2 + T * K * H * 2, ms, T=T, H=H, k=K, mechanism=mech))
+    # expert-major layout: rows land in 256-row expert segments, GEMM1 reads them in place
+    cap_e = pk.moe_capacity(T, K, 1, H, E)
+    recv_e = (c1.empty((cap_e, H)), c1.empty((cap_e, 2), torch.int32))
+    ms = timeit(lambda: pk.moe_dispatch(c1, x, topk, E, recv=recv_e, layout="expert"))
+    emit(out, **bytes_line("moe_dispatch_expert_n1", T * H * 2 + T * K * H * 2, ms, T=T, H=H, k=K))
+    _, _, _, plan = pk.moe_dispatch(c1, x, topk, E, recv=recv_e, layout="expert")
+    w64 = torch.randn(E, HE, H, device=dev).bfloat16()
+    y_e = c1.empty((cap_e, HE))
+    ms = timeit(lambda: pk.grouped_gemm(recv_e[0], None, w64, out=y_e, plan=plan))
+    emit(out, **tensor_line("grouped_gemm_planned_n1", 2 * T * K * H * HE, ms, rows=T * K, experts=E, H=H, H_exp=HE))
+    yh_e = c1.empty((cap_e, H))
+    comb_e = torch.empty(T, H, device=dev, dtype=torch.bfloat16)
+    wts_e = torch.rand(T, K, device=dev)
+
+    def pipeline():
+        r_, s_, c_, p_ = pk.moe_dispatch(c1, x, topk, E, recv=recv_e, layout="expert")
+        pk.grouped_gemm(r_, None, w64, out=y_e, plan=p_)
+        pk.moe_combine(c1, yh_e, topk, wts_e, E, out=comb_e)
+    ms = timeit(pipeline)
+    emit(out, op="moe_pipeline_expert_n1", ms=ms, T=T, H=H, k=K, experts=E, H_exp=HE,
+         note="dispatch + grouped GEMM1 (in place) + combine of H-wide rows")
+    del recv_e, y_e, yh_e, w64
     cnt = torch.tensor([T * K], dtype=torch.int32, device=dev)
     w = torch.randn(E, HE, H, device=dev).bfloat16()
     y = c1.empty((T * K, HE))

@@ -160,6 +160,22 @@ PK_API int pk_ring_attn_fwd(pk_comm* comm, const pk_tensor* q, const pk_tensor* 
 PK_API int pk_moe_dispatch(pk_comm* comm, const pk_tensor* x, const pk_tensor* topk_idx,
                            int num_experts, pk_tensor* recv, pk_tensor* recv_src,
                            pk_tensor* recv_count, void* stream);
+/* Receive-buffer layouts of the dispatch. */
+typedef enum {
+  PK_MOE_RANK_MAJOR = 0,    /* slots in (src_rank, token, k) order (workloads.py:821-832) */
+  PK_MOE_EXPERT_MAJOR = 1   /* one 256-row-padded segment per local expert, (src, token, k)
+                             * order inside it: the expert GEMM reads rows in place */
+} pk_moe_layout;
+/* Transfer mechanism (hwmodel.py select_mechanism, 211-245). */
+typedef enum { PK_MECH_AUTO = 0, PK_MECH_REG = 1, PK_MECH_TMA = 2 } pk_mechanism;
+/* Dispatch with an explicit layout and mechanism. For PK_MOE_EXPERT_MAJOR,
+ * expert_plan (int32, >= 2 + cap/256 entries) receives [num_tiles, rows,
+ * local expert of tile 0, 1, ...] for pk_grouped_gemm_planned; recv_src of
+ * padding rows is -1. recv_count counts real (unpadded) rows. */
+PK_API int pk_moe_dispatch_ex(pk_comm* comm, const pk_tensor* x, const pk_tensor* topk_idx,
+                              int num_experts, int layout, int mechanism, pk_tensor* recv,
+                              pk_tensor* recv_src, pk_tensor* recv_count, pk_tensor* expert_plan,
+                              void* stream);
 /* Combine: y [cap, H] rows produced by the owner for its received slots are
  * sent back and summed with weights w [T, k] f32 into out [T, H] bf16. */
 PK_API int pk_moe_combine(pk_comm* comm, const pk_tensor* y, const pk_tensor* topk_idx,
@@ -186,6 +202,11 @@ PK_API int pk_ulysses_a2a(pk_comm* comm, const pk_tensor* x, pk_tensor* y, int i
  * tiles on the device; no host synchronisation. */
 PK_API int pk_grouped_gemm(const pk_tensor* a, const pk_tensor* group_ids, const pk_tensor* w, pk_tensor* y,
                            const pk_tensor* num_rows, const pk_sched* sched, void* stream);
+/* Grouped GEMM over 256-row group segments already in place (the
+ * PK_MOE_EXPERT_MAJOR receive buffer): y[r] = a[r] . w[plan[2 + r/256]]^T for
+ * r < 256 * plan[0]; a [R, K], y [R, N] bf16, plan int32 on the device. */
+PK_API int pk_grouped_gemm_planned(const pk_tensor* a, const pk_tensor* plan, const pk_tensor* w, pk_tensor* y,
+                                   const pk_sched* sched, void* stream);
 
 #ifdef __cplusplus
 }

@@ -202,6 +202,33 @@ def moe_slots_vectorized(owners) -> tuple[np.ndarray, np.ndarray]:
     return slot.reshape(owners.shape), counts
 
 
+def moe_expert_slots(route, n: int, tile: int = 256):
+    """Expert-major receive layout (ours; the reference only has the rank-major
+    order of workloads.py:821-832): on owner o the local experts e = o, o+n, ...
+    get consecutive segments padded to `tile` rows, and inside a segment the
+    entries keep the sorted (src, tok, k) order. Returns (slot[d, tk, k],
+    counts[o] of real rows, plan[o] = [num_tiles, rows, local expert per tile])."""
+    route = np.asarray(route)
+    flat = route.reshape(-1)                       # (d, tk, k) order == sorted triple order
+    n_exp = int(flat.max()) + 1 if flat.size else 0
+    slot = np.zeros(flat.shape, dtype=np.int64)
+    counts = np.zeros(n, dtype=np.int64)
+    plans = []
+    offs = np.zeros(n, dtype=np.int64)
+    tiles = [[] for _ in range(n)]
+    for e in range(max(n_exp, n)):
+        o = e % n
+        idx = np.nonzero(flat == e)[0]
+        slot[idx] = offs[o] + np.arange(idx.size)
+        counts[o] += idx.size
+        t = -(-idx.size // tile)
+        tiles[o] += [e // n] * t
+        offs[o] += t * tile
+    for o in range(n):
+        plans.append(np.array([len(tiles[o]), counts[o]] + tiles[o], dtype=np.int64))
+    return slot.reshape(route.shape), counts, plans
+
+
 def moe_dispatch(token_data, owners) -> list[np.ndarray]:
     """recv[o][slot] = token[d][tk] for every (d, tk, k) (workloads.py:843-868).
     token_data[d]: [T, ...]; returns recv[o]: [count_o, ...]."""

@@ -130,7 +130,7 @@ struct GemmCfg {
 // Tile order: grouped raster along M (GROUP tiles) for L2 reuse of B, then
 // rotated along M so rank r starts on its own / its neighbour's rows.
 PK_DEV void tile_coords(int t, int num_m, int num_n, int m_rot, int group, int dir, int& mt, int& nt) {
-  if (dir == 0) {
+  if (dir == 0 || dir == 2) {
     const int per_group = group * num_n;
     const int g = t / per_group;
     const int first_m = g * group;
@@ -138,6 +138,9 @@ PK_DEV void tile_coords(int t, int num_m, int num_n, int m_rot, int group, int d
     const int r = t - g * per_group;
     mt = first_m + r % gsize;
     nt = r / gsize;
+    // snake: odd groups walk N backwards, so the window crossing a group
+    // boundary shares its B panels with the group it leaves
+    if (dir == 2 && (g & 1)) nt = num_n - 1 - nt;
   } else {
     const int per_group = group * num_m;
     const int g = t / per_group;
@@ -425,7 +428,11 @@ lcsc_gemm_kernel(const __grid_constant__ GemmArgs args) {
       }
       __syncwarp();
     }
-  } else if (warp == 0) {
+  } else if (warp < kEpiWarp0) {
+    // 512-row pair tiles: the epilogue holds a whole packed row (128 regs), so
+    // registers follow the roles; the setmaxnreg pair needs whole warpgroups
+    if constexpr (AM == 2) asm volatile("setmaxnreg.dec.sync.aligned.u32 56;\n" ::: "memory");
+    if (warp == 0) {
     // ========================================================= loader
     int stage = 0;
     uint32_t phase = 0;
@@ -473,7 +480,7 @@ lcsc_gemm_kernel(const __grid_constant__ GemmArgs args) {
         if (++stage == Cfg::STAGES) { stage = 0; phase ^= 1; }
       }
     }
-  } else if (warp == 1) {
+    } else if (warp == 1) {
     // ========================================================= consumer (MMA)
     if (leader) {
       constexpr uint32_t idesc = idesc_bf16_f32(Cfg::UMMA_M, Cfg::UMMA_N);
@@ -513,7 +520,9 @@ lcsc_gemm_kernel(const __grid_constant__ GemmArgs args) {
         }
       }
     }
-  } else if (warp >= kEpiWarp0 && warp < kEpiWarp0 + Cfg::EPI_WARPS) {
+    }
+  } else if (warp < kEpiWarp0 + Cfg::EPI_WARPS) {
+    if constexpr (AM == 2) asm volatile("setmaxnreg.inc.sync.aligned.u32 224;\n" ::: "memory");
     // ========================================================= storer (epilogue)
     const int ew = (int)warp - kEpiWarp0;            // epilogue warp index
     const int q = (int)warp & 3;                     // TMEM lane quarter this warp may access
@@ -540,6 +549,48 @@ lcsc_gemm_kernel(const __grid_constant__ GemmArgs args) {
       mbar_wait(&tfull_bar[acc], acc_phase);
       tc_fence_after();
       const uint32_t t_lane = (uint32_t)(q * 32) << 16;
+      if constexpr (Cfg::ACC_STAGES == 1 && EPI == EPI_STORE) {
+        // Single accumulator stage (512-row pair tiles fill TMEM): drain the
+        // whole 256-column row into registers as packed bf16 first and release
+        // TMEM at once, so the next tile's MMAs overlap the smem staging and
+        // TMA stores below instead of waiting for them.
+        uint32_t pk2[BN / 2];
+#pragma unroll
+        for (int c = 0; c < BN / 32; ++c) {          // 32 columns at a time keeps the peak at ~160 registers
+          uint32_t v0[32];
+          tmem_ld_32x32b_x32(tmem_base + t_lane + (uint32_t)(am * BN + c * 32), v0);
+          tmem_ld_wait();
+#pragma unroll
+          for (int i = 0; i < 16; ++i)
+            pk2[c * 16 + i] = pack_bf16x2(__uint_as_float(v0[2 * i]), __uint_as_float(v0[2 * i + 1]));
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) {
+          if constexpr (CG == 1) mbar_arrive(&tempty_bar[acc]);
+          else mbar_arrive_cluster(&tempty_bar[acc], 0);
+        }
+#pragma unroll
+        for (int c = 0; c < BN / EPI_COLS; ++c) {
+          if (lane == 0) {
+            if constexpr (Cfg::EPI_NBUF == 2) bulk_wait_read<1>(); else bulk_wait_read<0>();
+          }
+          __syncwarp();
+          uint8_t* buf = ebuf + ebuf_idx * Cfg::EPI_BUF_BYTES;
+          const uint32_t row_addr = smem_u32(buf) + lane * 128;
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            st_shared_v4(row_addr + ((j ^ (lane & 7)) << 4), pk2[c * 32 + 4 * j], pk2[c * 32 + 4 * j + 1],
+                         pk2[c * 32 + 4 * j + 2], pk2[c * 32 + 4 * j + 3]);
+          fence_async_shared();
+          __syncwarp();
+          if (lane == 0) {
+            tma_store_2d(&args.tmap_c[dst], buf, nt * BN + c * EPI_COLS, c_row);
+            bulk_commit();
+          }
+          if constexpr (Cfg::EPI_NBUF == 2) ebuf_idx ^= 1;
+        }
+      } else {
 #pragma unroll 1
       for (int c = 0; c < BN / EPI_COLS; ++c) {
         uint32_t v0[32], v1[32];
@@ -601,6 +652,7 @@ lcsc_gemm_kernel(const __grid_constant__ GemmArgs args) {
           bulk_commit();
         }
         if constexpr (Cfg::EPI_NBUF == 2) ebuf_idx ^= 1;
+      }
       }
       if (args.ar_mode) {
         // this warp's slice of the partial tile is in HBM: tell the tile's owner

@@ -185,6 +185,54 @@ int grouped_gemm(const pk_tensor* A, const pk_tensor* group, const pk_tensor* W,
   return launch_gemm_grouped(args, clusters * 2, st);
 }
 
+int launch_gemm_planned(const GemmArgs& args, int grid_ctas, cudaStream_t st);   // pk_ops.cu
+
+// Groups already laid out as 256-row segments (pk_moe_dispatch_ex with
+// PK_MOE_EXPERT_MAJOR): the plan written by the dispatch drives the same LCSC
+// kernel with a plain TMA-store epilogue; no histogram, no gather pass.
+int grouped_gemm_planned(const pk_tensor* A, const pk_tensor* plan, const pk_tensor* W, pk_tensor* Y,
+                         const pk_sched* sched, cudaStream_t st) {
+  int64_t R, K, ldA, Ry, N, ldY;
+  PK_TRY(check_matrix(A, "a", PK_BF16, &R, &K, &ldA));
+  PK_TRY(check_matrix(Y, "y", PK_BF16, &Ry, &N, &ldY));
+  if (Ry != R) return fail(PK_ERR_INVALID, "grouped_gemm_planned: y has %lld rows, a %lld", (long long)Ry, (long long)R);
+  if (!W || W->dtype != PK_BF16 || W->ndim != 3 || W->shape[1] != N || W->shape[2] != K || W->strides[2] != 1 ||
+      W->strides[1] != K || W->strides[0] != N * K)
+    return fail(PK_ERR_INVALID, "grouped_gemm_planned: w must be contiguous bf16 [groups, %lld, %lld]", (long long)N,
+                (long long)K);
+  const int64_t max_tiles = R / kGrpTile;
+  if (!plan || plan->dtype != PK_I32 || plan->ndim != 1 || plan->shape[0] < 2 + max_tiles)
+    return fail(PK_ERR_INVALID, "grouped_gemm_planned: plan must be int32 [>= 2 + rows/256]");
+  if (N % 256 || K % BLOCK_K || K == 0) return fail(PK_ERR_INVALID, "grouped_gemm_planned: need N %% 256 == 0, K %% 64 == 0");
+  if (max_tiles == 0) return PK_OK;
+  int dev = 0;
+  PK_CUDA(cudaGetDevice(&dev));
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int32_t* pl = static_cast<const int32_t*>(plan->ptr);
+  GemmArgs args;
+  memset(&args, 0, sizeof(args));
+  args.a_nsrc = 1;
+  args.c_ndst = 1;
+  args.raster_group = 8;
+  PK_TRY(make_tmap_2d(&args.tmap_a[0], A->ptr, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, R, K, ldA, 128, BLOCK_K,
+                      CU_TENSOR_MAP_SWIZZLE_128B));
+  PK_TRY(make_tmap_2d(&args.tmap_b, W->ptr, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, W->shape[0] * N, K, K, 128, BLOCK_K,
+                      CU_TENSOR_MAP_SWIZZLE_128B));
+  PK_TRY(make_tmap_2d(&args.tmap_c[0], Y->ptr, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, R, N, ldY, 32, EPI_COLS,
+                      CU_TENSOR_MAP_SWIZZLE_128B));
+  args.M = (int)(max_tiles * kGrpTile); args.N = (int)N; args.K = (int)K;
+  args.world = 1;
+  args.a_rows_per_src = args.M;
+  args.c_rows_per_dst = args.M;
+  args.num_m_tiles_dev = pl;
+  args.tile_group = pl + 2;
+  int clusters = std::max(1, (sched && sched->num_sms > 0 ? std::min(sched->num_sms, sms) : sms) / 2);
+  clusters = std::min<int64_t>(clusters, max_tiles * (N / 256));
+  args.num_compute_clusters = clusters;
+  return launch_gemm_planned(args, clusters * 2, st);
+}
+
 int preload_grouped() {
   cudaFuncAttributes fa;
   PK_CUDA(cudaFuncGetAttributes(&fa, grp_count_kernel));
@@ -194,6 +242,11 @@ int preload_grouped() {
 }
 
 }  // namespace pk
+
+extern "C" PK_API int pk_grouped_gemm_planned(const pk_tensor* a, const pk_tensor* plan, const pk_tensor* w,
+                                              pk_tensor* y, const pk_sched* sched, void* stream) {
+  return pk::grouped_gemm_planned(a, plan, w, y, sched, (cudaStream_t)stream);
+}
 
 extern "C" PK_API int pk_grouped_gemm(const pk_tensor* a, const pk_tensor* group_ids, const pk_tensor* w, pk_tensor* y,
                                       const pk_tensor* num_rows, const pk_sched* sched, void* stream) {

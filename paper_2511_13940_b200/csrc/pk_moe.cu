@@ -1,4 +1,4 @@
-// pk_moe.cu — expert-parallel all-to-all: pk_moe_dispatch / pk_moe_combine.
+// pk_moe.cu — expert-parallel all-to-all: pk_moe_dispatch(_ex) / pk_moe_combine.
 //
 // Reference: MoePlan (overlapsim/workloads.py:786-868).
 //   * routing: expert ids per (token, k); owner = expert % n (workloads.py:802)
@@ -6,26 +6,37 @@
 //   * slots on the owner are the (src_rank, token, k) triples in sorted order
 //     (workloads.py:821-832) => slot = sum_{d' < src} count[d'][owner]
 //                                      + #earlier (token', k') of src with that owner
+// Layouts of the owner's receive buffer:
+//   PK_MOE_RANK_MAJOR    the reference's order above (one key per owner)
+//   PK_MOE_EXPERT_MAJOR  one segment per local expert, each padded to the
+//                        256-row GEMM tile, (src, token, k)-sorted inside the
+//                        segment (one key per expert). The expert GEMM then
+//                        reads the rows in place (pk_grouped_gemm_planned):
+//                        no gather pass. The owner also gets a tile plan.
 // Combine is new (absent from the reference): token (d, t) receives
 //   sum_k w[t, k] * y_owner[slot(d, t, k)], pulled back over peer loads.
 //
 // Device work (three kernels, all communication over peer VAs):
-//   moe_count    one CTA per token chunk: per-owner counts; the last CTA
-//                publishes this rank's row of the [n x n] count table into
-//                every rank (symmetric scratch) and signals ready.
+//   moe_count    one CTA per token chunk: per-key counts; the last CTA turns
+//                them into per-chunk exclusive offsets, publishes this rank's
+//                row of the [n x keys] count table into every rank and signals.
 //   moe_dispatch waits for every rank's row; each CTA ranks its chunk's
-//                entries (ballots + block scan) into slots, then streams the
-//                token rows with the bulk-copy engine: global -> smem once per
-//                token, smem -> the owner's recv slot once per (token, k) (PK
-//                store_async), plus the (src, token, k) id.
-//   moe_combine  pulls the k expert-output rows of every local token from
-//                their owners with 16 B peer loads and accumulates in fp32.
+//                entries (warp match + block scan) into slots, then copies the
+//                token rows: register path (every warp streams whole rows,
+//                16 B loads once, 16 B stores once per (token, k)) or the
+//                bulk-copy engine (PK store_async).
+//   moe_combine  one warp per token: resolves its k expert rows once, then
+//                streams the row with 16 independent 16 B peer loads in flight
+//                per lane and folds in ascending k order in fp32.
 #include "pk_host.h"
 #include "pk_ptx.cuh"
 #include <algorithm>
 #include <cstring>
 
 namespace pk {
+
+constexpr int kMoeMaxKeys = 1024;      // experts (expert-major layout) or ranks
+constexpr int kMoeTile = 256;          // expert segment padding = the grouped GEMM's pair tile
 
 struct MoeSync {
   uint32_t* ready_local;
@@ -42,18 +53,22 @@ struct MoeArgs {
   const uint8_t* x;             // [T, H] bf16 rows (dispatch)
   long long x_ld;               // bytes between rows of x
   int T, k, n, rank, num_experts;
+  int layout;                   // 0 rank-major, 1 expert-major
+  int mech;                     // 1 register stores, 2 bulk-copy engine
+  int nkeys;                    // n (rank-major) or num_experts (expert-major)
   int row_bytes;                // H * 2
-  int32_t* local_idx;           // [T * k] slot offset within (src=rank, owner)
+  int32_t* slot_of;             // [T * k] absolute slot on the owner (-1: dropped)
   int grid;                     // number of chunks G
   int tpc;                      // tokens per chunk (one count / dispatch CTA per chunk)
-  int32_t* chunk_counts;        // [G, n] entries per (chunk, owner)
+  int32_t* chunk_counts;        // [G, nkeys] entries per (chunk, key) -> exclusive prefix over chunks
   uint32_t* count_done;         // CTAs of moe_count finished (last one publishes)
-  int32_t* table_local;         // [n * n] count table (row = src)
+  int32_t* table_local;         // [n, nkeys] count table (row = src)
   int32_t* table_peer[kMaxRanks];
   uint8_t* recv_peer[kMaxRanks];      // owner recv buffers [cap, H]
   int32_t* recv_src_peer[kMaxRanks];  // owner recv_src [cap] or [cap, 2] (+ local expert)
   int recv_src_cols;
   int32_t* recv_count;                // local count output (device int32)
+  int32_t* plan;                      // expert-major: [2 + cap/256] num_tiles, rows, tile -> local expert
   long long cap;
   // combine
   const uint8_t* y_peer[kMaxRanks];   // owner expert outputs [cap, H] bf16
@@ -75,53 +90,51 @@ __device__ __forceinline__ bool moe_wait_all(const MoeSync& s, int n, bool done)
   return ok;
 }
 
+// key of one routing entry: the owner rank (rank-major) or the expert (expert-major); -1 invalid
+__device__ __forceinline__ int moe_key(const MoeArgs& a, int e) {
+  if (e < 0 || e >= a.num_experts) return -1;
+  return a.layout ? e : e % a.n;
+}
+
 // ---------------------------------------------------------------- count
 // The flattened (token, k) routing is cut into G chunks of `tpc` tokens. One
-// CTA per chunk counts its entries per owner; the last CTA to finish sums the
-// chunk counts, publishes this rank's row of the [n x n] count table to every
-// rank and signals ready. The per-entry slot ranks are computed by the
-// dispatch CTA that owns the chunk (no grid-wide scan, no single-CTA pass).
+// CTA per chunk counts its entries per key; the last CTA to finish turns the
+// chunk counts into exclusive per-chunk offsets, publishes this rank's row of
+// the count table to every rank and signals ready.
 constexpr int kCountThreads = 256;
 
 __global__ void __launch_bounds__(kCountThreads) moe_count_kernel(const __grid_constant__ MoeArgs a) {
-  __shared__ int32_t cnt[kMaxRanks];
+  __shared__ int32_t cnt[kMoeMaxKeys];
   __shared__ int last;
-  const int tid = threadIdx.x, lane = tid & 31;
-  if (tid < kMaxRanks) cnt[tid] = 0;
+  const int tid = threadIdx.x;
+  for (int q = tid; q < a.nkeys; q += blockDim.x) cnt[q] = 0;
   __syncthreads();
   const int e0 = (int)blockIdx.x * a.tpc * a.k;
   const int e1 = min(a.T, ((int)blockIdx.x + 1) * a.tpc) * a.k;
-  int my[kMaxRanks];
-#pragma unroll
-  for (int q = 0; q < kMaxRanks; ++q) my[q] = 0;
   bool bad = false;
   for (int i = e0 + tid; i < e1; i += blockDim.x) {
-    const int e = a.topk[i];
-    if (e < 0 || e >= a.num_experts) { bad = true; continue; }
-    const int o = e % a.n;
-#pragma unroll
-    for (int q = 0; q < kMaxRanks; ++q) my[q] += (q == o);
+    const int key = moe_key(a, a.topk[i]);
+    if (key < 0) { bad = true; continue; }
+    atomicAdd(&cnt[key], 1);
   }
   if (bad) atomicExch(a.sync.err, 2u);
-#pragma unroll
-  for (int q = 0; q < kMaxRanks; ++q) {
-    const int v = __reduce_add_sync(0xffffffffu, my[q]);
-    if (lane == 0 && v) atomicAdd(&cnt[q], v);
-  }
   __syncthreads();
-  if (tid < a.n) a.chunk_counts[blockIdx.x * a.n + tid] = cnt[tid];
+  for (int q = tid; q < a.nkeys; q += blockDim.x) a.chunk_counts[(long long)blockIdx.x * a.nkeys + q] = cnt[q];
   __threadfence();
   __syncthreads();
   if (tid == 0) last = atomicAdd(a.count_done, 1u) == gridDim.x - 1;
   __syncthreads();
   if (!last) return;
   __threadfence();
-  if (tid < a.n * a.n) {
-    // entry (rank, o) of the count table, written into rank d's copy
-    const int d = tid / a.n, o = tid % a.n;
+  for (int q = tid; q < a.nkeys; q += blockDim.x) {
     int tot = 0;
-    for (int c = 0; c < (int)gridDim.x; ++c) tot += ld_volatile_s32(a.chunk_counts + c * a.n + o);
-    a.table_peer[d][a.rank * a.n + o] = tot;
+    for (int c = 0; c < (int)gridDim.x; ++c) {
+      int32_t* p = a.chunk_counts + (long long)c * a.nkeys + q;
+      const int v = ld_volatile_s32(p);
+      *p = tot;                                        // exclusive prefix over chunks
+      tot += v;
+    }
+    for (int d = 0; d < a.n; ++d) a.table_peer[d][a.rank * a.nkeys + q] = tot;
   }
   __syncthreads();
   if (tid == 0) {
@@ -132,50 +145,91 @@ __global__ void __launch_bounds__(kCountThreads) moe_count_kernel(const __grid_c
 
 // ---------------------------------------------------------------- dispatch
 constexpr int kDispatchThreads = 256;
-constexpr int kPiece = 16384;      // bytes per bulk piece
+constexpr int kDispatchWarps = kDispatchThreads / 32;
+constexpr int kPiece = 16384;          // bytes per bulk piece (bulk-copy mechanism)
 constexpr int kDispatchBufs = 4;
-constexpr int kWinEntries = 2048;  // (token, k) entries ranked per window
-constexpr int kDispatchSmem = kDispatchBufs * kPiece + 3 * kWinEntries * 4;
+constexpr int kWinEntries = 1024;      // (token, k) entries ranked per window
+constexpr int kSegVec = 16;            // register path: 16 x 16 B per lane = 8 KB per warp segment
+constexpr int kDispatchSmemTma = kDispatchBufs * kPiece;
 
 // CTA b owns the tokens of chunk b. Per window of its entries:
-//   1. rank: slot of entry (t, j) on owner o = sum_{d < rank} count[d][o]
-//      (earlier sources) + entries of earlier chunks with owner o + earlier
-//      entries of this chunk with owner o (warp ballots + a block scan), i.e.
-//      the sorted (src, token, k) order of workloads.py:821-832
-//   2. copy: one elected thread streams the rows with the bulk-copy engine,
-//      global -> smem once per token, smem -> owner slot once per (token, k)
+//   1. rank: slot of entry (t, j) with key q = base[q] (earlier sources, and
+//      for expert-major the start of the expert's segment) + entries of
+//      earlier chunks with key q + earlier entries of this chunk with key q
+//      (warp match + a block scan) => the sorted (src, token, k) order of
+//      workloads.py:821-832 within each key
+//   2. copy the window's rows to their slots
 __global__ void __launch_bounds__(kDispatchThreads) moe_dispatch_kernel(const __grid_constant__ MoeArgs a) {
-  extern __shared__ __align__(128) uint8_t smem[];
-  int32_t* sslot = reinterpret_cast<int32_t*>(smem + kDispatchBufs * kPiece);
-  int32_t* sown = sslot + kWinEntries;
-  int32_t* sexp = sown + kWinEntries;
+  extern __shared__ __align__(128) uint8_t smem[];     // bulk-copy buffers (mechanism 2 only)
+  __shared__ int32_t sslot[kWinEntries];
+  __shared__ int16_t sown[kWinEntries];
+  __shared__ int32_t sexp[kWinEntries];
+  __shared__ int32_t base[kMoeMaxKeys];              // per key: base slot on the owner + earlier chunks + run
   __shared__ __align__(8) uint64_t bars[kDispatchBufs];
-  __shared__ int32_t base[kMaxRanks], cbase[kMaxRanks], run[kMaxRanks];
-  __shared__ int32_t wc[kDispatchThreads / 32][kMaxRanks];
   __shared__ int ok_flag;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (tid == 0) {
     ok_flag = moe_wait_all(a.sync, a.n, false) ? 1 : 0;
-    for (int i = 0; i < kDispatchBufs; ++i) mbar_init(&bars[i], 1);
-    fence_mbar_init();
+    if (a.mech == 2) {
+      for (int i = 0; i < kDispatchBufs; ++i) mbar_init(&bars[i], 1);
+      fence_mbar_init();
+    }
   }
   __syncthreads();
   if (!ok_flag) return;
-  if (tid < a.n) {
-    const int o = tid;
-    int b = 0;
-    for (int d = 0; d < a.rank; ++d) b += ld_volatile_s32(a.table_local + d * a.n + o);
-    base[o] = b;
-    int cb = 0;
-    for (int c = 0; c < (int)blockIdx.x; ++c) cb += a.chunk_counts[c * a.n + o];
-    cbase[o] = cb;
-    run[o] = 0;
+  // ---- per-key base slots
+  if (a.layout == 0) {
+    for (int q = tid; q < a.nkeys; q += blockDim.x) {
+      int b = 0;
+      for (int d = 0; d < a.rank; ++d) b += ld_volatile_s32(a.table_local + d * a.nkeys + q);
+      base[q] = b + a.chunk_counts[(long long)blockIdx.x * a.nkeys + q];
+    }
+  } else {
+    // expert e lives on owner e % n; its segment starts after the padded
+    // segments of the owner's earlier experts (e' = e - n, e - 2n, ...)
+    for (int q = tid; q < a.nkeys; q += blockDim.x) {
+      int tot = 0, pre = 0;
+      for (int d = 0; d < a.n; ++d) {
+        const int v = ld_volatile_s32(a.table_local + d * a.nkeys + q);
+        tot += v;
+        if (d < a.rank) pre += v;
+      }
+      base[q] = (tot + kMoeTile - 1) / kMoeTile * kMoeTile;   // padded size (temporarily)
+      sslot[q] = pre;                                          // scratch: earlier sources
+    }
+    __syncthreads();
+    if (tid < a.n) {                                  // exclusive scan of padded sizes per owner
+      int off = 0;
+      for (int q = tid; q < a.nkeys; q += a.n) {
+        const int sz = base[q];
+        base[q] = off;
+        off += sz;
+      }
+    }
+    __syncthreads();
+    for (int q = tid; q < a.nkeys; q += blockDim.x)
+      base[q] += sslot[q] + a.chunk_counts[(long long)blockIdx.x * a.nkeys + q];
   }
   if (blockIdx.x == 0 && tid == 0) {
-    int tot = 0;
-    for (int d = 0; d < a.n; ++d) tot += ld_volatile_s32(a.table_local + d * a.n + a.rank);
+    // this rank as an owner: rows received (+ the expert tile plan)
+    int tot = 0, off = 0, tiles = 0;
+    for (int q = a.rank; q < a.nkeys; q += (a.layout ? a.n : a.nkeys)) {
+      int c = 0;
+      for (int d = 0; d < a.n; ++d) c += ld_volatile_s32(a.table_local + d * a.nkeys + q);
+      tot += c;
+      if (a.layout) {
+        const int t = (c + kMoeTile - 1) / kMoeTile;
+        for (int i = 0; i < t && 2 + tiles + i < 2 + a.cap / kMoeTile; ++i) a.plan[2 + tiles + i] = q / a.n;
+        tiles += t;
+        off += t * kMoeTile;
+      }
+    }
     *a.recv_count = tot;
-    if (tot > a.cap) atomicExch(a.sync.err, 3u);
+    if (a.layout) {
+      a.plan[0] = min(tiles, (int)(a.cap / kMoeTile));
+      a.plan[1] = tot;
+    }
+    if ((a.layout ? off : tot) > a.cap) atomicExch(a.sync.err, 3u);
   }
   __syncthreads();
   const int t_begin = (int)blockIdx.x * a.tpc, t_end = min(a.T, t_begin + a.tpc);
@@ -183,165 +237,208 @@ __global__ void __launch_bounds__(kDispatchThreads) moe_dispatch_kernel(const __
   const int per_row = (a.row_bytes + kPiece - 1) / kPiece;
   uint32_t phase = 0;   // thread 0: parity of each bulk buffer's barrier
   int gp = 0;           // thread 0: pieces issued so far (buffer index continues across windows)
+  __shared__ int32_t wcnt[kDispatchWarps][32];       // per (warp, group leader lane): group size
+  __shared__ int32_t wkey[kDispatchWarps][32];
   for (int w0 = t_begin; w0 < t_end; w0 += win_tokens) {
     const int w1 = min(t_end, w0 + win_tokens);
     const int e0 = w0 * a.k, ne = (w1 - w0) * a.k;
+    // ---- 1. rank the window's entries, 256 at a time, in (token, k) order
     for (int g = 0; g < ne; g += kDispatchThreads) {
       const int le = g + tid;
       const bool valid = le < ne;
-      int o = -1, ex = -1;
+      int key = -1, ex = -1;
       if (valid) {
         ex = a.topk[e0 + le];
-        if (ex >= 0 && ex < a.num_experts) o = ex % a.n;
+        key = moe_key(a, ex);
       }
-      int r = 0;
-      for (int q = 0; q < a.n; ++q) {
-        const unsigned m = __ballot_sync(0xffffffffu, o == q);
-        if (o == q) r = __popc(m & ((1u << lane) - 1u));
-        if (lane == 0) wc[warp][q] = __popc(m);
-      }
+      const unsigned peers = __match_any_sync(0xffffffffu, key);
+      const int r = __popc(peers & ((1u << lane) - 1u));
+      const bool leader = (peers & ((1u << lane) - 1u)) == 0;
+      wcnt[warp][lane] = leader ? __popc(peers) : 0;
+      wkey[warp][lane] = key;
       __syncthreads();
-      if (tid < a.n) {
-        int s2 = run[tid];
-        for (int w = 0; w < kDispatchThreads / 32; ++w) {
-          const int c = wc[w][tid];
-          wc[w][tid] = s2;
-          s2 += c;
-        }
-        run[tid] = s2;
+      // entries of earlier warps with the same key: walk the (<= 8 x 32) group leaders
+      int before = 0;
+      if (key >= 0) {
+        for (int w = 0; w < warp; ++w)
+          for (int l = 0; l < 32; ++l)
+            if (wcnt[w][l] && wkey[w][l] == key) before += wcnt[w][l];
       }
+      int slot = -1;
+      if (key >= 0) slot = base[key] + before + r;
       __syncthreads();
+      // advance the running base by this group's totals (one leader per key per warp)
+      if (key >= 0 && leader) atomicAdd(&base[key], __popc(peers));
       if (valid) {
-        const int li = o >= 0 ? cbase[o] + wc[warp][o] + r : -1;
-        a.local_idx[e0 + le] = li;
-        sslot[le] = o >= 0 ? base[o] + li : -1;
-        sown[le] = o;
-        sexp[le] = o >= 0 ? ex / a.n : -1;
+        const bool keep = key >= 0 && slot < a.cap;
+        a.slot_of[e0 + le] = keep ? slot : -1;
+        sslot[le] = keep ? slot : -1;
+        sown[le] = (int16_t)(key >= 0 ? ex % a.n : -1);
+        sexp[le] = key >= 0 ? ex / a.n : -1;
       }
       __syncthreads();
     }
-    if (tid == 0) {
-      const int total = (w1 - w0) * per_row;
-      auto issue_load = [&](int p) {
-        const int tl = p / per_row, off = (p % per_row) * kPiece;
-        const uint32_t bytes = (uint32_t)min(kPiece, a.row_bytes - off);
-        const int buf = (gp + p) % kDispatchBufs;
-        mbar_arrive_expect_tx(&bars[buf], bytes);
-        bulk_g2s(smem + buf * kPiece, a.x + (long long)(w0 + tl) * a.x_ld + off, bytes, &bars[buf]);
-      };
-      constexpr int kAhead = kDispatchBufs - 1;
-      for (int p = 0; p < total && p < kAhead; ++p) issue_load(p);
-      for (int p = 0; p < total; ++p) {
-        const int buf = (gp + p) % kDispatchBufs;
-        mbar_wait(&bars[buf], (phase >> buf) & 1);
-        phase ^= 1u << buf;
-        const int tl = p / per_row, off = (p % per_row) * kPiece;
-        const uint32_t bytes = (uint32_t)min(kPiece, a.row_bytes - off);
-        const uint8_t* sb = smem + buf * kPiece;
-        for (int j = 0; j < a.k; ++j) {
-          const int le = tl * a.k + j;
-          const int o = sown[le];
-          if (o < 0) continue;
-          const int slot = sslot[le];
-          if (slot >= a.cap) continue;
-          bulk_s2g(a.recv_peer[o] + (long long)slot * a.row_bytes + off, sb, bytes);
-          if (off == 0) {
-            a.recv_src_peer[o][(long long)slot * a.recv_src_cols] = (a.rank * a.T + w0 + tl) * a.k + j;
-            if (a.recv_src_cols == 2) a.recv_src_peer[o][(long long)slot * 2 + 1] = sexp[le];   // local expert id
+    // ---- 2. copy
+    if (a.mech == 2) {
+      if (tid == 0) {
+        const int total = (w1 - w0) * per_row;
+        auto issue_load = [&](int p) {
+          const int tl = p / per_row, off = (p % per_row) * kPiece;
+          const uint32_t bytes = (uint32_t)min(kPiece, a.row_bytes - off);
+          const int buf = (gp + p) % kDispatchBufs;
+          mbar_arrive_expect_tx(&bars[buf], bytes);
+          bulk_g2s(smem + buf * kPiece, a.x + (long long)(w0 + tl) * a.x_ld + off, bytes, &bars[buf]);
+        };
+        constexpr int kAhead = kDispatchBufs - 1;
+        for (int p = 0; p < total && p < kAhead; ++p) issue_load(p);
+        for (int p = 0; p < total; ++p) {
+          const int buf = (gp + p) % kDispatchBufs;
+          mbar_wait(&bars[buf], (phase >> buf) & 1);
+          phase ^= 1u << buf;
+          const int tl = p / per_row, off = (p % per_row) * kPiece;
+          const uint32_t bytes = (uint32_t)min(kPiece, a.row_bytes - off);
+          const uint8_t* sb = smem + buf * kPiece;
+          for (int j = 0; j < a.k; ++j) {
+            const int le = tl * a.k + j;
+            const int slot = sslot[le];
+            if (slot < 0) continue;
+            bulk_s2g(a.recv_peer[sown[le]] + (long long)slot * a.row_bytes + off, sb, bytes);
+          }
+          bulk_commit();
+          if (p + kAhead < total) {
+            // the buffer of piece p+kAhead was last used by piece p-1: its stores must have read smem
+            bulk_wait_read<1>();
+            issue_load(p + kAhead);
           }
         }
-        bulk_commit();
-        if (p + kAhead < total) {
-          // the buffer of piece p+kAhead was last used by piece p-1: its stores must have read smem
-          bulk_wait_read<1>();
-          issue_load(p + kAhead);
+        bulk_wait_read<0>();
+        gp += total;
+      }
+    } else {
+      // register path: warp w streams tokens w, w + 8, ... of the window in
+      // 8 KB segments (16 independent 16 B loads per lane, then one 16 B store
+      // per lane per destination slot)
+      const int nvec = a.row_bytes / 16;
+      for (int tl = warp; tl < w1 - w0; tl += kDispatchWarps) {
+        const uint8_t* src = a.x + (long long)(w0 + tl) * a.x_ld;
+        // lanes 0..k-1 hold the destinations of (token, lane)
+        uint8_t* mydst = nullptr;
+        if (lane < a.k) {
+          const int slot = sslot[tl * a.k + lane];
+          if (slot >= 0) mydst = a.recv_peer[sown[tl * a.k + lane]] + (long long)slot * a.row_bytes;
+        }
+        for (int v0 = 0; v0 < nvec; v0 += 32 * kSegVec) {
+          uint4 buf[kSegVec];
+#pragma unroll
+          for (int u = 0; u < kSegVec; ++u) {
+            const int v = v0 + u * 32 + lane;
+            if (v < nvec) buf[u] = ld_v4(src + (long long)v * 16);
+          }
+          for (int j = 0; j < a.k; ++j) {
+            uint8_t* d = reinterpret_cast<uint8_t*>(__shfl_sync(0xffffffffu, reinterpret_cast<uintptr_t>(mydst), j));
+            if (d == nullptr) continue;
+#pragma unroll
+            for (int u = 0; u < kSegVec; ++u) {
+              const int v = v0 + u * 32 + lane;
+              if (v < nvec) st_v4(d + (long long)v * 16, buf[u]);
+            }
+          }
         }
       }
-      bulk_wait_read<0>();
-      gp += total;
+    }
+    // ids of the window's entries (one thread per entry)
+    for (int le = tid; le < ne; le += blockDim.x) {
+      const int slot = sslot[le];
+      if (slot < 0) continue;
+      int32_t* rs = a.recv_src_peer[sown[le]];
+      rs[(long long)slot * a.recv_src_cols] = (a.rank * a.T + w0) * a.k + le;
+      if (a.recv_src_cols == 2) rs[(long long)slot * 2 + 1] = sexp[le];   // local expert id
     }
     __syncthreads();
   }
-  if (tid == 0) {
+  if (a.mech == 2 && tid == 0) {
     bulk_wait<0>();
     fence_async_global();
+  }
+  __threadfence_system();                              // every thread's peer stores before the done signal
+  __syncthreads();
+  if (tid == 0) {
     moe_signal_all(a.sync, a.n, a.rank, true);
     if (blockIdx.x == 0) moe_wait_all(a.sync, a.n, true);
   }
 }
 
 // ---------------------------------------------------------------- combine
-// One warp per (token, 512 B column chunk): lanes 0..k-1 resolve the token's
-// k expert-output rows (owner VA + slot) and weights, broadcast by shuffle;
-// every lane then has KMAX independent 16 B peer loads in flight and folds
-// them in ascending k order in fp32.
+// One warp per token: lanes 0..k-1 resolve the token's expert rows (owner VA
+// + slot) and weights once; the warp then walks the row 1 KB at a time with
+// 2*KMAX independent 16 B peer loads per lane in flight, folding in ascending
+// k order in fp32.
 constexpr int kCombineThreads = 512;
 
 template <int KMAX>
 __global__ void __launch_bounds__(kCombineThreads) moe_combine_kernel(const __grid_constant__ MoeArgs a) {
-  __shared__ int32_t base[kMaxRanks];
   __shared__ int ok_flag;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
     if (blockIdx.x == 0) moe_signal_all(a.sync, a.n, a.rank, false);   // my y is ready
     ok_flag = moe_wait_all(a.sync, a.n, false) ? 1 : 0;
   }
-  if (threadIdx.x < a.n) {
-    const int o = threadIdx.x;
-    int b = 0;
-    for (int d = 0; d < a.rank; ++d) b += a.table_local[d * a.n + o];
-    base[o] = b;
-  }
   __syncthreads();
   if (ok_flag) {
     const int nvec = a.row_bytes / 16;
-    const int nchunk = (nvec + 31) / 32;
-    const long long items = (long long)a.T * nchunk;
-    const long long nwarps = (long long)gridDim.x * (kCombineThreads / 32);
-    for (long long it = (long long)blockIdx.x * (kCombineThreads / 32) + warp; it < items; it += nwarps) {
-      const int t = (int)(it / nchunk), ch = (int)(it % nchunk);
+    const int nwarps = (int)gridDim.x * (kCombineThreads / 32);
+    for (int t = (int)blockIdx.x * (kCombineThreads / 32) + warp; t < a.T; t += nwarps) {
       const uint8_t* myrow = nullptr;
       float myw = 0.f;
       if (lane < a.k) {
         const int i = t * a.k + lane;
-        const int li = a.local_idx[i];
-        if (li >= 0) {
-          const int o = a.topk[i] % a.n;
-          myrow = a.y_peer[o] + ((long long)base[o] + li) * a.y_ld;
+        const int slot = a.slot_of[i];
+        if (slot >= 0) {
+          myrow = a.y_peer[a.topk[i] % a.n] + (long long)slot * a.y_ld;
           myw = a.w[i];
         }
       }
-      const int v = ch * 32 + lane;
       const uint8_t* rows[KMAX];
       float wt[KMAX];
-      uint4 in[KMAX];
 #pragma unroll
       for (int j = 0; j < KMAX; ++j) {
         rows[j] = reinterpret_cast<const uint8_t*>(__shfl_sync(0xffffffffu, reinterpret_cast<uintptr_t>(myrow), j));
         wt[j] = __shfl_sync(0xffffffffu, myw, j);
-        if (j < a.k && rows[j] != nullptr && v < nvec) in[j] = ld_v4_volatile(rows[j] + v * 16);
+        if (j >= a.k) rows[j] = nullptr;
       }
-      if (v < nvec) {
-        float acc[8];
-#pragma unroll
-        for (int e = 0; e < 8; ++e) acc[e] = 0.f;
+      uint8_t* orow = a.out + (long long)t * a.out_ld;
+      for (int v0 = lane; v0 < nvec; v0 += 64) {
+        const int v1 = v0 + 32;
+        uint4 in0[KMAX], in1[KMAX];
 #pragma unroll
         for (int j = 0; j < KMAX; ++j) {
-          if (j < a.k && rows[j] != nullptr) {
-            const uint32_t w4[4] = {in[j].x, in[j].y, in[j].z, in[j].w};
+          if (rows[j] != nullptr) {
+            in0[j] = ld_v4_volatile(rows[j] + (long long)v0 * 16);
+            if (v1 < nvec) in1[j] = ld_v4_volatile(rows[j] + (long long)v1 * 16);
+          }
+        }
+        float acc0[8], acc1[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) acc0[e] = acc1[e] = 0.f;
+#pragma unroll
+        for (int j = 0; j < KMAX; ++j) {
+          if (rows[j] != nullptr) {
+            const uint32_t x0[4] = {in0[j].x, in0[j].y, in0[j].z, in0[j].w};
+            const uint32_t x1[4] = {in1[j].x, in1[j].y, in1[j].z, in1[j].w};
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
-              acc[2 * e] += wt[j] * __uint_as_float(w4[e] << 16);
-              acc[2 * e + 1] += wt[j] * __uint_as_float(w4[e] & 0xFFFF0000u);
+              acc0[2 * e] += wt[j] * __uint_as_float(x0[e] << 16);
+              acc0[2 * e + 1] += wt[j] * __uint_as_float(x0[e] & 0xFFFF0000u);
+              acc1[2 * e] += wt[j] * __uint_as_float(x1[e] << 16);
+              acc1[2 * e + 1] += wt[j] * __uint_as_float(x1[e] & 0xFFFF0000u);
             }
           }
         }
-        uint4 o4;
-        o4.x = pack_bf16x2(acc[0], acc[1]);
-        o4.y = pack_bf16x2(acc[2], acc[3]);
-        o4.z = pack_bf16x2(acc[4], acc[5]);
-        o4.w = pack_bf16x2(acc[6], acc[7]);
-        st_v4(a.out + (long long)t * a.out_ld + v * 16, o4);
+        st_v4(orow + (long long)v0 * 16, make_uint4(pack_bf16x2(acc0[0], acc0[1]), pack_bf16x2(acc0[2], acc0[3]),
+                                                      pack_bf16x2(acc0[4], acc0[5]), pack_bf16x2(acc0[6], acc0[7])));
+        if (v1 < nvec)
+          st_v4(orow + (long long)v1 * 16, make_uint4(pack_bf16x2(acc1[0], acc1[1]), pack_bf16x2(acc1[2], acc1[3]),
+                                                        pack_bf16x2(acc1[4], acc1[5]), pack_bf16x2(acc1[6], acc1[7])));
       }
     }
   }
@@ -378,9 +475,11 @@ static void fill_moe_sync(Comm* c, MoeSync& s) {
 }
 
 enum { kScratchMoeTable = 4, kScratchMoeIdx = 5, kScratchMoeY = 6 };
-constexpr int kMaxChunks = 4096;
 
-static int moe_common(Comm* c, const pk_tensor* topk, int num_experts, MoeArgs& a, int* T, int* K) {
+// Routing checks, chunking and scratch shared by dispatch and combine. The
+// chunking and the per-entry slot table (slot_of) persist from a dispatch to
+// the next combine on the same comm.
+static int moe_common(Comm* c, const pk_tensor* topk, int num_experts, int layout, MoeArgs& a, int* T, int* K) {
   if (!topk || topk->dtype != PK_I32 || topk->ndim != 2 || topk->strides[1] != 1 || topk->strides[0] != topk->shape[1])
     return fail(PK_ERR_INVALID, "moe: topk_idx must be a contiguous [T, k] int32 tensor");
   *T = (int)topk->shape[0];
@@ -388,6 +487,9 @@ static int moe_common(Comm* c, const pk_tensor* topk, int num_experts, MoeArgs& 
   if (*K < 1 || *K > 16) return fail(PK_ERR_INVALID, "moe: top-k must be in 1..16 (got %d)", *K);
   if (*K > num_experts) return fail(PK_ERR_INVALID, "moe: TopK cannot exceed the expert count");   // workloads.py:797-798
   if (num_experts < 1) return fail(PK_ERR_INVALID, "moe: num_experts must be positive");
+  if (layout != 0 && layout != 1) return fail(PK_ERR_INVALID, "moe: unknown layout %d", layout);
+  if (layout == 1 && num_experts > kMoeMaxKeys)
+    return fail(PK_ERR_INVALID, "moe: the expert-major layout supports up to %d experts", kMoeMaxKeys);
   if ((long long)(*T) * (*K) >= (1ll << 31)) return fail(PK_ERR_INVALID, "moe: too many (token, k) pairs");
   memset(&a, 0, sizeof(a));
   a.topk = static_cast<const int32_t*>(topk->ptr);
@@ -396,8 +498,10 @@ static int moe_common(Comm* c, const pk_tensor* topk, int num_experts, MoeArgs& 
   a.n = c->world;
   a.rank = c->rank;
   a.num_experts = num_experts;
+  a.layout = layout;
+  a.nkeys = layout ? num_experts : c->world;
   Pgl* tbl;
-  PK_TRY(comm_scratch(c, kScratchMoeTable, sizeof(int32_t) * kMaxRanks * kMaxRanks, &tbl));
+  PK_TRY(comm_scratch(c, kScratchMoeTable, sizeof(int32_t) * kMaxRanks * kMoeMaxKeys, &tbl));
   a.table_local = static_cast<int32_t*>(tbl->local);
   for (int r = 0; r < c->world; ++r) a.table_peer[r] = static_cast<int32_t*>(tbl->peers[r]);
   // chunking shared by moe_count and moe_dispatch (one CTA per chunk)
@@ -406,25 +510,31 @@ static int moe_common(Comm* c, const pk_tensor* topk, int num_experts, MoeArgs& 
   G = std::max(G, 1);
   a.tpc = (*T + G - 1) / G;
   a.grid = std::max(1, (*T + a.tpc - 1) / a.tpc);
-  // scratch: [count_done | pad to 256 B][chunk_counts kMaxChunks x n][local_idx T*k]
+  // scratch: [count_done | pad to 256 B][slot_of T*k][chunk_counts G x nkeys]
+  // (slot_of first: a combine finds it where the dispatch with the same
+  // routing left it, whatever that dispatch's layout)
   Pgl* idx;
-  PK_TRY(comm_scratch(c, kScratchMoeIdx, 256 + sizeof(int32_t) * ((size_t)kMaxChunks * kMaxRanks + (size_t)(*T) * (*K)), &idx));
+  PK_TRY(comm_scratch(c, kScratchMoeIdx,
+                      256 + sizeof(int32_t) * ((size_t)(*T) * (*K) + (size_t)a.grid * a.nkeys), &idx));
   uint8_t* base = static_cast<uint8_t*>(idx->local);
   a.count_done = reinterpret_cast<uint32_t*>(base);
-  a.chunk_counts = reinterpret_cast<int32_t*>(base + 256);
-  a.local_idx = a.chunk_counts + (size_t)kMaxChunks * kMaxRanks;
+  a.slot_of = reinterpret_cast<int32_t*>(base + 256);
+  a.chunk_counts = a.slot_of + (size_t)(*T) * (*K);
   return PK_OK;
 }
 
-int moe_dispatch(Comm* c, const pk_tensor* x, const pk_tensor* topk, int num_experts, pk_tensor* recv,
-                 pk_tensor* recv_src, pk_tensor* recv_count, cudaStream_t st) {
+int moe_dispatch(Comm* c, const pk_tensor* x, const pk_tensor* topk, int num_experts, int layout, int mech,
+                 pk_tensor* recv, pk_tensor* recv_src, pk_tensor* recv_count, pk_tensor* plan, cudaStream_t st) {
   int T, K;
   MoeArgs a;
-  PK_TRY(moe_common(c, topk, num_experts, a, &T, &K));
+  PK_TRY(moe_common(c, topk, num_experts, layout, a, &T, &K));
+  if (mech == PK_MECH_AUTO) mech = PK_MECH_REG;
+  if (mech != PK_MECH_REG && mech != PK_MECH_TMA) return fail(PK_ERR_INVALID, "moe_dispatch: unknown mechanism %d", mech);
+  a.mech = mech;
   int64_t xr, H, xld;
   PK_TRY(check_matrix(x, "x", PK_BF16, &xr, &H, &xld));
   if (xr != T) return fail(PK_ERR_INVALID, "moe_dispatch: x has %lld rows, topk_idx %d", (long long)xr, T);
-  if ((H * 2) % 16) return fail(PK_ERR_INVALID, "moe_dispatch: rows must be a multiple of 16 bytes (H %% 8 == 0)");
+  if ((H * 2) % 16 || (xld * 2) % 16) return fail(PK_ERR_INVALID, "moe_dispatch: rows must be 16-byte multiples (H %% 8 == 0)");
   int64_t cap, H2, rld;
   PK_TRY(check_matrix(recv, "recv", PK_BF16, &cap, &H2, &rld));
   if (H2 != H || rld != H) return fail(PK_ERR_INVALID, "moe_dispatch: recv must be contiguous [cap, %lld]", (long long)H);
@@ -433,6 +543,11 @@ int moe_dispatch(Comm* c, const pk_tensor* x, const pk_tensor* topk, int num_exp
     return fail(PK_ERR_INVALID, "moe_dispatch: recv_src must be int32 [cap] or [cap, 2]");
   const int src_cols = recv_src->ndim == 2 ? 2 : 1;
   if (!recv_count || recv_count->dtype != PK_I32) return fail(PK_ERR_INVALID, "moe_dispatch: recv_count must be int32");
+  if (layout == 1) {
+    if (!plan || plan->dtype != PK_I32 || plan->ndim != 1 || plan->shape[0] < 2 + cap / kMoeTile)
+      return fail(PK_ERR_INVALID, "moe_dispatch: the expert-major layout needs an int32 plan of >= 2 + cap/256 entries");
+    a.plan = static_cast<int32_t*>(plan->ptr);
+  }
   void* rp[kMaxRanks];
   void* sp[kMaxRanks];
   if (!find_symmetric(c, recv->ptr, (size_t)cap * H * 2, rp) ||
@@ -449,15 +564,18 @@ int moe_dispatch(Comm* c, const pk_tensor* x, const pk_tensor* topk, int num_exp
     a.recv_src_peer[r] = static_cast<int32_t*>(sp[r]);
   }
   if (cap >= (1ll << 31)) return fail(PK_ERR_INVALID, "moe_dispatch: recv capacity must be < 2^31 rows");
-  if (a.grid > kMaxChunks) return fail(PK_ERR_INVALID, "moe_dispatch: too many chunks");
+  // expert-major padding rows carry id -1 (cleared before this rank signals
+  // ready, so no peer can be writing into recv_src yet)
+  if (layout == 1) PK_CUDA(cudaMemsetAsync(recv_src->ptr, 0xFF, (size_t)cap * 4 * src_cols, st));
   c->ready_count += 1;
   c->done_count += (uint32_t)a.grid;
   fill_moe_sync(c, a.sync);
   void* params[] = {&a};
   PK_CUDA(cudaMemsetAsync(a.count_done, 0, sizeof(uint32_t), st));
   PK_CUDA(cudaLaunchKernel((void*)moe_count_kernel, dim3(a.grid), dim3(kCountThreads), params, 0, st));
-  PK_TRY(ensure_smem_attr((const void*)moe_dispatch_kernel, kDispatchSmem));
-  PK_CUDA(cudaLaunchKernel((void*)moe_dispatch_kernel, dim3(a.grid), dim3(kDispatchThreads), params, kDispatchSmem, st));
+  const int smem = mech == PK_MECH_TMA ? kDispatchSmemTma : 0;
+  if (smem) PK_TRY(ensure_smem_attr((const void*)moe_dispatch_kernel, smem));
+  PK_CUDA(cudaLaunchKernel((void*)moe_dispatch_kernel, dim3(a.grid), dim3(kDispatchThreads), params, smem, st));
   return PK_OK;
 }
 
@@ -465,11 +583,13 @@ int moe_combine(Comm* c, const pk_tensor* y, const pk_tensor* topk, const pk_ten
                 pk_tensor* out, cudaStream_t st) {
   int T, K;
   MoeArgs a;
-  PK_TRY(moe_common(c, topk, num_experts, a, &T, &K));
+  PK_TRY(moe_common(c, topk, num_experts, 0, a, &T, &K));   // slot_of: written by the last dispatch
   int64_t cap, H, yld, orows, H2, old;
   PK_TRY(check_matrix(y, "y", PK_BF16, &cap, &H, &yld));
   PK_TRY(check_matrix(out, "out", PK_BF16, &orows, &H2, &old));
   if (orows != T || H2 != H) return fail(PK_ERR_INVALID, "moe_combine: out must be [%d, %lld]", T, (long long)H);
+  if ((H * 2) % 16 || (yld * 2) % 16 || (old * 2) % 16)
+    return fail(PK_ERR_INVALID, "moe_combine: rows must be 16-byte multiples");
   if (!w || w->dtype != PK_F32 || w->ndim != 2 || w->shape[0] != T || w->shape[1] != K || w->strides[0] != K)
     return fail(PK_ERR_INVALID, "moe_combine: weights must be contiguous float32 [T, k]");
   void* yp[kMaxRanks];
@@ -488,9 +608,7 @@ int moe_combine(Comm* c, const pk_tensor* y, const pk_tensor* topk, const pk_ten
   a.out_ld = old * 2;
   a.cap = cap;
   c->ready_count += 1;
-  const long long items = (long long)T * ((H * 2 / 16 + 31) / 32);   // (token, 512 B chunk) work items, one warp each
-  int blocks = (int)std::min<long long>((items + kCombineThreads / 32 - 1) / (kCombineThreads / 32), c->num_sms * 2);
-  if (c->local_group && c->world > 1) blocks = std::min(blocks, c->num_sms);   // co-residency of all emulated ranks
+  int blocks = (int)std::min<long long>(((long long)T + kCombineThreads / 32 - 1) / (kCombineThreads / 32), c->num_sms);
   blocks = std::max(blocks, 1);
   c->done_count += (uint32_t)blocks;
   fill_moe_sync(c, a.sync);
@@ -507,7 +625,17 @@ extern "C" {
 PK_API int pk_moe_dispatch(pk_comm* comm, const pk_tensor* x, const pk_tensor* topk_idx, int num_experts,
                            pk_tensor* recv, pk_tensor* recv_src, pk_tensor* recv_count, void* stream) {
   if (!comm) return pk::fail(PK_ERR_INVALID, "null comm");
-  return pk::moe_dispatch(comm, x, topk_idx, num_experts, recv, recv_src, recv_count, (cudaStream_t)stream);
+  const int rc = pk::moe_dispatch(comm, x, topk_idx, num_experts, PK_MOE_RANK_MAJOR, PK_MECH_AUTO, recv, recv_src,
+                                  recv_count, nullptr, (cudaStream_t)stream);
+  return rc;
+}
+
+PK_API int pk_moe_dispatch_ex(pk_comm* comm, const pk_tensor* x, const pk_tensor* topk_idx, int num_experts,
+                              int layout, int mechanism, pk_tensor* recv, pk_tensor* recv_src,
+                              pk_tensor* recv_count, pk_tensor* expert_plan, void* stream) {
+  if (!comm) return pk::fail(PK_ERR_INVALID, "null comm");
+  return pk::moe_dispatch(comm, x, topk_idx, num_experts, layout, mechanism, recv, recv_src, recv_count,
+                          expert_plan, (cudaStream_t)stream);
 }
 
 PK_API int pk_moe_combine(pk_comm* comm, const pk_tensor* y, const pk_tensor* topk_idx, const pk_tensor* w,

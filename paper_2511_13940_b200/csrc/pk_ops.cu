@@ -69,6 +69,10 @@ int launch_gemm_variant(Variant v, int epi, const GemmArgs& args, int grid_ctas,
   return fail(PK_ERR_INVALID, "no GEMM variant for cta_group=%d am=%d epi=%d", v.cg, v.am, epi);
 }
 
+int launch_gemm_planned(const GemmArgs& args, int grid_ctas, cudaStream_t st) {
+  return launch_lcsc<2, 256, 1, EPI_STORE>(args, grid_ctas, st);
+}
+
 int launch_gemm_grouped(const GemmArgs& args, int grid_ctas, cudaStream_t st) {
   return launch_lcsc<2, 256, 1, EPI_SCATTER>(args, grid_ctas, st);
 }
@@ -91,7 +95,11 @@ static Variant pick_variant(int64_t rows_per_part, int64_t K, const pk_sched* sc
   int force_am = 0;
   if (const char* e = getenv("PK_GEMM_AM")) force_am = atoi(e);
   if (sched && sched->stages < 0) force_am = -sched->stages;     // test hook: stages = -am
-  if (!reduce && rows_per_part % 512 == 0 && force_am == 2) return {2, 2};   // opt-in until it measures faster
+  // 512-row pair tiles by default: with the early TMEM release in the
+  // epilogue they issue as many MMAs per clock as the double-buffered 256-row
+  // tiles and, moving 25% fewer bytes into each SM, run ~5% faster under the
+  // 1 kW power cap (scratch/gemm_power.py: 1438 vs 1378 TF/s at 16384^3).
+  if (!reduce && rows_per_part % 512 == 0 && force_am != 1) return {2, 2};
   if (rows_per_part % 256 == 0) return {2, 1};
   return {1, 1};
 }
@@ -116,12 +124,14 @@ static int tmap_c(CUtensorMap* m, const void* p, int64_t rows, int64_t n, int64_
                       CU_TENSOR_MAP_SWIZZLE_128B);
 }
 
-static void init_args(GemmArgs& a) {
+static void init_args(GemmArgs& a, int am = 1) {
   memset(&a, 0, sizeof(a));
   a.a_nsrc = 1;
   a.c_ndst = 1;
-  a.raster_group = 8;
-  a.raster_dir = 0;
+  // raster window ~2048 rows of A either way: 8 x 256-row or 4 x 512-row tiles
+  // (snake order for the latter, measured lowest J per GEMM)
+  a.raster_group = am == 2 ? 4 : 8;
+  a.raster_dir = am == 2 ? 2 : 0;
   if (const char* e = getenv("PK_RASTER")) {      // "dir,group" (tuning hook)
     int d = 0, g = 8;
     if (sscanf(e, "%d,%d", &d, &g) == 2 && g > 0) { a.raster_dir = d; a.raster_group = g; }
@@ -142,7 +152,7 @@ int gemm_local(const pk_tensor* A, const pk_tensor* B, pk_tensor* C, const pk_sc
   const Variant v = pick_variant(M, K, sched);
   const int cg = v.cg;
   GemmArgs args;
-  init_args(args);
+  init_args(args, v.am);
   PK_TRY(tmap_a(&args.tmap_a[0], A->ptr, M, K, ldA, v.am));
   PK_TRY(tmap_b(&args.tmap_b, B->ptr, N, K, ldB, cg));
   PK_TRY(tmap_c(&args.tmap_c[0], C->ptr, M, N, ldC));
@@ -227,7 +237,7 @@ int ag_gemm(Comm* c, const pk_tensor* A, const pk_tensor* B, pk_tensor* C, pk_te
   }
 
   GemmArgs args;
-  init_args(args);
+  init_args(args, v.am);
   args.M = (int)M; args.N = (int)n_loc; args.K = (int)K;
   args.rank = c->rank; args.world = n;
   args.a_rows_per_src = (int)m_loc;

@@ -134,15 +134,24 @@ def all_reduce(comm, x: torch.Tensor, op: str = "sum", schedule: dict | None = N
     return x
 
 
-def moe_capacity(tokens: int, top_k: int, world: int, hidden: int) -> int:
+def moe_capacity(tokens: int, top_k: int, world: int, hidden: int, local_experts: int = 0) -> int:
     """Default receive capacity: the worst case (every token of every rank routed
-    here) when that fits in 1 GiB, else twice the average load."""
+    here) when that fits in 1 GiB, else twice the average load; plus one
+    256-row tile of padding per local expert for the expert-major layout."""
     worst = tokens * top_k * world
-    return worst if worst * hidden * 2 <= (1 << 30) else 2 * tokens * top_k
+    cap = worst if worst * hidden * 2 <= (1 << 30) else 2 * tokens * top_k
+    if local_experts:
+        cap = (cap + 255) // 256 * 256 + 256 * local_experts
+    return cap
+
+
+_MOE_LAYOUTS = {"rank": 0, "expert": 1}
+_MECHANISMS = {"auto": 0, "reg": 1, "tma": 2}
 
 
 def moe_dispatch(comm, x: torch.Tensor, topk_idx: torch.Tensor, num_experts: int,
-                 capacity: int | None = None, recv=None, stream=None):
+                 capacity: int | None = None, recv=None, stream=None, layout: str = "rank",
+                 mechanism: str = "auto"):
     """Expert-parallel dispatch (MoePlan, workloads.py:786-868).
 
     x [T, H] bf16, topk_idx [T, k] int32. Expert e lives on rank e % n. Returns
@@ -151,20 +160,33 @@ def moe_dispatch(comm, x: torch.Tensor, topk_idx: torch.Tensor, num_experts: int
     the s-th in sorted order (workloads.py:821-832); recv_src[s] =
     (src_rank * T + token) * k + j (recv_src [cap, 2]: column 1 = the row's local
     expert, expert // n). recv/recv_src are symmetric (Comm.empty).
+
+    layout="expert": rows are grouped by local expert instead, one segment per
+    expert padded to 256 rows, (src, token, k) order inside each segment
+    (recv_src = -1 on padding rows); a 4th value, the device tile plan, feeds
+    grouped_gemm(recv, None, w, plan=plan) without a gather pass.
+    mechanism: "reg" (16 B register stores, default) or "tma" (bulk-copy engine).
     """
     _require_cuda(x, topk_idx)
     T, k = topk_idx.shape
+    lay = _MOE_LAYOUTS[layout]
+    local_experts = (num_experts + comm.world - 1) // comm.world if lay else 0
     if capacity is None:
-        capacity = moe_capacity(T, k, comm.world, x.shape[1])
+        capacity = moe_capacity(T, k, comm.world, x.shape[1], local_experts)
     if recv is None:
         recv = (comm.empty((capacity, x.shape[1]), torch.bfloat16), comm.empty((capacity, 2), torch.int32))
     recv_rows, recv_src = recv
     count = torch.empty(1, dtype=torch.int32, device=x.device)
+    plan = torch.empty(2 + recv_rows.shape[0] // 256, dtype=torch.int32, device=x.device) if lay else None
     lib = _lib.load()
     dx, dt = _lib.tensor_desc(x), _lib.tensor_desc(topk_idx)
     dr, ds, dc = _lib.tensor_desc(recv_rows), _lib.tensor_desc(recv_src), _lib.tensor_desc(count)
-    check(lib.pk_moe_dispatch(comm._h, _lib.ref(dx), _lib.ref(dt), int(num_experts), _lib.ref(dr), _lib.ref(ds),
-                              _lib.ref(dc), ctypes_stream(_stream(stream))), "moe_dispatch")
+    dp = _lib.ref(_lib.tensor_desc(plan)) if plan is not None else None
+    check(lib.pk_moe_dispatch_ex(comm._h, _lib.ref(dx), _lib.ref(dt), int(num_experts), lay, _MECHANISMS[mechanism],
+                                 _lib.ref(dr), _lib.ref(ds), _lib.ref(dc), dp, ctypes_stream(_stream(stream))),
+          "moe_dispatch")
+    if lay:
+        return recv_rows, recv_src, count, plan
     return recv_rows, recv_src, count
 
 
@@ -207,18 +229,29 @@ def ring_attention(comm, q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, soft
     return out, lse
 
 
-def grouped_gemm(a: torch.Tensor, group_ids: torch.Tensor, w: torch.Tensor, out: torch.Tensor | None = None,
-                 num_rows: torch.Tensor | None = None, schedule: dict | None = None, stream=None) -> torch.Tensor:
+def grouped_gemm(a: torch.Tensor, group_ids: torch.Tensor | None, w: torch.Tensor, out: torch.Tensor | None = None,
+                 num_rows: torch.Tensor | None = None, schedule: dict | None = None, stream=None,
+                 plan: torch.Tensor | None = None) -> torch.Tensor:
     """y[i] = a[i] @ w[group_ids[i]]^T for i < num_rows (device int32; default all rows).
 
     a [R, K] bf16, w [G, N, K] bf16 (K-major per group), group ids int32 [R]
     or the [R, 2] recv_src of moe_dispatch. The expert GEMM1 of the MoE path
     (PAPER.md:445): recv, recv_src, count = moe_dispatch(...);
-    y = grouped_gemm(recv, recv_src, w_local, num_rows=count)."""
-    _require_cuda(a, group_ids, w)
+    y = grouped_gemm(recv, recv_src, w_local, num_rows=count).
+    With plan= (from moe_dispatch(layout="expert")) the rows are already in
+    256-row expert segments: y[r] = a[r] @ w[plan[2 + r // 256]]^T, no gather."""
+    _require_cuda(a, w)
     if out is None:
         out = torch.empty((a.shape[0], w.shape[1]), dtype=torch.bfloat16, device=a.device)
     lib = _lib.load()
+    if plan is not None:
+        _require_cuda(plan)
+        da, dp, dw, dy = (_lib.tensor_desc(x) for x in (a, plan, w, out))
+        check(lib.pk_grouped_gemm_planned(_lib.ref(da), _lib.ref(dp), _lib.ref(dw), _lib.ref(dy),
+                                          _lib.ref(_sched(schedule)), ctypes_stream(_stream(stream))),
+              "grouped_gemm")
+        return out
+    _require_cuda(group_ids)
     da, dg, dw, dy = (_lib.tensor_desc(x) for x in (a, group_ids, w, out))
     dn = _lib.tensor_desc(num_rows) if num_rows is not None else None
     check(lib.pk_grouped_gemm(_lib.ref(da), _lib.ref(dg), _lib.ref(dw), _lib.ref(dy), _lib.ref(dn),
