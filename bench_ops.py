@@ -133,7 +133,7 @@ def main():
 def moe(args, out, c1, T, K, E, H, HE):
     dev = "cuda"
     x = torch.randn(T, H, device=dev).bfloat16()
-    topk = torch.stack([torch.randperm(E, device=dev)[:K] for _ in range(T)]).int()
+    topk = torch.rand(T, E, device=dev).argsort(dim=1)[:, :K].int().contiguous()
     recv = (c1.empty((T * K, H)), c1.empty((T * K, 2), torch.int32))
     for mech in ("reg", "tma"):
         ms = timeit(lambda: pk.moe_dispatch(c1, x, topk, E, recv=recv, mechanism=mech))
@@ -148,6 +148,17 @@ def moe(args, out, c1, T, K, E, H, HE):
     y_e = c1.empty((cap_e, HE))
     ms = timeit(lambda: pk.grouped_gemm(recv_e[0], None, w64, out=y_e, plan=plan))
     emit(out, **tensor_line("grouped_gemm_planned_n1", 2 * T * K * H * HE, ms, rows=T * K, experts=E, H=H, H_exp=HE))
+    # per-rank view of the 8-GPU deployment: 8 local experts, T*k rows received
+    e8 = torch.rand(T, 8, device=dev).argsort(dim=1)[:, :K].int().contiguous()
+    cap8 = pk.moe_capacity(T, K, 1, H, 8)
+    recv8 = (c1.empty((cap8, H)), c1.empty((cap8, 2), torch.int32))
+    _, _, _, plan8 = pk.moe_dispatch(c1, x, e8, 8, recv=recv8, layout="expert")
+    w8p = torch.randn(8, HE, H, device=dev).bfloat16()
+    y8 = c1.empty((cap8, HE))
+    ms = timeit(lambda: pk.grouped_gemm(recv8[0], None, w8p, out=y8, plan=plan8))
+    emit(out, **tensor_line("grouped_gemm_planned_8experts", 2 * T * K * H * HE, ms, rows=T * K, experts=8, H=H,
+                            H_exp=HE))
+    del recv8, y8, w8p
     yh_e = c1.empty((cap_e, H))
     comb_e = torch.empty(T, H, device=dev, dtype=torch.bfloat16)
     wts_e = torch.rand(T, K, device=dev)

@@ -549,7 +549,7 @@ lcsc_gemm_kernel(const __grid_constant__ GemmArgs args) {
       mbar_wait(&tfull_bar[acc], acc_phase);
       tc_fence_after();
       const uint32_t t_lane = (uint32_t)(q * 32) << 16;
-      if constexpr (Cfg::ACC_STAGES == 1 && EPI == EPI_STORE) {
+      if constexpr (Cfg::ACC_STAGES == 1 && (EPI == EPI_STORE || EPI == EPI_REDUCE_ADD)) {
         // Single accumulator stage (512-row pair tiles fill TMEM): drain the
         // whole 256-column row into registers as packed bf16 first and release
         // TMEM at once, so the next tile's MMAs overlap the smem staging and
@@ -585,7 +585,8 @@ lcsc_gemm_kernel(const __grid_constant__ GemmArgs args) {
           fence_async_shared();
           __syncwarp();
           if (lane == 0) {
-            tma_store_2d(&args.tmap_c[dst], buf, nt * BN + c * EPI_COLS, c_row);
+            if constexpr (EPI == EPI_STORE) tma_store_2d(&args.tmap_c[dst], buf, nt * BN + c * EPI_COLS, c_row);
+            else tma_reduce_add_2d(&args.tmap_c[dst], buf, nt * BN + c * EPI_COLS, c_row);
             bulk_commit();
           }
           if constexpr (Cfg::EPI_NBUF == 2) ebuf_idx ^= 1;

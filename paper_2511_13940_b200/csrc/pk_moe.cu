@@ -126,15 +126,38 @@ __global__ void __launch_bounds__(kCountThreads) moe_count_kernel(const __grid_c
   __syncthreads();
   if (!last) return;
   __threadfence();
-  for (int q = tid; q < a.nkeys; q += blockDim.x) {
-    int tot = 0;
-    for (int c = 0; c < (int)gridDim.x; ++c) {
-      int32_t* p = a.chunk_counts + (long long)c * a.nkeys + q;
-      const int v = ld_volatile_s32(p);
-      *p = tot;                                        // exclusive prefix over chunks
-      tot += v;
+  // exclusive prefix over chunks, per key, in two passes: thread (q, seg)
+  // sums a contiguous run of chunks, the segment sums are scanned in smem,
+  // then each thread rewrites its run as offsets (G x nkeys can be ~300 x 1024)
+  __shared__ int32_t segsum[kCountThreads];
+  const int G = (int)gridDim.x;
+  const int nseg = a.nkeys >= kCountThreads ? 1 : kCountThreads / a.nkeys;
+  const int per_seg = (G + nseg - 1) / nseg;
+  for (int base_q = 0; base_q < a.nkeys; base_q += kCountThreads / nseg) {
+    const int q = base_q + tid % (kCountThreads / nseg), sg = tid / (kCountThreads / nseg);
+    const bool act = q < a.nkeys && sg < nseg;
+    const int c0 = sg * per_seg, c1 = min(G, c0 + per_seg);
+    int sum = 0;
+    if (act)
+      for (int c = c0; c < c1; ++c) sum += __ldcg(a.chunk_counts + (long long)c * a.nkeys + q);
+    segsum[tid] = sum;
+    __syncthreads();
+    int run = 0;
+    if (act) {
+      const int stride = kCountThreads / nseg;
+      for (int j = 0; j < sg; ++j) run += segsum[j * stride + tid % stride];
+      if (sg == nseg - 1) {
+        const int tot = run + sum;
+        for (int d = 0; d < a.n; ++d) a.table_peer[d][a.rank * a.nkeys + q] = tot;
+      }
+      for (int c = c0; c < c1; ++c) {
+        int32_t* p = a.chunk_counts + (long long)c * a.nkeys + q;
+        const int v = __ldcg(p);
+        *p = run;
+        run += v;
+      }
     }
-    for (int d = 0; d < a.n; ++d) a.table_peer[d][a.rank * a.nkeys + q] = tot;
+    __syncthreads();
   }
   __syncthreads();
   if (tid == 0) {
@@ -148,7 +171,7 @@ constexpr int kDispatchThreads = 256;
 constexpr int kDispatchWarps = kDispatchThreads / 32;
 constexpr int kPiece = 16384;          // bytes per bulk piece (bulk-copy mechanism)
 constexpr int kDispatchBufs = 4;
-constexpr int kWinEntries = 1024;      // (token, k) entries ranked per window
+constexpr int kWinEntries = 512;       // (token, k) entries ranked per window
 constexpr int kSegVec = 16;            // register path: 16 x 16 B per lane = 8 KB per warp segment
 constexpr int kDispatchSmemTma = kDispatchBufs * kPiece;
 
@@ -165,6 +188,7 @@ __global__ void __launch_bounds__(kDispatchThreads) moe_dispatch_kernel(const __
   __shared__ int16_t sown[kWinEntries];
   __shared__ int32_t sexp[kWinEntries];
   __shared__ int32_t base[kMoeMaxKeys];              // per key: base slot on the owner + earlier chunks + run
+  __shared__ int32_t wc[kDispatchWarps][kMoeMaxKeys]; // per (warp, key): group size, then its first slot
   __shared__ __align__(8) uint64_t bars[kDispatchBufs];
   __shared__ int ok_flag;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -195,7 +219,7 @@ __global__ void __launch_bounds__(kDispatchThreads) moe_dispatch_kernel(const __
         if (d < a.rank) pre += v;
       }
       base[q] = (tot + kMoeTile - 1) / kMoeTile * kMoeTile;   // padded size (temporarily)
-      sslot[q] = pre;                                          // scratch: earlier sources
+      wc[0][q] = pre;                                          // scratch: earlier sources
     }
     __syncthreads();
     if (tid < a.n) {                                  // exclusive scan of padded sizes per owner
@@ -208,7 +232,7 @@ __global__ void __launch_bounds__(kDispatchThreads) moe_dispatch_kernel(const __
     }
     __syncthreads();
     for (int q = tid; q < a.nkeys; q += blockDim.x)
-      base[q] += sslot[q] + a.chunk_counts[(long long)blockIdx.x * a.nkeys + q];
+      base[q] += wc[0][q] + a.chunk_counts[(long long)blockIdx.x * a.nkeys + q];
   }
   if (blockIdx.x == 0 && tid == 0) {
     // this rank as an owner: rows received (+ the expert tile plan)
@@ -237,8 +261,8 @@ __global__ void __launch_bounds__(kDispatchThreads) moe_dispatch_kernel(const __
   const int per_row = (a.row_bytes + kPiece - 1) / kPiece;
   uint32_t phase = 0;   // thread 0: parity of each bulk buffer's barrier
   int gp = 0;           // thread 0: pieces issued so far (buffer index continues across windows)
-  __shared__ int32_t wcnt[kDispatchWarps][32];       // per (warp, group leader lane): group size
-  __shared__ int32_t wkey[kDispatchWarps][32];
+  for (int i = tid; i < kDispatchWarps * a.nkeys; i += blockDim.x) wc[i / a.nkeys][i % a.nkeys] = 0;
+  __syncthreads();
   for (int w0 = t_begin; w0 < t_end; w0 += win_tokens) {
     const int w1 = min(t_end, w0 + win_tokens);
     const int e0 = w0 * a.k, ne = (w1 - w0) * a.k;
@@ -253,22 +277,27 @@ __global__ void __launch_bounds__(kDispatchThreads) moe_dispatch_kernel(const __
       }
       const unsigned peers = __match_any_sync(0xffffffffu, key);
       const int r = __popc(peers & ((1u << lane) - 1u));
-      const bool leader = (peers & ((1u << lane) - 1u)) == 0;
-      wcnt[warp][lane] = leader ? __popc(peers) : 0;
-      wkey[warp][lane] = key;
+      const bool leader = key >= 0 && r == 0;
+      if (leader) wc[warp][key] = __popc(peers);
       __syncthreads();
-      // entries of earlier warps with the same key: walk the (<= 8 x 32) group leaders
-      int before = 0;
-      if (key >= 0) {
-        for (int w = 0; w < warp; ++w)
-          for (int l = 0; l < 32; ++l)
-            if (wcnt[w][l] && wkey[w][l] == key) before += wcnt[w][l];
+      // exclusive scan over warps per key; base[] advances past this group
+      for (int q = tid; q < a.nkeys; q += blockDim.x) {
+        int run = base[q];
+#pragma unroll
+        for (int w = 0; w < kDispatchWarps; ++w) {
+          const int cnt = wc[w][q];
+          wc[w][q] = run;
+          run += cnt;
+        }
+        base[q] = run;
       }
-      int slot = -1;
-      if (key >= 0) slot = base[key] + before + r;
       __syncthreads();
-      // advance the running base by this group's totals (one leader per key per warp)
-      if (key >= 0 && leader) atomicAdd(&base[key], __popc(peers));
+      int slot = -1;
+      if (key >= 0) slot = wc[warp][key] + r;
+      __syncthreads();
+      for (int q = tid; q < a.nkeys; q += blockDim.x)   // table back to zero for the next group
+#pragma unroll
+        for (int w = 0; w < kDispatchWarps; ++w) wc[w][q] = 0;
       if (valid) {
         const bool keep = key >= 0 && slot < a.cap;
         a.slot_of[e0 + le] = keep ? slot : -1;

@@ -62,7 +62,7 @@ struct Variant { int cg, am; };
 
 int launch_gemm_variant(Variant v, int epi, const GemmArgs& args, int grid_ctas, cudaStream_t st) {
 #define PK_V(CG, AM, E) if (v.cg == CG && v.am == AM && epi == E) return launch_lcsc<CG, 256, AM, E>(args, grid_ctas, st);
-  PK_V(2, 2, EPI_STORE) PK_V(2, 1, EPI_DIRECT)
+  PK_V(2, 2, EPI_STORE) PK_V(2, 2, EPI_REDUCE_ADD) PK_V(2, 1, EPI_DIRECT)
   PK_V(2, 1, EPI_STORE) PK_V(2, 1, EPI_REDUCE_ADD)
   PK_V(1, 1, EPI_STORE) PK_V(1, 1, EPI_REDUCE_ADD)
 #undef PK_V
@@ -81,7 +81,7 @@ int launch_gemm_grouped(const GemmArgs& args, int grid_ctas, cudaStream_t st) {
 int preload_gemm() {
   cudaFuncAttributes fa;
 #define PK_L(CG, AM, E) PK_CUDA(cudaFuncGetAttributes(&fa, lcsc_gemm_kernel<CG, 256, AM, E>));
-  PK_L(2, 2, EPI_STORE) PK_L(2, 1, EPI_DIRECT) PK_L(2, 1, EPI_STORE) PK_L(2, 1, EPI_REDUCE_ADD)
+  PK_L(2, 2, EPI_STORE) PK_L(2, 2, EPI_REDUCE_ADD) PK_L(2, 1, EPI_DIRECT) PK_L(2, 1, EPI_STORE) PK_L(2, 1, EPI_REDUCE_ADD)
   PK_L(1, 1, EPI_STORE) PK_L(1, 1, EPI_REDUCE_ADD) PK_L(2, 1, EPI_SCATTER)
 #undef PK_L
   return PK_OK;
@@ -98,8 +98,9 @@ static Variant pick_variant(int64_t rows_per_part, int64_t K, const pk_sched* sc
   // 512-row pair tiles by default: with the early TMEM release in the
   // epilogue they issue as many MMAs per clock as the double-buffered 256-row
   // tiles and, moving 25% fewer bytes into each SM, run ~5% faster under the
-  // 1 kW power cap (scratch/gemm_power.py: 1438 vs 1378 TF/s at 16384^3).
-  if (!reduce && rows_per_part % 512 == 0 && force_am != 1) return {2, 2};
+  // 1 kW power cap (profiles/gemm_power.py: 1438 vs 1378 TF/s at 16384^3).
+  (void)reduce;
+  if (rows_per_part % 512 == 0 && force_am != 1) return {2, 2};
   if (rows_per_part % 256 == 0) return {2, 1};
   return {1, 1};
 }
@@ -393,7 +394,7 @@ int gemm_rs(Comm* c, const pk_tensor* A, const pk_tensor* B, pk_tensor* O, const
   }
   PK_CUDA(cudaMemsetAsync(dst[c->rank], 0, out_bytes, st));
   GemmArgs args;
-  init_args(args);
+  init_args(args, v.am);
   args.M = (int)M; args.N = (int)N; args.K = (int)k_loc;
   args.rank = c->rank; args.world = n;
   args.a_rows_per_src = (int)M;

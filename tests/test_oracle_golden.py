@@ -107,3 +107,27 @@ def test_moe_combine_inverts_dispatch_with_unit_weights():
     back = oracle.moe_combine(recv, owners, w)
     for d in range(n):
         assert np.allclose(back[d], tokens[d])
+
+
+def test_moe_expert_major_slots_are_a_regrouping():
+    """The expert-major layout only regroups the reference's rows: within each
+    expert's segment the (src, tok, k) order of workloads.py:821-832 is kept,
+    segments are 256-row aligned, and the plan covers exactly the segments."""
+    for n, E, T, K, seed in [(2, 8, 40, 3, 0), (4, 16, 33, 4, 1), (1, 64, 300, 8, 2)]:
+        route, owners = oracle.moe_route(oracle.plan_rng(seed), n, T, E, K)
+        slot, counts, plans = oracle.moe_expert_slots(route, n)
+        rank_slot, rank_counts = oracle.moe_slots_vectorized(owners)
+        assert list(counts) == list(rank_counts)
+        for o in range(n):
+            plan = plans[o]
+            assert plan[1] == counts[o] and len(plan) == 2 + plan[0]
+            for le in range(E // n):
+                e = le * n + o
+                mask = route == e
+                s_exp, s_rank = slot[mask], rank_slot[mask]
+                assert np.all(np.diff(s_exp) == 1)                    # contiguous segment
+                assert np.all(np.diff(s_rank) > 0)                    # same relative order
+                if s_exp.size:
+                    assert s_exp[0] % 256 == 0
+                    tiles = [i for i, g in enumerate(plan[2:]) if g == le]
+                    assert tiles and tiles[0] * 256 == s_exp[0] and len(tiles) == -(-s_exp.size // 256)
