@@ -122,6 +122,24 @@ def main():
         emit(out, **tensor_line("ring_attention_n1", 4 * B * H * S * S * D, ms, shape=[B, S, H, D],
                                 sdpa_ms=ms_sdpa, vs_sdpa=ms_sdpa / ms))
 
+    # ---------------------------------------------------------------- ring attention: one rank's step at n = 8
+    # (BASELINE config 4: S = 32K..128K over 8 GPUs -> S/8 queries against all S keys)
+    for S in ([32768] if args.quick else [32768, 65536, 131072]) if want("attn") else []:
+        B, H, D, n = 1, 16, 128, 8
+        q = torch.randn(B, S // n, H, D, device=dev).bfloat16()
+        k, v = torch.randn(B, S, H, D, device=dev).bfloat16(), torch.randn(B, S, H, D, device=dev).bfloat16()
+        o, lse = torch.empty_like(q), torch.empty(B, H, S // n, device=dev)
+        flops = 4 * B * H * (S // n) * S * D
+        ms = timeit(lambda: pk.attention(q, k, v, out=o, lse=lse), iters=5)
+        os.environ["PK_ATTN_NO_SPLIT"] = "1"
+        ms_ns = timeit(lambda: pk.attention(q, k, v, out=o, lse=lse), iters=5)
+        del os.environ["PK_ATTN_NO_SPLIT"]
+        qt, kt, vt = (x.transpose(1, 2).contiguous() for x in (q, k, v))
+        ms_sdpa = timeit(lambda: torch.nn.functional.scaled_dot_product_attention(qt, kt, vt), iters=5)
+        emit(out, **tensor_line("attention_rank_step_n8", flops, ms, shape=[B, S // n, S, H, D],
+                                ms_no_stream_k=ms_ns, sdpa_ms=ms_sdpa, vs_sdpa=ms_sdpa / ms))
+        del q, k, v, o, qt, kt, vt
+
     # ---------------------------------------------------------------- MoE (n = 1): dispatch, grouped GEMM, combine
     T, K, E, H, HE = (1024, 8, 64, 7168, 2048) if args.quick else (4096, 8, 64, 7168, 2048)
     moe(args, out, c1, T, K, E, H, HE) if want("moe") else None

@@ -151,6 +151,12 @@ PK_API int pk_ring_attn_fwd(pk_comm* comm, const pk_tensor* q, const pk_tensor* 
                             const pk_tensor* v, pk_tensor* o, pk_tensor* lse, float softmax_scale,
                             const pk_sched* sched, void* stream);
 
+/* Single-GPU attention forward, non-causal (the compute step of one ring
+ * rank): q, o [B, S_q, H, D], k, v [B, S_kv, H, D] bf16 (D = 128, S % 128 == 0),
+ * lse [B, H, S_q] f32 natural log. */
+PK_API int pk_attn_fwd(const pk_tensor* q, const pk_tensor* k, const pk_tensor* v, pk_tensor* o, pk_tensor* lse,
+                       float softmax_scale, void* stream);
+
 /* Expert-parallel dispatch: x [T, H] bf16, topk_idx [T, k] int32 (expert ids);
  * expert e lives on rank e % n (workloads.py:802). Tokens are placed on their
  * owner in slots sorted by (src_rank, token, k) (workloads.py:821-832).

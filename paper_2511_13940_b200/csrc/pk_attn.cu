@@ -33,6 +33,8 @@
 #include <algorithm>
 #include <cmath>
 #include <cstring>
+#include <map>
+#include <mutex>
 
 namespace pk {
 
@@ -56,11 +58,6 @@ struct AttnArgs {
   CUtensorMap tm_q, tm_k, tm_v;  // 4-D maps over [B, S, H, D] (dims D, H, S, B)
   int B, S_q, S_kv, H;
   float scale_log2;              // softmax_scale * log2(e)
-  // ring state (fp32), [B, H, S_q, D] / [B, H, S_q]; unused for single-step
-  float* o_acc;
-  float* m_acc;
-  float* l_acc;
-  int first, last;               // first / last ring step
   // single-launch ring: KV of ring step s lives at batch coordinate s*B + b of
   // the K/V maps; steps >= 1 are usable once step_flags[s] >= flag_epoch
   int blocks_per_step;           // 128-key blocks per ring step (S/n / 128)
@@ -68,8 +65,36 @@ struct AttnArgs {
   uint32_t flag_epoch;
   uint32_t* err;
   uint64_t timeout_ns;
-  uint16_t* o;                   // [B, S_q, H, D] bf16 output (last step)
-  float* lse;                    // [B, H, S_q] natural-log LSE (last step)
+  uint16_t* o;                   // [B, S_q, H, D] bf16 output
+  float* lse;                    // [B, H, S_q] natural-log LSE
+  // stream-K work split: gridDim.x CTAs share items * nblk key blocks evenly;
+  // an item cut between CTAs is merged by whichever of them finishes last
+  float* part;                   // [2 * grid] slots of [2 tiles][128 rows][D + 2] fp32 (O, m, l)
+  uint32_t* item_count;          // [items * 2] segments finished per (item, tile); re-armed by the merger
+};
+
+// Partial state of one (slot, tile, row): D floats of unnormalised O, then m, l.
+constexpr int AT_PART_ROW = AT_D + 4;            // padded to 16 B (float4 rows)
+constexpr int AT_PART_SLOT = 2 * AT_BM * AT_PART_ROW;
+
+// Work split over G persistent CTAs (data-parallel waves + a stream-K tail):
+// items = Q*G + R. CTA c first runs the whole items c, c + G, ..., c + (Q-1)G
+// — the CTAs in flight work on consecutive items (the same heads, so the K/V
+// they stream stays in L2) — then shares the R tail items' key blocks evenly:
+// tail block range [tstart(c), tstart(c+1)) of T = R * nblk. A segment is the
+// part of one item a CTA owns; only tail items are ever cut.
+struct AtSplit {
+  int G, nblk, Q, R;
+  long long T;
+  PK_DEV long long tstart(int c) const { return (long long)c * T / G; }
+  PK_DEV int tcta_of(long long p) const {      // the CTA whose tail range holds tail block p
+    int c = (int)(((p + 1) * (long long)G - 1) / T);
+    while (c > 0 && tstart(c) > p) --c;
+    while (c + 1 < G && tstart(c + 1) <= p) ++c;
+    return c;
+  }
+  // partial slot of CTA c's segment of tail item ti: its first segment 2c, else 2c + 1
+  PK_DEV int slot(int c, int ti) const { return (tstart(c) / nblk == ti) ? 2 * c : 2 * c + 1; }
 };
 
 // MN-major (N contiguous) SW128 descriptor for the V operand: 64-element
@@ -140,6 +165,15 @@ PK_DEV void poly_exp2x2(float x0, float x1, float& p0, float& p1) {
 // Ordering: the MMAs of one thread complete in issue order, so s_full_X(j)
 // (committed after QK_X(j), which is issued after PV_X(j-1)) also means PV_X(j-1)
 // has finished reading P_X(j-1) and updating O_X.
+//
+// Work split (stream-K): an item = (batch, head, query-tile pair) with nblk
+// key blocks. The CTAs are persistent and share the items * nblk blocks
+// evenly, so no wave is left partly idle; a CTA walks its range as segments
+// (the part of one item it owns). A whole item is finished in place; a cut
+// item leaves (O, m, l) partials and the CTA finishing its last segment merges
+// them in ascending CTA order (deterministic) and writes o / lse.
+// Barrier phases count K/V blocks (g), blocks per tile (gx) and segments per
+// tile (segx) across segments.
 __global__ void __launch_bounds__(AT_THREADS, 1) attn_fwd_kernel(const __grid_constant__ AttnArgs a) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -148,33 +182,72 @@ __global__ void __launch_bounds__(AT_THREADS, 1) attn_fwd_kernel(const __grid_co
   uint8_t* sv = sk + AT_KSTAGES * AT_K_BYTES;
   uint64_t* bars = reinterpret_cast<uint64_t*>(sv + AT_VSTAGES * AT_V_BYTES);
   uint64_t* q_full = bars + 0;
-  uint64_t* k_full = bars + 1;      // [2]
-  uint64_t* k_empty = bars + 3;     // [2]
-  uint64_t* v_full = bars + 5;      // [2]
-  uint64_t* v_empty = bars + 7;     // [2]
-  uint64_t* s_full = bars + 9;      // [2] per tile
-  uint64_t* p_full = bars + 11;     // [2 tiles][2 halves]: P of keys [64h, 64h+64) in TMEM
-  uint64_t* o_full = bars + 15;     // [2] per tile
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 17);
+  uint64_t* q_empty = bars + 1;
+  uint64_t* k_full = bars + 2;      // [2]
+  uint64_t* k_empty = bars + 4;     // [2]
+  uint64_t* v_full = bars + 6;      // [2]
+  uint64_t* v_empty = bars + 8;     // [2]
+  uint64_t* s_full = bars + 10;     // [2] per tile
+  uint64_t* p_full = bars + 12;     // [2 tiles][2 halves]: P of keys [64h, 64h+64) in TMEM
+  uint64_t* o_full = bars + 16;     // [2] per tile
+  uint64_t* o_empty = bars + 18;    // [2] per tile: the epilogue has read O
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 20);
+  __shared__ int merge_flag[2];
 
   const uint32_t warp = warp_id_sync();
   const uint32_t lane = lane_id();
   const int q_tiles = a.S_q / AT_BM;
   const int pairs = (q_tiles + 1) / 2;
-  const int tile = blockIdx.x;
-  const int qp = tile % pairs;
-  const int h = (tile / pairs) % a.H;
-  const int b = tile / (pairs * a.H);
-  const int ntile = (2 * qp + 1 < q_tiles) ? 2 : 1;   // the last pair may hold one tile
   const int nblk = a.S_kv / AT_BN;
+  const int items = a.B * a.H * pairs;
+  AtSplit sp;
+  sp.G = (int)gridDim.x;
+  sp.nblk = nblk;
+  sp.Q = items / sp.G;
+  sp.R = items - sp.Q * sp.G;
+  sp.T = (long long)sp.R * nblk;
+  const int me = (int)blockIdx.x;
+  const long long t0 = sp.tstart(me), t1 = sp.tstart(me + 1);
+  // segment walk shared by every role: item, key blocks [j0, j1), pair shape;
+  // cursor k < Q: whole item k*G + me; then tail blocks from t0 to t1
+  struct SegInfo { int item, ti, j0, j1, qp, h, b, ntile; };
+  struct SegIter {
+    long long k;                                     // wave index, then Q + tail block position
+  };
+  auto seg_next = [&](SegIter& it, SegInfo& g) -> bool {
+    if (it.k < sp.Q) {
+      g.item = (int)it.k * sp.G + me;
+      g.ti = -1;
+      g.j0 = 0;
+      g.j1 = nblk;
+      ++it.k;
+      if (it.k == sp.Q) it.k = sp.Q + t0;            // continue with the tail
+    } else {
+      const long long p = it.k - sp.Q;
+      if (p >= t1) return false;
+      g.ti = (int)(p / nblk);
+      g.item = sp.Q * sp.G + g.ti;
+      g.j0 = (int)(p - (long long)g.ti * nblk);
+      g.j1 = (int)min((long long)nblk, t1 - (long long)g.ti * nblk);
+      it.k = sp.Q + (long long)g.ti * nblk + g.j1;
+    }
+    g.qp = g.item % pairs;
+    g.h = (g.item / pairs) % a.H;
+    g.b = g.item / (pairs * a.H);
+    g.ntile = (2 * g.qp + 1 < q_tiles) ? 2 : 1;      // the last pair may hold one tile
+    return true;
+  };
+  auto seg_begin = [&]() { SegIter it; it.k = sp.Q > 0 ? 0 : t0; return it; };
 
   if (warp == 0 && lane == 0) {
     mbar_init(q_full, 1);
+    mbar_init(q_empty, 1);
     for (int i = 0; i < 2; ++i) {
       mbar_init(&k_full[i], 1); mbar_init(&k_empty[i], 1);
       mbar_init(&v_full[i], 1); mbar_init(&v_empty[i], 1);
       mbar_init(&s_full[i], 1); mbar_init(&o_full[i], 1);
       mbar_init(&p_full[2 * i], 4); mbar_init(&p_full[2 * i + 1], 4);
+      mbar_init(&o_empty[i], 4);
     }
     fence_mbar_init();
   }
@@ -192,12 +265,6 @@ __global__ void __launch_bounds__(AT_THREADS, 1) attn_fwd_kernel(const __grid_co
   if (warp == 0) {
     // ------------------------------------------------------------ loader (lane 0)
     if (lane == 0) {
-      mbar_arrive_expect_tx(q_full, ntile * AT_Q_BYTES);
-      for (int x = 0; x < ntile; ++x) {
-        const int qrow = (2 * qp + x) * AT_BM;
-        tma_load_4d(&a.tm_q, q_full, sq + x * AT_Q_BYTES, 0, h, qrow, b);
-        tma_load_4d(&a.tm_q, q_full, sq + x * AT_Q_BYTES + AT_Q_BYTES / 2, 64, h, qrow, b);
-      }
       // key block j = ring step j / bps, block j % bps of that step's shard
       const int bps = a.blocks_per_step;
       int ready_steps = 1;                               // step 0 (own shard) is always resident
@@ -208,26 +275,40 @@ __global__ void __launch_bounds__(AT_THREADS, 1) attn_fwd_kernel(const __grid_co
           ++ready_steps;
         }
       };
-      auto load_k = [&](int j) {
-        const int st = j & 1;
+      auto load_k = [&](int g, int j, int h, int b) {
+        const int st = g & 1;
         const int step = j / bps, row = (j % bps) * AT_BN;
         step_ready(step);
-        mbar_wait(&k_empty[st], ((j >> 1) & 1) ^ 1);
+        mbar_wait(&k_empty[st], ((g >> 1) & 1) ^ 1);
         uint8_t* kb = sk + st * AT_K_BYTES;
         mbar_arrive_expect_tx(&k_full[st], AT_K_BYTES);
         tma_load_4d(&a.tm_k, &k_full[st], kb, 0, h, row, step * a.B + b);
         tma_load_4d(&a.tm_k, &k_full[st], kb + AT_K_BYTES / 2, 64, h, row, step * a.B + b);
       };
-      if (nblk > 0) load_k(0);
-      for (int j = 0; j < nblk; ++j) {
-        if (j + 1 < nblk) load_k(j + 1);
-        const int vs = j & 1;
-        const int step = j / bps, row = (j % bps) * AT_BN;
-        mbar_wait(&v_empty[vs], ((j >> 1) & 1) ^ 1);
-        uint8_t* vb = sv + vs * AT_V_BYTES;
-        mbar_arrive_expect_tx(&v_full[vs], AT_V_BYTES);
-        tma_load_4d(&a.tm_v, &v_full[vs], vb, 0, h, row, step * a.B + b);
-        tma_load_4d(&a.tm_v, &v_full[vs], vb + AT_V_BYTES / 2, 64, h, row, step * a.B + b);
+      int g = 0, seg = 0;
+      SegIter it = seg_begin();
+      for (SegInfo sg; seg_next(it, sg); ++seg) {
+        mbar_wait(q_empty, (seg & 1) ^ 1);
+        mbar_arrive_expect_tx(q_full, sg.ntile * AT_Q_BYTES);
+        for (int x = 0; x < sg.ntile; ++x) {
+          const int qrow = (2 * sg.qp + x) * AT_BM;
+          tma_load_4d(&a.tm_q, q_full, sq + x * AT_Q_BYTES, 0, sg.h, qrow, sg.b);
+          tma_load_4d(&a.tm_q, q_full, sq + x * AT_Q_BYTES + AT_Q_BYTES / 2, 64, sg.h, qrow, sg.b);
+        }
+        const int len = sg.j1 - sg.j0;
+        load_k(g, sg.j0, sg.h, sg.b);
+        for (int i = 0; i < len; ++i) {
+          const int j = sg.j0 + i, gg = g + i;
+          if (i + 1 < len) load_k(gg + 1, j + 1, sg.h, sg.b);
+          const int vs = gg & 1;
+          const int step = j / bps, row = (j % bps) * AT_BN;
+          mbar_wait(&v_empty[vs], ((gg >> 1) & 1) ^ 1);
+          uint8_t* vb = sv + vs * AT_V_BYTES;
+          mbar_arrive_expect_tx(&v_full[vs], AT_V_BYTES);
+          tma_load_4d(&a.tm_v, &v_full[vs], vb, 0, sg.h, row, step * a.B + sg.b);
+          tma_load_4d(&a.tm_v, &v_full[vs], vb + AT_V_BYTES / 2, 64, sg.h, row, step * a.B + sg.b);
+        }
+        g += len;
       }
     }
     __syncwarp();
@@ -235,11 +316,9 @@ __global__ void __launch_bounds__(AT_THREADS, 1) attn_fwd_kernel(const __grid_co
     // ------------------------------------------------------------ MMA issuer
     constexpr uint32_t id_s = idesc_bf16(AT_BM, AT_BN, 0);
     constexpr uint32_t id_o = idesc_bf16(AT_BM, AT_D, 1);
-    mbar_wait(q_full, 0);
-    tc_fence_after();
-    auto issue_qk = [&](int x, int j) {                 // S_x = Q_x K_j^T
+    auto issue_qk = [&](int x, int g) {                 // S_x = Q_x K_g^T
       const uint32_t q_addr = smem_u32(sq + x * AT_Q_BYTES);
-      const uint32_t k_addr = smem_u32(sk + (j & 1) * AT_K_BYTES);
+      const uint32_t k_addr = smem_u32(sk + (g & 1) * AT_K_BYTES);
 #pragma unroll
       for (int kk = 0; kk < AT_D / 16; ++kk) {
         const int atom = kk >> 2, sub = kk & 3;
@@ -249,65 +328,80 @@ __global__ void __launch_bounds__(AT_THREADS, 1) attn_fwd_kernel(const __grid_co
       }
       umma_commit<1>(&s_full[x]);
     };
-    auto issue_pv = [&](int x, int j, int half) {       // O_x += P_x V_j over keys [64 half, 64 half + 64)
-      const uint32_t v_addr = smem_u32(sv + (j & 1) * AT_V_BYTES);
+    auto issue_pv = [&](int x, int g, int half, bool first) {   // O_x += P_x V_g over keys [64 half, 64 half + 64)
+      const uint32_t v_addr = smem_u32(sv + (g & 1) * AT_V_BYTES);
 #pragma unroll
       for (int k4 = 0; k4 < AT_BN / 32; ++k4) {
         const int kk = half * (AT_BN / 32) + k4;
         const uint64_t bd = sdesc_mnmajor_sw128(v_addr + kk * 2048, AT_V_BYTES / 2, 1024);
-        umma_f16_ts(tmem + 256 * x + 128, tmem + 256 * x + kk * 8, bd, id_o, (j > 0 || kk > 0) ? 1u : 0u);
+        umma_f16_ts(tmem + 256 * x + 128, tmem + 256 * x + kk * 8, bd, id_o, (!first || kk > 0) ? 1u : 0u);
       }
-      if (half == 1 && j == nblk - 1) umma_commit<1>(&o_full[x]);
     };
-    if (nblk > 0) {
-      mbar_wait(&k_full[0], 0);
+    int g = 0, seg = 0;
+    int gx[2] = {0, 0}, segx[2] = {0, 0};
+    SegIter it = seg_begin();
+    for (SegInfo sg; seg_next(it, sg); ++seg) {
+      const int len = sg.j1 - sg.j0;
+      mbar_wait(q_full, seg & 1);
+      mbar_wait(&k_full[g & 1], (g >> 1) & 1);
       tc_fence_after();
       if (elect_one()) {
-        for (int x = 0; x < ntile; ++x) issue_qk(x, 0);
-        umma_commit<1>(&k_empty[0]);
+        for (int x = 0; x < sg.ntile; ++x) issue_qk(x, g);
+        umma_commit<1>(&k_empty[g & 1]);
       }
       __syncwarp();
-    }
-    for (int j = 0; j < nblk; ++j) {
-      mbar_wait(&v_full[j & 1], (j >> 1) & 1);
-      const bool more = j + 1 < nblk;
-      if (more) mbar_wait(&k_full[(j + 1) & 1], ((j + 1) >> 1) & 1);
-      for (int x = 0; x < ntile; ++x) {
-        // the first half of P is consumed while the softmax still works on the second
-        mbar_wait(&p_full[2 * x], j & 1);
-        tc_fence_after();
-        if (elect_one()) issue_pv(x, j, 0);
-        __syncwarp();
-        mbar_wait(&p_full[2 * x + 1], j & 1);
-        tc_fence_after();
+      for (int i = 0; i < len; ++i) {
+        const int gg = g + i;
+        mbar_wait(&v_full[gg & 1], (gg >> 1) & 1);
+        const bool more = i + 1 < len;
+        if (more) mbar_wait(&k_full[(gg + 1) & 1], ((gg + 1) >> 1) & 1);
+        for (int x = 0; x < sg.ntile; ++x) {
+          // O_x of the previous segment must have been read by its epilogue
+          if (i == 0 && segx[x] > 0) mbar_wait(&o_empty[x], (segx[x] - 1) & 1);
+          // the first half of P is consumed while the softmax still works on the second
+          mbar_wait(&p_full[2 * x], gx[x] & 1);
+          tc_fence_after();
+          if (elect_one()) issue_pv(x, gg, 0, i == 0);
+          __syncwarp();
+          mbar_wait(&p_full[2 * x + 1], gx[x] & 1);
+          tc_fence_after();
+          if (elect_one()) {
+            issue_pv(x, gg, 1, i == 0);
+            if (more) issue_qk(x, gg + 1);
+            else umma_commit<1>(&o_full[x]);
+          }
+          __syncwarp();
+          ++gx[x];
+        }
         if (elect_one()) {
-          issue_pv(x, j, 1);
-          if (more) issue_qk(x, j + 1);
+          umma_commit<1>(&v_empty[gg & 1]);
+          if (more) umma_commit<1>(&k_empty[(gg + 1) & 1]);
+          else umma_commit<1>(q_empty);
         }
         __syncwarp();
       }
-      if (elect_one()) {
-        umma_commit<1>(&v_empty[j & 1]);
-        if (more) umma_commit<1>(&k_empty[(j + 1) & 1]);
-      }
-      __syncwarp();
+      for (int x = 0; x < sg.ntile; ++x) ++segx[x];
+      g += len;
     }
   }
   } else {
   asm volatile("setmaxnreg.inc.sync.aligned.u32 224;\n" ::: "memory");
-  if ((int)(warp - 4) / 4 < ntile) {
-    // ------------------------------------------------------------ softmax + epilogue (tile x)
-    const int x = (warp - 4) / 4;
-    const int qt = 2 * qp + x;
-    const int q = warp & 3;
-    const int row = q * 32 + (int)lane;
-    const uint32_t lane_off = (uint32_t)(q * 32) << 16;
-    const uint32_t t_s = tmem + 256 * x + lane_off;
-    const uint32_t t_o = t_s + 128;
+  // ------------------------------------------------------------ softmax + epilogue (tile x)
+  const int x = (warp - 4) / 4;
+  const int q = warp & 3;
+  const int row = q * 32 + (int)lane;
+  const uint32_t lane_off = (uint32_t)(q * 32) << 16;
+  const uint32_t t_s = tmem + 256 * x + lane_off;
+  const uint32_t t_o = t_s + 128;
+  const float sc = a.scale_log2;
+  int gx = 0, segx = 0;
+  SegIter it = seg_begin();
+  for (SegInfo sg; seg_next(it, sg);) {
+    if (x >= sg.ntile) continue;
+    const int len = sg.j1 - sg.j0;
     float m = -INFINITY, l = 0.f;     // m: the max the current P values are relative to (log2 units)
-    const float sc = a.scale_log2;
-    for (int j = 0; j < nblk; ++j) {
-      mbar_wait(&s_full[x], j & 1);
+    for (int i = 0; i < len; ++i, ++gx) {
+      mbar_wait(&s_full[x], gx & 1);
       tc_fence_after();
 #ifdef AT_MMA_ONLY   // timing diagnostic only: the MMA pipeline without softmax (wrong results)
       if (lane == 0) { mbar_arrive(&p_full[2 * x]); mbar_arrive(&p_full[2 * x + 1]); }
@@ -324,12 +418,12 @@ __global__ void __launch_bounds__(AT_THREADS, 1) attn_fwd_kernel(const __grid_co
 #pragma unroll
       for (int t = 0; t < 8; ++t) m8[t] = fmax3(__uint_as_float(r[2 * t]), __uint_as_float(r[2 * t + 1]), -INFINITY);
 #pragma unroll
-      for (int i = 8; i < AT_BN / 2; ++i)
-        m8[i & 7] = fmax3(m8[i & 7], __uint_as_float(r[2 * i]), __uint_as_float(r[2 * i + 1]));
+      for (int i2 = 8; i2 < AT_BN / 2; ++i2)
+        m8[i2 & 7] = fmax3(m8[i2 & 7], __uint_as_float(r[2 * i2]), __uint_as_float(r[2 * i2 + 1]));
       float mx = fmax3(fmax3(m8[0], m8[1], m8[2]), fmax3(m8[3], m8[4], m8[5]), fmaxf(m8[6], m8[7]));
       mx *= sc;
       const bool grow = mx > m + AT_RESCALE_THRESHOLD;
-      if (j > 0 && __any_sync(0xffffffffu, grow)) {
+      if (i > 0 && __any_sync(0xffffffffu, grow)) {
         const float alpha = grow ? fast_exp2(m - mx) : 1.f;
 #pragma unroll 1
         for (int c = 0; c < 4; ++c) {
@@ -337,7 +431,7 @@ __global__ void __launch_bounds__(AT_THREADS, 1) attn_fwd_kernel(const __grid_co
           tmem_ld_32x32b_x32(t_o + c * 32, o);
           tmem_ld_wait();
 #pragma unroll
-          for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
+          for (int i2 = 0; i2 < 32; ++i2) o[i2] = __float_as_uint(__uint_as_float(o[i2]) * alpha);
           tmem_st_32x32b_x32(t_o + c * 32, o);
         }
         l *= alpha;
@@ -353,18 +447,18 @@ __global__ void __launch_bounds__(AT_THREADS, 1) attn_fwd_kernel(const __grid_co
       for (int c = 0; c < 4; ++c) {
         uint32_t pk[16];
 #pragma unroll
-        for (int i = 0; i < 16; ++i) {
+        for (int i2 = 0; i2 < 16; ++i2) {
           float x0, x1, p0, p1;
-          f2_unpack(f2_fma(f2_pack(__uint_as_float(r[32 * c + 2 * i]), __uint_as_float(r[32 * c + 2 * i + 1])), sc2, nm2),
+          f2_unpack(f2_fma(f2_pack(__uint_as_float(r[32 * c + 2 * i2]), __uint_as_float(r[32 * c + 2 * i2 + 1])), sc2, nm2),
                     x0, x1);
-          if ((i & 3) < AT_EXP_EMU) {
+          if ((i2 & 3) < AT_EXP_EMU) {
             poly_exp2x2(x0, x1, p0, p1);
           } else {
             p0 = fast_exp2(x0);
             p1 = fast_exp2(x1);
           }
-          rs2[i & 3] = f2_add(rs2[i & 3], f2_pack(p0, p1));
-          pk[i] = pack_bf16x2(p0, p1);
+          rs2[i2 & 3] = f2_add(rs2[i2 & 3], f2_pack(p0, p1));
+          pk[i2] = pack_bf16x2(p0, p1);
         }
         tmem_st_32x32b_x16(t_s + c * 16, pk);          // columns [16c, 16c+16): already in registers
         if (c & 1) {                                    // keys [64h, 64h+64) are in TMEM: release that half
@@ -379,7 +473,7 @@ __global__ void __launch_bounds__(AT_THREADS, 1) attn_fwd_kernel(const __grid_co
       l += rs_lo + rs_hi;
     }
     // ------------------------------------------------------------ epilogue
-    mbar_wait(&o_full[x], 0);
+    mbar_wait(&o_full[x], segx & 1);
     tc_fence_after();
     float o[AT_D];
 #pragma unroll
@@ -388,47 +482,78 @@ __global__ void __launch_bounds__(AT_THREADS, 1) attn_fwd_kernel(const __grid_co
       tmem_ld_32x32b_x32(t_o + c * 32, t);
       tmem_ld_wait();
 #pragma unroll
-      for (int i = 0; i < 32; ++i) o[c * 32 + i] = __uint_as_float(t[i]);
+      for (int i2 = 0; i2 < 32; ++i2) o[c * 32 + i2] = __uint_as_float(t[i2]);
     }
-    const int sq_idx = qt * AT_BM + row;                     // query index within the local shard
-    const long long srow = ((long long)(b * a.H + h) * a.S_q + sq_idx);   // [B, H, S_q] row
-    if (!a.first) {
-      // merge with the running state of earlier ring steps (log2 domain)
-      const float mg = a.m_acc[srow], lg = a.l_acc[srow];
-      const float mt = fmaxf(mg, m);
-      const float wg = (mg == -INFINITY) ? 0.f : fast_exp2(mg - mt);
-      const float wn = (m == -INFINITY) ? 0.f : fast_exp2(m - mt);
-      const float4* og = reinterpret_cast<const float4*>(a.o_acc + srow * AT_D);
+    tc_fence_before();
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&o_empty[x]);        // the next segment's PV may overwrite O
+    ++segx;
+    const int sq_idx = (2 * sg.qp + x) * AT_BM + row;                      // query index within the local shard
+    const long long srow = ((long long)(sg.b * a.H + sg.h) * a.S_q + sq_idx);   // [B, H, S_q] row
+    bool write_final = true;
+    const long long ib = (long long)sg.ti * nblk;              // tail items only
+    const int c_lo = (sg.ti < 0 || sg.j0 == 0) ? me : sp.tcta_of(ib);
+    const int c_hi = (sg.ti < 0 || sg.j1 == nblk) ? me : sp.tcta_of(ib + nblk - 1);
+    if (c_lo != c_hi) {
+      // cut item: publish this segment's partial, the last finisher merges
+      float* mine = a.part + (long long)sp.slot(me, sg.ti) * AT_PART_SLOT + (x * AT_BM + row) * AT_PART_ROW;
 #pragma unroll
-      for (int i = 0; i < AT_D / 4; ++i) {
-        const float4 v = og[i];
-        o[4 * i + 0] = v.x * wg + o[4 * i + 0] * wn;
-        o[4 * i + 1] = v.y * wg + o[4 * i + 1] * wn;
-        o[4 * i + 2] = v.z * wg + o[4 * i + 2] * wn;
-        o[4 * i + 3] = v.w * wg + o[4 * i + 3] * wn;
+      for (int i2 = 0; i2 < AT_D / 4; ++i2)
+        reinterpret_cast<float4*>(mine)[i2] = make_float4(o[4 * i2], o[4 * i2 + 1], o[4 * i2 + 2], o[4 * i2 + 3]);
+      mine[AT_D] = m;
+      mine[AT_D + 1] = l;
+      __threadfence();
+      asm volatile("bar.sync %0, 128;" :: "r"(1 + x) : "memory");
+      if (row == 0) {
+        const uint32_t done = atomicAdd(a.item_count + 2 * sg.item + x, 1u);
+        int nseg = 0;                                 // CTAs with a non-empty share of this item
+        for (int c = c_lo; c <= c_hi; ++c) nseg += sp.tstart(c + 1) > sp.tstart(c);
+        merge_flag[x] = (done == (uint32_t)(nseg - 1)) ? 1 : 0;
       }
-      l = lg * wg + l * wn;
-      m = mt;
-    }
-    if (a.last) {
-      const float inv = (l > 0.f) ? 1.f / l : 0.f;
-      uint4* dst = reinterpret_cast<uint4*>(a.o + (((long long)b * a.S_q + sq_idx) * a.H + h) * AT_D);
+      asm volatile("bar.sync %0, 128;" :: "r"(1 + x) : "memory");
+      write_final = merge_flag[x] != 0;
+      if (write_final) {
+        __threadfence();
+        // merge every segment's partial in ascending CTA order (log2 domain)
+        float mt = -INFINITY, lt = 0.f;
 #pragma unroll
-      for (int i = 0; i < AT_D / 8; ++i) {
+        for (int i2 = 0; i2 < AT_D; ++i2) o[i2] = 0.f;
+        for (int c = c_lo; c <= c_hi; ++c) {
+          if (sp.tstart(c + 1) == sp.tstart(c)) continue;   // no share of the tail
+          const float* pr = a.part + (long long)sp.slot(c, sg.ti) * AT_PART_SLOT + (x * AT_BM + row) * AT_PART_ROW;
+          const float mc = __ldcg(pr + AT_D), lc = __ldcg(pr + AT_D + 1);
+          const float mn = fmaxf(mt, mc);
+          const float wa = (mt == -INFINITY) ? 0.f : fast_exp2(mt - mn);
+          const float wb = (mc == -INFINITY) ? 0.f : fast_exp2(mc - mn);
+#pragma unroll
+          for (int i2 = 0; i2 < AT_D / 4; ++i2) {
+            const float4 v = __ldcg(reinterpret_cast<const float4*>(pr) + i2);
+            o[4 * i2 + 0] = o[4 * i2 + 0] * wa + v.x * wb;
+            o[4 * i2 + 1] = o[4 * i2 + 1] * wa + v.y * wb;
+            o[4 * i2 + 2] = o[4 * i2 + 2] * wa + v.z * wb;
+            o[4 * i2 + 3] = o[4 * i2 + 3] * wa + v.w * wb;
+          }
+          lt = lt * wa + lc * wb;
+          mt = mn;
+        }
+        m = mt;
+        l = lt;
+        if (row == 0) a.item_count[2 * sg.item + x] = 0;   // re-armed for the next launch
+      }
+    }
+    if (write_final) {
+      const float inv = (l > 0.f) ? 1.f / l : 0.f;
+      uint4* dst = reinterpret_cast<uint4*>(a.o + (((long long)sg.b * a.S_q + sq_idx) * a.H + sg.h) * AT_D);
+#pragma unroll
+      for (int i2 = 0; i2 < AT_D / 8; ++i2) {
         uint4 w;
-        w.x = pack_bf16x2(o[8 * i + 0] * inv, o[8 * i + 1] * inv);
-        w.y = pack_bf16x2(o[8 * i + 2] * inv, o[8 * i + 3] * inv);
-        w.z = pack_bf16x2(o[8 * i + 4] * inv, o[8 * i + 5] * inv);
-        w.w = pack_bf16x2(o[8 * i + 6] * inv, o[8 * i + 7] * inv);
-        dst[i] = w;
+        w.x = pack_bf16x2(o[8 * i2 + 0] * inv, o[8 * i2 + 1] * inv);
+        w.y = pack_bf16x2(o[8 * i2 + 2] * inv, o[8 * i2 + 3] * inv);
+        w.z = pack_bf16x2(o[8 * i2 + 4] * inv, o[8 * i2 + 5] * inv);
+        w.w = pack_bf16x2(o[8 * i2 + 6] * inv, o[8 * i2 + 7] * inv);
+        dst[i2] = w;
       }
       a.lse[srow] = (m + log2f(l)) * 0.69314718055994531f;
-    } else {
-      float4* og = reinterpret_cast<float4*>(a.o_acc + srow * AT_D);
-#pragma unroll
-      for (int i = 0; i < AT_D / 4; ++i) og[i] = make_float4(o[4 * i], o[4 * i + 1], o[4 * i + 2], o[4 * i + 3]);
-      a.m_acc[srow] = m;
-      a.l_acc[srow] = l;
     }
   }
   }
@@ -503,13 +628,46 @@ static int tmap_bshd(CUtensorMap* m, const void* p, int64_t B, int64_t S, int64_
   return PK_OK;
 }
 
-static int launch_attn(const AttnArgs& a, cudaStream_t st) {
+// Grid: one CTA per item when the items fill whole waves, else a persistent
+// stream-K grid of one CTA per SM sharing all key blocks evenly.
+static int launch_attn(AttnScratch& scr, int num_sms, AttnArgs& a, cudaStream_t st) {
   PK_TRY(ensure_smem_attr((const void*)attn_fwd_kernel, AT_SMEM));
-  const int grid = a.B * a.H * ((a.S_q / AT_BM + 1) / 2);
+  const int items = a.B * a.H * ((a.S_q / AT_BM + 1) / 2);
+  const int nblk = a.S_kv / AT_BN;
+  int sms = num_sms;
+  if (const char* e = getenv("PK_ATTN_SMS")) sms = std::max(1, atoi(e));   // tuning / test hook
+  // persistent grid of one CTA per SM: whole items in waves, the leftover
+  // items split evenly (one CTA per item when they fill whole waves)
+  int grid = items;
+  if (items % sms != 0 && nblk > 1 && !getenv("PK_ATTN_NO_SPLIT")) grid = sms;
+  const size_t part_bytes = (size_t)2 * grid * AT_PART_SLOT * sizeof(float);
+  if (scr.part_bytes < part_bytes) {
+    if (scr.part) PK_CUDA(cudaFreeAsync(scr.part, st));
+    PK_CUDA(cudaMallocAsync(&scr.part, part_bytes, st));
+    scr.part_bytes = part_bytes;
+  }
+  if (scr.count_n < (size_t)2 * items) {
+    if (scr.count) PK_CUDA(cudaFreeAsync(scr.count, st));
+    const size_t n = std::max<size_t>((size_t)2 * items, 4096);
+    PK_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&scr.count), n * sizeof(uint32_t), st));
+    PK_CUDA(cudaMemsetAsync(scr.count, 0, n * sizeof(uint32_t), st));
+    scr.count_n = n;
+  }
+  a.part = static_cast<float*>(scr.part);
+  a.item_count = scr.count;
   attn_fwd_kernel<<<grid, AT_THREADS, AT_SMEM, st>>>(a);
   PK_CUDA(cudaGetLastError());
   return PK_OK;
 }
+
+// Single-GPU attention (the compute step of one ring rank): q [B, S_q, H, D],
+// k / v [B, S_kv, H, D]. Scratch per (device, stream): launches on one stream
+// are ordered, so they can share the counters.
+static std::mutex g_attn_mu;
+static std::map<std::pair<int, cudaStream_t>, AttnScratch> g_attn_scratch;
+
+int attn_local(const pk_tensor* q, const pk_tensor* k, const pk_tensor* v, pk_tensor* o, pk_tensor* lse,
+               float scale, cudaStream_t st);
 
 enum { kScratchAttnK = 0, kScratchAttnV = 1, kScratchAttnStage = 7 };
 
@@ -541,10 +699,8 @@ int ring_attn_fwd(Comm* c, const pk_tensor* q, const pk_tensor* k, const pk_tens
   if (n == 1) {
     PK_TRY(tmap_bshd(&a.tm_k, k->ptr, B, S, H, AT_BN));
     PK_TRY(tmap_bshd(&a.tm_v, v->ptr, B, S, H, AT_BN));
-    a.first = 1;
-    a.last = 1;
     a.blocks_per_step = (int)(S / AT_BN);
-    return launch_attn(a, st);
+    return launch_attn(c->attn, c->num_sms, a, st);
   }
 
   // Every rank's K/V shard must be readable by its peers (symmetric memory).
@@ -619,16 +775,54 @@ int ring_attn_fwd(Comm* c, const pk_tensor* q, const pk_tensor* k, const pk_tens
   }
   a.err = static_cast<uint32_t*>(c->sync->local) + kSyncErr;
   a.timeout_ns = c->timeout_ns;
-  a.first = 1;
-  a.last = 1;
-  PK_TRY(launch_attn(a, st));
+  PK_TRY(launch_attn(c->attn, c->num_sms, a, st));
   // 4. wait until every peer is done with my shard before the caller may reuse it.
   PK_CUDA(cudaStreamWaitEvent(st, ev_side, 0));
   PK_TRY(wait_all(c, kSyncDone, c->done_count, st));
   return PK_OK;
 }
 
+int attn_local(const pk_tensor* q, const pk_tensor* k, const pk_tensor* v, pk_tensor* o, pk_tensor* lse,
+               float scale, cudaStream_t st) {
+  int64_t B, S, H, D, B2, S2, H2, D2;
+  PK_TRY(check_bshd(q, "q", &B, &S, &H, &D));
+  PK_TRY(check_bshd(o, "o", &B2, &S2, &H2, &D2));
+  if (B2 != B || S2 != S || H2 != H || D2 != D) return fail(PK_ERR_INVALID, "attention: o shape differs from q");
+  int64_t Skv;
+  PK_TRY(check_bshd(k, "k", &B2, &Skv, &H2, &D2));
+  if (B2 != B || H2 != H || D2 != D) return fail(PK_ERR_INVALID, "attention: k batch / heads / dim differ from q");
+  PK_TRY(check_bshd(v, "v", &B2, &S2, &H2, &D2));
+  if (B2 != B || S2 != Skv || H2 != H || D2 != D) return fail(PK_ERR_INVALID, "attention: v shape differs from k");
+  if (D != AT_D) return fail(PK_ERR_CAPABILITY, "attention: head dim %lld unsupported (128 only)", (long long)D);
+  if (S % AT_BM || Skv % AT_BN || Skv == 0)
+    return fail(PK_ERR_INVALID, "attention: sequence lengths must be multiples of 128 (q %lld, kv %lld)", (long long)S,
+                (long long)Skv);
+  if (!lse || !lse->ptr || lse->dtype != PK_F32 || lse->ndim != 3 || lse->shape[0] != B || lse->shape[1] != H ||
+      lse->shape[2] != S || lse->strides[2] != 1 || lse->strides[1] != S || lse->strides[0] != H * S)
+    return fail(PK_ERR_INVALID, "attention: lse must be contiguous float32 [B, H, S_q]");
+  int dev = 0, sms = 148;
+  PK_CUDA(cudaGetDevice(&dev));
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  AttnArgs a;
+  memset(&a, 0, sizeof(a));
+  a.B = (int)B; a.S_q = (int)S; a.S_kv = (int)Skv; a.H = (int)H;
+  a.scale_log2 = scale * 1.4426950408889634f;
+  a.o = static_cast<uint16_t*>(o->ptr);
+  a.lse = static_cast<float*>(lse->ptr);
+  a.blocks_per_step = (int)(Skv / AT_BN);
+  PK_TRY(tmap_bshd(&a.tm_q, q->ptr, B, S, H, AT_BM));
+  PK_TRY(tmap_bshd(&a.tm_k, k->ptr, B, Skv, H, AT_BN));
+  PK_TRY(tmap_bshd(&a.tm_v, v->ptr, B, Skv, H, AT_BN));
+  std::lock_guard<std::mutex> lk(g_attn_mu);
+  return launch_attn(g_attn_scratch[{dev, st}], sms, a, st);
+}
+
 }  // namespace pk
+
+extern "C" PK_API int pk_attn_fwd(const pk_tensor* q, const pk_tensor* k, const pk_tensor* v, pk_tensor* o,
+                                  pk_tensor* lse, float softmax_scale, void* stream) {
+  return pk::attn_local(q, k, v, o, lse, softmax_scale, (cudaStream_t)stream);
+}
 
 extern "C" PK_API int pk_ring_attn_fwd(pk_comm* comm, const pk_tensor* q, const pk_tensor* k, const pk_tensor* v,
                                        pk_tensor* o, pk_tensor* lse, float softmax_scale, const pk_sched* sched,

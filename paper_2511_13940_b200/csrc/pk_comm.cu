@@ -689,6 +689,8 @@ PK_API int pk_comm_destroy(pk_comm* c) {
   c->sync = nullptr;
   if (c->listen_fd >= 0) ::close(c->listen_fd);
   if (c->side) cudaStreamDestroy(c->side);
+  if (c->attn.part) cudaFree(c->attn.part);
+  if (c->attn.count) cudaFree(c->attn.count);
   for (auto& m : c->pending) if (m.fd >= 0) ::close(m.fd);
   LocalGroup* g = c->group;
   delete c;

@@ -108,6 +108,15 @@ struct Pgl {
 
 struct LocalGroup;
 
+// Stream-K attention scratch: partial (O, m, l) slots and per-(item, tile)
+// segment counters (zero between launches). Stream-ordered allocations.
+struct AttnScratch {
+  void* part = nullptr;
+  size_t part_bytes = 0;
+  uint32_t* count = nullptr;
+  size_t count_n = 0;
+};
+
 struct Comm {
   int rank = 0, world = 1, device = 0;
   bool local_group = false;          // single-process emulated peers
@@ -133,6 +142,7 @@ struct Comm {
   std::vector<Pgl*> user_pgls;       // PGLs handed out through pk_pgl_alloc (zero-copy lookup)
   std::vector<Pgl*> retired;         // outgrown scratch PGLs (local groups free them at destroy)
   cudaStream_t side = nullptr;       // side stream for copy-engine staging (ring attention)
+  AttnScratch attn;                  // ring attention: stream-K partials + per-item counters
 };
 
 // If [ptr, ptr+bytes) lies inside one of c's user PGLs, fill peers[] with the

@@ -229,6 +229,27 @@ def ring_attention(comm, q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, soft
     return out, lse
 
 
+def attention(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, softmax_scale: float | None = None,
+              out: torch.Tensor | None = None, lse: torch.Tensor | None = None, stream=None):
+    """Single-GPU non-causal attention, the compute step of one ring rank:
+    q [B, S_q, H, D], k / v [B, S_kv, H, D] bf16 (D = 128). Returns
+    (o [B, S_q, H, D] bf16, lse [B, H, S_q] fp32, natural log)."""
+    _require_cuda(q, k, v)
+    B, S, H, D = q.shape
+    if softmax_scale is None:
+        softmax_scale = D ** -0.5
+    if out is None:
+        out = torch.empty_like(q)
+    if lse is None:
+        lse = torch.empty((B, H, S), dtype=torch.float32, device=q.device)
+    lib = _lib.load()
+    dq, dk, dv, do, dl = (_lib.tensor_desc(x) for x in (q, k, v, out, lse))
+    import ctypes
+    check(lib.pk_attn_fwd(_lib.ref(dq), _lib.ref(dk), _lib.ref(dv), _lib.ref(do), _lib.ref(dl),
+                          ctypes.c_float(softmax_scale), ctypes_stream(_stream(stream))), "attention")
+    return out, lse
+
+
 def grouped_gemm(a: torch.Tensor, group_ids: torch.Tensor | None, w: torch.Tensor, out: torch.Tensor | None = None,
                  num_rows: torch.Tensor | None = None, schedule: dict | None = None, stream=None,
                  plan: torch.Tensor | None = None) -> torch.Tensor:

@@ -70,3 +70,37 @@ def test_ring_attention_rejects_bad_shapes():
         pk.ring_attention(comms[0], q64, q64, q64)
     for c in comms:
         c.destroy()
+
+
+@pytest.mark.parametrize("sms", [3, 5, 7])
+@pytest.mark.parametrize("world,S_loc,H", [(1, 1024, 3), (1, 384, 5), (2, 640, 3)])
+def test_stream_k_split_matches_oracle(monkeypatch, sms, world, S_loc, H):
+    """A persistent grid smaller than the item count cuts items between CTAs;
+    the last finisher of each item merges the partial (O, m, l) states."""
+    monkeypatch.setenv("PK_ATTN_SMS", str(sms))
+    run(world, 2, S_loc, H, seed=sms)
+    run(world, 2, S_loc, H, seed=sms + 1)          # the per-item counters re-arm between launches
+
+
+@pytest.mark.parametrize("B,Sq,Skv,H,sms", [(1, 256, 1024, 2, 0), (2, 384, 640, 3, 0), (1, 1024, 4096, 4, 5)])
+def test_local_attention_uneven_lengths(monkeypatch, B, Sq, Skv, H, sms):
+    """pk.attention: the compute step of one ring rank (S_q = S/n queries over S keys)."""
+    pk = _pk()
+    if sms:
+        monkeypatch.setenv("PK_ATTN_SMS", str(sms))
+    g = torch.Generator(device="cuda").manual_seed(Sq + Skv)
+    q = torch.randn(B, Sq, H, 128, device="cuda", generator=g).bfloat16()
+    k = torch.randn(B, Skv, H, 128, device="cuda", generator=g).bfloat16()
+    v = torch.randn(B, Skv, H, 128, device="cuda", generator=g).bfloat16()
+    o, lse = pk.attention(q, k, v)
+    torch.cuda.synchronize()
+    npy = lambda t: t.float().cpu().numpy()
+    ref_o, ref_l = oracle.attention_fwd(npy(q), npy(k), npy(v), 128 ** -0.5)
+    assert np.abs(npy(o) - ref_o).max() <= 2e-2
+    assert np.abs(lse.cpu().numpy() - ref_l).max() <= 1e-3 * max(1.0, np.abs(ref_l).max())
+
+
+def test_stream_k_more_ctas_than_tail_blocks(monkeypatch):
+    """Fewer tail key blocks than CTAs: some CTAs own nothing, items split one block per CTA."""
+    monkeypatch.setenv("PK_ATTN_SMS", "40")
+    run(1, 1, 512, 3, seed=9)        # 6 items x 4 blocks = 24 tail blocks over 40 CTAs
