@@ -19,6 +19,7 @@ _os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
 from .errors import (DeadlockError, LcscError, MemSimError, MulticastReadError,  # noqa: F401
                      PkCudaError, PkError, PrimitiveError, ProtocolViolation, WorkloadError)
 from .comm import Comm, Pgl, local_group  # noqa: F401
+from . import tune  # noqa: F401
 from .ops import (all_gather, all_gather_gemm, attention, all_reduce, all_to_all, gemm, gemm_all_reduce,  # noqa: F401
                   gemm_reduce_scatter, grouped_gemm, moe_capacity, moe_combine, moe_dispatch, reduce_scatter,
                   ring_attention,

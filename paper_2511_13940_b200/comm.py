@@ -89,6 +89,10 @@ class Comm:
         self.has_multicast = bool(mc.value)
         self._pgls: list[Pgl] = []
         self._keep = keepalive
+        self.is_local_group = False
+        n = ctypes.c_int()
+        check(lib.pk_num_sms(device, ctypes.byref(n)), "num_sms")
+        self.num_sms = n.value                   # SMs this rank's kernels may occupy
 
     # ------------------------------------------------------------------ construction
     @classmethod
@@ -157,4 +161,9 @@ def local_group(world: int, device: int = 0) -> list[Comm]:
     lib = _lib.load()
     arr = (ctypes.c_void_p * world)()
     check(lib.pk_comm_init_local(world, device, arr), "comm_init_local")
-    return [Comm(ctypes.c_void_p(arr[i]), device) for i in range(world)]
+    comms = [Comm(ctypes.c_void_p(arr[i]), device) for i in range(world)]
+    for c in comms:
+        c.is_local_group = True
+        if world > 1:
+            c.num_sms = max(2, (c.num_sms // world) & ~1)   # pk_comm.cu: co-resident share per rank
+    return comms

@@ -681,3 +681,59 @@ def check_oracle(plan: WorkloadPlan):
                 idx = np.argwhere(exp != got)[0]
                 return name, (dev, *map(int, idx))
     return None
+
+
+# -- SM-partition autotuning (lcsc.py:164-191) --------------------------------
+
+def autotune_partition(spec: LcscKernelSpec, workload_factory, profile=None, stride: int = 1,
+                       overheads=None, seed: int = 0, max_comm_sms: Optional[int] = None, comms=None):
+    """Sweep the communicator-SM count of a dedicated-SM schedule by running
+    the plan on the GPU for every count (lcsc.py:164-191). Returns (best
+    count, [(num_comm_sms, t_total_ns, achieved_flops)]); ties break toward
+    fewer communication SMs. `t_total_ns` is execute_kernel's measured time.
+    For real shapes, tune.sweep / `python -m paper_2511_13940_b200.tune` time
+    the fused ops with CUDA events instead."""
+    from dataclasses import replace
+    if spec.schedule_mode is not ScheduleMode.INTER_SM:
+        raise LcscError("partition sweep applies to dedicated-SM scheduling")
+    if stride < 1:
+        raise LcscError("stride must be at least 1")
+    hi = max_comm_sms if max_comm_sms is not None else B200_SMS - 1
+    hi = min(hi, B200_SMS - 1)
+    table = []
+    best_k, best_t = None, None
+    for k in range(1, hi + 1, stride):
+        res = execute_kernel(replace(spec, num_comm_sms=k), workload_factory(), profile, overheads=overheads,
+                             seed=seed, comms=comms)
+        row = (k, res.report.t_total, res.report.achieved_flops)
+        table.append(row)
+        if best_t is None or row[1] < best_t:
+            best_k, best_t = k, row[1]
+    return best_k, table
+
+
+def sweep_table_csv(table) -> str:                # lcsc.py:194-198
+    lines = ["num_comm_sms,t_total_ns,achieved_flops"]
+    for k, t, fl in table:
+        lines.append(f"{k},{t:.6g},{fl:.6g}")
+    return "\n".join(lines) + "\n"
+
+
+class ReusePolicy(Enum):                           # lcsc.py:203-205
+    DIRECT_REMOTE_READ = "direct_remote_read"
+    STAGE_TO_LOCAL_HBM = "stage_to_local_hbm"
+
+
+def remote_reuse_policy(reuse_count: int, nbytes: float, link_bandwidth_B: float = 770e9,
+                        hbm_bandwidth: float = 6.5e12) -> ReusePolicy:
+    """Re-read a peer buffer k times vs stage it once (lcsc.py:208-223). The
+    AG-GEMM launcher applies this rule: with more than one 256-wide N tile the
+    gathered rows are re-read, so the inter-SM schedule stages them locally.
+    Defaults: measured B200 peer-copy and HBM bandwidths."""
+    if reuse_count < 0:
+        raise LcscError("reuse count must be nonnegative")
+    if reuse_count <= 1:
+        return ReusePolicy.DIRECT_REMOTE_READ
+    direct = reuse_count * nbytes / link_bandwidth_B
+    staged = nbytes / link_bandwidth_B + reuse_count * nbytes / hbm_bandwidth
+    return ReusePolicy.STAGE_TO_LOCAL_HBM if staged < direct else ReusePolicy.DIRECT_REMOTE_READ

@@ -67,34 +67,37 @@ struct AttnArgs {
   uint64_t timeout_ns;
   uint16_t* o;                   // [B, S_q, H, D] bf16 output
   float* lse;                    // [B, H, S_q] natural-log LSE
-  // stream-K work split: gridDim.x CTAs share items * nblk key blocks evenly;
+  // partial-last-wave split (AtSplit): the tail CTAs share the last items' key blocks;
   // an item cut between CTAs is merged by whichever of them finishes last
-  float* part;                   // [2 * grid] slots of [2 tiles][128 rows][D + 2] fp32 (O, m, l)
+  float* part;                   // [2 * tail_units] slots of [2 tiles][128 rows][D + 4] fp32 (O, m, l)
   uint32_t* item_count;          // [items * 2] segments finished per (item, tile); re-armed by the merger
+  int tail_items;                // R: the last R items are split over tail_units CTAs (0: no split)
+  int tail_units;
 };
 
 // Partial state of one (slot, tile, row): D floats of unnormalised O, then m, l.
 constexpr int AT_PART_ROW = AT_D + 4;            // padded to 16 B (float4 rows)
 constexpr int AT_PART_SLOT = 2 * AT_BM * AT_PART_ROW;
 
-// Work split over G persistent CTAs (data-parallel waves + a stream-K tail):
-// items = Q*G + R. CTA c first runs the whole items c, c + G, ..., c + (Q-1)G
-// — the CTAs in flight work on consecutive items (the same heads, so the K/V
-// they stream stays in L2) — then shares the R tail items' key blocks evenly:
-// tail block range [tstart(c), tstart(c+1)) of T = R * nblk. A segment is the
-// part of one item a CTA owns; only tail items are ever cut.
+// Work split: one CTA per item, except that the last R = items mod (SMs)
+// items — the partial last wave — are cut evenly over U = SMs tail CTAs (the
+// last wave then keeps every SM busy for R/U of an item instead of leaving
+// U - R idle). Tail CTA u owns the tail key blocks [tstart(u), tstart(u+1))
+// of T = R * nblk; a CTA's share can span two items (two segments). CTAs are
+// launched in item order, so the CTAs in flight work on consecutive items
+// (the same heads: the K/V they stream stays in L2).
 struct AtSplit {
-  int G, nblk, Q, R;
-  long long T;
-  PK_DEV long long tstart(int c) const { return (long long)c * T / G; }
-  PK_DEV int tcta_of(long long p) const {      // the CTA whose tail range holds tail block p
-    int c = (int)(((p + 1) * (long long)G - 1) / T);
+  uint32_t G, nblk;                              // G = tail CTAs
+  uint32_t T;                                    // host guarantees G * T < 2^32 (32-bit divisions)
+  PK_DEV uint32_t tstart(uint32_t c) const { return c * T / G; }
+  PK_DEV int tcta_of(uint32_t p) const {       // the tail CTA whose range holds tail block p
+    uint32_t c = ((p + 1) * G - 1) / T;
     while (c > 0 && tstart(c) > p) --c;
     while (c + 1 < G && tstart(c + 1) <= p) ++c;
-    return c;
+    return (int)c;
   }
-  // partial slot of CTA c's segment of tail item ti: its first segment 2c, else 2c + 1
-  PK_DEV int slot(int c, int ti) const { return (tstart(c) / nblk == ti) ? 2 * c : 2 * c + 1; }
+  // partial slot of tail CTA c's segment of tail item ti: its first segment 2c, else 2c + 1
+  PK_DEV int slot(int c, int ti) const { return ((int)(tstart(c) / nblk) == ti) ? 2 * c : 2 * c + 1; }
 };
 
 // MN-major (N contiguous) SW128 descriptor for the V operand: 64-element
@@ -201,35 +204,32 @@ __global__ void __launch_bounds__(AT_THREADS, 1) attn_fwd_kernel(const __grid_co
   const int nblk = a.S_kv / AT_BN;
   const int items = a.B * a.H * pairs;
   AtSplit sp;
-  sp.G = (int)gridDim.x;
-  sp.nblk = nblk;
-  sp.Q = items / sp.G;
-  sp.R = items - sp.Q * sp.G;
-  sp.T = (long long)sp.R * nblk;
-  const int me = (int)blockIdx.x;
-  const long long t0 = sp.tstart(me), t1 = sp.tstart(me + 1);
-  // segment walk shared by every role: item, key blocks [j0, j1), pair shape;
-  // cursor k < Q: whole item k*G + me; then tail blocks from t0 to t1
+  sp.G = a.tail_units > 0 ? (uint32_t)a.tail_units : 1u;
+  sp.nblk = (uint32_t)nblk;
+  sp.T = (uint32_t)a.tail_items * (uint32_t)nblk;
+  const int nfull = items - a.tail_items;           // CTAs [0, nfull) run whole items
+  const int me = (int)blockIdx.x - nfull;           // tail CTA index (< 0: a whole-item CTA)
+  const int t0 = me >= 0 ? (int)sp.tstart(me) : 0, t1 = me >= 0 ? (int)sp.tstart(me + 1) : 0;
+  // segment walk shared by every role: item, key blocks [j0, j1), pair shape
   struct SegInfo { int item, ti, j0, j1, qp, h, b, ntile; };
   struct SegIter {
-    long long k;                                     // wave index, then Q + tail block position
+    int k;                                           // -1: the whole item pending, -2: done; else tail block
   };
   auto seg_next = [&](SegIter& it, SegInfo& g) -> bool {
-    if (it.k < sp.Q) {
-      g.item = (int)it.k * sp.G + me;
+    if (it.k == -2) return false;
+    if (it.k == -1) {
+      g.item = (int)blockIdx.x;
       g.ti = -1;
       g.j0 = 0;
       g.j1 = nblk;
-      ++it.k;
-      if (it.k == sp.Q) it.k = sp.Q + t0;            // continue with the tail
+      it.k = -2;
     } else {
-      const long long p = it.k - sp.Q;
-      if (p >= t1) return false;
-      g.ti = (int)(p / nblk);
-      g.item = sp.Q * sp.G + g.ti;
-      g.j0 = (int)(p - (long long)g.ti * nblk);
-      g.j1 = (int)min((long long)nblk, t1 - (long long)g.ti * nblk);
-      it.k = sp.Q + (long long)g.ti * nblk + g.j1;
+      if (it.k >= t1) return false;
+      g.ti = it.k / nblk;
+      g.item = nfull + g.ti;
+      g.j0 = it.k - g.ti * nblk;
+      g.j1 = min(nblk, t1 - g.ti * nblk);
+      it.k = g.ti * nblk + g.j1;
     }
     g.qp = g.item % pairs;
     g.h = (g.item / pairs) % a.H;
@@ -237,7 +237,7 @@ __global__ void __launch_bounds__(AT_THREADS, 1) attn_fwd_kernel(const __grid_co
     g.ntile = (2 * g.qp + 1 < q_tiles) ? 2 : 1;      // the last pair may hold one tile
     return true;
   };
-  auto seg_begin = [&]() { SegIter it; it.k = sp.Q > 0 ? 0 : t0; return it; };
+  auto seg_begin = [&]() { SegIter it; it.k = me < 0 ? -1 : t0; return it; };
 
   if (warp == 0 && lane == 0) {
     mbar_init(q_full, 1);
@@ -338,7 +338,9 @@ __global__ void __launch_bounds__(AT_THREADS, 1) attn_fwd_kernel(const __grid_co
       }
     };
     int g = 0, seg = 0;
-    int gx[2] = {0, 0}, segx[2] = {0, 0};
+    // per-tile block / segment counts as scalars (a runtime-indexed array
+    // would live in local memory on the MMA issuer's critical path)
+    int gx0 = 0, gx1 = 0, segx0 = 0, segx1 = 0;
     SegIter it = seg_begin();
     for (SegInfo sg; seg_next(it, sg); ++seg) {
       const int len = sg.j1 - sg.j0;
@@ -356,14 +358,15 @@ __global__ void __launch_bounds__(AT_THREADS, 1) attn_fwd_kernel(const __grid_co
         const bool more = i + 1 < len;
         if (more) mbar_wait(&k_full[(gg + 1) & 1], ((gg + 1) >> 1) & 1);
         for (int x = 0; x < sg.ntile; ++x) {
+          const int gxx = x ? gx1 : gx0, sgx = x ? segx1 : segx0;
           // O_x of the previous segment must have been read by its epilogue
-          if (i == 0 && segx[x] > 0) mbar_wait(&o_empty[x], (segx[x] - 1) & 1);
+          if (i == 0 && sgx > 0) mbar_wait(&o_empty[x], (sgx - 1) & 1);
           // the first half of P is consumed while the softmax still works on the second
-          mbar_wait(&p_full[2 * x], gx[x] & 1);
+          mbar_wait(&p_full[2 * x], gxx & 1);
           tc_fence_after();
           if (elect_one()) issue_pv(x, gg, 0, i == 0);
           __syncwarp();
-          mbar_wait(&p_full[2 * x + 1], gx[x] & 1);
+          mbar_wait(&p_full[2 * x + 1], gxx & 1);
           tc_fence_after();
           if (elect_one()) {
             issue_pv(x, gg, 1, i == 0);
@@ -371,8 +374,9 @@ __global__ void __launch_bounds__(AT_THREADS, 1) attn_fwd_kernel(const __grid_co
             else umma_commit<1>(&o_full[x]);
           }
           __syncwarp();
-          ++gx[x];
         }
+        ++gx0;
+        gx1 += sg.ntile > 1;
         if (elect_one()) {
           umma_commit<1>(&v_empty[gg & 1]);
           if (more) umma_commit<1>(&k_empty[(gg + 1) & 1]);
@@ -380,7 +384,8 @@ __global__ void __launch_bounds__(AT_THREADS, 1) attn_fwd_kernel(const __grid_co
         }
         __syncwarp();
       }
-      for (int x = 0; x < sg.ntile; ++x) ++segx[x];
+      ++segx0;
+      segx1 += sg.ntile > 1;
       g += len;
     }
   }
@@ -491,7 +496,7 @@ __global__ void __launch_bounds__(AT_THREADS, 1) attn_fwd_kernel(const __grid_co
     const int sq_idx = (2 * sg.qp + x) * AT_BM + row;                      // query index within the local shard
     const long long srow = ((long long)(sg.b * a.H + sg.h) * a.S_q + sq_idx);   // [B, H, S_q] row
     bool write_final = true;
-    const long long ib = (long long)sg.ti * nblk;              // tail items only
+    const uint32_t ib = (uint32_t)(sg.ti * nblk);              // tail items only
     const int c_lo = (sg.ti < 0 || sg.j0 == 0) ? me : sp.tcta_of(ib);
     const int c_hi = (sg.ti < 0 || sg.j1 == nblk) ? me : sp.tcta_of(ib + nblk - 1);
     if (c_lo != c_hi) {
@@ -636,11 +641,15 @@ static int launch_attn(AttnScratch& scr, int num_sms, AttnArgs& a, cudaStream_t 
   const int nblk = a.S_kv / AT_BN;
   int sms = num_sms;
   if (const char* e = getenv("PK_ATTN_SMS")) sms = std::max(1, atoi(e));   // tuning / test hook
-  // persistent grid of one CTA per SM: whole items in waves, the leftover
-  // items split evenly (one CTA per item when they fill whole waves)
-  int grid = items;
-  if (items % sms != 0 && nblk > 1 && !getenv("PK_ATTN_NO_SPLIT")) grid = sms;
-  const size_t part_bytes = (size_t)2 * grid * AT_PART_SLOT * sizeof(float);
+  // split the partial last wave when the items are long enough for the
+  // partial-state write and merge to pay (measured: not at 32 key blocks)
+  int min_blocks = 64;
+  if (const char* e = getenv("PK_ATTN_SPLIT_MIN_BLOCKS")) min_blocks = atoi(e);   // test hook
+  a.tail_items = (nblk >= min_blocks && !getenv("PK_ATTN_NO_SPLIT")) ? items % sms : 0;
+  if ((uint64_t)sms * ((uint64_t)a.tail_items * nblk + 1) >= (1ull << 32)) a.tail_items = 0;   // 32-bit split math
+  a.tail_units = a.tail_items ? sms : 0;
+  const int grid = items - a.tail_items + a.tail_units;
+  const size_t part_bytes = (size_t)2 * std::max(1, a.tail_units) * AT_PART_SLOT * sizeof(float);
   if (scr.part_bytes < part_bytes) {
     if (scr.part) PK_CUDA(cudaFreeAsync(scr.part, st));
     PK_CUDA(cudaMallocAsync(&scr.part, part_bytes, st));

@@ -11,7 +11,7 @@ from __future__ import annotations
 
 import torch
 
-from . import _lib
+from . import _lib, tune
 from .errors import WorkloadError, check
 
 
@@ -76,6 +76,8 @@ def all_gather_gemm(comm, a_shard: torch.Tensor, b: torch.Tensor, out: torch.Ten
     lib = _lib.load()
     da, db, dc = _lib.tensor_desc(a_shard), _lib.tensor_desc(b), _lib.tensor_desc(out)
     dg = _lib.tensor_desc(a_gathered) if a_gathered is not None else None
+    if schedule is None and comm.world > 1:
+        schedule = tune.auto_schedule("ag_gemm", comm.world, m, b.shape[0] * comm.world, a_shard.shape[1])
     sc = _sched(schedule)
     check(lib.pk_ag_gemm(comm._h, _lib.ref(da), _lib.ref(db), _lib.ref(dc), _lib.ref(dg), _lib.ref(sc),
                          ctypes_stream(_stream(stream))), "all_gather_gemm")
@@ -90,6 +92,8 @@ def gemm_reduce_scatter(comm, a: torch.Tensor, b: torch.Tensor, out: torch.Tenso
         out = torch.empty((a.shape[0] // comm.world, b.shape[0]), dtype=torch.bfloat16, device=a.device)
     lib = _lib.load()
     da, db, do = _lib.tensor_desc(a), _lib.tensor_desc(b), _lib.tensor_desc(out)
+    if schedule is None and comm.world > 1:
+        schedule = tune.auto_schedule("gemm_rs", comm.world, a.shape[0], b.shape[0], a.shape[1] * comm.world)
     sc = _sched(schedule)
     check(lib.pk_gemm_rs(comm._h, _lib.ref(da), _lib.ref(db), _lib.ref(do), _lib.ref(sc),
                          ctypes_stream(_stream(stream))), "gemm_reduce_scatter")
@@ -107,6 +111,8 @@ def gemm_all_reduce(comm, a: torch.Tensor, b: torch.Tensor, out: torch.Tensor | 
         out = comm.empty((a.shape[0], b.shape[0]), torch.bfloat16, multicast=comm.has_multicast)
     lib = _lib.load()
     da, db, do = _lib.tensor_desc(a), _lib.tensor_desc(b), _lib.tensor_desc(out)
+    if schedule is None and comm.world > 1:
+        schedule = tune.auto_schedule("gemm_ar", comm.world, a.shape[0], b.shape[0], a.shape[1])
     check(lib.pk_gemm_ar(comm._h, _lib.ref(da), _lib.ref(db), _lib.ref(do), _lib.ref(_sched(schedule)),
                          ctypes_stream(_stream(stream))), "gemm_all_reduce")
     return out
