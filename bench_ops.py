@@ -137,7 +137,7 @@ def main():
         qt, kt, vt = (x.transpose(1, 2).contiguous() for x in (q, k, v))
         ms_sdpa = timeit(lambda: torch.nn.functional.scaled_dot_product_attention(qt, kt, vt), iters=5)
         emit(out, **tensor_line("attention_rank_step_n8", flops, ms, shape=[B, S // n, S, H, D],
-                                ms_no_stream_k=ms_ns, sdpa_ms=ms_sdpa, vs_sdpa=ms_sdpa / ms))
+                                ms_no_split=ms_ns, sdpa_ms=ms_sdpa, vs_sdpa=ms_sdpa / ms))
         del q, k, v, o, qt, kt, vt
 
     # ---------------------------------------------------------------- MoE (n = 1): dispatch, grouped GEMM, combine

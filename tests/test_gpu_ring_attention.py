@@ -78,7 +78,7 @@ def test_stream_k_split_matches_oracle(monkeypatch, sms, world, S_loc, H):
     """A persistent grid smaller than the item count cuts items between CTAs;
     the last finisher of each item merges the partial (O, m, l) states."""
     monkeypatch.setenv("PK_ATTN_SMS", str(sms))
-    monkeypatch.setenv("PK_ATTN_SPLIT_MIN_BLOCKS", "1")
+    monkeypatch.setenv("PK_ATTN_FORCE_SPLIT", "1")
     run(world, 2, S_loc, H, seed=sms)
     run(world, 2, S_loc, H, seed=sms + 1)          # the per-item counters re-arm between launches
 
@@ -89,7 +89,7 @@ def test_local_attention_uneven_lengths(monkeypatch, B, Sq, Skv, H, sms):
     pk = _pk()
     if sms:
         monkeypatch.setenv("PK_ATTN_SMS", str(sms))
-        monkeypatch.setenv("PK_ATTN_SPLIT_MIN_BLOCKS", "1")
+        monkeypatch.setenv("PK_ATTN_FORCE_SPLIT", "1")
     g = torch.Generator(device="cuda").manual_seed(Sq + Skv)
     q = torch.randn(B, Sq, H, 128, device="cuda", generator=g).bfloat16()
     k = torch.randn(B, Skv, H, 128, device="cuda", generator=g).bfloat16()
@@ -105,5 +105,5 @@ def test_local_attention_uneven_lengths(monkeypatch, B, Sq, Skv, H, sms):
 def test_stream_k_more_ctas_than_tail_blocks(monkeypatch):
     """Fewer tail key blocks than CTAs: some CTAs own nothing, items split one block per CTA."""
     monkeypatch.setenv("PK_ATTN_SMS", "40")
-    monkeypatch.setenv("PK_ATTN_SPLIT_MIN_BLOCKS", "1")
+    monkeypatch.setenv("PK_ATTN_FORCE_SPLIT", "1")
     run(1, 1, 512, 3, seed=9)        # 6 items x 4 blocks = 24 tail blocks over 40 CTAs
