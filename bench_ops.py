@@ -101,7 +101,7 @@ def main():
     c1 = pk.local_group(1)[0]
 
     # ---------------------------------------------------------------- GEMM (n = 1 AG-GEMM / GEMM-RS)
-    for S in ([8192] if args.quick else [8192, 16384]) if want("gemm") else []:
+    for S in ([8192] if args.quick else [4096, 8192, 16384, 32768]) if want("gemm") else []:
         a = torch.randn(S, S, device=dev).bfloat16()
         b = torch.randn(S, S, device=dev).bfloat16()
         c = torch.empty(S, S, device=dev, dtype=torch.bfloat16)

@@ -110,6 +110,11 @@ PK_API int pk_comm_check(pk_comm* comm, int* code);
 /* Diagnostics: host-only self test of the multi-process rendezvous (rank-id
  * allgather, barrier, SCM_RIGHTS fd exchange). Needs no GPU. */
 PK_API int pk_debug_rendezvous(int rank, int world, const char* uid);
+/* Diagnostic: run multimem.ld_reduce / multimem.st / multimem.red once over a
+ * multicast PGL laid out as [nvec x 16 B data][nvec x 16 B result][u32
+ * counter] (see pk_allreduce.cu mm_selftest_kernel). PK_ERR_CAPABILITY when
+ * the PGL has no multicast VA. */
+PK_API int pk_debug_multimem(pk_comm* comm, pk_pgl* pgl, size_t nvec, void* stream);
 
 /* ---- parallel global layouts --------------------------------------------- */
 PK_API int pk_pgl_alloc(pk_comm* comm, size_t bytes, uint32_t flags, pk_pgl** out);

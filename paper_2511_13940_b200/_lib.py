@@ -28,7 +28,7 @@ PK_BF16, PK_F32, PK_F16, PK_I32, PK_I64, PK_U8 = range(6)
 EXPORTS = (
     "pk_last_error", "pk_version", "pk_num_sms",
     "pk_comm_init", "pk_comm_init_local", "pk_comm_destroy", "pk_comm_rank",
-    "pk_comm_has_multicast", "pk_comm_set_timeout", "pk_comm_check", "pk_debug_rendezvous",
+    "pk_comm_has_multicast", "pk_comm_set_timeout", "pk_comm_check", "pk_debug_rendezvous", "pk_debug_multimem",
     "pk_pgl_alloc", "pk_pgl_ptrs", "pk_pgl_free",
     "pk_gemm", "pk_ag_gemm", "pk_gemm_rs", "pk_gemm_ar", "pk_all_reduce",
     "pk_ring_attn_fwd", "pk_attn_fwd", "pk_moe_dispatch", "pk_moe_dispatch_ex", "pk_moe_combine", "pk_grouped_gemm",

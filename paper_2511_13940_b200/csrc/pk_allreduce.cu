@@ -279,7 +279,47 @@ int all_reduce(Comm* c, pk_tensor* x, int op, const pk_sched* sched, cudaStream_
   return PK_OK;
 }
 
+// ---------------------------------------------------------------- NVLS self-test
+// Exercises the three multimem primitives on a multicast PGL of this comm:
+// for every 16 B vector v of [0, nvec): res[v] = ld_reduce(mc[v]) (f32 add
+// over every bound device), then mc[v] = 2 * res[v] through a multicast
+// store; one multicast red.add bumps the counter word after the data. With a
+// world-1 comm the reduction is the identity, so the caller checks res ==
+// data, data == 2 * old data and counter + 1 — the instruction encodings,
+// the multicast mapping and the sys-scope ordering on real hardware.
+__global__ void mm_selftest_kernel(uint8_t* mc, uint8_t* local, long long nvec) {
+  uint8_t* res = local + nvec * 16;
+  for (long long v = blockIdx.x * (long long)blockDim.x + threadIdx.x; v < nvec; v += (long long)gridDim.x * blockDim.x) {
+    uint32_t r[4];
+    mm_ld_reduce_f32x4(mc + v * 16, r);
+    st_v4(res + v * 16, make_uint4(r[0], r[1], r[2], r[3]));
+    uint32_t w[4];
+    for (int e = 0; e < 4; ++e) w[e] = __float_as_uint(2.f * __uint_as_float(r[e]));
+    mm_st_v4(mc + v * 16, w);
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    __threadfence_system();
+    mm_signal_add(reinterpret_cast<uint32_t*>(mc + 2 * nvec * 16), 1u);
+  }
+}
+
+int debug_multimem(Comm* c, Pgl* p, size_t nvec, cudaStream_t st) {
+  if (!p || !p->mc) return fail(PK_ERR_CAPABILITY, "debug_multimem: the PGL has no multicast VA");
+  if (p->bytes < 2 * nvec * 16 + 16) return fail(PK_ERR_INVALID, "debug_multimem: PGL smaller than 2 * nvec * 16 + 16 bytes");
+  (void)c;
+  const int blocks = (int)std::min<size_t>(1184, (nvec + 255) / 256 + 1);
+  mm_selftest_kernel<<<blocks, 256, 0, st>>>(static_cast<uint8_t*>(p->mc), static_cast<uint8_t*>(p->local),
+                                             (long long)nvec);
+  PK_CUDA(cudaGetLastError());
+  return PK_OK;
+}
+
 }  // namespace pk
+
+extern "C" PK_API int pk_debug_multimem(pk_comm* comm, pk_pgl* pgl, size_t nvec, void* stream) {
+  if (!comm) return pk::fail(PK_ERR_INVALID, "null comm");
+  return pk::debug_multimem(comm, pgl, nvec, (cudaStream_t)stream);
+}
 
 extern "C" PK_API int pk_all_reduce(pk_comm* comm, pk_tensor* x, int op, const pk_sched* sched, void* stream) {
   if (!comm) return pk::fail(PK_ERR_INVALID, "null comm");

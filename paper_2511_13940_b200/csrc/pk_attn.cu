@@ -50,6 +50,9 @@ constexpr int AT_VSTAGES = 2;
 constexpr int AT_SMEM = 2 * AT_Q_BYTES + AT_KSTAGES * AT_K_BYTES + AT_VSTAGES * AT_V_BYTES + 512 + 1024;
 constexpr int AT_TMEM_COLS = 512;                // per tile: S (128, P aliased in its first 64) + O (128)
 constexpr float AT_RESCALE_THRESHOLD = 8.0f;     // log2 units: P stays <= 2^8 between rescales
+#ifndef AT_POLY_DEG
+#define AT_POLY_DEG 3                            // degree of the FMA-pipe 2^f polynomial
+#endif
 #ifndef AT_EXP_EMU
 #define AT_EXP_EMU 1                             // of every 4 key pairs, this many take 2^x on the FMA pipe (MUFU offload)
 #endif
@@ -145,9 +148,15 @@ PK_DEV void poly_exp2x2(float x0, float x1, float& p0, float& p1) {
   const uint64_t big = f2_pack(12582912.f, 12582912.f);
   const uint64_t t2 = f2_add(x2, big);
   const uint64_t f2 = f2_add(x2, f2_fma(t2, f2_pack(-1.f, -1.f), big));
+#if AT_POLY_DEG == 2
+  // degree 2 (rel. error 1.7e-3, under bf16's 2^-9 rounding of P): one FFMA2 less
+  uint64_t q = f2_fma(f2_pack(2.3842697e-1f, 2.3842697e-1f), f2, f2_pack(7.034453e-1f, 7.034453e-1f));
+  q = f2_fma(q, f2, f2_pack(1.00044307f, 1.00044307f));
+#else
   uint64_t q = f2_fma(f2_pack(5.5171456e-2f, 5.5171456e-2f), f2, f2_pack(2.4261115e-1f, 2.4261115e-1f));
   q = f2_fma(q, f2, f2_pack(6.9326103e-1f, 6.9326103e-1f));
   q = f2_fma(q, f2, f2_pack(9.9992806e-1f, 9.9992806e-1f));
+#endif
   float q0, q1, t0, t1;
   f2_unpack(q, q0, q1);
   f2_unpack(t2, t0, t1);

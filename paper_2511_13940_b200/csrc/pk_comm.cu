@@ -497,14 +497,31 @@ bool find_symmetric(Comm* c, const void* ptr, size_t bytes, void** peers) {
   return false;
 }
 
-static int query_multicast(int device, bool* out) {
+// Multicast (NVLS) is usable only if the device says so AND a multicast
+// object for `ndev` devices can actually be created: a GPU can report the
+// attribute while its fabric is not reachable (measured on this pool's
+// single-GPU boxes: cuMulticastCreate -> CUDA_ERROR_INVALID_VALUE for every
+// handle type), in which case every multicast PGL would fail later.
+static int query_multicast(int device, bool* out, int ndev) {
   *out = false;
   const Driver* d;
-  if (driver(&d) != PK_OK || !d->multicastCreate) return PK_OK;
+  if (driver(&d) != PK_OK || !d->multicastCreate || !d->multicastGetGranularity) return PK_OK;
   CUdevice cudev;
   if (d->deviceGet(&cudev, device) != CUDA_SUCCESS) return PK_OK;
   int v = 0;
-  if (d->deviceGetAttribute(&v, CU_DEVICE_ATTRIBUTE_MULTICAST_SUPPORTED, cudev) == CUDA_SUCCESS) *out = v != 0;
+  if (d->deviceGetAttribute(&v, CU_DEVICE_ATTRIBUTE_MULTICAST_SUPPORTED, cudev) != CUDA_SUCCESS || !v) return PK_OK;
+  CUmulticastObjectProp mprop;
+  memset(&mprop, 0, sizeof(mprop));
+  mprop.numDevices = (unsigned)std::max(ndev, 1);
+  mprop.handleTypes = CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR;
+  mprop.size = 2u << 20;
+  size_t g = 0;
+  if (d->multicastGetGranularity(&g, &mprop, CU_MULTICAST_GRANULARITY_RECOMMENDED) == CUDA_SUCCESS && g > mprop.size)
+    mprop.size = g;
+  CUmemGenericAllocationHandle h;
+  if (d->multicastCreate(&h, &mprop) != CUDA_SUCCESS) return PK_OK;
+  d->memRelease(h);
+  *out = true;
   return PK_OK;
 }
 
@@ -625,7 +642,7 @@ PK_API int pk_comm_init(int rank, int world, int device, const char* uid, pk_com
   c->uid = uid;
   cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device);
   bool mc = false;
-  query_multicast(device, &mc);
+  if (world > 1) query_multicast(device, &mc, world);
   c->multicast_supported = mc && world > 1;
   if (world > 1) {
     int st = open_listener(c);
@@ -641,6 +658,12 @@ PK_API int pk_comm_init(int rank, int world, int device, const char* uid, pk_com
     for (int i = 0; i < world; ++i)
       for (int j = i + 1; j < world; ++j)
         if (memcmp(&ids[i], &ids[j], sizeof(cudaUUID_t)) == 0) c->multicast_supported = false;
+    // every rank must agree (PGL allocation is collective)
+    int mine = c->multicast_supported ? 1 : 0;
+    std::vector<int> all(world);
+    st = comm_allgather(c, &mine, all.data(), sizeof(int));
+    if (st != PK_OK) { ::close(c->listen_fd); delete c; return st; }
+    for (int r = 0; r < world; ++r) if (!all[r]) c->multicast_supported = false;
   }
   int st = comm_finish_init(c);
   if (st != PK_OK) { if (c->listen_fd >= 0) ::close(c->listen_fd); delete c; return st; }
@@ -657,7 +680,7 @@ PK_API int pk_comm_init_local(int world, int device, pk_comm** comms_out) {
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
   bool mc = false;
-  query_multicast(device, &mc);
+  if (world == 1) query_multicast(device, &mc, 1);
   for (int r = 0; r < world; ++r) {
     pk_comm* c = new pk_comm();
     c->rank = r;

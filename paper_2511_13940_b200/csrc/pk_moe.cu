@@ -60,7 +60,7 @@ struct MoeArgs {
   int32_t* slot_of;             // [T * k] absolute slot on the owner (-1: dropped)
   int grid;                     // number of chunks G
   int tpc;                      // tokens per chunk (one count / dispatch CTA per chunk)
-  int32_t* chunk_counts;        // [G, nkeys] entries per (chunk, key) -> exclusive prefix over chunks
+  int32_t* chunk_counts;        // [nkeys, G] entries per (key, chunk) -> exclusive prefix over chunks
   uint32_t* count_done;         // CTAs of moe_count finished (last one publishes)
   int32_t* table_local;         // [n, nkeys] count table (row = src)
   int32_t* table_peer[kMaxRanks];
@@ -119,45 +119,40 @@ __global__ void __launch_bounds__(kCountThreads) moe_count_kernel(const __grid_c
   }
   if (bad) atomicExch(a.sync.err, 2u);
   __syncthreads();
-  for (int q = tid; q < a.nkeys; q += blockDim.x) a.chunk_counts[(long long)blockIdx.x * a.nkeys + q] = cnt[q];
+  for (int q = tid; q < a.nkeys; q += blockDim.x) a.chunk_counts[(long long)q * gridDim.x + blockIdx.x] = cnt[q];
   __threadfence();
   __syncthreads();
   if (tid == 0) last = atomicAdd(a.count_done, 1u) == gridDim.x - 1;
   __syncthreads();
   if (!last) return;
   __threadfence();
-  // exclusive prefix over chunks, per key, in two passes: thread (q, seg)
-  // sums a contiguous run of chunks, the segment sums are scanned in smem,
-  // then each thread rewrites its run as offsets (G x nkeys can be ~300 x 1024)
-  __shared__ int32_t segsum[kCountThreads];
-  const int G = (int)gridDim.x;
-  const int nseg = a.nkeys >= kCountThreads ? 1 : kCountThreads / a.nkeys;
-  const int per_seg = (G + nseg - 1) / nseg;
-  for (int base_q = 0; base_q < a.nkeys; base_q += kCountThreads / nseg) {
-    const int q = base_q + tid % (kCountThreads / nseg), sg = tid / (kCountThreads / nseg);
-    const bool act = q < a.nkeys && sg < nseg;
-    const int c0 = sg * per_seg, c1 = min(G, c0 + per_seg);
-    int sum = 0;
-    if (act)
-      for (int c = c0; c < c1; ++c) sum += __ldcg(a.chunk_counts + (long long)c * a.nkeys + q);
-    segsum[tid] = sum;
-    __syncthreads();
+  // exclusive prefix over chunks, one warp per key: coalesced 32-chunk
+  // strips of the key's row, warp-shuffle scans (G x nkeys is up to ~300 x 1024)
+  const int G = (int)gridDim.x, lane = tid & 31;
+  for (int q = tid >> 5; q < a.nkeys; q += kCountThreads / 32) {
+    int32_t* row = a.chunk_counts + (long long)q * G;
     int run = 0;
-    if (act) {
-      const int stride = kCountThreads / nseg;
-      for (int j = 0; j < sg; ++j) run += segsum[j * stride + tid % stride];
-      if (sg == nseg - 1) {
-        const int tot = run + sum;
-        for (int d = 0; d < a.n; ++d) a.table_peer[d][a.rank * a.nkeys + q] = tot;
+    for (int c0 = 0; c0 < G; c0 += 32 * 8) {
+      int v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {                  // 8 strips' loads in flight
+        const int c = c0 + u * 32 + lane;
+        v[u] = c < G ? __ldcg(row + c) : 0;
       }
-      for (int c = c0; c < c1; ++c) {
-        int32_t* p = a.chunk_counts + (long long)c * a.nkeys + q;
-        const int v = __ldcg(p);
-        *p = run;
-        run += v;
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int c = c0 + u * 32 + lane;
+        int inc = v[u];
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int t = __shfl_up_sync(0xffffffffu, inc, o);
+          if (lane >= o) inc += t;
+        }
+        if (c < G) row[c] = run + inc - v[u];
+        run += __shfl_sync(0xffffffffu, inc, 31);
       }
     }
-    __syncthreads();
+    if (lane < a.n) a.table_peer[lane][a.rank * a.nkeys + q] = run;
   }
   __syncthreads();
   if (tid == 0) {
@@ -206,7 +201,7 @@ __global__ void __launch_bounds__(kDispatchThreads) moe_dispatch_kernel(const __
     for (int q = tid; q < a.nkeys; q += blockDim.x) {
       int b = 0;
       for (int d = 0; d < a.rank; ++d) b += ld_volatile_s32(a.table_local + d * a.nkeys + q);
-      base[q] = b + a.chunk_counts[(long long)blockIdx.x * a.nkeys + q];
+      base[q] = b + a.chunk_counts[(long long)q * gridDim.x + blockIdx.x];
     }
   } else {
     // expert e lives on owner e % n; its segment starts after the padded
@@ -232,7 +227,7 @@ __global__ void __launch_bounds__(kDispatchThreads) moe_dispatch_kernel(const __
     }
     __syncthreads();
     for (int q = tid; q < a.nkeys; q += blockDim.x)
-      base[q] += wc[0][q] + a.chunk_counts[(long long)blockIdx.x * a.nkeys + q];
+      base[q] += wc[0][q] + a.chunk_counts[(long long)q * gridDim.x + blockIdx.x];
   }
   if (blockIdx.x == 0 && tid == 0) {
     // this rank as an owner: rows received (+ the expert tile plan)
@@ -539,7 +534,7 @@ static int moe_common(Comm* c, const pk_tensor* topk, int num_experts, int layou
   G = std::max(G, 1);
   a.tpc = (*T + G - 1) / G;
   a.grid = std::max(1, (*T + a.tpc - 1) / a.tpc);
-  // scratch: [count_done | pad to 256 B][slot_of T*k][chunk_counts G x nkeys]
+  // scratch: [count_done | pad to 256 B][slot_of T*k][chunk_counts nkeys x G]
   // (slot_of first: a combine finds it where the dispatch with the same
   // routing left it, whatever that dispatch's layout)
   Pgl* idx;
