@@ -288,37 +288,63 @@ lcsc_gemm_kernel(const __grid_constant__ GemmArgs args) {
       // RS: destination row inside the owner's [M / world, N] output
       const long long rs_base = rs ? ((long long)(t / num_n) * Cfg::TILE_M - (long long)args.rank * args.ar_owner_rows) *
                                          args.rs_ld + (long long)(t % num_n) * BN * 2 : 0;
-      for (int v = threadIdx.x; v < vecs; v += blockDim.x) {
-        const long long off = base + (long long)(v / vec_per_row) * args.ar_ld + (v % vec_per_row) * 16;
+      // CU vectors per thread per pass: CU (NVLS) or CU x world (P2P) 16 B
+      // loads in flight per thread; one vector at a time left the
+      // communicator SMs latency-bound (~8 GB/s each)
+      constexpr int CU = 4;
+      for (int v0 = threadIdx.x; v0 < vecs; v0 += blockDim.x * CU) {
+        long long off[CU];
+        bool ok[CU];
+#pragma unroll
+        for (int u = 0; u < CU; ++u) {
+          const int v = v0 + u * (int)blockDim.x;
+          ok[u] = v < vecs;
+          off[u] = base + (long long)(v / vec_per_row) * args.ar_ld + (v % vec_per_row) * 16;
+        }
+        auto rs_dst = [&](int u) {
+          const int v = v0 + u * (int)blockDim.x;
+          return args.rs_out + rs_base + (long long)(v / vec_per_row) * args.rs_ld + (v % vec_per_row) * 16;
+        };
         if (args.ar_mc != nullptr) {
-          uint32_t r[4];
-          mm_ld_reduce_bf16x8(args.ar_mc + off, r);                  // reduce(): one in-fabric reduction load
-          if (rs) {
-            st_v4(args.rs_out + rs_base + (long long)(v / vec_per_row) * args.rs_ld + (v % vec_per_row) * 16,
-                  make_uint4(r[0], r[1], r[2], r[3]));
-          } else {
-            mm_st_v4(args.ar_mc + off, r);                           // all_reduce(): + multicast write-back
+          uint32_t r[CU][4];
+#pragma unroll
+          for (int u = 0; u < CU; ++u)
+            if (ok[u]) mm_ld_reduce_bf16x8(args.ar_mc + off[u], r[u]);      // reduce(): in-fabric reduction loads
+#pragma unroll
+          for (int u = 0; u < CU; ++u) {
+            if (!ok[u]) continue;
+            if (rs) st_v4(rs_dst(u), make_uint4(r[u][0], r[u][1], r[u][2], r[u][3]));
+            else mm_st_v4(args.ar_mc + off[u], r[u]);                       // all_reduce(): + multicast write-back
           }
         } else {
-          float acc[8];
+          float acc[CU][8];
 #pragma unroll
-          for (int e = 0; e < 8; ++e) acc[e] = 0.f;
-          for (int d = 0; d < args.world; ++d) {
-            const uint4 x = ld_v4_volatile(args.ar_buf_peer[d] + off);
-            const uint32_t w[4] = {x.x, x.y, x.z, x.w};
+          for (int u = 0; u < CU; ++u)
 #pragma unroll
-            for (int e = 0; e < 4; ++e) {
-              acc[2 * e] += __uint_as_float(w[e] << 16);
-              acc[2 * e + 1] += __uint_as_float(w[e] & 0xFFFF0000u);
+            for (int e = 0; e < 8; ++e) acc[u][e] = 0.f;
+          for (int d = 0; d < args.world; ++d) {              // ascending fold, primitives.py:187-195
+            uint4 x[CU];
+#pragma unroll
+            for (int u = 0; u < CU; ++u)
+              if (ok[u]) x[u] = __ldcg(reinterpret_cast<const uint4*>(args.ar_buf_peer[d] + off[u]));
+#pragma unroll
+            for (int u = 0; u < CU; ++u) {
+              const uint32_t w[4] = {x[u].x, x[u].y, x[u].z, x[u].w};
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                acc[u][2 * e] += __uint_as_float(w[e] << 16);
+                acc[u][2 * e + 1] += __uint_as_float(w[e] & 0xFFFF0000u);
+              }
             }
           }
-          uint4 o;
-          o.x = pack_bf16x2(acc[0], acc[1]);
-          o.y = pack_bf16x2(acc[2], acc[3]);
-          o.z = pack_bf16x2(acc[4], acc[5]);
-          o.w = pack_bf16x2(acc[6], acc[7]);
-          if (rs) st_v4(args.rs_out + rs_base + (long long)(v / vec_per_row) * args.rs_ld + (v % vec_per_row) * 16, o);
-          else for (int d = 0; d < args.world; ++d) st_v4(args.ar_buf_peer[d] + off, o);
+#pragma unroll
+          for (int u = 0; u < CU; ++u) {
+            if (!ok[u]) continue;
+            const uint4 o = make_uint4(pack_bf16x2(acc[u][0], acc[u][1]), pack_bf16x2(acc[u][2], acc[u][3]),
+                                       pack_bf16x2(acc[u][4], acc[u][5]), pack_bf16x2(acc[u][6], acc[u][7]));
+            if (rs) st_v4(rs_dst(u), o);
+            else for (int d = 0; d < args.world; ++d) st_v4(args.ar_buf_peer[d] + off[u], o);
+          }
         }
       }
       __syncthreads();

@@ -167,7 +167,7 @@ constexpr int kDispatchWarps = kDispatchThreads / 32;
 constexpr int kPiece = 16384;          // bytes per bulk piece (bulk-copy mechanism)
 constexpr int kDispatchBufs = 4;
 constexpr int kWinEntries = 512;       // (token, k) entries ranked per window
-constexpr int kSegVec = 16;            // register path: 16 x 16 B per lane = 8 KB per warp segment
+constexpr int kSegVec = 8;             // register path: 8 x 16 B per lane = 4 KB per warp item
 constexpr int kDispatchSmemTma = kDispatchBufs * kPiece;
 
 // CTA b owns the tokens of chunk b. Per window of its entries:
@@ -339,33 +339,35 @@ __global__ void __launch_bounds__(kDispatchThreads) moe_dispatch_kernel(const __
         gp += total;
       }
     } else {
-      // register path: warp w streams tokens w, w + 8, ... of the window in
-      // 8 KB segments (16 independent 16 B loads per lane, then one 16 B store
-      // per lane per destination slot)
+      // register path: the window's rows are cut into 4 KB segments and the
+      // (token, segment) items are dealt to the warps round robin (whole rows
+      // per warp left some warps a row short); per item each lane loads 8
+      // independent 16 B vectors once and stores them once per destination slot
       const int nvec = a.row_bytes / 16;
-      for (int tl = warp; tl < w1 - w0; tl += kDispatchWarps) {
+      const int nseg = (nvec + 32 * kSegVec - 1) / (32 * kSegVec);
+      const int items = (w1 - w0) * nseg;
+      for (int it = warp; it < items; it += kDispatchWarps) {
+        const int tl = it / nseg, v0 = (it - tl * nseg) * 32 * kSegVec;
         const uint8_t* src = a.x + (long long)(w0 + tl) * a.x_ld;
+        uint4 buf[kSegVec];
+#pragma unroll
+        for (int u = 0; u < kSegVec; ++u) {
+          const int v = v0 + u * 32 + lane;
+          if (v < nvec) buf[u] = ld_v4(src + (long long)v * 16);
+        }
         // lanes 0..k-1 hold the destinations of (token, lane)
         uint8_t* mydst = nullptr;
         if (lane < a.k) {
           const int slot = sslot[tl * a.k + lane];
           if (slot >= 0) mydst = a.recv_peer[sown[tl * a.k + lane]] + (long long)slot * a.row_bytes;
         }
-        for (int v0 = 0; v0 < nvec; v0 += 32 * kSegVec) {
-          uint4 buf[kSegVec];
+        for (int j = 0; j < a.k; ++j) {
+          uint8_t* d = reinterpret_cast<uint8_t*>(__shfl_sync(0xffffffffu, reinterpret_cast<uintptr_t>(mydst), j));
+          if (d == nullptr) continue;
 #pragma unroll
           for (int u = 0; u < kSegVec; ++u) {
             const int v = v0 + u * 32 + lane;
-            if (v < nvec) buf[u] = ld_v4(src + (long long)v * 16);
-          }
-          for (int j = 0; j < a.k; ++j) {
-            uint8_t* d = reinterpret_cast<uint8_t*>(__shfl_sync(0xffffffffu, reinterpret_cast<uintptr_t>(mydst), j));
-            if (d == nullptr) continue;
-#pragma unroll
-            for (int u = 0; u < kSegVec; ++u) {
-              const int v = v0 + u * 32 + lane;
-              if (v < nvec) st_v4(d + (long long)v * 16, buf[u]);
-            }
+            if (v < nvec) st_v4(d + (long long)v * 16, buf[u]);
           }
         }
       }
