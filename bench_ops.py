@@ -153,9 +153,18 @@ def moe(args, out, c1, T, K, E, H, HE):
     x = torch.randn(T, H, device=dev).bfloat16()
     topk = torch.rand(T, E, device=dev).argsort(dim=1)[:, :K].int().contiguous()
     recv = (c1.empty((T * K, H)), c1.empty((T * K, 2), torch.int32))
+    # HBM write bandwidth (the dispatch writes k x what it reads): a plain fill
+    # of the receive buffer's size, and the same gather done by torch
+    fill = torch.empty(T * K * H, device=dev, dtype=torch.bfloat16)
+    ms_fill = timeit(lambda: fill.fill_(1.0))
+    idx = torch.arange(T, device=dev).repeat_interleave(K)
+    ms_torch = timeit(lambda: torch.index_select(x, 0, idx, out=fill.view(T * K, H)))
+    del fill
     for mech in ("reg", "tma"):
         ms = timeit(lambda: pk.moe_dispatch(c1, x, topk, E, recv=recv, mechanism=mech))
-        emit(out, **bytes_line("moe_dispatch_n1", T * H * 2 + T * K * H * 2, ms, T=T, H=H, k=K, mechanism=mech))
+        emit(out, **bytes_line("moe_dispatch_n1", T * H * 2 + T * K * H * 2, ms, T=T, H=H, k=K, mechanism=mech,
+                               write_gbs=T * K * H * 2 / ms / 1e6, fill_write_gbs=T * K * H * 2 / ms_fill / 1e6,
+                               torch_index_select_ms=ms_torch, vs_torch=ms_torch / ms))
     # expert-major layout: rows land in 256-row expert segments, GEMM1 reads them in place
     cap_e = pk.moe_capacity(T, K, 1, H, E)
     recv_e = (c1.empty((cap_e, H)), c1.empty((cap_e, 2), torch.int32))
@@ -205,7 +214,11 @@ def moe(args, out, c1, T, K, E, H, HE):
     wts = torch.rand(T, K, device=dev)
     comb = torch.empty(T, H, device=dev, dtype=torch.bfloat16)
     ms = timeit(lambda: pk.moe_combine(c1, yh, topk, wts, E, out=comb))
-    emit(out, **bytes_line("moe_combine_n1", T * K * H * 2 + T * H * 2, ms, T=T, H=H, k=K))
+    yt = yh[:T * K].view(T, K, H)
+    ms_torch = timeit(lambda: torch.bmm(wts.bfloat16().unsqueeze(1), yt, out=comb.view(T, 1, H)))
+    emit(out, **bytes_line("moe_combine_n1", T * K * H * 2 + T * H * 2, ms, T=T, H=H, k=K,
+                           torch_bmm_ms=ms_torch, vs_torch=ms_torch / ms,
+                           note="torch reference reads the k rows contiguously (no slot indirection)"))
     del recv, y, yh, w
 
 

@@ -101,11 +101,10 @@ __device__ __forceinline__ int moe_key(const MoeArgs& a, int e) {
 // CTA per chunk counts its entries per key; the last CTA to finish turns the
 // chunk counts into exclusive per-chunk offsets, publishes this rank's row of
 // the count table to every rank and signals ready.
-constexpr int kCountThreads = 256;
+constexpr int kCountThreads = 256;   // = the dispatch CTA size (the count is its first phase)
 
-__global__ void __launch_bounds__(kCountThreads) moe_count_kernel(const __grid_constant__ MoeArgs a) {
-  __shared__ int32_t cnt[kMoeMaxKeys];
-  __shared__ int last;
+// cnt: kMoeMaxKeys ints of shared scratch; last: one shared int
+__device__ __forceinline__ void moe_count_phase(const MoeArgs& a, int32_t* cnt, int* last) {
   const int tid = threadIdx.x;
   for (int q = tid; q < a.nkeys; q += blockDim.x) cnt[q] = 0;
   __syncthreads();
@@ -122,9 +121,9 @@ __global__ void __launch_bounds__(kCountThreads) moe_count_kernel(const __grid_c
   for (int q = tid; q < a.nkeys; q += blockDim.x) a.chunk_counts[(long long)q * gridDim.x + blockIdx.x] = cnt[q];
   __threadfence();
   __syncthreads();
-  if (tid == 0) last = atomicAdd(a.count_done, 1u) == gridDim.x - 1;
+  if (tid == 0) *last = atomicAdd(a.count_done, 1u) == gridDim.x - 1;
   __syncthreads();
-  if (!last) return;
+  if (!*last) return;
   __threadfence();
   // exclusive prefix over chunks, one warp per key: coalesced 32-chunk
   // strips of the key's row, warp-shuffle scans (G x nkeys is up to ~300 x 1024)
@@ -185,8 +184,13 @@ __global__ void __launch_bounds__(kDispatchThreads) moe_dispatch_kernel(const __
   __shared__ int32_t base[kMoeMaxKeys];              // per key: base slot on the owner + earlier chunks + run
   __shared__ int32_t wc[kDispatchWarps][kMoeMaxKeys]; // per (warp, key): group size, then its first slot
   __shared__ __align__(8) uint64_t bars[kDispatchBufs];
-  __shared__ int ok_flag;
+  __shared__ int ok_flag, last_flag;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  // ---- phase 0: count this chunk's entries; the last CTA to finish
+  // publishes the count table and signals ready (no separate count launch;
+  // the grid is sized so every CTA is resident, see moe_common)
+  moe_count_phase(a, &wc[0][0], &last_flag);
+  __syncthreads();
   if (tid == 0) {
     ok_flag = moe_wait_all(a.sync, a.n, false) ? 1 : 0;
     if (a.mech == 2) {
@@ -201,7 +205,7 @@ __global__ void __launch_bounds__(kDispatchThreads) moe_dispatch_kernel(const __
     for (int q = tid; q < a.nkeys; q += blockDim.x) {
       int b = 0;
       for (int d = 0; d < a.rank; ++d) b += ld_volatile_s32(a.table_local + d * a.nkeys + q);
-      base[q] = b + a.chunk_counts[(long long)q * gridDim.x + blockIdx.x];
+      base[q] = b + __ldcg(a.chunk_counts + (long long)q * gridDim.x + blockIdx.x);
     }
   } else {
     // expert e lives on owner e % n; its segment starts after the padded
@@ -227,7 +231,7 @@ __global__ void __launch_bounds__(kDispatchThreads) moe_dispatch_kernel(const __
     }
     __syncthreads();
     for (int q = tid; q < a.nkeys; q += blockDim.x)
-      base[q] += wc[0][q] + a.chunk_counts[(long long)q * gridDim.x + blockIdx.x];
+      base[q] += wc[0][q] + __ldcg(a.chunk_counts + (long long)q * gridDim.x + blockIdx.x);
   }
   if (blockIdx.x == 0 && tid == 0) {
     // this rank as an owner: rows received (+ the expert tile plan)
@@ -478,7 +482,6 @@ __global__ void __launch_bounds__(kCombineThreads) moe_combine_kernel(const __gr
 // ---------------------------------------------------------------- host
 int preload_moe() {
   cudaFuncAttributes fa;
-  PK_CUDA(cudaFuncGetAttributes(&fa, moe_count_kernel));
   PK_CUDA(cudaFuncGetAttributes(&fa, moe_dispatch_kernel));
   PK_CUDA(cudaFuncGetAttributes(&fa, moe_combine_kernel<8>));
   PK_CUDA(cudaFuncGetAttributes(&fa, moe_combine_kernel<16>));
@@ -531,7 +534,9 @@ static int moe_common(Comm* c, const pk_tensor* topk, int num_experts, int layou
   a.table_local = static_cast<int32_t*>(tbl->local);
   for (int r = 0; r < c->world; ++r) a.table_peer[r] = static_cast<int32_t*>(tbl->peers[r]);
   // chunking shared by moe_count and moe_dispatch (one CTA per chunk)
-  int G = std::min(*T, c->num_sms * 2);
+  int per_sm = 2;
+  if (const char* e = getenv("PK_MOE_CTAS_PER_SM")) per_sm = std::max(1, atoi(e));   // tuning hook
+  int G = std::min(*T, c->num_sms * per_sm);
   if (c->local_group && c->world > 1) G = std::min(G, c->num_sms);   // co-residency of all emulated ranks
   G = std::max(G, 1);
   a.tpc = (*T + G - 1) / G;
@@ -593,14 +598,22 @@ int moe_dispatch(Comm* c, const pk_tensor* x, const pk_tensor* topk, int num_exp
   // expert-major padding rows carry id -1 (cleared before this rank signals
   // ready, so no peer can be writing into recv_src yet)
   if (layout == 1) PK_CUDA(cudaMemsetAsync(recv_src->ptr, 0xFF, (size_t)cap * 4 * src_cols, st));
+  const int smem = mech == PK_MECH_TMA ? kDispatchSmemTma : 0;
+  if (smem) PK_TRY(ensure_smem_attr((const void*)moe_dispatch_kernel, smem));
+  // the count phase ends in a grid-wide hand-off (the last CTA publishes, all
+  // wait): every CTA must be resident at once
+  int occ = 0;
+  PK_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void*)moe_dispatch_kernel, kDispatchThreads, smem));
+  const int max_grid = std::max(1, occ * c->num_sms);
+  if (a.grid > max_grid) {
+    a.tpc = (T + max_grid - 1) / max_grid;
+    a.grid = std::max(1, (T + a.tpc - 1) / a.tpc);
+  }
   c->ready_count += 1;
   c->done_count += (uint32_t)a.grid;
   fill_moe_sync(c, a.sync);
   void* params[] = {&a};
   PK_CUDA(cudaMemsetAsync(a.count_done, 0, sizeof(uint32_t), st));
-  PK_CUDA(cudaLaunchKernel((void*)moe_count_kernel, dim3(a.grid), dim3(kCountThreads), params, 0, st));
-  const int smem = mech == PK_MECH_TMA ? kDispatchSmemTma : 0;
-  if (smem) PK_TRY(ensure_smem_attr((const void*)moe_dispatch_kernel, smem));
   PK_CUDA(cudaLaunchKernel((void*)moe_dispatch_kernel, dim3(a.grid), dim3(kDispatchThreads), params, smem, st));
   return PK_OK;
 }
