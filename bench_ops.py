@@ -144,6 +144,7 @@ def main():
     T, K, E, H, HE = (1024, 8, 64, 7168, 2048) if args.quick else (4096, 8, 64, 7168, 2048)
     moe(args, out, c1, T, K, E, H, HE) if want("moe") else None
     local(args, out) if want("local") else None
+    ablation(args, out) if want("ablation") else None
     c1.destroy()
     out.close()
 
@@ -278,6 +279,33 @@ def local(args, out):
         for c in comms:
             c.check()
             c.destroy()
+
+
+def ablation(args, out):
+    """Design-overhead ablation (OverheadConfig, engine.py:49-60; PAPER.md
+    Fig. all-reduce): the P2P all-reduce of an emulated world 2 with each
+    library-style overhead switched on, against the direct design."""
+    from paper_2511_13940_b200.compat import OverheadConfig
+    world = 2
+    comms = pk.local_group(world)
+    variants = [("direct", OverheadConfig()),
+                ("two_way_handshake", OverheadConfig(two_way_handshake=True)),
+                ("staging_buffers", OverheadConfig(staging_buffers=True)),
+                ("peer_addr_indirection", OverheadConfig(peer_addr_indirection=True)),
+                ("all", OverheadConfig(True, True, True))]
+    for mb in ([16] if args.quick else [1, 16, 64, 256]):
+        n_el = mb * (1 << 20) // 2
+        ts = [c.empty((n_el,)) for c in comms]
+        base = None
+        for name, ov in variants:
+            ms = timeit(ranks(comms, lambda r, c, s: pk.all_reduce_with_overheads(c, ts[r], ov, stream=s)))
+            base = base or ms
+            emit(out, **bytes_line(f"all_reduce_ablation_local{world}", 2 * world * n_el * 2, ms, mib=mb,
+                                   overheads=name, slowdown=ms / base))
+        del ts
+    for c in comms:
+        c.check()
+        c.destroy()
 
 
 if __name__ == "__main__":

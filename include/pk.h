@@ -149,6 +149,13 @@ PK_API int pk_gemm_ar(pk_comm* comm, const pk_tensor* a, const pk_tensor* b, pk_
 
 /* In-place all-reduce of x (bf16 or f32, contiguous) over all ranks. */
 PK_API int pk_all_reduce(pk_comm* comm, pk_tensor* x, int op, const pk_sched* sched, void* stream);
+/* Design-overhead ablation (OverheadConfig, engine.py:49-60): the P2P sum
+ * all-reduce of a symmetric x with library-style overheads switched on.
+ * overheads: bit 0 two-way handshake per transfer, bit 1 staging buffers
+ * (transfers of staging_channel_bytes through local buffers, 0 = 512 KB),
+ * bit 2 peer-address indirection (pointer load + group sync per access). */
+PK_API int pk_all_reduce_ablate(pk_comm* comm, pk_tensor* x, uint32_t overheads, size_t staging_channel_bytes,
+                                void* stream);
 
 /* Ring attention forward (non-causal): q,k,v,o [B, S/n, H, D] bf16 local
  * shards; lse [B, H, S/n] f32. KV rotates d -> d+1 (workloads.py:666-681). */

@@ -20,9 +20,8 @@ from .errors import (DeadlockError, LcscError, MemSimError, MulticastReadError, 
                      PkCudaError, PkError, PrimitiveError, ProtocolViolation, WorkloadError)
 from .comm import Comm, Pgl, local_group  # noqa: F401
 from . import tune  # noqa: F401
-from .ops import (all_gather, all_gather_gemm, attention, all_reduce, all_to_all, gemm, gemm_all_reduce,  # noqa: F401
-                  gemm_reduce_scatter, grouped_gemm, moe_capacity, moe_combine, moe_dispatch, reduce_scatter,
-                  ring_attention,
-                  ulysses_all_to_all)
+from .ops import (all_gather, all_gather_gemm, all_reduce, all_reduce_with_overheads, all_to_all,  # noqa: F401
+                  attention, gemm, gemm_all_reduce, gemm_reduce_scatter, grouped_gemm, moe_capacity,
+                  moe_combine, moe_dispatch, reduce_scatter, ring_attention, ulysses_all_to_all)
 
 __version__ = "0.1.0"

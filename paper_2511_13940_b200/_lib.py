@@ -30,7 +30,7 @@ EXPORTS = (
     "pk_comm_init", "pk_comm_init_local", "pk_comm_destroy", "pk_comm_rank",
     "pk_comm_has_multicast", "pk_comm_set_timeout", "pk_comm_check", "pk_debug_rendezvous", "pk_debug_multimem",
     "pk_pgl_alloc", "pk_pgl_ptrs", "pk_pgl_free",
-    "pk_gemm", "pk_ag_gemm", "pk_gemm_rs", "pk_gemm_ar", "pk_all_reduce",
+    "pk_gemm", "pk_ag_gemm", "pk_gemm_rs", "pk_gemm_ar", "pk_all_reduce", "pk_all_reduce_ablate",
     "pk_ring_attn_fwd", "pk_attn_fwd", "pk_moe_dispatch", "pk_moe_dispatch_ex", "pk_moe_combine", "pk_grouped_gemm",
     "pk_grouped_gemm_planned",
     "pk_all_gather", "pk_reduce_scatter", "pk_all_to_all", "pk_ulysses_a2a",

@@ -84,6 +84,17 @@ class LcscKernelSpec:          # lcsc.py:45-76
 
 
 @dataclass
+class OverheadConfig:          # engine.py:49-60: all off reproduces the direct design
+    two_way_handshake: bool = False
+    staging_buffers: bool = False
+    peer_addr_indirection: bool = False
+    staging_channel_bytes: int = 512 * 1024
+
+    def any_enabled(self) -> bool:
+        return self.two_way_handshake or self.staging_buffers or self.peer_addr_indirection
+
+
+@dataclass
 class CostReport:              # costmodel.py CostReport, measured instead of simulated
     t_launch: float = 0.0
     t_comp: float = 0.0

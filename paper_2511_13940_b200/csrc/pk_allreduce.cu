@@ -166,6 +166,129 @@ __global__ void __launch_bounds__(512) ar_p2p_kernel(const __grid_constant__ ArA
   ar_end_barrier(a);
 }
 
+// ---------------------------------------------------------------- design-overhead ablation
+// The reference models three library-style overheads PK avoids
+// (OverheadConfig, engine.py:49-60, charged per transfer at engine.py:296-306;
+// PAPER.md:306-310): a two-way handshake before every transfer, staging
+// through bounded intermediate buffers (every byte moved twice, messages
+// capped at staging_channel_bytes), and peer addresses fetched from global
+// memory with a group sync on every access. ar_ablate_kernel re-expresses them
+// on the real P2P all-reduce (sum), one "transfer" = one chunk of a rank's
+// slice (staging_channel_bytes, or 512 KB):
+//   TWO_WAY   per chunk, the owner requests every peer and waits for its ack
+//             (the peer's CTA for the same chunk index answers) before reading
+//   STAGING   peer data is copied into a local staging buffer, reduced from
+//             there into a staging output, and copied out to the peers
+//   INDIRECT  peer pointers are loaded from a global table around a
+//             __syncthreads on every access
+enum { PK_OVH_TWO_WAY = 1, PK_OVH_STAGING = 2, PK_OVH_INDIRECT = 4 };
+
+struct ArAblateArgs {
+  ArArgs base;
+  uint8_t* const* peer_table;        // global copy of base.peers (INDIRECT)
+  uint32_t* req_local;               // [world][max_chunks] requests received (from owner r at r*max_chunks + c)
+  uint32_t* req_peer[kMaxRanks];
+  uint32_t* ack_local;               // [world][max_chunks] acks received (from peer d at d*max_chunks + c)
+  uint32_t* ack_peer[kMaxRanks];
+  uint32_t calls;                    // handshake round of this call (counters only grow)
+  uint8_t* staging;                  // [gridDim.x][world + 1][chunk_vecs * 16] local staging
+  long long chunk_vecs;
+  int max_chunks;
+};
+
+template <int DT, int FLAGS>
+__global__ void __launch_bounds__(512) ar_ablate_kernel(const __grid_constant__ ArAblateArgs A) {
+  const ArArgs& a = A.base;
+  ar_start_barrier(a);
+  const long long per = (a.nvec + a.world - 1) / a.world;
+  const long long lo = per * a.rank;
+  const long long hi = min(a.nvec, lo + per);
+  const int nch = (int)((per + A.chunk_vecs - 1) / A.chunk_vecs);     // the same on every rank
+  uint8_t* stg = A.staging + (long long)blockIdx.x * (a.world + 1) * A.chunk_vecs * 16;
+  for (int c = blockIdx.x; c < nch; c += gridDim.x) {
+    if constexpr ((FLAGS & PK_OVH_TWO_WAY) != 0) {
+      if (threadIdx.x == 0) {
+        __threadfence_system();
+        for (int d = 0; d < a.world; ++d) signal_add(A.req_peer[d] + a.rank * A.max_chunks + c, 1u);   // request
+        for (int r = 0; r < a.world; ++r) {                                                         // answer
+          wait_geq(A.req_local + r * A.max_chunks + c, A.calls, a.err, a.timeout_ns);
+          signal_add(A.ack_peer[r] + a.rank * A.max_chunks + c, 1u);
+        }
+        for (int d = 0; d < a.world; ++d) wait_geq(A.ack_local + d * A.max_chunks + c, A.calls, a.err, a.timeout_ns);
+      }
+      __syncthreads();
+    }
+    const long long c0 = lo + (long long)c * A.chunk_vecs, c1 = min(hi, c0 + A.chunk_vecs);
+    auto peer = [&](int d) -> uint8_t* {
+      if constexpr ((FLAGS & PK_OVH_INDIRECT) != 0) {
+        // NVSHMEM-style access: the peer address comes from global memory and
+        // the accessing group synchronises
+        uint8_t* p;
+        asm volatile("ld.volatile.global.u64 %0, [%1];" : "=l"(p) : "l"(A.peer_table + d) : "memory");
+        __syncwarp(__activemask());
+        return p;
+      } else {
+        return a.peers[d];
+      }
+    };
+    if constexpr ((FLAGS & PK_OVH_STAGING) != 0) {
+      for (int d = 0; d < a.world; ++d)                      // peer -> staging d
+        for (long long i = c0 + threadIdx.x; i < c1; i += blockDim.x)
+          st_v4(stg + ((long long)d * A.chunk_vecs + (i - c0)) * 16, ld_v4_volatile(peer(d) + i * 16));
+      __syncthreads();
+    }
+    for (long long i = c0 + threadIdx.x; i < c1; i += blockDim.x) {
+      float acc[8];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) acc[e] = 0.f;
+      for (int d = 0; d < a.world; ++d) {                    // ascending fold, primitives.py:187-195
+        uint4 x;
+        if constexpr ((FLAGS & PK_OVH_STAGING) != 0) x = ld_v4(stg + ((long long)d * A.chunk_vecs + (i - c0)) * 16);
+        else x = ld_v4_volatile(peer(d) + i * 16);
+        if constexpr (DT == PK_BF16) {
+          float t[8];
+          unpack8(x, t);
+#pragma unroll
+          for (int e = 0; e < 8; ++e) acc[e] += t[e];
+        } else {
+          acc[0] += __uint_as_float(x.x); acc[1] += __uint_as_float(x.y);
+          acc[2] += __uint_as_float(x.z); acc[3] += __uint_as_float(x.w);
+        }
+      }
+      const uint4 o = (DT == PK_BF16) ? pack8(acc)
+                                      : make_uint4(__float_as_uint(acc[0]), __float_as_uint(acc[1]),
+                                                   __float_as_uint(acc[2]), __float_as_uint(acc[3]));
+      if constexpr ((FLAGS & PK_OVH_STAGING) != 0) {
+        st_v4(stg + ((long long)a.world * A.chunk_vecs + (i - c0)) * 16, o);
+      } else {
+        for (int d = 0; d < a.world; ++d) st_v4(peer(d) + i * 16, o);
+      }
+    }
+    if constexpr ((FLAGS & PK_OVH_STAGING) != 0) {
+      __syncthreads();
+      for (int d = 0; d < a.world; ++d)                      // staging out -> peers
+        for (long long i = c0 + threadIdx.x; i < c1; i += blockDim.x)
+          st_v4(peer(d) + i * 16, ld_v4(stg + ((long long)a.world * A.chunk_vecs + (i - c0)) * 16));
+      __syncthreads();
+    }
+  }
+  ar_end_barrier(a);
+}
+
+template <int DT>
+static void* ablate_kernel_for(int flags) {
+  switch (flags & 7) {
+    case 0: return (void*)ar_ablate_kernel<DT, 0>;
+    case 1: return (void*)ar_ablate_kernel<DT, 1>;
+    case 2: return (void*)ar_ablate_kernel<DT, 2>;
+    case 3: return (void*)ar_ablate_kernel<DT, 3>;
+    case 4: return (void*)ar_ablate_kernel<DT, 4>;
+    case 5: return (void*)ar_ablate_kernel<DT, 5>;
+    case 6: return (void*)ar_ablate_kernel<DT, 6>;
+    default: return (void*)ar_ablate_kernel<DT, 7>;
+  }
+}
+
 template <int DT, int OP>
 static void* p2p_kernel_for(int n) {
   switch (n) {
@@ -182,6 +305,10 @@ static void* p2p_kernel_for(int n) {
 
 int preload_allreduce() {
   cudaFuncAttributes fa;
+  for (int f = 0; f < 8; ++f) {
+    PK_CUDA(cudaFuncGetAttributes(&fa, ablate_kernel_for<PK_BF16>(f)));
+    PK_CUDA(cudaFuncGetAttributes(&fa, ablate_kernel_for<PK_F32>(f)));
+  }
   PK_CUDA(cudaFuncGetAttributes(&fa, ar_nvls_kernel<PK_BF16>));
   PK_CUDA(cudaFuncGetAttributes(&fa, ar_nvls_kernel<PK_F32>));
   for (int n = 1; n <= 8; ++n) {
@@ -194,6 +321,8 @@ int preload_allreduce() {
   }
   return PK_OK;
 }
+
+int all_reduce_ablate(Comm* c, pk_tensor* x, uint32_t flags, size_t channel_bytes, cudaStream_t st);
 
 int all_reduce(Comm* c, pk_tensor* x, int op, const pk_sched* sched, cudaStream_t st) {
   if (!x || !x->ptr) return fail(PK_ERR_INVALID, "all_reduce: null tensor");
@@ -314,7 +443,100 @@ int debug_multimem(Comm* c, Pgl* p, size_t nvec, cudaStream_t st) {
   return PK_OK;
 }
 
+enum { kScratchAblate = 11 };
+constexpr int kAblateMaxChunks = 4096;
+
+int all_reduce_ablate(Comm* c, pk_tensor* x, uint32_t flags, size_t channel_bytes, cudaStream_t st) {
+  if (!x || !x->ptr) return fail(PK_ERR_INVALID, "all_reduce_ablate: null tensor");
+  if (x->dtype != PK_BF16 && x->dtype != PK_F32) return fail(PK_ERR_CAPABILITY, "all_reduce_ablate: dtype must be bf16 or f32");
+  if (flags > 7) return fail(PK_ERR_INVALID, "all_reduce_ablate: unknown overhead flags %u", flags);
+  long long numel = 1;
+  for (int i = 0; i < x->ndim; ++i) numel *= x->shape[i];
+  for (int i = x->ndim - 1, expect = 1; i >= 0; --i) {
+    if (x->shape[i] != 1 && x->strides[i] != expect) return fail(PK_ERR_INVALID, "all_reduce_ablate: tensor must be contiguous");
+    expect *= (int)x->shape[i];
+  }
+  const size_t bytes = (size_t)numel * dtype_bytes(x->dtype);
+  if (bytes % 16) return fail(PK_ERR_INVALID, "all_reduce_ablate: size must be a multiple of 16 bytes");
+  if (channel_bytes == 0) channel_bytes = 512 * 1024;                 // engine.py:56
+  if (channel_bytes % 16) return fail(PK_ERR_INVALID, "all_reduce_ablate: channel bytes must be a multiple of 16");
+  if (bytes == 0 || c->world == 1) return PK_OK;
+  // the buffer must be symmetric (the ablation compares transfer designs, not staging of user tensors)
+  void* peers[kMaxRanks];
+  if (!find_symmetric(c, x->ptr, bytes, peers))
+    return fail(PK_ERR_INVALID, "all_reduce_ablate: x must be a symmetric (Comm.empty) tensor");
+  // control block (symmetric): [peer table 64 B | pad][req world x max][ack world x max]
+  const size_t ctl_bytes = 256 + 2 * sizeof(uint32_t) * kMaxRanks * kAblateMaxChunks;
+  Pgl* ctl;
+  const void* before = c->scratch[kScratchAblate] ? c->scratch[kScratchAblate]->local : nullptr;
+  PK_TRY(comm_scratch(c, kScratchAblate, ctl_bytes, &ctl));
+  if (ctl->local != before) {                                          // fresh counters
+    PK_CUDA(cudaMemsetAsync(ctl->local, 0, ctl_bytes, st));
+    c->ablate_calls = 0;
+  }
+  uint8_t* cb = static_cast<uint8_t*>(ctl->local);
+  PK_CUDA(cudaMemcpyAsync(cb, peers, sizeof(void*) * c->world, cudaMemcpyHostToDevice, st));
+  ArAblateArgs A;
+  memset(&A, 0, sizeof(A));
+  ArArgs& a = A.base;
+  for (int r = 0; r < c->world; ++r) a.peers[r] = (uint8_t*)peers[r];
+  a.nvec = (long long)(bytes / 16);
+  a.rank = c->rank;
+  a.world = c->world;
+  a.dtype = x->dtype;
+  a.op = PK_OP_SUM;
+  uint32_t* local = static_cast<uint32_t*>(c->sync->local);
+  a.ready_local = local + kSyncReady;
+  a.done_local = local + kSyncDone;
+  a.err = local + kSyncErr;
+  for (int r = 0; r < c->world; ++r) {
+    uint32_t* pr = static_cast<uint32_t*>(c->sync->peers[r]);
+    a.ready_peer[r] = pr + kSyncReady;
+    a.done_peer[r] = pr + kSyncDone;
+  }
+  A.peer_table = reinterpret_cast<uint8_t* const*>(cb);
+  A.max_chunks = kAblateMaxChunks;
+  A.req_local = reinterpret_cast<uint32_t*>(cb + 256);
+  A.ack_local = A.req_local + kMaxRanks * kAblateMaxChunks;
+  for (int r = 0; r < c->world; ++r) {
+    uint8_t* pb = static_cast<uint8_t*>(ctl->peers[r]);
+    A.req_peer[r] = reinterpret_cast<uint32_t*>(pb + 256);
+    A.ack_peer[r] = A.req_peer[r] + kMaxRanks * kAblateMaxChunks;
+  }
+  const long long per = (a.nvec + c->world - 1) / c->world;
+  A.chunk_vecs = std::max<long long>((long long)(channel_bytes / 16), (per + kAblateMaxChunks - 1) / kAblateMaxChunks);
+  const int nch = (int)((per + A.chunk_vecs - 1) / A.chunk_vecs);
+  int blocks = std::max(1, std::min(nch, c->num_sms));
+  if (flags & PK_OVH_STAGING) {
+    blocks = std::min(blocks, 32);                                     // a few channels' worth of staging
+    const size_t need = (size_t)blocks * (c->world + 1) * A.chunk_vecs * 16;
+    if (c->ablate_stage_bytes < need) {
+      if (c->ablate_stage) PK_CUDA(cudaFreeAsync(c->ablate_stage, st));
+      PK_CUDA(cudaMallocAsync(&c->ablate_stage, need, st));
+      c->ablate_stage_bytes = need;
+    }
+    A.staging = static_cast<uint8_t*>(c->ablate_stage);
+  }
+  c->ablate_calls += 1;
+  A.calls = c->ablate_calls;
+  c->ready_count += 1;
+  c->done_count += (uint32_t)blocks;
+  a.ready_expect = c->ready_count;
+  a.done_expect = c->done_count;
+  a.timeout_ns = c->timeout_ns;
+  void* kern = x->dtype == PK_BF16 ? ablate_kernel_for<PK_BF16>((int)flags) : ablate_kernel_for<PK_F32>((int)flags);
+  void* params[] = {&A};
+  PK_CUDA(cudaLaunchKernel(kern, dim3(blocks), dim3(512), params, 0, st));
+  return PK_OK;
+}
+
 }  // namespace pk
+
+extern "C" PK_API int pk_all_reduce_ablate(pk_comm* comm, pk_tensor* x, uint32_t overheads, size_t staging_channel_bytes,
+                                           void* stream) {
+  if (!comm) return pk::fail(PK_ERR_INVALID, "null comm");
+  return pk::all_reduce_ablate(comm, x, overheads, staging_channel_bytes, (cudaStream_t)stream);
+}
 
 extern "C" PK_API int pk_debug_multimem(pk_comm* comm, pk_pgl* pgl, size_t nvec, void* stream) {
   if (!comm) return pk::fail(PK_ERR_INVALID, "null comm");

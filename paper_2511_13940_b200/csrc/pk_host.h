@@ -143,6 +143,9 @@ struct Comm {
   std::vector<Pgl*> retired;         // outgrown scratch PGLs (local groups free them at destroy)
   cudaStream_t side = nullptr;       // side stream for copy-engine staging (ring attention)
   AttnScratch attn;                  // ring attention: stream-K partials + per-item counters
+  void* ablate_stage = nullptr;      // all_reduce_ablate staging channels (local)
+  size_t ablate_stage_bytes = 0;
+  uint32_t ablate_calls = 0;         // handshake round counter (req/ack counters only grow)
 };
 
 // If [ptr, ptr+bytes) lies inside one of c's user PGLs, fill peers[] with the

@@ -140,6 +140,30 @@ def all_reduce(comm, x: torch.Tensor, op: str = "sum", schedule: dict | None = N
     return x
 
 
+def all_reduce_with_overheads(comm, x: torch.Tensor, overheads=None, *, two_way_handshake: bool = False,
+                              staging_buffers: bool = False, peer_addr_indirection: bool = False,
+                              staging_channel_bytes: int = 512 * 1024, stream=None) -> torch.Tensor:
+    """The P2P sum all-reduce with the reference's library-style design
+    overheads switched on (OverheadConfig, engine.py:49-60),
+    for ablations: a two-way handshake per transfer, staging through bounded
+    buffers (every byte moved twice), peer addresses loaded from global memory
+    with a group sync per access. `overheads` may be an OverheadConfig-like
+    object (fields as in the reference); x must be symmetric (Comm.empty)."""
+    _require_cuda(x)
+    if overheads is not None:
+        two_way_handshake = bool(getattr(overheads, "two_way_handshake", False))
+        staging_buffers = bool(getattr(overheads, "staging_buffers", False))
+        peer_addr_indirection = bool(getattr(overheads, "peer_addr_indirection", False))
+        staging_channel_bytes = int(getattr(overheads, "staging_channel_bytes", staging_channel_bytes))
+    flags = (1 if two_way_handshake else 0) | (2 if staging_buffers else 0) | (4 if peer_addr_indirection else 0)
+    import ctypes
+    dx = _lib.tensor_desc(x)
+    check(_lib.load().pk_all_reduce_ablate(comm._h, _lib.ref(dx), ctypes.c_uint32(flags),
+                                           ctypes.c_size_t(staging_channel_bytes), ctypes_stream(_stream(stream))),
+          "all_reduce_with_overheads")
+    return x
+
+
 def moe_capacity(tokens: int, top_k: int, world: int, hidden: int, local_experts: int = 0) -> int:
     """Default receive capacity: the worst case (every token of every rank routed
     here) when that fits in 1 GiB, else twice the average load; plus one

@@ -84,3 +84,36 @@ def test_all_reduce_rejects_bad_input():
         pk.all_reduce(comms[0], torch.zeros(8, device="cuda"), op="xor")
     for c in comms:
         c.destroy()
+
+
+@pytest.mark.parametrize("world", [2, 4])
+@pytest.mark.parametrize("flags", list(range(8)))
+def test_all_reduce_with_overheads_is_exact(world, flags):
+    """Every overhead combination (OverheadConfig, engine.py:49-60) computes the
+    same ascending-order fold as the direct design (bit-exact on integers)."""
+    import paper_2511_13940_b200 as pk
+    from paper_2511_13940_b200.compat import OverheadConfig
+    ov = OverheadConfig(two_way_handshake=bool(flags & 1), staging_buffers=bool(flags & 2),
+                        peer_addr_indirection=bool(flags & 4), staging_channel_bytes=64 * 1024)
+    comms = pk.local_group(world)
+    n = 3 * 65536 + 8 * 5                     # several channel-sized chunks plus a ragged tail
+    rng = np.random.default_rng(world * 8 + flags)
+    data = [rng.integers(-8, 9, size=n).astype(np.float32) for _ in range(world)]
+    xs = [c.empty((n,), torch.float32) for c in comms]
+    for x, d in zip(xs, data):
+        x.copy_(torch.from_numpy(d))
+    torch.cuda.synchronize()
+    for _ in range(2):                        # twice: the handshake counters carry over between calls
+        streams = [torch.cuda.Stream() for _ in comms]
+        for r, c in enumerate(comms):
+            with torch.cuda.stream(streams[r]):
+                pk.all_reduce_with_overheads(c, xs[r], ov, stream=streams[r])
+        torch.cuda.synchronize()
+        for c in comms:
+            c.check()
+        exp = oracle.fold(data)
+        for x in xs:
+            assert np.array_equal(x.cpu().numpy(), exp)
+        data = [exp.copy() for _ in range(world)]
+    for c in comms:
+        c.destroy()
