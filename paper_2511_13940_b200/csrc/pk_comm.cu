@@ -554,7 +554,7 @@ static int preload_kernels() {
 static int comm_finish_init(Comm* c) {
   PK_TRY(preload_kernels());
   PK_TRY(pgl_alloc(c, kSyncBytes, 0, &c->sync));
-  c->max_flags = kSyncArTiles - kSyncFlags;
+  c->max_flags = 32768;                        // kAgCountOffset: AG piece counters follow the flags
   return PK_OK;
 }
 

@@ -35,6 +35,7 @@ constexpr int kEpiWarp0 = 4;
 
 enum EpiMode : int { EPI_STORE = 0, EPI_REDUCE_ADD = 1, EPI_SCATTER = 2, EPI_DIRECT = 3 };
 constexpr int kTileRing = 4;                // depth of the tile-index broadcast ring
+constexpr int kAgCountOffset = 32768;       // AG piece counters live after the first 32K m-tile flags
 
 // Cross-rank sync state for one fused call (all pointers are device VAs).
 struct SyncArgs {
@@ -357,9 +358,14 @@ lcsc_gemm_kernel(const __grid_constant__ GemmArgs args) {
   } else if (is_comm) {
     // ========================================================= communicator
     // Inter-SM all-gather: copy every shard (peer VA -> smem ring -> local
-    // gathered buffer) in TILE_M-row chunks and publish flags[m_tile] per
-    // chunk. One elected thread per CTA drives the bulk-copy engine (TMA
-    // needs ~15 SMs to saturate NVLink).
+    // gathered buffer) in TILE_M-row chunks, right neighbour's shard first,
+    // and publish flags[m_tile] per chunk. One elected thread per CTA drives
+    // the bulk-copy engine (TMA needs ~15 SMs to saturate NVLink,
+    // PAPER.md:34,184). The 32 KB pieces of each chunk are striped over all
+    // communicator CTAs, so the first chunk lands at the full aggregate rate
+    // (a chunk per CTA made the first remote tiles wait for one CTA's share of
+    // the link); each CTA adds to the chunk's piece counter when its pieces
+    // of it are in HBM and the last one publishes the flag.
     if (warp == 0) {
       const int ncomm = (int)(gridDim.x / CG) - args.num_compute_clusters;
       const int cidx = cluster - args.num_compute_clusters;
@@ -367,33 +373,32 @@ lcsc_gemm_kernel(const __grid_constant__ GemmArgs args) {
       const int me = cidx * CG + (int)cta_rank;
       const long long chunk_bytes = (long long)Cfg::TILE_M * args.K * 2;
       const int chunks_per_shard = args.a_rows_per_src / Cfg::TILE_M;
-      const int total_chunks = args.world * chunks_per_shard;
+      // visited chunks: right neighbour's shard first, the local shard last (if copied at all)
+      const int nvis = (args.comm_copy_local ? args.world : args.world - 1) * chunks_per_shard;
       constexpr int PIECE = 32768;
       constexpr int NBUF = (Cfg::STAGES * Cfg::STAGE_BYTES) / PIECE < 8 ? (Cfg::STAGES * Cfg::STAGE_BYTES) / PIECE : 8;
       static_assert(NBUF >= 3, "communicator needs >= 3 smem pieces");
-      constexpr int kLag = NBUF - 2;                   // stores allowed in flight before flags are published
-      const int pieces_per_chunk = (int)((chunk_bytes + PIECE - 1) / PIECE);
-      // this CTA's chunks in visiting order (right neighbour's shard first, local last)
-      int my_chunks[64];
-      int nmine = 0;
-      for (int i = 0; i < total_chunks && nmine < 64; ++i) {
-        const int src = (args.rank + 1 + i / chunks_per_shard) % args.world;
-        const int mt = (src * args.a_rows_per_src) / Cfg::TILE_M + i % chunks_per_shard;
-        if ((mt % comm_ctas) != me) continue;
-        if (src == args.rank && !args.comm_copy_local) continue;
-        my_chunks[nmine++] = i;
-      }
-      const int total = nmine * pieces_per_chunk;
-      auto piece_of = [&](int p, const uint8_t** srcp, uint8_t** dstp, uint32_t* bytes, int* src_rank) {
-        const int i = my_chunks[p / pieces_per_chunk];
-        const int src = (args.rank + 1 + i / chunks_per_shard) % args.world;
-        const int j = i % chunks_per_shard;
-        const int mt = (src * args.a_rows_per_src) / Cfg::TILE_M + j;
-        const long long off = (long long)(p % pieces_per_chunk) * PIECE;
-        *srcp = args.comm_src[src] + (long long)j * chunk_bytes + off;
+      constexpr int kLag = NBUF - 2;                   // stores allowed in flight before counters are bumped
+      const int ppc = (int)((chunk_bytes + PIECE - 1) / PIECE);          // pieces per chunk
+      const long long gtotal = (long long)nvis * ppc;
+      const int total = me < gtotal ? (int)((gtotal - 1 - me) / comm_ctas + 1) : 0;   // this CTA's pieces
+      const int parts = ppc < comm_ctas ? ppc : comm_ctas;               // CTAs sharing one chunk
+      uint32_t* piece_count = args.sync.flags + kAgCountOffset;          // per m-tile, re-armed by the publisher
+      auto chunk_of = [&](int k, int* vi, int* src, int* mt, long long* off) {   // k-th piece of this CTA
+        const long long g = me + (long long)k * comm_ctas;
+        *vi = (int)(g / ppc);
+        *src = (args.rank + 1 + *vi / chunks_per_shard) % args.world;
+        *mt = (*src * args.a_rows_per_src) / Cfg::TILE_M + *vi % chunks_per_shard;
+        *off = (g % ppc) * (long long)PIECE;
+      };
+      auto piece_of = [&](int k, const uint8_t** srcp, uint8_t** dstp, uint32_t* bytes, int* src_rank) {
+        int vi, mt;
+        long long off;
+        chunk_of(k, &vi, src_rank, &mt, &off);
+        const int j = vi % chunks_per_shard;
+        *srcp = args.comm_src[*src_rank] + (long long)j * chunk_bytes + off;
         *dstp = args.comm_dst + (long long)mt * chunk_bytes + off;
         *bytes = (uint32_t)min((long long)PIECE, chunk_bytes - off);
-        *src_rank = src;
       };
       bool failed = false;
       uint32_t ready_mask = 0;
@@ -416,16 +421,23 @@ lcsc_gemm_kernel(const __grid_constant__ GemmArgs args) {
         bulk_g2s(smem + buf * PIECE, sp, bytes, &full_bar[buf]);
         return true;
       };
-      int published = 0;                               // chunks whose flag is out
+      int counted = 0;                                 // this CTA's pieces [0, counted) are accounted
       auto publish_upto = [&](int done_pieces) {       // pieces [0, done_pieces) fully written
-        while (published < nmine && (published + 1) * pieces_per_chunk <= done_pieces) {
-          const int i = my_chunks[published];
-          const int src = (args.rank + 1 + i / chunks_per_shard) % args.world;
-          const int mt = (src * args.a_rows_per_src) / Cfg::TILE_M + i % chunks_per_shard;
-          fence_async_global();
-          __threadfence();
-          asm volatile("st.release.gpu.global.u32 [%0], %1;" :: "l"(args.sync.flags + mt), "r"(args.sync.epoch) : "memory");
-          ++published;
+        while (counted < done_pieces) {
+          int vi, src, mt, vi2 = -1, s2, mt2;
+          long long off, off2;
+          chunk_of(counted, &vi, &src, &mt, &off);
+          if (counted + 1 < total) chunk_of(counted + 1, &vi2, &s2, &mt2, &off2);
+          if (vi2 != vi) {                             // my last piece of chunk vi is in HBM
+            fence_async_global();
+            __threadfence();
+            if (atomicAdd(piece_count + mt, 1u) == (uint32_t)parts - 1) {
+              piece_count[mt] = 0;                     // every share landed: re-arm, then publish
+              __threadfence();
+              asm volatile("st.release.gpu.global.u32 [%0], %1;" :: "l"(args.sync.flags + mt), "r"(args.sync.epoch) : "memory");
+            }
+          }
+          ++counted;
         }
       };
       if (lane == 0) {

@@ -269,8 +269,6 @@ int ag_gemm(Comm* c, const pk_tensor* A, const pk_tensor* B, pk_tensor* C, pk_te
       gathered = s1->local;
     }
     if (M / tile_m > c->max_flags) return fail(PK_ERR_INVALID, "ag_gemm: too many row tiles for the flag array");
-    if ((M / tile_m + comm_clusters * cg - 1) / (comm_clusters * cg) > 64)
-      return fail(PK_ERR_INVALID, "ag_gemm: more than 64 row tiles per communicator CTA; raise num_comm_sms");
     for (int r = 0; r < n; ++r) {
       if (r == c->rank) {
         PK_TRY(tmap_a(&args.tmap_a[r], shard[r], m_loc, K, K, v.am));

@@ -19,6 +19,15 @@ ncu -i "$OUT/gemm16k.ncu-rep" --page details --csv > "$OUT/gemm16k_details.csv" 
 timeout 300 ncu --clock-control none -k regex:"moe|grp|lcsc" \
   --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --csv \
   python profiles/moe_once.py > "$OUT/moe_launches.csv" 2>&1
-# 4. the bench line itself (not under a profiler)
+# 4. full captures of the attention rank step (n = 8, S = 32K) and the MoE dispatch kernel
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:attn_fwd -s 1 -c 1 \
+  -o "$OUT/attn_rank" python profiles/attn_once.py > "$OUT/attn_capture.log" 2>&1
+ncu -i "$OUT/attn_rank.ncu-rep" --page raw --csv > "$OUT/attn_rank_raw.csv" 2>/dev/null
+ncu -i "$OUT/attn_rank.ncu-rep" --page details --csv > "$OUT/attn_rank_details.csv" 2>/dev/null
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:moe_dispatch -s 1 -c 1 \
+  -o "$OUT/moe_dispatch" python profiles/moe_once.py > "$OUT/moe_capture.log" 2>&1
+ncu -i "$OUT/moe_dispatch.ncu-rep" --page raw --csv > "$OUT/moe_dispatch_raw.csv" 2>/dev/null
+ncu -i "$OUT/moe_dispatch.ncu-rep" --page details --csv > "$OUT/moe_dispatch_details.csv" 2>/dev/null
+# 5. the bench line itself (not under a profiler)
 timeout 600 python bench.py > "$OUT/bench.json" 2> "$OUT/bench.err"
 tail -1 "$OUT/bench.json"
