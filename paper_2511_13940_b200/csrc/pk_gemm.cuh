@@ -291,15 +291,17 @@ lcsc_gemm_kernel(const __grid_constant__ GemmArgs args) {
                                          args.rs_ld + (long long)(t % num_n) * BN * 2 : 0;
       // CU vectors per thread per pass: CU (NVLS) or CU x world (P2P) 16 B
       // loads in flight per thread; one vector at a time left the
-      // communicator SMs latency-bound (~8 GB/s each)
-      constexpr int CU = 4;
-      for (int v0 = threadIdx.x; v0 < vecs; v0 += blockDim.x * CU) {
+      // communicator SMs latency-bound (~8 GB/s each). NVLS takes 8 (one
+      // reduced load per vector), P2P 4 (world loads per vector).
+      constexpr int CU = 8;
+      const int cu = args.ar_mc != nullptr ? CU : CU / 2;
+      for (int v0 = threadIdx.x; v0 < vecs; v0 += blockDim.x * cu) {
         long long off[CU];
         bool ok[CU];
 #pragma unroll
         for (int u = 0; u < CU; ++u) {
           const int v = v0 + u * (int)blockDim.x;
-          ok[u] = v < vecs;
+          ok[u] = u < cu && v < vecs;
           off[u] = base + (long long)(v / vec_per_row) * args.ar_ld + (v % vec_per_row) * 16;
         }
         auto rs_dst = [&](int u) {
@@ -318,18 +320,19 @@ lcsc_gemm_kernel(const __grid_constant__ GemmArgs args) {
             else mm_st_v4(args.ar_mc + off[u], r[u]);                       // all_reduce(): + multicast write-back
           }
         } else {
-          float acc[CU][8];
+          constexpr int CP = CU / 2;
+          float acc[CP][8];
 #pragma unroll
-          for (int u = 0; u < CU; ++u)
+          for (int u = 0; u < CP; ++u)
 #pragma unroll
             for (int e = 0; e < 8; ++e) acc[u][e] = 0.f;
           for (int d = 0; d < args.world; ++d) {              // ascending fold, primitives.py:187-195
-            uint4 x[CU];
+            uint4 x[CP];
 #pragma unroll
-            for (int u = 0; u < CU; ++u)
+            for (int u = 0; u < CP; ++u)
               if (ok[u]) x[u] = __ldcg(reinterpret_cast<const uint4*>(args.ar_buf_peer[d] + off[u]));
 #pragma unroll
-            for (int u = 0; u < CU; ++u) {
+            for (int u = 0; u < CP; ++u) {
               const uint32_t w[4] = {x[u].x, x[u].y, x[u].z, x[u].w};
 #pragma unroll
               for (int e = 0; e < 4; ++e) {
@@ -339,7 +342,7 @@ lcsc_gemm_kernel(const __grid_constant__ GemmArgs args) {
             }
           }
 #pragma unroll
-          for (int u = 0; u < CU; ++u) {
+          for (int u = 0; u < CP; ++u) {
             if (!ok[u]) continue;
             const uint4 o = make_uint4(pack_bf16x2(acc[u][0], acc[u][1]), pack_bf16x2(acc[u][2], acc[u][3]),
                                        pack_bf16x2(acc[u][4], acc[u][5]), pack_bf16x2(acc[u][6], acc[u][7]));
