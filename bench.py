@@ -408,13 +408,18 @@ def main():
                 "peak_source": f"{src} bf16_tflops (burst); sustained {peak_sus}",
                 "ag_ms": ag_ms, "rs_ms": rs_ms}
     if n > 1:
-        link_bytes = (n - 1) / n * S * S * 2
-        t_comp = flops_launch / (peak_burst * 1e12)
-        t_link = link_bytes / 770e9
-        roofline["overlapped"] = {"t_roof_ms": max(t_comp, t_link) * 1e3,
-                                  "limit": "tensor" if t_comp >= t_link else "nvlink",
-                                  "frac": max(t_comp, t_link) * 1e3 / launch_ms,
-                                  "link_bytes_per_launch": link_bytes, "link_gbs": 770}
+        # overlapped roofline of one AG-GEMM / GEMM-RS launch (costmodel.py,
+        # SURVEY.md §8d): max(compute at peak, link bytes at link bandwidth),
+        # against the measured peaks and against the north_star's nominal ones
+        from paper_2511_13940_b200 import costmodel as cm
+        meas = cm.Profile(name="measured", tensor_R=peak_burst * 1e12, link_B=770e9)
+        r_meas, r_nom = cm.ag_gemm(S, n, meas), cm.ag_gemm(S, n, cm.B200_NOMINAL)
+        roofline["overlapped"] = {"t_roof_ms": r_meas["t_roof_s"] * 1e3, "limit": r_meas["bound"],
+                                  "frac": r_meas["t_roof_s"] * 1e3 / launch_ms,
+                                  "t_roof_ms_nominal": r_nom["t_roof_s"] * 1e3,
+                                  "frac_nominal": r_nom["t_roof_s"] * 1e3 / launch_ms,
+                                  "link_bytes_per_launch": r_meas["link_bytes"], "link_gbs": 770,
+                                  "nominal": "2.25 PF/s, 900 GB/s (north_star)"}
 
     cpu = None
     if rank == 0 and world == 1:
