@@ -229,7 +229,9 @@ def local(args, out):
     for world in (2, 4):
         comms = pk.local_group(world)
         # all-reduce, P2P two-shot: every rank reads and writes S per op -> 2*n*S HBM bytes
-        for mb in ([64] if args.quick else [64, 256]):
+        # BASELINE config 3 sweeps 1 MB - 1 GB per rank (the full sweep at world 2)
+        sizes = [64] if args.quick else ([1, 4, 16, 64, 256, 1024] if world == 2 else [64, 256])
+        for mb in sizes:
             n_el = mb * (1 << 20) // 2
             ts = [c.empty((n_el,)) for c in comms]
             ms = timeit(ranks(comms, lambda r, c, s: pk.all_reduce(c, ts[r], stream=s)))
