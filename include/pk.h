@@ -20,9 +20,16 @@
  *   pk_all_reduce                      <- primitives.all_reduce (primitives.py:237-261)
  *                                         and GemmArPlan's communicator
  *                                         (workloads.py:517-546)
+ *   pk_all_reduce_ablate               <- OverheadConfig design overheads
+ *                                         (engine.py:49-60, 296-306)
  *   pk_ring_attn_fwd                   <- RingAttentionPlan (workloads.py:616-716)
- *   pk_moe_dispatch / pk_moe_combine   <- MoePlan (workloads.py:786-868); combine is new
- *   pk_grouped_gemm                    <- MoePlan's GEMM1 (workloads.py:808-815)
+ *   pk_attn_fwd                        <- the attention step of one ring rank
+ *   pk_moe_dispatch(_ex) / pk_moe_combine <- MoePlan (workloads.py:786-868); combine
+ *                                         and the expert-major layout are new
+ *   pk_grouped_gemm(_planned)          <- MoePlan's GEMM1 (workloads.py:808-815)
+ *   pk_debug_multimem                  <- the multicast primitives reduce /
+ *                                         all_reduce / signal_all
+ *                                         (primitives.py:211-288), self-test
  *   pk_gemm_ar                         <- GemmArPlan inter-SM (workloads.py:415-546)
  *   pk_ulysses_a2a                     <- UlyssesPlan (workloads.py:723-779)
  *   pk_all_gather / pk_reduce_scatter  <- AllGatherTdPlan / ReduceScatterTdPlan
