@@ -164,6 +164,23 @@ PK_DEV void poly_exp2x2(float x0, float x1, float& p0, float& p1) {
   p1 = __int_as_float(__float_as_int(q1) + (__float_as_int(t1) << 23));
 }
 
+// Cycle profile of the softmax loop (AT_PROFILE builds only): per phase,
+// summed over lane-0 threads of the softmax warps: [0] wait for S,
+// [1] TMEM load of S, [2] row max + rescale, [3] exp / P store, [4] count.
+#ifdef AT_PROFILE
+__device__ unsigned long long g_attn_prof[8];
+#define AT_PROF_MARK(k) const long long _t##k = clock64();
+#define AT_PROF_FLUSH() if (lane == 0) { \
+    atomicAdd(&g_attn_prof[0], (unsigned long long)(_t1 - _t0)); \
+    atomicAdd(&g_attn_prof[1], (unsigned long long)(_t2 - _t1)); \
+    atomicAdd(&g_attn_prof[2], (unsigned long long)(_t3 - _t2)); \
+    atomicAdd(&g_attn_prof[3], (unsigned long long)(_t4 - _t3)); \
+    atomicAdd(&g_attn_prof[4], 1ull); }
+#else
+#define AT_PROF_MARK(k)
+#define AT_PROF_FLUSH()
+#endif
+
 // Two 128-query tiles (X = 0, 1) share every K/V block; the single MMA warp
 // ping-pongs between them so one tile's softmax overlaps the other tile's
 // tensor-core work (FA4-style).
@@ -290,6 +307,9 @@ __global__ void __launch_bounds__(AT_THREADS, 1) attn_fwd_kernel(const __grid_co
         step_ready(step);
         mbar_wait(&k_empty[st], ((g >> 1) & 1) ^ 1);
         uint8_t* kb = sk + st * AT_K_BYTES;
+#ifdef AT_NO_KV_LOADS   // timing diagnostic only: K/V loaded for the first two blocks, then reused (wrong results)
+        if (g >= 2) { mbar_arrive(&k_full[st]); return; }
+#endif
         mbar_arrive_expect_tx(&k_full[st], AT_K_BYTES);
         tma_load_4d(&a.tm_k, &k_full[st], kb, 0, h, row, step * a.B + b);
         tma_load_4d(&a.tm_k, &k_full[st], kb + AT_K_BYTES / 2, 64, h, row, step * a.B + b);
@@ -313,6 +333,9 @@ __global__ void __launch_bounds__(AT_THREADS, 1) attn_fwd_kernel(const __grid_co
           const int step = j / bps, row = (j % bps) * AT_BN;
           mbar_wait(&v_empty[vs], ((gg >> 1) & 1) ^ 1);
           uint8_t* vb = sv + vs * AT_V_BYTES;
+#ifdef AT_NO_KV_LOADS
+          if (gg >= 2) { mbar_arrive(&v_full[vs]); continue; }
+#endif
           mbar_arrive_expect_tx(&v_full[vs], AT_V_BYTES);
           tma_load_4d(&a.tm_v, &v_full[vs], vb, 0, sg.h, row, step * a.B + sg.b);
           tma_load_4d(&a.tm_v, &v_full[vs], vb + AT_V_BYTES / 2, 64, sg.h, row, step * a.B + sg.b);
@@ -415,8 +438,10 @@ __global__ void __launch_bounds__(AT_THREADS, 1) attn_fwd_kernel(const __grid_co
     const int len = sg.j1 - sg.j0;
     float m = -INFINITY, l = 0.f;     // m: the max the current P values are relative to (log2 units)
     for (int i = 0; i < len; ++i, ++gx) {
+      AT_PROF_MARK(0);
       mbar_wait(&s_full[x], gx & 1);
       tc_fence_after();
+      AT_PROF_MARK(1);
 #ifdef AT_MMA_ONLY   // timing diagnostic only: the MMA pipeline without softmax (wrong results)
       if (lane == 0) { mbar_arrive(&p_full[2 * x]); mbar_arrive(&p_full[2 * x + 1]); }
       continue;
@@ -427,6 +452,7 @@ __global__ void __launch_bounds__(AT_THREADS, 1) attn_fwd_kernel(const __grid_co
 #pragma unroll
       for (int c = 0; c < 4; ++c) tmem_ld_32x32b_x32(t_s + c * 32, *reinterpret_cast<uint32_t(*)[32]>(r + c * 32));
       tmem_ld_wait();
+      AT_PROF_MARK(2);
       // row max as 8 independent FMNMX3 chains (a single chain is 64 dependent ops)
       float m8[8];
 #pragma unroll
@@ -451,6 +477,7 @@ __global__ void __launch_bounds__(AT_THREADS, 1) attn_fwd_kernel(const __grid_co
         l *= alpha;
       }
       if (grow) m = mx;
+      AT_PROF_MARK(3);
       // packed fp32 pairs: one FFMA2 computes s*scale - m for two keys, one FADD2
       // accumulates two probabilities (the softmax warps are issue-bound)
       const uint64_t sc2 = f2_pack(sc, sc), nm2 = f2_pack(-m, -m);
@@ -485,6 +512,8 @@ __global__ void __launch_bounds__(AT_THREADS, 1) attn_fwd_kernel(const __grid_co
       float rs_lo, rs_hi;
       f2_unpack(f2_add(f2_add(rs2[0], rs2[1]), f2_add(rs2[2], rs2[3])), rs_lo, rs_hi);
       l += rs_lo + rs_hi;
+      AT_PROF_MARK(4);
+      AT_PROF_FLUSH();
     }
     // ------------------------------------------------------------ epilogue
     mbar_wait(&o_full[x], segx & 1);
@@ -844,6 +873,17 @@ int attn_local(const pk_tensor* q, const pk_tensor* k, const pk_tensor* v, pk_te
 }
 
 }  // namespace pk
+
+#ifdef AT_PROFILE
+extern "C" PK_API int pk_debug_attn_prof(unsigned long long* out, int reset) {
+  PK_CUDA(cudaMemcpyFromSymbol(out, pk::g_attn_prof, sizeof(unsigned long long) * 8));
+  if (reset) {
+    unsigned long long z[8] = {};
+    PK_CUDA(cudaMemcpyToSymbol(pk::g_attn_prof, z, sizeof(z)));
+  }
+  return PK_OK;
+}
+#endif
 
 extern "C" PK_API int pk_attn_fwd(const pk_tensor* q, const pk_tensor* k, const pk_tensor* v, pk_tensor* o,
                                   pk_tensor* lse, float softmax_scale, void* stream) {
