@@ -87,20 +87,37 @@ int preload_gemm() {
   return PK_OK;
 }
 
-// Pick the tile shape for a row partition of `rows_per_part` rows:
-//   512-row pair tiles (256 x 256 per CTA, one TMEM accumulator stage) cut
-//   L2->SM traffic by 25% vs 256-row pair tiles; the latter double-buffer
-//   TMEM so the epilogue overlaps the next tile, which wins at small K.
-static Variant pick_variant(int64_t rows_per_part, int64_t K, const pk_sched* sched, bool reduce = false) {
+// Pick the tile shape for a row partition of `rows_per_part` rows of a GEMM
+// with M x N outputs run on `clusters` CTA pairs:
+//   512-row pair tiles (256 x 256 per CTA, one TMEM accumulator stage) move
+//   25% fewer bytes into each SM and, with the early TMEM release in the
+//   epilogue, issue as many MMAs per clock as the double-buffered 256-row
+//   tiles: ~5% faster under the 1 kW power cap (profiles/gemm_power.py: 1438
+//   vs 1378 TF/s at 16384^3). But half as many tiles can leave a partial last
+//   wave: take 256-row tiles when their wave efficiency beats the 512-row
+//   tiles' by more than that 5% (e.g. 8192 x 4096 on 74 pairs: 256 tiles,
+//   3.46 waves -> 86.5 %, vs 512 tiles, 6.92 waves -> 98.8 %).
+static double wave_eff(int64_t tiles, int64_t clusters) {
+  if (tiles <= 0 || clusters <= 0) return 1.0;
+  const int64_t waves = (tiles + clusters - 1) / clusters;
+  return (double)tiles / (double)(waves * clusters);
+}
+
+static Variant pick_variant(int64_t rows_per_part, int64_t K, const pk_sched* sched, bool reduce = false,
+                            int64_t M = 0, int64_t N = 0, int64_t clusters = 0) {
   int force_am = 0;
   if (const char* e = getenv("PK_GEMM_AM")) force_am = atoi(e);
   if (sched && sched->stages < 0) force_am = -sched->stages;     // test hook: stages = -am
-  // 512-row pair tiles by default: with the early TMEM release in the
-  // epilogue they issue as many MMAs per clock as the double-buffered 256-row
-  // tiles and, moving 25% fewer bytes into each SM, run ~5% faster under the
-  // 1 kW power cap (profiles/gemm_power.py: 1438 vs 1378 TF/s at 16384^3).
   (void)reduce;
-  if (rows_per_part % 512 == 0 && force_am != 1) return {2, 2};
+  (void)K;
+  if (rows_per_part % 512 == 0 && force_am != 1) {
+    if (force_am != 2 && M > 0 && N > 0 && clusters > 0) {
+      const double e2 = wave_eff((M / 512) * (N / 256), clusters);
+      const double e1 = wave_eff((M / 256) * (N / 256), clusters);
+      if (e1 * 0.95 > e2) return {2, 1};
+    }
+    return {2, 2};
+  }
   if (rows_per_part % 256 == 0) return {2, 1};
   return {1, 1};
 }
@@ -150,7 +167,7 @@ int gemm_local(const pk_tensor* A, const pk_tensor* B, pk_tensor* C, const pk_sc
   if (M % 128 || N % 256 || K % BLOCK_K || K == 0)
     return fail(PK_ERR_INVALID, "gemm: need M %% 128 == 0, N %% 256 == 0, K %% 64 == 0 (got %lld, %lld, %lld)",
                 (long long)M, (long long)N, (long long)K);
-  const Variant v = pick_variant(M, K, sched);
+  const Variant v = pick_variant(M, K, sched, false, M, N, default_sms(device, sched) / 2);
   const int cg = v.cg;
   GemmArgs args;
   init_args(args, v.am);
@@ -219,7 +236,10 @@ int ag_gemm(Comm* c, const pk_tensor* A, const pk_tensor* B, pk_tensor* C, pk_te
     if (AG) PK_CUDA(cudaMemcpy2DAsync(AG->ptr, K * 2, A->ptr, ldA * 2, K * 2, m_loc, cudaMemcpyDeviceToDevice, st));
     return PK_OK;
   }
-  const Variant v = pick_variant(m_loc, K, sched);
+  // compute pairs: all of this rank's SMs less the communicator share (as below)
+  const int64_t ag_pairs = std::max(1, (sched && sched->num_sms > 0 ? std::min(sched->num_sms, c->num_sms) : c->num_sms) / 2 -
+                                           ((sched && sched->num_comm_sms > 0) ? sched->num_comm_sms : 16) / 2);
+  const Variant v = pick_variant(m_loc, K, sched, false, M, n_loc, ag_pairs);
   const int cg = v.cg;
   const int tile_m = 128 * v.am * cg;
   const int num_n = (int)(n_loc / 256);
@@ -377,7 +397,8 @@ int gemm_rs(Comm* c, const pk_tensor* A, const pk_tensor* B, pk_tensor* O, const
                 (long long)m_own, (long long)N, (long long)k_loc);
   if (n == 1) return gemm_local(A, B, O, sched, st, c->device);
   if (sched && (sched->mode == PK_INTER_SM || sched->mode == PK_HYBRID)) return gemm_rs_inter(c, A, B, O, sched, st);
-  const Variant v = pick_variant(m_own, k_loc, sched, /*reduce=*/true);
+  const Variant v = pick_variant(m_own, k_loc, sched, /*reduce=*/true, M, N,
+                                 (sched && sched->num_sms > 0 ? std::min(sched->num_sms, c->num_sms) : c->num_sms) / 2);
   const int cg = v.cg;
   const int tile_m = 128 * v.am * cg;
   // Destination of every rank (zero-copy when `out` is symmetric).
