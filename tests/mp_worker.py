@@ -57,6 +57,33 @@ def main():
     torch.cuda.synchronize()
     comm.check()
     assert np.array_equal(x.cpu().numpy(), oracle.all_reduce(X)[rank]), "all_reduce"
+    # ring attention: every peer's KV shard pulled by the copy engine from its VMM mapping
+    B_, S_, H_ = 1, 256, 2
+    gq = torch.Generator().manual_seed(11)
+    qs = [torch.randn(B_, S_, H_, 128, generator=gq).bfloat16() for _ in range(world)]
+    ks = [torch.randn(B_, S_, H_, 128, generator=gq).bfloat16() for _ in range(world)]
+    vs = [torch.randn(B_, S_, H_, 128, generator=gq).bfloat16() for _ in range(world)]
+    o, lse = pk.ring_attention(comm, qs[rank].cuda(), ks[rank].cuda(), vs[rank].cuda())
+    torch.cuda.synchronize()
+    comm.check()
+    npy = lambda t: t.float().numpy()
+    ref_o, ref_l = oracle.ring_attention([npy(t) for t in qs], [npy(t) for t in ks], [npy(t) for t in vs], 128 ** -0.5)
+    assert np.abs(o.float().cpu().numpy() - ref_o[rank]).max() <= 2e-2, "ring_attention"
+    # MoE dispatch (reference slot order) + combine
+    T, E, Kk, Hm = 64, 4 * world, 2, 256
+    route, owners = oracle.moe_route(oracle.plan_rng(3), world, T, E, Kk)
+    toks = [rng.integers(-8, 9, size=(T, Hm)).astype(np.float32) for _ in range(world)]
+    recv, src, cnt = pk.moe_dispatch(comm, bf(toks[rank]), torch.from_numpy(route[rank].astype(np.int32)).cuda(), E)
+    torch.cuda.synchronize()
+    comm.check()
+    exp_recv = oracle.moe_dispatch(toks, owners)[rank]
+    assert int(cnt.item()) == exp_recv.shape[0], "moe count"
+    assert np.array_equal(recv[:exp_recv.shape[0]].float().cpu().numpy(), exp_recv), "moe_dispatch"
+    w = torch.ones(T, Kk, device="cuda")
+    comb = pk.moe_combine(comm, recv, torch.from_numpy(route[rank].astype(np.int32)).cuda(), w, E)
+    torch.cuda.synchronize()
+    comm.check()
+    assert np.array_equal(comb.float().cpu().numpy(), Kk * toks[rank]), "moe_combine"
     comm.destroy()
     dist.barrier()
     dist.destroy_process_group()
