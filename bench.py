@@ -136,6 +136,13 @@ def cpu_oracle_rate(size: int, seconds: float, slab_div: int = 1):
     a = (rng.standard_normal((rows, size)) * 0.1).astype(np.float32)
     b = (rng.standard_normal((size, size)) * 0.1).astype(np.float32)
     flops_per = 2 * 2.0 * rows * size * size
+    # every host thread (torchrun exports OMP_NUM_THREADS=1 to each rank, which
+    # would otherwise pin the BLAS under the oracle to one core)
+    try:
+        from threadpoolctl import threadpool_limits
+        limiter = threadpool_limits(limits=cpu_threads())
+    except Exception:
+        limiter = None
     oracle.ag_gemm([a], [b], dtype=np.float32)  # warm
     reps, t0 = 0, time.perf_counter()
     while True:
@@ -145,6 +152,8 @@ def cpu_oracle_rate(size: int, seconds: float, slab_div: int = 1):
         dt = time.perf_counter() - t0
         if dt >= seconds:
             break
+    if limiter is not None:
+        limiter.restore_original_limits()
     tf = flops_per * reps / dt / 1e12
     sample = (f"oracle.ag_gemm + oracle.gemm_rs (numpy float32) at n=1, rows {rows} of M={size}, "
               f"N=K={size}; {reps} steps in {dt:.1f}s")
@@ -168,6 +177,11 @@ def run_reference(args):
     a = (rng.standard_normal((rows, S)) * 0.1).astype(np.float32)
     b = (rng.standard_normal((S, S)) * 0.1).astype(np.float32)
     flops = 2 * 2.0 * rows * S * S
+    try:                                   # every host thread, even under torchrun's OMP_NUM_THREADS=1
+        from threadpoolctl import threadpool_limits
+        threadpool_limits(limits=cpu_threads())
+    except Exception:
+        pass
     for _ in range(args.warmup):
         oracle.ag_gemm([a], [b], dtype=np.float32)
         oracle.gemm_rs([a], [b], dtype=np.float32)
