@@ -59,6 +59,7 @@ constexpr float AT_RESCALE_THRESHOLD = 8.0f;     // log2 units: P stays <= 2^8 b
 
 struct AttnArgs {
   CUtensorMap tm_q, tm_k, tm_v;  // 4-D maps over [B, S, H, D] (dims D, H, S, B)
+  CUtensorMap tm_k2;             // K with 64-row boxes (the CTA-pair kernel's half blocks)
   int B, S_q, S_kv, H;
   float scale_log2;              // softmax_scale * log2(e)
   // single-launch ring: KV of ring step s lives at batch coordinate s*B + b of
@@ -608,6 +609,297 @@ __global__ void __launch_bounds__(AT_THREADS, 1) attn_fwd_kernel(const __grid_co
   }
 }
 
+// ---------------------------------------------------------------- CTA-pair kernel
+// attn2_fwd_kernel: the same FA4-style pipeline on a CTA pair (cluster of 2,
+// tcgen05 cta_group::2). A cluster owns four 128-query tiles of one
+// (batch, head): CTA c holds tiles 2c and 2c+1 ("tile x" of CTA c is query
+// tile 2c + x). Every MMA spans the pair (M = 256: tile x of CTA 0 over tile x
+// of CTA 1), with the B operand split across the two CTAs' shared memory:
+//   S_x = Q_x K^T : each CTA stages half of the K block (64 of the 128 keys)
+//   O_x += P_x V  : each CTA stages half of the V block (64 of the 128 dims)
+// so each SM reads 6 KB of smem per K16 step of QK instead of 8 KB, 2 KB
+// instead of 4 KB per PV step, and TMA-writes half the K/V bytes: the
+// single-CTA kernel's smem traffic (~98 % of its 128 B/clk) was what held its
+// MMA pipeline to ~80 % of peak. The leader CTA's MMA warp issues for the
+// pair; TMA completions and the softmax warps' P-ready arrivals go to the
+// leader's barriers, MMA commits multicast to both CTAs. One item per
+// cluster (no split tail).
+constexpr int AT2_KH_BYTES = (AT_BN / 2) * AT_D * 2;   // 16 KB: 64 keys x 128 dims
+constexpr int AT2_VH_BYTES = AT_BN * (AT_D / 2) * 2;   // 16 KB: 128 keys x 64 dims
+constexpr int AT2_SMEM = 2 * AT_Q_BYTES + 2 * AT2_KH_BYTES + 2 * AT2_VH_BYTES + 512 + 1024;
+
+PK_DEV void tma_load_4d_2sm(const CUtensorMap* m, uint64_t* bar, void* dst, int c0, int c1, int c2, int c3) {
+  const uint32_t b = smem_u32(bar) & 0xFEFFFFFFu;     // completion on the leader CTA's barrier
+  asm volatile(
+      "cp.async.bulk.tensor.4d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5, %6}], [%2];"
+      :: "r"(smem_u32(dst)), "l"(reinterpret_cast<uint64_t>(m)), "r"(b),
+         "r"(c0), "r"(c1), "r"(c2), "r"(c3) : "memory");
+}
+PK_DEV void umma_f16_ts2(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc, uint32_t idesc, uint32_t accum) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], [%1], %2, %3, p;\n\t}"
+      :: "r"(tmem_d), "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(accum) : "memory");
+}
+
+__global__ void __launch_bounds__(AT_THREADS, 1) attn2_fwd_kernel(const __grid_constant__ AttnArgs a) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sq = smem;                               // [2][32 KB]: this CTA's two query tiles
+  uint8_t* sk = sq + 2 * AT_Q_BYTES;                // [2][16 KB]: keys [64c, 64c+64) of the block
+  uint8_t* sv = sk + 2 * AT2_KH_BYTES;              // [2][16 KB]: dims [64c, 64c+64) of the block
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sv + 2 * AT2_VH_BYTES);
+  uint64_t* q_full = bars + 0;      // leader: both CTAs' Q
+  uint64_t* k_full = bars + 1;      // [2] leader: both K halves
+  uint64_t* k_empty = bars + 3;     // [2] both CTAs (multicast commit)
+  uint64_t* v_full = bars + 5;      // [2] leader
+  uint64_t* v_empty = bars + 7;     // [2] both
+  uint64_t* s_full = bars + 9;      // [2] both, per tile
+  uint64_t* p_full = bars + 11;     // [2 tiles][2 halves] leader: 8 arrivals (4 warps x 2 CTAs)
+  uint64_t* o_full = bars + 15;     // [2] both
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 17);
+
+  const uint32_t warp = warp_id_sync();
+  const uint32_t lane = lane_id();
+  const uint32_t cta = cluster_ctarank();
+  const bool leader = cta == 0;
+  const int quads = a.S_q / (4 * AT_BM);
+  const int cl = (int)cluster_id_x();
+  const int qd = cl % quads;
+  const int h = (cl / quads) % a.H;
+  const int b = cl / (quads * a.H);
+  const int nblk = a.S_kv / AT_BN;
+
+  if (warp == 0 && lane == 0) {
+    mbar_init(q_full, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&k_full[i], 1); mbar_init(&k_empty[i], 1);
+      mbar_init(&v_full[i], 1); mbar_init(&v_empty[i], 1);
+      mbar_init(&s_full[i], 1); mbar_init(&o_full[i], 1);
+      mbar_init(&p_full[2 * i], 8); mbar_init(&p_full[2 * i + 1], 8);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 2) tmem_alloc<AT_TMEM_COLS, 2>(tmem_slot);
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp < 4) {
+  asm volatile("setmaxnreg.dec.sync.aligned.u32 56;\n" ::: "memory");
+  if (warp == 0) {
+    // ------------------------------------------------------------ loader (lane 0, both CTAs)
+    if (lane == 0) {
+      const int bps = a.blocks_per_step;
+      int ready_steps = 1;
+      auto step_ready = [&](int step) {
+        while (a.step_flags != nullptr && ready_steps <= step) {
+          wait_geq(a.step_flags + ready_steps, a.flag_epoch, a.err, a.timeout_ns);
+          fence_async_global();
+          ++ready_steps;
+        }
+      };
+      if (leader) mbar_arrive_expect_tx(q_full, 2 * 2 * AT_Q_BYTES);
+      for (int x = 0; x < 2; ++x) {
+        const int qrow = (4 * qd + 2 * (int)cta + x) * AT_BM;
+        tma_load_4d_2sm(&a.tm_q, q_full, sq + x * AT_Q_BYTES, 0, h, qrow, b);
+        tma_load_4d_2sm(&a.tm_q, q_full, sq + x * AT_Q_BYTES + AT_Q_BYTES / 2, 64, h, qrow, b);
+      }
+      auto load_k = [&](int j) {
+        const int st = j & 1;
+        const int step = j / bps, row = (j % bps) * AT_BN + (int)cta * (AT_BN / 2);
+        step_ready(step);
+        mbar_wait(&k_empty[st], ((j >> 1) & 1) ^ 1);
+        uint8_t* kb = sk + st * AT2_KH_BYTES;
+        if (leader) mbar_arrive_expect_tx(&k_full[st], 2 * AT2_KH_BYTES);
+        tma_load_4d_2sm(&a.tm_k2, &k_full[st], kb, 0, h, row, step * a.B + b);
+        tma_load_4d_2sm(&a.tm_k2, &k_full[st], kb + AT2_KH_BYTES / 2, 64, h, row, step * a.B + b);
+      };
+      if (nblk > 0) load_k(0);
+      for (int j = 0; j < nblk; ++j) {
+        if (j + 1 < nblk) load_k(j + 1);
+        const int vs = j & 1;
+        const int step = j / bps, row = (j % bps) * AT_BN;
+        mbar_wait(&v_empty[vs], ((j >> 1) & 1) ^ 1);
+        if (leader) mbar_arrive_expect_tx(&v_full[vs], 2 * AT2_VH_BYTES);
+        tma_load_4d_2sm(&a.tm_v, &v_full[vs], sv + vs * AT2_VH_BYTES, (int)cta * 64, h, row, step * a.B + b);
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1 && leader) {
+    // ------------------------------------------------------------ MMA issuer (leader)
+    constexpr uint32_t id_s = idesc_bf16(2 * AT_BM, AT_BN, 0);
+    constexpr uint32_t id_o = idesc_bf16(2 * AT_BM, AT_D, 1);
+    auto issue_qk = [&](int x, int j) {
+      const uint32_t q_addr = smem_u32(sq + x * AT_Q_BYTES);
+      const uint32_t k_addr = smem_u32(sk + (j & 1) * AT2_KH_BYTES);
+#pragma unroll
+      for (int kk = 0; kk < AT_D / 16; ++kk) {
+        const int atom = kk >> 2, sub = kk & 3;
+        const uint64_t ad = sdesc_kmajor_sw128(q_addr + atom * (AT_Q_BYTES / 2)) + (uint64_t)(sub * 2);
+        const uint64_t bd = sdesc_kmajor_sw128(k_addr + atom * (AT2_KH_BYTES / 2)) + (uint64_t)(sub * 2);
+        umma_f16<2>(tmem + 256 * x, ad, bd, id_s, kk > 0 ? 1u : 0u);
+      }
+      umma_commit<2>(&s_full[x]);
+    };
+    auto issue_pv = [&](int x, int j, int half) {
+      const uint32_t v_addr = smem_u32(sv + (j & 1) * AT2_VH_BYTES);
+#pragma unroll
+      for (int k4 = 0; k4 < AT_BN / 32; ++k4) {
+        const int kk = half * (AT_BN / 32) + k4;
+        const uint64_t bd = sdesc_mnmajor_sw128(v_addr + kk * 2048, AT2_VH_BYTES, 1024);
+        umma_f16_ts2(tmem + 256 * x + 128, tmem + 256 * x + kk * 8, bd, id_o, (j > 0 || kk > 0) ? 1u : 0u);
+      }
+      if (half == 1 && j == nblk - 1) umma_commit<2>(&o_full[x]);
+    };
+    mbar_wait(q_full, 0);
+    tc_fence_after();
+    if (nblk > 0) {
+      mbar_wait(&k_full[0], 0);
+      tc_fence_after();
+      if (elect_one()) {
+        for (int x = 0; x < 2; ++x) issue_qk(x, 0);
+        umma_commit<2>(&k_empty[0]);
+      }
+      __syncwarp();
+    }
+    for (int j = 0; j < nblk; ++j) {
+      mbar_wait(&v_full[j & 1], (j >> 1) & 1);
+      const bool more = j + 1 < nblk;
+      if (more) mbar_wait(&k_full[(j + 1) & 1], ((j + 1) >> 1) & 1);
+      for (int x = 0; x < 2; ++x) {
+        mbar_wait(&p_full[2 * x], j & 1);
+        tc_fence_after();
+        if (elect_one()) issue_pv(x, j, 0);
+        __syncwarp();
+        mbar_wait(&p_full[2 * x + 1], j & 1);
+        tc_fence_after();
+        if (elect_one()) {
+          issue_pv(x, j, 1);
+          if (more) issue_qk(x, j + 1);
+        }
+        __syncwarp();
+      }
+      if (elect_one()) {
+        umma_commit<2>(&v_empty[j & 1]);
+        if (more) umma_commit<2>(&k_empty[(j + 1) & 1]);
+      }
+      __syncwarp();
+    }
+  }
+  } else {
+  asm volatile("setmaxnreg.inc.sync.aligned.u32 224;\n" ::: "memory");
+  // ------------------------------------------------------------ softmax + epilogue (tile x of this CTA)
+  const int x = (warp - 4) / 4;
+  const int qt = 4 * qd + 2 * (int)cta + x;
+  const int q = warp & 3;
+  const int row = q * 32 + (int)lane;
+  const uint32_t lane_off = (uint32_t)(q * 32) << 16;
+  const uint32_t t_s = tmem + 256 * x + lane_off;
+  const uint32_t t_o = t_s + 128;
+  float m = -INFINITY, l = 0.f;
+  const float sc = a.scale_log2;
+  for (int j = 0; j < nblk; ++j) {
+    mbar_wait(&s_full[x], j & 1);
+    tc_fence_after();
+    uint32_t r[AT_BN];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) tmem_ld_32x32b_x32(t_s + c * 32, *reinterpret_cast<uint32_t(*)[32]>(r + c * 32));
+    tmem_ld_wait();
+    float m8[8];
+#pragma unroll
+    for (int t = 0; t < 8; ++t) m8[t] = fmax3(__uint_as_float(r[2 * t]), __uint_as_float(r[2 * t + 1]), -INFINITY);
+#pragma unroll
+    for (int i2 = 8; i2 < AT_BN / 2; ++i2)
+      m8[i2 & 7] = fmax3(m8[i2 & 7], __uint_as_float(r[2 * i2]), __uint_as_float(r[2 * i2 + 1]));
+    float mx = fmax3(fmax3(m8[0], m8[1], m8[2]), fmax3(m8[3], m8[4], m8[5]), fmaxf(m8[6], m8[7]));
+    mx *= sc;
+    const bool grow = mx > m + AT_RESCALE_THRESHOLD;
+    if (j > 0 && __any_sync(0xffffffffu, grow)) {
+      const float alpha = grow ? fast_exp2(m - mx) : 1.f;
+#pragma unroll 1
+      for (int c = 0; c < 4; ++c) {
+        uint32_t o[32];
+        tmem_ld_32x32b_x32(t_o + c * 32, o);
+        tmem_ld_wait();
+#pragma unroll
+        for (int i2 = 0; i2 < 32; ++i2) o[i2] = __float_as_uint(__uint_as_float(o[i2]) * alpha);
+        tmem_st_32x32b_x32(t_o + c * 32, o);
+      }
+      l *= alpha;
+    }
+    if (grow) m = mx;
+    const uint64_t sc2 = f2_pack(sc, sc), nm2 = f2_pack(-m, -m);
+    uint64_t rs2[4];
+#pragma unroll
+    for (int t = 0; t < 4; ++t) rs2[t] = f2_pack(0.f, 0.f);
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      uint32_t pk[16];
+#pragma unroll
+      for (int i2 = 0; i2 < 16; ++i2) {
+        float x0, x1, p0, p1;
+        f2_unpack(f2_fma(f2_pack(__uint_as_float(r[32 * c + 2 * i2]), __uint_as_float(r[32 * c + 2 * i2 + 1])), sc2, nm2),
+                  x0, x1);
+        if ((i2 & 3) < AT_EXP_EMU) {
+          poly_exp2x2(x0, x1, p0, p1);
+        } else {
+          p0 = fast_exp2(x0);
+          p1 = fast_exp2(x1);
+        }
+        rs2[i2 & 3] = f2_add(rs2[i2 & 3], f2_pack(p0, p1));
+        pk[i2] = pack_bf16x2(p0, p1);
+      }
+      tmem_st_32x32b_x16(t_s + c * 16, pk);
+      if (c & 1) {                                     // keys [64h, 64h+64) in TMEM: tell the leader's MMA warp
+        tmem_st_wait();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_cluster(&p_full[2 * x + (c >> 1)], 0);
+      }
+    }
+    float rs_lo, rs_hi;
+    f2_unpack(f2_add(f2_add(rs2[0], rs2[1]), f2_add(rs2[2], rs2[3])), rs_lo, rs_hi);
+    l += rs_lo + rs_hi;
+  }
+  // ------------------------------------------------------------ epilogue
+  mbar_wait(&o_full[x], 0);
+  tc_fence_after();
+  float o[AT_D];
+#pragma unroll
+  for (int c = 0; c < AT_D / 32; ++c) {
+    uint32_t t[32];
+    tmem_ld_32x32b_x32(t_o + c * 32, t);
+    tmem_ld_wait();
+#pragma unroll
+    for (int i2 = 0; i2 < 32; ++i2) o[c * 32 + i2] = __uint_as_float(t[i2]);
+  }
+  const int sq_idx = qt * AT_BM + row;
+  const long long srow = ((long long)(b * a.H + h) * a.S_q + sq_idx);
+  const float inv = (l > 0.f) ? 1.f / l : 0.f;
+  uint4* dst = reinterpret_cast<uint4*>(a.o + (((long long)b * a.S_q + sq_idx) * a.H + h) * AT_D);
+#pragma unroll
+  for (int i2 = 0; i2 < AT_D / 8; ++i2) {
+    uint4 w;
+    w.x = pack_bf16x2(o[8 * i2 + 0] * inv, o[8 * i2 + 1] * inv);
+    w.y = pack_bf16x2(o[8 * i2 + 2] * inv, o[8 * i2 + 3] * inv);
+    w.z = pack_bf16x2(o[8 * i2 + 4] * inv, o[8 * i2 + 5] * inv);
+    w.w = pack_bf16x2(o[8 * i2 + 6] * inv, o[8 * i2 + 7] * inv);
+    dst[i2] = w;
+  }
+  a.lse[srow] = (m + log2f(l)) * 0.69314718055994531f;
+  }
+  tc_fence_before();
+  cluster_sync();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc<AT_TMEM_COLS, 2>(tmem);
+  }
+}
+
 // ---------------------------------------------------------------- sync kernels
 __global__ void sync_signal_kernel(uint32_t* p0, uint32_t* p1, uint32_t* p2, uint32_t* p3, uint32_t* p4,
                                    uint32_t* p5, uint32_t* p6, uint32_t* p7, int n) {
@@ -626,6 +918,7 @@ __global__ void sync_wait_kernel(const uint32_t* counters, int n, uint32_t expec
 int preload_attn() {
   cudaFuncAttributes fa;
   PK_CUDA(cudaFuncGetAttributes(&fa, attn_fwd_kernel));
+  PK_CUDA(cudaFuncGetAttributes(&fa, attn2_fwd_kernel));
   PK_CUDA(cudaFuncGetAttributes(&fa, sync_signal_kernel));
   PK_CUDA(cudaFuncGetAttributes(&fa, sync_wait_kernel));
   PK_CUDA(cudaFuncGetAttributes(&fa, flag_set_kernel));
@@ -674,6 +967,24 @@ static int tmap_bshd(CUtensorMap* m, const void* p, int64_t B, int64_t S, int64_
 // Grid: one CTA per item when the items fill whole waves, else a persistent
 // stream-K grid of one CTA per SM sharing all key blocks evenly.
 static int launch_attn(AttnScratch& scr, int num_sms, AttnArgs& a, cudaStream_t st) {
+  // CTA-pair kernel (tuning hook for now): four query tiles per cluster
+  if (getenv("PK_ATTN_PAIR") && a.S_q % (4 * AT_BM) == 0) {
+    PK_TRY(ensure_smem_attr((const void*)attn2_fwd_kernel, AT2_SMEM));
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(2 * a.B * a.H * (a.S_q / (4 * AT_BM)), 1, 1);
+    cfg.blockDim = dim3(AT_THREADS, 1, 1);
+    cfg.dynamicSmemBytes = AT2_SMEM;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    PK_CUDA(cudaLaunchKernelEx(&cfg, attn2_fwd_kernel, a));
+    return PK_OK;
+  }
   PK_TRY(ensure_smem_attr((const void*)attn_fwd_kernel, AT_SMEM));
   const int items = a.B * a.H * ((a.S_q / AT_BM + 1) / 2);
   const int nblk = a.S_kv / AT_BN;
@@ -753,6 +1064,7 @@ int ring_attn_fwd(Comm* c, const pk_tensor* q, const pk_tensor* k, const pk_tens
   PK_TRY(tmap_bshd(&a.tm_q, q->ptr, B, S, H, AT_BM));
   if (n == 1) {
     PK_TRY(tmap_bshd(&a.tm_k, k->ptr, B, S, H, AT_BN));
+    PK_TRY(tmap_bshd(&a.tm_k2, k->ptr, B, S, H, AT_BN / 2));
     PK_TRY(tmap_bshd(&a.tm_v, v->ptr, B, S, H, AT_BN));
     a.blocks_per_step = (int)(S / AT_BN);
     return launch_attn(c->attn, c->num_sms, a, st);
@@ -816,6 +1128,7 @@ int ring_attn_fwd(Comm* c, const pk_tensor* q, const pk_tensor* k, const pk_tens
   PK_CUDA(cudaEventRecord(ev_side, side));
   // 3. one attention launch over all n*S/n keys; the loader waits step flags.
   PK_TRY(tmap_bshd(&a.tm_k, kst, (int64_t)n * B, S, H, AT_BN));
+  PK_TRY(tmap_bshd(&a.tm_k2, kst, (int64_t)n * B, S, H, AT_BN / 2));
   PK_TRY(tmap_bshd(&a.tm_v, vst, (int64_t)n * B, S, H, AT_BN));
   a.S_kv = (int)(n * S);
   a.blocks_per_step = (int)(S / AT_BN);
@@ -867,6 +1180,7 @@ int attn_local(const pk_tensor* q, const pk_tensor* k, const pk_tensor* v, pk_te
   a.blocks_per_step = (int)(Skv / AT_BN);
   PK_TRY(tmap_bshd(&a.tm_q, q->ptr, B, S, H, AT_BM));
   PK_TRY(tmap_bshd(&a.tm_k, k->ptr, B, Skv, H, AT_BN));
+  PK_TRY(tmap_bshd(&a.tm_k2, k->ptr, B, Skv, H, AT_BN / 2));
   PK_TRY(tmap_bshd(&a.tm_v, v->ptr, B, Skv, H, AT_BN));
   std::lock_guard<std::mutex> lk(g_attn_mu);
   return launch_attn(g_attn_scratch[{dev, st}], sms, a, st);

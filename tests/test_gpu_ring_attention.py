@@ -107,3 +107,21 @@ def test_stream_k_more_ctas_than_tail_blocks(monkeypatch):
     monkeypatch.setenv("PK_ATTN_SMS", "40")
     monkeypatch.setenv("PK_ATTN_FORCE_SPLIT", "1")
     run(1, 1, 512, 3, seed=9)        # 6 items x 4 blocks = 24 tail blocks over 40 CTAs
+
+
+@pytest.mark.parametrize("B,Sq,Skv,H", [(1, 512, 512, 1), (1, 1024, 2048, 2), (2, 512, 1024, 3)])
+def test_cta_pair_kernel_matches_oracle(monkeypatch, B, Sq, Skv, H):
+    """The experimental cta_group::2 attention kernel (PK_ATTN_PAIR=1): four
+    query tiles per cluster, K and V halves split across the pair."""
+    pk = _pk()
+    monkeypatch.setenv("PK_ATTN_PAIR", "1")
+    g = torch.Generator(device="cuda").manual_seed(Sq + Skv + H)
+    q = torch.randn(B, Sq, H, 128, device="cuda", generator=g).bfloat16()
+    k = torch.randn(B, Skv, H, 128, device="cuda", generator=g).bfloat16()
+    v = torch.randn(B, Skv, H, 128, device="cuda", generator=g).bfloat16()
+    o, lse = pk.attention(q, k, v)
+    torch.cuda.synchronize()
+    npy = lambda t: t.float().cpu().numpy()
+    ref_o, ref_l = oracle.attention_fwd(npy(q), npy(k), npy(v), 128 ** -0.5)
+    assert np.abs(npy(o) - ref_o).max() <= 2e-2
+    assert np.abs(lse.cpu().numpy() - ref_l).max() <= 1e-3 * max(1.0, np.abs(ref_l).max())
