@@ -19,7 +19,7 @@ _os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
 from .errors import (DeadlockError, LcscError, MemSimError, MulticastReadError,  # noqa: F401
                      PkCudaError, PkError, PrimitiveError, ProtocolViolation, WorkloadError)
 from .comm import Comm, Pgl, local_group  # noqa: F401
-from . import costmodel, tune  # noqa: F401
+from . import costmodel, hwmodel, tune  # noqa: F401
 from .ops import (all_gather, all_gather_gemm, all_reduce, all_reduce_with_overheads, all_to_all,  # noqa: F401
                   attention, gemm, gemm_all_reduce, gemm_reduce_scatter, grouped_gemm, moe_capacity,
                   moe_combine, moe_dispatch, reduce_scatter, ring_attention, ulysses_all_to_all)
