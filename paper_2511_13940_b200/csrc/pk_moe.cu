@@ -559,8 +559,7 @@ int moe_dispatch(Comm* c, const pk_tensor* x, const pk_tensor* topk, int num_exp
   int T, K;
   MoeArgs a;
   PK_TRY(moe_common(c, topk, num_experts, layout, a, &T, &K));
-  if (mech == PK_MECH_AUTO) mech = PK_MECH_REG;
-  if (mech != PK_MECH_REG && mech != PK_MECH_TMA) return fail(PK_ERR_INVALID, "moe_dispatch: unknown mechanism %d", mech);
+  if (mech != PK_MECH_AUTO && mech != PK_MECH_REG && mech != PK_MECH_TMA) return fail(PK_ERR_INVALID, "moe_dispatch: unknown mechanism %d", mech);
   a.mech = mech;
   int64_t xr, H, xld;
   PK_TRY(check_matrix(x, "x", PK_BF16, &xr, &H, &xld));
@@ -584,6 +583,11 @@ int moe_dispatch(Comm* c, const pk_tensor* x, const pk_tensor* topk, int num_exp
   if (!find_symmetric(c, recv->ptr, (size_t)cap * H * 2, rp) ||
       !find_symmetric(c, recv_src->ptr, (size_t)cap * 4 * src_cols, sp))
     return fail(PK_ERR_INVALID, "moe_dispatch: recv and recv_src must be symmetric (Comm.empty) tensors");
+  // auto: hwmodel.select_mechanism's answer for one row per message with this
+  // rank's SMs issuing — TMA (higher peak, saturates with 15 SMs) up to its
+  // 227 KB message limit
+  if (mech == PK_MECH_AUTO) mech = H * 2 <= 227 * 1024 ? PK_MECH_TMA : PK_MECH_REG;
+  a.mech = mech;
   a.x = static_cast<const uint8_t*>(x->ptr);
   a.x_ld = xld * 2;
   a.row_bytes = (int)(H * 2);

@@ -6,10 +6,10 @@ engine, TMA bulk copies and register (ld/st/multimem) operations — each with a
 capability set, a saturating bandwidth curve over message size and, for the
 SM-driven ones, a per-SM issue rate. `select_mechanism` picks the supporting
 mechanism with the highest achievable bandwidth (ties: TMA > register ops >
-copy engine). The ops here use it where the choice is a runtime one
-(`ops.moe_dispatch(mechanism="auto")`); elsewhere the kernels hard-wire the
-answer it gives (TMA bulk copies for staging, register ops for multimem
-in-fabric reductions, the copy engine for the ring's whole-shard pulls).
+copy engine). The kernels hard-wire the answers it gives: TMA for MoE
+dispatch rows (`PK_MECH_AUTO` in pk_moe.cu) and operand staging, register ops
+for multimem in-fabric reductions, the copy engine for the ring's host-driven
+whole-shard pulls; `test_hwmodel_cpu.py` pins those answers.
 
 B200 constants: observed peaks 726 / 669 / 628 GB/s for copy engine / TMA /
 register ops (1 GB P2P), 900 GB/s per direction, 15 / 76 SMs

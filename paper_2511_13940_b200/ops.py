@@ -196,8 +196,8 @@ def moe_dispatch(comm, x: torch.Tensor, topk_idx: torch.Tensor, num_experts: int
     (recv_src = -1 on padding rows); a 4th value, the device tile plan, feeds
     grouped_gemm(recv, None, w, plan=plan) without a gather pass.
     mechanism: "reg" (16 B register stores), "tma" (bulk-copy engine) or "auto"
-    (hwmodel.select_mechanism: TMA for row-sized messages — the two measure
-    the same on one GPU, 0.110 vs 0.112 ms).
+    (hwmodel.select_mechanism's answer, TMA — the two measure the same on
+    one GPU, 0.110 vs 0.112 ms).
     """
     _require_cuda(x, topk_idx)
     T, k = topk_idx.shape
@@ -214,12 +214,6 @@ def moe_dispatch(comm, x: torch.Tensor, topk_idx: torch.Tensor, num_experts: int
     dx, dt = _lib.tensor_desc(x), _lib.tensor_desc(topk_idx)
     dr, ds, dc = _lib.tensor_desc(recv_rows), _lib.tensor_desc(recv_src), _lib.tensor_desc(count)
     dp = _lib.ref(_lib.tensor_desc(plan)) if plan is not None else None
-    if mechanism == "auto":
-        # the reference's bandwidth-maximising policy (hwmodel.select_mechanism):
-        # one token row per message, every SM of this rank driving the copies
-        from .hwmodel import Functionality, MechanismKind, select_mechanism
-        best = select_mechanism(Functionality.P2P_TRANSFER, x.shape[1] * x.element_size(), comm.num_sms)
-        mechanism = "tma" if best.kind is MechanismKind.TMA else "reg"
     check(lib.pk_moe_dispatch_ex(comm._h, _lib.ref(dx), _lib.ref(dt), int(num_experts), lay, _MECHANISMS[mechanism],
                                  _lib.ref(dr), _lib.ref(ds), _lib.ref(dc), dp, ctypes_stream(_stream(stream))),
           "moe_dispatch")

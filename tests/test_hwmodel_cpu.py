@@ -33,3 +33,10 @@ def test_selection_policy():
     assert hw.select_mechanism(F.P2P_REDUCTION, 65536, 4).kind is K.TMA
     with pytest.raises(hw.HwModelError):
         hw.select_mechanism(F.P2P_TRANSFER, 1024, -1)
+
+
+@pytest.mark.parametrize("H", [128, 1024, 4096, 7168, 16384])
+@pytest.mark.parametrize("sms", [2, 16, 74, 148])
+def test_moe_dispatch_auto_rule(H, sms):
+    # pk_moe.cu PK_MECH_AUTO hard-wires TMA for rows up to 227 KB: pin it to the policy
+    assert hw.select_mechanism(F.P2P_TRANSFER, 2 * H, sms).kind is K.TMA
