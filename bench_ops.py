@@ -54,10 +54,10 @@ def timeit(fn, iters=10, warm=3, min_ms=50.0):
 
 def ranks(comms, fn):
     """Launch fn(r, comm, stream) for every local-group rank, joined into the current stream."""
-    cur = torch.cuda.current_stream()
     streams = ranks.streams.setdefault(len(comms), [torch.cuda.Stream() for _ in comms])
 
     def run():
+        cur = torch.cuda.current_stream()             # looked up per call: also right under graph capture
         for r, c in enumerate(comms):
             streams[r].wait_stream(cur)
             with torch.cuda.stream(streams[r]):
@@ -145,6 +145,7 @@ def main():
     moe(args, out, c1, T, K, E, H, HE) if want("moe") else None
     local(args, out) if want("local") else None
     ablation(args, out) if want("ablation") else None
+    graphs(args, out) if want("graphs") else None
     c1.destroy()
     out.close()
 
@@ -305,6 +306,38 @@ def ablation(args, out):
             emit(out, **bytes_line(f"all_reduce_ablation_local{world}", 2 * world * n_el * 2, ms, mib=mb,
                                    overheads=name, slowdown=ms / base))
         del ts
+    for c in comms:
+        c.check()
+        c.destroy()
+
+
+def graphs(args, out):
+    """Launch overhead of small all-reduces, eager vs CUDA-graph replay
+    (multi-rank ops count their cross-rank calls on the device once captured):
+    an emulated world 2, `reps` all-reduces per graph."""
+    import time
+    world, reps = 2, 20
+    comms = pk.local_group(world)
+    for kib in ([1024] if args.quick else [64, 256, 1024, 4096, 16384]):
+        n_el = kib * 1024 // 2
+        ts = [c.empty((n_el,)) for c in comms]
+        step = ranks(comms, lambda r, c, s: pk.all_reduce(c, ts[r], stream=s))
+        ms_eager = timeit(step)
+        t0 = time.perf_counter()                 # host cost of issuing one step (both ranks)
+        for _ in range(200):
+            step()
+        host_us = (time.perf_counter() - t0) / 200 * 1e6
+        torch.cuda.synchronize()
+        cap = torch.cuda.Stream()
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph, stream=cap):
+            for _ in range(reps):
+                step()
+        ms_graph = timeit(graph.replay) / reps
+        emit(out, **bytes_line(f"all_reduce_local{world}_graph", 2 * world * n_el * 2, ms_graph, kib=kib,
+                               eager_ms=ms_eager, speedup=ms_eager / ms_graph, host_us_per_step=host_us,
+                               algbw_gbs=n_el * 2 / (ms_graph / 1e3) / 1e9))
+        del graph, ts
     for c in comms:
         c.check()
         c.destroy()

@@ -8,6 +8,7 @@ shape, strides); streams as raw cudaStream_t handles.
 from __future__ import annotations
 
 import ctypes
+import struct
 import os
 import threading
 
@@ -102,16 +103,17 @@ def dtype_code(dtype) -> int:
 
 def tensor_desc(t) -> PkTensor:
     """Describe a torch tensor (device or host) for the C ABI."""
-    if t.dim() > 4:
+    n = t.dim()
+    if n > 4:
         raise ValueError("pk tensors have at most 4 dimensions")
-    d = PkTensor()
-    d.ptr = t.data_ptr()
-    d.dtype = dtype_code(t.dtype)
-    d.ndim = t.dim()
-    for i, (s, st) in enumerate(zip(t.shape, t.stride())):
-        d.shape[i] = s
-        d.strides[i] = st
-    return d
+    pad = _PAD[n]
+    # packed in one go: ctypes' per-field (and array-from-tuple) setters cost
+    # microseconds, which small ops pay on every call
+    return PkTensor.from_buffer_copy(_PACK(t.data_ptr(), dtype_code(t.dtype), n, *t.shape, *pad, *t.stride(), *pad))
+
+
+_PAD = [(0,) * (4 - i) for i in range(5)]
+_PACK = struct.Struct("=Qii4q4q").pack
 
 
 def sched_desc(schedule) -> PkSched | None:

@@ -36,7 +36,7 @@ struct ArArgs {
   uint32_t* done_local;
   uint32_t* done_peer[kMaxRanks];
   uint32_t* err;
-  uint32_t ready_expect, done_expect;
+  CallRef call;                   // cumulative ready / done counts expected from every rank
   uint64_t timeout_ns;
 };
 
@@ -70,7 +70,9 @@ __device__ __forceinline__ void ar_start_barrier(const ArArgs& a) {
       __threadfence_system();
       for (int d = 0; d < a.world; ++d) signal_add(a.ready_peer[d] + a.rank, 1u);
     }
-    for (int d = 0; d < a.world; ++d) wait_geq(a.ready_local + d, a.ready_expect, a.err, a.timeout_ns);
+    call_note(a.call);
+    const uint32_t expect = call_get(a.call, 1);
+    for (int d = 0; d < a.world; ++d) wait_geq(a.ready_local + d, expect, a.err, a.timeout_ns);
   }
   __syncthreads();
 }
@@ -81,7 +83,7 @@ __device__ __forceinline__ void ar_end_barrier(const ArArgs& a) {
     __threadfence_system();
     for (int d = 0; d < a.world; ++d) signal_add(a.done_peer[d] + a.rank, 1u);
     if (blockIdx.x == 0)
-      for (int d = 0; d < a.world; ++d) wait_geq(a.done_local + d, a.done_expect, a.err, a.timeout_ns);
+      for (int d = 0; d < a.world; ++d) wait_geq(a.done_local + d, call_get(a.call, 2), a.err, a.timeout_ns);
   }
 }
 
@@ -384,10 +386,7 @@ int all_reduce(Comm* c, pk_tensor* x, int op, const pk_sched* sched, cudaStream_
   const int threads = 512;
   int blocks = (int)std::min<long long>((long long)sms * 2, std::max<long long>(1, (per + threads - 1) / threads));
   if (c->local_group) blocks = std::min(blocks, sms);   // co-residency of all ranks
-  c->ready_count += 1;
-  c->done_count += (uint32_t)blocks;
-  a.ready_expect = c->ready_count;
-  a.done_expect = c->done_count;
+  PK_TRY(begin_call(c, 0, 1, (uint32_t)blocks, st, &a.call));
   a.timeout_ns = c->timeout_ns;
 
   void* kern;
@@ -517,12 +516,13 @@ int all_reduce_ablate(Comm* c, pk_tensor* x, uint32_t flags, size_t channel_byte
     }
     A.staging = static_cast<uint8_t*>(c->ablate_stage);
   }
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  PK_CUDA(cudaStreamIsCapturing(st, &cs));
+  if (cs != cudaStreamCaptureStatusNone)   // the handshake rounds are host-counted
+    return fail(PK_ERR_INVALID, "all_reduce_ablate: not capturable into a CUDA graph");
   c->ablate_calls += 1;
   A.calls = c->ablate_calls;
-  c->ready_count += 1;
-  c->done_count += (uint32_t)blocks;
-  a.ready_expect = c->ready_count;
-  a.done_expect = c->done_count;
+  PK_TRY(begin_call(c, 0, 1, (uint32_t)blocks, st, &a.call));
   a.timeout_ns = c->timeout_ns;
   void* kern = x->dtype == PK_BF16 ? ablate_kernel_for<PK_BF16>((int)flags) : ablate_kernel_for<PK_F32>((int)flags);
   void* params[] = {&A};

@@ -63,10 +63,10 @@ struct AttnArgs {
   int B, S_q, S_kv, H;
   float scale_log2;              // softmax_scale * log2(e)
   // single-launch ring: KV of ring step s lives at batch coordinate s*B + b of
-  // the K/V maps; steps >= 1 are usable once step_flags[s] >= flag_epoch
+  // the K/V maps; steps >= 1 are usable once step_flags[s] >= the call's epoch
   int blocks_per_step;           // 128-key blocks per ring step (S/n / 128)
   const uint32_t* step_flags;    // null: all KV resident
-  uint32_t flag_epoch;
+  CallRef call;                  // this call's epoch (index 0)
   uint32_t* err;
   uint64_t timeout_ns;
   uint16_t* o;                   // [B, S_q, H, D] bf16 output
@@ -295,9 +295,10 @@ __global__ void __launch_bounds__(AT_THREADS, 1) attn_fwd_kernel(const __grid_co
       // key block j = ring step j / bps, block j % bps of that step's shard
       const int bps = a.blocks_per_step;
       int ready_steps = 1;                               // step 0 (own shard) is always resident
+      const uint32_t flag_epoch = a.step_flags != nullptr ? call_get(a.call, 0) : 0u;
       auto step_ready = [&](int step) {
         while (a.step_flags != nullptr && ready_steps <= step) {
-          wait_geq(a.step_flags + ready_steps, a.flag_epoch, a.err, a.timeout_ns);
+          wait_geq(a.step_flags + ready_steps, flag_epoch, a.err, a.timeout_ns);
           fence_async_global();
           ++ready_steps;
         }
@@ -695,9 +696,10 @@ __global__ void __launch_bounds__(AT_THREADS, 1) attn2_fwd_kernel(const __grid_c
     if (lane == 0) {
       const int bps = a.blocks_per_step;
       int ready_steps = 1;
+      const uint32_t flag_epoch = a.step_flags != nullptr ? call_get(a.call, 0) : 0u;
       auto step_ready = [&](int step) {
         while (a.step_flags != nullptr && ready_steps <= step) {
-          wait_geq(a.step_flags + ready_steps, a.flag_epoch, a.err, a.timeout_ns);
+          wait_geq(a.step_flags + ready_steps, flag_epoch, a.err, a.timeout_ns);
           fence_async_global();
           ++ready_steps;
         }
@@ -907,11 +909,15 @@ __global__ void sync_signal_kernel(uint32_t* p0, uint32_t* p1, uint32_t* p2, uin
   __threadfence_system();
   for (int d = 0; d < n; ++d) signal_add(ps[d], 1u);
 }
-__global__ void flag_set_kernel(uint32_t* flag, uint32_t value) {
+__global__ void flag_set_kernel(uint32_t* flag, const CallRef call) {
   __threadfence_system();
-  asm volatile("st.release.gpu.global.u32 [%0], %1;" :: "l"(flag), "r"(value) : "memory");
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" :: "l"(flag), "r"(call_get(call, 0)) : "memory");
 }
-__global__ void sync_wait_kernel(const uint32_t* counters, int n, uint32_t expected, uint32_t* err, uint64_t timeout) {
+// wait until every rank's counter reaches the call's count `which` (1 ready, 2 done)
+__global__ void sync_wait_kernel(const uint32_t* counters, int n, const CallRef call, int which, uint32_t* err,
+                                 uint64_t timeout) {
+  call_note(call);
+  const uint32_t expected = call_get(call, which);
   for (int d = 0; d < n; ++d) wait_geq(counters + d, expected, err, timeout);
 }
 
@@ -932,9 +938,10 @@ static int signal_all(Comm* c, int which_off, cudaStream_t st) {
   PK_CUDA(cudaGetLastError());
   return PK_OK;
 }
-static int wait_all(Comm* c, int which_off, uint32_t expected, cudaStream_t st) {
+static int wait_all(Comm* c, int which_off, const CallRef& call, cudaStream_t st) {
   uint32_t* local = static_cast<uint32_t*>(c->sync->local);
-  sync_wait_kernel<<<1, 1, 0, st>>>(local + which_off, c->world, expected, local + kSyncErr, c->timeout_ns);
+  sync_wait_kernel<<<1, 1, 0, st>>>(local + which_off, c->world, call, which_off == kSyncReady ? 1 : 2,
+                                    local + kSyncErr, c->timeout_ns);
   PK_CUDA(cudaGetLastError());
   return PK_OK;
 }
@@ -1105,25 +1112,23 @@ int ring_attn_fwd(Comm* c, const pk_tensor* q, const pk_tensor* k, const pk_tens
   for (auto& x : evs.e) PK_CUDA(cudaEventCreateWithFlags(&x, cudaEventDisableTiming));
   cudaEvent_t ev_start = evs.e[0], ev_side = evs.e[1], ev_copies = evs.e[2];
   uint32_t* flags = static_cast<uint32_t*>(c->sync->local) + kSyncFlags;    // per-step "staged" flags
-  c->epoch += 1;
+  CallRef call;
+  PK_TRY(begin_call(c, 1, 1, 1, st, &call));
   // 1. my shard is ready -> tell everyone; the side stream pulls every peer shard
   //    with the copy engine in ring order and flags each step as it lands.
-  c->ready_count += 1;
-  const uint32_t ready_expect = c->ready_count;
   PK_TRY(signal_all(c, kSyncReady, st));
   PK_CUDA(cudaEventRecord(ev_start, st));
   PK_CUDA(cudaStreamWaitEvent(side, ev_start, 0));
-  PK_TRY(wait_all(c, kSyncReady, ready_expect, side));
+  PK_TRY(wait_all(c, kSyncReady, call, side));
   for (int s = 1; s < n; ++s) {
     const int src = ((c->rank - s) % n + n) % n;                             // workloads.py:666-681
     PK_CUDA(cudaMemcpyAsync(kst + (size_t)s * shard, kp[src], shard, cudaMemcpyDeviceToDevice, side));
     PK_CUDA(cudaMemcpyAsync(vst + (size_t)s * shard, vp[src], shard, cudaMemcpyDeviceToDevice, side));
-    flag_set_kernel<<<1, 1, 0, side>>>(flags + s, c->epoch);
+    flag_set_kernel<<<1, 1, 0, side>>>(flags + s, call);
     PK_CUDA(cudaGetLastError());
   }
   PK_CUDA(cudaEventRecord(ev_copies, side));
   // 2. done reading every peer's shard (side) -> signal; join the side stream.
-  c->done_count += 1;
   PK_TRY(signal_all(c, kSyncDone, side));
   PK_CUDA(cudaEventRecord(ev_side, side));
   // 3. one attention launch over all n*S/n keys; the loader waits step flags.
@@ -1133,7 +1138,7 @@ int ring_attn_fwd(Comm* c, const pk_tensor* q, const pk_tensor* k, const pk_tens
   a.S_kv = (int)(n * S);
   a.blocks_per_step = (int)(S / AT_BN);
   a.step_flags = flags;
-  a.flag_epoch = c->epoch;
+  a.call = call;
   if (c->local_group) {
     // Emulated ranks share this GPU's SMs: CTAs spinning on a step flag could
     // hold the SMs the flag's producer chain needs (another rank's previous
@@ -1146,7 +1151,7 @@ int ring_attn_fwd(Comm* c, const pk_tensor* q, const pk_tensor* k, const pk_tens
   PK_TRY(launch_attn(c->attn, c->num_sms, a, st));
   // 4. wait until every peer is done with my shard before the caller may reuse it.
   PK_CUDA(cudaStreamWaitEvent(st, ev_side, 0));
-  PK_TRY(wait_all(c, kSyncDone, c->done_count, st));
+  PK_TRY(wait_all(c, kSyncDone, call, st));
   return PK_OK;
 }
 

@@ -35,7 +35,7 @@ struct CollArgs {
   uint32_t* done_local;
   uint32_t* done_peer[kMaxRanks];
   uint32_t* err;
-  uint32_t ready_expect, done_expect;
+  CallRef call;                      // cumulative ready / done counts expected from every rank
   uint64_t timeout_ns;
 };
 
@@ -51,7 +51,9 @@ __global__ void __launch_bounds__(1024) coll_kernel(const __grid_constant__ Coll
       __threadfence_system();
       for (int d = 0; d < a.world; ++d) signal_add(a.ready_peer[d] + a.rank, 1u);
     }
-    for (int d = 0; d < a.world; ++d) wait_geq(a.ready_local + d, a.ready_expect, a.err, a.timeout_ns);
+    call_note(a.call);
+    const uint32_t expect = call_get(a.call, 1);
+    for (int d = 0; d < a.world; ++d) wait_geq(a.ready_local + d, expect, a.err, a.timeout_ns);
   }
   __syncthreads();
   const int lane = threadIdx.x & 31;
@@ -120,7 +122,7 @@ __global__ void __launch_bounds__(1024) coll_kernel(const __grid_constant__ Coll
     __threadfence_system();
     for (int d = 0; d < a.world; ++d) signal_add(a.done_peer[d] + a.rank, 1u);
     if (blockIdx.x == 0)
-      for (int d = 0; d < a.world; ++d) wait_geq(a.done_local + d, a.done_expect, a.err, a.timeout_ns);
+      for (int d = 0; d < a.world; ++d) wait_geq(a.done_local + d, call_get(a.call, 2), a.err, a.timeout_ns);
   }
 }
 
@@ -171,10 +173,7 @@ static int run_coll(Comm* c, const pk_tensor* x, CollArgs& a, long long units, c
   }
   int blocks = (int)std::min<long long>((long long)c->num_sms, std::max<long long>(1, (units + 31) / 32));
   if (c->local_group && c->world > 1) blocks = std::min(blocks, c->num_sms);   // co-residency of all ranks' kernels
-  c->ready_count += 1;
-  c->done_count += (uint32_t)blocks;
-  a.ready_expect = c->ready_count;
-  a.done_expect = c->done_count;
+  PK_TRY(begin_call(c, 0, 1, (uint32_t)blocks, st, &a.call));
   a.timeout_ns = c->timeout_ns;
   coll_kernel<<<blocks, 1024, 0, st>>>(a);   // 32 warps x 4 loads in flight per lane per SM
   PK_CUDA(cudaGetLastError());

@@ -532,6 +532,41 @@ int preload_attn();
 int preload_grouped();
 int preload_coll();
 
+// Device call counting (CallRef): advance the base counters and fill this
+// call's slot; stream order puts it after the previous call's kernels and
+// before this call's.
+__global__ void call_arm_kernel(uint32_t* base, uint32_t* slot, uint32_t de, uint32_t dr, uint32_t dd) {
+  base[0] += de;
+  base[1] += dr;
+  base[2] += dd;
+  slot[0] = base[0];
+  slot[1] = base[1];
+  slot[2] = base[2];
+}
+
+int begin_call(Comm* c, uint32_t de, uint32_t dr, uint32_t dd, cudaStream_t st, CallRef* out) {
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  PK_CUDA(cudaStreamIsCapturing(st, &cs));
+  if (cs != cudaStreamCaptureStatusNone) c->device_counts = true;
+  c->epoch += de;
+  c->ready_count += dr;
+  c->done_count += dd;
+  uint32_t* base = static_cast<uint32_t*>(c->sync->local) + kSyncCall;
+  *out = CallRef{};
+  if (!c->device_counts) {
+    out->mirror = base;
+    out->v[0] = c->epoch;
+    out->v[1] = c->ready_count;
+    out->v[2] = c->done_count;
+    return PK_OK;
+  }
+  uint32_t* slot = base + 4 + 4 * (c->call_seq++ % kSyncCallSlots);
+  call_arm_kernel<<<1, 1, 0, st>>>(base, slot, de, dr, dd);
+  PK_CUDA(cudaGetLastError());
+  out->dev = slot;
+  return PK_OK;
+}
+
 // Load every kernel image up front. With lazy module loading the first launch
 // of a kernel can synchronise the context; in a local group that launch may
 // come after another rank's kernel is already spinning in wait() for this
@@ -546,6 +581,8 @@ static int preload_kernels() {
     if (s == PK_OK) s = preload_attn();
     if (s == PK_OK) s = preload_grouped();
     if (s == PK_OK) s = preload_coll();
+    cudaFuncAttributes fa;
+    if (s == PK_OK && cudaFuncGetAttributes(&fa, call_arm_kernel) != cudaSuccess) s = fail(PK_ERR_CUDA, "preload call_arm_kernel");
     status = s;
   });
   return status;

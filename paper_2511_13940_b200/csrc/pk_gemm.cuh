@@ -45,9 +45,8 @@ struct SyncArgs {
   uint32_t* done_peer[kMaxRanksDev];
   uint32_t* flags;                        // [num_m_tiles] local per-m-tile "rows landed" flags (inter-SM AG)
   uint32_t* err;                          // timeout flag
-  uint32_t epoch;                         // this call's epoch (>= 1): value published in flags
-  uint32_t ready_expect;                  // cumulative ready count expected from every rank
-  uint32_t done_expect;                   // cumulative done count expected from every rank
+  CallRef call;                           // this call's epoch (>= 1, published in flags) and the
+                                          // cumulative ready / done counts expected from every rank
   uint64_t timeout_ns;
 };
 
@@ -172,6 +171,7 @@ lcsc_gemm_kernel(const __grid_constant__ GemmArgs args) {
   uint64_t* tile_empty = tile_full + kTileRing;       // [kTileRing]
   int32_t* tile_ring = reinterpret_cast<int32_t*>(tile_empty + kTileRing);   // [kTileRing]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tile_ring + kTileRing);
+  uint32_t* s_call = tmem_slot + 1;                   // [3] this call's epoch / ready / done counts
 
   const uint32_t warp = warp_id_sync();
   const uint32_t lane = lane_id();
@@ -202,6 +202,10 @@ lcsc_gemm_kernel(const __grid_constant__ GemmArgs args) {
       mbar_init(&tile_empty[i], 1 + Cfg::EPI_WARPS * CG + (CG - 1));
     }
     fence_mbar_init();
+  }
+  if (warp == 3 && lane == 0) {
+    for (int i = 0; i < 3; ++i) s_call[i] = call_get(args.sync.call, i);
+    call_note(args.sync.call);
   }
   if (warp == 2 && !is_comm) tmem_alloc<Cfg::TMEM_COLS, CG>(tmem_slot);
   if (warp == 1 && lane == 0) {
@@ -408,7 +412,7 @@ lcsc_gemm_kernel(const __grid_constant__ GemmArgs args) {
       // make sure a shard's owner published it before its first piece is read
       auto ensure_ready = [&](int src) -> bool {
         if (src == args.rank || args.sync.ready_local == nullptr || ((ready_mask >> src) & 1)) return true;
-        if (!wait_geq(args.sync.ready_local + src, args.sync.ready_expect, args.sync.err, args.sync.timeout_ns)) return false;
+        if (!wait_geq(args.sync.ready_local + src, s_call[1], args.sync.err, args.sync.timeout_ns)) return false;
         ready_mask |= 1u << src;
         return true;
       };
@@ -437,7 +441,7 @@ lcsc_gemm_kernel(const __grid_constant__ GemmArgs args) {
             if (atomicAdd(piece_count + mt, 1u) == (uint32_t)parts - 1) {
               piece_count[mt] = 0;                     // every share landed: re-arm, then publish
               __threadfence();
-              asm volatile("st.release.gpu.global.u32 [%0], %1;" :: "l"(args.sync.flags + mt), "r"(args.sync.epoch) : "memory");
+              asm volatile("st.release.gpu.global.u32 [%0], %1;" :: "l"(args.sync.flags + mt), "r"(s_call[0]) : "memory");
             }
           }
           ++counted;
@@ -494,11 +498,11 @@ lcsc_gemm_kernel(const __grid_constant__ GemmArgs args) {
       const int a_row = args.a_base[src] + m_row - src * args.a_rows_per_src;
       const int b_row = (args.tile_group ? args.tile_group[mt] * args.N : 0) + nt * BN + (int)cta_rank * Cfg::B_ROWS;
       if (args.a_wait_flag[src]) {
-        wait_geq(args.sync.flags + mt, args.sync.epoch, args.sync.err, args.sync.timeout_ns);
+        wait_geq(args.sync.flags + mt, s_call[0], args.sync.err, args.sync.timeout_ns);
         fence_async_global();
       }
       if (args.sync_ready_before_load && !((peers_ready >> src) & 1)) {
-        wait_geq(args.sync.ready_local + src, args.sync.ready_expect, args.sync.err, args.sync.timeout_ns);
+        wait_geq(args.sync.ready_local + src, s_call[1], args.sync.err, args.sync.timeout_ns);
         fence_async_global();
         peers_ready |= 1u << src;
       }
@@ -583,7 +587,7 @@ lcsc_gemm_kernel(const __grid_constant__ GemmArgs args) {
       const int dst = (args.c_ndst > 1) ? row0 / args.c_rows_per_dst : 0;
       const int c_row = row0 - dst * args.c_rows_per_dst;
       if (EPI == EPI_REDUCE_ADD && args.sync_ready_before_store && !((owners_ready >> dst) & 1)) {
-        if (lane == 0) wait_geq(args.sync.ready_local + dst, args.sync.ready_expect, args.sync.err, args.sync.timeout_ns);
+        if (lane == 0) wait_geq(args.sync.ready_local + dst, s_call[1], args.sync.err, args.sync.timeout_ns);
         __syncwarp();
         owners_ready |= 1u << dst;
       }
@@ -731,7 +735,7 @@ lcsc_gemm_kernel(const __grid_constant__ GemmArgs args) {
   // rank's buffers, so the caller may reuse them once the kernel returns.
   if (args.sync_done_wait && blockIdx.x == 0 && threadIdx.x == 0) {
     for (int s = 0; s < args.world; ++s)
-      wait_geq(args.sync.done_local + s, args.sync.done_expect, args.sync.err, args.sync.timeout_ns);
+      wait_geq(args.sync.done_local + s, s_call[2], args.sync.err, args.sync.timeout_ns);
   }
 }
 

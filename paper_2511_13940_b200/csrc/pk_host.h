@@ -117,6 +117,18 @@ struct AttnScratch {
   size_t count_n = 0;
 };
 
+// One fused call's cross-rank counts {epoch, ready, done}. Host-counted
+// communicators pass them by value (and the kernels keep the device copy of
+// the counters current in `mirror`); once a communicator is used under CUDA
+// graph capture it counts on the device: an arm kernel advances the base and
+// fills a call slot that the call's kernels read (`dev`), so every replay of a
+// captured call sees fresh counts.
+struct CallRef {
+  const uint32_t* dev = nullptr;
+  uint32_t* mirror = nullptr;
+  uint32_t v[3] = {0, 0, 0};
+};
+
 struct Comm {
   int rank = 0, world = 1, device = 0;
   bool local_group = false;          // single-process emulated peers
@@ -146,6 +158,8 @@ struct Comm {
   void* ablate_stage = nullptr;      // all_reduce_ablate staging channels (local)
   size_t ablate_stage_bytes = 0;
   uint32_t ablate_calls = 0;         // handshake round counter (req/ack counters only grow)
+  bool device_counts = false;        // sticky: set by the first call made under stream capture
+  uint32_t call_seq = 0;             // device-counted calls issued (call slot ring index)
 };
 
 // If [ptr, ptr+bytes) lies inside one of c's user PGLs, fill peers[] with the
@@ -153,7 +167,16 @@ struct Comm {
 bool find_symmetric(Comm* c, const void* ptr, size_t bytes, void** peers);
 
 // Word offsets inside the per-comm sync PGL.
-enum { kSyncReady = 0, kSyncDone = 8, kSyncErr = 16, kSyncFlags = 32, kSyncArTiles = 32 + 65536, kSyncBytes = 1 << 20 };
+// kSyncCall: the device call counters {epoch, ready, done} and 8 call slots
+// of 4 words (begin_call).
+enum { kSyncReady = 0, kSyncDone = 8, kSyncErr = 16, kSyncFlags = 32, kSyncArTiles = 32 + 65536,
+       kSyncCall = (1 << 18) - 64, kSyncCallSlots = 8, kSyncBytes = 1 << 20 };
+
+// Advance c's cross-rank counts for one fused call (epoch, ready and done
+// increments) and describe them for the call's kernels (see CallRef). Call it
+// after every check that can fail and right before the launches, on the
+// call's stream.
+int begin_call(Comm* c, uint32_t d_epoch, uint32_t d_ready, uint32_t d_done, cudaStream_t st, CallRef* out);
 
 // Exchange `len` bytes from every rank (allgather) — multi-process through
 // the Unix-socket rendezvous; local groups copy in-process.

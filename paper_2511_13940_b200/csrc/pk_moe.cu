@@ -44,7 +44,7 @@ struct MoeSync {
   uint32_t* done_local;
   uint32_t* done_peer[kMaxRanks];
   uint32_t* err;
-  uint32_t ready_expect, done_expect;
+  CallRef call;                   // cumulative ready / done counts expected from every rank
   uint64_t timeout_ns;
 };
 
@@ -85,8 +85,10 @@ __device__ __forceinline__ void moe_signal_all(const MoeSync& s, int n, int rank
 }
 __device__ __forceinline__ bool moe_wait_all(const MoeSync& s, int n, bool done) {
   bool ok = true;
+  call_note(s.call);
+  const uint32_t expect = call_get(s.call, done ? 2 : 1);
   for (int d = 0; d < n; ++d)
-    ok &= wait_geq((done ? s.done_local : s.ready_local) + d, done ? s.done_expect : s.ready_expect, s.err, s.timeout_ns);
+    ok &= wait_geq((done ? s.done_local : s.ready_local) + d, expect, s.err, s.timeout_ns);
   return ok;
 }
 
@@ -488,7 +490,7 @@ int preload_moe() {
   return PK_OK;
 }
 
-static void fill_moe_sync(Comm* c, MoeSync& s) {
+static void fill_moe_sync(Comm* c, MoeSync& s, const CallRef& call) {
   uint32_t* local = static_cast<uint32_t*>(c->sync->local);
   s.ready_local = local + kSyncReady;
   s.done_local = local + kSyncDone;
@@ -498,8 +500,7 @@ static void fill_moe_sync(Comm* c, MoeSync& s) {
     s.ready_peer[r] = pr + kSyncReady;
     s.done_peer[r] = pr + kSyncDone;
   }
-  s.ready_expect = c->ready_count;
-  s.done_expect = c->done_count;
+  s.call = call;
   s.timeout_ns = c->timeout_ns;
 }
 
@@ -613,9 +614,9 @@ int moe_dispatch(Comm* c, const pk_tensor* x, const pk_tensor* topk, int num_exp
     a.tpc = (T + max_grid - 1) / max_grid;
     a.grid = std::max(1, (T + a.tpc - 1) / a.tpc);
   }
-  c->ready_count += 1;
-  c->done_count += (uint32_t)a.grid;
-  fill_moe_sync(c, a.sync);
+  CallRef call;
+  PK_TRY(begin_call(c, 0, 1, (uint32_t)a.grid, st, &call));
+  fill_moe_sync(c, a.sync, call);
   void* params[] = {&a};
   PK_CUDA(cudaMemsetAsync(a.count_done, 0, sizeof(uint32_t), st));
   PK_CUDA(cudaLaunchKernel((void*)moe_dispatch_kernel, dim3(a.grid), dim3(kDispatchThreads), params, smem, st));
@@ -650,11 +651,11 @@ int moe_combine(Comm* c, const pk_tensor* y, const pk_tensor* topk, const pk_ten
   a.out = static_cast<uint8_t*>(out->ptr);
   a.out_ld = old * 2;
   a.cap = cap;
-  c->ready_count += 1;
   int blocks = (int)std::min<long long>(((long long)T + kCombineThreads / 32 - 1) / (kCombineThreads / 32), c->num_sms);
   blocks = std::max(blocks, 1);
-  c->done_count += (uint32_t)blocks;
-  fill_moe_sync(c, a.sync);
+  CallRef call;
+  PK_TRY(begin_call(c, 0, 1, (uint32_t)blocks, st, &call));
+  fill_moe_sync(c, a.sync, call);
   void* params[] = {&a};
   const void* kern = K <= 8 ? (const void*)moe_combine_kernel<8> : (const void*)moe_combine_kernel<16>;
   PK_CUDA(cudaLaunchKernel(kern, dim3(blocks), dim3(kCombineThreads), params, 0, st));

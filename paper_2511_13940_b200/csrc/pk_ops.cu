@@ -193,7 +193,7 @@ int gemm_local(const pk_tensor* A, const pk_tensor* B, pk_tensor* C, const pk_sc
 }
 
 // Fill the cross-rank sync block of one fused call.
-static void fill_sync(Comm* c, SyncArgs& sy) {
+static void fill_sync(Comm* c, SyncArgs& sy, const CallRef& call) {
   uint32_t* local = static_cast<uint32_t*>(c->sync->local);
   sy.ready_local = local + kSyncReady;
   sy.done_local = local + kSyncDone;
@@ -204,9 +204,7 @@ static void fill_sync(Comm* c, SyncArgs& sy) {
     sy.ready_peer[r] = peer + kSyncReady;
     sy.done_peer[r] = peer + kSyncDone;
   }
-  sy.epoch = c->epoch;
-  sy.ready_expect = c->ready_count;
-  sy.done_expect = c->done_count;
+  sy.call = call;
   sy.timeout_ns = c->timeout_ns;
 }
 
@@ -308,10 +306,9 @@ int ag_gemm(Comm* c, const pk_tensor* A, const pk_tensor* B, pk_tensor* C, pk_te
   args.num_compute_clusters = compute_clusters;
   args.sync_done_signal = 1;
   args.sync_done_wait = 1;
-  c->epoch += 1;
-  c->ready_count += 1;
-  c->done_count += (uint32_t)(compute_clusters * cg * 4 * v.am);
-  fill_sync(c, args.sync);
+  CallRef call;
+  PK_TRY(begin_call(c, 1, 1, (uint32_t)(compute_clusters * cg * 4 * v.am), st, &call));
+  fill_sync(c, args.sync, call);
   PK_TRY(launch_gemm_variant(v, EPI_STORE, args, (compute_clusters + comm_clusters) * cg, st));
   if (AG && mode == PK_INTRA_SM) {
     // intra-SM never materialises the gathered rows; copy them on demand
@@ -374,9 +371,9 @@ static int gemm_rs_inter(Comm* c, const pk_tensor* A, const pk_tensor* B, pk_ten
   args.rs_ld = ldO * 2;
   args.ar_expect = (uint32_t)(n * 4 * 2);                          // every rank's 4 epilogue warps x 2 CTAs
   args.sync_done_wait = 1;
-  c->epoch += 1;
-  c->done_count += (uint32_t)(comm_clusters * 2);
-  fill_sync(c, args.sync);
+  CallRef call;
+  PK_TRY(begin_call(c, 1, 0, (uint32_t)(comm_clusters * 2), st, &call));
+  fill_sync(c, args.sync, call);
   args.sync.ready_local = nullptr;
   return launch_gemm_variant(v, EPI_STORE, args, (compute_clusters + comm_clusters) * 2, st);
 }
@@ -430,10 +427,9 @@ int gemm_rs(Comm* c, const pk_tensor* A, const pk_tensor* B, pk_tensor* O, const
   args.sync_ready_before_store = 1;
   args.sync_done_signal = 1;
   args.sync_done_wait = 1;
-  c->epoch += 1;
-  c->ready_count += 1;
-  c->done_count += (uint32_t)(compute_clusters * cg * 4 * v.am);
-  fill_sync(c, args.sync);
+  CallRef call;
+  PK_TRY(begin_call(c, 1, 1, (uint32_t)(compute_clusters * cg * 4 * v.am), st, &call));
+  fill_sync(c, args.sync, call);
   PK_TRY(launch_gemm_variant(v, EPI_REDUCE_ADD, args, compute_clusters * cg, st));
   if (staged)
     PK_CUDA(cudaMemcpy2DAsync(O->ptr, ldO * 2, dst[c->rank], N * 2, N * 2, m_own, cudaMemcpyDeviceToDevice, st));
@@ -507,9 +503,9 @@ int gemm_ar(Comm* c, const pk_tensor* A, const pk_tensor* B, pk_tensor* O, const
   args.ar_ld = N * 2;
   args.ar_expect = (uint32_t)(n * 4 * 2);                          // every rank's 4 epilogue warps x 2 CTAs per tile
   args.sync_done_wait = 1;                                         // block 0 waits for every rank's comm CTAs
-  c->epoch += 1;
-  c->done_count += (uint32_t)(comm_clusters * 2);
-  fill_sync(c, args.sync);
+  CallRef call;
+  PK_TRY(begin_call(c, 1, 0, (uint32_t)(comm_clusters * 2), st, &call));
+  fill_sync(c, args.sync, call);
   args.sync.ready_local = nullptr;                                 // no ready handshake: tiles are flagged
   PK_TRY(launch_gemm_variant(v, EPI_STORE, args, (compute_clusters + comm_clusters) * 2, st));
   if (staged)

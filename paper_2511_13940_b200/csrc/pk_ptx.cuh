@@ -16,6 +16,7 @@
 #include <cstdint>
 #include <cuda.h>
 #include <cuda_bf16.h>
+#include "pk_host.h"
 
 #define PK_DEV __device__ __forceinline__
 
@@ -313,6 +314,18 @@ PK_DEV uint32_t ld_relaxed_sys(const uint32_t* p) {
   asm volatile("ld.relaxed.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
+// A fused call's counts (CallRef, pk_host.h): i = 0 epoch, 1 ready, 2 done.
+PK_DEV uint32_t call_get(const CallRef& c, int i) { return c.dev ? ld_relaxed_sys(c.dev + i) : c.v[i]; }
+// Host-counted calls keep the communicator's device counters current, so a
+// later switch to device counting continues from them. Call from one thread.
+PK_DEV void call_note(const CallRef& c) {
+  if (c.mirror != nullptr && blockIdx.x == 0) {
+    c.mirror[0] = c.v[0];
+    c.mirror[1] = c.v[1];
+    c.mirror[2] = c.v[2];
+  }
+}
+
 // wait(): spin until *p >= expected (wrap-safe compare). Returns false on
 // timeout and raises *err (the device analogue of overlapsim's DeadlockError,
 // engine.py:35-40) instead of hanging the GPU.
