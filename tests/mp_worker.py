@@ -84,6 +84,20 @@ def main():
     torch.cuda.synchronize()
     comm.check()
     assert np.array_equal(comb.float().cpu().numpy(), Kk * toks[rank]), "moe_combine"
+    # CUDA graph: the communicator switches to device-side call counting at
+    # capture; replays and the eager call after them must pair up across processes
+    side = torch.cuda.Stream()
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph, stream=side):
+        pk.all_reduce(comm, x, stream=side)
+    for it in range(3):
+        X = [rng.integers(-8, 9, size=4096).astype(np.float32) for _ in range(world)]
+        x.copy_(torch.from_numpy(X[rank]))
+        torch.cuda.synchronize()
+        graph.replay() if it < 2 else pk.all_reduce(comm, x)
+        torch.cuda.synchronize()
+        comm.check()
+        assert np.array_equal(x.cpu().numpy(), oracle.all_reduce(X)[rank]), f"all_reduce graph {it}"
     comm.destroy()
     dist.barrier()
     dist.destroy_process_group()
