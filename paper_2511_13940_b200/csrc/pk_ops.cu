@@ -58,15 +58,17 @@ static int launch_lcsc(const GemmArgs& args_in, int grid_ctas, cudaStream_t st) 
 }
 
 // Kernel variants: (cta_group, A row blocks per CTA) x epilogue.
-struct Variant { int cg, am; };
+struct Variant { int cg, am, bn = 256; };
 
 int launch_gemm_variant(Variant v, int epi, const GemmArgs& args, int grid_ctas, cudaStream_t st) {
-#define PK_V(CG, AM, E) if (v.cg == CG && v.am == AM && epi == E) return launch_lcsc<CG, 256, AM, E>(args, grid_ctas, st);
+#define PK_V(CG, AM, E) if (v.cg == CG && v.am == AM && v.bn == 256 && epi == E) return launch_lcsc<CG, 256, AM, E>(args, grid_ctas, st);
   PK_V(2, 2, EPI_STORE) PK_V(2, 2, EPI_REDUCE_ADD) PK_V(2, 1, EPI_DIRECT)
   PK_V(2, 1, EPI_STORE) PK_V(2, 1, EPI_REDUCE_ADD)
   PK_V(1, 1, EPI_STORE) PK_V(1, 1, EPI_REDUCE_ADD)
 #undef PK_V
-  return fail(PK_ERR_INVALID, "no GEMM variant for cta_group=%d am=%d epi=%d", v.cg, v.am, epi);
+  if (v.cg == 1 && v.am == 1 && v.bn == 128 && epi == EPI_STORE) return launch_lcsc<1, 128, 1, EPI_STORE>(args, grid_ctas, st);
+  if (v.cg == 2 && v.am == 1 && v.bn == 128 && epi == EPI_STORE) return launch_lcsc<2, 128, 1, EPI_STORE>(args, grid_ctas, st);
+  return fail(PK_ERR_INVALID, "no GEMM variant for cta_group=%d am=%d bn=%d epi=%d", v.cg, v.am, v.bn, epi);
 }
 
 int launch_gemm_planned(const GemmArgs& args, int grid_ctas, cudaStream_t st) {
@@ -84,6 +86,8 @@ int preload_gemm() {
   PK_L(2, 2, EPI_STORE) PK_L(2, 2, EPI_REDUCE_ADD) PK_L(2, 1, EPI_DIRECT) PK_L(2, 1, EPI_STORE) PK_L(2, 1, EPI_REDUCE_ADD)
   PK_L(1, 1, EPI_STORE) PK_L(1, 1, EPI_REDUCE_ADD) PK_L(2, 1, EPI_SCATTER)
 #undef PK_L
+  PK_CUDA(cudaFuncGetAttributes(&fa, lcsc_gemm_kernel<1, 128, 1, EPI_STORE>));
+  PK_CUDA(cudaFuncGetAttributes(&fa, lcsc_gemm_kernel<2, 128, 1, EPI_STORE>));
   return PK_OK;
 }
 
@@ -104,22 +108,39 @@ static double wave_eff(int64_t tiles, int64_t clusters) {
 }
 
 static Variant pick_variant(int64_t rows_per_part, int64_t K, const pk_sched* sched, bool reduce = false,
-                            int64_t M = 0, int64_t N = 0, int64_t clusters = 0) {
+                            int64_t M = 0, int64_t N = 0, int64_t clusters = 0, bool allow_narrow = false) {
   int force_am = 0;
   if (const char* e = getenv("PK_GEMM_AM")) force_am = atoi(e);
   if (sched && sched->stages < 0) force_am = -sched->stages;     // test hook: stages = -am
   (void)reduce;
   (void)K;
+  Variant v{1, 1};
   if (rows_per_part % 512 == 0 && force_am != 1) {
+    v = {2, 2};
     if (force_am != 2 && M > 0 && N > 0 && clusters > 0) {
       const double e2 = wave_eff((M / 512) * (N / 256), clusters);
       const double e1 = wave_eff((M / 256) * (N / 256), clusters);
-      if (e1 * 0.95 > e2) return {2, 1};
+      if (e1 * 0.95 > e2) v = {2, 1};
     }
-    return {2, 2};
+  } else if (rows_per_part % 256 == 0) {
+    v = {2, 1};
   }
-  if (rows_per_part % 256 == 0) return {2, 1};
-  return {1, 1};
+  // Too few output tiles to fill the SMs (e.g. an 8-way AG-GEMM's 4096 x 512
+  // slab: 32 pair tiles for 74 pairs): 128-column tiles instead — 256 x 128
+  // per CTA pair (each SM loads half of B, as in the wide pair tiles), or
+  // 128 x 128 per CTA when the rows only split by 128. Estimated time =
+  // waves x per-SM work of one tile (128 x 256 x K = 1; the narrow tiles run
+  // ~15 % less efficiently per flop).
+  if (allow_narrow && force_am == 0 && M > 0 && N > 0 && clusters > 0 && rows_per_part % 128 == 0 && N % 128 == 0) {
+    auto waves = [](int64_t tiles, int64_t slots) { return (double)((tiles + slots - 1) / slots); };
+    const double t_cur = waves((M / (128 * v.am * v.cg)) * (N / 256), v.cg == 2 ? clusters : 2 * clusters) *
+                         (v.cg == 2 ? v.am : 0.5);
+    const bool pair = rows_per_part % 256 == 0;
+    const double t_narrow = (pair ? waves((M / 256) * (N / 128), clusters) : waves((M / 128) * (N / 128), 2 * clusters)) *
+                            0.5 * 1.15;
+    if (t_narrow < 0.85 * t_cur) v = pair ? Variant{2, 1, 128} : Variant{1, 1, 128};
+  }
+  return v;
 }
 
 static int default_sms(int device, const pk_sched* sched) {
@@ -133,8 +154,8 @@ static int tmap_a(CUtensorMap* m, const void* p, int64_t rows, int64_t k, int64_
   return make_tmap_2d(m, p, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, rows, k, ld, 128 * am, BLOCK_K,
                       CU_TENSOR_MAP_SWIZZLE_128B);
 }
-static int tmap_b(CUtensorMap* m, const void* p, int64_t rows, int64_t k, int64_t ld, int cg) {
-  return make_tmap_2d(m, p, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, rows, k, ld, 256 / cg, BLOCK_K,
+static int tmap_b(CUtensorMap* m, const void* p, int64_t rows, int64_t k, int64_t ld, int cg, int bn = 256) {
+  return make_tmap_2d(m, p, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, rows, k, ld, bn / cg, BLOCK_K,
                       CU_TENSOR_MAP_SWIZZLE_128B);
 }
 static int tmap_c(CUtensorMap* m, const void* p, int64_t rows, int64_t n, int64_t ld) {
@@ -167,18 +188,18 @@ int gemm_local(const pk_tensor* A, const pk_tensor* B, pk_tensor* C, const pk_sc
   if (M % 128 || N % 256 || K % BLOCK_K || K == 0)
     return fail(PK_ERR_INVALID, "gemm: need M %% 128 == 0, N %% 256 == 0, K %% 64 == 0 (got %lld, %lld, %lld)",
                 (long long)M, (long long)N, (long long)K);
-  const Variant v = pick_variant(M, K, sched, false, M, N, default_sms(device, sched) / 2);
+  const Variant v = pick_variant(M, K, sched, false, M, N, default_sms(device, sched) / 2, true);
   const int cg = v.cg;
   GemmArgs args;
   init_args(args, v.am);
   PK_TRY(tmap_a(&args.tmap_a[0], A->ptr, M, K, ldA, v.am));
-  PK_TRY(tmap_b(&args.tmap_b, B->ptr, N, K, ldB, cg));
+  PK_TRY(tmap_b(&args.tmap_b, B->ptr, N, K, ldB, cg, v.bn));
   PK_TRY(tmap_c(&args.tmap_c[0], C->ptr, M, N, ldC));
   args.M = (int)M; args.N = (int)N; args.K = (int)K;
   args.rank = 0; args.world = 1;
   args.a_rows_per_src = (int)M;
   args.c_rows_per_dst = (int)M;
-  const int tiles = (int)((M / (128 * v.am * cg)) * (N / 256));
+  const int tiles = (int)((M / (128 * v.am * cg)) * (N / v.bn));
   const int sms = default_sms(device, sched);
   int clusters = std::min(tiles, sms / cg);
   if (clusters < 1) clusters = 1;
@@ -237,12 +258,12 @@ int ag_gemm(Comm* c, const pk_tensor* A, const pk_tensor* B, pk_tensor* C, pk_te
   // compute pairs: all of this rank's SMs less the communicator share (as below)
   const int64_t ag_pairs = std::max(1, (sched && sched->num_sms > 0 ? std::min(sched->num_sms, c->num_sms) : c->num_sms) / 2 -
                                            ((sched && sched->num_comm_sms > 0) ? sched->num_comm_sms : 16) / 2);
-  const Variant v = pick_variant(m_loc, K, sched, false, M, n_loc, ag_pairs);
+  const Variant v = pick_variant(m_loc, K, sched, false, M, n_loc, ag_pairs, true);
   const int cg = v.cg;
   const int tile_m = 128 * v.am * cg;
-  const int num_n = (int)(n_loc / 256);
+  const int num_n = (int)(n_loc / v.bn);
   int mode = sched ? sched->mode : PK_SCHED_AUTO;
-  if (mode == PK_SCHED_AUTO) mode = (num_n == 1 && !AG) ? PK_INTRA_SM : PK_INTER_SM;
+  if (mode == PK_SCHED_AUTO) mode = (n_loc <= 256 && !AG) ? PK_INTRA_SM : PK_INTER_SM;
   if (mode == PK_HYBRID) mode = PK_INTER_SM;   // HYBRID behaves like INTER_SM
 
   // Shard of every rank: zero-copy if the caller's tensor is symmetric.
@@ -263,7 +284,7 @@ int ag_gemm(Comm* c, const pk_tensor* A, const pk_tensor* B, pk_tensor* C, pk_te
   args.a_nsrc = n;
   args.c_rows_per_dst = (int)M;
   args.m_rot = (int)(c->rank * (m_loc / tile_m));
-  PK_TRY(tmap_b(&args.tmap_b, B->ptr, n_loc, K, ldB, cg));
+  PK_TRY(tmap_b(&args.tmap_b, B->ptr, n_loc, K, ldB, cg, v.bn));
   PK_TRY(tmap_c(&args.tmap_c[0], C->ptr, M, n_loc, ldC));
   const int tiles = (int)((M / tile_m) * num_n);
   const int clusters_total = std::max(1, (sched && sched->num_sms > 0 ? std::min(sched->num_sms, c->num_sms) : c->num_sms) / cg);
