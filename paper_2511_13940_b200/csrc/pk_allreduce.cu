@@ -327,7 +327,7 @@ int preload_allreduce() {
 int all_reduce_ablate(Comm* c, pk_tensor* x, uint32_t flags, size_t channel_bytes, cudaStream_t st);
 
 int all_reduce(Comm* c, pk_tensor* x, int op, const pk_sched* sched, cudaStream_t st) {
-  if (!x || !x->ptr) return fail(PK_ERR_INVALID, "all_reduce: null tensor");
+  if (!x || (!x->ptr && numel_of(x) != 0)) return fail(PK_ERR_INVALID, "all_reduce: null tensor");
   if (x->dtype != PK_BF16 && x->dtype != PK_F32) return fail(PK_ERR_CAPABILITY, "all_reduce: dtype must be bf16 or f32");
   if (op < PK_OP_SUM || op > PK_OP_MIN) return fail(PK_ERR_CAPABILITY, "all_reduce: unsupported reduce op %d", op);
   long long numel = 1;
@@ -446,7 +446,7 @@ enum { kScratchAblate = 11 };
 constexpr int kAblateMaxChunks = 4096;
 
 int all_reduce_ablate(Comm* c, pk_tensor* x, uint32_t flags, size_t channel_bytes, cudaStream_t st) {
-  if (!x || !x->ptr) return fail(PK_ERR_INVALID, "all_reduce_ablate: null tensor");
+  if (!x || (!x->ptr && numel_of(x) != 0)) return fail(PK_ERR_INVALID, "all_reduce_ablate: null tensor");
   if (x->dtype != PK_BF16 && x->dtype != PK_F32) return fail(PK_ERR_CAPABILITY, "all_reduce_ablate: dtype must be bf16 or f32");
   if (flags > 7) return fail(PK_ERR_INVALID, "all_reduce_ablate: unknown overhead flags %u", flags);
   long long numel = 1;

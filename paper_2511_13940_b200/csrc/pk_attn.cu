@@ -1080,7 +1080,8 @@ int ring_attn_fwd(Comm* c, const pk_tensor* q, const pk_tensor* k, const pk_tens
   PK_TRY(check_bshd(o, "o", &B2, &S2, &H2, &D2));
   if (B2 != B || S2 != S || H2 != H || D2 != D) return fail(PK_ERR_INVALID, "ring_attention: o shape differs from q");
   if (D != AT_D) return fail(PK_ERR_CAPABILITY, "ring_attention: head dim %lld unsupported (128 only)", (long long)D);
-  if (S % AT_BM) return fail(PK_ERR_INVALID, "ring_attention: local sequence %lld must be a multiple of %d", (long long)S, AT_BM);
+  if (S <= 0 || S % AT_BM || B <= 0 || H <= 0)
+    return fail(PK_ERR_INVALID, "ring_attention: local sequence %lld must be a positive multiple of %d", (long long)S, AT_BM);
   if (!lse || !lse->ptr || lse->dtype != PK_F32 || lse->ndim != 3 || lse->shape[0] != B || lse->shape[1] != H ||
       lse->shape[2] != S || lse->strides[2] != 1 || lse->strides[1] != S || lse->strides[0] != H * S)
     return fail(PK_ERR_INVALID, "ring_attention: lse must be contiguous float32 [B, H, S/n]");

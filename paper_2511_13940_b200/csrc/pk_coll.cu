@@ -132,11 +132,6 @@ int preload_coll() {
   return PK_OK;
 }
 
-static long long numel_of(const pk_tensor* t) {
-  long long n = 1;
-  for (int i = 0; i < t->ndim; ++i) n *= t->shape[i];
-  return n;
-}
 static bool contiguous(const pk_tensor* t) {
   long long expect = 1;
   for (int i = t->ndim - 1; i >= 0; --i) {
@@ -181,7 +176,8 @@ static int run_coll(Comm* c, const pk_tensor* x, CollArgs& a, long long units, c
 }
 
 int all_gather(Comm* c, const pk_tensor* x, pk_tensor* y, cudaStream_t st) {
-  if (!x || !y || !x->ptr || !y->ptr) return fail(PK_ERR_INVALID, "all_gather: null tensor");
+  if (!x || !y || ((!x->ptr || !y->ptr) && numel_of(x) != 0)) return fail(PK_ERR_INVALID, "all_gather: null tensor");
+  if (numel_of(x) == 0) return PK_OK;                 // same shapes on every rank: all skip
   if (x->dtype != y->dtype || !contiguous(x) || !contiguous(y)) return fail(PK_ERR_INVALID, "all_gather: contiguous tensors of one dtype");
   const long long xb = numel_of(x) * dtype_bytes(x->dtype);
   if (numel_of(y) != numel_of(x) * c->world) return fail(PK_ERR_INVALID, "all_gather: y must hold world * x elements");
@@ -194,7 +190,8 @@ int all_gather(Comm* c, const pk_tensor* x, pk_tensor* y, cudaStream_t st) {
 }
 
 int reduce_scatter(Comm* c, const pk_tensor* x, pk_tensor* y, int op, cudaStream_t st) {
-  if (!x || !y || !x->ptr || !y->ptr) return fail(PK_ERR_INVALID, "reduce_scatter: null tensor");
+  if (!x || !y || ((!x->ptr || !y->ptr) && numel_of(x) != 0)) return fail(PK_ERR_INVALID, "reduce_scatter: null tensor");
+  if (numel_of(x) == 0) return PK_OK;                 // same shapes on every rank: all skip
   if (x->dtype != y->dtype || (x->dtype != PK_BF16 && x->dtype != PK_F32))
     return fail(PK_ERR_CAPABILITY, "reduce_scatter: bf16 or f32");
   if (op < PK_OP_SUM || op > PK_OP_MIN) return fail(PK_ERR_CAPABILITY, "reduce_scatter: unsupported reduce op %d", op);
@@ -213,7 +210,8 @@ int reduce_scatter(Comm* c, const pk_tensor* x, pk_tensor* y, int op, cudaStream
 }
 
 int all_to_all(Comm* c, const pk_tensor* x, pk_tensor* y, cudaStream_t st) {
-  if (!x || !y || !x->ptr || !y->ptr) return fail(PK_ERR_INVALID, "all_to_all: null tensor");
+  if (!x || !y || ((!x->ptr || !y->ptr) && numel_of(x) != 0)) return fail(PK_ERR_INVALID, "all_to_all: null tensor");
+  if (numel_of(x) == 0) return PK_OK;                 // same shapes on every rank: all skip
   if (x->dtype != y->dtype || !contiguous(x) || !contiguous(y) || numel_of(x) != numel_of(y))
     return fail(PK_ERR_INVALID, "all_to_all: x and y must be contiguous, same size and dtype");
   if (x->ndim < 1 || x->shape[0] != c->world) return fail(PK_ERR_INVALID, "all_to_all: leading dim must equal world");

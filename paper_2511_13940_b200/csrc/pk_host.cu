@@ -72,9 +72,17 @@ int driver(const Driver** out) {
 }
 
 int check_matrix(const pk_tensor* t, const char* name, int dtype, int64_t* rows, int64_t* cols, int64_t* ld) {
-  if (t == nullptr || t->ptr == nullptr) return fail(PK_ERR_INVALID, "%s: null tensor", name);
+  if (t == nullptr) return fail(PK_ERR_INVALID, "%s: null tensor", name);
+  if (t->ptr == nullptr && (t->ndim != 2 || (t->shape[0] != 0 && t->shape[1] != 0)))   // empty tensors have no storage
+    return fail(PK_ERR_INVALID, "%s: null tensor", name);
   if (t->dtype != dtype) return fail(PK_ERR_INVALID, "%s: dtype %d, expected %d", name, t->dtype, dtype);
   if (t->ndim != 2) return fail(PK_ERR_INVALID, "%s: expected 2-D, got %d-D", name, t->ndim);
+  if (t->shape[0] == 0 || t->shape[1] == 0) {        // empty: strides carry no meaning
+    *rows = t->shape[0];
+    *cols = t->shape[1];
+    *ld = t->shape[1];
+    return PK_OK;
+  }
   if (t->strides[1] != 1) return fail(PK_ERR_INVALID, "%s: inner dimension must be contiguous", name);
   *rows = t->shape[0];
   *cols = t->shape[1];

@@ -162,6 +162,12 @@ struct Comm {
   uint32_t call_seq = 0;             // device-counted calls issued (call slot ring index)
 };
 
+inline long long numel_of(const pk_tensor* t) {
+  long long n = 1;
+  for (int i = 0; i < t->ndim; ++i) n *= t->shape[i];
+  return n;
+}
+
 // If [ptr, ptr+bytes) lies inside one of c's user PGLs, fill peers[] with the
 // same offset in every rank's buffer and return true.
 bool find_symmetric(Comm* c, const void* ptr, size_t bytes, void** peers);

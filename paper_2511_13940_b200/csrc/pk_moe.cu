@@ -92,6 +92,19 @@ __device__ __forceinline__ bool moe_wait_all(const MoeSync& s, int n, bool done)
   return ok;
 }
 
+// Rank-level done: the last CTA of this rank to finish signals every peer once,
+// so ranks may launch different grids (ragged token counts, T = 0). The
+// counter is the count phase's (idle by then: every CTA has passed the ready
+// wait, which follows its re-arm) and is re-armed here for the next kernel.
+__device__ __forceinline__ void moe_done(const MoeArgs& a) {
+  __threadfence_system();
+  if (atomicAdd(a.count_done, 1u) == gridDim.x - 1) {
+    *a.count_done = 0;
+    moe_signal_all(a.sync, a.n, a.rank, true);
+  }
+  if (blockIdx.x == 0) moe_wait_all(a.sync, a.n, true);
+}
+
 // key of one routing entry: the owner rank (rank-major) or the expert (expert-major); -1 invalid
 __device__ __forceinline__ int moe_key(const MoeArgs& a, int e) {
   if (e < 0 || e >= a.num_experts) return -1;
@@ -394,10 +407,7 @@ __global__ void __launch_bounds__(kDispatchThreads) moe_dispatch_kernel(const __
   }
   __threadfence_system();                              // every thread's peer stores before the done signal
   __syncthreads();
-  if (tid == 0) {
-    moe_signal_all(a.sync, a.n, a.rank, true);
-    if (blockIdx.x == 0) moe_wait_all(a.sync, a.n, true);
-  }
+  if (tid == 0) moe_done(a);
 }
 
 // ---------------------------------------------------------------- combine
@@ -475,10 +485,7 @@ __global__ void __launch_bounds__(kCombineThreads) moe_combine_kernel(const __gr
     }
   }
   __syncthreads();
-  if (threadIdx.x == 0) {
-    moe_signal_all(a.sync, a.n, a.rank, true);      // done reading everyone's y
-    if (blockIdx.x == 0) moe_wait_all(a.sync, a.n, true);
-  }
+  if (threadIdx.x == 0) moe_done(a);                 // done reading everyone's y
 }
 
 // ---------------------------------------------------------------- host
@@ -510,7 +517,8 @@ enum { kScratchMoeTable = 4, kScratchMoeIdx = 5, kScratchMoeY = 6 };
 // chunking and the per-entry slot table (slot_of) persist from a dispatch to
 // the next combine on the same comm.
 static int moe_common(Comm* c, const pk_tensor* topk, int num_experts, int layout, MoeArgs& a, int* T, int* K) {
-  if (!topk || topk->dtype != PK_I32 || topk->ndim != 2 || topk->strides[1] != 1 || topk->strides[0] != topk->shape[1])
+  if (!topk || topk->dtype != PK_I32 || topk->ndim != 2 ||
+      (topk->shape[0] != 0 && (topk->strides[1] != 1 || topk->strides[0] != topk->shape[1])))
     return fail(PK_ERR_INVALID, "moe: topk_idx must be a contiguous [T, k] int32 tensor");
   *T = (int)topk->shape[0];
   *K = (int)topk->shape[1];
@@ -540,7 +548,7 @@ static int moe_common(Comm* c, const pk_tensor* topk, int num_experts, int layou
   int G = std::min(*T, c->num_sms * per_sm);
   if (c->local_group && c->world > 1) G = std::min(G, c->num_sms);   // co-residency of all emulated ranks
   G = std::max(G, 1);
-  a.tpc = (*T + G - 1) / G;
+  a.tpc = std::max(1, (*T + G - 1) / G);             // T = 0: one CTA, no entries (it still joins the handshakes)
   a.grid = std::max(1, (*T + a.tpc - 1) / a.tpc);
   // scratch: [count_done | pad to 256 B][slot_of T*k][chunk_counts nkeys x G]
   // (slot_of first: a combine finds it where the dispatch with the same
@@ -615,7 +623,7 @@ int moe_dispatch(Comm* c, const pk_tensor* x, const pk_tensor* topk, int num_exp
     a.grid = std::max(1, (T + a.tpc - 1) / a.tpc);
   }
   CallRef call;
-  PK_TRY(begin_call(c, 0, 1, (uint32_t)a.grid, st, &call));
+  PK_TRY(begin_call(c, 0, 1, 1, st, &call));
   fill_moe_sync(c, a.sync, call);
   void* params[] = {&a};
   PK_CUDA(cudaMemsetAsync(a.count_done, 0, sizeof(uint32_t), st));
@@ -634,7 +642,7 @@ int moe_combine(Comm* c, const pk_tensor* y, const pk_tensor* topk, const pk_ten
   if (orows != T || H2 != H) return fail(PK_ERR_INVALID, "moe_combine: out must be [%d, %lld]", T, (long long)H);
   if ((H * 2) % 16 || (yld * 2) % 16 || (old * 2) % 16)
     return fail(PK_ERR_INVALID, "moe_combine: rows must be 16-byte multiples");
-  if (!w || w->dtype != PK_F32 || w->ndim != 2 || w->shape[0] != T || w->shape[1] != K || w->strides[0] != K)
+  if (!w || w->dtype != PK_F32 || w->ndim != 2 || w->shape[0] != T || w->shape[1] != K || (T != 0 && w->strides[0] != K))
     return fail(PK_ERR_INVALID, "moe_combine: weights must be contiguous float32 [T, k]");
   void* yp[kMaxRanks];
   if (!find_symmetric(c, y->ptr, (size_t)cap * yld * 2, yp)) {
@@ -654,7 +662,7 @@ int moe_combine(Comm* c, const pk_tensor* y, const pk_tensor* topk, const pk_ten
   int blocks = (int)std::min<long long>(((long long)T + kCombineThreads / 32 - 1) / (kCombineThreads / 32), c->num_sms);
   blocks = std::max(blocks, 1);
   CallRef call;
-  PK_TRY(begin_call(c, 0, 1, (uint32_t)blocks, st, &call));
+  PK_TRY(begin_call(c, 0, 1, 1, st, &call));
   fill_moe_sync(c, a.sync, call);
   void* params[] = {&a};
   const void* kern = K <= 8 ? (const void*)moe_combine_kernel<8> : (const void*)moe_combine_kernel<16>;

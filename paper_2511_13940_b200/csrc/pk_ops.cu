@@ -185,7 +185,7 @@ int gemm_local(const pk_tensor* A, const pk_tensor* B, pk_tensor* C, const pk_sc
   PK_TRY(check_matrix(C, "c", PK_BF16, &Mc, &Nc, &ldC));
   if (Kb != K) return fail(PK_ERR_INVALID, "gemm: K mismatch (a %lld, b %lld)", (long long)K, (long long)Kb);
   if (Mc != M || Nc != N) return fail(PK_ERR_INVALID, "gemm: c must be [%lld, %lld]", (long long)M, (long long)N);
-  if (M % 128 || N % 256 || K % BLOCK_K || K == 0)
+  if (M <= 0 || N <= 0 || M % 128 || N % 256 || K % BLOCK_K || K == 0)
     return fail(PK_ERR_INVALID, "gemm: need M %% 128 == 0, N %% 256 == 0, K %% 64 == 0 (got %lld, %lld, %lld)",
                 (long long)M, (long long)N, (long long)K);
   const Variant v = pick_variant(M, K, sched, false, M, N, default_sms(device, sched) / 2, true);
@@ -247,7 +247,7 @@ int ag_gemm(Comm* c, const pk_tensor* A, const pk_tensor* B, pk_tensor* C, pk_te
     PK_TRY(check_matrix(AG, "a_gathered", PK_BF16, &r, &k2, &ld));
     if (r != M || k2 != K || ld != K) return fail(PK_ERR_INVALID, "ag_gemm: a_gathered must be contiguous [%lld, %lld]", (long long)M, (long long)K);
   }
-  if (m_loc % 128 || n_loc % 256 || K % BLOCK_K || K == 0)
+  if (m_loc <= 0 || n_loc <= 0 || m_loc % 128 || n_loc % 256 || K % BLOCK_K || K == 0)
     return fail(PK_ERR_INVALID, "ag_gemm: need (M/n) %% 128 == 0, N_local %% 256 == 0, K %% 64 == 0 (got %lld, %lld, %lld)",
                 (long long)m_loc, (long long)n_loc, (long long)K);
   if (n == 1) {
@@ -410,7 +410,7 @@ int gemm_rs(Comm* c, const pk_tensor* A, const pk_tensor* B, pk_tensor* O, const
   const int64_t m_own = M / n;
   if (Mo != m_own || No != N)
     return fail(PK_ERR_INVALID, "gemm_rs: out must be [%lld, %lld]", (long long)m_own, (long long)N);
-  if (m_own % 128 || N % 256 || k_loc % BLOCK_K || k_loc == 0)
+  if (m_own <= 0 || N <= 0 || m_own % 128 || N % 256 || k_loc % BLOCK_K || k_loc == 0)
     return fail(PK_ERR_INVALID, "gemm_rs: need (M/n) %% 128 == 0, N %% 256 == 0, K %% 64 == 0 (got %lld, %lld, %lld)",
                 (long long)m_own, (long long)N, (long long)k_loc);
   if (n == 1) return gemm_local(A, B, O, sched, st, c->device);
@@ -465,7 +465,7 @@ int gemm_ar(Comm* c, const pk_tensor* A, const pk_tensor* B, pk_tensor* O, const
   const int n = c->world;
   if (Kb != K) return fail(PK_ERR_INVALID, "gemm_ar: K mismatch (a %lld, b %lld)", (long long)K, (long long)Kb);
   if (Mo != M || No != N) return fail(PK_ERR_INVALID, "gemm_ar: out must be [%lld, %lld]", (long long)M, (long long)N);
-  if (M % 256 || N % 256 || K % BLOCK_K || K == 0)   // workloads.py:445-447 (extent divisibility)
+  if (M <= 0 || N <= 0 || M % 256 || N % 256 || K % BLOCK_K || K == 0)   // workloads.py:445-447 (extents)
     return fail(PK_ERR_INVALID, "gemm_ar: need M %% 256 == 0, N %% 256 == 0, K %% 64 == 0 (got %lld, %lld, %lld)",
                 (long long)M, (long long)N, (long long)K);
   if (n == 1) return gemm_local(A, B, O, sched, st, c->device);
