@@ -3,10 +3,10 @@
 against float64 math on the same device, row checksums, exact integer
 reductions, and the dispatch / combine permutation identities.
 
-Sizes: AG-GEMM and GEMM-RS at M = N = K = 16384 (cfg2, n = 1 and an emulated
-n = 2), all-reduce of 1 GiB per rank (cfg3's largest), ring attention at
-S = 32768 over an emulated n = 8 (cfg4), MoE at T = 4096, E = 64, k = 8,
-H = 7168 (cfg5)."""
+Sizes: GEMM at 16384³ and 32768³ (cfg2, n = 1), AG-GEMM and GEMM-RS at
+M = N = K = 16384 over an emulated n = 2, all-reduce of 1 GiB per rank (cfg3's
+largest), ring attention at S = 32768 and 131072 over an emulated n = 8
+(cfg4), MoE at T = 1024 / 4096 / 16384, E = 64, k = 8, H = 7168 (cfg5)."""
 import numpy as np
 import pytest
 import torch
@@ -53,15 +53,16 @@ def _check_gemm(c, a_rows_fn, b, rows, K):
     assert (rs - rs_ref).abs().max().item() <= tol
 
 
-def test_gemm_16384_cubed():
+@pytest.mark.parametrize("size", [16384, 32768])
+def test_gemm_cubed(size):
     pk = _pk()
     g = torch.Generator(device="cuda").manual_seed(0)
-    a = (torch.randn(S, S, device="cuda", generator=g) * 0.1).bfloat16()
-    b = (torch.randn(S, S, device="cuda", generator=g) * 0.1).bfloat16()
+    a = (torch.randn(size, size, device="cuda", generator=g) * 0.1).bfloat16()
+    b = (torch.randn(size, size, device="cuda", generator=g) * 0.1).bfloat16()
     c = pk.gemm(a, b)
     torch.cuda.synchronize()
-    rows = torch.randint(0, S, (64,), device="cuda", generator=g)
-    _check_gemm(c, lambda r: a[r], b, rows, S)
+    rows = torch.randint(0, size, (64,), device="cuda", generator=g)
+    _check_gemm(c, lambda r: a[r], b, rows, size)
 
 
 def test_ag_gemm_and_gemm_rs_16384_emulated_world2():
@@ -113,10 +114,10 @@ def test_all_reduce_1gib_integer_exact():
         c.destroy()
 
 
-def test_ring_attention_32k_emulated_world8():
+@pytest.mark.parametrize("S_tot", [32768, 131072])
+def test_ring_attention_emulated_world8(S_tot):
     pk = _pk()
     world, B, H, D = 8, 1, 16, 128
-    S_tot = 32768
     S_loc = S_tot // world
     comms = pk.local_group(world)
     g = torch.Generator(device="cuda").manual_seed(3)
@@ -140,12 +141,13 @@ def test_ring_attention_32k_emulated_world8():
         c.destroy()
 
 
-def test_moe_dispatch_combine_full_shape():
+@pytest.mark.parametrize("T", [1024, 4096, 16384])
+def test_moe_dispatch_combine_full_shape(T):
     """cfg5 (T 4096, E 64, k 8, H 7168) over an emulated n = 2: every received
     row is its source token (recv_src names it), the counts add up, and
     combine with weights 1/k inverts dispatch exactly."""
     pk = _pk()
-    world, T, E, K, H = 2, 4096, 64, 8, 7168
+    world, E, K, H = 2, 64, 8, 7168
     comms = pk.local_group(world)
     g = torch.Generator(device="cuda").manual_seed(4)
     xs = [torch.randint(-64, 65, (T, H), device="cuda", generator=g).bfloat16() for _ in comms]
