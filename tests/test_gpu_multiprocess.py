@@ -30,3 +30,27 @@ def test_torchrun_world2():
     r = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     assert r.stdout.count("multiprocess ok") == 2, r.stdout
+
+
+@pytest.mark.parametrize("impl", ["pk", "reference"])
+def test_bench_under_torchrun_world2(impl):
+    """bench.py's N > 1 contract path (as the driver launches it): one JSON line
+    from rank 0 with the whole-job value, e2e and roofline keys."""
+    import json
+    env = dict(os.environ)
+    if torch.cuda.device_count() < 2:
+        env.update(PK_BENCH_DEVICE="0", PK_BENCH_BACKEND="gloo")
+    root = os.path.dirname(HERE)
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr", "127.0.0.1", "--master-port", str(_port()), os.path.join(root, "bench.py"),
+           "--gpus", "2", "--steps", "3", "--warmup", "3", "--size", "4096", "--impl", impl, "--cpu-seconds", "1"]
+    r = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=600, cwd=root)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    lines = [json.loads(x) for x in r.stdout.splitlines() if x.startswith("{")]
+    assert len(lines) == 1, r.stdout
+    line = lines[0]
+    assert line["n_gpus"] == 2 and line["value"] > 0 and line["e2e"]["value"] > 0
+    if impl == "pk":
+        assert line["roofline"]["overlapped"]["t_roof_ms"] > 0 and line["gpu_launches"] == 6
+    else:
+        assert line["impl"] == "reference" and line["cpu_baseline"]["kind"] == "port"
