@@ -1028,12 +1028,12 @@ static int launch_attn(AttnScratch& scr, int num_sms, AttnArgs& a, cudaStream_t 
   if (const char* e = getenv("PK_ATTN_SPLIT_MIN_BLOCKS")) min_blocks = atoi(e);   // test hook
   // The tail CTAs work on the tail items at staggered key offsets, so their
   // K/V only hits L2 if the heads the tail spans fit in it: at S_kv = 131072
-  // (64 MB of K/V per head) the split measured 4-10 % slower, at 32768-65536
-  // 4-13 % faster.
+  // (64 MB of K/V per head, 268 MB over the tail's heads) the split measured
+  // 4-10 % slower, at 32768-65536 (134 MB) 4-13 % faster.
   const int pairs = (a.S_q / AT_BM + 1) / 2;
   const int R = items % sms;
   const double tail_kv = (double)(R / pairs + 2) * a.S_kv * AT_D * 2 * 2;
-  const bool split = nblk >= min_blocks && R > 0 && tail_kv <= 100e6 && !getenv("PK_ATTN_NO_SPLIT");
+  const bool split = nblk >= min_blocks && R > 0 && tail_kv <= 200e6 && !getenv("PK_ATTN_NO_SPLIT");
   a.tail_items = split || getenv("PK_ATTN_FORCE_SPLIT") ? R : 0;
   if ((uint64_t)sms * ((uint64_t)a.tail_items * nblk + 1) >= (1ull << 32)) a.tail_items = 0;   // 32-bit split math
   a.tail_units = a.tail_items ? sms : 0;
