@@ -48,7 +48,10 @@ constexpr int AT_THREADS = 384;  // loader, MMA, TMEM alloc, idle, 2 x 4 softmax
 constexpr int AT_Q_BYTES = AT_BM * AT_D * 2;     // 32 KB per tile (2 swizzle atoms of 16 KB)
 constexpr int AT_K_BYTES = AT_BN * AT_D * 2;     // 32 KB
 constexpr int AT_V_BYTES = AT_BN * AT_D * 2;     // 32 KB
-constexpr int AT_KSTAGES = 2;
+#ifndef AT_KS
+#define AT_KS 2          // K stages (3 fits beside 2 V stages and both Q tiles)
+#endif
+constexpr int AT_KSTAGES = AT_KS;
 constexpr int AT_VSTAGES = 2;
 constexpr int AT_SMEM = 2 * AT_Q_BYTES + AT_KSTAGES * AT_K_BYTES + AT_VSTAGES * AT_V_BYTES + 512 + 1024;
 constexpr int AT_TMEM_COLS = 512;                // per tile: S (128, P aliased in its first 64) + O (128)
@@ -216,15 +219,15 @@ __global__ void __launch_bounds__(AT_THREADS, 1) attn_fwd_kernel(const __grid_co
   uint64_t* bars = reinterpret_cast<uint64_t*>(sv + AT_VSTAGES * AT_V_BYTES);
   uint64_t* q_full = bars + 0;
   uint64_t* q_empty = bars + 1;
-  uint64_t* k_full = bars + 2;      // [2]
-  uint64_t* k_empty = bars + 4;     // [2]
-  uint64_t* v_full = bars + 6;      // [2]
-  uint64_t* v_empty = bars + 8;     // [2]
-  uint64_t* s_full = bars + 10;     // [2] per tile
-  uint64_t* p_full = bars + 12;     // [2 tiles][2 halves]: P of keys [64h, 64h+64) in TMEM
-  uint64_t* o_full = bars + 16;     // [2] per tile
-  uint64_t* o_empty = bars + 18;    // [2] per tile: the epilogue has read O
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 20);
+  uint64_t* k_full = bars + 2;                  // [AT_KSTAGES]
+  uint64_t* k_empty = k_full + AT_KSTAGES;      // [AT_KSTAGES]
+  uint64_t* v_full = k_empty + AT_KSTAGES;      // [2]
+  uint64_t* v_empty = v_full + 2;               // [2]
+  uint64_t* s_full = v_empty + 2;               // [2] per tile
+  uint64_t* p_full = s_full + 2;                // [2 tiles][2 halves]: P of keys [64h, 64h+64) in TMEM
+  uint64_t* o_full = p_full + 4;                // [2] per tile
+  uint64_t* o_empty = o_full + 2;               // [2] per tile: the epilogue has read O
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_empty + 2);
   __shared__ int merge_flag[2];
 
   const uint32_t warp = warp_id_sync();
@@ -272,8 +275,8 @@ __global__ void __launch_bounds__(AT_THREADS, 1) attn_fwd_kernel(const __grid_co
   if (warp == 0 && lane == 0) {
     mbar_init(q_full, 1);
     mbar_init(q_empty, 1);
+    for (int i = 0; i < AT_KSTAGES; ++i) { mbar_init(&k_full[i], 1); mbar_init(&k_empty[i], 1); }
     for (int i = 0; i < 2; ++i) {
-      mbar_init(&k_full[i], 1); mbar_init(&k_empty[i], 1);
       mbar_init(&v_full[i], 1); mbar_init(&v_empty[i], 1);
       mbar_init(&s_full[i], 1); mbar_init(&o_full[i], 1);
       mbar_init(&p_full[2 * i], 4); mbar_init(&p_full[2 * i + 1], 4);
@@ -307,10 +310,10 @@ __global__ void __launch_bounds__(AT_THREADS, 1) attn_fwd_kernel(const __grid_co
         }
       };
       auto load_k = [&](int g, int j, int h, int b) {
-        const int st = g & 1;
+        const int st = g % AT_KSTAGES;
         const int step = j / bps, row = (j % bps) * AT_BN;
         step_ready(step);
-        mbar_wait(&k_empty[st], ((g >> 1) & 1) ^ 1);
+        mbar_wait(&k_empty[st], ((g / AT_KSTAGES) & 1) ^ 1);
         uint8_t* kb = sk + st * AT_K_BYTES;
 #ifdef AT_NO_KV_LOADS   // timing diagnostic only: K/V loaded for the first two blocks, then reused (wrong results)
         if (g >= 2) { mbar_arrive(&k_full[st]); return; }
@@ -355,7 +358,7 @@ __global__ void __launch_bounds__(AT_THREADS, 1) attn_fwd_kernel(const __grid_co
     constexpr uint32_t id_o = idesc_bf16(AT_BM, AT_D, 1);
     auto issue_qk = [&](int x, int g) {                 // S_x = Q_x K_g^T
       const uint32_t q_addr = smem_u32(sq + x * AT_Q_BYTES);
-      const uint32_t k_addr = smem_u32(sk + (g & 1) * AT_K_BYTES);
+      const uint32_t k_addr = smem_u32(sk + (g % AT_KSTAGES) * AT_K_BYTES);
 #pragma unroll
       for (int kk = 0; kk < AT_D / 16; ++kk) {
         const int atom = kk >> 2, sub = kk & 3;
@@ -382,18 +385,18 @@ __global__ void __launch_bounds__(AT_THREADS, 1) attn_fwd_kernel(const __grid_co
     for (SegInfo sg; seg_next(it, sg); ++seg) {
       const int len = sg.j1 - sg.j0;
       mbar_wait(q_full, seg & 1);
-      mbar_wait(&k_full[g & 1], (g >> 1) & 1);
+      mbar_wait(&k_full[g % AT_KSTAGES], (g / AT_KSTAGES) & 1);
       tc_fence_after();
       if (elect_one()) {
         for (int x = 0; x < sg.ntile; ++x) issue_qk(x, g);
-        umma_commit<1>(&k_empty[g & 1]);
+        umma_commit<1>(&k_empty[g % AT_KSTAGES]);
       }
       __syncwarp();
       for (int i = 0; i < len; ++i) {
         const int gg = g + i;
         mbar_wait(&v_full[gg & 1], (gg >> 1) & 1);
         const bool more = i + 1 < len;
-        if (more) mbar_wait(&k_full[(gg + 1) & 1], ((gg + 1) >> 1) & 1);
+        if (more) mbar_wait(&k_full[(gg + 1) % AT_KSTAGES], ((gg + 1) / AT_KSTAGES) & 1);
         for (int x = 0; x < sg.ntile; ++x) {
           const int gxx = x ? gx1 : gx0, sgx = x ? segx1 : segx0;
           // O_x of the previous segment must have been read by its epilogue
@@ -416,7 +419,7 @@ __global__ void __launch_bounds__(AT_THREADS, 1) attn_fwd_kernel(const __grid_co
         gx1 += sg.ntile > 1;
         if (elect_one()) {
           umma_commit<1>(&v_empty[gg & 1]);
-          if (more) umma_commit<1>(&k_empty[(gg + 1) & 1]);
+          if (more) umma_commit<1>(&k_empty[(gg + 1) % AT_KSTAGES]);
           else umma_commit<1>(q_empty);
         }
         __syncwarp();
