@@ -1,6 +1,8 @@
 """Seeded randomized sweep over shapes, world sizes and schedules for every op
 (bit-exact on integer data against the oracle). Complements the hand-picked
 cases: catches tile-boundary, rotation, staging and counter-reuse bugs."""
+import os
+
 import numpy as np
 import pytest
 import torch
@@ -8,6 +10,9 @@ import torch
 import oracle
 
 pytestmark = pytest.mark.gpu
+# long soak runs: PK_FUZZ_SEED shifts every seed, PK_FUZZ_SCALE multiplies the iterations
+SEED = int(os.environ.get("PK_FUZZ_SEED", "0"))
+SCALE = int(os.environ.get("PK_FUZZ_SCALE", "1"))
 
 
 def _pk():
@@ -37,8 +42,8 @@ def run_ranks(comms, fn):
 
 def test_fuzz_gemm():
     pk = _pk()
-    rng = np.random.default_rng(1234)
-    for _ in range(12):
+    rng = np.random.default_rng(1234 + SEED)
+    for _ in range(12 * SCALE):
         M = 128 * int(rng.integers(1, 12))
         N = 256 * int(rng.integers(1, 5))
         K = 64 * int(rng.integers(1, 10))
@@ -53,10 +58,10 @@ def test_fuzz_ag_rs_ar_one_group_many_calls():
     """One communicator group, many back-to-back calls of different ops and
     shapes: ready/done counters, flags and scratch growth must stay consistent."""
     pk = _pk()
-    rng = np.random.default_rng(99)
+    rng = np.random.default_rng(99 + SEED)
     world = 4
     comms = pk.local_group(world)
-    for it in range(10):
+    for it in range(10 * SCALE):
         op = ["ag", "rs", "ar", "gemm_ar", "allreduce"][it % 5]
         if op == "ag":
             m_loc, n_loc, K = 128 * int(rng.integers(1, 5)), 256 * int(rng.integers(1, 3)), 64 * int(rng.integers(1, 4))
@@ -99,8 +104,8 @@ def test_fuzz_ag_rs_ar_one_group_many_calls():
 
 def test_fuzz_moe_routing():
     pk = _pk()
-    rng = np.random.default_rng(7)
-    for _ in range(4):
+    rng = np.random.default_rng(7 + SEED)
+    for _ in range(4 * SCALE):
         world = int(rng.integers(1, 5))
         T, K = int(rng.integers(1, 200)), int(rng.integers(1, 5))
         E = world * int(rng.integers(K, K + 4))
@@ -125,8 +130,8 @@ def test_fuzz_moe_routing():
 
 def test_fuzz_ring_attention_shapes():
     pk = _pk()
-    rng = np.random.default_rng(5)
-    for _ in range(4):
+    rng = np.random.default_rng(5 + SEED)
+    for _ in range(4 * SCALE):
         world = int(rng.integers(1, 5))
         B, H = int(rng.integers(1, 3)), int(rng.integers(1, 4))
         S_loc = 128 * int(rng.integers(1, 4))
