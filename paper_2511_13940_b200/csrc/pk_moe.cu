@@ -416,6 +416,11 @@ __global__ void __launch_bounds__(kDispatchThreads) moe_dispatch_kernel(const __
 // 2*KMAX independent 16 B peer loads per lane in flight, folding in ascending
 // k order in fp32.
 constexpr int kCombineThreads = 512;
+// y rows were published before the ready handshake (acquire at sys scope), so
+// the loads need no volatile semantics: L2-only (.cg) loads
+#ifndef MOE_COMBINE_LD
+#define MOE_COMBINE_LD(p) ld_v4_cg(p)
+#endif
 
 template <int KMAX>
 __global__ void __launch_bounds__(kCombineThreads) moe_combine_kernel(const __grid_constant__ MoeArgs a) {
@@ -455,8 +460,8 @@ __global__ void __launch_bounds__(kCombineThreads) moe_combine_kernel(const __gr
 #pragma unroll
         for (int j = 0; j < KMAX; ++j) {
           if (rows[j] != nullptr) {
-            in0[j] = ld_v4_volatile(rows[j] + (long long)v0 * 16);
-            if (v1 < nvec) in1[j] = ld_v4_volatile(rows[j] + (long long)v1 * 16);
+            in0[j] = MOE_COMBINE_LD(rows[j] + (long long)v0 * 16);
+            if (v1 < nvec) in1[j] = MOE_COMBINE_LD(rows[j] + (long long)v1 * 16);
           }
         }
         float acc0[8], acc1[8];

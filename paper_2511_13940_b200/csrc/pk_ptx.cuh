@@ -366,6 +366,11 @@ PK_DEV uint4 ld_v4(const void* p) {
   asm volatile("ld.global.v4.b32 {%0, %1, %2, %3}, [%4];" : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p) : "memory");
   return r;
 }
+PK_DEV uint4 ld_v4_cg(const void* p) {      // L2-only load (peer rows published before an acquire)
+  uint4 r;
+  asm volatile("ld.global.cg.v4.b32 {%0, %1, %2, %3}, [%4];" : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p) : "memory");
+  return r;
+}
 PK_DEV uint4 ld_v4_volatile(const void* p) {
   uint4 r;
   asm volatile("ld.volatile.global.v4.b32 {%0, %1, %2, %3}, [%4];" : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p) : "memory");
