@@ -4,6 +4,10 @@
  * returns a pk_status; on failure pk_last_error() returns a thread-local
  * message. Device work is enqueued on the caller's cudaStream_t (passed as
  * void*) and is asynchronous; inputs are borrowed for the stream-ordered call.
+ * Every call may be captured into a CUDA graph (warm it up once outside the
+ * capture so symmetric scratch exists): a communicator's first captured call
+ * switches it to device-side call counting. Calls on one communicator must be
+ * issued in the same order on every rank and from one stream at a time.
  *
  * Reference interfaces replaced (all paths into /root/reference):
  *   pk_comm_init / pk_comm_init_local  <- the simulated "devices" of one engine
@@ -191,7 +195,8 @@ typedef enum {
   PK_MOE_EXPERT_MAJOR = 1   /* one 256-row-padded segment per local expert, (src, token, k)
                              * order inside it: the expert GEMM reads rows in place */
 } pk_moe_layout;
-/* Transfer mechanism (hwmodel.py select_mechanism, 211-245). */
+/* Transfer mechanism (hwmodel.py select_mechanism, 211-245). AUTO resolves
+ * to the policy's answer for row-sized messages, TMA (bulk copies). */
 typedef enum { PK_MECH_AUTO = 0, PK_MECH_REG = 1, PK_MECH_TMA = 2 } pk_mechanism;
 /* Dispatch with an explicit layout and mechanism. For PK_MOE_EXPERT_MAJOR,
  * expert_plan (int32, >= 2 + cap/256 entries) receives [num_tiles, rows,
@@ -202,7 +207,8 @@ PK_API int pk_moe_dispatch_ex(pk_comm* comm, const pk_tensor* x, const pk_tensor
                               pk_tensor* recv_src, pk_tensor* recv_count, pk_tensor* expert_plan,
                               void* stream);
 /* Combine: y [cap, H] rows produced by the owner for its received slots are
- * sent back and summed with weights w [T, k] f32 into out [T, H] bf16. */
+ * sent back and summed with weights w [T, k] f32 into out [T, H] bf16.
+ * Ranks may hold different token counts (T = 0 included) in both calls. */
 PK_API int pk_moe_combine(pk_comm* comm, const pk_tensor* y, const pk_tensor* topk_idx,
                           const pk_tensor* w, int num_experts, pk_tensor* out, void* stream);
 
