@@ -196,6 +196,7 @@ struct ArAblateArgs {
   uint8_t* staging;                  // [gridDim.x][world + 1][chunk_vecs * 16] local staging
   long long chunk_vecs;
   int max_chunks;
+  int hw;                            // chunks [0, hw) took part in every earlier two-way round
 };
 
 template <int DT, int FLAGS>
@@ -207,14 +208,29 @@ __global__ void __launch_bounds__(512) ar_ablate_kernel(const __grid_constant__ 
   const long long hi = min(a.nvec, lo + per);
   const int nch = (int)((per + A.chunk_vecs - 1) / A.chunk_vecs);     // the same on every rank
   uint8_t* stg = A.staging + (long long)blockIdx.x * (a.world + 1) * A.chunk_vecs * 16;
+  if constexpr ((FLAGS & PK_OVH_TWO_WAY) != 0) {
+    // every chunk's counters must equal the number of two-way calls (A.calls)
+    // whatever the sizes of the calls in between: chunks used before but not
+    // now count this round here; chunks used for the first time (>= hw) add
+    // the rounds they missed in their handshake below
+    if (blockIdx.x == 0) {
+      for (int i = nch * a.world + threadIdx.x; i < A.hw * a.world; i += blockDim.x) {
+        const int c = i / a.world, d = i % a.world;
+        // relaxed: nothing is published by these rounds
+        asm volatile("red.relaxed.sys.global.add.u32 [%0], 1;" :: "l"(A.req_peer[d] + a.rank * A.max_chunks + c) : "memory");
+        asm volatile("red.relaxed.sys.global.add.u32 [%0], 1;" :: "l"(A.ack_peer[d] + a.rank * A.max_chunks + c) : "memory");
+      }
+    }
+  }
   for (int c = blockIdx.x; c < nch; c += gridDim.x) {
     if constexpr ((FLAGS & PK_OVH_TWO_WAY) != 0) {
       if (threadIdx.x == 0) {
         __threadfence_system();
-        for (int d = 0; d < a.world; ++d) signal_add(A.req_peer[d] + a.rank * A.max_chunks + c, 1u);   // request
+        const uint32_t inc = c >= A.hw ? A.calls : 1u;
+        for (int d = 0; d < a.world; ++d) signal_add(A.req_peer[d] + a.rank * A.max_chunks + c, inc);   // request
         for (int r = 0; r < a.world; ++r) {                                                         // answer
           wait_geq(A.req_local + r * A.max_chunks + c, A.calls, a.err, a.timeout_ns);
-          signal_add(A.ack_peer[r] + a.rank * A.max_chunks + c, 1u);
+          signal_add(A.ack_peer[r] + a.rank * A.max_chunks + c, inc);
         }
         for (int d = 0; d < a.world; ++d) wait_geq(A.ack_local + d * A.max_chunks + c, A.calls, a.err, a.timeout_ns);
       }
@@ -472,6 +488,7 @@ int all_reduce_ablate(Comm* c, pk_tensor* x, uint32_t flags, size_t channel_byte
   if (ctl->local != before) {                                          // fresh counters
     PK_CUDA(cudaMemsetAsync(ctl->local, 0, ctl_bytes, st));
     c->ablate_calls = 0;
+    c->ablate_hw = 0;
   }
   uint8_t* cb = static_cast<uint8_t*>(ctl->local);
   PK_CUDA(cudaMemcpyAsync(cb, peers, sizeof(void*) * c->world, cudaMemcpyHostToDevice, st));
@@ -520,7 +537,11 @@ int all_reduce_ablate(Comm* c, pk_tensor* x, uint32_t flags, size_t channel_byte
   PK_CUDA(cudaStreamIsCapturing(st, &cs));
   if (cs != cudaStreamCaptureStatusNone)   // the handshake rounds are host-counted
     return fail(PK_ERR_INVALID, "all_reduce_ablate: not capturable into a CUDA graph");
-  c->ablate_calls += 1;
+  if (flags & PK_OVH_TWO_WAY) {                                      // handshake rounds only
+    c->ablate_calls += 1;
+    A.hw = c->ablate_hw;
+    c->ablate_hw = std::max(c->ablate_hw, nch);
+  }
   A.calls = c->ablate_calls;
   PK_TRY(begin_call(c, 0, 1, (uint32_t)blocks, st, &a.call));
   a.timeout_ns = c->timeout_ns;

@@ -158,6 +158,7 @@ struct Comm {
   void* ablate_stage = nullptr;      // all_reduce_ablate staging channels (local)
   size_t ablate_stage_bytes = 0;
   uint32_t ablate_calls = 0;         // handshake round counter (req/ack counters only grow)
+  int ablate_hw = 0;                 // chunks used by the two-way rounds so far
   bool device_counts = false;        // sticky: set by the first call made under stream capture
   uint32_t call_seq = 0;             // device-counted calls issued (call slot ring index)
 };
