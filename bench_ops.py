@@ -49,6 +49,8 @@ def timeit(fn, iters=10, warm=3, min_ms=50.0):
         fn()
     e1.record()
     torch.cuda.synchronize()
+    for c in getattr(fn, "comms", ()):             # a timed-out wait invalidates the number: fail loudly
+        c.check()
     return e0.elapsed_time(e1) / iters
 
 
@@ -64,6 +66,7 @@ def ranks(comms, fn):
                 fn(r, c, streams[r])
         for s in streams:
             cur.wait_stream(s)
+    run.comms = comms
     return run
 
 
