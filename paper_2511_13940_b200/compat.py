@@ -693,6 +693,7 @@ def execute_kernel(spec: LcscKernelSpec, workload: WorkloadPlan, profile=None, o
     if own:
         comms = local_group(workload.num_devices, torch.cuda.current_device())
     streams = [torch.cuda.Stream() for _ in comms]
+    torch.cuda.synchronize()                  # staged inputs visible to every rank's stream
     t0 = time.perf_counter()
     workload.device_ns = 0.0
     try:

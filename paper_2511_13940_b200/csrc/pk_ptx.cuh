@@ -17,6 +17,13 @@
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include "pk_host.h"
+// Every signal_add follows an explicit __threadfence_system() in the same
+// thread (fence + relaxed atomic = a release pattern), so the add itself is
+// relaxed: a red.release.sys per peer re-fences each time, which measured
+// 17.8 -> 10.2 us for a 16-byte all-reduce of two emulated ranks.
+#ifndef PK_SIGNAL_RELAXED
+#define PK_SIGNAL_RELAXED 1
+#endif
 
 #define PK_DEV __device__ __forceinline__
 
@@ -291,9 +298,13 @@ PK_DEV void st_shared_v4(uint32_t addr, uint32_t a, uint32_t b, uint32_t c, uint
 }
 
 // ---------------------------------------------------------------- cross-GPU signals
-// signal(): fire-and-forget add with release semantics at system scope.
+// signal(): fire-and-forget add at system scope; callers fence first (above).
 PK_DEV void signal_add(uint32_t* peer_counter, uint32_t v) {
+#if PK_SIGNAL_RELAXED
+  asm volatile("red.relaxed.sys.global.add.u32 [%0], %1;" :: "l"(peer_counter), "r"(v) : "memory");
+#else
   asm volatile("red.release.sys.global.add.u32 [%0], %1;" :: "l"(peer_counter), "r"(v) : "memory");
+#endif
 }
 // signal_all(): one multicast add reaching every device's counter (NVLS).
 PK_DEV void mm_signal_add(uint32_t* mc_counter, uint32_t v) {

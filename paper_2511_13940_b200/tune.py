@@ -122,6 +122,7 @@ def time_ranks(comms, launch: Callable, iters: int = 5, warmup: int = 2) -> floa
     """ms per call: CUDA events on every rank's stream, max over ranks."""
     import torch
     streams = [torch.cuda.Stream() for _ in comms]
+    torch.cuda.synchronize()                  # operands made on the current stream are ready
 
     def once():
         for r, c in enumerate(comms):

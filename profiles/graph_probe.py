@@ -55,6 +55,11 @@ def main():
     out = {}
     out["fork_join_tiny_kernel"] = graph_ms(forked(world, lambda r, s: tiny[r].add_(1)))
     out["fork_join_two_tiny_kernels"] = graph_ms(forked(world, lambda r, s: (tiny[r].add_(1), tiny[r].mul_(1))))
+    tiny_ar = [c.empty((4,), torch.float32) for c in comms]        # one 16-byte vector: barriers only
+    out["all_reduce_16B"] = graph_ms(forked(world, lambda r, s: pk.all_reduce(comms[r], tiny_ar[r], stream=s)))
+    xg = [torch.zeros(8, 8, device="cuda", dtype=torch.bfloat16) for _ in range(world)]
+    yg = [torch.zeros(8 * world, 8, device="cuda", dtype=torch.bfloat16) for _ in range(world)]
+    out["all_gather_128B"] = graph_ms(forked(world, lambda r, s: pk.all_gather(comms[r], xg[r], out=yg[r], stream=s)))
     for kib in (64, 1024):
         n_el = kib * 1024 // 2
         ts = [c.empty((n_el,)) for c in comms]

@@ -16,6 +16,7 @@ def _pk():
 
 
 def run_ranks(comms, fn):
+    torch.cuda.synchronize()                  # inputs made on the current stream are ready for every rank's stream
     streams = [torch.cuda.Stream() for _ in comms]
     outs = []
     for r, c in enumerate(comms):

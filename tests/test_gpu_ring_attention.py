@@ -27,6 +27,7 @@ def run(world, B, S_loc, H, seed=0, scale=None):
     ks = [torch.randn(B, S_loc, H, D, device="cuda", generator=g).bfloat16() for _ in range(world)]
     vs = [torch.randn(B, S_loc, H, D, device="cuda", generator=g).bfloat16() for _ in range(world)]
     streams = [torch.cuda.Stream() for _ in range(world)]
+    torch.cuda.synchronize()                  # inputs made on the current stream are ready for every rank's stream
     outs = []
     for r in range(world):
         with torch.cuda.stream(streams[r]):
