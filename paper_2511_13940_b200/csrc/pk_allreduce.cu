@@ -67,7 +67,7 @@ __device__ __forceinline__ uint4 pack8(const float (&f)[8]) {
 __device__ __forceinline__ void ar_start_barrier(const ArArgs& a) {
   if (threadIdx.x == 0) {
     if (blockIdx.x == 0) {
-      __threadfence_system();
+      fence_sys();
       for (int d = 0; d < a.world; ++d) signal_add(a.ready_peer[d] + a.rank, 1u);
     }
     call_note(a.call);
@@ -80,7 +80,7 @@ __device__ __forceinline__ void ar_start_barrier(const ArArgs& a) {
 __device__ __forceinline__ void ar_end_barrier(const ArArgs& a) {
   __syncthreads();
   if (threadIdx.x == 0) {
-    __threadfence_system();
+    fence_sys();
     for (int d = 0; d < a.world; ++d) signal_add(a.done_peer[d] + a.rank, 1u);
     if (blockIdx.x == 0)
       for (int d = 0; d < a.world; ++d) wait_geq(a.done_local + d, call_get(a.call, 2), a.err, a.timeout_ns);
@@ -225,7 +225,7 @@ __global__ void __launch_bounds__(512) ar_ablate_kernel(const __grid_constant__ 
   for (int c = blockIdx.x; c < nch; c += gridDim.x) {
     if constexpr ((FLAGS & PK_OVH_TWO_WAY) != 0) {
       if (threadIdx.x == 0) {
-        __threadfence_system();
+        fence_sys();
         const uint32_t inc = c >= A.hw ? A.calls : 1u;
         for (int d = 0; d < a.world; ++d) signal_add(A.req_peer[d] + a.rank * A.max_chunks + c, inc);   // request
         for (int r = 0; r < a.world; ++r) {                                                         // answer
@@ -442,7 +442,7 @@ __global__ void mm_selftest_kernel(uint8_t* mc, uint8_t* local, long long nvec) 
     mm_st_v4(mc + v * 16, w);
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) {
-    __threadfence_system();
+    fence_sys();
     mm_signal_add(reinterpret_cast<uint32_t*>(mc + 2 * nvec * 16), 1u);
   }
 }

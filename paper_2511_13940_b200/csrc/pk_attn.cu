@@ -934,11 +934,11 @@ __global__ void __launch_bounds__(AT_THREADS, 1) attn2_fwd_kernel(const __grid_c
 __global__ void sync_signal_kernel(uint32_t* p0, uint32_t* p1, uint32_t* p2, uint32_t* p3, uint32_t* p4,
                                    uint32_t* p5, uint32_t* p6, uint32_t* p7, int n) {
   uint32_t* ps[8] = {p0, p1, p2, p3, p4, p5, p6, p7};
-  __threadfence_system();
+  fence_sys();
   for (int d = 0; d < n; ++d) signal_add(ps[d], 1u);
 }
 __global__ void flag_set_kernel(uint32_t* flag, const CallRef call) {
-  __threadfence_system();
+  fence_sys();
   asm volatile("st.release.gpu.global.u32 [%0], %1;" :: "l"(flag), "r"(call_get(call, 0)) : "memory");
 }
 // wait until every rank's counter reaches the call's count `which` (1 ready, 2 done)

@@ -48,7 +48,7 @@ __device__ __forceinline__ float coll_op(int op, float a, float b) {
 __global__ void __launch_bounds__(1024) coll_kernel(const __grid_constant__ CollArgs a) {
   if (threadIdx.x == 0) {
     if (blockIdx.x == 0) {
-      __threadfence_system();
+      fence_sys();
       for (int d = 0; d < a.world; ++d) signal_add(a.ready_peer[d] + a.rank, 1u);
     }
     call_note(a.call);
@@ -119,7 +119,7 @@ __global__ void __launch_bounds__(1024) coll_kernel(const __grid_constant__ Coll
   }
   __syncthreads();
   if (threadIdx.x == 0) {
-    __threadfence_system();
+    fence_sys();
     for (int d = 0; d < a.world; ++d) signal_add(a.done_peer[d] + a.rank, 1u);
     if (blockIdx.x == 0)
       for (int d = 0; d < a.world; ++d) wait_geq(a.done_local + d, call_get(a.call, 2), a.err, a.timeout_ns);

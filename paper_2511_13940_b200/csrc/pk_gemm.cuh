@@ -216,7 +216,7 @@ lcsc_gemm_kernel(const __grid_constant__ GemmArgs args) {
   // every rank (signal(), primitives.py:264-272); the stream order guarantees
   // this rank's inputs/zeroed outputs are in place when the kernel runs.
   if (args.sync.ready_local != nullptr && blockIdx.x == 0 && threadIdx.x == 0) {
-    __threadfence_system();
+    fence_sys();
     for (int d = 0; d < args.world; ++d) signal_add(args.sync.ready_peer[d] + args.rank, 1u);
   }
   tc_fence_before();
@@ -359,7 +359,7 @@ lcsc_gemm_kernel(const __grid_constant__ GemmArgs args) {
     }
     __syncthreads();
     if (threadIdx.x == 0) {
-      __threadfence_system();
+      fence_sys();
       for (int d = 0; d < args.world; ++d) signal_add(args.sync.done_peer[d] + args.rank, 1u);
     }
   } else if (is_comm) {
@@ -705,7 +705,7 @@ lcsc_gemm_kernel(const __grid_constant__ GemmArgs args) {
         if (lane == 0) {
           bulk_wait<0>();
           fence_async_global();
-          __threadfence_system();
+          fence_sys();
           const int tile_id = mt * num_n + nt;
           const int owner = args.ar_mode == 2 ? (mt * Cfg::TILE_M) / args.ar_owner_rows : tile_id % args.world;
           signal_add(args.ar_tile_peer[owner] + tile_id, 1u);
@@ -719,7 +719,7 @@ lcsc_gemm_kernel(const __grid_constant__ GemmArgs args) {
     // done[rank] on every peer (one per epilogue warp).
     if (args.sync_done_signal && lane == 0) {
       fence_async_global();
-      __threadfence_system();
+      fence_sys();
       for (int d = 0; d < args.world; ++d) signal_add(args.sync.done_peer[d] + args.rank, 1u);
     }
   }

@@ -80,7 +80,7 @@ struct MoeArgs {
 };
 
 __device__ __forceinline__ void moe_signal_all(const MoeSync& s, int n, int rank, bool done) {
-  __threadfence_system();
+  fence_sys();
   for (int d = 0; d < n; ++d) signal_add((done ? s.done_peer[d] : s.ready_peer[d]) + rank, 1u);
 }
 __device__ __forceinline__ bool moe_wait_all(const MoeSync& s, int n, bool done) {
@@ -97,7 +97,7 @@ __device__ __forceinline__ bool moe_wait_all(const MoeSync& s, int n, bool done)
 // counter is the count phase's (idle by then: every CTA has passed the ready
 // wait, which follows its re-arm) and is re-armed here for the next kernel.
 __device__ __forceinline__ void moe_done(const MoeArgs& a) {
-  __threadfence_system();
+  fence_sys();
   if (atomicAdd(a.count_done, 1u) == gridDim.x - 1) {
     *a.count_done = 0;
     moe_signal_all(a.sync, a.n, a.rank, true);
@@ -405,7 +405,7 @@ __global__ void __launch_bounds__(kDispatchThreads) moe_dispatch_kernel(const __
     bulk_wait<0>();
     fence_async_global();
   }
-  __threadfence_system();                              // every thread's peer stores before the done signal
+  fence_sys();                              // every thread's peer stores before the done signal
   __syncthreads();
   if (tid == 0) moe_done(a);
 }

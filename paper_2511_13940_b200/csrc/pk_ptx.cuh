@@ -17,10 +17,13 @@
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include "pk_host.h"
-// Every signal_add follows an explicit __threadfence_system() in the same
+// Every signal_add follows an explicit fence_sys() in the same
 // thread (fence + relaxed atomic = a release pattern), so the add itself is
 // relaxed: a red.release.sys per peer re-fences each time, which measured
 // 17.8 -> 10.2 us for a 16-byte all-reduce of two emulated ranks.
+#ifndef PK_FENCE_SC   // 0: fence.acq_rel.sys instead (enough for the release pattern; measured the same)
+#define PK_FENCE_SC 1
+#endif
 #ifndef PK_SIGNAL_RELAXED
 #define PK_SIGNAL_RELAXED 1
 #endif
@@ -298,6 +301,16 @@ PK_DEV void st_shared_v4(uint32_t addr, uint32_t a, uint32_t b, uint32_t c, uint
 }
 
 // ---------------------------------------------------------------- cross-GPU signals
+// The fence every signalling thread issues before its signal_add (fence.sc.sys
+// by default; acq_rel would be enough for the release pattern and measured
+// the same on one GPU).
+PK_DEV void fence_sys() {
+#if PK_FENCE_SC
+  __threadfence_system();
+#else
+  asm volatile("fence.acq_rel.sys;" ::: "memory");
+#endif
+}
 // signal(): fire-and-forget add at system scope; callers fence first (above).
 PK_DEV void signal_add(uint32_t* peer_counter, uint32_t v) {
 #if PK_SIGNAL_RELAXED
