@@ -6,6 +6,7 @@
 #include "pk_host.h"
 #include "pk_gemm.cuh"
 #include <algorithm>
+#include <cmath>
 #include <atomic>
 #include <cstring>
 #include <mutex>
@@ -231,6 +232,20 @@ static void fill_sync(Comm* c, SyncArgs& sy, const CallRef& call) {
 
 static int contiguous_rows(const pk_tensor* t) { return t->strides[0] == t->shape[1]; }
 
+// Default communicator SMs of the inter-SM AG-GEMM: enough TMA-driven SMs to
+// pull the (n-1)/n remote rows within the GEMM's own time, +30 % margin —
+// per-SM rate from hwmodel.py's B200 constants (669 GB/s saturating at 15
+// SMs), GEMM at a sustained 1.4 PF/s. 16 at n = 8 (S = 16384), 8 at n = 4,
+// 4 at n = 2, instead of 16 everywhere.
+static int ag_default_comm_sms(int64_t M, int64_t n_loc, int64_t K, int world, int num_sms) {
+  const double remote = (double)(world - 1) / world * (double)M * K * 2;
+  const double t_gemm = 2.0 * (double)M * n_loc * K / 1.4e15;
+  const double per_sm = 669e9 / 15;
+  int k = (int)std::ceil(1.3 * remote / (t_gemm * per_sm));
+  k = (k + 1) & ~1;                                    // whole CTA pairs
+  return std::max(2, std::min(k, std::min(16, num_sms / 8)));
+}
+
 int ag_gemm(Comm* c, const pk_tensor* A, const pk_tensor* B, pk_tensor* C, pk_tensor* AG,
             const pk_sched* sched, cudaStream_t st) {
   int64_t m_loc, K, ldA, n_loc, Kb, ldB, Mc, Nc, ldC;
@@ -255,9 +270,10 @@ int ag_gemm(Comm* c, const pk_tensor* A, const pk_tensor* B, pk_tensor* C, pk_te
     if (AG) PK_CUDA(cudaMemcpy2DAsync(AG->ptr, K * 2, A->ptr, ldA * 2, K * 2, m_loc, cudaMemcpyDeviceToDevice, st));
     return PK_OK;
   }
+  const int def_comm = ag_default_comm_sms(M, n_loc, K, n, c->num_sms);
   // compute pairs: all of this rank's SMs less the communicator share (as below)
   const int64_t ag_pairs = std::max(1, (sched && sched->num_sms > 0 ? std::min(sched->num_sms, c->num_sms) : c->num_sms) / 2 -
-                                           ((sched && sched->num_comm_sms > 0) ? sched->num_comm_sms : 16) / 2);
+                                           ((sched && sched->num_comm_sms > 0) ? sched->num_comm_sms : def_comm) / 2);
   const Variant v = pick_variant(m_loc, K, sched, false, M, n_loc, ag_pairs, true);
   const int cg = v.cg;
   const int tile_m = 128 * v.am * cg;
@@ -293,7 +309,7 @@ int ag_gemm(Comm* c, const pk_tensor* A, const pk_tensor* B, pk_tensor* C, pk_te
     for (int r = 0; r < n; ++r) PK_TRY(tmap_a(&args.tmap_a[r], shard[r], m_loc, K, K, v.am));
     args.sync_ready_before_load = 1;
   } else {
-    const int comm_sms = (sched && sched->num_comm_sms > 0) ? sched->num_comm_sms : std::max(2, std::min(16, c->num_sms / 8));
+    const int comm_sms = (sched && sched->num_comm_sms > 0) ? sched->num_comm_sms : def_comm;
     comm_clusters = std::max(1, comm_sms / cg);
     // An emulated rank owns only num_sms/world SMs: scale the communicator
     // share down with it instead of starving the GEMM.
