@@ -97,19 +97,45 @@ int check_matrix(const pk_tensor* t, const char* name, int dtype, int64_t* rows,
 int make_tmap_2d(CUtensorMap* map, const void* ptr, CUtensorMapDataType dt, int elem_bytes,
                  int64_t rows, int64_t cols, int64_t ld, int box_rows, int box_cols,
                  CUtensorMapSwizzle swz) {
+  // Encoded maps are cached per thread (direct-mapped on the key): repeated
+  // calls on the same tensors — every step of a layer — skip the driver encode.
+  struct Key {
+    const void* ptr;
+    int64_t rows, cols, ld;
+    int dt, elem_bytes, box_rows, box_cols, swz, promo;
+    bool operator==(const Key& o) const {
+      return ptr == o.ptr && rows == o.rows && cols == o.cols && ld == o.ld && dt == o.dt &&
+             elem_bytes == o.elem_bytes && box_rows == o.box_rows && box_cols == o.box_cols && swz == o.swz &&
+             promo == o.promo;
+    }
+  };
+  struct Entry { Key key; CUtensorMap map; bool valid = false; };
+  constexpr int kSlots = 64;
+  thread_local Entry cache[kSlots];
+  CUtensorMapL2promotion promo = CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
+  if (const char* e = getenv("PK_L2PROMO")) promo = (CUtensorMapL2promotion)atoi(e);   // tuning hook
+  const Key key{ptr, rows, cols, ld, (int)dt, elem_bytes, box_rows, box_cols, (int)swz, (int)promo};
+  const size_t h = (reinterpret_cast<uintptr_t>(ptr) >> 8) ^ (size_t)rows * 31 ^ (size_t)cols * 131 ^
+                   (size_t)box_rows * 7 ^ (size_t)box_cols * 17 ^ (size_t)ld * 3;
+  Entry& slot = cache[h % kSlots];
+  if (slot.valid && slot.key == key) {
+    *map = slot.map;
+    return PK_OK;
+  }
   const Driver* d;
   PK_TRY(driver(&d));
   cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
   cuuint64_t strides[1] = {(cuuint64_t)(ld * elem_bytes)};
   cuuint32_t box[2] = {(cuuint32_t)box_cols, (cuuint32_t)box_rows};
   cuuint32_t estr[2] = {1, 1};
-  CUtensorMapL2promotion promo = CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
-  if (const char* e = getenv("PK_L2PROMO")) promo = (CUtensorMapL2promotion)atoi(e);   // tuning hook
   CUresult r = d->tensorMapEncodeTiled(map, dt, 2, const_cast<void*>(ptr), dims, strides, box, estr,
                                        CU_TENSOR_MAP_INTERLEAVE_NONE, swz, promo, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS)
     return fail(PK_ERR_INVALID, "cuTensorMapEncodeTiled failed (%d): rows=%lld cols=%lld ld=%lld box=%dx%d",
                 (int)r, (long long)rows, (long long)cols, (long long)ld, box_rows, box_cols);
+  slot.key = key;
+  slot.map = *map;
+  slot.valid = true;
   return PK_OK;
 }
 
