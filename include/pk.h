@@ -141,7 +141,9 @@ PK_API int pk_gemm(const pk_tensor* a, const pk_tensor* b, pk_tensor* c,
 
 /* AG-GEMM: C_r[M, N/n] = AllGather_rows(A_r[M/n, K]) . B_r[N/n, K]^T.
  * a_gathered (nullable): if given, receives the rank-major gathered A[M,K]
- * (the reference's `ag` layout, workloads.py:603-609). */
+ * (the reference's `ag` layout, workloads.py:603-609); the communicator CTAs
+ * write it inside the kernel, so a call with a_gathered always runs the
+ * inter-SM schedule. */
 PK_API int pk_ag_gemm(pk_comm* comm, const pk_tensor* a_shard, const pk_tensor* b,
                       pk_tensor* c, pk_tensor* a_gathered, const pk_sched* sched, void* stream);
 
@@ -158,7 +160,9 @@ PK_API int pk_gemm_rs(pk_comm* comm, const pk_tensor* a, const pk_tensor* b,
 PK_API int pk_gemm_ar(pk_comm* comm, const pk_tensor* a, const pk_tensor* b, pk_tensor* out,
                       const pk_sched* sched, void* stream);
 
-/* In-place all-reduce of x (bf16 or f32, contiguous) over all ranks. */
+/* In-place all-reduce of x (bf16 or f32, contiguous) over all ranks. A
+ * world-1 call is the identity and launches nothing unless `sched` is given
+ * (then the one-rank kernel runs). */
 PK_API int pk_all_reduce(pk_comm* comm, pk_tensor* x, int op, const pk_sched* sched, void* stream);
 /* Design-overhead ablation (OverheadConfig, engine.py:49-60): the P2P sum
  * all-reduce of a symmetric x with library-style overheads switched on.
@@ -183,8 +187,10 @@ PK_API int pk_attn_fwd(const pk_tensor* q, const pk_tensor* k, const pk_tensor* 
 /* Expert-parallel dispatch: x [T, H] bf16, topk_idx [T, k] int32 (expert ids);
  * expert e lives on rank e % n (workloads.py:802). Tokens are placed on their
  * owner in slots sorted by (src_rank, token, k) (workloads.py:821-832).
- * recv [cap, H] bf16 receives rows; recv_src [cap] int32 (src*T*k + tok*k + j)
- * — or [cap, 2] to also receive each row's local expert (expert / n) — and
+ * recv [cap, H] bf16 receives rows; recv_src [cap] int32 ((T_<src + tok)*k + j,
+ * T_<src = tokens held by the ranks below src, i.e. src*T*k + tok*k + j when
+ * every rank holds T tokens) — or [cap, 2] to also receive each row's local
+ * expert (expert / n) — and
  * *recv_count (device int32) describe them. */
 PK_API int pk_moe_dispatch(pk_comm* comm, const pk_tensor* x, const pk_tensor* topk_idx,
                            int num_experts, pk_tensor* recv, pk_tensor* recv_src,

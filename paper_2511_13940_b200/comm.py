@@ -88,6 +88,7 @@ class Comm:
         check(lib.pk_comm_has_multicast(handle, ctypes.byref(mc)), "comm_has_multicast")
         self.has_multicast = bool(mc.value)
         self._pgls: list[Pgl] = []
+        self._defaults: dict = {}       # default symmetric outputs of the ops, per (use, shape, dtype)
         self._keep = keepalive
         self.is_local_group = False
         n = ctypes.c_int()
@@ -127,6 +128,20 @@ class Comm:
         nbytes = max(16, numel * torch.empty((), dtype=dtype).element_size())
         return self.pgl(nbytes, multicast).tensor(shape, dtype)
 
+    def default_buffer(self, use: str, shape, dtype=torch.bfloat16, multicast: bool = False) -> torch.Tensor:
+        """The symmetric buffer an op writes when the caller passes no output:
+        one per (use, shape, dtype), reused by every later call of that shape
+        (like a collective library's registered buffers) instead of a new PGL
+        per call. A result kept across calls must be copied or given as out=.
+        Must be requested in the same order on every rank (allocation is
+        collective the first time)."""
+        key = (use, tuple(int(x) for x in shape), dtype, bool(multicast))
+        t = self._defaults.get(key)
+        if t is None:
+            t = self.empty(shape, dtype, multicast)
+            self._defaults[key] = t
+        return t
+
     # ------------------------------------------------------------------ misc
     def set_timeout(self, seconds: float):
         check(_lib.load().pk_comm_set_timeout(self._h, ctypes.c_uint64(int(seconds * 1e9))), "set_timeout")
@@ -152,6 +167,7 @@ class Comm:
             for p in self._pgls:
                 p.free()
             self._pgls.clear()
+            self._defaults.clear()
             _lib.load().pk_comm_destroy(self._h)
             self._h = None
 

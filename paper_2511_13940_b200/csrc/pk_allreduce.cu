@@ -359,7 +359,10 @@ int all_reduce(Comm* c, pk_tensor* x, int op, const pk_sched* sched, cudaStream_
   }
   const size_t bytes = (size_t)numel * dtype_bytes(x->dtype);
   if (bytes % 16) return fail(PK_ERR_INVALID, "all_reduce: size must be a multiple of 16 bytes (got %zu)", bytes);
-  if (bytes == 0 || c->world == 1) return PK_OK;
+  // A world-1 all-reduce is the identity: no launch, unless a schedule is
+  // given explicitly (then the one-rank kernel runs with its own barriers,
+  // which exercises the path on a single GPU).
+  if (bytes == 0 || (c->world == 1 && !sched)) return PK_OK;
 
   void* peers[kMaxRanks];
   void* mc = nullptr;

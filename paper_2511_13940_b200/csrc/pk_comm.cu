@@ -752,6 +752,7 @@ PK_API int pk_comm_destroy(pk_comm* c) {
   if (c->attn.part) cudaFree(c->attn.part);
   if (c->attn.count) cudaFree(c->attn.count);
   if (c->ablate_stage) cudaFree(c->ablate_stage);
+  if (c->moe_idx) cudaFree(c->moe_idx);
   for (auto& m : c->pending) if (m.fd >= 0) ::close(m.fd);
   LocalGroup* g = c->group;
   delete c;

@@ -155,6 +155,8 @@ struct Comm {
   std::vector<Pgl*> retired;         // outgrown scratch PGLs (local groups free them at destroy)
   cudaStream_t side = nullptr;       // side stream for copy-engine staging (ring attention)
   AttnScratch attn;                  // ring attention: stream-K partials + per-item counters
+  void* moe_idx = nullptr;           // MoE rank-local index scratch (count_done | slot_of | chunk counts)
+  size_t moe_idx_bytes = 0;
   void* ablate_stage = nullptr;      // all_reduce_ablate staging channels (local)
   size_t ablate_stage_bytes = 0;
   uint32_t ablate_calls = 0;         // handshake round counter (req/ack counters only grow)

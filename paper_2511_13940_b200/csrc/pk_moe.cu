@@ -37,6 +37,7 @@ namespace pk {
 
 constexpr int kMoeMaxKeys = 1024;      // experts (expert-major layout) or ranks
 constexpr int kMoeTile = 256;          // expert segment padding = the grouped GEMM's pair tile
+constexpr int kTblTokens = kMaxRanks * kMoeMaxKeys;   // table words after the counts: T of every rank
 
 struct MoeSync {
   uint32_t* ready_local;
@@ -168,6 +169,7 @@ __device__ __forceinline__ void moe_count_phase(const MoeArgs& a, int32_t* cnt, 
     }
     if (lane < a.n) a.table_peer[lane][a.rank * a.nkeys + q] = run;
   }
+  if (tid < a.n) a.table_peer[tid][kTblTokens + a.rank] = a.T;   // token count, for the id prefix
   __syncthreads();
   if (tid == 0) {
     *a.count_done = 0;                                // re-armed for the next call
@@ -215,6 +217,11 @@ __global__ void __launch_bounds__(kDispatchThreads) moe_dispatch_kernel(const __
   }
   __syncthreads();
   if (!ok_flag) return;
+  // global id of this rank's first token: tokens of the lower ranks (ragged
+  // T allowed), so recv_src names the token's position in the rank-major
+  // concatenation of every rank's tokens
+  int tok_prefix = 0;
+  for (int d = 0; d < a.rank; ++d) tok_prefix += ld_volatile_s32(a.table_local + kTblTokens + d);
   // ---- per-key base slots
   if (a.layout == 0) {
     for (int q = tid; q < a.nkeys; q += blockDim.x) {
@@ -396,7 +403,7 @@ __global__ void __launch_bounds__(kDispatchThreads) moe_dispatch_kernel(const __
       const int slot = sslot[le];
       if (slot < 0) continue;
       int32_t* rs = a.recv_src_peer[sown[le]];
-      rs[(long long)slot * a.recv_src_cols] = (a.rank * a.T + w0) * a.k + le;
+      rs[(long long)slot * a.recv_src_cols] = (tok_prefix + w0) * a.k + le;
       if (a.recv_src_cols == 2) rs[(long long)slot * 2 + 1] = sexp[le];   // local expert id
     }
     __syncthreads();
@@ -516,12 +523,13 @@ static void fill_moe_sync(Comm* c, MoeSync& s, const CallRef& call) {
   s.timeout_ns = c->timeout_ns;
 }
 
-enum { kScratchMoeTable = 4, kScratchMoeIdx = 5, kScratchMoeY = 6 };
+enum { kScratchMoeTable = 4, kScratchMoeY = 6 };
 
 // Routing checks, chunking and scratch shared by dispatch and combine. The
 // chunking and the per-entry slot table (slot_of) persist from a dispatch to
 // the next combine on the same comm.
-static int moe_common(Comm* c, const pk_tensor* topk, int num_experts, int layout, MoeArgs& a, int* T, int* K) {
+static int moe_common(Comm* c, const pk_tensor* topk, int num_experts, int layout, MoeArgs& a, int* T, int* K,
+                      cudaStream_t st) {
   if (!topk || topk->dtype != PK_I32 || topk->ndim != 2 ||
       (topk->shape[0] != 0 && (topk->strides[1] != 1 || topk->strides[0] != topk->shape[1])))
     return fail(PK_ERR_INVALID, "moe: topk_idx must be a contiguous [T, k] int32 tensor");
@@ -544,7 +552,7 @@ static int moe_common(Comm* c, const pk_tensor* topk, int num_experts, int layou
   a.layout = layout;
   a.nkeys = layout ? num_experts : c->world;
   Pgl* tbl;
-  PK_TRY(comm_scratch(c, kScratchMoeTable, sizeof(int32_t) * kMaxRanks * kMoeMaxKeys, &tbl));
+  PK_TRY(comm_scratch(c, kScratchMoeTable, sizeof(int32_t) * (kTblTokens + kMaxRanks), &tbl));
   a.table_local = static_cast<int32_t*>(tbl->local);
   for (int r = 0; r < c->world; ++r) a.table_peer[r] = static_cast<int32_t*>(tbl->peers[r]);
   // chunking shared by moe_count and moe_dispatch (one CTA per chunk)
@@ -557,11 +565,19 @@ static int moe_common(Comm* c, const pk_tensor* topk, int num_experts, int layou
   a.grid = std::max(1, (*T + a.tpc - 1) / a.tpc);
   // scratch: [count_done | pad to 256 B][slot_of T*k][chunk_counts nkeys x G]
   // (slot_of first: a combine finds it where the dispatch with the same
-  // routing left it, whatever that dispatch's layout)
-  Pgl* idx;
-  PK_TRY(comm_scratch(c, kScratchMoeIdx,
-                      256 + sizeof(int32_t) * ((size_t)(*T) * (*K) + (size_t)a.grid * a.nkeys), &idx));
-  uint8_t* base = static_cast<uint8_t*>(idx->local);
+  // routing left it, whatever that dispatch's layout). Only this rank touches
+  // it and its size follows this rank's T, so it is a rank-local,
+  // stream-ordered allocation — not a collective symmetric one (ranks with
+  // different token counts would otherwise grow it on some ranks only).
+  const size_t idx_bytes = 256 + sizeof(int32_t) * ((size_t)(*T) * (*K) + (size_t)a.grid * a.nkeys);
+  if (c->moe_idx_bytes < idx_bytes) {
+    const size_t want = std::max(idx_bytes, std::max((size_t)2 << 20, 2 * c->moe_idx_bytes));
+    if (c->moe_idx) PK_CUDA(cudaFreeAsync(c->moe_idx, st));
+    PK_CUDA(cudaMallocAsync(&c->moe_idx, want, st));
+    PK_CUDA(cudaMemsetAsync(c->moe_idx, 0, want, st));
+    c->moe_idx_bytes = want;
+  }
+  uint8_t* base = static_cast<uint8_t*>(c->moe_idx);
   a.count_done = reinterpret_cast<uint32_t*>(base);
   a.slot_of = reinterpret_cast<int32_t*>(base + 256);
   a.chunk_counts = a.slot_of + (size_t)(*T) * (*K);
@@ -572,7 +588,7 @@ int moe_dispatch(Comm* c, const pk_tensor* x, const pk_tensor* topk, int num_exp
                  pk_tensor* recv, pk_tensor* recv_src, pk_tensor* recv_count, pk_tensor* plan, cudaStream_t st) {
   int T, K;
   MoeArgs a;
-  PK_TRY(moe_common(c, topk, num_experts, layout, a, &T, &K));
+  PK_TRY(moe_common(c, topk, num_experts, layout, a, &T, &K, st));
   if (mech != PK_MECH_AUTO && mech != PK_MECH_REG && mech != PK_MECH_TMA) return fail(PK_ERR_INVALID, "moe_dispatch: unknown mechanism %d", mech);
   a.mech = mech;
   int64_t xr, H, xld;
@@ -640,7 +656,7 @@ int moe_combine(Comm* c, const pk_tensor* y, const pk_tensor* topk, const pk_ten
                 pk_tensor* out, cudaStream_t st) {
   int T, K;
   MoeArgs a;
-  PK_TRY(moe_common(c, topk, num_experts, 0, a, &T, &K));   // slot_of: written by the last dispatch
+  PK_TRY(moe_common(c, topk, num_experts, 0, a, &T, &K, st));   // slot_of: written by the last dispatch
   int64_t cap, H, yld, orows, H2, old;
   PK_TRY(check_matrix(y, "y", PK_BF16, &cap, &H, &yld));
   PK_TRY(check_matrix(out, "out", PK_BF16, &orows, &H2, &old));

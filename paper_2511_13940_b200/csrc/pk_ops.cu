@@ -281,6 +281,10 @@ int ag_gemm(Comm* c, const pk_tensor* A, const pk_tensor* B, pk_tensor* C, pk_te
   int mode = sched ? sched->mode : PK_SCHED_AUTO;
   if (mode == PK_SCHED_AUTO) mode = (n_loc <= 256 && !AG) ? PK_INTRA_SM : PK_INTER_SM;
   if (mode == PK_HYBRID) mode = PK_INTER_SM;   // HYBRID behaves like INTER_SM
+  // The gathered rows are materialised by the communicator CTAs, inside the
+  // kernel and before this rank's done signal; an intra-SM launch would have to
+  // copy peer shards after it (racing the peers' next writes into them).
+  if (AG && mode == PK_INTRA_SM) mode = PK_INTER_SM;
 
   // Shard of every rank: zero-copy if the caller's tensor is symmetric.
   void* shard[kMaxRanks];
@@ -347,12 +351,6 @@ int ag_gemm(Comm* c, const pk_tensor* A, const pk_tensor* B, pk_tensor* C, pk_te
   PK_TRY(begin_call(c, 1, 1, (uint32_t)(compute_clusters * cg * 4 * v.am), st, &call));
   fill_sync(c, args.sync, call);
   PK_TRY(launch_gemm_variant(v, EPI_STORE, args, (compute_clusters + comm_clusters) * cg, st));
-  if (AG && mode == PK_INTRA_SM) {
-    // intra-SM never materialises the gathered rows; copy them on demand
-    for (int r = 0; r < n; ++r)
-      PK_CUDA(cudaMemcpyAsync(static_cast<char*>(AG->ptr) + (size_t)r * shard_bytes, shard[r], shard_bytes,
-                              cudaMemcpyDeviceToDevice, st));
-  }
   return PK_OK;
 }
 
@@ -374,7 +372,7 @@ static int gemm_rs_inter(Comm* c, const pk_tensor* A, const pk_tensor* B, pk_ten
   if (m_own % 256) return fail(PK_ERR_INVALID, "gemm_rs (inter-SM): need (M/n) %% 256 == 0");
   const Variant v{2, 1};
   const int tiles = (int)((M / 256) * (N / 256));
-  if (tiles > (kSyncBytes / 4) - kSyncArTiles) return fail(PK_ERR_INVALID, "gemm_rs: too many tiles");
+  if (tiles > kSyncCall - kSyncArTiles) return fail(PK_ERR_INVALID, "gemm_rs: too many tiles");
   Pgl* part;
   PK_TRY(comm_scratch(c, 10, (size_t)M * N * 2, &part, PK_PGL_MULTICAST));
   GemmArgs args;
@@ -488,7 +486,7 @@ int gemm_ar(Comm* c, const pk_tensor* A, const pk_tensor* B, pk_tensor* O, const
   const Variant v{2, 1};
   const int tile_m = 256;
   const int tiles = (int)((M / tile_m) * (N / 256));
-  if (tiles > (kSyncBytes / 4) - kSyncArTiles) return fail(PK_ERR_INVALID, "gemm_ar: too many tiles");
+  if (tiles > kSyncCall - kSyncArTiles) return fail(PK_ERR_INVALID, "gemm_ar: too many tiles");
   // Output of every rank (zero-copy when `out` is symmetric; NVLS when it has a multicast VA).
   void* dst[kMaxRanks];
   void* mc = nullptr;

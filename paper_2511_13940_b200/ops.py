@@ -105,10 +105,13 @@ def gemm_all_reduce(comm, a: torch.Tensor, b: torch.Tensor, out: torch.Tensor | 
     """Fused GEMM + all-reduce: out = sum_d A_d @ B_d^T on every rank (GemmArPlan,
     workloads.py:415-546). Tiles are reduced by the owner's
     communicator SMs as soon as all partials landed (NVLS when `out` is a
-    multicast symmetric tensor, P2P otherwise)."""
+    multicast symmetric tensor, P2P otherwise). Without `out` the result lands
+    in the communicator's cached symmetric buffer for this shape
+    (`Comm.default_buffer`), which the next call of the same shape reuses."""
     _require_cuda(a, b)
     if out is None:
-        out = comm.empty((a.shape[0], b.shape[0]), torch.bfloat16, multicast=comm.has_multicast)
+        out = comm.default_buffer("gemm_ar.out", (a.shape[0], b.shape[0]), torch.bfloat16,
+                                  multicast=comm.has_multicast)
     lib = _lib.load()
     da, db, do = _lib.tensor_desc(a), _lib.tensor_desc(b), _lib.tensor_desc(out)
     if schedule is None and comm.world > 1:
@@ -188,8 +191,12 @@ def moe_dispatch(comm, x: torch.Tensor, topk_idx: torch.Tensor, num_experts: int
     (recv [cap, H] bf16, recv_src [cap] int32, recv_count [1] int32 on device):
     on the owner, slot s holds the token whose (src_rank, token, k) triple is
     the s-th in sorted order (workloads.py:821-832); recv_src[s] =
-    (src_rank * T + token) * k + j (recv_src [cap, 2]: column 1 = the row's local
-    expert, expert // n). recv/recv_src are symmetric (Comm.empty).
+    (T_below(src_rank) + token) * k + j, T_below = tokens held by the lower
+    ranks — (src_rank * T + token) * k + j when every rank holds T tokens, and
+    still decodable with ragged T (recv_src [cap, 2]: column 1 = the row's
+    local expert, expert // n). recv/recv_src are symmetric; without `recv`
+    they are the communicator's cached buffers for this capacity
+    (`Comm.default_buffer`), reused by the next dispatch of the same shape.
 
     layout="expert": rows are grouped by local expert instead, one segment per
     expert padded to 256 rows, (src, token, k) order inside each segment
@@ -206,7 +213,8 @@ def moe_dispatch(comm, x: torch.Tensor, topk_idx: torch.Tensor, num_experts: int
     if capacity is None:
         capacity = moe_capacity(T, k, comm.world, x.shape[1], local_experts)
     if recv is None:
-        recv = (comm.empty((capacity, x.shape[1]), torch.bfloat16), comm.empty((capacity, 2), torch.int32))
+        recv = (comm.default_buffer("moe.recv", (capacity, x.shape[1]), torch.bfloat16),
+                comm.default_buffer("moe.recv_src", (capacity, 2), torch.int32))
     recv_rows, recv_src = recv
     count = torch.empty(1, dtype=torch.int32, device=x.device)
     plan = torch.empty(2 + recv_rows.shape[0] // 256, dtype=torch.int32, device=x.device) if lay else None

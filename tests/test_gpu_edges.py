@@ -76,11 +76,16 @@ def test_moe_ragged_token_counts(Ts):
     cap = max(256, pk.moe_capacity(max(Ts), K, world, H))
     bufs = [(c.empty((cap, H)), c.empty((cap, 2), torch.int32)) for c in comms]
     outs = run_ranks(comms, lambda r, c, s: pk.moe_dispatch(c, x[r], topk[r], E, recv=bufs[r], stream=s))
+    prefix = np.concatenate([[0], np.cumsum(Ts)])            # tokens held by the lower ranks
     for o in range(world):
-        rows = [toks[d][t] for d in range(world) for t in range(Ts[d]) for j in range(K) if routes[d][t, j] % world == o]
+        trip = [(d, t, j) for d in range(world) for t in range(Ts[d]) for j in range(K) if routes[d][t, j] % world == o]
+        rows = [toks[d][t] for (d, t, j) in trip]
         assert int(outs[o][2].item()) == len(rows)
         if rows:
             assert np.array_equal(outs[o][0][:len(rows)].float().cpu().numpy(), np.stack(rows))
+            # ids stay decodable with ragged T: (T_below(src) + token) * K + j
+            ids = outs[o][1][:len(rows), 0].cpu().numpy()
+            assert ids.tolist() == [int((prefix[d] + t) * K + j) for (d, t, j) in trip]
     w = [torch.ones(t, K, device="cuda") for t in Ts]
     comb = run_ranks(comms, lambda r, c, s: pk.moe_combine(c, outs[r][0], topk[r], w[r], E, stream=s))
     for r in range(world):
