@@ -225,6 +225,31 @@ def _agree_uid(dist, rank: int, world: int) -> str:
     return uid[0]
 
 
+
+class Watchdog:
+    """If the optional legs after the headline measurement hang (a peer that
+    never signals, a wedged collective), print what was measured so far and
+    exit instead of losing the run."""
+
+    def __init__(self, seconds: float, fire):
+        self.t = threading.Timer(seconds, fire)
+        self.t.daemon = True
+
+    def start(self):
+        self.t.start()
+
+    def cancel(self):
+        self.t.cancel()
+
+
+def _leg(line: dict, key: str, fn):
+    """Run one optional leg; its failure is recorded, never fatal to the line."""
+    try:
+        line[key] = fn()
+    except Exception as e:                                  # noqa: BLE001
+        line[key] = {"error": f"{type(e).__name__}: {e}"[:400]}
+
+
 # ----------------------------------------------------------------------------- pk arm
 def main():
     args = parse()
@@ -300,6 +325,13 @@ def main():
         t = torch.tensor([x], device=dev if backend == "nccl" else "cpu", dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
+
+    def max_vec(xs: list) -> list:
+        if world == 1:
+            return list(xs)
+        t = torch.tensor(xs, device=dev if backend == "nccl" else "cpu", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return t.tolist()
 
     for _ in range(args.warmup):
         step()
@@ -457,22 +489,180 @@ def main():
                "sample": "measured on rank 0 at N=1 only"}
 
     comm.check()
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": n, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "bf16", "data": "synthetic (torch.randn*0.1, seeded per rank)",
+        "config": {"workload": f"ag_gemm+gemm_rs M=N=K={S} (one AG-GEMM then one GEMM-RS per step)",
+                   "size": S, "parallelism": f"tp{n}", "global_batch": S,
+                   "l2": l2_note(S, n)},
+        "e2e": e2e, "gpu_launches": 2 * args.steps, "roofline": roofline, "cpu_baseline": cpu,
+        "nccl_cublas": base, "clocks": clk, "nvls": bool(comm.has_multicast),
+    }
+    if n > 1:
+        # per-op NVLink rate: (n-1)/n of the S x S bf16 operand crosses the
+        # links per launch (A rows gathered in, or partial rows reduced out)
+        link_bytes = (n - 1) / n * S * S * 2
+        ag_max, rs_max = max_over_ranks(ag_ms), max_over_ranks(rs_ms)
+        line["link"] = {"bytes_per_launch": link_bytes,
+                        "ag_gemm_gbs": link_bytes / (ag_max / 1e3) / 1e9,
+                        "gemm_rs_gbs": link_bytes / (rs_max / 1e3) / 1e9,
+                        "ag_gemm_frac_of_900": link_bytes / (ag_max / 1e3) / 900e9,
+                        "gemm_rs_frac_of_900": link_bytes / (rs_max / 1e3) / 900e9,
+                        "note": "algorithmic link bytes / device time of the fused launch (max over ranks)"}
+
+    # ---------------------------------------------------------------- optional legs (never lose the line)
+    def emit_and_exit():
+        if rank == 0:
+            line["watchdog"] = "optional legs did not finish within the limit; line printed as measured so far"
+            print(json.dumps(line), flush=True)
+        os._exit(0)
+    dog = Watchdog(float(os.environ.get("PK_BENCH_LEG_LIMIT_S", "420")), emit_and_exit)
+    dog.start()
+    _leg(line, "parity", lambda: parity_check(pk, comm, dist, dev, rank, n, S, a_ag, b_ag, c_ag, a_rs, b_rs, o_rs,
+                                              max_over_ranks))
+    if n > 1:
+        _leg(line, "all_reduce", lambda: all_reduce_leg(pk, comm, dist, dev, n, barrier, max_over_ranks,
+                                                        backend == "nccl"))
+    else:
+        line["all_reduce"] = {"skipped": "world 1: an all-reduce is the identity"}
+    _leg(line, "nvlink", lambda: nvlink_leg(comm, n, barrier, max_vec))
+    dog.cancel()
+    comm.check()
+    ok = not (isinstance(line.get("parity"), dict) and line["parity"].get("ok") is False)
     if rank == 0:
-        line = {
-            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": n, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
-            "vs_baseline": None, "dtype": "bf16", "data": "synthetic (torch.randn*0.1, seeded per rank)",
-            "config": {"workload": f"ag_gemm+gemm_rs M=N=K={S} (one AG-GEMM then one GEMM-RS per step)",
-                       "size": S, "parallelism": f"tp{n}", "global_batch": S,
-                       "l2": l2_note(S, n)},
-            "e2e": e2e, "gpu_launches": 2 * args.steps, "roofline": roofline, "cpu_baseline": cpu,
-            "nccl_cublas": base, "clocks": clk,
-        }
         print(json.dumps(line), flush=True)
     comm.destroy()
     if world > 1:
         dist.destroy_process_group()
-    return 0
+    return 0 if ok else 1
+
+
+# ----------------------------------------------------------------------------- optional legs
+def parity_check(pk, comm, dist, dev, rank, n, S, a_ag, b_ag, c_ag, a_rs, b_rs, o_rs, max_over_ranks) -> dict:
+    """Exact integer-data parity of the two timed ops at the timed size, on
+    every rank, against an independent path: NCCL all-gather / reduce-scatter
+    plus an fp32 torch GEMM (integer sums below 2^24 are exact in fp32, so the
+    bf16-rounded results must match bit for bit). GEMM-RS inputs are nonzero
+    in only 256/n columns of K, so every partial and every running sum of the
+    cross-rank bf16 reduce-add stays within bf16's exact integers (|x| <= 256)."""
+    import torch
+    g = torch.Generator(device=dev)
+    g.manual_seed(4321 + rank)
+
+    def ints(shape, lo, hi):
+        return torch.randint(lo, hi + 1, shape, device=dev, generator=g).to(torch.bfloat16)
+
+    out = {"inputs": "integers: AG-GEMM A, B in [-2, 2]; GEMM-RS A, B in [-1, 1], A nonzero in 256/n K columns",
+           "reference": "NCCL all_gather / reduce_scatter + fp32 torch.matmul, rounded to bf16"}
+    a_ag.copy_(ints(tuple(a_ag.shape), -2, 2))
+    b_ag.copy_(ints(tuple(b_ag.shape), -2, 2))
+    pk.all_gather_gemm(comm, a_ag, b_ag, out=c_ag)
+    nccl = dist.is_initialized() and dist.get_backend() == "nccl"
+    if n > 1 and nccl:
+        full = torch.empty(S, S, device=dev, dtype=torch.bfloat16)
+        dist.all_gather_into_tensor(full, a_ag)
+    elif n > 1:                                   # gloo test plumbing: gather on the host
+        parts = [torch.empty(tuple(a_ag.shape), dtype=torch.bfloat16) for _ in range(n)]
+        dist.all_gather(parts, a_ag.cpu())
+        full = torch.cat(parts).to(dev)
+    else:
+        full = a_ag
+    ref = (full.float() @ b_ag.float().t()).to(torch.bfloat16)
+    del full
+    bad_ag = int((c_ag != ref).sum().item())
+    del ref
+    k_loc = a_rs.shape[1]
+    a_rs.zero_()
+    a_rs[:, :max(1, min(k_loc, 256 // n))] = ints((S, max(1, min(k_loc, 256 // n))), -1, 1)
+    b_rs.copy_(ints(tuple(b_rs.shape), -1, 1))
+    pk.gemm_reduce_scatter(comm, a_rs, b_rs, out=o_rs)
+    part = a_rs.float() @ b_rs.float().t()
+    if n > 1 and nccl:
+        red = torch.empty(S // n, S, device=dev, dtype=torch.float32)
+        dist.reduce_scatter_tensor(red, part)
+    elif n > 1:
+        host = part.cpu()
+        dist.all_reduce(host)
+        red = host[rank * (S // n):(rank + 1) * (S // n)].to(dev)
+    else:
+        red = part
+    bad_rs = int((o_rs != red.to(torch.bfloat16)).sum().item())
+    del part, red
+    torch.cuda.synchronize()
+    comm.check()
+    bad = max_over_ranks(float(bad_ag + bad_rs))
+    bad_ag_all, bad_rs_all = max_over_ranks(float(bad_ag)), max_over_ranks(float(bad_rs))
+    out.update({"ag_gemm_mismatches": int(bad_ag_all), "gemm_rs_mismatches": int(bad_rs_all),
+                "elements_checked_per_rank": int(c_ag.numel() + o_rs.numel()), "ok": bad == 0})
+    return out
+
+
+def all_reduce_leg(pk, comm, dist, dev, n, barrier, max_over_ranks, with_nccl: bool) -> dict:
+    """NVLS (or P2P) all-reduce at 64 MiB and 1 GiB per rank, bf16, in a
+    symmetric (multicast when available) buffer; exactness checked on integer
+    data first; NCCL all_reduce of the same size alongside. algbw = bytes / t
+    (the NVLS roofline moves ~S per direction per GPU)."""
+    import torch
+    rank = comm.rank
+    res = {"path": "nvls (multimem.ld_reduce + multimem.st)" if comm.has_multicast else "p2p register ops",
+           "sizes": []}
+    cap = int(os.environ.get("PK_BENCH_AR_MAX_BYTES", str(1 << 30)))      # test hook: smaller sizes
+    for nbytes, iters in ((64 << 20, 20), (1 << 30, 5)):
+        if nbytes > cap:
+            continue
+        numel = nbytes // 2
+        x = comm.empty((numel,), torch.bfloat16, multicast=comm.has_multicast)
+        idx = torch.arange(numel, device=dev, dtype=torch.int32) % 17 - 8
+        x.copy_((idx + rank % 4).to(torch.bfloat16))
+        pk.all_reduce(comm, x)
+        exp = (idx * n + sum(r % 4 for r in range(n))).to(torch.bfloat16)
+        bad = max_over_ranks(float((x != exp).sum().item()))
+        del idx, exp
+        pk.all_reduce(comm, x)
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(iters):
+            pk.all_reduce(comm, x)
+        e1.record()
+        barrier()
+        comm.check()
+        t = max_over_ranks(e0.elapsed_time(e1) / iters) / 1e3
+        algbw = nbytes / t
+        ent = {"bytes_per_rank": nbytes, "ms": t * 1e3, "algbw_gbs": algbw / 1e9,
+               "busbw_gbs": algbw * 2 * (n - 1) / n / 1e9, "frac_of_900": algbw / 900e9,
+               "exact_on_integers": bad == 0, "iters": iters}
+        if with_nccl:
+            y = torch.zeros(numel, device=dev, dtype=torch.bfloat16)
+            dist.all_reduce(y)
+            barrier()
+            e0.record()
+            for _ in range(iters):
+                dist.all_reduce(y)
+            e1.record()
+            barrier()
+            tn = max_over_ranks(e0.elapsed_time(e1) / iters) / 1e3
+            ent["nccl_ms"] = tn * 1e3
+            ent["speedup_vs_nccl"] = tn / t
+            del y
+        res["sizes"].append(ent)
+        x._pk_pgl.free()
+        del x
+    return res
+
+
+def nvlink_leg(comm, n, barrier, max_vec) -> dict:
+    """Transfer-mechanism calibration (mechanisms.py / pk_mech_probe): GB/s
+    over message size and SM count for the copy engine, TMA, register ops and
+    multimem, every rank pushing to rank + 1 at once. One GPU: loopback only."""
+    from paper_2511_13940_b200 import mechanisms
+    if n == 1:
+        res = mechanisms.measure(comm, nbytes=64 << 20, quick=True, reps=2)
+        return {"skipped": "one GPU: no NVLink to measure", "loopback_peak_gbs": res["peak_gbs"],
+                "loopback_sms_to_saturate": res["sms_to_saturate"]}
+
+    return mechanisms.measure(comm, barrier, max_vec, nbytes=128 << 20, reps=3)
 
 
 if __name__ == "__main__":

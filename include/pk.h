@@ -15,6 +15,8 @@
  *                                         IPC/VMM/multicast setup FSMs
  *                                         (overlapsim/memsim.py:205-341,
  *                                         PAPER.md:796-859)
+ *   pk_setup_*                         <- SetupSession / advance_setup
+ *                                         (memsim.py:209-341)
  *   pk_pgl_alloc / pk_pgl_ptrs         <- allocate_pgl + attach_multicast
  *                                         (memsim.py:145-149, 333-341)
  *   pk_gemm                            <- the consumer role of LcscKernelSpec
@@ -36,6 +38,8 @@
  *                                         (primitives.py:211-288), self-test
  *   pk_gemm_ar                         <- GemmArPlan inter-SM (workloads.py:415-546)
  *   pk_ulysses_a2a                     <- UlyssesPlan (workloads.py:723-779)
+ *   pk_mech_probe                      <- the mechanism curves / select_mechanism
+ *                                         inputs (hwmodel.py:147-245), measured
  *   pk_all_gather / pk_reduce_scatter  <- AllGatherTdPlan / ReduceScatterTdPlan
  *   / pk_all_to_all                       / AllToAll4DPlan (workloads.py:875-1028)
  *
@@ -43,7 +47,8 @@
  * layer: PK_ERR_INVALID -> WorkloadError (workloads.py:62),
  * PK_ERR_CAPABILITY -> PrimitiveError (primitives.py:31),
  * PK_ERR_PROTOCOL -> ProtocolViolation (memsim.py:26),
- * PK_ERR_TIMEOUT -> DeadlockError (engine.py:35).
+ * PK_ERR_TIMEOUT -> DeadlockError (engine.py:35),
+ * PK_ERR_MEMORY -> MemSimError (memsim.py:22).
  */
 #ifndef PK_H_
 #define PK_H_
@@ -64,7 +69,8 @@ typedef enum {
   PK_ERR_PROTOCOL = 3,    /* setup step out of order                         */
   PK_ERR_TIMEOUT = 4,     /* a device-side wait() timed out (deadlock)       */
   PK_ERR_CUDA = 5,        /* CUDA runtime / driver failure                   */
-  PK_ERR_NOMEM = 6
+  PK_ERR_NOMEM = 6,
+  PK_ERR_MEMORY = 7       /* memory-layout rule (e.g. strict VMM granularity) */
 } pk_status;
 
 typedef enum { PK_BF16 = 0, PK_F32 = 1, PK_F16 = 2, PK_I32 = 3, PK_I64 = 4, PK_U8 = 5 } pk_dtype;
@@ -89,7 +95,12 @@ typedef struct {
   int32_t num_comm_sms;   /* communicator SMs when mode == PK_INTER_SM */
   int32_t stages;         /* pipeline stages (informational; compiled per config) */
   int32_t num_sms;        /* SMs the kernel may occupy (0 = all) */
+  uint32_t flags;         /* PK_SCHED_* option bits */
 } pk_sched;
+/* GEMM-RS (intra-SM): reduce-add fp32 partial tiles into fp32 sums on the
+ * owner and round to bf16 once (2x the link bytes of bf16 partials, which
+ * round once per rank in hardware order). */
+#define PK_SCHED_FP32_PARTIALS 1u
 
 typedef struct pk_comm pk_comm;   /* one rank's communicator */
 typedef struct pk_pgl pk_pgl;     /* one parallel global layout (symmetric buffer) */
@@ -111,6 +122,9 @@ PK_API int pk_comm_init_local(int world, int device, pk_comm** comms_out);
 PK_API int pk_comm_destroy(pk_comm* comm);
 PK_API int pk_comm_rank(const pk_comm* comm, int* rank, int* world);
 PK_API int pk_comm_has_multicast(const pk_comm* comm, int* out);
+/* 1 when every rank of a multi-process communicator runs on its own GPU (peer
+ * traffic crosses NVLink); 0 for local groups and ranks sharing a device. */
+PK_API int pk_comm_distinct_devices(const pk_comm* comm, int* out);
 /* Device-side timeout of every wait() in ns (default 10 s). */
 PK_API int pk_comm_set_timeout(pk_comm* comm, uint64_t ns);
 /* Read (and clear) the sticky device error code of the last calls:
@@ -126,6 +140,32 @@ PK_API int pk_debug_rendezvous(int rank, int world, const char* uid);
  * counter] (see pk_allreduce.cu mm_selftest_kernel). PK_ERR_CAPABILITY when
  * the PGL has no multicast VA. */
 PK_API int pk_debug_multimem(pk_comm* comm, pk_pgl* pgl, size_t nvec, void* stream);
+
+/* ---- memory-setup sessions (SetupSession, memsim.py:209-341) ------------- */
+/* Drive one buffer's IPC / VMM / multicast setup protocol step by step
+ * against the driver. Steps (pk_setup_advance) per mode, numbered as the
+ * reference's enums:
+ *   IPC:       0 get_mem_handle, 1 share_stub, 2 open_mem_handle
+ *   VMM:       0 create_physical, 1 export_handle, 2 transfer_handle_over_socket,
+ *              3 import_handle, 4 map_virtual
+ *   MULTICAST: 0 create_multicast_stub, 1 register_all_devices,
+ *              2 bind_each_device_memory, 3 export_stub, 4 transfer_stub,
+ *              5 import_stub, 6 map_virtual
+ * A step whose prerequisites are not done, or that was already taken, returns
+ * PK_ERR_PROTOCOL and changes nothing. The create step rounds `bytes` up to
+ * the driver's granularity (PK_ERR_MEMORY instead with
+ * PK_SETUP_STRICT_GRANULARITY). PK_SETUP_DRY checks the order only (no driver
+ * calls; comm may be NULL; 2 MiB granularity). Sockets are an in-process
+ * AF_UNIX pair; a live multicast session needs NVLS. */
+typedef enum { PK_SETUP_IPC = 0, PK_SETUP_VMM = 1, PK_SETUP_MULTICAST = 2 } pk_setup_mode;
+#define PK_SETUP_DRY 1u
+#define PK_SETUP_STRICT_GRANULARITY 2u
+typedef struct pk_setup pk_setup;
+PK_API int pk_setup_begin(pk_comm* comm, int mode, size_t bytes, uint32_t flags, pk_setup** out);
+PK_API int pk_setup_advance(pk_setup* setup, int step);
+/* done_mask bit i = step i taken; reserved_bytes = bytes rounded to the granularity */
+PK_API int pk_setup_state(const pk_setup* setup, uint32_t* done_mask, size_t* reserved_bytes, int* complete);
+PK_API int pk_setup_end(pk_setup* setup);
 
 /* ---- parallel global layouts --------------------------------------------- */
 PK_API int pk_pgl_alloc(pk_comm* comm, size_t bytes, uint32_t flags, pk_pgl** out);
@@ -203,7 +243,10 @@ typedef enum {
 } pk_moe_layout;
 /* Transfer mechanism (hwmodel.py select_mechanism, 211-245). AUTO resolves
  * to the policy's answer for row-sized messages, TMA (bulk copies). */
-typedef enum { PK_MECH_AUTO = 0, PK_MECH_REG = 1, PK_MECH_TMA = 2 } pk_mechanism;
+typedef enum { PK_MECH_AUTO = 0, PK_MECH_REG = 1, PK_MECH_TMA = 2,
+               PK_MECH_CE = 3,        /* copy engine (pk_mech_probe only) */
+               PK_MECH_MULTIMEM = 4   /* multimem.st through the multicast VA (pk_mech_probe only) */
+} pk_mechanism;
 /* Dispatch with an explicit layout and mechanism. For PK_MOE_EXPERT_MAJOR,
  * expert_plan (int32, >= 2 + cap/256 entries) receives [num_tiles, rows,
  * local expert of tile 0, 1, ...] for pk_grouped_gemm_planned; recv_src of
@@ -217,6 +260,18 @@ PK_API int pk_moe_dispatch_ex(pk_comm* comm, const pk_tensor* x, const pk_tensor
  * Ranks may hold different token counts (T = 0 included) in both calls. */
 PK_API int pk_moe_combine(pk_comm* comm, const pk_tensor* y, const pk_tensor* topk_idx,
                           const pk_tensor* w, int num_experts, pk_tensor* out, void* stream);
+
+/* Mechanism calibration (replaces the reference's modelled mechanism curves,
+ * overlapsim/hwmodel.py:147-245, and the paper's Table 1, PAPER.md:117-131,
+ * with measurement): move `bytes` between this rank and `peer` with one
+ * pk_mechanism in messages of `msg_bytes`, on at most `num_sms` SMs (0 = all;
+ * ignored by PK_MECH_CE). push (pull = 0): src's local buffer -> peer's dst;
+ * pull = 1: peer's src -> local dst. PK_MECH_MULTIMEM stores the local src
+ * through dst's multicast VA (every rank receives it; PK_ERR_CAPABILITY
+ * without one). No cross-rank synchronisation: the caller brackets the probe
+ * with barriers and times it on `stream`. */
+PK_API int pk_mech_probe(pk_comm* comm, pk_pgl* src, pk_pgl* dst, int peer, size_t bytes, size_t msg_bytes,
+                         int mechanism, int pull, int num_sms, void* stream);
 
 /* ---- pure collectives on strided layouts (pull-based over peer memory) --- */
 /* Tensor-dim all-gather, rank-major: y = [x_0; x_1; ...] (AllGatherTdPlan,

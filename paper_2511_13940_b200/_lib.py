@@ -22,19 +22,22 @@ PK_ERR_PROTOCOL = 3
 PK_ERR_TIMEOUT = 4
 PK_ERR_CUDA = 5
 PK_ERR_NOMEM = 6
+PK_ERR_MEMORY = 7
 
 PK_BF16, PK_F32, PK_F16, PK_I32, PK_I64, PK_U8 = range(6)
+PK_SCHED_FP32_PARTIALS = 1
 
 # Every symbol include/pk.h declares (tests check the library exports them all).
 EXPORTS = (
     "pk_last_error", "pk_version", "pk_num_sms",
     "pk_comm_init", "pk_comm_init_local", "pk_comm_destroy", "pk_comm_rank",
-    "pk_comm_has_multicast", "pk_comm_set_timeout", "pk_comm_check", "pk_debug_rendezvous", "pk_debug_multimem",
+    "pk_comm_has_multicast", "pk_comm_distinct_devices", "pk_comm_set_timeout", "pk_comm_check", "pk_debug_rendezvous", "pk_debug_multimem",
     "pk_pgl_alloc", "pk_pgl_ptrs", "pk_pgl_free",
+    "pk_setup_begin", "pk_setup_advance", "pk_setup_state", "pk_setup_end",
     "pk_gemm", "pk_ag_gemm", "pk_gemm_rs", "pk_gemm_ar", "pk_all_reduce", "pk_all_reduce_ablate",
     "pk_ring_attn_fwd", "pk_attn_fwd", "pk_moe_dispatch", "pk_moe_dispatch_ex", "pk_moe_combine", "pk_grouped_gemm",
     "pk_grouped_gemm_planned",
-    "pk_all_gather", "pk_reduce_scatter", "pk_all_to_all", "pk_ulysses_a2a",
+    "pk_all_gather", "pk_reduce_scatter", "pk_all_to_all", "pk_ulysses_a2a", "pk_mech_probe",
 )
 
 
@@ -58,6 +61,7 @@ class PkSched(ctypes.Structure):
         ("num_comm_sms", ctypes.c_int32),
         ("stages", ctypes.c_int32),
         ("num_sms", ctypes.c_int32),
+        ("flags", ctypes.c_uint32),
     ]
 
 
@@ -124,6 +128,7 @@ def sched_desc(schedule) -> PkSched | None:
     s.num_comm_sms = int(schedule.get("num_comm_sms", 0))
     s.stages = int(schedule.get("stages", 0))
     s.num_sms = int(schedule.get("num_sms", 0))
+    s.flags = PK_SCHED_FP32_PARTIALS if schedule.get("partials") == "fp32" else 0
     return s
 
 

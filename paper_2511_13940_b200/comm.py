@@ -87,6 +87,9 @@ class Comm:
         mc = ctypes.c_int()
         check(lib.pk_comm_has_multicast(handle, ctypes.byref(mc)), "comm_has_multicast")
         self.has_multicast = bool(mc.value)
+        dd = ctypes.c_int()
+        check(lib.pk_comm_distinct_devices(handle, ctypes.byref(dd)), "comm_distinct_devices")
+        self.distinct_devices = bool(dd.value)      # peers on other GPUs: traffic crosses NVLink
         self._pgls: list[Pgl] = []
         self._defaults: dict = {}       # default symmetric outputs of the ops, per (use, shape, dtype)
         self._keep = keepalive
@@ -104,12 +107,14 @@ class Comm:
         return cls(h, device)
 
     @classmethod
-    def init_from_env(cls) -> "Comm":
-        """torchrun: RANK / WORLD_SIZE / LOCAL_RANK; uid agreed via torch.distributed."""
+    def init_from_env(cls, device: int | None = None) -> "Comm":
+        """torchrun: RANK / WORLD_SIZE / LOCAL_RANK (the device unless given);
+        uid agreed via torch.distributed."""
         import torch.distributed as dist
         rank = int(os.environ.get("RANK", "0"))
         world = int(os.environ.get("WORLD_SIZE", "1"))
-        device = int(os.environ.get("LOCAL_RANK", "0"))
+        if device is None:
+            device = int(os.environ.get("LOCAL_RANK", "0"))
         uid = [uuid.uuid4().hex[:16] if rank == 0 else None]
         if world > 1 and dist.is_initialized():
             dist.broadcast_object_list(uid, src=0)

@@ -38,35 +38,6 @@
 
 namespace pk {
 
-// ------------------------------------------------------------------ setup FSMs
-// Steps and prerequisites of memsim.py:215-264.
-enum VmmStep { VMM_CREATE, VMM_EXPORT, VMM_TRANSFER, VMM_IMPORT, VMM_MAP, VMM_NSTEPS };
-enum McStep { MC_CREATE, MC_REGISTER, MC_BIND, MC_EXPORT, MC_TRANSFER, MC_IMPORT, MC_MAP, MC_NSTEPS };
-
-struct SetupFsm {
-  const int (*prereq)[2];
-  int nsteps;
-  uint32_t done = 0;
-  const char* name;
-  int advance(int step) {
-    if (step < 0 || step >= nsteps) return fail(PK_ERR_PROTOCOL, "%s: unknown step %d", name, step);
-    if (done & (1u << step)) return fail(PK_ERR_PROTOCOL, "%s: step %d already taken", name, step);
-    for (int i = 0; i < 2; ++i) {
-      const int need = prereq[step][i];
-      if (need >= 0 && !(done & (1u << need)))
-        return fail(PK_ERR_PROTOCOL, "%s: step %d requires step %d first", name, step, need);
-    }
-    done |= 1u << step;
-    return PK_OK;
-  }
-  bool complete() const { return done == (1u << nsteps) - 1; }
-};
-static const int kVmmPrereq[VMM_NSTEPS][2] = {
-    {-1, -1}, {VMM_CREATE, -1}, {VMM_EXPORT, -1}, {VMM_TRANSFER, -1}, {VMM_IMPORT, -1}};
-static const int kMcPrereq[MC_NSTEPS][2] = {
-    {-1, -1}, {MC_CREATE, -1}, {MC_REGISTER, -1}, {MC_CREATE, -1},
-    {MC_EXPORT, -1}, {MC_TRANSFER, -1}, {MC_IMPORT, -1}};
-
 // ------------------------------------------------------------------ sockets
 static void sock_name(const std::string& uid, int rank, sockaddr_un* a, socklen_t* len) {
   memset(a, 0, sizeof(*a));
@@ -531,6 +502,7 @@ int preload_moe();
 int preload_attn();
 int preload_grouped();
 int preload_coll();
+int preload_mech();
 
 // Device call counting (CallRef): advance the base counters and fill this
 // call's slot; stream order puts it after the previous call's kernels and
@@ -581,6 +553,7 @@ static int preload_kernels() {
     if (s == PK_OK) s = preload_attn();
     if (s == PK_OK) s = preload_grouped();
     if (s == PK_OK) s = preload_coll();
+    if (s == PK_OK) s = preload_mech();
     cudaFuncAttributes fa;
     if (s == PK_OK && cudaFuncGetAttributes(&fa, call_arm_kernel) != cudaSuccess) s = fail(PK_ERR_CUDA, "preload call_arm_kernel");
     status = s;
@@ -692,9 +665,10 @@ PK_API int pk_comm_init(int rank, int world, int device, const char* uid, pk_com
     std::vector<cudaUUID_t> ids(world);
     st = comm_allgather(c, &prop.uuid, ids.data(), sizeof(cudaUUID_t));
     if (st != PK_OK) { ::close(c->listen_fd); delete c; return st; }
+    c->distinct_devices = true;
     for (int i = 0; i < world; ++i)
       for (int j = i + 1; j < world; ++j)
-        if (memcmp(&ids[i], &ids[j], sizeof(cudaUUID_t)) == 0) c->multicast_supported = false;
+        if (memcmp(&ids[i], &ids[j], sizeof(cudaUUID_t)) == 0) c->multicast_supported = c->distinct_devices = false;
     // every rank must agree (PGL allocation is collective)
     int mine = c->multicast_supported ? 1 : 0;
     std::vector<int> all(world);
@@ -774,6 +748,12 @@ PK_API int pk_comm_rank(const pk_comm* c, int* rank, int* world) {
 PK_API int pk_comm_has_multicast(const pk_comm* c, int* out) {
   if (!c) return fail(PK_ERR_INVALID, "null comm");
   *out = c->multicast_supported ? 1 : 0;
+  return PK_OK;
+}
+
+PK_API int pk_comm_distinct_devices(const pk_comm* c, int* out) {
+  if (!c) return fail(PK_ERR_INVALID, "null comm");
+  *out = c->distinct_devices ? 1 : 0;
   return PK_OK;
 }
 

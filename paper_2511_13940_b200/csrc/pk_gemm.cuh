@@ -33,7 +33,10 @@ constexpr int EPI_COLS = 64;                // epilogue chunk = 64 cols = 128 B 
 constexpr int kNumThreads = 256;
 constexpr int kEpiWarp0 = 4;
 
-enum EpiMode : int { EPI_STORE = 0, EPI_REDUCE_ADD = 1, EPI_SCATTER = 2, EPI_DIRECT = 3 };
+// EPI_REDUCE_ADD_F32: the fp32 accumulator itself is reduce-added (32-column
+// fp32 sub-tiles, 128 B rows) into fp32 partial sums on the owner — one
+// rounding to bf16 at the end instead of one per rank (GEMM-RS fp32 partials)
+enum EpiMode : int { EPI_STORE = 0, EPI_REDUCE_ADD = 1, EPI_SCATTER = 2, EPI_DIRECT = 3, EPI_REDUCE_ADD_F32 = 4 };
 constexpr int kTileRing = 4;                // depth of the tile-index broadcast ring
 constexpr int kAgCountOffset = 32768;       // AG piece counters live after the first 32K m-tile flags
 
@@ -157,6 +160,7 @@ template <int CG, int BN, int AM, int EPI>
 __global__ void __launch_bounds__(GemmCfg<CG, BN, AM>::NUM_THREADS, 1)
 lcsc_gemm_kernel(const __grid_constant__ GemmArgs args) {
   using Cfg = GemmCfg<CG, BN, AM>;
+  static_assert(EPI != EPI_REDUCE_ADD_F32 || Cfg::EPI_NBUF == 2, "fp32 partials need the double-buffered epilogue");
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* smem_a = smem;
@@ -586,7 +590,8 @@ lcsc_gemm_kernel(const __grid_constant__ GemmArgs args) {
       const int row0 = mt * Cfg::TILE_M + (int)cta_rank * Cfg::BM + am * 128 + q * 32;   // global M row of lane 0
       const int dst = (args.c_ndst > 1) ? row0 / args.c_rows_per_dst : 0;
       const int c_row = row0 - dst * args.c_rows_per_dst;
-      if (EPI == EPI_REDUCE_ADD && args.sync_ready_before_store && !((owners_ready >> dst) & 1)) {
+      if ((EPI == EPI_REDUCE_ADD || EPI == EPI_REDUCE_ADD_F32) && args.sync_ready_before_store &&
+          !((owners_ready >> dst) & 1)) {
         if (lane == 0) wait_geq(args.sync.ready_local + dst, s_call[1], args.sync.err, args.sync.timeout_ns);
         __syncwarp();
         owners_ready |= 1u << dst;
@@ -670,6 +675,28 @@ lcsc_gemm_kernel(const __grid_constant__ GemmArgs args) {
               w.w = pack_bf16x2(__uint_as_float(src[6]), __uint_as_float(src[7]));
               dstp[j] = w;
             }
+          }
+          continue;
+        }
+        if constexpr (EPI == EPI_REDUCE_ADD_F32) {
+          // two 32-column fp32 sub-tiles (32 rows x 128 B, same 128 B swizzle)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const uint32_t* src = h == 0 ? v0 : v1;
+            if (lane == 0) bulk_wait_read<1>();
+            __syncwarp();
+            uint8_t* buf = ebuf + ebuf_idx * Cfg::EPI_BUF_BYTES;
+            const uint32_t row_addr = smem_u32(buf) + lane * 128;
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+              st_shared_v4(row_addr + ((j ^ (lane & 7)) << 4), src[4 * j], src[4 * j + 1], src[4 * j + 2], src[4 * j + 3]);
+            fence_async_shared();
+            __syncwarp();
+            if (lane == 0) {
+              tma_reduce_add_2d(&args.tmap_c[dst], buf, nt * BN + c * EPI_COLS + h * 32, c_row);
+              bulk_commit();
+            }
+            ebuf_idx ^= 1;
           }
           continue;
         }

@@ -88,6 +88,47 @@ int make_tmap_2d(CUtensorMap* map, const void* ptr, CUtensorMapDataType dt, int 
 // device once (the attribute is per device; cached per (kernel, device)).
 int ensure_smem_attr(const void* kern, int bytes);
 
+// ---------------------------------------------------------------- setup FSMs
+// The IPC / VMM / multicast setup protocols as strict prerequisite DAGs
+// (memsim.py:209-264): a step is taken only once, and only after its
+// prerequisites; anything else is PK_ERR_PROTOCOL (ProtocolViolation). Used
+// by the PGL allocator (pk_comm.cu) and the step-by-step setup sessions
+// (pk_setup.cu).
+enum IpcStep { IPC_GET, IPC_SHARE, IPC_OPEN, IPC_NSTEPS };
+enum VmmStep { VMM_CREATE, VMM_EXPORT, VMM_TRANSFER, VMM_IMPORT, VMM_MAP, VMM_NSTEPS };
+enum McStep { MC_CREATE, MC_REGISTER, MC_BIND, MC_EXPORT, MC_TRANSFER, MC_IMPORT, MC_MAP, MC_NSTEPS };
+inline constexpr int kIpcPrereq[IPC_NSTEPS][2] = {{-1, -1}, {IPC_GET, -1}, {IPC_SHARE, -1}};
+inline constexpr int kVmmPrereq[VMM_NSTEPS][2] = {
+    {-1, -1}, {VMM_CREATE, -1}, {VMM_EXPORT, -1}, {VMM_TRANSFER, -1}, {VMM_IMPORT, -1}};
+// bind needs every device registered; the export branch needs only the stub
+inline constexpr int kMcPrereq[MC_NSTEPS][2] = {
+    {-1, -1}, {MC_CREATE, -1}, {MC_REGISTER, -1}, {MC_CREATE, -1},
+    {MC_EXPORT, -1}, {MC_TRANSFER, -1}, {MC_IMPORT, -1}};
+
+struct SetupFsm {
+  const int (*prereq)[2];
+  int nsteps;
+  uint32_t done = 0;
+  const char* name;
+  // PK_OK if `step` may be taken now (nothing is recorded)
+  int check(int step) const {
+    if (step < 0 || step >= nsteps) return fail(PK_ERR_PROTOCOL, "%s: step %d is not part of the protocol", name, step);
+    if (done & (1u << step)) return fail(PK_ERR_PROTOCOL, "%s: step %d already taken", name, step);
+    for (int i = 0; i < 2; ++i) {
+      const int need = prereq[step][i];
+      if (need >= 0 && !(done & (1u << need)))
+        return fail(PK_ERR_PROTOCOL, "%s: step %d requires step %d first", name, step, need);
+    }
+    return PK_OK;
+  }
+  int advance(int step) {
+    const int st = check(step);
+    if (st == PK_OK) done |= 1u << step;
+    return st;
+  }
+  bool complete() const { return done == (1u << nsteps) - 1; }
+};
+
 // ---------------------------------------------------------------- communicator
 struct Comm;
 
@@ -136,6 +177,7 @@ struct Comm {
   std::string uid;
   int num_sms = 148;
   bool multicast_supported = false;
+  bool distinct_devices = false;     // every rank on its own GPU (peer traffic crosses NVLink)
   uint64_t timeout_ns = 10ull * 1000 * 1000 * 1000;
   // sync PGL: [0,n) ready counters, [n,2n) done counters, [2n, 2n+1) err,
   // then per-m-tile flags.

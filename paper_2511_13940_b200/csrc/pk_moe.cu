@@ -613,10 +613,11 @@ int moe_dispatch(Comm* c, const pk_tensor* x, const pk_tensor* topk, int num_exp
   if (!find_symmetric(c, recv->ptr, (size_t)cap * H * 2, rp) ||
       !find_symmetric(c, recv_src->ptr, (size_t)cap * 4 * src_cols, sp))
     return fail(PK_ERR_INVALID, "moe_dispatch: recv and recv_src must be symmetric (Comm.empty) tensors");
-  // auto: hwmodel.select_mechanism's answer for one row per message with this
-  // rank's SMs issuing — TMA (higher peak, saturates with 15 SMs) up to its
-  // 227 KB message limit
-  if (mech == PK_MECH_AUTO) mech = H * 2 <= 227 * 1024 ? PK_MECH_TMA : PK_MECH_REG;
+  // auto (C-ABI callers; the Python layer resolves it through hwmodel): the
+  // policy's answer under the paper's B200 points for one row per message —
+  // TMA from 2 KB rows (74 % of the link there) up to its 227 KB message
+  // limit, register ops for smaller rows
+  if (mech == PK_MECH_AUTO) mech = (H * 2 >= 2048 && H * 2 <= 227 * 1024) ? PK_MECH_TMA : PK_MECH_REG;
   a.mech = mech;
   a.x = static_cast<const uint8_t*>(x->ptr);
   a.x_ld = xld * 2;

@@ -65,7 +65,7 @@ int launch_gemm_variant(Variant v, int epi, const GemmArgs& args, int grid_ctas,
 #define PK_V(CG, AM, E) if (v.cg == CG && v.am == AM && v.bn == 256 && epi == E) return launch_lcsc<CG, 256, AM, E>(args, grid_ctas, st);
   PK_V(2, 2, EPI_STORE) PK_V(2, 2, EPI_REDUCE_ADD) PK_V(2, 1, EPI_DIRECT)
   PK_V(2, 1, EPI_STORE) PK_V(2, 1, EPI_REDUCE_ADD)
-  PK_V(1, 1, EPI_STORE) PK_V(1, 1, EPI_REDUCE_ADD)
+  PK_V(1, 1, EPI_STORE) PK_V(1, 1, EPI_REDUCE_ADD) PK_V(2, 1, EPI_REDUCE_ADD_F32)
 #undef PK_V
   if (v.cg == 1 && v.am == 1 && v.bn == 128 && epi == EPI_STORE) return launch_lcsc<1, 128, 1, EPI_STORE>(args, grid_ctas, st);
   if (v.cg == 2 && v.am == 1 && v.bn == 128 && epi == EPI_STORE) return launch_lcsc<2, 128, 1, EPI_STORE>(args, grid_ctas, st);
@@ -80,15 +80,19 @@ int launch_gemm_grouped(const GemmArgs& args, int grid_ctas, cudaStream_t st) {
   return launch_lcsc<2, 256, 1, EPI_SCATTER>(args, grid_ctas, st);
 }
 
+__global__ void f32_to_bf16_rows_kernel(const float* __restrict__ src, uint8_t* dst, long long rows, long long cols,
+                                        long long dst_ld);
+
 // Force-load every kernel image now (see preload_kernels in pk_comm.cu).
 int preload_gemm() {
   cudaFuncAttributes fa;
 #define PK_L(CG, AM, E) PK_CUDA(cudaFuncGetAttributes(&fa, lcsc_gemm_kernel<CG, 256, AM, E>));
   PK_L(2, 2, EPI_STORE) PK_L(2, 2, EPI_REDUCE_ADD) PK_L(2, 1, EPI_DIRECT) PK_L(2, 1, EPI_STORE) PK_L(2, 1, EPI_REDUCE_ADD)
-  PK_L(1, 1, EPI_STORE) PK_L(1, 1, EPI_REDUCE_ADD) PK_L(2, 1, EPI_SCATTER)
+  PK_L(1, 1, EPI_STORE) PK_L(1, 1, EPI_REDUCE_ADD) PK_L(2, 1, EPI_SCATTER) PK_L(2, 1, EPI_REDUCE_ADD_F32)
 #undef PK_L
   PK_CUDA(cudaFuncGetAttributes(&fa, lcsc_gemm_kernel<1, 128, 1, EPI_STORE>));
   PK_CUDA(cudaFuncGetAttributes(&fa, lcsc_gemm_kernel<2, 128, 1, EPI_STORE>));
+  PK_CUDA(cudaFuncGetAttributes(&fa, f32_to_bf16_rows_kernel));
   return PK_OK;
 }
 
@@ -162,6 +166,28 @@ static int tmap_b(CUtensorMap* m, const void* p, int64_t rows, int64_t k, int64_
 static int tmap_c(CUtensorMap* m, const void* p, int64_t rows, int64_t n, int64_t ld) {
   return make_tmap_2d(m, p, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, rows, n, ld, 32, EPI_COLS,
                       CU_TENSOR_MAP_SWIZZLE_128B);
+}
+
+static int tmap_c_f32(CUtensorMap* m, const void* p, int64_t rows, int64_t n, int64_t ld) {
+  return make_tmap_2d(m, p, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, rows, n, ld, 32, 32, CU_TENSOR_MAP_SWIZZLE_128B);
+}
+
+// fp32 partial sums -> bf16 output rows (GEMM-RS with fp32 partials)
+__global__ void __launch_bounds__(256) f32_to_bf16_rows_kernel(const float* __restrict__ src, uint8_t* dst,
+                                                                long long rows, long long cols, long long dst_ld) {
+  const long long per_row = cols / 8;
+  const long long total = rows * per_row;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (long long)gridDim.x * blockDim.x) {
+    const long long r = i / per_row, c8 = i - r * per_row;
+    const float4 a = __ldcs(reinterpret_cast<const float4*>(src + r * cols + c8 * 8));
+    const float4 b = __ldcs(reinterpret_cast<const float4*>(src + r * cols + c8 * 8 + 4));
+    uint4 o;
+    o.x = pack_bf16x2(a.x, a.y);
+    o.y = pack_bf16x2(a.z, a.w);
+    o.z = pack_bf16x2(b.x, b.y);
+    o.w = pack_bf16x2(b.z, b.w);
+    *reinterpret_cast<uint4*>(dst + (r * dst_ld + c8 * 8) * 2) = o;
+  }
 }
 
 static void init_args(GemmArgs& a, int am = 1) {
@@ -429,15 +455,24 @@ int gemm_rs(Comm* c, const pk_tensor* A, const pk_tensor* B, pk_tensor* O, const
                 (long long)m_own, (long long)N, (long long)k_loc);
   if (n == 1) return gemm_local(A, B, O, sched, st, c->device);
   if (sched && (sched->mode == PK_INTER_SM || sched->mode == PK_HYBRID)) return gemm_rs_inter(c, A, B, O, sched, st);
-  const Variant v = pick_variant(m_own, k_loc, sched, /*reduce=*/true, M, N,
-                                 (sched && sched->num_sms > 0 ? std::min(sched->num_sms, c->num_sms) : c->num_sms) / 2);
+  const bool f32 = sched && (sched->flags & PK_SCHED_FP32_PARTIALS);
+  const Variant v = f32 ? Variant{2, 1} :
+      pick_variant(m_own, k_loc, sched, /*reduce=*/true, M, N,
+                   (sched && sched->num_sms > 0 ? std::min(sched->num_sms, c->num_sms) : c->num_sms) / 2);
   const int cg = v.cg;
   const int tile_m = 128 * v.am * cg;
-  // Destination of every rank (zero-copy when `out` is symmetric).
+  if (m_own % tile_m) return fail(PK_ERR_INVALID, "gemm_rs: (M/n) %% %d != 0 for this schedule", tile_m);
+  // Destination of every rank: the owners' fp32 partial sums (scratch slot
+  // 5), or the bf16 output itself (zero-copy when `out` is symmetric).
   void* dst[kMaxRanks];
-  const size_t out_bytes = (size_t)m_own * N * 2;
+  const size_t out_bytes = (size_t)m_own * N * (f32 ? 4 : 2);
   bool staged = false;
-  if (!(contiguous_rows(O) && find_symmetric(c, O->ptr, out_bytes, dst))) {
+  if (f32) {
+    Pgl* s5;
+    PK_TRY(comm_scratch(c, 5, out_bytes, &s5));
+    for (int r = 0; r < n; ++r) dst[r] = s5->peers[r];
+    staged = true;
+  } else if (!(contiguous_rows(O) && find_symmetric(c, O->ptr, out_bytes, dst))) {
     Pgl* s2;
     PK_TRY(comm_scratch(c, 2, out_bytes, &s2));
     for (int r = 0; r < n; ++r) dst[r] = s2->peers[r];
@@ -451,7 +486,8 @@ int gemm_rs(Comm* c, const pk_tensor* A, const pk_tensor* B, pk_tensor* O, const
   args.a_rows_per_src = (int)M;
   PK_TRY(tmap_a(&args.tmap_a[0], A->ptr, M, k_loc, ldA, v.am));
   PK_TRY(tmap_b(&args.tmap_b, B->ptr, N, k_loc, ldB, cg));
-  for (int r = 0; r < n; ++r) PK_TRY(tmap_c(&args.tmap_c[r], dst[r], m_own, N, N));
+  for (int r = 0; r < n; ++r)
+    PK_TRY(f32 ? tmap_c_f32(&args.tmap_c[r], dst[r], m_own, N, N) : tmap_c(&args.tmap_c[r], dst[r], m_own, N, N));
   args.c_rows_per_dst = (int)m_own;
   args.c_ndst = n;
   args.m_rot = (int)(((c->rank + 1) % n) * (m_own / tile_m));   // right neighbour's rows first, own last
@@ -465,9 +501,17 @@ int gemm_rs(Comm* c, const pk_tensor* A, const pk_tensor* B, pk_tensor* O, const
   CallRef call;
   PK_TRY(begin_call(c, 1, 1, (uint32_t)(compute_clusters * cg * 4 * v.am), st, &call));
   fill_sync(c, args.sync, call);
-  PK_TRY(launch_gemm_variant(v, EPI_REDUCE_ADD, args, compute_clusters * cg, st));
-  if (staged)
+  PK_TRY(launch_gemm_variant(v, f32 ? EPI_REDUCE_ADD_F32 : EPI_REDUCE_ADD, args, compute_clusters * cg, st));
+  if (f32) {
+    // the kernel returned only after every rank's partials landed (done wait)
+    const long long total = (long long)m_own * (N / 8);
+    const int blocks = (int)std::max<long long>(1, std::min<long long>((total + 255) / 256, (long long)c->num_sms * 8));
+    f32_to_bf16_rows_kernel<<<blocks, 256, 0, st>>>(static_cast<const float*>(dst[c->rank]),
+                                                    static_cast<uint8_t*>(O->ptr), m_own, N, ldO);
+    PK_CUDA(cudaGetLastError());
+  } else if (staged) {
     PK_CUDA(cudaMemcpy2DAsync(O->ptr, ldO * 2, dst[c->rank], N * 2, N * 2, m_own, cudaMemcpyDeviceToDevice, st));
+  }
   return PK_OK;
 }
 

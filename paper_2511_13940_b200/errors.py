@@ -5,6 +5,7 @@ libpk status codes.
   PK_ERR_CAPABILITY -> PrimitiveError     (overlapsim/primitives.py:31)
   PK_ERR_PROTOCOL   -> ProtocolViolation  (overlapsim/memsim.py:26)
   PK_ERR_TIMEOUT    -> DeadlockError      (overlapsim/engine.py:35-40)
+  PK_ERR_MEMORY     -> MemSimError        (overlapsim/memsim.py:22)
   PK_ERR_CUDA/NOMEM -> PkCudaError
 """
 from __future__ import annotations
@@ -55,6 +56,7 @@ _MAP = {
     _lib.PK_ERR_TIMEOUT: DeadlockError,
     _lib.PK_ERR_CUDA: PkCudaError,
     _lib.PK_ERR_NOMEM: PkCudaError,
+    _lib.PK_ERR_MEMORY: MemSimError,
 }
 
 

@@ -11,7 +11,7 @@ from __future__ import annotations
 
 import torch
 
-from . import _lib, tune
+from . import _lib, hwmodel, tune
 from .errors import WorkloadError, check
 
 
@@ -78,6 +78,15 @@ def all_gather_gemm(comm, a_shard: torch.Tensor, b: torch.Tensor, out: torch.Ten
     dg = _lib.tensor_desc(a_gathered) if a_gathered is not None else None
     if schedule is None and comm.world > 1:
         schedule = tune.auto_schedule("ag_gemm", comm.world, m, b.shape[0] * comm.world, a_shard.shape[1])
+        if schedule is None:
+            # communicator sized by the mechanism policy (hwmodel: measured
+            # calibration, else the paper's B200 points): TMA SMs enough to pull
+            # the remote rows within the GEMM's time at ~1.4 PF/s sustained
+            K = a_shard.shape[1]
+            remote = (comm.world - 1) / comm.world * m * K * 2
+            t_gemm = 2.0 * m * b.shape[0] * K / 1.4e15
+            cap = max(2, min(16, comm.num_sms // 8) & ~1)
+            schedule = {"mode": "auto", "num_comm_sms": hwmodel.comm_sms_for(remote, t_gemm, cap=cap)}
     sc = _sched(schedule)
     check(lib.pk_ag_gemm(comm._h, _lib.ref(da), _lib.ref(db), _lib.ref(dc), _lib.ref(dg), _lib.ref(sc),
                          ctypes_stream(_stream(stream))), "all_gather_gemm")
@@ -203,8 +212,9 @@ def moe_dispatch(comm, x: torch.Tensor, topk_idx: torch.Tensor, num_experts: int
     (recv_src = -1 on padding rows); a 4th value, the device tile plan, feeds
     grouped_gemm(recv, None, w, plan=plan) without a gather pass.
     mechanism: "reg" (16 B register stores), "tma" (bulk-copy engine) or "auto"
-    (hwmodel.select_mechanism's answer, TMA — the two measure the same on
-    one GPU, 0.110 vs 0.112 ms).
+    (hwmodel.select_mechanism's answer for row-sized messages under the active
+    calibration: TMA for rows of >= 2 KB; the two measure the same on one GPU,
+    0.110 vs 0.112 ms).
     """
     _require_cuda(x, topk_idx)
     T, k = topk_idx.shape
@@ -212,6 +222,9 @@ def moe_dispatch(comm, x: torch.Tensor, topk_idx: torch.Tensor, num_experts: int
     local_experts = (num_experts + comm.world - 1) // comm.world if lay else 0
     if capacity is None:
         capacity = moe_capacity(T, k, comm.world, x.shape[1], local_experts)
+    if mechanism == "auto":          # the policy's answer for one row per message with this rank's SMs
+        kind = hwmodel.select_mechanism(hwmodel.Functionality.P2P_TRANSFER, 2 * x.shape[1], comm.num_sms).kind
+        mechanism = "tma" if kind is hwmodel.MechanismKind.TMA else "reg"
     if recv is None:
         recv = (comm.default_buffer("moe.recv", (capacity, x.shape[1]), torch.bfloat16),
                 comm.default_buffer("moe.recv_src", (capacity, 2), torch.int32))

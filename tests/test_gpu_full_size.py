@@ -97,6 +97,47 @@ def test_ag_gemm_and_gemm_rs_16384_emulated_world2():
         c.destroy()
 
 
+def rs_errors_world8(pk, schedules, S_=S, world=8, seed=5):
+    """GEMM-RS at M = N = S, local K = S / n over an emulated n = 8 (the
+    north_star's 8 x B200 shape): max |out - fp64 ref| on sampled rows of every
+    rank, relative to max |ref|, per schedule. Shared with
+    profiles/rs_precision.py."""
+    comms = pk.local_group(world)
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    rnd = lambda *s: (torch.randn(*s, device="cuda", generator=g) * 0.1).bfloat16()
+    kl = S_ // world
+    a = [rnd(S_, kl) for _ in comms]
+    b = [rnd(S_, kl) for _ in comms]
+    o = [c.empty((S_ // world, S_)) for c in comms]
+    sub = torch.randint(0, S_ // world, (16,), device="cuda", generator=g)
+    refs = [sum(a[d][r * (S_ // world) + sub].double() @ b[d].double().t() for d in range(world))
+            for r in range(world)]
+    scale = max(x.abs().max().item() for x in refs)
+    out = {}
+    for name, sch in schedules.items():
+        run_ranks(comms, lambda r, c, s: pk.gemm_reduce_scatter(c, a[r], b[r], out=o[r], schedule=sch, stream=s))
+        out[name] = max((o[r][sub].double() - refs[r]).abs().max().item() for r in range(world)) / scale
+    for c in comms:
+        c.destroy()
+    return out
+
+
+def test_gemm_rs_16384_emulated_world8_precision():
+    """SURVEY §7 "reduction precision": bf16 partials reduce-added in hardware
+    order (default), fp32 partials (one rounding) and the inter-SM fold, all
+    within 2e-2 * sqrt(K / 1024) * max|ref| (K = S, the full contraction); fp32
+    partials at least as accurate as bf16 ones."""
+    pk = _pk()
+    err = rs_errors_world8(pk, {"bf16_partials": None, "fp32_partials": {"partials": "fp32"},
+                                "inter_sm": {"mode": "inter_sm", "num_comm_sms": 4}})
+    tol = 2e-2 * (S / 1024) ** 0.5
+    for name, e in err.items():
+        assert e <= tol, (name, e, tol)
+    assert err["fp32_partials"] <= err["bf16_partials"] + 1e-6, err
+    # one bf16 rounding of the sum (<= 2^-9 relative) plus fp32 noise
+    assert err["fp32_partials"] <= 2 ** -8, err
+
+
 def test_all_reduce_1gib_integer_exact():
     pk = _pk()
     world = 2

@@ -159,6 +159,27 @@ def test_gemm_rs_matches_oracle(world):
         c.destroy()
 
 
+@pytest.mark.parametrize("world", [2, 3, 4, 8])
+def test_gemm_rs_fp32_partials_exact(world):
+    """fp32 partial sums (PK_SCHED_FP32_PARTIALS): integer partials up to
+    |x| = k_loc * n (beyond bf16's exact range only at the final rounding, which
+    both sides do once), exact against the oracle rounded to bf16."""
+    pk = _pk()
+    rng = np.random.default_rng(200 + world)
+    M, N, k_loc = 256 * world, 512, 128
+    comms = pk.local_group(world)
+    a = [ints(rng, (M, k_loc), -1, 1) for _ in range(world)]
+    b = [ints(rng, (N, k_loc), -1, 1) for _ in range(world)]
+    outs = run_ranks(comms, lambda r, c, s: pk.gemm_reduce_scatter(c, to_dev(a[r]), to_dev(b[r]),
+                                                                   schedule={"partials": "fp32"}, stream=s))
+    exp = oracle.gemm_rs(a, b)
+    for r in range(world):
+        ref = torch.from_numpy(exp[r].astype(np.float32)).bfloat16().float().numpy()
+        assert np.array_equal(outs[r].float().cpu().numpy(), ref)
+    for c in comms:
+        c.destroy()
+
+
 @pytest.mark.parametrize("world", [2, 4])
 def test_gemm_rs_randn_tolerance_symmetric_out(world):
     pk = _pk()
