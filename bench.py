@@ -526,6 +526,9 @@ def main():
                                                         backend == "nccl"))
     else:
         line["all_reduce"] = {"skipped": "world 1: an all-reduce is the identity"}
+    if n > 1:
+        _leg(line, "decomposition", lambda: decomposition_leg(pk, comm, dev, n, S, a_ag, b_ag, c_ag, a_rs, b_rs, o_rs,
+                                                              ag_max, rs_max, barrier, max_over_ranks))
     _leg(line, "nvlink", lambda: nvlink_leg(comm, n, barrier, max_vec))
     dog.cancel()
     comm.check()
@@ -650,6 +653,45 @@ def all_reduce_leg(pk, comm, dist, dev, n, barrier, max_over_ranks, with_nccl: b
         x._pk_pgl.free()
         del x
     return res
+
+
+def decomposition_leg(pk, comm, dev, n, S, a_ag, b_ag, c_ag, a_rs, b_rs, o_rs, ag_ms, rs_ms, barrier,
+                      max_over_ranks) -> dict:
+    """The paper's time decomposition (lcsc.py:110-138) of the
+    two fused ops, measured: the compute-only twin (the same per-rank GEMM
+    with no communication), the communication-only twin (pk all-gather of the
+    A shards / pk reduce-scatter of a bf16 partial) and the non-overlapped
+    residual t_fused - max(t_comp, t_comm); comm_ratio = (t_fused - t_comp) /
+    t_fused, the paper's non-overlapped communication ratio."""
+    import torch
+
+    def timed(fn, iters=5):
+        fn()
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(iters):
+            fn()
+        e1.record()
+        barrier()
+        return max_over_ranks(e0.elapsed_time(e1) / iters)
+    full = comm.empty((S, S))            # symmetric: the reduce-scatter twin reads peers' partials in place
+    out = {}
+    t_comp = timed(lambda: pk.gemm(full, b_ag, out=c_ag))
+    t_comm = timed(lambda: pk.all_gather(comm, a_ag, out=full))
+    out["ag_gemm"] = {"t_fused_ms": ag_ms, "t_comp_ms": t_comp, "t_comm_ms": t_comm,
+                      "t_non_overlap_ms": max(0.0, ag_ms - max(t_comp, t_comm)),
+                      "comm_ratio": max(0.0, (ag_ms - t_comp) / ag_ms)}
+    t_comp = timed(lambda: pk.gemm(a_rs, b_rs, out=full))
+    part = torch.empty(S // n, S, device=dev, dtype=torch.bfloat16)
+    t_comm = timed(lambda: pk.reduce_scatter(comm, full, out=part))
+    out["gemm_rs"] = {"t_fused_ms": rs_ms, "t_comp_ms": t_comp, "t_comm_ms": t_comm,
+                      "t_non_overlap_ms": max(0.0, rs_ms - max(t_comp, t_comm)),
+                      "comm_ratio": max(0.0, (rs_ms - t_comp) / rs_ms)}
+    full._pk_pgl.free()
+    del full, part
+    comm.check()
+    return out
 
 
 def nvlink_leg(comm, n, barrier, max_vec) -> dict:

@@ -96,7 +96,7 @@ class OverheadConfig:          # engine.py:49-60: all off reproduces the direct 
 
 
 @dataclass
-class CostReport:              # costmodel.py CostReport, measured instead of simulated
+class CostReport:              # costmodel.py CostReport, measured instead of simulated (ns)
     t_launch: float = 0.0
     t_comp: float = 0.0
     t_mem: float = 0.0
@@ -162,6 +162,10 @@ class WorkloadPlan:
         self.pgls: dict[str, list[np.ndarray]] = {}
         self.check_names: list[str] = []
         self.flops_per_device = 0.0
+        # compute-only / communication-only twins of the fused launch, set by
+        # run() over the same operands: (rank, comm, stream) -> None
+        self._comp = None
+        self._comm = None
         self._build()
 
     def _build(self):
@@ -182,6 +186,22 @@ class WorkloadPlan:
             e1.record(s)
         torch.cuda.synchronize()
         self.device_ns = getattr(self, "device_ns", 0.0) + 1e6 * max(a.elapsed_time(b) for a, b in ev)
+
+    def time_variant(self, comms, streams, fn) -> float:
+        """Device time (ns, CUDA events, max over ranks) of one launch of `fn`
+        on every rank's stream — the compute-only / comm-only twins."""
+        for r, c in enumerate(comms):             # warm (lazy scratch allocation happens here)
+            with torch.cuda.stream(streams[r]):
+                fn(r, c, streams[r])
+        torch.cuda.synchronize()
+        saved = getattr(self, "device_ns", 0.0)
+        self.device_ns = 0.0
+        with self._timed(streams):
+            for r, c in enumerate(comms):
+                with torch.cuda.stream(streams[r]):
+                    fn(r, c, streams[r])
+        t, self.device_ns = self.device_ns, saved
+        return t
 
     def oracle(self) -> dict[str, list[np.ndarray]]:
         raise NotImplementedError
@@ -248,6 +268,10 @@ class AgGemmPlan(WorkloadPlan):
             for d in range(n):
                 self.pgls["ag"][r][0, 0, d * t:(d + 1) * t] = g[d * m_loc:d * m_loc + t, :t]
                 self.pgls["c"][r][0, 0, d * t:(d + 1) * t] = cc[d * m_loc:d * m_loc + t, :t]
+        # twins: the local GEMM over the gathered rows; the all-gather alone
+        tmp = [(torch.empty_like(o[1]), torch.empty_like(o[0])) for o in outs]
+        self._comp = lambda r, c, s: ops.gemm(outs[r][0], ins[r][1], out=tmp[r][0])
+        self._comm = lambda r, c, s: ops.all_gather(c, ins[r][0], out=tmp[r][1], stream=s)
 
     def oracle(self):
         t, n = FUNC_TILE, self.num_devices
@@ -297,6 +321,10 @@ class GemmRsPlan(WorkloadPlan):
             o = o.float().cpu().numpy()
             self.pgls["out"][r][:] = 0
             self.pgls["out"][r][0, 0, r * blk:(r + 1) * blk] = o[:blk, :nd]
+        # twins: the local partial GEMM; the reduce-scatter of a partial alone
+        tmp = [(torch.empty_like(x), torch.empty_like(o)) for x, o in zip(ins, outs)]
+        self._comp = lambda r, c, s: ops.gemm(ins[r], eye, out=tmp[r][0])
+        self._comm = lambda r, c, s: ops.reduce_scatter(c, ins[r], out=tmp[r][1], stream=s)
 
     def oracle(self):
         n = self.num_devices
@@ -364,6 +392,10 @@ class GemmArPlan(WorkloadPlan):
         torch.cuda.synchronize()
         for r, o in enumerate(outs):
             self.pgls["acc"][r][0, 0] = o[:m, :nd].float().cpu().numpy()
+        # twins: the local GEMM; the all-reduce of the output alone
+        tmp = [torch.empty_like(o) for o in outs]
+        self._comp = lambda r, c, s: ops.gemm(ins[r], eye, out=tmp[r])
+        self._comm = lambda r, c, s: ops.all_reduce(c, outs[r], stream=s)
 
     def oracle(self):
         total = np.sum(self.inputs, axis=0)
@@ -412,9 +444,21 @@ class RingAttentionPlan(WorkloadPlan):
                 with torch.cuda.stream(streams[r]):
                     ops.ring_attention(c, q, q, v, out=outs[r][0], lse=outs[r][1], stream=streams[r])
         torch.cuda.synchronize()
+        twin = [(torch.empty(1, S_loc * n, H, D, device="cuda", dtype=torch.bfloat16),
+                 torch.empty(n * S_loc, H * D, device="cuda", dtype=torch.bfloat16),
+                 torch.empty(1, S_loc, H, D, device="cuda", dtype=torch.bfloat16),
+                 torch.empty(1, H, S_loc, device="cuda", dtype=torch.float32)) for _ in range(n)]
         outs = [o for o, _ in outs]
         for r, o in enumerate(outs):
             self.pgls["visited"][r][0, 0] = o[0, 0, :, :t].float().cpu().numpy() * (S_loc * n)
+        # twins: attention over all n shards held locally; the K and V all-gathers alone
+        self._comp = lambda r, c, s: ops.attention(ins[r][0], twin[r][0], twin[r][0], out=twin[r][2], lse=twin[r][3],
+                                                   stream=s)
+
+        def comm(r, c, s):
+            ops.all_gather(c, ins[r][0].reshape(S_loc, H * D), out=twin[r][1], stream=s)
+            ops.all_gather(c, ins[r][1].reshape(S_loc, H * D), out=twin[r][1], stream=s)
+        self._comm = comm
 
     def oracle(self):
         total = np.sum(self.kv, axis=0)
@@ -696,8 +740,17 @@ def execute_kernel(spec: LcscKernelSpec, workload: WorkloadPlan, profile=None, o
     torch.cuda.synchronize()                  # staged inputs visible to every rank's stream
     t0 = time.perf_counter()
     workload.device_ns = 0.0
+    t_comp = t_comm = None
     try:
         workload.run(comms, spec, streams)
+        for c in comms:
+            c.check()
+        # time decomposition (assemble_report, lcsc.py:110-138), measured: the
+        # plan's compute-only and communication-only twins on the same operands
+        if workload._comp is not None:
+            t_comp = workload.time_variant(comms, streams, workload._comp)
+        if workload._comm is not None:
+            t_comm = workload.time_variant(comms, streams, workload._comm)
         for c in comms:
             c.check()
     finally:
@@ -707,8 +760,25 @@ def execute_kernel(spec: LcscKernelSpec, workload: WorkloadPlan, profile=None, o
     # device time of the fused ops (CUDA events, max over ranks); host wall
     # time only if a plan launched nothing under the timer
     t_ns = workload.device_ns or (time.perf_counter() - t0) * 1e9
-    report = CostReport(t_total=t_ns, achieved_flops=workload.flops_per_device * workload.num_devices / (t_ns / 1e9))
-    return ExecResult(report=report, pgls=dict(workload.pgls))
+    return ExecResult(report=assemble_report(t_ns, t_comp, t_comm, workload.flops_per_device * workload.num_devices),
+                      pgls=dict(workload.pgls))
+
+
+def assemble_report(t_total: float, t_comp: Optional[float], t_comm: Optional[float],
+                    total_flops: float = 0.0) -> CostReport:
+    """CostReport from measured device times (ns): the fused launch, its
+    compute-only twin (the reference's compute baseline) and its
+    communication-only twin; a pure collective is all communication.
+    comm_ratio = the share of the fused time not explained by compute
+    (lcsc.py:130-134, the paper's non-overlapped communication ratio)."""
+    comp = t_comp or 0.0
+    comm = t_comm if t_comm is not None else (t_total if t_comp is None else 0.0)
+    non_overlap = max(0.0, t_total - max(comp, comm))
+    r = CostReport(t_comp=comp, t_comm=comm, t_non_overlap=non_overlap, t_total=t_total)
+    if t_total > 0:
+        r.comm_ratio = max(0.0, (t_total - comp) / t_total) if comp > 0 else non_overlap / t_total
+        r.achieved_flops = total_flops / (t_total / 1e9)
+    return r
 
 
 def check_oracle(plan: WorkloadPlan):

@@ -77,3 +77,17 @@ def test_check_oracle_reports_first_divergence():
     assert compat.check_oracle(plan) is None
     plan.pgls["acc"][2][0, 0, 1, 5] += 1.0
     assert compat.check_oracle(plan) == ("acc", (2, 0, 0, 1, 5))
+
+
+def test_assemble_report_decomposition():
+    """Measured decomposition (lcsc.py:110-138 semantics): non-overlap = the
+    fused time not covered by the larger twin; comm ratio against the compute
+    baseline; a pure collective is all communication."""
+    r = compat.assemble_report(100.0, 60.0, 30.0, 1e9)
+    assert r.t_comp == 60.0 and r.t_comm == 30.0
+    assert r.t_non_overlap == 40.0 and r.comm_ratio == pytest.approx(0.4)
+    assert r.achieved_flops == pytest.approx(1e9 / 100e-9)
+    r = compat.assemble_report(100.0, None, None)
+    assert r.t_comm == 100.0 and r.t_non_overlap == 0.0 and r.comm_ratio == 0.0
+    r = compat.assemble_report(50.0, 60.0, 10.0)            # faster than the compute twin: ratio floors at 0
+    assert r.comm_ratio == 0.0 and r.t_non_overlap == 0.0
