@@ -20,14 +20,18 @@
 //       warps 4-7 / 8-11 softmax of tile 0 / 1: max pass, lazy rescale of O
 //                              in TMEM, exp2, P (bf16x2) back into TMEM;
 //                              final epilogue
-//     The running (O, m, l) state crosses ring steps through global memory
-//     (fp32), merged by log-sum-exp; the last step writes o (bf16) and lse.
-//   * communication: the shard of step s+1 is pulled from its owner's
-//     symmetric buffer by the copy engine (the paper's 726 GB/s CE path,
-//     PAPER.md:127) on a side stream while step s computes; a 2-slot local
-//     buffer and CUDA events order reuse. Pulling from the owner (not the
-//     neighbour) moves the same bytes per link on a uniform NVSwitch fabric
-//     and needs no per-step neighbour handshake.
+//   * ring (n > 1), the reference's schedule (workloads.py:644-685): work
+//     units are (step, item) in step-major order over the persistent compute
+//     CTAs. Step 0 reads the local shard; step s >= 1 reads slot s & 1 of a
+//     2-slot local stage. Communicator CTAs (the last CTAs of the grid, the
+//     inter-SM schedule) TMA-pull the shard of rank (r - s) mod n from its
+//     owner's symmetric K/V (peer VA -> smem -> slot, cp.async.bulk) as soon
+//     as every unit of step s - 2 has finished reading that slot, and publish
+//     the step (signal -> wait); a unit's loader waits for its step. Each
+//     unit leaves its (O, m, l) for the item in an fp32 state that the next
+//     step's unit of the same item merges in ascending step order
+//     (log-sum-exp); the last step writes o (bf16) and lse. Per rank: 2
+//     K/V slots, not n.
 #include "pk_host.h"
 #include "pk_ptx.cuh"
 #include <algorithm>
@@ -83,7 +87,40 @@ struct AttnArgs {
   uint32_t* item_count;          // [items * 2] segments finished per (item, tile); re-armed by the merger
   int tail_items;                // R: the last R items are split over tail_units CTAs (0: no split)
   int tail_units;
+  // device-staged ring (ring_steps > 1): see the header comment
+  CUtensorMap tm_ks, tm_vs;      // the 2-slot stage, [2B, S, H, D] (slot = batch / B)
+  int ring_steps;                // n
+  int ring_comm;                 // communicator CTAs (the last ones of the grid)
+  int rank, world;
+  const uint8_t* ring_src_k[8];  // every rank's K / V shard (peer VAs)
+  const uint8_t* ring_src_v[8];
+  uint8_t* stage_k;              // [2][shard]
+  uint8_t* stage_v;
+  long long shard_bytes;
+  float* ring_state;             // [items][2 tiles][128 rows][AT_PART_ROW]: running (O, m, l)
+  uint32_t* ring_ctr;            // counters (RingCtr); zero at launch, re-armed by the last CTA
+  uint32_t* ready_local;         // [n] shard-ready signals received (source rank)
+  uint32_t* ready_peer[8];
+  uint32_t* done_local;          // [n] done-reading-my-shard signals received
+  uint32_t* done_peer[8];
 };
+
+// Word offsets of the ring counters (ring_ctr): per step [0, n) slot ready,
+// [n, 2n) units finished reading their step's K/V, [2n, 3n) communicator CTAs
+// finished their share of the step; 3n communicator CTAs finished; 3n + 1
+// CTAs finished (the last re-arms everything); then per (item, tile) the steps
+// merged so far.
+struct RingCtr {
+  uint32_t* base;
+  int n;
+  PK_DEV uint32_t* ready(int s) const { return base + s; }
+  PK_DEV uint32_t* units(int s) const { return base + n + s; }
+  PK_DEV uint32_t* pieces(int s) const { return base + 2 * n + s; }
+  PK_DEV uint32_t* comm_done() const { return base + 3 * n; }
+  PK_DEV uint32_t* ctas_done() const { return base + 3 * n + 1; }
+  PK_DEV uint32_t* merged(int item, int x) const { return base + 3 * n + 2 + 2 * item + x; }
+};
+__host__ __device__ inline size_t ring_ctr_words(int n, int items) { return (size_t)3 * n + 2 + 2 * (size_t)items; }
 
 // Partial state of one (slot, tile, row): D floats of unnormalised O, then m, l.
 constexpr int AT_PART_ROW = AT_D + 4;            // padded to 16 B (float4 rows)
@@ -210,6 +247,9 @@ __device__ unsigned long long g_attn_prof[8];
 // them in ascending CTA order (deterministic) and writes o / lse.
 // Barrier phases count K/V blocks (g), blocks per tile (gx) and segments per
 // tile (segx) across segments.
+// RING: the device-staged ring schedule (a separate instantiation, so the
+// single-GPU kernel's register allocation is untouched by the ring code)
+template <bool RING>
 __global__ void __launch_bounds__(AT_THREADS, 1) attn_fwd_kernel(const __grid_constant__ AttnArgs a) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -242,6 +282,13 @@ __global__ void __launch_bounds__(AT_THREADS, 1) attn_fwd_kernel(const __grid_co
   sp.T = (uint32_t)a.tail_items * (uint32_t)nblk;
   const int nfull = items - a.tail_items;           // CTAs [0, nfull) run whole items
   const int me = (int)blockIdx.x - nfull;           // tail CTA index (< 0: a whole-item CTA)
+  // ring mode: units (step, item) step-major over the compute CTAs; the last
+  // ring_comm CTAs are communicators
+  constexpr bool ring = RING;
+  const int ncompute = ring ? (int)gridDim.x - a.ring_comm : (int)gridDim.x;
+  const bool is_comm = ring && (int)blockIdx.x >= ncompute;
+  const RingCtr rc{a.ring_ctr, a.ring_steps};
+  const int bps = a.blocks_per_step;
   const int t0 = me >= 0 ? (int)sp.tstart(me) : 0, t1 = me >= 0 ? (int)sp.tstart(me + 1) : 0;
   // segment walk shared by every role: item, key blocks [j0, j1), pair shape
   struct SegInfo { int item, ti, j0, j1, qp, h, b, ntile; };
@@ -249,8 +296,17 @@ __global__ void __launch_bounds__(AT_THREADS, 1) attn_fwd_kernel(const __grid_co
     int k;                                           // -1: the whole item pending, -2: done; else tail block
   };
   auto seg_next = [&](SegIter& it, SegInfo& g) -> bool {
-    if (it.k == -2) return false;
-    if (it.k == -1) {
+    if (ring) {                                      // it.k = next unit index
+      if (it.k >= a.ring_steps * items) return false;
+      const int u = it.k;
+      it.k += ncompute;
+      g.item = u % items;
+      g.ti = -1;
+      g.j0 = (u / items) * bps;
+      g.j1 = g.j0 + bps;
+    } else if (it.k == -2) {
+      return false;
+    } else if (it.k == -1) {
       g.item = (int)blockIdx.x;
       g.ti = -1;
       g.j0 = 0;
@@ -270,9 +326,9 @@ __global__ void __launch_bounds__(AT_THREADS, 1) attn_fwd_kernel(const __grid_co
     g.ntile = (2 * g.qp + 1 < q_tiles) ? 2 : 1;      // the last pair may hold one tile
     return true;
   };
-  auto seg_begin = [&]() { SegIter it; it.k = me < 0 ? -1 : t0; return it; };
+  auto seg_begin = [&]() { SegIter it; it.k = ring ? (int)blockIdx.x : (me < 0 ? -1 : t0); return it; };
 
-  if (warp == 0 && lane == 0) {
+  if (warp == 0 && lane == 0 && !is_comm) {
     mbar_init(q_full, 1);
     mbar_init(q_empty, 1);
     for (int i = 0; i < AT_KSTAGES; ++i) { mbar_init(&k_full[i], 1); mbar_init(&k_empty[i], 1); }
@@ -284,7 +340,13 @@ __global__ void __launch_bounds__(AT_THREADS, 1) attn_fwd_kernel(const __grid_co
     }
     fence_mbar_init();
   }
-  if (warp == 2) tmem_alloc<AT_TMEM_COLS, 1>(tmem_slot);
+  if (warp == 2 && !is_comm) tmem_alloc<AT_TMEM_COLS, 1>(tmem_slot);
+  // ring: this rank's shard is readable (stream order) -> signal() every rank
+  if (ring && blockIdx.x == 0 && threadIdx.x == 0) {
+    call_note(a.call);
+    fence_sys();
+    for (int d = 0; d < a.world; ++d) signal_add(a.ready_peer[d] + a.rank, 1u);
+  }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -293,16 +355,110 @@ __global__ void __launch_bounds__(AT_THREADS, 1) attn_fwd_kernel(const __grid_co
 
   // registers follow the roles: warpgroup 0 (loader, MMA, allocator, idle)
   // needs few, the two softmax warpgroups hold a whole 128-key S row each
-  if (warp < 4) {
+  if (is_comm) {
+    // ------------------------------------------------------------ ring communicator
+    // Pull step s's shard (rank (r - s) mod n, workloads.py:666-681) into slot
+    // s & 1 once every unit of step s - 2 has read that slot: the K and V
+    // shards are cut into 32 KB pieces striped over the communicator CTAs;
+    // one thread per CTA moves its pieces peer VA -> smem -> slot
+    // (cp.async.bulk, store_async) and the last CTA done with a step
+    // publishes it (signal; the compute loaders wait).
+    if (warp == 0 && lane == 0) {
+      constexpr int PIECE = 32768;
+      constexpr int NBUF = 6;                         // 192 KB: the Q / K / V buffers, unused here
+      uint64_t* cbar = bars;
+      for (int i = 0; i < NBUF; ++i) mbar_init(&cbar[i], 1);
+      fence_mbar_init();
+      const int me_c = (int)blockIdx.x - ncompute, nc = a.ring_comm, n = a.ring_steps;
+      const long long ppt = (a.shard_bytes + PIECE - 1) / PIECE;           // pieces per tensor
+      const long long per_step = 2 * ppt;                                  // K pieces, then V pieces
+      const long long mine = per_step > me_c ? (per_step - 1 - me_c) / nc + 1 : 0;
+      const uint32_t ready_expect = call_get(a.call, 1);
+      uint32_t phase = 0;
+      long long gp = 0;                                                    // pieces moved so far
+      bool ok = true;
+      for (int s = 1; s < n; ++s) {
+        const int src = (a.rank - s + n) % n;
+        if (ok && s >= 3) ok = wait_geq(rc.units(s - 2), (uint32_t)items, a.err, a.timeout_ns);
+        if (ok) ok = wait_geq(a.ready_local + src, ready_expect, a.err, a.timeout_ns);
+        fence_async_global();
+        uint8_t* dk = a.stage_k + (long long)(s & 1) * a.shard_bytes;
+        uint8_t* dv = a.stage_v + (long long)(s & 1) * a.shard_bytes;
+        auto piece = [&](long long k, const uint8_t** sp, uint8_t** dp, uint32_t* bytes) {
+          const long long q = me_c + k * nc;
+          const bool isv = q >= ppt;
+          const long long off = (isv ? q - ppt : q) * PIECE;
+          *sp = (isv ? a.ring_src_v[src] : a.ring_src_k[src]) + off;
+          *dp = (isv ? dv : dk) + off;
+          *bytes = (uint32_t)min((long long)PIECE, a.shard_bytes - off);
+        };
+        auto issue = [&](long long k) {
+          const uint8_t* sp;
+          uint8_t* dp;
+          uint32_t bytes;
+          piece(k, &sp, &dp, &bytes);
+          const int b = (int)((gp + k) % NBUF);
+          mbar_arrive_expect_tx(&cbar[b], bytes);
+          bulk_g2s(smem + (size_t)b * PIECE, sp, bytes, &cbar[b]);
+        };
+        if (ok) {
+          for (long long k = 0; k < mine && k < NBUF - 1; ++k) issue(k);
+          for (long long k = 0; k < mine; ++k) {
+            const int b = (int)((gp + k) % NBUF);
+            mbar_wait(&cbar[b], (phase >> b) & 1);
+            phase ^= 1u << b;
+            const uint8_t* sp;
+            uint8_t* dp;
+            uint32_t bytes;
+            piece(k, &sp, &dp, &bytes);
+            bulk_s2g(dp, smem + (size_t)b * PIECE, bytes);
+            bulk_commit();
+            if (k + NBUF - 1 < mine) {
+              bulk_wait_read<1>();                     // the buffer of piece k + NBUF - 1 (last used by k - 1) was read
+              issue(k + NBUF - 1);
+            }
+          }
+          bulk_wait<0>();                              // my share of step s is in the slot
+          gp += mine;
+        }
+        fence_async_global();
+        __threadfence();
+        if (atomicAdd(rc.pieces(s), 1u) == (uint32_t)nc - 1)
+          asm volatile("st.release.gpu.global.u32 [%0], %1;" :: "l"(rc.ready(s)), "r"(1u) : "memory");
+      }
+      // every peer shard has been read: the last communicator CTA tells the owners
+      __threadfence();
+      if (atomicAdd(rc.comm_done(), 1u) == (uint32_t)nc - 1) {
+        fence_sys();
+        for (int d = 0; d < a.world; ++d) signal_add(a.done_peer[d] + a.rank, 1u);
+      }
+    }
+    __syncwarp();
+  } else if (warp < 4) {
+  // (the CTA holds 168 x 384 registers: 56 + 2 x 224 uses exactly that, so
+  // the softmax warpgroups' increase can complete)
   asm volatile("setmaxnreg.dec.sync.aligned.u32 56;\n" ::: "memory");
   if (warp == 0) {
     // ------------------------------------------------------------ loader (lane 0)
     if (lane == 0) {
       // key block j = ring step j / bps, block j % bps of that step's shard
-      const int bps = a.blocks_per_step;
       int ready_steps = 1;                               // step 0 (own shard) is always resident
+      int ring_ok = 0;                                   // ring: last step seen published
       const uint32_t flag_epoch = a.step_flags != nullptr ? call_get(a.call, 0) : 0u;
+      // ring: step 0 from the local shard, step s >= 1 from stage slot s & 1
+      auto kvmap = [&](const CUtensorMap* local, const CUtensorMap* stage, int step) {
+        return (ring && step > 0) ? stage : local;
+      };
+      auto kvb = [&](int step, int b) { return ring ? (step > 0 ? (step & 1) * a.B + b : b) : step * a.B + b; };
       auto step_ready = [&](int step) {
+        if (ring) {
+          if (step > 0 && step != ring_ok) {
+            wait_geq(rc.ready(step), 1u, a.err, a.timeout_ns);
+            fence_async_global();
+            ring_ok = step;
+          }
+          return;
+        }
         while (a.step_flags != nullptr && ready_steps <= step) {
           wait_geq(a.step_flags + ready_steps, flag_epoch, a.err, a.timeout_ns);
           fence_async_global();
@@ -319,8 +475,9 @@ __global__ void __launch_bounds__(AT_THREADS, 1) attn_fwd_kernel(const __grid_co
         if (g >= 2) { mbar_arrive(&k_full[st]); return; }
 #endif
         mbar_arrive_expect_tx(&k_full[st], AT_K_BYTES);
-        tma_load_4d(&a.tm_k, &k_full[st], kb, 0, h, row, step * a.B + b);
-        tma_load_4d(&a.tm_k, &k_full[st], kb + AT_K_BYTES / 2, 64, h, row, step * a.B + b);
+        const CUtensorMap* km = kvmap(&a.tm_k, &a.tm_ks, step);
+        tma_load_4d(km, &k_full[st], kb, 0, h, row, kvb(step, b));
+        tma_load_4d(km, &k_full[st], kb + AT_K_BYTES / 2, 64, h, row, kvb(step, b));
       };
       int g = 0, seg = 0;
       SegIter it = seg_begin();
@@ -345,8 +502,9 @@ __global__ void __launch_bounds__(AT_THREADS, 1) attn_fwd_kernel(const __grid_co
           if (gg >= 2) { mbar_arrive(&v_full[vs]); continue; }
 #endif
           mbar_arrive_expect_tx(&v_full[vs], AT_V_BYTES);
-          tma_load_4d(&a.tm_v, &v_full[vs], vb, 0, sg.h, row, step * a.B + sg.b);
-          tma_load_4d(&a.tm_v, &v_full[vs], vb + AT_V_BYTES / 2, 64, sg.h, row, step * a.B + sg.b);
+          const CUtensorMap* vm = kvmap(&a.tm_v, &a.tm_vs, step);
+          tma_load_4d(vm, &v_full[vs], vb, 0, sg.h, row, kvb(step, sg.b));
+          tma_load_4d(vm, &v_full[vs], vb + AT_V_BYTES / 2, 64, sg.h, row, kvb(step, sg.b));
         }
         g += len;
       }
@@ -396,6 +554,11 @@ __global__ void __launch_bounds__(AT_THREADS, 1) attn_fwd_kernel(const __grid_co
         const int gg = g + i;
         mbar_wait(&v_full[gg & 1], (gg >> 1) & 1);
         const bool more = i + 1 < len;
+        if (ring && !more && lane == 0) {
+          // every K/V block of this unit is in smem: its step's slot may be refilled
+          fence_async_global();
+          asm volatile("red.release.gpu.global.add.u32 [%0], 1;" :: "l"(rc.units(sg.j0 / bps)) : "memory");
+        }
         if (more) mbar_wait(&k_full[(gg + 1) % AT_KSTAGES], ((gg + 1) / AT_KSTAGES) & 1);
         for (int x = 0; x < sg.ntile; ++x) {
           const int gxx = x ? gx1 : gx0, sgx = x ? segx1 : segx0;
@@ -564,6 +727,51 @@ __global__ void __launch_bounds__(AT_THREADS, 1) attn_fwd_kernel(const __grid_co
     const int sq_idx = (2 * sg.qp + x) * AT_BM + row;                      // query index within the local shard
     const long long srow = ((long long)(sg.b * a.H + sg.h) * a.S_q + sq_idx);   // [B, H, S_q] row
     bool write_final = true;
+    if (ring) {
+      // merge with the item's state from steps < s (ascending steps), keep it
+      // for step s + 1, or finish at the last step
+      const int step = sg.j0 / bps;
+      float* stt = a.ring_state + ((long long)(2 * sg.item + x) * AT_BM + row) * AT_PART_ROW;
+      if (step > 0) {
+        if (lane == 0) wait_geq(rc.merged(sg.item, x), (uint32_t)step, a.err, a.timeout_ns);
+        __syncwarp();
+        const float mc = __ldcg(stt + AT_D), lc = __ldcg(stt + AT_D + 1);
+        const float mn = fmaxf(mc, m);
+        const float wa = (mc == -INFINITY) ? 0.f : fast_exp2(mc - mn);
+        const float wb = (m == -INFINITY) ? 0.f : fast_exp2(m - mn);
+        // 8 float4 in flight at a time: o[] already holds 128 registers
+#pragma unroll
+        for (int c8 = 0; c8 < AT_D / 32; ++c8) {
+          float4 v[8];
+#pragma unroll
+          for (int i2 = 0; i2 < 8; ++i2) v[i2] = __ldcg(reinterpret_cast<const float4*>(stt) + c8 * 8 + i2);
+#pragma unroll
+          for (int i2 = 0; i2 < 8; ++i2) {
+            const int e = 4 * (c8 * 8 + i2);
+            o[e + 0] = v[i2].x * wa + o[e + 0] * wb;
+            o[e + 1] = v[i2].y * wa + o[e + 1] * wb;
+            o[e + 2] = v[i2].z * wa + o[e + 2] * wb;
+            o[e + 3] = v[i2].w * wa + o[e + 3] * wb;
+          }
+          asm volatile("" ::: "memory");                // keep the next chunk's loads behind this one
+        }
+        l = lc * wa + l * wb;
+        m = mn;
+      }
+      if (step + 1 < a.ring_steps) {
+#pragma unroll
+        for (int i2 = 0; i2 < AT_D / 4; ++i2)
+          reinterpret_cast<float4*>(stt)[i2] = make_float4(o[4 * i2], o[4 * i2 + 1], o[4 * i2 + 2], o[4 * i2 + 3]);
+        stt[AT_D] = m;
+        stt[AT_D + 1] = l;
+        __threadfence();
+        asm volatile("bar.sync %0, 128;" :: "r"(1 + x) : "memory");
+        if (row == 0)
+          asm volatile("st.release.gpu.global.u32 [%0], %1;" :: "l"(rc.merged(sg.item, x)), "r"((uint32_t)step + 1)
+                       : "memory");
+        write_final = false;
+      }
+    }
     const uint32_t ib = (uint32_t)(sg.ti * nblk);              // tail items only
     const int c_lo = (sg.ti < 0 || sg.j0 == 0) ? me : sp.tcta_of(ib);
     const int c_hi = (sg.ti < 0 || sg.j1 == nblk) ? me : sp.tcta_of(ib + nblk - 1);
@@ -632,9 +840,25 @@ __global__ void __launch_bounds__(AT_THREADS, 1) attn_fwd_kernel(const __grid_co
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 2) {
+  if (warp == 2 && !is_comm) {
     tc_fence_after();
     tmem_dealloc<AT_TMEM_COLS, 1>(tmem);
+  }
+  if (ring) {
+    __shared__ int ring_last;
+    // the caller may reuse k / v once every rank has read them
+    if (blockIdx.x == 0 && threadIdx.x == 0)
+      for (int d = 0; d < a.world; ++d) wait_geq(a.done_local + d, call_get(a.call, 2), a.err, a.timeout_ns);
+    if (threadIdx.x == 0) {
+      __threadfence();
+      ring_last = atomicAdd(rc.ctas_done(), 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (ring_last) {                                 // every CTA is done: re-arm the counters for the next launch
+      __threadfence();
+      const int words = (int)ring_ctr_words(a.ring_steps, items);
+      for (int i = threadIdx.x; i < words; i += blockDim.x) a.ring_ctr[i] = 0u;
+    }
   }
 }
 
@@ -930,47 +1154,11 @@ __global__ void __launch_bounds__(AT_THREADS, 1) attn2_fwd_kernel(const __grid_c
   }
 }
 
-// ---------------------------------------------------------------- sync kernels
-__global__ void sync_signal_kernel(uint32_t* p0, uint32_t* p1, uint32_t* p2, uint32_t* p3, uint32_t* p4,
-                                   uint32_t* p5, uint32_t* p6, uint32_t* p7, int n) {
-  uint32_t* ps[8] = {p0, p1, p2, p3, p4, p5, p6, p7};
-  fence_sys();
-  for (int d = 0; d < n; ++d) signal_add(ps[d], 1u);
-}
-__global__ void flag_set_kernel(uint32_t* flag, const CallRef call) {
-  fence_sys();
-  asm volatile("st.release.gpu.global.u32 [%0], %1;" :: "l"(flag), "r"(call_get(call, 0)) : "memory");
-}
-// wait until every rank's counter reaches the call's count `which` (1 ready, 2 done)
-__global__ void sync_wait_kernel(const uint32_t* counters, int n, const CallRef call, int which, uint32_t* err,
-                                 uint64_t timeout) {
-  call_note(call);
-  const uint32_t expected = call_get(call, which);
-  for (int d = 0; d < n; ++d) wait_geq(counters + d, expected, err, timeout);
-}
-
 int preload_attn() {
   cudaFuncAttributes fa;
-  PK_CUDA(cudaFuncGetAttributes(&fa, attn_fwd_kernel));
+  PK_CUDA(cudaFuncGetAttributes(&fa, attn_fwd_kernel<false>));
+  PK_CUDA(cudaFuncGetAttributes(&fa, attn_fwd_kernel<true>));
   PK_CUDA(cudaFuncGetAttributes(&fa, attn2_fwd_kernel));
-  PK_CUDA(cudaFuncGetAttributes(&fa, sync_signal_kernel));
-  PK_CUDA(cudaFuncGetAttributes(&fa, sync_wait_kernel));
-  PK_CUDA(cudaFuncGetAttributes(&fa, flag_set_kernel));
-  return PK_OK;
-}
-
-static int signal_all(Comm* c, int which_off, cudaStream_t st) {
-  uint32_t* ps[8] = {};
-  for (int r = 0; r < c->world; ++r) ps[r] = static_cast<uint32_t*>(c->sync->peers[r]) + which_off + c->rank;
-  sync_signal_kernel<<<1, 1, 0, st>>>(ps[0], ps[1], ps[2], ps[3], ps[4], ps[5], ps[6], ps[7], c->world);
-  PK_CUDA(cudaGetLastError());
-  return PK_OK;
-}
-static int wait_all(Comm* c, int which_off, const CallRef& call, cudaStream_t st) {
-  uint32_t* local = static_cast<uint32_t*>(c->sync->local);
-  sync_wait_kernel<<<1, 1, 0, st>>>(local + which_off, c->world, call, which_off == kSyncReady ? 1 : 2,
-                                    local + kSyncErr, c->timeout_ns);
-  PK_CUDA(cudaGetLastError());
   return PK_OK;
 }
 
@@ -1020,7 +1208,7 @@ static int launch_attn(AttnScratch& scr, int num_sms, AttnArgs& a, cudaStream_t 
     PK_CUDA(cudaLaunchKernelEx(&cfg, attn2_fwd_kernel, a));
     return PK_OK;
   }
-  PK_TRY(ensure_smem_attr((const void*)attn_fwd_kernel, AT_SMEM));
+  PK_TRY(ensure_smem_attr((const void*)attn_fwd_kernel<false>, AT_SMEM));
   const int items = a.B * a.H * ((a.S_q / AT_BM + 1) / 2);
   const int nblk = a.S_kv / AT_BN;
   int sms = num_sms;
@@ -1056,7 +1244,7 @@ static int launch_attn(AttnScratch& scr, int num_sms, AttnArgs& a, cudaStream_t 
   }
   a.part = static_cast<float*>(scr.part);
   a.item_count = scr.count;
-  attn_fwd_kernel<<<grid, AT_THREADS, AT_SMEM, st>>>(a);
+  attn_fwd_kernel<false><<<grid, AT_THREADS, AT_SMEM, st>>>(a);
   PK_CUDA(cudaGetLastError());
   return PK_OK;
 }
@@ -1070,10 +1258,10 @@ static std::map<std::pair<int, cudaStream_t>, AttnScratch> g_attn_scratch;
 int attn_local(const pk_tensor* q, const pk_tensor* k, const pk_tensor* v, pk_tensor* o, pk_tensor* lse,
                float scale, cudaStream_t st);
 
-enum { kScratchAttnK = 0, kScratchAttnV = 1, kScratchAttnStage = 7 };
+enum { kScratchAttnK = 0, kScratchAttnV = 1 };
 
 int ring_attn_fwd(Comm* c, const pk_tensor* q, const pk_tensor* k, const pk_tensor* v, pk_tensor* o, pk_tensor* lse,
-                  float scale, cudaStream_t st) {
+                  float scale, const pk_sched* sched, cudaStream_t st) {
   int64_t B, S, H, D, B2, S2, H2, D2;
   PK_TRY(check_bshd(q, "q", &B, &S, &H, &D));
   PK_TRY(check_bshd(k, "k", &B2, &S2, &H2, &D2));
@@ -1121,66 +1309,78 @@ int ring_attn_fwd(Comm* c, const pk_tensor* q, const pk_tensor* k, const pk_tens
     PK_CUDA(cudaMemcpyAsync(s->local, v->ptr, shard, cudaMemcpyDeviceToDevice, st));
     for (int r = 0; r < n; ++r) vp[r] = s->peers[r];
   }
-  // Local staging: K and V of every ring step, step s at batch index s*B + b
-  // ([n*B, S/n, H, D] each); slot 0 is this rank's own shard. B200's HBM holds
-  // all n shards, so the ring's 2-slot rotation (workloads.py:644-681) becomes
-  // a single pass over n*S/n keys in the same visiting order (r, r-1, ...):
-  // one launch, O stays in TMEM across steps, no per-step LSE merge.
-  Pgl* stage;
-  PK_TRY(comm_scratch(c, kScratchAttnStage, 2 * (size_t)n * shard, &stage));
-  uint8_t* kst = static_cast<uint8_t*>(stage->local);
-  uint8_t* vst = kst + (size_t)n * shard;
-  PK_CUDA(cudaMemcpyAsync(kst, kp[c->rank], shard, cudaMemcpyDeviceToDevice, st));
-  PK_CUDA(cudaMemcpyAsync(vst, vp[c->rank], shard, cudaMemcpyDeviceToDevice, st));
-  if (!c->side) PK_CUDA(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
-  cudaStream_t side = c->side;
-  struct Events {
-    cudaEvent_t e[3] = {nullptr, nullptr, nullptr};
-    ~Events() { for (auto x : e) if (x) cudaEventDestroy(x); }
-  } evs;
-  for (auto& x : evs.e) PK_CUDA(cudaEventCreateWithFlags(&x, cudaEventDisableTiming));
-  cudaEvent_t ev_start = evs.e[0], ev_side = evs.e[1], ev_copies = evs.e[2];
-  uint32_t* flags = static_cast<uint32_t*>(c->sync->local) + kSyncFlags;    // per-step "staged" flags
-  CallRef call;
-  PK_TRY(begin_call(c, 1, 1, 1, st, &call));
-  // 1. my shard is ready -> tell everyone; the side stream pulls every peer shard
-  //    with the copy engine in ring order and flags each step as it lands.
-  PK_TRY(signal_all(c, kSyncReady, st));
-  PK_CUDA(cudaEventRecord(ev_start, st));
-  PK_CUDA(cudaStreamWaitEvent(side, ev_start, 0));
-  PK_TRY(wait_all(c, kSyncReady, call, side));
-  for (int s = 1; s < n; ++s) {
-    const int src = ((c->rank - s) % n + n) % n;                             // workloads.py:666-681
-    PK_CUDA(cudaMemcpyAsync(kst + (size_t)s * shard, kp[src], shard, cudaMemcpyDeviceToDevice, side));
-    PK_CUDA(cudaMemcpyAsync(vst + (size_t)s * shard, vp[src], shard, cudaMemcpyDeviceToDevice, side));
-    flag_set_kernel<<<1, 1, 0, side>>>(flags + s, call);
-    PK_CUDA(cudaGetLastError());
+  // Rank-local buffers (stream-ordered): the 2-slot K / V stage, the running
+  // (O, m, l) state of every item, the ring counters (zeroed once here, then
+  // re-armed by each launch's last CTA).
+  const int items = (int)(B * H * ((S / AT_BM + 1) / 2));
+  const size_t stage_bytes = 4 * shard;
+  const size_t state_bytes = (size_t)items * 2 * AT_BM * AT_PART_ROW * sizeof(float);
+  const size_t ctr_bytes = ring_ctr_words(n, items) * sizeof(uint32_t);
+  const size_t need = stage_bytes + state_bytes + ctr_bytes;
+  if (c->ring_buf_bytes < need) {
+    if (c->ring_buf) PK_CUDA(cudaFreeAsync(c->ring_buf, st));
+    PK_CUDA(cudaMallocAsync(&c->ring_buf, need, st));
+    c->ring_buf_bytes = need;
+    c->ring_ctr_bytes = 0;
   }
-  PK_CUDA(cudaEventRecord(ev_copies, side));
-  // 2. done reading every peer's shard (side) -> signal; join the side stream.
-  PK_TRY(signal_all(c, kSyncDone, side));
-  PK_CUDA(cudaEventRecord(ev_side, side));
-  // 3. one attention launch over all n*S/n keys; the loader waits step flags.
-  PK_TRY(tmap_bshd(&a.tm_k, kst, (int64_t)n * B, S, H, AT_BN));
-  PK_TRY(tmap_bshd(&a.tm_k2, kst, (int64_t)n * B, S, H, AT_BN / 2));
-  PK_TRY(tmap_bshd(&a.tm_v, vst, (int64_t)n * B, S, H, AT_BN));
+  uint8_t* rb = static_cast<uint8_t*>(c->ring_buf);
+  uint32_t* ctr = reinterpret_cast<uint32_t*>(rb + stage_bytes + state_bytes);
+  if (c->ring_ctr_ptr != ctr || c->ring_ctr_bytes < ctr_bytes) {   // fresh counters at a new offset
+    PK_CUDA(cudaMemsetAsync(ctr, 0, c->ring_buf_bytes - stage_bytes - state_bytes, st));
+    c->ring_ctr_ptr = ctr;
+    c->ring_ctr_bytes = c->ring_buf_bytes - stage_bytes - state_bytes;
+  }
+  a.stage_k = rb;
+  a.stage_v = rb + 2 * shard;
+  a.ring_state = reinterpret_cast<float*>(rb + stage_bytes);
+  a.ring_ctr = ctr;
+  a.shard_bytes = (long long)shard;
+  a.ring_steps = n;
+  a.rank = c->rank;
+  a.world = n;
+  for (int r = 0; r < n; ++r) {
+    a.ring_src_k[r] = static_cast<const uint8_t*>(kp[r]);
+    a.ring_src_v[r] = static_cast<const uint8_t*>(vp[r]);
+  }
+  uint32_t* local = static_cast<uint32_t*>(c->sync->local);
+  a.ready_local = local + kSyncReady;
+  a.done_local = local + kSyncDone;
+  for (int r = 0; r < n; ++r) {
+    a.ready_peer[r] = static_cast<uint32_t*>(c->sync->peers[r]) + kSyncReady;
+    a.done_peer[r] = static_cast<uint32_t*>(c->sync->peers[r]) + kSyncDone;
+  }
+  // step 0 reads the local shard, step s >= 1 stage slot s & 1 ([2B, S, H, D])
+  PK_TRY(tmap_bshd(&a.tm_k, kp[c->rank], B, S, H, AT_BN));
+  PK_TRY(tmap_bshd(&a.tm_v, vp[c->rank], B, S, H, AT_BN));
+  PK_TRY(tmap_bshd(&a.tm_ks, a.stage_k, 2 * B, S, H, AT_BN));
+  PK_TRY(tmap_bshd(&a.tm_vs, a.stage_v, 2 * B, S, H, AT_BN));
   a.S_kv = (int)(n * S);
   a.blocks_per_step = (int)(S / AT_BN);
-  a.step_flags = flags;
-  a.call = call;
-  if (c->local_group) {
-    // Emulated ranks share this GPU's SMs: CTAs spinning on a step flag could
-    // hold the SMs the flag's producer chain needs (another rank's previous
-    // kernel). Start the attention after the copies instead of overlapping.
-    PK_CUDA(cudaStreamWaitEvent(st, ev_copies, 0));
-    a.step_flags = nullptr;
+  // Communicator CTAs (inter-SM schedule): enough TMA-driven SMs to pull a
+  // step's K + V within the step's compute (+30 %), at the paper's B200 TMA
+  // rate (669 GB/s saturating at 15 SMs) and ~1.2 PF/s of
+  // attention over this rank's SMs; the schedule may set it. Emulated ranks
+  // keep a quarter of their SMs at most.
+  int ncomm;
+  if (sched && sched->num_comm_sms > 0) {
+    ncomm = sched->num_comm_sms;
+  } else {
+    const double t_step = 4.0 * B * H * (double)S * S * AT_D / (1.2e15 * c->num_sms / 148.0);   // this rank's SMs
+    ncomm = (int)std::ceil(1.3 * 2.0 * (double)shard / (t_step * (669e9 / 15)));
+    ncomm = std::max(2, std::min(16, ncomm));
   }
-  a.err = static_cast<uint32_t*>(c->sync->local) + kSyncErr;
+  if (c->local_group) ncomm = std::min(ncomm, std::max(1, c->num_sms / 4));
+  const int ncompute = std::min(n * items, c->num_sms - ncomm);
+  if (ncompute < 1) return fail(PK_ERR_INVALID, "ring_attention: num_comm_sms leaves no compute SMs");
+  a.ring_comm = ncomm;
+  a.err = local + kSyncErr;
   a.timeout_ns = c->timeout_ns;
-  PK_TRY(launch_attn(c->attn, c->num_sms, a, st));
-  // 4. wait until every peer is done with my shard before the caller may reuse it.
-  PK_CUDA(cudaStreamWaitEvent(st, ev_side, 0));
-  PK_TRY(wait_all(c, kSyncDone, call, st));
+  CallRef call;
+  PK_TRY(begin_call(c, 1, 1, 1, st, &call));
+  a.call = call;
+  PK_TRY(ensure_smem_attr((const void*)attn_fwd_kernel<true>, AT_SMEM));
+  attn_fwd_kernel<true><<<ncompute + ncomm, AT_THREADS, AT_SMEM, st>>>(a);
+  PK_CUDA(cudaGetLastError());
   return PK_OK;
 }
 
@@ -1241,7 +1441,6 @@ extern "C" PK_API int pk_attn_fwd(const pk_tensor* q, const pk_tensor* k, const 
 extern "C" PK_API int pk_ring_attn_fwd(pk_comm* comm, const pk_tensor* q, const pk_tensor* k, const pk_tensor* v,
                                        pk_tensor* o, pk_tensor* lse, float softmax_scale, const pk_sched* sched,
                                        void* stream) {
-  (void)sched;
   if (!comm) return pk::fail(PK_ERR_INVALID, "null comm");
-  return pk::ring_attn_fwd(comm, q, k, v, o, lse, softmax_scale, (cudaStream_t)stream);
+  return pk::ring_attn_fwd(comm, q, k, v, o, lse, softmax_scale, sched, (cudaStream_t)stream);
 }

@@ -722,7 +722,7 @@ PK_API int pk_comm_destroy(pk_comm* c) {
   if (c->sync) pgl_free(c->sync);
   c->sync = nullptr;
   if (c->listen_fd >= 0) ::close(c->listen_fd);
-  if (c->side) cudaStreamDestroy(c->side);
+  if (c->ring_buf) cudaFree(c->ring_buf);
   if (c->attn.part) cudaFree(c->attn.part);
   if (c->attn.count) cudaFree(c->attn.count);
   if (c->ablate_stage) cudaFree(c->ablate_stage);

@@ -195,8 +195,11 @@ struct Comm {
   std::vector<Pending> pending;      // messages that arrived for a later collective
   std::vector<Pgl*> user_pgls;       // PGLs handed out through pk_pgl_alloc (zero-copy lookup)
   std::vector<Pgl*> retired;         // outgrown scratch PGLs (local groups free them at destroy)
-  cudaStream_t side = nullptr;       // side stream for copy-engine staging (ring attention)
   AttnScratch attn;                  // ring attention: stream-K partials + per-item counters
+  void* ring_buf = nullptr;          // ring attention (rank-local): 2-slot K/V stage | item states | counters
+  size_t ring_buf_bytes = 0;
+  uint32_t* ring_ctr_ptr = nullptr;  // where the zeroed counters start (a re-layout re-zeroes them)
+  size_t ring_ctr_bytes = 0;
   void* moe_idx = nullptr;           // MoE rank-local index scratch (count_done | slot_of | chunk counts)
   size_t moe_idx_bytes = 0;
   void* ablate_stage = nullptr;      // all_reduce_ablate staging channels (local)

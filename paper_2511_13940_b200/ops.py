@@ -260,11 +260,14 @@ def moe_combine(comm, y: torch.Tensor, topk_idx: torch.Tensor, weights: torch.Te
 
 
 def ring_attention(comm, q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, softmax_scale: float | None = None,
-                   out: torch.Tensor | None = None, lse: torch.Tensor | None = None, stream=None):
+                   out: torch.Tensor | None = None, lse: torch.Tensor | None = None, stream=None,
+                   schedule: dict | None = None):
     """Sequence-parallel ring attention forward, non-causal (RingAttentionPlan,
     workloads.py:616-716). q, k, v: this rank's [B, S/n, H, D] bf16 shards
     (D = 128, S/n % 128 == 0). At ring step s rank r attends to the KV shard of
-    rank (r - s) mod n. Returns (o [B, S/n, H, D] bf16, lse [B, H, S/n] fp32,
+    rank (r - s) mod n, which communicator CTAs of the same kernel pull into a
+    2-slot local stage while step s - 1 computes (schedule={"num_comm_sms": k}
+    sets their number). Returns (o [B, S/n, H, D] bf16, lse [B, H, S/n] fp32,
     natural log)."""
     _require_cuda(q, k, v)
     B, S, H, D = q.shape
@@ -278,7 +281,8 @@ def ring_attention(comm, q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, soft
     dq, dk, dv, do, dl = (_lib.tensor_desc(x) for x in (q, k, v, out, lse))
     import ctypes
     check(lib.pk_ring_attn_fwd(comm._h, _lib.ref(dq), _lib.ref(dk), _lib.ref(dv), _lib.ref(do), _lib.ref(dl),
-                               ctypes.c_float(softmax_scale), None, ctypes_stream(_stream(stream))), "ring_attention")
+                               ctypes.c_float(softmax_scale), _lib.ref(_sched(schedule)),
+                               ctypes_stream(_stream(stream))), "ring_attention")
     return out, lse
 
 
