@@ -709,68 +709,71 @@ __global__ void __launch_bounds__(AT_THREADS, 1) attn_fwd_kernel(const __grid_co
       AT_PROF_FLUSH();
     }
     // ------------------------------------------------------------ epilogue
+    float o[AT_D];
+    // ring, step s > 0: the item's running state from steps < s is loaded
+    // (all 32 vectors in flight) while the unit's last PV finishes, then
+    // merged chunk by chunk with O as it leaves TMEM (o[] holds the merge)
+    const int rstep = ring ? sg.j0 / bps : 0;
+    const bool has_state = ring && rstep > 0;
+    float* stt = ring ? a.ring_state + ((long long)(2 * sg.item + x) * AT_BM + row) * AT_PART_ROW : nullptr;
+    float m_s = -INFINITY, l_s = 0.f;
+    if constexpr (RING) {
+#pragma unroll
+      for (int i2 = 0; i2 < AT_D; ++i2) o[i2] = 0.f;            // no state: w_s = 0, w_u = 1 below
+    }
+    if (has_state) {
+      if (lane == 0) wait_geq(rc.merged(sg.item, x), (uint32_t)rstep, a.err, a.timeout_ns);
+      __syncwarp();
+#pragma unroll
+      for (int i2 = 0; i2 < AT_D / 4; ++i2) {
+        const float4 v = __ldcg(reinterpret_cast<const float4*>(stt) + i2);
+        o[4 * i2] = v.x; o[4 * i2 + 1] = v.y; o[4 * i2 + 2] = v.z; o[4 * i2 + 3] = v.w;
+      }
+      m_s = __ldcg(stt + AT_D);
+      l_s = __ldcg(stt + AT_D + 1);
+    }
     mbar_wait(&o_full[x], segx & 1);
     tc_fence_after();
-    float o[AT_D];
+    const float m_n = fmaxf(m_s, m);
+    const float w_s = (m_s == -INFINITY) ? 0.f : fast_exp2(m_s - m_n);     // state weight
+    const float w_u = (m == -INFINITY) ? 0.f : fast_exp2(m - m_n);         // this unit's weight
 #pragma unroll
     for (int c = 0; c < AT_D / 32; ++c) {
       uint32_t t[32];
       tmem_ld_32x32b_x32(t_o + c * 32, t);
       tmem_ld_wait();
+      if constexpr (RING) {
 #pragma unroll
-      for (int i2 = 0; i2 < 32; ++i2) o[c * 32 + i2] = __uint_as_float(t[i2]);
+        for (int i2 = 0; i2 < 32; ++i2) o[c * 32 + i2] = o[c * 32 + i2] * w_s + __uint_as_float(t[i2]) * w_u;
+      } else {
+#pragma unroll
+        for (int i2 = 0; i2 < 32; ++i2) o[c * 32 + i2] = __uint_as_float(t[i2]);
+      }
     }
     tc_fence_before();
     __syncwarp();
     if (lane == 0) mbar_arrive(&o_empty[x]);        // the next segment's PV may overwrite O
     ++segx;
+    if constexpr (RING) {
+      l = l_s * w_s + l * w_u;
+      m = m_n;
+    }
     const int sq_idx = (2 * sg.qp + x) * AT_BM + row;                      // query index within the local shard
     const long long srow = ((long long)(sg.b * a.H + sg.h) * a.S_q + sq_idx);   // [B, H, S_q] row
     bool write_final = true;
-    if (ring) {
-      // merge with the item's state from steps < s (ascending steps), keep it
-      // for step s + 1, or finish at the last step
-      const int step = sg.j0 / bps;
-      float* stt = a.ring_state + ((long long)(2 * sg.item + x) * AT_BM + row) * AT_PART_ROW;
-      if (step > 0) {
-        if (lane == 0) wait_geq(rc.merged(sg.item, x), (uint32_t)step, a.err, a.timeout_ns);
-        __syncwarp();
-        const float mc = __ldcg(stt + AT_D), lc = __ldcg(stt + AT_D + 1);
-        const float mn = fmaxf(mc, m);
-        const float wa = (mc == -INFINITY) ? 0.f : fast_exp2(mc - mn);
-        const float wb = (m == -INFINITY) ? 0.f : fast_exp2(m - mn);
-        // 8 float4 in flight at a time: o[] already holds 128 registers
+    if (ring && rstep + 1 < a.ring_steps) {
+      // keep the merged state for step s + 1 (steps merge in ascending order);
+      // the tile's 128 threads sync, then one release publishes all their rows
 #pragma unroll
-        for (int c8 = 0; c8 < AT_D / 32; ++c8) {
-          float4 v[8];
-#pragma unroll
-          for (int i2 = 0; i2 < 8; ++i2) v[i2] = __ldcg(reinterpret_cast<const float4*>(stt) + c8 * 8 + i2);
-#pragma unroll
-          for (int i2 = 0; i2 < 8; ++i2) {
-            const int e = 4 * (c8 * 8 + i2);
-            o[e + 0] = v[i2].x * wa + o[e + 0] * wb;
-            o[e + 1] = v[i2].y * wa + o[e + 1] * wb;
-            o[e + 2] = v[i2].z * wa + o[e + 2] * wb;
-            o[e + 3] = v[i2].w * wa + o[e + 3] * wb;
-          }
-          asm volatile("" ::: "memory");                // keep the next chunk's loads behind this one
-        }
-        l = lc * wa + l * wb;
-        m = mn;
-      }
-      if (step + 1 < a.ring_steps) {
-#pragma unroll
-        for (int i2 = 0; i2 < AT_D / 4; ++i2)
-          reinterpret_cast<float4*>(stt)[i2] = make_float4(o[4 * i2], o[4 * i2 + 1], o[4 * i2 + 2], o[4 * i2 + 3]);
-        stt[AT_D] = m;
-        stt[AT_D + 1] = l;
-        __threadfence();
-        asm volatile("bar.sync %0, 128;" :: "r"(1 + x) : "memory");
-        if (row == 0)
-          asm volatile("st.release.gpu.global.u32 [%0], %1;" :: "l"(rc.merged(sg.item, x)), "r"((uint32_t)step + 1)
-                       : "memory");
-        write_final = false;
-      }
+      for (int i2 = 0; i2 < AT_D / 4; ++i2)
+        reinterpret_cast<float4*>(stt)[i2] = make_float4(o[4 * i2], o[4 * i2 + 1], o[4 * i2 + 2], o[4 * i2 + 3]);
+      stt[AT_D] = m;
+      stt[AT_D + 1] = l;
+      asm volatile("bar.sync %0, 128;" :: "r"(1 + x) : "memory");
+      if (row == 0)
+        asm volatile("st.release.gpu.global.u32 [%0], %1;" :: "l"(rc.merged(sg.item, x)), "r"((uint32_t)rstep + 1)
+                     : "memory");
+      write_final = false;
     }
     const uint32_t ib = (uint32_t)(sg.ti * nblk);              // tail items only
     const int c_lo = (sg.ti < 0 || sg.j0 == 0) ? me : sp.tcta_of(ib);
