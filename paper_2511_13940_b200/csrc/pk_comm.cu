@@ -31,6 +31,7 @@
 #include <cstring>
 #include <mutex>
 #include <thread>
+#include <poll.h>
 #include <sys/socket.h>
 #include <sys/mman.h>
 #include <sys/un.h>
@@ -129,6 +130,11 @@ static int recv_msg(Comm* c, uint32_t tag, int* src, std::vector<char>* payload,
     }
   }
   while (true) {
+    // bounded: a peer that died or took another branch must not hang this rank
+    pollfd pfd = {c->listen_fd, POLLIN, 0};
+    const int pr = ::poll(&pfd, 1, 120 * 1000);
+    if (pr < 0 && errno == EINTR) continue;
+    if (pr == 0) return fail(PK_ERR_TIMEOUT, "rendezvous: rank %d got no message %u within 120 s", c->rank, tag);
     int s = ::accept(c->listen_fd, nullptr, nullptr);
     if (s < 0) {
       if (errno == EINTR) continue;
@@ -297,7 +303,9 @@ static int vmm_pgl_alloc(Comm* c, size_t bytes, uint32_t flags, Pgl* p) {
     mprop.handleTypes = CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR;
     mprop.size = bytes;
     size_t mg = 0;
-    PK_CU(d->multicastGetGranularity(&mg, &mprop, CU_MULTICAST_GRANULARITY_RECOMMENDED));
+    // the minimum multicast granularity: the recommended one can be far larger
+    // than small buffers (sync words, small all-reduces) need
+    PK_CU(d->multicastGetGranularity(&mg, &mprop, CU_MULTICAST_GRANULARITY_MINIMUM));
     gran = std::max(gran, mg);
   }
   const size_t size = (bytes + gran - 1) / gran * gran;   // memsim.py:308-318 rounding
@@ -451,7 +459,13 @@ int comm_scratch(Comm* c, int slot, size_t bytes, Pgl** out, uint32_t flags) {
     }
     c->scratch[slot] = nullptr;
   }
-  PK_TRY(pgl_alloc(c, want, flags, &c->scratch[slot]));
+  int st = pgl_alloc(c, want, flags, &c->scratch[slot]);
+  if (st != PK_OK && (flags & PK_PGL_MULTICAST)) {
+    // scratch only: a multicast object that cannot be created (collectively,
+    // on every rank alike) leaves the op on its P2P path instead of failing
+    st = pgl_alloc(c, want, flags & ~PK_PGL_MULTICAST, &c->scratch[slot]);
+  }
+  PK_TRY(st);
   *out = c->scratch[slot];
   return PK_OK;
 }
