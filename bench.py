@@ -529,6 +529,9 @@ def main():
     if n > 1:
         _leg(line, "decomposition", lambda: decomposition_leg(pk, comm, dev, n, S, a_ag, b_ag, c_ag, a_rs, b_rs, o_rs,
                                                               ag_max, rs_max, barrier, max_over_ranks))
+    if n > 1:
+        _leg(line, "schedule", lambda: schedule_leg(pk, comm, n, S, a_ag, b_ag, c_ag, a_rs, b_rs, o_rs, barrier,
+                                                    max_over_ranks))
     _leg(line, "nvlink", lambda: nvlink_leg(comm, n, barrier, max_vec))
     dog.cancel()
     comm.check()
@@ -690,6 +693,43 @@ def decomposition_leg(pk, comm, dev, n, S, a_ag, b_ag, c_ag, a_rs, b_rs, o_rs, a
                       "comm_ratio": max(0.0, (rs_ms - t_comp) / rs_ms)}
     full._pk_pgl.free()
     del full, part
+    comm.check()
+    return out
+
+
+def schedule_leg(pk, comm, n, S, a_ag, b_ag, c_ag, a_rs, b_rs, o_rs, barrier, max_over_ranks) -> dict:
+    """The reference's autotune_partition (lcsc.py:164-191) on the real ranks:
+    intra-SM vs inter-SM with several communicator-SM counts for AG-GEMM, and
+    intra-SM (bf16 / fp32 partials) vs inter-SM for GEMM-RS, at the timed
+    size; device time max over ranks; ties toward fewer communicator SMs. The
+    `table` entry is a measured schedule table (tune.ScheduleTable format)."""
+    import torch
+
+    from paper_2511_13940_b200 import tune
+
+    def timed(fn, iters=3):
+        fn()
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(iters):
+            fn()
+        e1.record()
+        barrier()
+        return max_over_ranks(e0.elapsed_time(e1) / iters)
+    out = {"size": S, "world": n}
+    table = tune.ScheduleTable()
+    ag_c = [{"mode": "intra_sm"}] + [{"mode": "inter_sm", "num_comm_sms": k} for k in (4, 8, 16, 24)]
+    rows = [(sc, timed(lambda: pk.all_gather_gemm(comm, a_ag, b_ag, out=c_ag, schedule=sc))) for sc in ag_c]
+    best, t = tune.pick_best(rows)
+    table.put("ag_gemm", n, S, S, S, best, ms=round(t, 4), emulated=False, sms_per_rank=comm.num_sms)
+    out["ag_gemm"] = {"rows": [[sc, ms] for sc, ms in rows], "best": best}
+    rs_c = [{"mode": "intra_sm"}, {"mode": "intra_sm", "partials": "fp32"}, {"mode": "inter_sm", "num_comm_sms": 16}]
+    rows = [(sc, timed(lambda: pk.gemm_reduce_scatter(comm, a_rs, b_rs, out=o_rs, schedule=sc))) for sc in rs_c]
+    best, t = tune.pick_best(rows)
+    table.put("gemm_rs", n, S, S, S, best, ms=round(t, 4), emulated=False, sms_per_rank=comm.num_sms)
+    out["gemm_rs"] = {"rows": [[sc, ms] for sc, ms in rows], "best": best}
+    out["table"] = table.entries
     comm.check()
     return out
 

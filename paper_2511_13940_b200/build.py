@@ -15,13 +15,17 @@ from concurrent.futures import ThreadPoolExecutor
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 INCLUDE = os.path.join(os.path.dirname(HERE), "include")
-BUILD = os.path.join(HERE, "_build")
-LIB = os.path.join(HERE, "libpk.so")
+# diagnostic variants (e.g. PK_BUILD_DEFINES="-DAT_RING_PROF"): a separate
+# object dir and library, loaded with PK_LIB=<path>; the product build is the default
+DEFINES = os.environ.get("PK_BUILD_DEFINES", "").split()
+_TAG = "".join(c if c.isalnum() else "_" for c in " ".join(DEFINES)).strip("_")
+BUILD = os.path.join(HERE, "_build" + ("_" + _TAG if _TAG else ""))
+LIB = os.path.join(HERE, "libpk.so" if not _TAG else f"libpk_{_TAG}.so")
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-std=c++17", "-O3", "-lineinfo", "-Xcompiler", "-fPIC,-fvisibility=hidden",
-         "-I" + INCLUDE, "-I" + CSRC, "--expt-relaxed-constexpr"]
+         "-I" + INCLUDE, "-I" + CSRC, "--expt-relaxed-constexpr", *DEFINES]
 
 SOURCES = sorted(f for f in os.listdir(CSRC) if f.endswith(".cu"))
 HEADERS = sorted(f for f in os.listdir(CSRC) if f.endswith((".cuh", ".h")))

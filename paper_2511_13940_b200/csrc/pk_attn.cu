@@ -211,6 +211,17 @@ PK_DEV void poly_exp2x2(float x0, float x1, float& p0, float& p1) {
 // Cycle profile of the softmax loop (AT_PROFILE builds only): per phase,
 // summed over lane-0 threads of the softmax warps: [0] wait for S,
 // [1] TMEM load of S, [2] row max + rescale, [3] exp / P store, [4] count.
+// Ring-schedule cycle profile (AT_RING_PROF builds only): [0] loader waits
+// for a step's slot, [1] softmax waits for the previous step's merge, [2]
+// epilogue (O drain + merge + state store), [3] MMA waits for a unit's Q,
+// [4] units, [5] communicator waits for a free slot, [6] communicator copying,
+// [7] compute CTA lifetime.
+#ifdef AT_RING_PROF
+__device__ unsigned long long g_ring_prof[8];
+#define RP_ADD(i, v) atomicAdd(&g_ring_prof[i], (unsigned long long)(v))
+#else
+#define RP_ADD(i, v)
+#endif
 #ifdef AT_PROFILE
 __device__ unsigned long long g_attn_prof[8];
 #define AT_PROF_MARK(k) const long long _t##k = clock64();
@@ -285,6 +296,9 @@ __global__ void __launch_bounds__(AT_THREADS, 1) attn_fwd_kernel(const __grid_co
   // ring mode: units (step, item) step-major over the compute CTAs; the last
   // ring_comm CTAs are communicators
   constexpr bool ring = RING;
+#ifdef AT_RING_PROF
+  const long long t_kernel0 = clock64();
+#endif
   const int ncompute = ring ? (int)gridDim.x - a.ring_comm : (int)gridDim.x;
   const bool is_comm = ring && (int)blockIdx.x >= ncompute;
   const RingCtr rc{a.ring_ctr, a.ring_steps};
@@ -379,8 +393,15 @@ __global__ void __launch_bounds__(AT_THREADS, 1) attn_fwd_kernel(const __grid_co
       bool ok = true;
       for (int s = 1; s < n; ++s) {
         const int src = (a.rank - s + n) % n;
+#ifdef AT_RING_PROF
+        const long long tw = clock64();
+#endif
         if (ok && s >= 3) ok = wait_geq(rc.units(s - 2), (uint32_t)items, a.err, a.timeout_ns);
         if (ok) ok = wait_geq(a.ready_local + src, ready_expect, a.err, a.timeout_ns);
+#ifdef AT_RING_PROF
+        const long long tc0 = clock64();
+        RP_ADD(5, tc0 - tw);
+#endif
         fence_async_global();
         uint8_t* dk = a.stage_k + (long long)(s & 1) * a.shard_bytes;
         uint8_t* dv = a.stage_v + (long long)(s & 1) * a.shard_bytes;
@@ -421,6 +442,9 @@ __global__ void __launch_bounds__(AT_THREADS, 1) attn_fwd_kernel(const __grid_co
           bulk_wait<0>();                              // my share of step s is in the slot
           gp += mine;
         }
+#ifdef AT_RING_PROF
+        RP_ADD(6, clock64() - tc0);
+#endif
         fence_async_global();
         __threadfence();
         if (atomicAdd(rc.pieces(s), 1u) == (uint32_t)nc - 1)
@@ -453,7 +477,13 @@ __global__ void __launch_bounds__(AT_THREADS, 1) attn_fwd_kernel(const __grid_co
       auto step_ready = [&](int step) {
         if (ring) {
           if (step > 0 && step != ring_ok) {
+#ifdef AT_RING_PROF
+            const long long t0p = clock64();
             wait_geq(rc.ready(step), 1u, a.err, a.timeout_ns);
+            RP_ADD(0, clock64() - t0p);
+#else
+            wait_geq(rc.ready(step), 1u, a.err, a.timeout_ns);
+#endif
             fence_async_global();
             ring_ok = step;
           }
@@ -542,12 +572,19 @@ __global__ void __launch_bounds__(AT_THREADS, 1) attn_fwd_kernel(const __grid_co
     SegIter it = seg_begin();
     for (SegInfo sg; seg_next(it, sg); ++seg) {
       const int len = sg.j1 - sg.j0;
+#ifdef AT_RING_PROF
+      const long long tq = clock64();
       mbar_wait(q_full, seg & 1);
+      if (ring && lane == 0) { RP_ADD(3, clock64() - tq); RP_ADD(4, 1); }
+#else
+      mbar_wait(q_full, seg & 1);
+#endif
       mbar_wait(&k_full[g % AT_KSTAGES], (g / AT_KSTAGES) & 1);
       tc_fence_after();
       if (elect_one()) {
         for (int x = 0; x < sg.ntile; ++x) issue_qk(x, g);
         umma_commit<1>(&k_empty[g % AT_KSTAGES]);
+        if (RING && len == 1) umma_commit<1>(q_empty);
       }
       __syncwarp();
       for (int i = 0; i < len; ++i) {
@@ -583,7 +620,14 @@ __global__ void __launch_bounds__(AT_THREADS, 1) attn_fwd_kernel(const __grid_co
         if (elect_one()) {
           umma_commit<1>(&v_empty[gg & 1]);
           if (more) umma_commit<1>(&k_empty[(gg + 1) % AT_KSTAGES]);
-          else umma_commit<1>(q_empty);
+          // ring units are short: release Q once the unit's last QK is issued
+          // (the commit lands when it completes), so the next unit's Q loads
+          // under the last PV and the epilogue instead of after them
+          if constexpr (RING) {
+            if (i + 2 == len) umma_commit<1>(q_empty);
+          } else {
+            if (!more) umma_commit<1>(q_empty);
+          }
         }
         __syncwarp();
       }
@@ -721,8 +765,19 @@ __global__ void __launch_bounds__(AT_THREADS, 1) attn_fwd_kernel(const __grid_co
 #pragma unroll
       for (int i2 = 0; i2 < AT_D; ++i2) o[i2] = 0.f;            // no state: w_s = 0, w_u = 1 below
     }
+#ifdef AT_RING_PROF
+    const long long tep = clock64();
+#endif
     if (has_state) {
+#ifdef AT_RING_PROF
+      if (lane == 0) {
+        const long long t0p = clock64();
+        wait_geq(rc.merged(sg.item, x), (uint32_t)rstep, a.err, a.timeout_ns);
+        RP_ADD(1, clock64() - t0p);
+      }
+#else
       if (lane == 0) wait_geq(rc.merged(sg.item, x), (uint32_t)rstep, a.err, a.timeout_ns);
+#endif
       __syncwarp();
 #pragma unroll
       for (int i2 = 0; i2 < AT_D / 4; ++i2) {
@@ -775,6 +830,9 @@ __global__ void __launch_bounds__(AT_THREADS, 1) attn_fwd_kernel(const __grid_co
                      : "memory");
       write_final = false;
     }
+#ifdef AT_RING_PROF
+    if (ring && lane == 0) RP_ADD(2, clock64() - tep);
+#endif
     const uint32_t ib = (uint32_t)(sg.ti * nblk);              // tail items only
     const int c_lo = (sg.ti < 0 || sg.j0 == 0) ? me : sp.tcta_of(ib);
     const int c_hi = (sg.ti < 0 || sg.j1 == nblk) ? me : sp.tcta_of(ib + nblk - 1);
@@ -849,6 +907,9 @@ __global__ void __launch_bounds__(AT_THREADS, 1) attn_fwd_kernel(const __grid_co
   }
   if (ring) {
     __shared__ int ring_last;
+#ifdef AT_RING_PROF
+    if (!is_comm && threadIdx.x == 0) RP_ADD(7, clock64() - t_kernel0);
+#endif
     // the caller may reuse k / v once every rank has read them
     if (blockIdx.x == 0 && threadIdx.x == 0)
       for (int d = 0; d < a.world; ++d) wait_geq(a.done_local + d, call_get(a.call, 2), a.err, a.timeout_ns);
@@ -1360,7 +1421,7 @@ int ring_attn_fwd(Comm* c, const pk_tensor* q, const pk_tensor* k, const pk_tens
   a.S_kv = (int)(n * S);
   a.blocks_per_step = (int)(S / AT_BN);
   // Communicator CTAs (inter-SM schedule): enough TMA-driven SMs to pull a
-  // step's K + V within the step's compute (+30 %), at the paper's B200 TMA
+  // step's K + V within half the step's compute (+30 %), at the paper's B200 TMA
   // rate (669 GB/s saturating at 15 SMs) and ~1.2 PF/s of
   // attention over this rank's SMs; the schedule may set it. Emulated ranks
   // keep a quarter of their SMs at most.
@@ -1368,8 +1429,10 @@ int ring_attn_fwd(Comm* c, const pk_tensor* q, const pk_tensor* k, const pk_tens
   if (sched && sched->num_comm_sms > 0) {
     ncomm = sched->num_comm_sms;
   } else {
+    // A slot is refilled for step s + 1 only once every unit of step s - 1 has
+    // read it, so the copy has about half a step, not a whole one.
     const double t_step = 4.0 * B * H * (double)S * S * AT_D / (1.2e15 * c->num_sms / 148.0);   // this rank's SMs
-    ncomm = (int)std::ceil(1.3 * 2.0 * (double)shard / (t_step * (669e9 / 15)));
+    ncomm = (int)std::ceil(1.3 * 2.0 * (double)shard / (0.5 * t_step * (669e9 / 15)));
     ncomm = std::max(2, std::min(16, ncomm));
   }
   if (c->local_group) ncomm = std::min(ncomm, std::max(1, c->num_sms / 4));
@@ -1424,6 +1487,17 @@ int attn_local(const pk_tensor* q, const pk_tensor* k, const pk_tensor* v, pk_te
 }
 
 }  // namespace pk
+
+#ifdef AT_RING_PROF
+extern "C" PK_API int pk_debug_ring_prof(unsigned long long* out, int reset) {
+  PK_CUDA(cudaMemcpyFromSymbol(out, pk::g_ring_prof, sizeof(unsigned long long) * 8));
+  if (reset) {
+    unsigned long long z[8] = {};
+    PK_CUDA(cudaMemcpyToSymbol(pk::g_ring_prof, z, sizeof(z)));
+  }
+  return PK_OK;
+}
+#endif
 
 #ifdef AT_PROFILE
 extern "C" PK_API int pk_debug_attn_prof(unsigned long long* out, int reset) {
