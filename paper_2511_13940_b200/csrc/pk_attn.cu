@@ -97,7 +97,7 @@ struct AttnArgs {
   uint8_t* stage_k;              // [2][shard]
   uint8_t* stage_v;
   long long shard_bytes;
-  float* ring_state;             // [items][2 tiles][128 rows][AT_PART_ROW]: running (O, m, l)
+  float* ring_state;             // per (item, tile): O as [32 column quads][128 rows] float4, then (m, l) per row
   uint32_t* ring_ctr;            // counters (RingCtr); zero at launch, re-armed by the last CTA
   uint32_t* ready_local;         // [n] shard-ready signals received (source rank)
   uint32_t* ready_peer[8];
@@ -110,6 +110,10 @@ struct AttnArgs {
 // finished their share of the step; 3n communicator CTAs finished; 3n + 1
 // CTAs finished (the last re-arms everything); then per (item, tile) the steps
 // merged so far.
+// One (item, tile) of the ring state, column-quad-major so that a warp's 16 B
+// accesses (one row per lane) are contiguous: O[c4][row] float4, then (m, l)[row].
+constexpr int AT_STATE_FLOATS = (AT_D / 4) * AT_BM * 4 + AT_BM * 2;
+
 struct RingCtr {
   uint32_t* base;
   int n;
@@ -122,9 +126,8 @@ struct RingCtr {
 };
 __host__ __device__ inline size_t ring_ctr_words(int n, int items) { return (size_t)3 * n + 2 + 2 * (size_t)items; }
 
-// Partial state of one (slot, tile, row): D floats of unnormalised O, then m, l.
-constexpr int AT_PART_ROW = AT_D + 4;            // padded to 16 B (float4 rows)
-constexpr int AT_PART_SLOT = 2 * AT_BM * AT_PART_ROW;
+// Partial state of one slot: per tile, unnormalised O column-quad-major
+// ([D/4][128 rows] float4) then (m, l) per row (AT_STATE_FLOATS, below).
 
 // Work split: one CTA per item, except that the last R = items mod (SMs)
 // items — the partial last wave — are cut evenly over U = SMs tail CTAs (the
@@ -217,7 +220,7 @@ PK_DEV void poly_exp2x2(float x0, float x1, float& p0, float& p1) {
 // [4] units, [5] communicator waits for a free slot, [6] communicator copying,
 // [7] compute CTA lifetime.
 #ifdef AT_RING_PROF
-__device__ unsigned long long g_ring_prof[8];
+__device__ unsigned long long g_ring_prof[12];
 #define RP_ADD(i, v) atomicAdd(&g_ring_prof[i], (unsigned long long)(v))
 #else
 #define RP_ADD(i, v)
@@ -759,7 +762,9 @@ __global__ void __launch_bounds__(AT_THREADS, 1) attn_fwd_kernel(const __grid_co
     // merged chunk by chunk with O as it leaves TMEM (o[] holds the merge)
     const int rstep = ring ? sg.j0 / bps : 0;
     const bool has_state = ring && rstep > 0;
-    float* stt = ring ? a.ring_state + ((long long)(2 * sg.item + x) * AT_BM + row) * AT_PART_ROW : nullptr;
+    float* stt = ring ? a.ring_state + (long long)(2 * sg.item + x) * AT_STATE_FLOATS : nullptr;
+    float4* st_o = reinterpret_cast<float4*>(stt) + row;                         // + c4 * AT_BM
+    float2* st_ml = reinterpret_cast<float2*>(stt + (AT_D / 4) * AT_BM * 4) + row;
     float m_s = -INFINITY, l_s = 0.f;
     if constexpr (RING) {
 #pragma unroll
@@ -781,14 +786,22 @@ __global__ void __launch_bounds__(AT_THREADS, 1) attn_fwd_kernel(const __grid_co
       __syncwarp();
 #pragma unroll
       for (int i2 = 0; i2 < AT_D / 4; ++i2) {
-        const float4 v = __ldcg(reinterpret_cast<const float4*>(stt) + i2);
+        const float4 v = __ldcg(st_o + i2 * AT_BM);
         o[4 * i2] = v.x; o[4 * i2 + 1] = v.y; o[4 * i2 + 2] = v.z; o[4 * i2 + 3] = v.w;
       }
-      m_s = __ldcg(stt + AT_D);
-      l_s = __ldcg(stt + AT_D + 1);
+      const float2 ml = __ldcg(st_ml);
+      m_s = ml.x;
+      l_s = ml.y;
     }
+#ifdef AT_RING_PROF
+    const long long tof = clock64();
+#endif
     mbar_wait(&o_full[x], segx & 1);
     tc_fence_after();
+#ifdef AT_RING_PROF
+    const long long tdr = clock64();
+    if (ring && lane == 0) RP_ADD(8, tdr - tof);
+#endif
     const float m_n = fmaxf(m_s, m);
     const float w_s = (m_s == -INFINITY) ? 0.f : fast_exp2(m_s - m_n);     // state weight
     const float w_u = (m == -INFINITY) ? 0.f : fast_exp2(m - m_n);         // this unit's weight
@@ -808,6 +821,10 @@ __global__ void __launch_bounds__(AT_THREADS, 1) attn_fwd_kernel(const __grid_co
     tc_fence_before();
     __syncwarp();
     if (lane == 0) mbar_arrive(&o_empty[x]);        // the next segment's PV may overwrite O
+#ifdef AT_RING_PROF
+    const long long tst = clock64();
+    if (ring && lane == 0) RP_ADD(9, tst - tdr);
+#endif
     ++segx;
     if constexpr (RING) {
       l = l_s * w_s + l * w_u;
@@ -821,14 +838,16 @@ __global__ void __launch_bounds__(AT_THREADS, 1) attn_fwd_kernel(const __grid_co
       // the tile's 128 threads sync, then one release publishes all their rows
 #pragma unroll
       for (int i2 = 0; i2 < AT_D / 4; ++i2)
-        reinterpret_cast<float4*>(stt)[i2] = make_float4(o[4 * i2], o[4 * i2 + 1], o[4 * i2 + 2], o[4 * i2 + 3]);
-      stt[AT_D] = m;
-      stt[AT_D + 1] = l;
+        st_o[i2 * AT_BM] = make_float4(o[4 * i2], o[4 * i2 + 1], o[4 * i2 + 2], o[4 * i2 + 3]);
+      *st_ml = make_float2(m, l);
       asm volatile("bar.sync %0, 128;" :: "r"(1 + x) : "memory");
       if (row == 0)
         asm volatile("st.release.gpu.global.u32 [%0], %1;" :: "l"(rc.merged(sg.item, x)), "r"((uint32_t)rstep + 1)
                      : "memory");
       write_final = false;
+#ifdef AT_RING_PROF
+      if (lane == 0) RP_ADD(10, clock64() - tst);
+#endif
     }
 #ifdef AT_RING_PROF
     if (ring && lane == 0) RP_ADD(2, clock64() - tep);
@@ -838,12 +857,12 @@ __global__ void __launch_bounds__(AT_THREADS, 1) attn_fwd_kernel(const __grid_co
     const int c_hi = (sg.ti < 0 || sg.j1 == nblk) ? me : sp.tcta_of(ib + nblk - 1);
     if (c_lo != c_hi) {
       // cut item: publish this segment's partial, the last finisher merges
-      float* mine = a.part + (long long)sp.slot(me, sg.ti) * AT_PART_SLOT + (x * AT_BM + row) * AT_PART_ROW;
+      // (column-quad-major like the ring state: a warp's 16 B accesses are contiguous)
+      float* mine = a.part + ((long long)sp.slot(me, sg.ti) * 2 + x) * AT_STATE_FLOATS;
 #pragma unroll
       for (int i2 = 0; i2 < AT_D / 4; ++i2)
-        reinterpret_cast<float4*>(mine)[i2] = make_float4(o[4 * i2], o[4 * i2 + 1], o[4 * i2 + 2], o[4 * i2 + 3]);
-      mine[AT_D] = m;
-      mine[AT_D + 1] = l;
+        reinterpret_cast<float4*>(mine)[i2 * AT_BM + row] = make_float4(o[4 * i2], o[4 * i2 + 1], o[4 * i2 + 2], o[4 * i2 + 3]);
+      reinterpret_cast<float2*>(mine + (AT_D / 4) * AT_BM * 4)[row] = make_float2(m, l);
       __threadfence();
       asm volatile("bar.sync %0, 128;" :: "r"(1 + x) : "memory");
       if (row == 0) {
@@ -862,14 +881,15 @@ __global__ void __launch_bounds__(AT_THREADS, 1) attn_fwd_kernel(const __grid_co
         for (int i2 = 0; i2 < AT_D; ++i2) o[i2] = 0.f;
         for (int c = c_lo; c <= c_hi; ++c) {
           if (sp.tstart(c + 1) == sp.tstart(c)) continue;   // no share of the tail
-          const float* pr = a.part + (long long)sp.slot(c, sg.ti) * AT_PART_SLOT + (x * AT_BM + row) * AT_PART_ROW;
-          const float mc = __ldcg(pr + AT_D), lc = __ldcg(pr + AT_D + 1);
+          const float* pr = a.part + ((long long)sp.slot(c, sg.ti) * 2 + x) * AT_STATE_FLOATS;
+          const float2 mlc = __ldcg(reinterpret_cast<const float2*>(pr + (AT_D / 4) * AT_BM * 4) + row);
+          const float mc = mlc.x, lc = mlc.y;
           const float mn = fmaxf(mt, mc);
           const float wa = (mt == -INFINITY) ? 0.f : fast_exp2(mt - mn);
           const float wb = (mc == -INFINITY) ? 0.f : fast_exp2(mc - mn);
 #pragma unroll
           for (int i2 = 0; i2 < AT_D / 4; ++i2) {
-            const float4 v = __ldcg(reinterpret_cast<const float4*>(pr) + i2);
+            const float4 v = __ldcg(reinterpret_cast<const float4*>(pr) + i2 * AT_BM + row);
             o[4 * i2 + 0] = o[4 * i2 + 0] * wa + v.x * wb;
             o[4 * i2 + 1] = o[4 * i2 + 1] * wa + v.y * wb;
             o[4 * i2 + 2] = o[4 * i2 + 2] * wa + v.z * wb;
@@ -1293,7 +1313,7 @@ static int launch_attn(AttnScratch& scr, int num_sms, AttnArgs& a, cudaStream_t 
   if ((uint64_t)sms * ((uint64_t)a.tail_items * nblk + 1) >= (1ull << 32)) a.tail_items = 0;   // 32-bit split math
   a.tail_units = a.tail_items ? sms : 0;
   const int grid = items - a.tail_items + a.tail_units;
-  const size_t part_bytes = (size_t)2 * std::max(1, a.tail_units) * AT_PART_SLOT * sizeof(float);
+  const size_t part_bytes = (size_t)2 * std::max(1, a.tail_units) * 2 * AT_STATE_FLOATS * sizeof(float);
   if (scr.part_bytes < part_bytes) {
     if (scr.part) PK_CUDA(cudaFreeAsync(scr.part, st));
     PK_CUDA(cudaMallocAsync(&scr.part, part_bytes, st));
@@ -1378,7 +1398,7 @@ int ring_attn_fwd(Comm* c, const pk_tensor* q, const pk_tensor* k, const pk_tens
   // re-armed by each launch's last CTA).
   const int items = (int)(B * H * ((S / AT_BM + 1) / 2));
   const size_t stage_bytes = 4 * shard;
-  const size_t state_bytes = (size_t)items * 2 * AT_BM * AT_PART_ROW * sizeof(float);
+  const size_t state_bytes = (size_t)items * 2 * AT_STATE_FLOATS * sizeof(float);
   const size_t ctr_bytes = ring_ctr_words(n, items) * sizeof(uint32_t);
   const size_t need = stage_bytes + state_bytes + ctr_bytes;
   if (c->ring_buf_bytes < need) {
@@ -1490,9 +1510,9 @@ int attn_local(const pk_tensor* q, const pk_tensor* k, const pk_tensor* v, pk_te
 
 #ifdef AT_RING_PROF
 extern "C" PK_API int pk_debug_ring_prof(unsigned long long* out, int reset) {
-  PK_CUDA(cudaMemcpyFromSymbol(out, pk::g_ring_prof, sizeof(unsigned long long) * 8));
+  PK_CUDA(cudaMemcpyFromSymbol(out, pk::g_ring_prof, sizeof(unsigned long long) * 12));
   if (reset) {
-    unsigned long long z[8] = {};
+    unsigned long long z[12] = {};
     PK_CUDA(cudaMemcpyToSymbol(pk::g_ring_prof, z, sizeof(z)));
   }
   return PK_OK;

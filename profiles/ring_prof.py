@@ -19,7 +19,7 @@ from paper_2511_13940_b200 import _lib  # noqa: E402
 
 def main():
     lib = _lib.load()
-    buf = (ctypes.c_ulonglong * 8)()
+    buf = (ctypes.c_ulonglong * 12)()
     for n, S in ((2, 32768), (8, 32768), (8, 131072)):
         B, H, D = 1, 16, 128
         sl = S // n
@@ -56,6 +56,8 @@ def main():
         out = {"world": n, "S": S, "ms": e0.elapsed_time(e1), "units": units, "items_per_step": items,
                "loader_slot_wait_frac": v[0] / life, "merge_wait_frac(warp-lane0 sum / 8 warps)": v[1] / life / 8,
                "epilogue_frac(per warp)": v[2] / life / 8, "mma_q_wait_frac": v[3] / life,
+               "epi_o_full_wait_frac": v[8] / life / 8, "epi_drain_merge_frac": v[9] / life / 8,
+               "epi_state_store_frac": v[10] / life / 8,
                "comm_slot_wait_cycles": v[5], "comm_copy_cycles": v[6], "cta_lifetime_cycles_sum": life}
         print(json.dumps(out), flush=True)
         for c in comms:
