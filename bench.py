@@ -532,10 +532,14 @@ def main():
     if n > 1:
         _leg(line, "schedule", lambda: schedule_leg(pk, comm, n, S, a_ag, b_ag, c_ag, a_rs, b_rs, o_rs, barrier,
                                                     max_over_ranks))
+    _leg(line, "ring_attention", lambda: ring_leg(pk, comm, dist, dev, n, barrier, max_over_ranks,
+                                                  backend == "nccl", args.size))
+    _leg(line, "moe", lambda: moe_leg(pk, comm, dist, dev, n, barrier, max_over_ranks, backend == "nccl"))
     _leg(line, "nvlink", lambda: nvlink_leg(comm, n, barrier, max_vec))
     dog.cancel()
     comm.check()
-    ok = not (isinstance(line.get("parity"), dict) and line["parity"].get("ok") is False)
+    ok = not any(isinstance(line.get(key), dict) and line[key].get("ok") is False
+                 for key in ("parity", "ring_attention", "moe"))
     if rank == 0:
         print(json.dumps(line), flush=True)
     comm.destroy()
@@ -731,6 +735,148 @@ def schedule_leg(pk, comm, n, S, a_ag, b_ag, c_ag, a_rs, b_rs, o_rs, barrier, ma
     out["gemm_rs"] = {"rows": [[sc, ms] for sc, ms in rows], "best": best}
     out["table"] = table.entries
     comm.check()
+    return out
+
+
+def _gather0(dist, t, n: int, nccl: bool):
+    """Rank-major concatenation of every rank's t along dim 0 (NCCL, or gloo on the host)."""
+    import torch
+    if n == 1:
+        return t
+    if nccl:
+        out = torch.empty((n * t.shape[0],) + tuple(t.shape[1:]), device=t.device, dtype=t.dtype)
+        dist.all_gather_into_tensor(out, t.contiguous())
+        return out
+    parts = [torch.empty(tuple(t.shape), dtype=t.dtype) for _ in range(n)]
+    dist.all_gather(parts, t.cpu())
+    return torch.cat(parts).to(t.device)
+
+
+def ring_leg(pk, comm, dist, dev, n, barrier, max_over_ranks, nccl: bool, S_gemm: int) -> dict:
+    """BASELINE config 4 on this run's ranks: ring attention B1 H16 D128,
+    non-causal, S = 32768 and 131072 split over the ranks (the 2-slot device
+    ring; n = 1 is the single-GPU kernel). Parity: 16 sampled query rows per
+    rank against float64 softmax over every key (K/V gathered with NCCL),
+    |o| <= 2e-2, |lse| <= 1e-3 * max(1, |lse|). Whole-job TFLOP/s; the
+    non-overlapped baseline is NCCL all-gather of K and V then torch SDPA."""
+    import torch
+    out = {"B": 1, "H": 16, "D": 128, "sizes": []}
+    if S_gemm < 16384:                                # small test runs: small attention too
+        sizes = (8192,)
+    else:
+        sizes = (32768, 131072)
+    for S in sizes:
+        sl = S // n
+        g = torch.Generator(device=dev)
+        g.manual_seed(77 + comm.rank)
+        q = torch.randn(1, sl, 16, 128, device=dev, generator=g).bfloat16()
+        k = comm.empty((1, sl, 16, 128))
+        v = comm.empty((1, sl, 16, 128))
+        k.copy_(torch.randn(k.shape, device=dev, generator=g).bfloat16())
+        v.copy_(torch.randn(v.shape, device=dev, generator=g).bfloat16())
+        o, lse = pk.ring_attention(comm, q, k, v)
+        torch.cuda.synchronize()
+        comm.check()
+        K_ = _gather0(dist, k[0], n, nccl).double()
+        V_ = _gather0(dist, v[0], n, nccl).double()
+        rows = torch.randint(0, sl, (16,), device=dev, generator=g)
+        sc = torch.einsum("qhd,khd->hqk", q[0, rows].double(), K_) * 128 ** -0.5
+        ref_l = torch.logsumexp(sc, -1)
+        ref_o = torch.einsum("hqk,khd->qhd", torch.softmax(sc, -1), V_)
+        err_o = max_over_ranks((o[0, rows].double() - ref_o).abs().max().item())
+        err_l = max_over_ranks((lse[0][:, rows].double() - ref_l).abs().max().item())
+        lim_l = 1e-3 * max(1.0, ref_l.abs().max().item())
+        del K_, V_, sc, ref_o
+
+        def timed(fn, iters):
+            fn()
+            barrier()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            for _ in range(iters):
+                fn()
+            e1.record()
+            barrier()
+            return max_over_ranks(e0.elapsed_time(e1) / iters)
+        iters = 3 if S <= 32768 else 2
+        t = timed(lambda: pk.ring_attention(comm, q, k, v, out=o, lse=lse), iters)
+        flops = n * 4.0 * 16 * sl * S * 128
+        ent = {"S": S, "ms": t, "tflops": flops / t / 1e9, "max_err_o": err_o, "max_err_lse": err_l,
+               "ok": err_o <= 2e-2 and err_l <= lim_l, "link_bytes_per_rank": (n - 1) * 2 * sl * 16 * 128 * 2}
+        if n > 1:
+            ent["link_gbs"] = ent["link_bytes_per_rank"] / (t / 1e3) / 1e9
+        if nccl and n > 1:
+            def base():
+                K2 = _gather0(dist, k[0], n, True)
+                V2 = _gather0(dist, v[0], n, True)
+                torch.nn.functional.scaled_dot_product_attention(q.transpose(1, 2), K2[None].transpose(1, 2),
+                                                                 V2[None].transpose(1, 2))
+            tb = timed(base, iters)
+            ent["nccl_sdpa_ms"] = tb
+            ent["speedup_vs_nccl_sdpa"] = tb / t
+        out["sizes"].append(ent)
+        k._pk_pgl.free()
+        v._pk_pgl.free()
+        del q, k, v, o, lse
+    out["ok"] = all(e["ok"] for e in out["sizes"])
+    return out
+
+
+def moe_leg(pk, comm, dist, dev, n, barrier, max_over_ranks, nccl: bool) -> dict:
+    """BASELINE config 5 on this run's ranks: 64 experts, top-8, H 7168,
+    H_exp 2048, T 4096 tokens per rank, expert e on rank e % n (workloads.py:
+    799-802 routing). Dispatch (expert-major) -> planned grouped GEMM1 ->
+    combine of the dispatched rows. Parity: every received row is the token
+    its id names (tokens gathered with NCCL), counts add up to n * T * k, and
+    combine with weights 1/k returns every token exactly."""
+    import torch
+    T, E, K, H, HE = 4096, 64, 8, 7168, 2048
+    g = torch.Generator(device=dev)
+    g.manual_seed(99 + comm.rank)
+    x = torch.randint(-8, 9, (T, H), device=dev, generator=g).bfloat16()
+    topk = torch.rand(T, E, device=dev, generator=g).argsort(1)[:, :K].int().contiguous()
+    le = (E + n - 1) // n
+    w = (torch.randn(le, HE, H, device=dev, generator=g) * 0.02).bfloat16()
+    recv, src, cnt, plan = pk.moe_dispatch(comm, x, topk, E, layout="expert")
+    torch.cuda.synchronize()
+    comm.check()
+    allx = _gather0(dist, x, n, nccl)
+    ids = src[:, 0].long()
+    real = ids >= 0
+    rows_ok = bool(torch.equal(recv[real], allx[ids[real] // K]))
+    t_all = torch.tensor([float(int(cnt.item()))], device=dev if nccl else "cpu", dtype=torch.float64)
+    if n > 1:
+        dist.all_reduce(t_all)
+    counts_ok = int(t_all.item()) == n * T * K
+    y = pk.grouped_gemm(recv, None, w, plan=plan)
+    comb = pk.moe_combine(comm, recv, topk, torch.full((T, K), 1.0 / K, device=dev), E)
+    torch.cuda.synchronize()
+    comm.check()
+    comb_ok = bool(torch.equal(comb, x))
+    del allx
+
+    def timed(fn, iters=5):
+        fn()
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(iters):
+            fn()
+        e1.record()
+        barrier()
+        return max_over_ranks(e0.elapsed_time(e1) / iters)
+    t_d = timed(lambda: pk.moe_dispatch(comm, x, topk, E, recv=(recv, src), layout="expert"))
+    t_g = timed(lambda: pk.grouped_gemm(recv, None, w, out=y, plan=plan))
+    t_c = timed(lambda: pk.moe_combine(comm, recv, topk, torch.full((T, K), 1.0 / K, device=dev), E, out=comb))
+    rows_moved = T * K                                   # per rank, both directions
+    link = rows_moved * (n - 1) / n * H * 2
+    out = {"T": T, "E": E, "top_k": K, "H": H, "H_expert": HE, "dispatch_ms": t_d, "grouped_gemm1_ms": t_g,
+           "combine_ms": t_c, "rows_ok": rows_ok, "counts_ok": counts_ok, "combine_exact": comb_ok,
+           "gemm1_tflops_per_rank": 2.0 * int(cnt.item()) * H * HE / (t_g / 1e3) / 1e12,
+           "ok": rows_ok and counts_ok and comb_ok}
+    if n > 1:
+        out["dispatch_link_gbs"] = link / (t_d / 1e3) / 1e9
+        out["combine_link_gbs"] = link / (t_c / 1e3) / 1e9
     return out
 
 
