@@ -564,7 +564,10 @@ def parity_check(pk, comm, dist, dev, rank, n, S, a_ag, b_ag, c_ag, a_rs, b_rs, 
         return torch.randint(lo, hi + 1, shape, device=dev, generator=g).to(torch.bfloat16)
 
     out = {"inputs": "integers: AG-GEMM A, B in [-2, 2]; GEMM-RS A, B in [-1, 1], A nonzero in 256/n K columns",
-           "reference": "NCCL all_gather / reduce_scatter + fp32 torch.matmul, rounded to bf16"}
+           "reference": "NCCL all_gather / reduce_scatter + cuBLAS bf16 GEMM (fp32 accumulation, no reduced-"
+                        "precision split-K reduction): every sum is an exact integer, rounded to bf16 once"}
+    prev = torch.backends.cuda.matmul.allow_bf16_reduced_precision_reduction
+    torch.backends.cuda.matmul.allow_bf16_reduced_precision_reduction = False
     a_ag.copy_(ints(tuple(a_ag.shape), -2, 2))
     b_ag.copy_(ints(tuple(b_ag.shape), -2, 2))
     pk.all_gather_gemm(comm, a_ag, b_ag, out=c_ag)
@@ -578,7 +581,7 @@ def parity_check(pk, comm, dist, dev, rank, n, S, a_ag, b_ag, c_ag, a_rs, b_rs, 
         full = torch.cat(parts).to(dev)
     else:
         full = a_ag
-    ref = (full.float() @ b_ag.float().t()).to(torch.bfloat16)
+    ref = full @ b_ag.t()
     del full
     bad_ag = int((c_ag != ref).sum().item())
     del ref
@@ -587,18 +590,19 @@ def parity_check(pk, comm, dist, dev, rank, n, S, a_ag, b_ag, c_ag, a_rs, b_rs, 
     a_rs[:, :max(1, min(k_loc, 256 // n))] = ints((S, max(1, min(k_loc, 256 // n))), -1, 1)
     b_rs.copy_(ints(tuple(b_rs.shape), -1, 1))
     pk.gemm_reduce_scatter(comm, a_rs, b_rs, out=o_rs)
-    part = a_rs.float() @ b_rs.float().t()
+    part = a_rs @ b_rs.t()                          # |partial| <= 256 / n: exact in bf16
     if n > 1 and nccl:
-        red = torch.empty(S // n, S, device=dev, dtype=torch.float32)
+        red = torch.empty(S // n, S, device=dev, dtype=torch.bfloat16)
         dist.reduce_scatter_tensor(red, part)
     elif n > 1:
-        host = part.cpu()
+        host = part.float().cpu()
         dist.all_reduce(host)
         red = host[rank * (S // n):(rank + 1) * (S // n)].to(dev)
     else:
         red = part
     bad_rs = int((o_rs != red.to(torch.bfloat16)).sum().item())
     del part, red
+    torch.backends.cuda.matmul.allow_bf16_reduced_precision_reduction = prev
     torch.cuda.synchronize()
     comm.check()
     bad = max_over_ranks(float(bad_ag + bad_rs))
