@@ -462,6 +462,8 @@ def main():
     roofline = {"bound": "tensor", "achieved": achieved, "peak": peak_burst, "unit": UNIT,
                 "frac": achieved / peak_burst, "frac_of_sustained_peak": achieved / peak_sus,
                 "traffic": traffic_for(S),
+                "traffic_source": "ncu --set full, one launch at this size (profiles/gemm_dram_traffic.json)"
+                                  if traffic_for(S) else None,
                 "kernel": "pk::lcsc_gemm_kernel<2,256,*>",
                 "per_launch": f"2*S^3/n = {flops_launch:.4g} FLOP per launch (one AG-GEMM or GEMM-RS)",
                 "peak_source": f"{src} bf16_tflops (burst); sustained {peak_sus}",
