@@ -42,6 +42,9 @@
 
 namespace pk {
 
+#ifndef AT_SPEC       // 1: the first half's P computed against the running max while the row max is found
+#define AT_SPEC 0       // measured: no gain at kv 32768 / 65536, 4 % slower at kv 131072 (profiles/r2/attn_spec_ab.jsonl)
+#endif
 #ifndef AT_SPLIT_LD   // 1: S row loaded in two TMEM waits (first half's max overlaps the second load)
 #define AT_SPLIT_LD 0   // measured +1 % at S 16384, -10 % on the n = 8 rank step
 #endif
@@ -692,41 +695,11 @@ __global__ void __launch_bounds__(AT_THREADS, 1) attn_fwd_kernel(const __grid_co
       for (int c = 0; c < 4; ++c) tmem_ld_32x32b_x32(t_s + c * 32, *reinterpret_cast<uint32_t(*)[32]>(r + c * 32));
       tmem_ld_wait();
       AT_PROF_MARK(2);
-      // row max as 8 independent FMNMX3 chains (a single chain is 64 dependent ops)
-      float m8[8];
-#pragma unroll
-      for (int t = 0; t < 8; ++t) m8[t] = fmax3(__uint_as_float(r[2 * t]), __uint_as_float(r[2 * t + 1]), -INFINITY);
-#pragma unroll
-      for (int i2 = 8; i2 < AT_BN / 2; ++i2)
-        m8[i2 & 7] = fmax3(m8[i2 & 7], __uint_as_float(r[2 * i2]), __uint_as_float(r[2 * i2 + 1]));
 #endif
-      float mx = fmax3(fmax3(m8[0], m8[1], m8[2]), fmax3(m8[3], m8[4], m8[5]), fmaxf(m8[6], m8[7]));
-      mx *= sc;
-      const bool grow = mx > m + AT_RESCALE_THRESHOLD;
-      if (i > 0 && __any_sync(0xffffffffu, grow)) {
-        const float alpha = grow ? fast_exp2(m - mx) : 1.f;
-#pragma unroll 1
-        for (int c = 0; c < 4; ++c) {
-          uint32_t o[32];
-          tmem_ld_32x32b_x32(t_o + c * 32, o);
-          tmem_ld_wait();
-#pragma unroll
-          for (int i2 = 0; i2 < 32; ++i2) o[i2] = __float_as_uint(__uint_as_float(o[i2]) * alpha);
-          tmem_st_32x32b_x32(t_o + c * 32, o);
-        }
-        l *= alpha;
-      }
-      if (grow) m = mx;
-      AT_PROF_MARK(3);
       // packed fp32 pairs: one FFMA2 computes s*scale - m for two keys, one FADD2
       // accumulates two probabilities (the softmax warps are issue-bound)
-      const uint64_t sc2 = f2_pack(sc, sc), nm2 = f2_pack(-m, -m);
-      uint64_t rs2[4];                                    // 4 independent row-sum chains
-#pragma unroll
-      for (int t = 0; t < 4; ++t) rs2[t] = f2_pack(0.f, 0.f);
-#pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        uint32_t pk[16];
+      auto exp_chunk = [&](int c, uint64_t nm2, uint32_t (&pk)[16], uint64_t (&rs2)[4]) {
+        const uint64_t sc2 = f2_pack(sc, sc);
 #pragma unroll
         for (int i2 = 0; i2 < 16; ++i2) {
           float x0, x1, p0, p1;
@@ -741,13 +714,94 @@ __global__ void __launch_bounds__(AT_THREADS, 1) attn_fwd_kernel(const __grid_co
           rs2[i2 & 3] = f2_add(rs2[i2 & 3], f2_pack(p0, p1));
           pk[i2] = pack_bf16x2(p0, p1);
         }
-        tmem_st_32x32b_x16(t_s + c * 16, pk);          // columns [16c, 16c+16): already in registers
-        if (c & 1) {                                    // keys [64h, 64h+64) are in TMEM: release that half
-          tmem_st_wait();
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&p_full[2 * x + (c >> 1)]);
+      };
+      auto publish_half = [&](int h) {                  // keys [64h, 64h+64) are in TMEM: release that half
+        tmem_st_wait();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&p_full[2 * x + h]);
+      };
+      auto rescale_o = [&](float alpha) {
+#pragma unroll 1
+        for (int c = 0; c < 4; ++c) {
+          uint32_t o[32];
+          tmem_ld_32x32b_x32(t_o + c * 32, o);
+          tmem_ld_wait();
+#pragma unroll
+          for (int i2 = 0; i2 < 32; ++i2) o[i2] = __float_as_uint(__uint_as_float(o[i2]) * alpha);
+          tmem_st_32x32b_x32(t_o + c * 32, o);
         }
+      };
+      uint64_t rs2[4];                                    // 4 independent row-sum chains
+#pragma unroll
+      for (int t = 0; t < 4; ++t) rs2[t] = f2_pack(0.f, 0.f);
+#if AT_SPEC && !AT_SPLIT_LD
+      if (i > 0) {
+        // speculative: the first half's P against the current max while the
+        // row max is computed alongside (independent instruction streams); the
+        // max only gates publishing. A row whose max grew past the threshold
+        // (rare after the first block) discards the speculation: rescale O,
+        // move m, recompute.
+        uint32_t pk0[16], pk1[16];
+        exp_chunk(0, f2_pack(-m, -m), pk0, rs2);
+        exp_chunk(1, f2_pack(-m, -m), pk1, rs2);
+        float m8[8];
+#pragma unroll
+        for (int t = 0; t < 8; ++t) m8[t] = fmax3(__uint_as_float(r[2 * t]), __uint_as_float(r[2 * t + 1]), -INFINITY);
+#pragma unroll
+        for (int i2 = 8; i2 < AT_BN / 2; ++i2)
+          m8[i2 & 7] = fmax3(m8[i2 & 7], __uint_as_float(r[2 * i2]), __uint_as_float(r[2 * i2 + 1]));
+        const float mx = sc * fmax3(fmax3(m8[0], m8[1], m8[2]), fmax3(m8[3], m8[4], m8[5]), fmaxf(m8[6], m8[7]));
+        const bool grow = mx > m + AT_RESCALE_THRESHOLD;
+        if (__any_sync(0xffffffffu, grow)) {
+          const float alpha = grow ? fast_exp2(m - mx) : 1.f;
+          rescale_o(alpha);
+          l *= alpha;
+          if (grow) m = mx;
+#pragma unroll
+          for (int t = 0; t < 4; ++t) rs2[t] = f2_pack(0.f, 0.f);
+          exp_chunk(0, f2_pack(-m, -m), pk0, rs2);
+          exp_chunk(1, f2_pack(-m, -m), pk1, rs2);
+        }
+        AT_PROF_MARK(3);
+        tmem_st_32x32b_x16(t_s, pk0);
+        tmem_st_32x32b_x16(t_s + 16, pk1);
+        publish_half(0);
+        exp_chunk(2, f2_pack(-m, -m), pk0, rs2);
+        exp_chunk(3, f2_pack(-m, -m), pk1, rs2);
+        tmem_st_32x32b_x16(t_s + 32, pk0);
+        tmem_st_32x32b_x16(t_s + 48, pk1);
+        publish_half(1);
+      } else
+#endif
+      {
+#if !AT_SPLIT_LD
+      // row max as 8 independent FMNMX3 chains (a single chain is 64 dependent ops)
+      float m8[8];
+#pragma unroll
+      for (int t = 0; t < 8; ++t) m8[t] = fmax3(__uint_as_float(r[2 * t]), __uint_as_float(r[2 * t + 1]), -INFINITY);
+#pragma unroll
+      for (int i2 = 8; i2 < AT_BN / 2; ++i2)
+        m8[i2 & 7] = fmax3(m8[i2 & 7], __uint_as_float(r[2 * i2]), __uint_as_float(r[2 * i2 + 1]));
+#endif
+      float mx = fmax3(fmax3(m8[0], m8[1], m8[2]), fmax3(m8[3], m8[4], m8[5]), fmaxf(m8[6], m8[7]));
+      mx *= sc;
+      const bool grow = mx > m + AT_RESCALE_THRESHOLD;
+      if (i > 0 && __any_sync(0xffffffffu, grow)) {
+        const float alpha = grow ? fast_exp2(m - mx) : 1.f;
+        rescale_o(alpha);
+        l *= alpha;
+      }
+      if (grow) m = mx;
+      AT_PROF_MARK(3);
+      const uint64_t nm2 = f2_pack(-m, -m);
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        uint32_t pk[16];
+        exp_chunk(c, nm2, pk, rs2);
+        tmem_st_32x32b_x16(t_s + c * 16, pk);          // columns [16c, 16c+16): already in registers
+        if (c & 1) publish_half(c >> 1);
+      }
       }
       float rs_lo, rs_hi;
       f2_unpack(f2_add(f2_add(rs2[0], rs2[1]), f2_add(rs2[2], rs2[3])), rs_lo, rs_hi);
