@@ -17,9 +17,11 @@
 //                              O_x += P_x V (P_x read from TMEM, V as an
 //                              MN-major smem operand) accumulated in TMEM;
 //                              ping-pongs between the two tiles
-//       warps 4-7 / 8-11 softmax of tile 0 / 1: max pass, lazy rescale of O
-//                              in TMEM, exp2, P (bf16x2) back into TMEM;
-//                              final epilogue
+//       warps 4-7 / 8-11 softmax of tile 0 / 1 (AT_CW = 2: two warps per
+//                              32-row quadrant, 64 key columns each, the
+//                              row max exchanged through smem): max pass,
+//                              lazy rescale of O in TMEM, exp2, P (bf16x2)
+//                              back into TMEM; final epilogue
 //   * ring (n > 1), the reference's schedule (workloads.py:644-685): work
 //     units are (step, item) in step-major order over the persistent compute
 //     CTAs. Step 0 reads the local shard; step s >= 1 reads slot s & 1 of a
@@ -42,16 +44,26 @@
 
 namespace pk {
 
-#ifndef AT_SPEC       // 1: the first half's P computed against the running max while the row max is found
-#define AT_SPEC 0       // measured: no gain at kv 32768 / 65536, 4 % slower at kv 131072 (profiles/r2/attn_spec_ab.jsonl)
-#endif
-#ifndef AT_SPLIT_LD   // 1: S row loaded in two TMEM waits (first half's max overlaps the second load)
-#define AT_SPLIT_LD 0   // measured +1 % at S 16384, -10 % on the n = 8 rank step
-#endif
+// (measured and removed: a speculative first-half softmax against the running
+// max, and an S row loaded in two TMEM waits — DESIGN.md §8)
 constexpr int AT_BM = 128;       // queries per tile (two tiles per CTA)
 constexpr int AT_BN = 128;       // keys per block
 constexpr int AT_D = 128;        // head dim
-constexpr int AT_THREADS = 384;  // loader, MMA, TMEM alloc, idle, 2 x 4 softmax warps
+#ifndef AT_CW
+#define AT_CW 1          // softmax warps per 32-row quadrant of a tile (1 or 2; 2 measured
+#endif                   // 13-17 % slower: +33 % instructions, profiles/r2/attn_power.jsonl)
+constexpr int AT_NC = AT_BN / AT_CW;             // S columns per softmax warp
+constexpr int AT_OC = AT_D / AT_CW;              // O columns per softmax warp
+constexpr int AT_THREADS = 128 + 256 * AT_CW;    // loader, MMA, TMEM alloc, idle, 2 tiles x 4 quadrants x AT_CW softmax warps
+constexpr int AT2_THREADS = 384;                 // the CTA-pair kernel: one softmax warp per quadrant
+// setmaxnreg budgets: the CTA holds AT_THREADS x (65536 / AT_THREADS rounded down to 8)
+// registers; what the first warpgroup gives back is what the softmax warps may take
+constexpr int AT_REG_OTHER = 56;
+constexpr int AT_REG_SOFTMAX = AT_CW == 1 ? 224 : 104;
+static_assert(128 * AT_REG_OTHER + 256 * AT_CW * AT_REG_SOFTMAX <= AT_THREADS * ((65536 / AT_THREADS) & ~7),
+              "setmaxnreg budgets exceed the CTA's launch allocation");
+// shared-memory row-max (double-buffered) and row-sum exchange between a quadrant's warps
+constexpr int AT_RED_BYTES = AT_CW > 1 ? (2 * 2 * AT_CW * AT_BM + 2 * AT_CW * AT_BM) * 4 : 0;
 constexpr int AT_Q_BYTES = AT_BM * AT_D * 2;     // 32 KB per tile (2 swizzle atoms of 16 KB)
 constexpr int AT_K_BYTES = AT_BN * AT_D * 2;     // 32 KB
 constexpr int AT_V_BYTES = AT_BN * AT_D * 2;     // 32 KB
@@ -60,7 +72,7 @@ constexpr int AT_V_BYTES = AT_BN * AT_D * 2;     // 32 KB
 #endif
 constexpr int AT_KSTAGES = AT_KS;
 constexpr int AT_VSTAGES = 2;
-constexpr int AT_SMEM = 2 * AT_Q_BYTES + AT_KSTAGES * AT_K_BYTES + AT_VSTAGES * AT_V_BYTES + 512 + 1024;
+constexpr int AT_SMEM = 2 * AT_Q_BYTES + AT_KSTAGES * AT_K_BYTES + AT_VSTAGES * AT_V_BYTES + 512 + AT_RED_BYTES + 1024;
 constexpr int AT_TMEM_COLS = 512;                // per tile: S (128, P aliased in its first 64) + O (128)
 constexpr float AT_RESCALE_THRESHOLD = 8.0f;     // log2 units: P stays <= 2^8 between rescales
 #ifndef AT_POLY_DEG
@@ -356,7 +368,7 @@ __global__ void __launch_bounds__(AT_THREADS, 1) attn_fwd_kernel(const __grid_co
       mbar_init(&v_full[i], 1); mbar_init(&v_empty[i], 1);
       mbar_init(&s_full[i], 1); mbar_init(&o_full[i], 1);
       mbar_init(&p_full[2 * i], 4); mbar_init(&p_full[2 * i + 1], 4);
-      mbar_init(&o_empty[i], 4);
+      mbar_init(&o_empty[i], 4 * AT_CW);
     }
     fence_mbar_init();
   }
@@ -465,9 +477,9 @@ __global__ void __launch_bounds__(AT_THREADS, 1) attn_fwd_kernel(const __grid_co
     }
     __syncwarp();
   } else if (warp < 4) {
-  // (the CTA holds 168 x 384 registers: 56 + 2 x 224 uses exactly that, so
-  // the softmax warpgroups' increase can complete)
-  asm volatile("setmaxnreg.dec.sync.aligned.u32 56;\n" ::: "memory");
+  // (the increase of the softmax warps can only complete from what this
+  // warpgroup gives back: see AT_REG_SOFTMAX)
+  asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" :: "n"(AT_REG_OTHER) : "memory");
   if (warp == 0) {
     // ------------------------------------------------------------ loader (lane 0)
     if (lane == 0) {
@@ -643,59 +655,52 @@ __global__ void __launch_bounds__(AT_THREADS, 1) attn_fwd_kernel(const __grid_co
     }
   }
   } else {
-  asm volatile("setmaxnreg.inc.sync.aligned.u32 224;\n" ::: "memory");
+  asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" :: "n"(AT_REG_SOFTMAX) : "memory");
   // ------------------------------------------------------------ softmax + epilogue (tile x)
-  const int x = (warp - 4) / 4;
+  // AT_CW warps share each 32-row quadrant of a tile: warp h of the quadrant
+  // owns S columns [h*AT_NC, (h+1)*AT_NC) (so P half h when AT_CW = 2) and O
+  // columns [h*AT_OC, (h+1)*AT_OC). The row max is exchanged through shared
+  // memory (one 64-thread named barrier per block), the row sums once per
+  // segment. Two warps per quadrant halve each tile's softmax latency — the
+  // chain S -> P -> PV -> next QK that paces a tile — and let one warp issue
+  // while the other waits on MUFU.
+  const int x = (warp - 4) / (4 * AT_CW);
+  const int h = ((warp - 4) / 4) % AT_CW;
   const int q = warp & 3;
   const int row = q * 32 + (int)lane;
   const uint32_t lane_off = (uint32_t)(q * 32) << 16;
   const uint32_t t_s = tmem + 256 * x + lane_off;
   const uint32_t t_o = t_s + 128;
+  const uint32_t t_my_s = t_s + h * AT_NC;        // my S columns
+  const uint32_t t_my_o = t_o + h * AT_OC;        // my O columns
+  const int bar_q = 3 + 4 * x + q;                // the quadrant's warps (AT_CW > 1)
+  const int bar_tile = 1 + x;                     // the tile's softmax warps
+  constexpr int TILE_THREADS = 128 * AT_CW;
+  float* red_m = reinterpret_cast<float*>(tmem_slot + 4);   // [2 parity][2 tiles][AT_CW][128]
+  float* red_l = red_m + 2 * 2 * AT_CW * AT_BM;             // [2 tiles][AT_CW][128]
   const float sc = a.scale_log2;
   int gx = 0, segx = 0;
   SegIter it = seg_begin();
   for (SegInfo sg; seg_next(it, sg);) {
     if (x >= sg.ntile) continue;
     const int len = sg.j1 - sg.j0;
-    float m = -INFINITY, l = 0.f;     // m: the max the current P values are relative to (log2 units)
+    float m = -INFINITY, l = 0.f;     // m: the max the current P values are relative to (log2 units); l: my columns' sum
     for (int i = 0; i < len; ++i, ++gx) {
       AT_PROF_MARK(0);
       mbar_wait(&s_full[x], gx & 1);
       tc_fence_after();
       AT_PROF_MARK(1);
 #ifdef AT_MMA_ONLY   // timing diagnostic only: the MMA pipeline without softmax (wrong results)
-      if (lane == 0) { mbar_arrive(&p_full[2 * x]); mbar_arrive(&p_full[2 * x + 1]); }
+      if (lane == 0)
+        for (int hh = h * (2 / AT_CW); hh < (h + 1) * (2 / AT_CW); ++hh) mbar_arrive(&p_full[2 * x + hh]);
       continue;
 #endif
-      // the whole S row (128 fp32) into registers with one TMEM wait; the max
-      // and exp passes both read registers
-      uint32_t r[AT_BN];
-#if AT_SPLIT_LD
-      // first half waited for, second half in flight while the first half's max runs
+      // my S columns into registers with one TMEM wait; the max and exp passes read registers
+      uint32_t r[AT_NC];
 #pragma unroll
-      for (int c = 0; c < 2; ++c) tmem_ld_32x32b_x32(t_s + c * 32, *reinterpret_cast<uint32_t(*)[32]>(r + c * 32));
-      tmem_ld_wait();
-#pragma unroll
-      for (int c = 2; c < 4; ++c) tmem_ld_32x32b_x32(t_s + c * 32, *reinterpret_cast<uint32_t(*)[32]>(r + c * 32));
-      float m8[8];
-#pragma unroll
-      for (int t = 0; t < 8; ++t) m8[t] = fmax3(__uint_as_float(r[2 * t]), __uint_as_float(r[2 * t + 1]), -INFINITY);
-#pragma unroll
-      for (int i2 = 8; i2 < AT_BN / 4; ++i2)
-        m8[i2 & 7] = fmax3(m8[i2 & 7], __uint_as_float(r[2 * i2]), __uint_as_float(r[2 * i2 + 1]));
-      tmem_ld_wait();
-#pragma unroll
-      for (int i2 = AT_BN / 2; i2 < AT_BN; ++i2) asm volatile("" : "+r"(r[i2]));   // no use before the wait
-#pragma unroll
-      for (int i2 = AT_BN / 4; i2 < AT_BN / 2; ++i2)
-        m8[i2 & 7] = fmax3(m8[i2 & 7], __uint_as_float(r[2 * i2]), __uint_as_float(r[2 * i2 + 1]));
-      AT_PROF_MARK(2);
-#else
-#pragma unroll
-      for (int c = 0; c < 4; ++c) tmem_ld_32x32b_x32(t_s + c * 32, *reinterpret_cast<uint32_t(*)[32]>(r + c * 32));
+      for (int c = 0; c < AT_NC / 32; ++c) tmem_ld_32x32b_x32(t_my_s + c * 32, *reinterpret_cast<uint32_t(*)[32]>(r + c * 32));
       tmem_ld_wait();
       AT_PROF_MARK(2);
-#endif
       // packed fp32 pairs: one FFMA2 computes s*scale - m for two keys, one FADD2
       // accumulates two probabilities (the softmax warps are issue-bound)
       auto exp_chunk = [&](int c, uint64_t nm2, uint32_t (&pk)[16], uint64_t (&rs2)[4]) {
@@ -715,76 +720,47 @@ __global__ void __launch_bounds__(AT_THREADS, 1) attn_fwd_kernel(const __grid_co
           pk[i2] = pack_bf16x2(p0, p1);
         }
       };
-      auto publish_half = [&](int h) {                  // keys [64h, 64h+64) are in TMEM: release that half
+      auto publish_half = [&](int hh) {                 // keys [64hh, 64hh+64) are in TMEM: release that half
         tmem_st_wait();
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(&p_full[2 * x + h]);
+        if (lane == 0) mbar_arrive(&p_full[2 * x + hh]);
       };
       auto rescale_o = [&](float alpha) {
 #pragma unroll 1
-        for (int c = 0; c < 4; ++c) {
+        for (int c = 0; c < AT_OC / 32; ++c) {
           uint32_t o[32];
-          tmem_ld_32x32b_x32(t_o + c * 32, o);
+          tmem_ld_32x32b_x32(t_my_o + c * 32, o);
           tmem_ld_wait();
 #pragma unroll
           for (int i2 = 0; i2 < 32; ++i2) o[i2] = __float_as_uint(__uint_as_float(o[i2]) * alpha);
-          tmem_st_32x32b_x32(t_o + c * 32, o);
+          tmem_st_32x32b_x32(t_my_o + c * 32, o);
         }
       };
       uint64_t rs2[4];                                    // 4 independent row-sum chains
 #pragma unroll
       for (int t = 0; t < 4; ++t) rs2[t] = f2_pack(0.f, 0.f);
-#if AT_SPEC && !AT_SPLIT_LD
-      if (i > 0) {
-        // speculative: the first half's P against the current max while the
-        // row max is computed alongside (independent instruction streams); the
-        // max only gates publishing. A row whose max grew past the threshold
-        // (rare after the first block) discards the speculation: rescale O,
-        // move m, recompute.
-        uint32_t pk0[16], pk1[16];
-        exp_chunk(0, f2_pack(-m, -m), pk0, rs2);
-        exp_chunk(1, f2_pack(-m, -m), pk1, rs2);
-        float m8[8];
-#pragma unroll
-        for (int t = 0; t < 8; ++t) m8[t] = fmax3(__uint_as_float(r[2 * t]), __uint_as_float(r[2 * t + 1]), -INFINITY);
-#pragma unroll
-        for (int i2 = 8; i2 < AT_BN / 2; ++i2)
-          m8[i2 & 7] = fmax3(m8[i2 & 7], __uint_as_float(r[2 * i2]), __uint_as_float(r[2 * i2 + 1]));
-        const float mx = sc * fmax3(fmax3(m8[0], m8[1], m8[2]), fmax3(m8[3], m8[4], m8[5]), fmaxf(m8[6], m8[7]));
-        const bool grow = mx > m + AT_RESCALE_THRESHOLD;
-        if (__any_sync(0xffffffffu, grow)) {
-          const float alpha = grow ? fast_exp2(m - mx) : 1.f;
-          rescale_o(alpha);
-          l *= alpha;
-          if (grow) m = mx;
-#pragma unroll
-          for (int t = 0; t < 4; ++t) rs2[t] = f2_pack(0.f, 0.f);
-          exp_chunk(0, f2_pack(-m, -m), pk0, rs2);
-          exp_chunk(1, f2_pack(-m, -m), pk1, rs2);
-        }
-        AT_PROF_MARK(3);
-        tmem_st_32x32b_x16(t_s, pk0);
-        tmem_st_32x32b_x16(t_s + 16, pk1);
-        publish_half(0);
-        exp_chunk(2, f2_pack(-m, -m), pk0, rs2);
-        exp_chunk(3, f2_pack(-m, -m), pk1, rs2);
-        tmem_st_32x32b_x16(t_s + 32, pk0);
-        tmem_st_32x32b_x16(t_s + 48, pk1);
-        publish_half(1);
-      } else
-#endif
-      {
-#if !AT_SPLIT_LD
-      // row max as 8 independent FMNMX3 chains (a single chain is 64 dependent ops)
+      // row max over my columns as 8 independent FMNMX3 chains
       float m8[8];
 #pragma unroll
       for (int t = 0; t < 8; ++t) m8[t] = fmax3(__uint_as_float(r[2 * t]), __uint_as_float(r[2 * t + 1]), -INFINITY);
 #pragma unroll
-      for (int i2 = 8; i2 < AT_BN / 2; ++i2)
+      for (int i2 = 8; i2 < AT_NC / 2; ++i2)
         m8[i2 & 7] = fmax3(m8[i2 & 7], __uint_as_float(r[2 * i2]), __uint_as_float(r[2 * i2 + 1]));
-#endif
       float mx = fmax3(fmax3(m8[0], m8[1], m8[2]), fmax3(m8[3], m8[4], m8[5]), fmaxf(m8[6], m8[7]));
+      if constexpr (AT_CW > 1) {
+        // exchange with the quadrant's other warps (double-buffered by block parity).
+        // The barrier also orders every warp's S loads before any warp's P stores
+        // (P half h aliases S columns another warp may own).
+        float* rm = red_m + ((gx & 1) * 2 + x) * AT_CW * AT_BM;
+        rm[h * AT_BM + row] = mx;
+        tc_fence_before();
+        asm volatile("bar.sync %0, %1;" :: "r"(bar_q), "n"(32 * AT_CW) : "memory");
+        tc_fence_after();
+#pragma unroll
+        for (int hh = 0; hh < AT_CW; ++hh)
+          if (hh != h) mx = fmaxf(mx, rm[hh * AT_BM + row]);
+      }
       mx *= sc;
       const bool grow = mx > m + AT_RESCALE_THRESHOLD;
       if (i > 0 && __any_sync(0xffffffffu, grow)) {
@@ -796,12 +772,12 @@ __global__ void __launch_bounds__(AT_THREADS, 1) attn_fwd_kernel(const __grid_co
       AT_PROF_MARK(3);
       const uint64_t nm2 = f2_pack(-m, -m);
 #pragma unroll
-      for (int c = 0; c < 4; ++c) {
+      for (int c = 0; c < AT_NC / 32; ++c) {
         uint32_t pk[16];
         exp_chunk(c, nm2, pk, rs2);
-        tmem_st_32x32b_x16(t_s + c * 16, pk);          // columns [16c, 16c+16): already in registers
-        if (c & 1) publish_half(c >> 1);
-      }
+        const int cg = h * (AT_NC / 32) + c;            // global 32-key chunk
+        tmem_st_32x32b_x16(t_s + cg * 16, pk);          // packed P columns [16cg, 16cg+16)
+        if (cg & 1) publish_half(cg >> 1);
       }
       float rs_lo, rs_hi;
       f2_unpack(f2_add(f2_add(rs2[0], rs2[1]), f2_add(rs2[2], rs2[3])), rs_lo, rs_hi);
@@ -810,19 +786,29 @@ __global__ void __launch_bounds__(AT_THREADS, 1) attn_fwd_kernel(const __grid_co
       AT_PROF_FLUSH();
     }
     // ------------------------------------------------------------ epilogue
-    float o[AT_D];
+    if constexpr (AT_CW > 1) {
+      // the row sum over all columns (the warps' m agree)
+      float* rl = red_l + x * AT_CW * AT_BM;
+      rl[h * AT_BM + row] = l;
+      asm volatile("bar.sync %0, %1;" :: "r"(bar_q), "n"(32 * AT_CW) : "memory");
+      float lt = 0.f;
+#pragma unroll
+      for (int hh = 0; hh < AT_CW; ++hh) lt += rl[hh * AT_BM + row];
+      l = lt;
+    }
+    float o[AT_OC];
     // ring, step s > 0: the item's running state from steps < s is loaded
-    // (all 32 vectors in flight) while the unit's last PV finishes, then
-    // merged chunk by chunk with O as it leaves TMEM (o[] holds the merge)
+    // (all vectors in flight) while the unit's last PV finishes, then merged
+    // chunk by chunk with O as it leaves TMEM (o[] holds the merge)
     const int rstep = ring ? sg.j0 / bps : 0;
     const bool has_state = ring && rstep > 0;
     float* stt = ring ? a.ring_state + (long long)(2 * sg.item + x) * AT_STATE_FLOATS : nullptr;
-    float4* st_o = reinterpret_cast<float4*>(stt) + row;                         // + c4 * AT_BM
+    float4* st_o = reinterpret_cast<float4*>(stt) + (h * AT_OC / 4) * AT_BM + row;   // + c4 * AT_BM
     float2* st_ml = reinterpret_cast<float2*>(stt + (AT_D / 4) * AT_BM * 4) + row;
     float m_s = -INFINITY, l_s = 0.f;
     if constexpr (RING) {
 #pragma unroll
-      for (int i2 = 0; i2 < AT_D; ++i2) o[i2] = 0.f;            // no state: w_s = 0, w_u = 1 below
+      for (int i2 = 0; i2 < AT_OC; ++i2) o[i2] = 0.f;            // no state: w_s = 0, w_u = 1 below
     }
 #ifdef AT_RING_PROF
     const long long tep = clock64();
@@ -839,7 +825,7 @@ __global__ void __launch_bounds__(AT_THREADS, 1) attn_fwd_kernel(const __grid_co
 #endif
       __syncwarp();
 #pragma unroll
-      for (int i2 = 0; i2 < AT_D / 4; ++i2) {
+      for (int i2 = 0; i2 < AT_OC / 4; ++i2) {
         const float4 v = __ldcg(st_o + i2 * AT_BM);
         o[4 * i2] = v.x; o[4 * i2 + 1] = v.y; o[4 * i2 + 2] = v.z; o[4 * i2 + 3] = v.w;
       }
@@ -860,9 +846,9 @@ __global__ void __launch_bounds__(AT_THREADS, 1) attn_fwd_kernel(const __grid_co
     const float w_s = (m_s == -INFINITY) ? 0.f : fast_exp2(m_s - m_n);     // state weight
     const float w_u = (m == -INFINITY) ? 0.f : fast_exp2(m - m_n);         // this unit's weight
 #pragma unroll
-    for (int c = 0; c < AT_D / 32; ++c) {
+    for (int c = 0; c < AT_OC / 32; ++c) {
       uint32_t t[32];
-      tmem_ld_32x32b_x32(t_o + c * 32, t);
+      tmem_ld_32x32b_x32(t_my_o + c * 32, t);
       tmem_ld_wait();
       if constexpr (RING) {
 #pragma unroll
@@ -889,13 +875,13 @@ __global__ void __launch_bounds__(AT_THREADS, 1) attn_fwd_kernel(const __grid_co
     bool write_final = true;
     if (ring && rstep + 1 < a.ring_steps) {
       // keep the merged state for step s + 1 (steps merge in ascending order);
-      // the tile's 128 threads sync, then one release publishes all their rows
+      // the tile's threads sync, then one release publishes all their rows
 #pragma unroll
-      for (int i2 = 0; i2 < AT_D / 4; ++i2)
+      for (int i2 = 0; i2 < AT_OC / 4; ++i2)
         st_o[i2 * AT_BM] = make_float4(o[4 * i2], o[4 * i2 + 1], o[4 * i2 + 2], o[4 * i2 + 3]);
-      *st_ml = make_float2(m, l);
-      asm volatile("bar.sync %0, 128;" :: "r"(1 + x) : "memory");
-      if (row == 0)
+      if (h == 0) *st_ml = make_float2(m, l);
+      asm volatile("bar.sync %0, %1;" :: "r"(bar_tile), "n"(TILE_THREADS) : "memory");
+      if (row == 0 && h == 0)
         asm volatile("st.release.gpu.global.u32 [%0], %1;" :: "l"(rc.merged(sg.item, x)), "r"((uint32_t)rstep + 1)
                      : "memory");
       write_final = false;
@@ -914,25 +900,26 @@ __global__ void __launch_bounds__(AT_THREADS, 1) attn_fwd_kernel(const __grid_co
       // (column-quad-major like the ring state: a warp's 16 B accesses are contiguous)
       float* mine = a.part + ((long long)sp.slot(me, sg.ti) * 2 + x) * AT_STATE_FLOATS;
 #pragma unroll
-      for (int i2 = 0; i2 < AT_D / 4; ++i2)
-        reinterpret_cast<float4*>(mine)[i2 * AT_BM + row] = make_float4(o[4 * i2], o[4 * i2 + 1], o[4 * i2 + 2], o[4 * i2 + 3]);
-      reinterpret_cast<float2*>(mine + (AT_D / 4) * AT_BM * 4)[row] = make_float2(m, l);
+      for (int i2 = 0; i2 < AT_OC / 4; ++i2)
+        reinterpret_cast<float4*>(mine)[(h * AT_OC / 4 + i2) * AT_BM + row] =
+            make_float4(o[4 * i2], o[4 * i2 + 1], o[4 * i2 + 2], o[4 * i2 + 3]);
+      if (h == 0) reinterpret_cast<float2*>(mine + (AT_D / 4) * AT_BM * 4)[row] = make_float2(m, l);
       __threadfence();
-      asm volatile("bar.sync %0, 128;" :: "r"(1 + x) : "memory");
-      if (row == 0) {
+      asm volatile("bar.sync %0, %1;" :: "r"(bar_tile), "n"(TILE_THREADS) : "memory");
+      if (row == 0 && h == 0) {
         const uint32_t done = atomicAdd(a.item_count + 2 * sg.item + x, 1u);
         int nseg = 0;                                 // CTAs with a non-empty share of this item
         for (int c = c_lo; c <= c_hi; ++c) nseg += sp.tstart(c + 1) > sp.tstart(c);
         merge_flag[x] = (done == (uint32_t)(nseg - 1)) ? 1 : 0;
       }
-      asm volatile("bar.sync %0, 128;" :: "r"(1 + x) : "memory");
+      asm volatile("bar.sync %0, %1;" :: "r"(bar_tile), "n"(TILE_THREADS) : "memory");
       write_final = merge_flag[x] != 0;
       if (write_final) {
         __threadfence();
         // merge every segment's partial in ascending CTA order (log2 domain)
         float mt = -INFINITY, lt = 0.f;
 #pragma unroll
-        for (int i2 = 0; i2 < AT_D; ++i2) o[i2] = 0.f;
+        for (int i2 = 0; i2 < AT_OC; ++i2) o[i2] = 0.f;
         for (int c = c_lo; c <= c_hi; ++c) {
           if (sp.tstart(c + 1) == sp.tstart(c)) continue;   // no share of the tail
           const float* pr = a.part + ((long long)sp.slot(c, sg.ti) * 2 + x) * AT_STATE_FLOATS;
@@ -942,8 +929,8 @@ __global__ void __launch_bounds__(AT_THREADS, 1) attn_fwd_kernel(const __grid_co
           const float wa = (mt == -INFINITY) ? 0.f : fast_exp2(mt - mn);
           const float wb = (mc == -INFINITY) ? 0.f : fast_exp2(mc - mn);
 #pragma unroll
-          for (int i2 = 0; i2 < AT_D / 4; ++i2) {
-            const float4 v = __ldcg(reinterpret_cast<const float4*>(pr) + i2 * AT_BM + row);
+          for (int i2 = 0; i2 < AT_OC / 4; ++i2) {
+            const float4 v = __ldcg(reinterpret_cast<const float4*>(pr) + (h * AT_OC / 4 + i2) * AT_BM + row);
             o[4 * i2 + 0] = o[4 * i2 + 0] * wa + v.x * wb;
             o[4 * i2 + 1] = o[4 * i2 + 1] * wa + v.y * wb;
             o[4 * i2 + 2] = o[4 * i2 + 2] * wa + v.z * wb;
@@ -954,14 +941,14 @@ __global__ void __launch_bounds__(AT_THREADS, 1) attn_fwd_kernel(const __grid_co
         }
         m = mt;
         l = lt;
-        if (row == 0) a.item_count[2 * sg.item + x] = 0;   // re-armed for the next launch
+        if (row == 0 && h == 0) a.item_count[2 * sg.item + x] = 0;   // re-armed for the next launch
       }
     }
     if (write_final) {
       const float inv = (l > 0.f) ? 1.f / l : 0.f;
-      uint4* dst = reinterpret_cast<uint4*>(a.o + (((long long)sg.b * a.S_q + sq_idx) * a.H + sg.h) * AT_D);
+      uint4* dst = reinterpret_cast<uint4*>(a.o + (((long long)sg.b * a.S_q + sq_idx) * a.H + sg.h) * AT_D + h * AT_OC);
 #pragma unroll
-      for (int i2 = 0; i2 < AT_D / 8; ++i2) {
+      for (int i2 = 0; i2 < AT_OC / 8; ++i2) {
         uint4 w;
         w.x = pack_bf16x2(o[8 * i2 + 0] * inv, o[8 * i2 + 1] * inv);
         w.y = pack_bf16x2(o[8 * i2 + 2] * inv, o[8 * i2 + 3] * inv);
@@ -969,7 +956,7 @@ __global__ void __launch_bounds__(AT_THREADS, 1) attn_fwd_kernel(const __grid_co
         w.w = pack_bf16x2(o[8 * i2 + 6] * inv, o[8 * i2 + 7] * inv);
         dst[i2] = w;
       }
-      a.lse[srow] = (m + log2f(l)) * 0.69314718055994531f;
+      if (h == 0) a.lse[srow] = (m + log2f(l)) * 0.69314718055994531f;
     }
   }
   }
@@ -1035,7 +1022,7 @@ PK_DEV void umma_f16_ts2(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc, uint3
       :: "r"(tmem_d), "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(accum) : "memory");
 }
 
-__global__ void __launch_bounds__(AT_THREADS, 1) attn2_fwd_kernel(const __grid_constant__ AttnArgs a) {
+__global__ void __launch_bounds__(AT2_THREADS, 1) attn2_fwd_kernel(const __grid_constant__ AttnArgs a) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sq = smem;                               // [2][32 KB]: this CTA's two query tiles
@@ -1333,7 +1320,7 @@ static int launch_attn(AttnScratch& scr, int num_sms, AttnArgs& a, cudaStream_t 
     PK_TRY(ensure_smem_attr((const void*)attn2_fwd_kernel, AT2_SMEM));
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(2 * a.B * a.H * (a.S_q / (4 * AT_BM)), 1, 1);
-    cfg.blockDim = dim3(AT_THREADS, 1, 1);
+    cfg.blockDim = dim3(AT2_THREADS, 1, 1);
     cfg.dynamicSmemBytes = AT2_SMEM;
     cfg.stream = st;
     cudaLaunchAttribute attr[1];
