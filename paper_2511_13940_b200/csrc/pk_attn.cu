@@ -102,6 +102,7 @@ struct AttnArgs {
   uint32_t* item_count;          // [items * 2] segments finished per (item, tile); re-armed by the merger
   int tail_items;                // R: the last R items are split over tail_units CTAs (0: no split)
   int tail_units;
+  int persistent;                // 1: gridDim CTAs walk the whole items round-robin, then the tail
   // device-staged ring (ring_steps > 1): see the header comment
   CUtensorMap tm_ks, tm_vs;      // the 2-slot stage, [2B, S, H, D] (slot = batch / B)
   int ring_steps;                // n
@@ -309,8 +310,11 @@ __global__ void __launch_bounds__(AT_THREADS, 1) attn_fwd_kernel(const __grid_co
   sp.G = a.tail_units > 0 ? (uint32_t)a.tail_units : 1u;
   sp.nblk = (uint32_t)nblk;
   sp.T = (uint32_t)a.tail_items * (uint32_t)nblk;
-  const int nfull = items - a.tail_items;           // CTAs [0, nfull) run whole items
-  const int me = (int)blockIdx.x - nfull;           // tail CTA index (< 0: a whole-item CTA)
+  const int nfull = items - a.tail_items;           // whole items (CTAs [0, nfull) when not persistent)
+  // tail CTA index (< 0: a one-item CTA); a persistent CTA c runs whole items
+  // c, c + grid, ... and then its share of the tail
+  const int me = a.persistent ? (int)blockIdx.x : (int)blockIdx.x - nfull;
+  const int wstride = a.persistent ? (int)gridDim.x : items;
   // ring mode: units (step, item) step-major over the compute CTAs; the last
   // ring_comm CTAs are communicators
   constexpr bool ring = RING;
@@ -321,11 +325,13 @@ __global__ void __launch_bounds__(AT_THREADS, 1) attn_fwd_kernel(const __grid_co
   const bool is_comm = ring && (int)blockIdx.x >= ncompute;
   const RingCtr rc{a.ring_ctr, a.ring_steps};
   const int bps = a.blocks_per_step;
-  const int t0 = me >= 0 ? (int)sp.tstart(me) : 0, t1 = me >= 0 ? (int)sp.tstart(me + 1) : 0;
+  const int t0 = (me >= 0 && a.tail_items) ? (int)sp.tstart(me) : 0;
+  const int t1 = (me >= 0 && a.tail_items) ? (int)sp.tstart(me + 1) : 0;
   // segment walk shared by every role: item, key blocks [j0, j1), pair shape
   struct SegInfo { int item, ti, j0, j1, qp, h, b, ntile; };
   struct SegIter {
-    int k;                                           // -1: the whole item pending, -2: done; else tail block
+    int k;                                           // ring: next unit; else next tail block
+    int w;                                           // next whole item
   };
   auto seg_next = [&](SegIter& it, SegInfo& g) -> bool {
     if (ring) {                                      // it.k = next unit index
@@ -336,14 +342,12 @@ __global__ void __launch_bounds__(AT_THREADS, 1) attn_fwd_kernel(const __grid_co
       g.ti = -1;
       g.j0 = (u / items) * bps;
       g.j1 = g.j0 + bps;
-    } else if (it.k == -2) {
-      return false;
-    } else if (it.k == -1) {
-      g.item = (int)blockIdx.x;
+    } else if (it.w < nfull) {
+      g.item = it.w;
       g.ti = -1;
       g.j0 = 0;
       g.j1 = nblk;
-      it.k = -2;
+      it.w += wstride;
     } else {
       if (it.k >= t1) return false;
       g.ti = it.k / nblk;
@@ -358,7 +362,12 @@ __global__ void __launch_bounds__(AT_THREADS, 1) attn_fwd_kernel(const __grid_co
     g.ntile = (2 * g.qp + 1 < q_tiles) ? 2 : 1;      // the last pair may hold one tile
     return true;
   };
-  auto seg_begin = [&]() { SegIter it; it.k = ring ? (int)blockIdx.x : (me < 0 ? -1 : t0); return it; };
+  auto seg_begin = [&]() {
+    SegIter it;
+    it.k = ring ? (int)blockIdx.x : t0;
+    it.w = (ring || (me >= 0 && !a.persistent)) ? nfull : (int)blockIdx.x;
+    return it;
+  };
 
   if (warp == 0 && lane == 0 && !is_comm) {
     mbar_init(q_full, 1);
@@ -1353,7 +1362,12 @@ static int launch_attn(AttnScratch& scr, int num_sms, AttnArgs& a, cudaStream_t 
   a.tail_items = split || getenv("PK_ATTN_FORCE_SPLIT") ? R : 0;
   if ((uint64_t)sms * ((uint64_t)a.tail_items * nblk + 1) >= (1ull << 32)) a.tail_items = 0;   // 32-bit split math
   a.tail_units = a.tail_items ? sms : 0;
-  const int grid = items - a.tail_items + a.tail_units;
+  // persistent CTAs (one per SM) walk the whole items round-robin: a CTA's
+  // next item starts (Q load, first QK) while its previous epilogue drains,
+  // instead of a new CTA's prologue after it exits
+  a.persistent = getenv("PK_ATTN_NO_PERSIST") ? 0 : 1;
+  const int grid = a.persistent ? (a.tail_items ? a.tail_units : std::min(items, sms))
+                                : items - a.tail_items + a.tail_units;
   const size_t part_bytes = (size_t)2 * std::max(1, a.tail_units) * 2 * AT_STATE_FLOATS * sizeof(float);
   if (scr.part_bytes < part_bytes) {
     if (scr.part) PK_CUDA(cudaFreeAsync(scr.part, st));

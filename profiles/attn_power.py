@@ -11,7 +11,7 @@ import paper_2511_13940_b200 as pk
 
 pynvml.nvmlInit()
 h = pynvml.nvmlDeviceGetHandleByIndex(0)
-lib = os.environ.get("PK_LIB", "libpk.so").split("/")[-1] + ("+pair" if os.environ.get("PK_ATTN_PAIR") else "")
+lib = os.environ.get("PK_LIB", "libpk.so").split("/")[-1] + "".join("+" + k[8:].lower() for k in sorted(os.environ) if k.startswith("PK_ATTN_"))
 out = open(sys.argv[1], "a") if len(sys.argv) > 1 else sys.stdout
 
 
