@@ -36,7 +36,15 @@ constexpr int kEpiWarp0 = 4;
 // EPI_REDUCE_ADD_F32: the fp32 accumulator itself is reduce-added (32-column
 // fp32 sub-tiles, 128 B rows) into fp32 partial sums on the owner — one
 // rounding to bf16 at the end instead of one per rank (GEMM-RS fp32 partials)
-enum EpiMode : int { EPI_STORE = 0, EPI_REDUCE_ADD = 1, EPI_SCATTER = 2, EPI_DIRECT = 3, EPI_REDUCE_ADD_F32 = 4 };
+enum EpiMode : int { EPI_STORE = 0, EPI_REDUCE_ADD = 1, EPI_SCATTER = 2, EPI_DIRECT = 3, EPI_REDUCE_ADD_F32 = 4,
+                     EPI_TOKENS_T = 5 };
+// EPI_TOKENS_T (grouped expert GEMM without row padding): each tile computes
+// Y^T = W_g . X^T for one plan tile of <= 256 token rows of group g (the
+// tile's valid rows, rounded up to 16, become the MMA's N) and 256 output
+// features of W_g (the MMA's M, the weight rows as the A operand). The
+// epilogue writes the tile transposed back into Y[token rows, features]
+// (through row_perm when set). The 256-row padding of every group's last tile
+// then costs at most 15 rows of tensor work instead of up to 255.
 constexpr int kTileRing = 4;                // depth of the tile-index broadcast ring
 constexpr int kAgCountOffset = 32768;       // AG piece counters live after the first 32K m-tile flags
 
@@ -56,6 +64,7 @@ struct SyncArgs {
 struct GemmArgs {
   CUtensorMap tmap_a[kMaxRanksDev];          // A row sources
   CUtensorMap tmap_b;                     // B^T [N, K] (K-major)
+  CUtensorMap tmap_b16;                   // EPI_TOKENS_T: the token rows again with 16-row boxes (partial tiles)
   CUtensorMap tmap_c[kMaxRanksDev];          // C destinations
   int M, N, K;
   int rank, world;
@@ -71,6 +80,7 @@ struct GemmArgs {
   const int32_t* num_m_tiles_dev;         // if set: number of valid M tiles (device)
   const int32_t* tile_group;              // [M tiles] group of each M tile (B rows group*N ..)
   const int32_t* row_perm;                // [M] destination row of each sorted row (-1 = padding)
+  const int32_t* tile_rows;               // EPI_TOKENS_T: [M tiles] valid token rows of each plan tile
   uint8_t* y;                             // EPI_SCATTER destination [rows, N] bf16
   long long y_ld;                         // bytes between rows of y
   uint32_t* tile_counter;                 // dynamic tile scheduler (0 at launch; reset by the last fetch)
@@ -156,11 +166,19 @@ PK_DEV void tile_coords(int t, int num_m, int num_n, int m_rot, int group, int d
   mt = (mt + m_rot) % num_m;
 }
 
+// EPI_TOKENS_T: the MMA N of plan tile mt, its valid rows rounded up to 32
+// (16 rows per CTA of the pair: one 16-row TMA box)
+PK_DEV int tokens_n(const GemmArgs& args, int mt) {
+  const int v = args.tile_rows[mt];
+  return v <= 32 ? 32 : (v >= 256 ? 256 : (v + 31) & ~31);
+}
+
 template <int CG, int BN, int AM, int EPI>
 __global__ void __launch_bounds__(GemmCfg<CG, BN, AM>::NUM_THREADS, 1)
 lcsc_gemm_kernel(const __grid_constant__ GemmArgs args) {
   using Cfg = GemmCfg<CG, BN, AM>;
   static_assert(EPI != EPI_REDUCE_ADD_F32 || Cfg::EPI_NBUF == 2, "fp32 partials need the double-buffered epilogue");
+  static_assert(EPI != EPI_TOKENS_T || (CG == 2 && AM == 1 && BN == 256), "token tiles: 256-feature pair tiles");
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* smem_a = smem;
@@ -499,8 +517,14 @@ lcsc_gemm_kernel(const __grid_constant__ GemmArgs args) {
       tile_coords(t, num_m, num_n, args.m_rot, args.raster_group, args.raster_dir, mt, nt);
       const int m_row = mt * Cfg::TILE_M + (int)cta_rank * Cfg::BM;
       const int src = (args.a_nsrc > 1) ? (mt * Cfg::TILE_M) / args.a_rows_per_src : 0;
-      const int a_row = args.a_base[src] + m_row - src * args.a_rows_per_src;
-      const int b_row = (args.tile_group ? args.tile_group[mt] * args.N : 0) + nt * BN + (int)cta_rank * Cfg::B_ROWS;
+      int a_row = args.a_base[src] + m_row - src * args.a_rows_per_src;
+      int b_row = (args.tile_group ? args.tile_group[mt] * args.N : 0) + nt * BN + (int)cta_rank * Cfg::B_ROWS;
+      if constexpr (EPI == EPI_TOKENS_T) {
+        // A operand: this CTA's 128 weight rows (features); B operand: its half
+        // of the tile's tokens (the pair splits the MMA's N)
+        a_row = args.tile_group[mt] * args.N + nt * BN + (int)cta_rank * Cfg::BM;
+        b_row = mt * Cfg::TILE_M + (int)cta_rank * (tokens_n(args, mt) / CG);
+      }
       if (args.a_wait_flag[src]) {
         wait_geq(args.sync.flags + mt, s_call[0], args.sync.err, args.sync.timeout_ns);
         fence_async_global();
@@ -514,7 +538,21 @@ lcsc_gemm_kernel(const __grid_constant__ GemmArgs args) {
         mbar_wait(&empty_bar[stage], phase ^ 1);
         uint8_t* sa = smem_a + stage * Cfg::A_BYTES;
         uint8_t* sb = smem_b + stage * Cfg::B_BYTES;
-        if (elect_one()) {
+        if constexpr (EPI == EPI_TOKENS_T) {
+          // a partial token tile loads only its rows (16-row boxes): a tile of
+          // a few tokens would otherwise move a full 128-row box per stage
+          const int rows = tokens_n(args, mt) / CG;
+          if (elect_one()) {
+            if (leader) mbar_arrive_expect_tx(&full_bar[stage], 2 * (Cfg::A_BYTES + rows * BLOCK_K * 2));
+            tma_load_2d_2sm(&args.tmap_a[0], &full_bar[stage], sa, kb * BLOCK_K, a_row);
+            if (rows == Cfg::B_ROWS) {
+              tma_load_2d_2sm(&args.tmap_b, &full_bar[stage], sb, kb * BLOCK_K, b_row);
+            } else {
+              for (int r = 0; r < rows; r += 16)
+                tma_load_2d_2sm(&args.tmap_b16, &full_bar[stage], sb + r * BLOCK_K * 2, kb * BLOCK_K, b_row + r);
+            }
+          }
+        } else if (elect_one()) {
           if constexpr (CG == 1) {
             mbar_arrive_expect_tx(&full_bar[stage], Cfg::STAGE_BYTES);
             tma_load_2d(&args.tmap_a[src], &full_bar[stage], sa, kb * BLOCK_K, a_row);
@@ -532,12 +570,18 @@ lcsc_gemm_kernel(const __grid_constant__ GemmArgs args) {
     } else if (warp == 1) {
     // ========================================================= consumer (MMA)
     if (leader) {
-      constexpr uint32_t idesc = idesc_bf16_f32(Cfg::UMMA_M, Cfg::UMMA_N);
+      constexpr uint32_t idesc_c = idesc_bf16_f32(Cfg::UMMA_M, Cfg::UMMA_N);
       int stage = 0;
       uint32_t phase = 0;
       for (int it = 0;; ++it) {
         const int t = tile_consume(it);
         if (t >= num_tiles) break;
+        uint32_t idesc = idesc_c;
+        if constexpr (EPI == EPI_TOKENS_T) {
+          int mt, nt;
+          tile_coords(t, num_m, num_n, args.m_rot, args.raster_group, args.raster_dir, mt, nt);
+          idesc = idesc_bf16_f32(Cfg::UMMA_M, tokens_n(args, mt));
+        }
         const int acc = (Cfg::ACC_STAGES == 2) ? (it & 1) : 0;
         const uint32_t acc_phase = (Cfg::ACC_STAGES == 2) ? ((it >> 1) & 1) : (it & 1);
         mbar_wait(&tempty_bar[acc], acc_phase ^ 1);
@@ -599,7 +643,45 @@ lcsc_gemm_kernel(const __grid_constant__ GemmArgs args) {
       mbar_wait(&tfull_bar[acc], acc_phase);
       tc_fence_after();
       const uint32_t t_lane = (uint32_t)(q * 32) << 16;
-      if constexpr (Cfg::ACC_STAGES == 1 && (EPI == EPI_STORE || EPI == EPI_REDUCE_ADD)) {
+      if constexpr (EPI == EPI_TOKENS_T) {
+        // lane = one output feature, TMEM columns = the tile's tokens: 32
+        // tokens per load; lane pairs swap halves so that each thread stores
+        // two adjacent features of one token (16 lanes cover 64 contiguous
+        // bytes of a token row)
+        const int valid = args.tile_rows[mt];
+        const int f0 = nt * BN + (int)cta_rank * Cfg::BM + q * 32;       // feature of lane 0
+        const int nch = (valid + 31) / 32;
+        const bool odd = lane & 1;
+        for (int c = 0; c < nch; ++c) {
+          uint32_t v[32];
+          tmem_ld_32x32b_x32(tmem_base + t_lane + (uint32_t)(acc * Cfg::ACC_COLS + c * 32), v);
+          tmem_ld_wait();
+          if (c == nch - 1) {
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive_cluster(&tempty_bar[acc], 0);
+          }
+#pragma unroll
+          for (int i = 0; i < 32; i += 2) {
+            const uint32_t send = odd ? v[i] : v[i + 1];
+            const uint32_t got = __shfl_xor_sync(0xffffffffu, send, 1);
+            const int tok = c * 32 + i + (odd ? 1 : 0);
+            const uint32_t w = odd ? pack_bf16x2(__uint_as_float(got), __uint_as_float(v[i + 1]))
+                                   : pack_bf16x2(__uint_as_float(v[i]), __uint_as_float(got));
+            if (tok < valid) {
+              int row = mt * Cfg::TILE_M + tok;
+              if (args.row_perm) row = args.row_perm[row];
+              if (row >= 0)
+                *reinterpret_cast<uint32_t*>(args.y + (long long)row * args.y_ld + (long long)(f0 + (lane & ~1u)) * 2) = w;
+            }
+          }
+        }
+        if (nch == 0) {
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive_cluster(&tempty_bar[acc], 0);
+        }
+      } else if constexpr (Cfg::ACC_STAGES == 1 && (EPI == EPI_STORE || EPI == EPI_REDUCE_ADD)) {
         // Single accumulator stage (512-row pair tiles fill TMEM): drain the
         // whole 256-column row into registers as packed bf16 first and release
         // TMEM at once, so the next tile's MMAs overlap the smem staging and

@@ -22,6 +22,11 @@
 namespace pk {
 
 int launch_gemm_grouped(const GemmArgs& args, int grid_ctas, cudaStream_t st);   // pk_ops.cu
+int launch_gemm_tokens(const GemmArgs& args, int grid_ctas, cudaStream_t st);    // pk_ops.cu
+
+// Token tiles (EPI_TOKENS_T) unless PK_GROUPED_PADDED is set (A/B hook: the
+// 256-row padded tiles with the weights as the B operand)
+static bool use_token_tiles() { return getenv("PK_GROUPED_PADDED") == nullptr; }
 
 constexpr int kGrpTile = 256;          // pair tile rows (CG = 2, AM = 1)
 constexpr int kMaxGroups = 1024;
@@ -35,6 +40,7 @@ struct GroupPlan {
   int32_t* offsets;            // [G]
   int32_t* cursor;             // [G]
   int32_t* tile_group;         // [max tiles]
+  int32_t* tile_rows;          // [max tiles] valid rows of each tile
   int32_t* num_tiles;          // [1]
   int32_t* row_perm;           // [R_pad]
   const uint8_t* a;            // [R, K] rows (bf16)
@@ -64,7 +70,10 @@ __global__ void grp_scan_kernel(const __grid_constant__ GroupPlan p, int max_til
     p.offsets[g] = off;
     p.cursor[g] = 0;
     const int tiles = (p.counts[g] + kGrpTile - 1) / kGrpTile;
-    for (int t = 0; t < tiles && off / kGrpTile + t < max_tiles; ++t) p.tile_group[off / kGrpTile + t] = g;
+    for (int t = 0; t < tiles && off / kGrpTile + t < max_tiles; ++t) {
+      p.tile_group[off / kGrpTile + t] = g;
+      p.tile_rows[off / kGrpTile + t] = min(kGrpTile, p.counts[g] - t * kGrpTile);
+    }
     off += tiles * kGrpTile;
   }
   *p.num_tiles = min(off / kGrpTile, max_tiles);
@@ -120,7 +129,7 @@ int grouped_gemm(const pk_tensor* A, const pk_tensor* group, const pk_tensor* W,
   static thread_local size_t plan_sz[64] = {};
   static thread_local void* abuf[64] = {};
   static thread_local size_t abuf_sz[64] = {};
-  const size_t plan_bytes = sizeof(int32_t) * (4 * (size_t)G + max_tiles + 2 + R_pad);
+  const size_t plan_bytes = sizeof(int32_t) * (4 * (size_t)G + 2 * (size_t)max_tiles + 2 + R_pad);
   const size_t a_bytes = (size_t)R_pad * K * 2;
   if (plan_sz[dev] < plan_bytes) {
     if (plan_buf[dev]) { PK_CUDA(cudaStreamSynchronize(st)); cudaFree(plan_buf[dev]); }
@@ -145,7 +154,8 @@ int grouped_gemm(const pk_tensor* A, const pk_tensor* group, const pk_tensor* W,
   p.cursor = base + 2 * G;
   p.num_tiles = base + 3 * G + 1;
   p.tile_group = base + 3 * G + 2;
-  p.row_perm = p.tile_group + max_tiles;
+  p.tile_rows = p.tile_group + max_tiles;
+  p.row_perm = p.tile_rows + max_tiles;
   p.a = static_cast<const uint8_t*>(A->ptr);
   p.a_ld = ldA * 2;
   p.a_sorted = static_cast<uint8_t*>(abuf[dev]);
@@ -166,6 +176,31 @@ int grouped_gemm(const pk_tensor* A, const pk_tensor* group, const pk_tensor* W,
   args.a_nsrc = 1;
   args.c_ndst = 1;
   args.raster_group = 8;
+  int clusters = std::max(1, (sched && sched->num_sms > 0 ? std::min(sched->num_sms, sms) : sms) / 2);
+  clusters = std::min<int64_t>(clusters, (int64_t)max_tiles * (N / 256));
+  args.num_compute_clusters = clusters;
+  if (use_token_tiles()) {
+    // weights as the A operand (256 features per pair tile), the sorted rows
+    // as the B operand, outputs scattered back through row_perm
+    PK_TRY(make_tmap_2d(&args.tmap_a[0], W->ptr, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, (int64_t)G * N, K, K, 128, BLOCK_K,
+                        CU_TENSOR_MAP_SWIZZLE_128B));
+    PK_TRY(make_tmap_2d(&args.tmap_b, p.a_sorted, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, R_pad, K, K, 128, BLOCK_K,
+                        CU_TENSOR_MAP_SWIZZLE_128B));
+    PK_TRY(make_tmap_2d(&args.tmap_b16, p.a_sorted, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, R_pad, K, K, 16, BLOCK_K,
+                        CU_TENSOR_MAP_SWIZZLE_128B));
+    args.M = (int)R_pad; args.N = (int)N; args.K = (int)K;
+    args.world = 1;
+    args.a_rows_per_src = (int)R_pad;
+    args.c_rows_per_dst = (int)R_pad;
+    args.num_m_tiles_dev = p.num_tiles;
+    args.tile_group = p.tile_group;
+    args.tile_rows = p.tile_rows;
+    args.row_perm = p.row_perm;
+    args.raster_group = 1;                 // the feature tiles of one token tile back to back
+    args.y = static_cast<uint8_t*>(Y->ptr);
+    args.y_ld = ldY * 2;
+    return launch_gemm_tokens(args, clusters * 2, st);
+  }
   PK_TRY(make_tmap_2d(&args.tmap_a[0], p.a_sorted, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, R_pad, K, K, 128, BLOCK_K,
                       CU_TENSOR_MAP_SWIZZLE_128B));
   PK_TRY(make_tmap_2d(&args.tmap_b, W->ptr, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, (int64_t)G * N, K, K, 128, BLOCK_K,
@@ -179,9 +214,6 @@ int grouped_gemm(const pk_tensor* A, const pk_tensor* group, const pk_tensor* W,
   args.row_perm = p.row_perm;
   args.y = static_cast<uint8_t*>(Y->ptr);
   args.y_ld = ldY * 2;
-  int clusters = std::max(1, (sched && sched->num_sms > 0 ? std::min(sched->num_sms, sms) : sms) / 2);
-  clusters = std::min<int64_t>(clusters, (int64_t)max_tiles * (N / 256));
-  args.num_compute_clusters = clusters;
   return launch_gemm_grouped(args, clusters * 2, st);
 }
 
@@ -215,6 +247,30 @@ int grouped_gemm_planned(const pk_tensor* A, const pk_tensor* plan, const pk_ten
   args.a_nsrc = 1;
   args.c_ndst = 1;
   args.raster_group = 8;
+  int clusters = std::max(1, (sched && sched->num_sms > 0 ? std::min(sched->num_sms, sms) : sms) / 2);
+  clusters = std::min<int64_t>(clusters, max_tiles * (N / 256));
+  args.num_compute_clusters = clusters;
+  if (plan->shape[0] >= 2 + 2 * max_tiles && use_token_tiles()) {
+    // the plan carries every tile's valid rows (pk_moe_dispatch_ex with a
+    // plan of >= 2 + 2 * rows/256 entries): token tiles, no padded work
+    PK_TRY(make_tmap_2d(&args.tmap_a[0], W->ptr, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, W->shape[0] * N, K, K, 128, BLOCK_K,
+                        CU_TENSOR_MAP_SWIZZLE_128B));
+    PK_TRY(make_tmap_2d(&args.tmap_b, A->ptr, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, R, K, ldA, 128, BLOCK_K,
+                        CU_TENSOR_MAP_SWIZZLE_128B));
+    PK_TRY(make_tmap_2d(&args.tmap_b16, A->ptr, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, R, K, ldA, 16, BLOCK_K,
+                        CU_TENSOR_MAP_SWIZZLE_128B));
+    args.M = (int)(max_tiles * kGrpTile); args.N = (int)N; args.K = (int)K;
+    args.world = 1;
+    args.a_rows_per_src = args.M;
+    args.c_rows_per_dst = args.M;
+    args.num_m_tiles_dev = pl;
+    args.tile_group = pl + 2;
+    args.tile_rows = pl + 2 + max_tiles;
+    args.raster_group = 1;
+    args.y = static_cast<uint8_t*>(Y->ptr);
+    args.y_ld = ldY * 2;
+    return launch_gemm_tokens(args, clusters * 2, st);
+  }
   PK_TRY(make_tmap_2d(&args.tmap_a[0], A->ptr, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, R, K, ldA, 128, BLOCK_K,
                       CU_TENSOR_MAP_SWIZZLE_128B));
   PK_TRY(make_tmap_2d(&args.tmap_b, W->ptr, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, W->shape[0] * N, K, K, 128, BLOCK_K,
@@ -227,9 +283,6 @@ int grouped_gemm_planned(const pk_tensor* A, const pk_tensor* plan, const pk_ten
   args.c_rows_per_dst = args.M;
   args.num_m_tiles_dev = pl;
   args.tile_group = pl + 2;
-  int clusters = std::max(1, (sched && sched->num_sms > 0 ? std::min(sched->num_sms, sms) : sms) / 2);
-  clusters = std::min<int64_t>(clusters, max_tiles * (N / 256));
-  args.num_compute_clusters = clusters;
   return launch_gemm_planned(args, clusters * 2, st);
 }
 

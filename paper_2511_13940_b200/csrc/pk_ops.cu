@@ -80,6 +80,10 @@ int launch_gemm_grouped(const GemmArgs& args, int grid_ctas, cudaStream_t st) {
   return launch_lcsc<2, 256, 1, EPI_SCATTER>(args, grid_ctas, st);
 }
 
+int launch_gemm_tokens(const GemmArgs& args, int grid_ctas, cudaStream_t st) {
+  return launch_lcsc<2, 256, 1, EPI_TOKENS_T>(args, grid_ctas, st);
+}
+
 __global__ void f32_to_bf16_rows_kernel(const float* __restrict__ src, uint8_t* dst, long long rows, long long cols,
                                         long long dst_ld);
 
@@ -89,6 +93,7 @@ int preload_gemm() {
 #define PK_L(CG, AM, E) PK_CUDA(cudaFuncGetAttributes(&fa, lcsc_gemm_kernel<CG, 256, AM, E>));
   PK_L(2, 2, EPI_STORE) PK_L(2, 2, EPI_REDUCE_ADD) PK_L(2, 1, EPI_DIRECT) PK_L(2, 1, EPI_STORE) PK_L(2, 1, EPI_REDUCE_ADD)
   PK_L(1, 1, EPI_STORE) PK_L(1, 1, EPI_REDUCE_ADD) PK_L(2, 1, EPI_SCATTER) PK_L(2, 1, EPI_REDUCE_ADD_F32)
+  PK_L(2, 1, EPI_TOKENS_T)
 #undef PK_L
   PK_CUDA(cudaFuncGetAttributes(&fa, lcsc_gemm_kernel<1, 128, 1, EPI_STORE>));
   PK_CUDA(cudaFuncGetAttributes(&fa, lcsc_gemm_kernel<2, 128, 1, EPI_STORE>));
