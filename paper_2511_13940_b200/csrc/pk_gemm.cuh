@@ -254,7 +254,9 @@ lcsc_gemm_kernel(const __grid_constant__ GemmArgs args) {
   const int num_clusters = args.num_compute_clusters;
   auto tile_publish = [&](int it) -> int {      // leader loader, one lane
     const int slot = it % kTileRing;
-    mbar_wait(&tile_empty[slot], ((it / kTileRing) & 1) ^ 1);
+    // the peer CTA read its copy of the slot before its release.cluster arrive
+    if (CG == 2) mbar_wait_cluster(&tile_empty[slot], ((it / kTileRing) & 1) ^ 1);
+    else mbar_wait(&tile_empty[slot], ((it / kTileRing) & 1) ^ 1);
     const uint32_t t = atomicAdd(args.tile_counter, 1u);
     if (t == (uint32_t)(num_tiles + num_clusters - 1)) *args.tile_counter = 0;   // last fetch of this launch
     tile_ring[slot] = (int)t;
@@ -271,7 +273,10 @@ lcsc_gemm_kernel(const __grid_constant__ GemmArgs args) {
   };
   auto tile_consume = [&](int it) -> int {      // any other role; one arrival per warp
     const int slot = it % kTileRing;
-    mbar_wait(&tile_full[slot], (it / kTileRing) & 1);
+    // the peer CTA's slot was written by the leader (st.shared::cluster before
+    // its release.cluster arrive): acquire at cluster scope
+    if (CG == 2 && !leader) mbar_wait_cluster(&tile_full[slot], (it / kTileRing) & 1);
+    else mbar_wait(&tile_full[slot], (it / kTileRing) & 1);
     const int t = tile_ring[slot];
     __syncwarp();
     if (lane_id() == 0) {

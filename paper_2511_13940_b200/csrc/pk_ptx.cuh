@@ -87,6 +87,20 @@ PK_DEV void mbar_wait(uint64_t* bar, uint32_t parity) {
   const uint32_t a = smem_u32(bar);
   while (!mbar_try_wait(a, parity)) {}
 }
+// Wait with cluster-scope acquire: pairs with a peer CTA's
+// mbarrier.arrive.release.cluster that publishes data it stored into this
+// CTA's shared memory (st.shared::cluster) before arriving.
+PK_DEV void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
+  const uint32_t a = smem_u32(bar);
+  uint32_t ok = 0;
+  while (!ok) {
+    asm volatile(
+        "{\n\t.reg .pred P1;\n\t"
+        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%1], %2;\n\t"
+        "selp.b32 %0, 1, 0, P1;\n\t}"
+        : "=r"(ok) : "r"(a), "r"(parity) : "memory");
+  }
+}
 
 // ---------------------------------------------------------------- TMA
 PK_DEV void prefetch_tmap(const CUtensorMap* m) {

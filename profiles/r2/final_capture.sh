@@ -1,0 +1,32 @@
+#!/bin/bash
+# Round-2 (second session) validation and captures on one B200:
+#   gpurun --timeout 3000 -- 'bash profiles/r2/final_capture.sh r2b'
+set -u
+R=${1:-r2b}
+OUT=gpurun_out/$R
+mkdir -p "$OUT"
+timeout 1200 python -m pytest tests -m gpu -x -q > "$OUT/pytest_all.log" 2>&1; echo rc=$? >> "$OUT/pytest_all.log"
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > "$OUT/smoke.log" 2>&1; echo smoke_rc=$? >> "$OUT/smoke.log"
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file "$OUT/launches_smoke.csv" \
+  python -c "import __graft_entry__ as g; g.smoke()" > "$OUT/ncu_smoke.log" 2>&1; echo ncu_rc=$? >> "$OUT/ncu_smoke.log"
+timeout 600 python bench.py > "$OUT/bench.json" 2> "$OUT/bench.err"; echo rc=$? >> "$OUT/bench.err"
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
+  --log-file "$OUT/launches_bench.csv" python bench.py --steps 2 --warmup 1 > "$OUT/bench_under_ncu.log" 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:lcsc_gemm -c 1 \
+  -o "$OUT/gemm16k" python bench.py --steps 1 --warmup 0 --no-e2e --no-baseline --cpu-seconds 0.5 > "$OUT/gemm16k_capture.log" 2>&1
+ncu -i "$OUT/gemm16k.ncu-rep" --page raw --csv > "$OUT/gemm16k_raw.csv" 2>/dev/null
+ncu -i "$OUT/gemm16k.ncu-rep" --page details --csv > "$OUT/gemm16k_details.csv" 2>/dev/null
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:attn_fwd -s 1 -c 1 \
+  -o "$OUT/attn_rank" python profiles/attn_once.py > "$OUT/attn_capture.log" 2>&1
+ncu -i "$OUT/attn_rank.ncu-rep" --page raw --csv > "$OUT/attn_rank_raw.csv" 2>/dev/null
+ncu -i "$OUT/attn_rank.ncu-rep" --page details --csv > "$OUT/attn_rank_details.csv" 2>/dev/null
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:"lcsc_gemm_kernel<2, 256, 1, 5>" -s 1 -c 1 \
+  -o "$OUT/grouped_tokens" python profiles/moe_once.py > "$OUT/grouped_capture.log" 2>&1
+ncu -i "$OUT/grouped_tokens.ncu-rep" --page raw --csv > "$OUT/grouped_tokens_raw.csv" 2>/dev/null
+ncu -i "$OUT/grouped_tokens.ncu-rep" --page details --csv > "$OUT/grouped_tokens_details.csv" 2>/dev/null
+timeout 300 ncu --clock-control none -k regex:"moe|grp|lcsc" \
+  --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --csv \
+  python profiles/moe_once.py > "$OUT/moe_launches.csv" 2>&1
+timeout 900 python bench_ops.py --out "$OUT/ops.jsonl" > "$OUT/ops.log" 2>&1
+rm -f "$OUT"/*.ncu-rep
+tail -1 "$OUT/bench.json"

@@ -103,3 +103,71 @@ def test_moe_dispatch_gemm_combine_pipeline(world):
         assert np.abs(outs[d].float().cpu().numpy() - ref).max() <= 1e-2 * max(1.0, np.abs(ref).max())
     for c in comms:
         c.destroy()
+
+
+# group sizes around every token-tile boundary (EPI_TOKENS_T: MMA N = valid rows
+# rounded up to 32, partial tiles loaded in 16-row boxes, full tiles at 256)
+_EDGE_COUNTS = [1, 15, 16, 17, 31, 32, 33, 47, 63, 64, 65, 127, 128, 129, 200, 255, 256, 257, 300, 511, 512, 513]
+
+
+@pytest.mark.parametrize("padded", [False, True])
+def test_grouped_gemm_token_tile_boundaries(monkeypatch, padded):
+    """Every group size around the token-tile edges, exact; the 256-row padded
+    tiles (PK_GROUPED_PADDED) must agree bit for bit."""
+    if padded:
+        monkeypatch.setenv("PK_GROUPED_PADDED", "1")
+    pk = _pk()
+    rng = np.random.default_rng(11)
+    G, N, K = len(_EDGE_COUNTS), 512, 128
+    g = np.concatenate([np.full(c, i, dtype=np.int32) for i, c in enumerate(_EDGE_COUNTS)])
+    rng.shuffle(g)
+    R = g.shape[0]
+    a = rng.integers(-2, 3, size=(R, K)).astype(np.float32)
+    w = rng.integers(-2, 3, size=(G, N, K)).astype(np.float32)
+    y = torch.full((R, N), 5.0, device="cuda", dtype=torch.bfloat16)
+    pk.grouped_gemm(torch.from_numpy(a).cuda().bfloat16(), torch.from_numpy(g).cuda(),
+                    torch.from_numpy(w).cuda().bfloat16(), out=y)
+    torch.cuda.synchronize()
+    assert np.array_equal(y.float().cpu().numpy(), bf16_round(oracle.grouped_gemm(a, g, w)))
+
+
+def test_planned_token_tiles_match_padded_tiles(monkeypatch):
+    """Expert-major dispatch -> planned grouped GEMM: the token-tile path (plan
+    with per-tile rows) writes exactly the padded path's valid rows and leaves
+    the segment padding untouched."""
+    pk = _pk()
+    T, E, K, H, HE = 700, 16, 4, 256, 512
+    rng = oracle.plan_rng(3)
+    route, _ = oracle.moe_route(rng, 1, T, E, K)
+    comm = pk.local_group(1)[0]
+    try:
+        x = torch.from_numpy(rng.integers(-2, 3, size=(T, H)).astype(np.float32)).cuda().bfloat16()
+        topk = torch.from_numpy(route[0].astype(np.int32)).cuda()
+        w = torch.from_numpy(rng.integers(-1, 2, size=(E, HE, H)).astype(np.float32)).cuda().bfloat16()
+        recv, src, cnt, plan = pk.moe_dispatch(comm, x, topk, E, layout="expert")
+        torch.cuda.synchronize()
+        tiles = int(plan[0].item())
+        cap_tiles = recv.shape[0] // 256
+        rows = plan[2 + cap_tiles:2 + cap_tiles + tiles].cpu().numpy()
+        experts = plan[2:2 + tiles].cpu().numpy()
+        valid = src[:, 0].cpu().numpy() >= 0
+        # the per-tile rows are the valid rows of each 256-row segment tile
+        assert np.array_equal(rows, valid[:tiles * 256].reshape(tiles, 256).sum(1))
+        assert int(rows.sum()) == int(cnt.item()) == T * K
+        y_tok = comm.empty((recv.shape[0], HE))
+        y_tok.fill_(3.0)
+        pk.grouped_gemm(recv, None, w, out=y_tok, plan=plan)
+        monkeypatch.setenv("PK_GROUPED_PADDED", "1")
+        y_pad = comm.empty((recv.shape[0], HE))
+        pk.grouped_gemm(recv, None, w, out=y_pad, plan=plan)
+        torch.cuda.synchronize()
+        assert torch.equal(y_tok[torch.from_numpy(valid).cuda()], y_pad[torch.from_numpy(valid).cuda()])
+        assert torch.all(y_tok[torch.from_numpy(~valid).cuda()] == 3.0)
+        # and they are the expert GEMM of each row (exact on integer data)
+        rec = recv.float().cpu().numpy()[:tiles * 256]
+        grp = np.repeat(experts, 256)
+        v = valid[:tiles * 256]
+        exp = oracle.grouped_gemm(rec[v], grp[v].astype(np.int32), w.float().cpu().numpy())
+        assert np.array_equal(y_tok[:tiles * 256][torch.from_numpy(v).cuda()].float().cpu().numpy(), bf16_round(exp))
+    finally:
+        comm.destroy()
