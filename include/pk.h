@@ -255,9 +255,9 @@ typedef enum { PK_MECH_AUTO = 0, PK_MECH_REG = 1, PK_MECH_TMA = 2,
 /* Dispatch with an explicit layout and mechanism. For PK_MOE_EXPERT_MAJOR,
  * expert_plan (int32, >= 2 + cap/256 entries) receives [num_tiles, rows,
  * local expert of tile 0, 1, ...] for pk_grouped_gemm_planned; a plan of
- * >= 2 + 2*cap/256 entries also receives the valid rows of every tile at
- * [2 + cap/256 + tile]. recv_src of padding rows is -1. recv_count counts
- * real (unpadded) rows. */
+ * >= 2 + 3*cap/256 entries also receives, per tile, the rows it computes at
+ * [2 + cap/256 + tile] and its first row at [2 + 2*cap/256 + tile]. recv_src of
+ * padding rows is -1. recv_count counts real (unpadded) rows. */
 PK_API int pk_moe_dispatch_ex(pk_comm* comm, const pk_tensor* x, const pk_tensor* topk_idx,
                               int num_experts, int layout, int mechanism, pk_tensor* recv,
                               pk_tensor* recv_src, pk_tensor* recv_count, pk_tensor* expert_plan,
@@ -304,8 +304,8 @@ PK_API int pk_grouped_gemm(const pk_tensor* a, const pk_tensor* group_ids, const
 /* Grouped GEMM over 256-row group segments already in place (the
  * PK_MOE_EXPERT_MAJOR receive buffer): y[r] = a[r] . w[plan[2 + r/256]]^T for
  * r < 256 * plan[0]; a [R, K], y [R, N] bf16, plan int32 on the device. With
- * the per-tile valid rows in the plan (>= 2 + 2*R/256 entries) only the valid
- * rows are computed and written; otherwise every row of the segments. */
+ * the per-tile rows in the plan (>= 2 + 3*R/256 entries) only the valid rows
+ * are computed and written; otherwise every row of the segments. */
 PK_API int pk_grouped_gemm_planned(const pk_tensor* a, const pk_tensor* plan, const pk_tensor* w, pk_tensor* y,
                                    const pk_sched* sched, void* stream);
 

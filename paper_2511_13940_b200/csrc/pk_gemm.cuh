@@ -40,11 +40,12 @@ enum EpiMode : int { EPI_STORE = 0, EPI_REDUCE_ADD = 1, EPI_SCATTER = 2, EPI_DIR
                      EPI_TOKENS_T = 5 };
 // EPI_TOKENS_T (grouped expert GEMM without row padding): each tile computes
 // Y^T = W_g . X^T for one plan tile of <= 256 token rows of group g (the
-// tile's valid rows, rounded up to 16, become the MMA's N) and 256 output
+// tile's valid rows, rounded up to 32, become the MMA's N) and 256 output
 // features of W_g (the MMA's M, the weight rows as the A operand). The
 // epilogue writes the tile transposed back into Y[token rows, features]
-// (through row_perm when set). The 256-row padding of every group's last tile
-// then costs at most 15 rows of tensor work instead of up to 255.
+// (through row_perm when set). tile_start / tile_rows give each tile's first
+// row and row count (full 256-row tiles and one remainder per group; an even
+// split of the group over its tiles measured 3-5 % slower).
 constexpr int kTileRing = 4;                // depth of the tile-index broadcast ring
 constexpr int kAgCountOffset = 32768;       // AG piece counters live after the first 32K m-tile flags
 
@@ -81,6 +82,7 @@ struct GemmArgs {
   const int32_t* tile_group;              // [M tiles] group of each M tile (B rows group*N ..)
   const int32_t* row_perm;                // [M] destination row of each sorted row (-1 = padding)
   const int32_t* tile_rows;               // EPI_TOKENS_T: [M tiles] valid token rows of each plan tile
+  const int32_t* tile_start;              // EPI_TOKENS_T: [M tiles] first token row of each tile (null: mt * 256)
   uint8_t* y;                             // EPI_SCATTER destination [rows, N] bf16
   long long y_ld;                         // bytes between rows of y
   uint32_t* tile_counter;                 // dynamic tile scheduler (0 at launch; reset by the last fetch)
@@ -528,7 +530,7 @@ lcsc_gemm_kernel(const __grid_constant__ GemmArgs args) {
         // A operand: this CTA's 128 weight rows (features); B operand: its half
         // of the tile's tokens (the pair splits the MMA's N)
         a_row = args.tile_group[mt] * args.N + nt * BN + (int)cta_rank * Cfg::BM;
-        b_row = mt * Cfg::TILE_M + (int)cta_rank * (tokens_n(args, mt) / CG);
+        b_row = (args.tile_start ? args.tile_start[mt] : mt * Cfg::TILE_M) + (int)cta_rank * (tokens_n(args, mt) / CG);
       }
       if (args.a_wait_flag[src]) {
         wait_geq(args.sync.flags + mt, s_call[0], args.sync.err, args.sync.timeout_ns);
@@ -654,6 +656,7 @@ lcsc_gemm_kernel(const __grid_constant__ GemmArgs args) {
         // two adjacent features of one token (16 lanes cover 64 contiguous
         // bytes of a token row)
         const int valid = args.tile_rows[mt];
+        const int row0 = args.tile_start ? args.tile_start[mt] : mt * Cfg::TILE_M;
         const int f0 = nt * BN + (int)cta_rank * Cfg::BM + q * 32;       // feature of lane 0
         const int nch = (valid + 31) / 32;
         const bool odd = lane & 1;
@@ -674,7 +677,7 @@ lcsc_gemm_kernel(const __grid_constant__ GemmArgs args) {
             const uint32_t w = odd ? pack_bf16x2(__uint_as_float(got), __uint_as_float(v[i + 1]))
                                    : pack_bf16x2(__uint_as_float(v[i]), __uint_as_float(got));
             if (tok < valid) {
-              int row = mt * Cfg::TILE_M + tok;
+              int row = row0 + tok;
               if (args.row_perm) row = args.row_perm[row];
               if (row >= 0)
                 *reinterpret_cast<uint32_t*>(args.y + (long long)row * args.y_ld + (long long)(f0 + (lane & ~1u)) * 2) = w;

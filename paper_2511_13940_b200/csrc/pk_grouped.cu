@@ -41,6 +41,7 @@ struct GroupPlan {
   int32_t* cursor;             // [G]
   int32_t* tile_group;         // [max tiles]
   int32_t* tile_rows;          // [max tiles] valid rows of each tile
+  int32_t* tile_start;         // [max tiles] first sorted row of each tile
   int32_t* num_tiles;          // [1]
   int32_t* row_perm;           // [R_pad]
   const uint8_t* a;            // [R, K] rows (bf16)
@@ -69,10 +70,13 @@ __global__ void grp_scan_kernel(const __grid_constant__ GroupPlan p, int max_til
   for (int g = 0; g < p.G; ++g) {
     p.offsets[g] = off;
     p.cursor[g] = 0;
-    const int tiles = (p.counts[g] + kGrpTile - 1) / kGrpTile;
+    const int c = p.counts[g];
+    const int tiles = (c + kGrpTile - 1) / kGrpTile;
+    const int per = kGrpTile;            // full tiles + one remainder (an even split measured slower)
     for (int t = 0; t < tiles && off / kGrpTile + t < max_tiles; ++t) {
       p.tile_group[off / kGrpTile + t] = g;
-      p.tile_rows[off / kGrpTile + t] = min(kGrpTile, p.counts[g] - t * kGrpTile);
+      p.tile_rows[off / kGrpTile + t] = min(per, c - t * per);
+      p.tile_start[off / kGrpTile + t] = off + t * per;
     }
     off += tiles * kGrpTile;
   }
@@ -129,7 +133,7 @@ int grouped_gemm(const pk_tensor* A, const pk_tensor* group, const pk_tensor* W,
   static thread_local size_t plan_sz[64] = {};
   static thread_local void* abuf[64] = {};
   static thread_local size_t abuf_sz[64] = {};
-  const size_t plan_bytes = sizeof(int32_t) * (4 * (size_t)G + 2 * (size_t)max_tiles + 2 + R_pad);
+  const size_t plan_bytes = sizeof(int32_t) * (4 * (size_t)G + 3 * (size_t)max_tiles + 2 + R_pad);
   const size_t a_bytes = (size_t)R_pad * K * 2;
   if (plan_sz[dev] < plan_bytes) {
     if (plan_buf[dev]) { PK_CUDA(cudaStreamSynchronize(st)); cudaFree(plan_buf[dev]); }
@@ -155,7 +159,8 @@ int grouped_gemm(const pk_tensor* A, const pk_tensor* group, const pk_tensor* W,
   p.num_tiles = base + 3 * G + 1;
   p.tile_group = base + 3 * G + 2;
   p.tile_rows = p.tile_group + max_tiles;
-  p.row_perm = p.tile_rows + max_tiles;
+  p.tile_start = p.tile_rows + max_tiles;
+  p.row_perm = p.tile_start + max_tiles;
   p.a = static_cast<const uint8_t*>(A->ptr);
   p.a_ld = ldA * 2;
   p.a_sorted = static_cast<uint8_t*>(abuf[dev]);
@@ -195,6 +200,7 @@ int grouped_gemm(const pk_tensor* A, const pk_tensor* group, const pk_tensor* W,
     args.num_m_tiles_dev = p.num_tiles;
     args.tile_group = p.tile_group;
     args.tile_rows = p.tile_rows;
+    args.tile_start = p.tile_start;
     args.row_perm = p.row_perm;
     args.raster_group = 1;                 // the feature tiles of one token tile back to back
     args.y = static_cast<uint8_t*>(Y->ptr);
@@ -250,9 +256,9 @@ int grouped_gemm_planned(const pk_tensor* A, const pk_tensor* plan, const pk_ten
   int clusters = std::max(1, (sched && sched->num_sms > 0 ? std::min(sched->num_sms, sms) : sms) / 2);
   clusters = std::min<int64_t>(clusters, max_tiles * (N / 256));
   args.num_compute_clusters = clusters;
-  if (plan->shape[0] >= 2 + 2 * max_tiles && use_token_tiles()) {
-    // the plan carries every tile's valid rows (pk_moe_dispatch_ex with a
-    // plan of >= 2 + 2 * rows/256 entries): token tiles, no padded work
+  if (plan->shape[0] >= 2 + 3 * max_tiles && use_token_tiles()) {
+    // the plan carries every tile's rows and first row (pk_moe_dispatch_ex
+    // with a plan of >= 2 + 3 * rows/256 entries): token tiles, no padded work
     PK_TRY(make_tmap_2d(&args.tmap_a[0], W->ptr, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, W->shape[0] * N, K, K, 128, BLOCK_K,
                         CU_TENSOR_MAP_SWIZZLE_128B));
     PK_TRY(make_tmap_2d(&args.tmap_b, A->ptr, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, R, K, ldA, 128, BLOCK_K,
@@ -266,6 +272,7 @@ int grouped_gemm_planned(const pk_tensor* A, const pk_tensor* plan, const pk_ten
     args.num_m_tiles_dev = pl;
     args.tile_group = pl + 2;
     args.tile_rows = pl + 2 + max_tiles;
+    args.tile_start = pl + 2 + 2 * max_tiles;
     args.raster_group = 1;
     args.y = static_cast<uint8_t*>(Y->ptr);
     args.y_ld = ldY * 2;

@@ -230,8 +230,8 @@ def moe_dispatch(comm, x: torch.Tensor, topk_idx: torch.Tensor, num_experts: int
                 comm.default_buffer("moe.recv_src", (capacity, 2), torch.int32))
     recv_rows, recv_src = recv
     count = torch.empty(1, dtype=torch.int32, device=x.device)
-    # plan: [num_tiles, rows, tile -> local expert (rows/256), tile -> valid rows (rows/256)]
-    plan = torch.empty(2 + 2 * (recv_rows.shape[0] // 256), dtype=torch.int32, device=x.device) if lay else None
+    # plan: [num_tiles, rows, tile -> local expert, tile -> rows, tile -> first row] (rows/256 entries each)
+    plan = torch.empty(2 + 3 * (recv_rows.shape[0] // 256), dtype=torch.int32, device=x.device) if lay else None
     lib = _lib.load()
     dx, dt = _lib.tensor_desc(x), _lib.tensor_desc(topk_idx)
     dr, ds, dc = _lib.tensor_desc(recv_rows), _lib.tensor_desc(recv_src), _lib.tensor_desc(count)

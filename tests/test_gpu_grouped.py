@@ -149,10 +149,16 @@ def test_planned_token_tiles_match_padded_tiles(monkeypatch):
         tiles = int(plan[0].item())
         cap_tiles = recv.shape[0] // 256
         rows = plan[2 + cap_tiles:2 + cap_tiles + tiles].cpu().numpy()
+        starts = plan[2 + 2 * cap_tiles:2 + 2 * cap_tiles + tiles].cpu().numpy()
         experts = plan[2:2 + tiles].cpu().numpy()
         valid = src[:, 0].cpu().numpy() >= 0
-        # the per-tile rows are the valid rows of each 256-row segment tile
-        assert np.array_equal(rows, valid[:tiles * 256].reshape(tiles, 256).sum(1))
+        # the token tiles cover exactly the valid rows, each inside its expert's segment
+        covered = np.zeros_like(valid)
+        for t_, (st, nr, e) in enumerate(zip(starts, rows, experts)):
+            assert 0 < nr <= 256 and not covered[st:st + nr].any()
+            covered[st:st + nr] = True
+            assert np.all(src[st:st + nr, 1].cpu().numpy() == e)
+        assert np.array_equal(covered, valid)
         assert int(rows.sum()) == int(cnt.item()) == T * K
         y_tok = comm.empty((recv.shape[0], HE))
         y_tok.fill_(3.0)
