@@ -214,11 +214,13 @@ PK_API int pk_all_reduce_ablate(pk_comm* comm, pk_tensor* x, uint32_t overheads,
 
 /* Ring attention forward (non-causal): q,k,v,o [B, S/n, H, D] bf16 local
  * shards; lse [B, H, S/n] f32. At step s rank r attends to the KV shard of
- * rank (r - s) mod n (workloads.py:666-681): one launch whose communicator
- * CTAs (sched->num_comm_sms, NULL = sized to the link) pull each step's shard
- * into a 2-slot local stage over peer memory while the compute CTAs work on
- * the previous step (step-major units, log-sum-exp merge in ascending step
- * order). k / v may be reused once the call completes on `stream`. */
+ * rank (r - s) mod n (workloads.py:666-681): one launch whose communicators
+ * pull each step's shard into a 2-slot local stage over peer memory while the
+ * compute CTAs work on the previous step (step-major units, log-sum-exp merge
+ * in ascending step order). Communicators: NULL / mode intra_sm = a comm warp
+ * in every compute CTA; mode inter_sm or num_comm_sms > 0 = dedicated CTAs
+ * (num_comm_sms, 0 = sized to the link). k / v may be reused once the call
+ * completes on `stream`. */
 PK_API int pk_ring_attn_fwd(pk_comm* comm, const pk_tensor* q, const pk_tensor* k,
                             const pk_tensor* v, pk_tensor* o, pk_tensor* lse, float softmax_scale,
                             const pk_sched* sched, void* stream);

@@ -73,6 +73,11 @@ constexpr int AT_V_BYTES = AT_BN * AT_D * 2;     // 32 KB
 constexpr int AT_KSTAGES = AT_KS;
 constexpr int AT_VSTAGES = 2;
 constexpr int AT_SMEM = 2 * AT_Q_BYTES + AT_KSTAGES * AT_K_BYTES + AT_VSTAGES * AT_V_BYTES + 512 + AT_RED_BYTES + 1024;
+// intra-SM ring communicator (warp 3 of each compute CTA): two pieces of smem
+// beside the Q / K / V stages (0: they do not fit this build's stages)
+constexpr int AT_RING_CBUF_OFF = 2 * AT_Q_BYTES + AT_KSTAGES * AT_K_BYTES + AT_VSTAGES * AT_V_BYTES + 512 + AT_RED_BYTES;
+constexpr int AT_RING_PIECE = (AT_SMEM + 2 * 16384 <= 232448 - 64) ? 16384 : 0;
+constexpr int AT_SMEM_RING = AT_SMEM + 2 * AT_RING_PIECE;
 constexpr int AT_TMEM_COLS = 512;                // per tile: S (128, P aliased in its first 64) + O (128)
 constexpr float AT_RESCALE_THRESHOLD = 8.0f;     // log2 units: P stays <= 2^8 between rescales
 #ifndef AT_POLY_DEG
@@ -396,94 +401,99 @@ __global__ void __launch_bounds__(AT_THREADS, 1) attn_fwd_kernel(const __grid_co
 
   // registers follow the roles: warpgroup 0 (loader, MMA, allocator, idle)
   // needs few, the two softmax warpgroups hold a whole 128-key S row each
-  if (is_comm) {
-    // ------------------------------------------------------------ ring communicator
-    // Pull step s's shard (rank (r - s) mod n, workloads.py:666-681) into slot
-    // s & 1 once every unit of step s - 2 has read that slot: the K and V
-    // shards are cut into 32 KB pieces striped over the communicator CTAs;
-    // one thread per CTA moves its pieces peer VA -> smem -> slot
-    // (cp.async.bulk, store_async) and the last CTA done with a step
-    // publishes it (signal; the compute loaders wait).
-    if (warp == 0 && lane == 0) {
-      constexpr int PIECE = 32768;
-      constexpr int NBUF = 6;                         // 192 KB: the Q / K / V buffers, unused here
-      uint64_t* cbar = bars;
-      for (int i = 0; i < NBUF; ++i) mbar_init(&cbar[i], 1);
-      fence_mbar_init();
-      const int me_c = (int)blockIdx.x - ncompute, nc = a.ring_comm, n = a.ring_steps;
-      const long long ppt = (a.shard_bytes + PIECE - 1) / PIECE;           // pieces per tensor
-      const long long per_step = 2 * ppt;                                  // K pieces, then V pieces
-      const long long mine = per_step > me_c ? (per_step - 1 - me_c) / nc + 1 : 0;
-      const uint32_t ready_expect = call_get(a.call, 1);
-      uint32_t phase = 0;
-      long long gp = 0;                                                    // pieces moved so far
-      bool ok = true;
-      for (int s = 1; s < n; ++s) {
-        const int src = (a.rank - s + n) % n;
+  // ------------------------------------------------------------ ring communicator
+  // Pull step s's shard (rank (r - s) mod n, workloads.py:666-681) into slot
+  // s & 1 once every unit of step s - 2 has read that slot: the K and V shards
+  // are cut into pieces striped over the nc communicators; one thread per
+  // communicator moves its pieces peer VA -> smem -> slot (cp.async.bulk,
+  // store_async) through nbuf smem buffers, and the last communicator done
+  // with a step publishes it (signal; the compute loaders wait).
+  // Communicators are either dedicated CTAs (inter-SM: 32 KB pieces, 6
+  // buffers in the CTA's whole smem) or warp 3 of every compute CTA (intra-SM:
+  // 16 KB pieces, 2 buffers beside the Q / K / V stages).
+  auto ring_pull = [&](int me_c, int nc, uint8_t* buf, int nbuf, int piece_bytes, uint64_t* cbar) {
+    const long long PIECE = piece_bytes;
+    for (int i = 0; i < nbuf; ++i) mbar_init(&cbar[i], 1);
+    fence_mbar_init();
+    const int n = a.ring_steps;
+    const long long ppt = (a.shard_bytes + PIECE - 1) / PIECE;           // pieces per tensor
+    const long long per_step = 2 * ppt;                                  // K pieces, then V pieces
+    const long long mine = per_step > me_c ? (per_step - 1 - me_c) / nc + 1 : 0;
+    const uint32_t ready_expect = call_get(a.call, 1);
+    uint32_t phase = 0;
+    long long gp = 0;                                                    // pieces moved so far
+    bool ok = true;
+    for (int s = 1; s < n; ++s) {
+      const int src = (a.rank - s + n) % n;
 #ifdef AT_RING_PROF
-        const long long tw = clock64();
+      const long long tw = clock64();
 #endif
-        if (ok && s >= 3) ok = wait_geq(rc.units(s - 2), (uint32_t)items, a.err, a.timeout_ns);
-        if (ok) ok = wait_geq(a.ready_local + src, ready_expect, a.err, a.timeout_ns);
+      if (ok && s >= 3) ok = wait_geq(rc.units(s - 2), (uint32_t)items, a.err, a.timeout_ns);
+      if (ok) ok = wait_geq(a.ready_local + src, ready_expect, a.err, a.timeout_ns);
 #ifdef AT_RING_PROF
-        const long long tc0 = clock64();
-        RP_ADD(5, tc0 - tw);
+      const long long tc0 = clock64();
+      RP_ADD(5, tc0 - tw);
 #endif
-        fence_async_global();
-        uint8_t* dk = a.stage_k + (long long)(s & 1) * a.shard_bytes;
-        uint8_t* dv = a.stage_v + (long long)(s & 1) * a.shard_bytes;
-        auto piece = [&](long long k, const uint8_t** sp, uint8_t** dp, uint32_t* bytes) {
-          const long long q = me_c + k * nc;
-          const bool isv = q >= ppt;
-          const long long off = (isv ? q - ppt : q) * PIECE;
-          *sp = (isv ? a.ring_src_v[src] : a.ring_src_k[src]) + off;
-          *dp = (isv ? dv : dk) + off;
-          *bytes = (uint32_t)min((long long)PIECE, a.shard_bytes - off);
-        };
-        auto issue = [&](long long k) {
+      fence_async_global();
+      uint8_t* dk = a.stage_k + (long long)(s & 1) * a.shard_bytes;
+      uint8_t* dv = a.stage_v + (long long)(s & 1) * a.shard_bytes;
+      auto piece = [&](long long k, const uint8_t** sp, uint8_t** dp, uint32_t* bytes) {
+        const long long q = me_c + k * nc;
+        const bool isv = q >= ppt;
+        const long long off = (isv ? q - ppt : q) * PIECE;
+        *sp = (isv ? a.ring_src_v[src] : a.ring_src_k[src]) + off;
+        *dp = (isv ? dv : dk) + off;
+        *bytes = (uint32_t)min(PIECE, a.shard_bytes - off);
+      };
+      auto issue = [&](long long k) {
+        const uint8_t* sp;
+        uint8_t* dp;
+        uint32_t bytes;
+        piece(k, &sp, &dp, &bytes);
+        const int b = (int)((gp + k) % nbuf);
+        mbar_arrive_expect_tx(&cbar[b], bytes);
+        bulk_g2s(buf + (size_t)b * PIECE, sp, bytes, &cbar[b]);
+      };
+      if (ok) {
+        for (long long k = 0; k < mine && k < nbuf - 1; ++k) issue(k);
+        for (long long k = 0; k < mine; ++k) {
+          const int b = (int)((gp + k) % nbuf);
+          mbar_wait(&cbar[b], (phase >> b) & 1);
+          phase ^= 1u << b;
           const uint8_t* sp;
           uint8_t* dp;
           uint32_t bytes;
           piece(k, &sp, &dp, &bytes);
-          const int b = (int)((gp + k) % NBUF);
-          mbar_arrive_expect_tx(&cbar[b], bytes);
-          bulk_g2s(smem + (size_t)b * PIECE, sp, bytes, &cbar[b]);
-        };
-        if (ok) {
-          for (long long k = 0; k < mine && k < NBUF - 1; ++k) issue(k);
-          for (long long k = 0; k < mine; ++k) {
-            const int b = (int)((gp + k) % NBUF);
-            mbar_wait(&cbar[b], (phase >> b) & 1);
-            phase ^= 1u << b;
-            const uint8_t* sp;
-            uint8_t* dp;
-            uint32_t bytes;
-            piece(k, &sp, &dp, &bytes);
-            bulk_s2g(dp, smem + (size_t)b * PIECE, bytes);
-            bulk_commit();
-            if (k + NBUF - 1 < mine) {
-              bulk_wait_read<1>();                     // the buffer of piece k + NBUF - 1 (last used by k - 1) was read
-              issue(k + NBUF - 1);
-            }
+          bulk_s2g(dp, buf + (size_t)b * PIECE, bytes);
+          bulk_commit();
+          if (k + nbuf - 1 < mine) {
+            bulk_wait_read<1>();                     // the buffer of piece k + nbuf - 1 (last used by k - 1) was read
+            issue(k + nbuf - 1);
           }
-          bulk_wait<0>();                              // my share of step s is in the slot
-          gp += mine;
         }
+        bulk_wait<0>();                              // my share of step s is in the slot
+        gp += mine;
+      }
 #ifdef AT_RING_PROF
-        RP_ADD(6, clock64() - tc0);
+      RP_ADD(6, clock64() - tc0);
 #endif
-        fence_async_global();
-        __threadfence();
-        if (atomicAdd(rc.pieces(s), 1u) == (uint32_t)nc - 1)
-          asm volatile("st.release.gpu.global.u32 [%0], %1;" :: "l"(rc.ready(s)), "r"(1u) : "memory");
-      }
-      // every peer shard has been read: the last communicator CTA tells the owners
+      fence_async_global();
       __threadfence();
-      if (atomicAdd(rc.comm_done(), 1u) == (uint32_t)nc - 1) {
-        fence_sys();
-        for (int d = 0; d < a.world; ++d) signal_add(a.done_peer[d] + a.rank, 1u);
-      }
+      if (atomicAdd(rc.pieces(s), 1u) == (uint32_t)nc - 1)
+        asm volatile("st.release.gpu.global.u32 [%0], %1;" :: "l"(rc.ready(s)), "r"(1u) : "memory");
     }
+    // every peer shard has been read: the last communicator tells the owners
+    __threadfence();
+    if (atomicAdd(rc.comm_done(), 1u) == (uint32_t)nc - 1) {
+      fence_sys();
+      for (int d = 0; d < a.world; ++d) signal_add(a.done_peer[d] + a.rank, 1u);
+    }
+  };
+  __shared__ __align__(8) uint64_t ring_cbar[6];
+
+  if (is_comm) {
+    if (warp == 0 && lane == 0)                       // 192 KB: the Q / K / V buffers, unused here
+      ring_pull((int)blockIdx.x - ncompute, a.ring_comm, smem, 6, 32768, ring_cbar);
     __syncwarp();
   } else if (warp < 4) {
   // (the increase of the softmax warps can only complete from what this
@@ -662,6 +672,13 @@ __global__ void __launch_bounds__(AT_THREADS, 1) attn_fwd_kernel(const __grid_co
       segx1 += sg.ntile > 1;
       g += len;
     }
+  } else if (warp == 3) {
+    // ------------------------------------------------------------ intra-SM ring communicator
+    if constexpr (RING && AT_RING_PIECE > 0) {
+      if (a.ring_comm == 0 && lane == 0)
+        ring_pull((int)blockIdx.x, ncompute, smem + AT_RING_CBUF_OFF, 2, AT_RING_PIECE, ring_cbar);
+    }
+    __syncwarp();
   }
   } else {
   asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" :: "n"(AT_REG_SOFTMAX) : "memory");
@@ -1495,22 +1512,28 @@ int ring_attn_fwd(Comm* c, const pk_tensor* q, const pk_tensor* k, const pk_tens
   PK_TRY(tmap_bshd(&a.tm_vs, a.stage_v, 2 * B, S, H, AT_BN));
   a.S_kv = (int)(n * S);
   a.blocks_per_step = (int)(S / AT_BN);
-  // Communicator CTAs (inter-SM schedule): enough TMA-driven SMs to pull a
-  // step's K + V within half the step's compute (+30 %), at the paper's B200 TMA
-  // rate (669 GB/s saturating at 15 SMs) and ~1.2 PF/s of
-  // attention over this rank's SMs; the schedule may set it. Emulated ranks
-  // keep a quarter of their SMs at most.
-  int ncomm;
-  if (sched && sched->num_comm_sms > 0) {
-    ncomm = sched->num_comm_sms;
-  } else {
-    // A slot is refilled for step s + 1 only once every unit of step s - 1 has
-    // read it, so the copy has about half a step, not a whole one.
-    const double t_step = 4.0 * B * H * (double)S * S * AT_D / (1.2e15 * c->num_sms / 148.0);   // this rank's SMs
-    ncomm = (int)std::ceil(1.3 * 2.0 * (double)shard / (0.5 * t_step * (669e9 / 15)));
-    ncomm = std::max(2, std::min(16, ncomm));
+  // Communicators. Intra-SM (the default): warp 3 of every compute CTA pulls
+  // its stripe of each step's shard through two 16 KB smem pieces beside the
+  // Q / K / V stages, so no SM is set aside — a step's shard is ~1/300 of the
+  // SM's TMA traffic per step. Inter-SM (mode inter_sm, or num_comm_sms > 0):
+  // dedicated communicator CTAs, enough TMA-driven SMs to pull a step's K + V
+  // within half the step's compute (+30 %), at the paper's B200 TMA rate
+  // (669 GB/s saturating at 15 SMs) and ~1.2 PF/s of attention
+  // over this rank's SMs. Emulated ranks keep a quarter of their SMs at most.
+  int ncomm = 0;
+  const bool inter = (sched && (sched->num_comm_sms > 0 || sched->mode == 1 || sched->mode == 2)) || AT_RING_PIECE == 0;
+  if (inter) {
+    if (sched && sched->num_comm_sms > 0) {
+      ncomm = sched->num_comm_sms;
+    } else {
+      // A slot is refilled for step s + 1 only once every unit of step s - 1 has
+      // read it, so the copy has about half a step, not a whole one.
+      const double t_step = 4.0 * B * H * (double)S * S * AT_D / (1.2e15 * c->num_sms / 148.0);   // this rank's SMs
+      ncomm = (int)std::ceil(1.3 * 2.0 * (double)shard / (0.5 * t_step * (669e9 / 15)));
+      ncomm = std::max(2, std::min(16, ncomm));
+    }
+    if (c->local_group) ncomm = std::min(ncomm, std::max(1, c->num_sms / 4));
   }
-  if (c->local_group) ncomm = std::min(ncomm, std::max(1, c->num_sms / 4));
   const int ncompute = std::min(n * items, c->num_sms - ncomm);
   if (ncompute < 1) return fail(PK_ERR_INVALID, "ring_attention: num_comm_sms leaves no compute SMs");
   a.ring_comm = ncomm;
@@ -1519,8 +1542,8 @@ int ring_attn_fwd(Comm* c, const pk_tensor* q, const pk_tensor* k, const pk_tens
   CallRef call;
   PK_TRY(begin_call(c, 1, 1, 1, st, &call));
   a.call = call;
-  PK_TRY(ensure_smem_attr((const void*)attn_fwd_kernel<true>, AT_SMEM));
-  attn_fwd_kernel<true><<<ncompute + ncomm, AT_THREADS, AT_SMEM, st>>>(a);
+  PK_TRY(ensure_smem_attr((const void*)attn_fwd_kernel<true>, AT_SMEM_RING));
+  attn_fwd_kernel<true><<<ncompute + ncomm, AT_THREADS, AT_SMEM_RING, st>>>(a);
   PK_CUDA(cudaGetLastError());
   return PK_OK;
 }

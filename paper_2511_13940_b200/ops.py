@@ -266,9 +266,10 @@ def ring_attention(comm, q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, soft
     """Sequence-parallel ring attention forward, non-causal (RingAttentionPlan,
     workloads.py:616-716). q, k, v: this rank's [B, S/n, H, D] bf16 shards
     (D = 128, S/n % 128 == 0). At ring step s rank r attends to the KV shard of
-    rank (r - s) mod n, which communicator CTAs of the same kernel pull into a
-    2-slot local stage while step s - 1 computes (schedule={"num_comm_sms": k}
-    sets their number). Returns (o [B, S/n, H, D] bf16, lse [B, H, S/n] fp32,
+    rank (r - s) mod n, which the kernel's communicators pull into a 2-slot
+    local stage while step s - 1 computes: by default (or mode "intra_sm") a
+    comm warp in every compute CTA, with mode "inter_sm" or
+    schedule={"num_comm_sms": k} dedicated communicator CTAs. Returns (o [B, S/n, H, D] bf16, lse [B, H, S/n] fp32,
     natural log)."""
     _require_cuda(q, k, v)
     B, S, H, D = q.shape

@@ -1,5 +1,6 @@
 """Ring attention cost breakdown on one B200 (emulated ranks): the
-device-staged ring at n = 2 / 4 / 8 and several communicator-CTA counts,
+device-staged ring at n = 2 / 4 / 8 with intra-SM communicator warps (the
+default) and several communicator-CTA counts,
 against the same attention work with no communication (each rank's query
 shard against the full K/V, back to back, every SM).
 
@@ -20,7 +21,8 @@ from ring_overlap import timed  # noqa: E402
 
 def main():
     B, H, D, S = 1, 16, 128, 32768
-    for n, comm_list in ((2, (None, 2, 4)), (4, (None, 1, 2)), (8, (None, 1, 2))):
+    inter = {"mode": "inter_sm"}
+    for n, comm_list in ((2, (None, inter, 2)), (4, (None, inter, 1)), (8, (None, inter, 1))):
         sl = S // n
         comms = pk.local_group(n)
         g = torch.Generator(device="cuda").manual_seed(0)
@@ -35,7 +37,7 @@ def main():
         o1, l1 = torch.empty_like(qs[0]), torch.empty(B, H, sl, device="cuda")
         t_attn = timed(lambda: [pk.attention(qs[r], k_all, v_all, out=o1, lse=l1) for r in range(n)], 3)
         for nc in comm_list:
-            sched = {"num_comm_sms": nc} if nc else None
+            sched = {"num_comm_sms": nc} if isinstance(nc, int) else nc
 
             def ring():
                 cur = torch.cuda.current_stream()
@@ -49,7 +51,7 @@ def main():
             t_ring = timed(ring, 3)
             for c in comms:
                 c.check()
-            print(json.dumps({"S": S, "world": n, "num_comm_sms": nc or "auto", "ring_ms": t_ring,
+            print(json.dumps({"S": S, "world": n, "communicators": "comm warps" if nc is None else ("comm CTAs (auto)" if nc is inter else f"{nc} comm CTAs"), "ring_ms": t_ring,
                               "attention_only_ms": t_attn, "ratio": t_ring / t_attn,
                               "sms_per_rank": comms[0].num_sms}), flush=True)
         for c in comms:

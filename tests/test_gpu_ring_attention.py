@@ -18,7 +18,7 @@ def _pk():
     return pk
 
 
-def run(world, B, S_loc, H, seed=0, scale=None):
+def run(world, B, S_loc, H, seed=0, scale=None, schedule=None):
     pk = _pk()
     D = 128
     comms = pk.local_group(world)
@@ -31,7 +31,8 @@ def run(world, B, S_loc, H, seed=0, scale=None):
     outs = []
     for r in range(world):
         with torch.cuda.stream(streams[r]):
-            outs.append(pk.ring_attention(comms[r], qs[r], ks[r], vs[r], softmax_scale=scale, stream=streams[r]))
+            outs.append(pk.ring_attention(comms[r], qs[r], ks[r], vs[r], softmax_scale=scale, stream=streams[r],
+                                          schedule=schedule))
     torch.cuda.synchronize()
     for c in comms:
         c.check()
@@ -54,6 +55,16 @@ def test_single_rank_attention(S_loc):
 @pytest.mark.parametrize("world", [2, 4, 8])
 def test_ring_attention_matches_oracle(world):
     run(world, 1, 256, 2, seed=world)
+
+
+@pytest.mark.parametrize("world", [2, 4, 8])
+@pytest.mark.parametrize("schedule", [{"mode": "intra_sm"}, {"mode": "inter_sm"}, {"num_comm_sms": 1}],
+                         ids=["comm-warps", "comm-ctas", "one-comm-cta"])
+def test_ring_attention_communicator_modes(world, schedule):
+    """Intra-SM (a comm warp in every compute CTA, the default) and inter-SM
+    (dedicated communicator CTAs) pulls give the same result; several steps
+    per slot so the slot-refill wait is exercised (n >= 3)."""
+    run(world, 1, 512, 2, seed=11 + world, schedule=schedule)
 
 
 def test_ring_attention_batch_heads_scale():
