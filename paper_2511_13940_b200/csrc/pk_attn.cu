@@ -1014,23 +1014,30 @@ __global__ void __launch_bounds__(AT_THREADS, 1) attn_fwd_kernel(const __grid_co
 }
 
 // ---------------------------------------------------------------- CTA-pair kernel
-// attn2_fwd_kernel: the same FA4-style pipeline on a CTA pair (cluster of 2,
-// tcgen05 cta_group::2). A cluster owns four 128-query tiles of one
+// attn2_fwd_kernel: the FA4-style pipeline on a CTA pair (cluster of 2,
+// tcgen05 cta_group::2), persistent. An item is four 128-query tiles of one
 // (batch, head): CTA c holds tiles 2c and 2c+1 ("tile x" of CTA c is query
-// tile 2c + x). Every MMA spans the pair (M = 256: tile x of CTA 0 over tile x
-// of CTA 1), with the B operand split across the two CTAs' shared memory:
+// tile 2c + x of the item). Every MMA spans the pair (M = 256: tile x of CTA 0
+// over tile x of CTA 1), with the B operand split across the two CTAs' smem:
 //   S_x = Q_x K^T : each CTA stages half of the K block (64 of the 128 keys)
 //   O_x += P_x V  : each CTA stages half of the V block (64 of the 128 dims)
 // so each SM reads 6 KB of smem per K16 step of QK instead of 8 KB, 2 KB
 // instead of 4 KB per PV step, and TMA-writes half the K/V bytes: the
-// single-CTA kernel's smem traffic (~98 % of its 128 B/clk) was what held its
-// MMA pipeline to ~80 % of peak. The leader CTA's MMA warp issues for the
-// pair; TMA completions and the softmax warps' P-ready arrivals go to the
-// leader's barriers, MMA commits multicast to both CTAs. One item per
-// cluster (no split tail).
+// single-CTA kernel's smem traffic (~98 % of its 128 B/clk with the K/V
+// writes) holds its MMA pipeline to ~83 % of peak even with the softmax
+// compiled out. The leader CTA's MMA warp issues for the pair; TMA completions
+// and the softmax warps' P-ready / O-drained arrivals go to the leader's
+// barriers, MMA commits multicast to both CTAs. The clusters are persistent
+// and walk the items round-robin: an item's Q is released once its last QK is
+// issued, so the next item's Q load and first QKs overlap the last PVs and the
+// epilogue. K / V halves are AT2_STAGES deep.
 constexpr int AT2_KH_BYTES = (AT_BN / 2) * AT_D * 2;   // 16 KB: 64 keys x 128 dims
 constexpr int AT2_VH_BYTES = AT_BN * (AT_D / 2) * 2;   // 16 KB: 128 keys x 64 dims
-constexpr int AT2_SMEM = 2 * AT_Q_BYTES + 2 * AT2_KH_BYTES + 2 * AT2_VH_BYTES + 512 + 1024;
+#ifndef AT2_STAGES
+#define AT2_STAGES 4
+#endif
+constexpr int AT2_SMEM = 2 * AT_Q_BYTES + AT2_STAGES * (AT2_KH_BYTES + AT2_VH_BYTES) + 512 + 1024;
+static_assert(AT2_SMEM <= 232448 - 1024, "pair kernel smem");
 
 PK_DEV void tma_load_4d_2sm(const CUtensorMap* m, uint64_t* bar, void* dst, int c0, int c1, int c2, int c3) {
   const uint32_t b = smem_u32(bar) & 0xFEFFFFFFu;     // completion on the leader CTA's barrier
@@ -1051,38 +1058,49 @@ PK_DEV void umma_f16_ts2(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc, uint3
 __global__ void __launch_bounds__(AT2_THREADS, 1) attn2_fwd_kernel(const __grid_constant__ AttnArgs a) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  constexpr int NS = AT2_STAGES;
   uint8_t* sq = smem;                               // [2][32 KB]: this CTA's two query tiles
-  uint8_t* sk = sq + 2 * AT_Q_BYTES;                // [2][16 KB]: keys [64c, 64c+64) of the block
-  uint8_t* sv = sk + 2 * AT2_KH_BYTES;              // [2][16 KB]: dims [64c, 64c+64) of the block
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sv + 2 * AT2_VH_BYTES);
-  uint64_t* q_full = bars + 0;      // leader: both CTAs' Q
-  uint64_t* k_full = bars + 1;      // [2] leader: both K halves
-  uint64_t* k_empty = bars + 3;     // [2] both CTAs (multicast commit)
-  uint64_t* v_full = bars + 5;      // [2] leader
-  uint64_t* v_empty = bars + 7;     // [2] both
-  uint64_t* s_full = bars + 9;      // [2] both, per tile
-  uint64_t* p_full = bars + 11;     // [2 tiles][2 halves] leader: 8 arrivals (4 warps x 2 CTAs)
-  uint64_t* o_full = bars + 15;     // [2] both
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 17);
+  uint8_t* sk = sq + 2 * AT_Q_BYTES;                // [NS][16 KB]: keys [64c, 64c+64) of a block
+  uint8_t* sv = sk + NS * AT2_KH_BYTES;             // [NS][16 KB]: dims [64c, 64c+64) of a block
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sv + NS * AT2_VH_BYTES);
+  uint64_t* q_full = bars + 0;      // leader: both CTAs' Q (tx)
+  uint64_t* q_empty = bars + 1;     // both (multicast commit): the item's QKs are done
+  uint64_t* k_full = bars + 2;      // [NS] leader (tx)
+  uint64_t* k_empty = k_full + NS;  // [NS] both
+  uint64_t* v_full = k_empty + NS;  // [NS] leader (tx)
+  uint64_t* v_empty = v_full + NS;  // [NS] both
+  uint64_t* s_full = v_empty + NS;  // [2] both, per tile
+  uint64_t* p_full = s_full + 2;    // [2 tiles][2 halves] leader: 8 arrivals (4 warps x 2 CTAs)
+  uint64_t* o_full = p_full + 4;    // [2] both
+  uint64_t* o_empty = o_full + 2;   // [2] leader: 8 arrivals (O drained in both CTAs)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_empty + 2);
 
   const uint32_t warp = warp_id_sync();
   const uint32_t lane = lane_id();
   const uint32_t cta = cluster_ctarank();
   const bool leader = cta == 0;
   const int quads = a.S_q / (4 * AT_BM);
-  const int cl = (int)cluster_id_x();
-  const int qd = cl % quads;
-  const int h = (cl / quads) % a.H;
-  const int b = cl / (quads * a.H);
+  const int items = a.B * a.H * quads;
+  const int cl0 = (int)cluster_id_x();
+  const int ncl = (int)nclusters_x();
   const int nblk = a.S_kv / AT_BN;
+  auto item_coords = [&](int it, int& qd, int& h, int& b) {
+    qd = it % quads;
+    h = (it / quads) % a.H;
+    b = it / (quads * a.H);
+  };
 
   if (warp == 0 && lane == 0) {
     mbar_init(q_full, 1);
-    for (int i = 0; i < 2; ++i) {
+    mbar_init(q_empty, 1);
+    for (int i = 0; i < NS; ++i) {
       mbar_init(&k_full[i], 1); mbar_init(&k_empty[i], 1);
       mbar_init(&v_full[i], 1); mbar_init(&v_empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
       mbar_init(&s_full[i], 1); mbar_init(&o_full[i], 1);
       mbar_init(&p_full[2 * i], 8); mbar_init(&p_full[2 * i + 1], 8);
+      mbar_init(&o_empty[i], 8);
     }
     fence_mbar_init();
   }
@@ -1097,40 +1115,38 @@ __global__ void __launch_bounds__(AT2_THREADS, 1) attn2_fwd_kernel(const __grid_
   if (warp == 0) {
     // ------------------------------------------------------------ loader (lane 0, both CTAs)
     if (lane == 0) {
-      const int bps = a.blocks_per_step;
-      int ready_steps = 1;
-      const uint32_t flag_epoch = a.step_flags != nullptr ? call_get(a.call, 0) : 0u;
-      auto step_ready = [&](int step) {
-        while (a.step_flags != nullptr && ready_steps <= step) {
-          wait_geq(a.step_flags + ready_steps, flag_epoch, a.err, a.timeout_ns);
-          fence_async_global();
-          ++ready_steps;
-        }
-      };
-      if (leader) mbar_arrive_expect_tx(q_full, 2 * 2 * AT_Q_BYTES);
-      for (int x = 0; x < 2; ++x) {
-        const int qrow = (4 * qd + 2 * (int)cta + x) * AT_BM;
-        tma_load_4d_2sm(&a.tm_q, q_full, sq + x * AT_Q_BYTES, 0, h, qrow, b);
-        tma_load_4d_2sm(&a.tm_q, q_full, sq + x * AT_Q_BYTES + AT_Q_BYTES / 2, 64, h, qrow, b);
-      }
-      auto load_k = [&](int j) {
-        const int st = j & 1;
-        const int step = j / bps, row = (j % bps) * AT_BN + (int)cta * (AT_BN / 2);
-        step_ready(step);
-        mbar_wait(&k_empty[st], ((j >> 1) & 1) ^ 1);
+      auto load_k = [&](int g, int j, int h, int b) {
+        const int st = g % NS;
+        mbar_wait(&k_empty[st], ((g / NS) & 1) ^ 1);
         uint8_t* kb = sk + st * AT2_KH_BYTES;
         if (leader) mbar_arrive_expect_tx(&k_full[st], 2 * AT2_KH_BYTES);
-        tma_load_4d_2sm(&a.tm_k2, &k_full[st], kb, 0, h, row, step * a.B + b);
-        tma_load_4d_2sm(&a.tm_k2, &k_full[st], kb + AT2_KH_BYTES / 2, 64, h, row, step * a.B + b);
+        const int row = j * AT_BN + (int)cta * (AT_BN / 2);
+        tma_load_4d_2sm(&a.tm_k2, &k_full[st], kb, 0, h, row, b);
+        tma_load_4d_2sm(&a.tm_k2, &k_full[st], kb + AT2_KH_BYTES / 2, 64, h, row, b);
       };
-      if (nblk > 0) load_k(0);
-      for (int j = 0; j < nblk; ++j) {
-        if (j + 1 < nblk) load_k(j + 1);
-        const int vs = j & 1;
-        const int step = j / bps, row = (j % bps) * AT_BN;
-        mbar_wait(&v_empty[vs], ((j >> 1) & 1) ^ 1);
-        if (leader) mbar_arrive_expect_tx(&v_full[vs], 2 * AT2_VH_BYTES);
-        tma_load_4d_2sm(&a.tm_v, &v_full[vs], sv + vs * AT2_VH_BYTES, (int)cta * 64, h, row, step * a.B + b);
+      auto load_v = [&](int g, int j, int h, int b) {
+        const int st = g % NS;
+        mbar_wait(&v_empty[st], ((g / NS) & 1) ^ 1);
+        if (leader) mbar_arrive_expect_tx(&v_full[st], 2 * AT2_VH_BYTES);
+        tma_load_4d_2sm(&a.tm_v, &v_full[st], sv + st * AT2_VH_BYTES, (int)cta * 64, h, j * AT_BN, b);
+      };
+      int g = 0, seg = 0;
+      for (int it = cl0; it < items; it += ncl, ++seg) {
+        int qd, h, b;
+        item_coords(it, qd, h, b);
+        mbar_wait(q_empty, (seg & 1) ^ 1);
+        if (leader) mbar_arrive_expect_tx(q_full, 2 * 2 * AT_Q_BYTES);
+        for (int x = 0; x < 2; ++x) {
+          const int qrow = (4 * qd + 2 * (int)cta + x) * AT_BM;
+          tma_load_4d_2sm(&a.tm_q, q_full, sq + x * AT_Q_BYTES, 0, h, qrow, b);
+          tma_load_4d_2sm(&a.tm_q, q_full, sq + x * AT_Q_BYTES + AT_Q_BYTES / 2, 64, h, qrow, b);
+        }
+        load_k(g, 0, h, b);
+        for (int j = 0; j < nblk; ++j) {
+          if (j + 1 < nblk) load_k(g + j + 1, j + 1, h, b);
+          load_v(g + j, j, h, b);
+        }
+        g += nblk;
       }
     }
     __syncwarp();
@@ -1138,9 +1154,9 @@ __global__ void __launch_bounds__(AT2_THREADS, 1) attn2_fwd_kernel(const __grid_
     // ------------------------------------------------------------ MMA issuer (leader)
     constexpr uint32_t id_s = idesc_bf16(2 * AT_BM, AT_BN, 0);
     constexpr uint32_t id_o = idesc_bf16(2 * AT_BM, AT_D, 1);
-    auto issue_qk = [&](int x, int j) {
+    auto issue_qk = [&](int x, int g) {
       const uint32_t q_addr = smem_u32(sq + x * AT_Q_BYTES);
-      const uint32_t k_addr = smem_u32(sk + (j & 1) * AT2_KH_BYTES);
+      const uint32_t k_addr = smem_u32(sk + (g % NS) * AT2_KH_BYTES);
 #pragma unroll
       for (int kk = 0; kk < AT_D / 16; ++kk) {
         const int atom = kk >> 2, sub = kk & 3;
@@ -1150,152 +1166,171 @@ __global__ void __launch_bounds__(AT2_THREADS, 1) attn2_fwd_kernel(const __grid_
       }
       umma_commit<2>(&s_full[x]);
     };
-    auto issue_pv = [&](int x, int j, int half) {
-      const uint32_t v_addr = smem_u32(sv + (j & 1) * AT2_VH_BYTES);
+    auto issue_pv = [&](int x, int g, int half, bool first) {
+      const uint32_t v_addr = smem_u32(sv + (g % NS) * AT2_VH_BYTES);
 #pragma unroll
       for (int k4 = 0; k4 < AT_BN / 32; ++k4) {
         const int kk = half * (AT_BN / 32) + k4;
         const uint64_t bd = sdesc_mnmajor_sw128(v_addr + kk * 2048, AT2_VH_BYTES, 1024);
-        umma_f16_ts2(tmem + 256 * x + 128, tmem + 256 * x + kk * 8, bd, id_o, (j > 0 || kk > 0) ? 1u : 0u);
+        umma_f16_ts2(tmem + 256 * x + 128, tmem + 256 * x + kk * 8, bd, id_o, (!first || kk > 0) ? 1u : 0u);
       }
-      if (half == 1 && j == nblk - 1) umma_commit<2>(&o_full[x]);
     };
-    mbar_wait(q_full, 0);
-    tc_fence_after();
-    if (nblk > 0) {
-      mbar_wait(&k_full[0], 0);
+    int g = 0, seg = 0;
+    for (int it = cl0; it < items; it += ncl, ++seg) {
+      mbar_wait(q_full, seg & 1);
+      mbar_wait(&k_full[g % NS], (g / NS) & 1);
       tc_fence_after();
       if (elect_one()) {
-        for (int x = 0; x < 2; ++x) issue_qk(x, 0);
-        umma_commit<2>(&k_empty[0]);
+        issue_qk(0, g);
+        issue_qk(1, g);
+        umma_commit<2>(&k_empty[g % NS]);
+        if (nblk == 1) umma_commit<2>(q_empty);
       }
       __syncwarp();
-    }
-    for (int j = 0; j < nblk; ++j) {
-      mbar_wait(&v_full[j & 1], (j >> 1) & 1);
-      const bool more = j + 1 < nblk;
-      if (more) mbar_wait(&k_full[(j + 1) & 1], ((j + 1) >> 1) & 1);
-      for (int x = 0; x < 2; ++x) {
-        mbar_wait(&p_full[2 * x], j & 1);
-        tc_fence_after();
-        if (elect_one()) issue_pv(x, j, 0);
-        __syncwarp();
-        mbar_wait(&p_full[2 * x + 1], j & 1);
-        tc_fence_after();
+      for (int i = 0; i < nblk; ++i) {
+        const int gg = g + i;
+        mbar_wait(&v_full[gg % NS], (gg / NS) & 1);
+        const bool more = i + 1 < nblk;
+        if (more) mbar_wait(&k_full[(gg + 1) % NS], ((gg + 1) / NS) & 1);
+        for (int x = 0; x < 2; ++x) {
+          // the previous item's O_x must have been drained in both CTAs
+          if (i == 0 && seg > 0) mbar_wait_cluster(&o_empty[x], (seg - 1) & 1);
+          mbar_wait_cluster(&p_full[2 * x], gg & 1);
+          tc_fence_after();
+          if (elect_one()) issue_pv(x, gg, 0, i == 0);
+          __syncwarp();
+          mbar_wait_cluster(&p_full[2 * x + 1], gg & 1);
+          tc_fence_after();
+          if (elect_one()) {
+            issue_pv(x, gg, 1, i == 0);
+            if (more) issue_qk(x, gg + 1);
+            else umma_commit<2>(&o_full[x]);
+          }
+          __syncwarp();
+        }
         if (elect_one()) {
-          issue_pv(x, j, 1);
-          if (more) issue_qk(x, j + 1);
+          umma_commit<2>(&v_empty[gg % NS]);
+          if (more) umma_commit<2>(&k_empty[(gg + 1) % NS]);
+          if (i + 2 == nblk) umma_commit<2>(q_empty);   // the item's last QKs are issued
         }
         __syncwarp();
       }
-      if (elect_one()) {
-        umma_commit<2>(&v_empty[j & 1]);
-        if (more) umma_commit<2>(&k_empty[(j + 1) & 1]);
-      }
-      __syncwarp();
+      g += nblk;
     }
   }
   } else {
   asm volatile("setmaxnreg.inc.sync.aligned.u32 224;\n" ::: "memory");
   // ------------------------------------------------------------ softmax + epilogue (tile x of this CTA)
   const int x = (warp - 4) / 4;
-  const int qt = 4 * qd + 2 * (int)cta + x;
   const int q = warp & 3;
   const int row = q * 32 + (int)lane;
   const uint32_t lane_off = (uint32_t)(q * 32) << 16;
   const uint32_t t_s = tmem + 256 * x + lane_off;
   const uint32_t t_o = t_s + 128;
-  float m = -INFINITY, l = 0.f;
   const float sc = a.scale_log2;
-  for (int j = 0; j < nblk; ++j) {
-    mbar_wait(&s_full[x], j & 1);
-    tc_fence_after();
-    uint32_t r[AT_BN];
+  int gx = 0, seg = 0;
+  for (int it = cl0; it < items; it += ncl, ++seg) {
+    int qd, h, b;
+    item_coords(it, qd, h, b);
+    const int qt = 4 * qd + 2 * (int)cta + x;
+    float m = -INFINITY, l = 0.f;
+    for (int j = 0; j < nblk; ++j, ++gx) {
+      mbar_wait(&s_full[x], gx & 1);
+      tc_fence_after();
+#ifdef AT_MMA_ONLY   // timing diagnostic only: the MMA pipeline without softmax (wrong results)
+      if (lane == 0) { mbar_arrive_cluster(&p_full[2 * x], 0); mbar_arrive_cluster(&p_full[2 * x + 1], 0); }
+      continue;
+#endif
+      uint32_t r[AT_BN];
 #pragma unroll
-    for (int c = 0; c < 4; ++c) tmem_ld_32x32b_x32(t_s + c * 32, *reinterpret_cast<uint32_t(*)[32]>(r + c * 32));
-    tmem_ld_wait();
-    float m8[8];
+      for (int c = 0; c < 4; ++c) tmem_ld_32x32b_x32(t_s + c * 32, *reinterpret_cast<uint32_t(*)[32]>(r + c * 32));
+      tmem_ld_wait();
+      float m8[8];
 #pragma unroll
-    for (int t = 0; t < 8; ++t) m8[t] = fmax3(__uint_as_float(r[2 * t]), __uint_as_float(r[2 * t + 1]), -INFINITY);
+      for (int t = 0; t < 8; ++t) m8[t] = fmax3(__uint_as_float(r[2 * t]), __uint_as_float(r[2 * t + 1]), -INFINITY);
 #pragma unroll
-    for (int i2 = 8; i2 < AT_BN / 2; ++i2)
-      m8[i2 & 7] = fmax3(m8[i2 & 7], __uint_as_float(r[2 * i2]), __uint_as_float(r[2 * i2 + 1]));
-    float mx = fmax3(fmax3(m8[0], m8[1], m8[2]), fmax3(m8[3], m8[4], m8[5]), fmaxf(m8[6], m8[7]));
-    mx *= sc;
-    const bool grow = mx > m + AT_RESCALE_THRESHOLD;
-    if (j > 0 && __any_sync(0xffffffffu, grow)) {
-      const float alpha = grow ? fast_exp2(m - mx) : 1.f;
+      for (int i2 = 8; i2 < AT_BN / 2; ++i2)
+        m8[i2 & 7] = fmax3(m8[i2 & 7], __uint_as_float(r[2 * i2]), __uint_as_float(r[2 * i2 + 1]));
+      float mx = fmax3(fmax3(m8[0], m8[1], m8[2]), fmax3(m8[3], m8[4], m8[5]), fmaxf(m8[6], m8[7]));
+      mx *= sc;
+      const bool grow = mx > m + AT_RESCALE_THRESHOLD;
+      if (j > 0 && __any_sync(0xffffffffu, grow)) {
+        const float alpha = grow ? fast_exp2(m - mx) : 1.f;
 #pragma unroll 1
-      for (int c = 0; c < 4; ++c) {
-        uint32_t o[32];
-        tmem_ld_32x32b_x32(t_o + c * 32, o);
-        tmem_ld_wait();
+        for (int c = 0; c < 4; ++c) {
+          uint32_t o[32];
+          tmem_ld_32x32b_x32(t_o + c * 32, o);
+          tmem_ld_wait();
 #pragma unroll
-        for (int i2 = 0; i2 < 32; ++i2) o[i2] = __float_as_uint(__uint_as_float(o[i2]) * alpha);
-        tmem_st_32x32b_x32(t_o + c * 32, o);
-      }
-      l *= alpha;
-    }
-    if (grow) m = mx;
-    const uint64_t sc2 = f2_pack(sc, sc), nm2 = f2_pack(-m, -m);
-    uint64_t rs2[4];
-#pragma unroll
-    for (int t = 0; t < 4; ++t) rs2[t] = f2_pack(0.f, 0.f);
-#pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      uint32_t pk[16];
-#pragma unroll
-      for (int i2 = 0; i2 < 16; ++i2) {
-        float x0, x1, p0, p1;
-        f2_unpack(f2_fma(f2_pack(__uint_as_float(r[32 * c + 2 * i2]), __uint_as_float(r[32 * c + 2 * i2 + 1])), sc2, nm2),
-                  x0, x1);
-        if ((i2 & 3) < AT_EXP_EMU) {
-          poly_exp2x2(x0, x1, p0, p1);
-        } else {
-          p0 = fast_exp2(x0);
-          p1 = fast_exp2(x1);
+          for (int i2 = 0; i2 < 32; ++i2) o[i2] = __float_as_uint(__uint_as_float(o[i2]) * alpha);
+          tmem_st_32x32b_x32(t_o + c * 32, o);
         }
-        rs2[i2 & 3] = f2_add(rs2[i2 & 3], f2_pack(p0, p1));
-        pk[i2] = pack_bf16x2(p0, p1);
+        l *= alpha;
       }
-      tmem_st_32x32b_x16(t_s + c * 16, pk);
-      if (c & 1) {                                     // keys [64h, 64h+64) in TMEM: tell the leader's MMA warp
-        tmem_st_wait();
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive_cluster(&p_full[2 * x + (c >> 1)], 0);
+      if (grow) m = mx;
+      const uint64_t sc2 = f2_pack(sc, sc), nm2 = f2_pack(-m, -m);
+      uint64_t rs2[4];
+#pragma unroll
+      for (int t = 0; t < 4; ++t) rs2[t] = f2_pack(0.f, 0.f);
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        uint32_t pk[16];
+#pragma unroll
+        for (int i2 = 0; i2 < 16; ++i2) {
+          float x0, x1, p0, p1;
+          f2_unpack(f2_fma(f2_pack(__uint_as_float(r[32 * c + 2 * i2]), __uint_as_float(r[32 * c + 2 * i2 + 1])), sc2, nm2),
+                    x0, x1);
+          if ((i2 & 3) < AT_EXP_EMU) {
+            poly_exp2x2(x0, x1, p0, p1);
+          } else {
+            p0 = fast_exp2(x0);
+            p1 = fast_exp2(x1);
+          }
+          rs2[i2 & 3] = f2_add(rs2[i2 & 3], f2_pack(p0, p1));
+          pk[i2] = pack_bf16x2(p0, p1);
+        }
+        tmem_st_32x32b_x16(t_s + c * 16, pk);
+        if (c & 1) {                                     // keys [64h, 64h+64) in TMEM: tell the leader's MMA warp
+          tmem_st_wait();
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive_cluster(&p_full[2 * x + (c >> 1)], 0);
+        }
       }
+      float rs_lo, rs_hi;
+      f2_unpack(f2_add(f2_add(rs2[0], rs2[1]), f2_add(rs2[2], rs2[3])), rs_lo, rs_hi);
+      l += rs_lo + rs_hi;
     }
-    float rs_lo, rs_hi;
-    f2_unpack(f2_add(f2_add(rs2[0], rs2[1]), f2_add(rs2[2], rs2[3])), rs_lo, rs_hi);
-    l += rs_lo + rs_hi;
-  }
-  // ------------------------------------------------------------ epilogue
-  mbar_wait(&o_full[x], 0);
-  tc_fence_after();
-  float o[AT_D];
+    // ------------------------------------------------------------ epilogue
+    mbar_wait(&o_full[x], seg & 1);
+    tc_fence_after();
+    float o[AT_D];
 #pragma unroll
-  for (int c = 0; c < AT_D / 32; ++c) {
-    uint32_t t[32];
-    tmem_ld_32x32b_x32(t_o + c * 32, t);
-    tmem_ld_wait();
+    for (int c = 0; c < AT_D / 32; ++c) {
+      uint32_t t[32];
+      tmem_ld_32x32b_x32(t_o + c * 32, t);
+      tmem_ld_wait();
 #pragma unroll
-    for (int i2 = 0; i2 < 32; ++i2) o[c * 32 + i2] = __uint_as_float(t[i2]);
-  }
-  const int sq_idx = qt * AT_BM + row;
-  const long long srow = ((long long)(b * a.H + h) * a.S_q + sq_idx);
-  const float inv = (l > 0.f) ? 1.f / l : 0.f;
-  uint4* dst = reinterpret_cast<uint4*>(a.o + (((long long)b * a.S_q + sq_idx) * a.H + h) * AT_D);
+      for (int i2 = 0; i2 < 32; ++i2) o[c * 32 + i2] = __uint_as_float(t[i2]);
+    }
+    tc_fence_before();
+    __syncwarp();
+    if (lane == 0) mbar_arrive_cluster(&o_empty[x], 0);   // the next item's PV may overwrite O_x
+    const int sq_idx = qt * AT_BM + row;
+    const long long srow = ((long long)(b * a.H + h) * a.S_q + sq_idx);
+    const float inv = (l > 0.f) ? 1.f / l : 0.f;
+    uint4* dst = reinterpret_cast<uint4*>(a.o + (((long long)b * a.S_q + sq_idx) * a.H + h) * AT_D);
 #pragma unroll
-  for (int i2 = 0; i2 < AT_D / 8; ++i2) {
-    uint4 w;
-    w.x = pack_bf16x2(o[8 * i2 + 0] * inv, o[8 * i2 + 1] * inv);
-    w.y = pack_bf16x2(o[8 * i2 + 2] * inv, o[8 * i2 + 3] * inv);
-    w.z = pack_bf16x2(o[8 * i2 + 4] * inv, o[8 * i2 + 5] * inv);
-    w.w = pack_bf16x2(o[8 * i2 + 6] * inv, o[8 * i2 + 7] * inv);
-    dst[i2] = w;
+    for (int i2 = 0; i2 < AT_D / 8; ++i2) {
+      uint4 w;
+      w.x = pack_bf16x2(o[8 * i2 + 0] * inv, o[8 * i2 + 1] * inv);
+      w.y = pack_bf16x2(o[8 * i2 + 2] * inv, o[8 * i2 + 3] * inv);
+      w.z = pack_bf16x2(o[8 * i2 + 4] * inv, o[8 * i2 + 5] * inv);
+      w.w = pack_bf16x2(o[8 * i2 + 6] * inv, o[8 * i2 + 7] * inv);
+      dst[i2] = w;
+    }
+    a.lse[srow] = (m + log2f(l)) * 0.69314718055994531f;
   }
-  a.lse[srow] = (m + log2f(l)) * 0.69314718055994531f;
   }
   tc_fence_before();
   cluster_sync();
@@ -1345,7 +1380,8 @@ static int launch_attn(AttnScratch& scr, int num_sms, AttnArgs& a, cudaStream_t 
   if (getenv("PK_ATTN_PAIR") && a.S_q % (4 * AT_BM) == 0) {
     PK_TRY(ensure_smem_attr((const void*)attn2_fwd_kernel, AT2_SMEM));
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(2 * a.B * a.H * (a.S_q / (4 * AT_BM)), 1, 1);
+    const int items2 = a.B * a.H * (a.S_q / (4 * AT_BM));
+    cfg.gridDim = dim3(2 * std::min(items2, num_sms / 2), 1, 1);     // persistent clusters
     cfg.blockDim = dim3(AT2_THREADS, 1, 1);
     cfg.dynamicSmemBytes = AT2_SMEM;
     cfg.stream = st;

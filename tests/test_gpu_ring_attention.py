@@ -121,10 +121,12 @@ def test_stream_k_more_ctas_than_tail_blocks(monkeypatch):
     run(1, 1, 512, 3, seed=9)        # 6 items x 4 blocks = 24 tail blocks over 40 CTAs
 
 
-@pytest.mark.parametrize("B,Sq,Skv,H", [(1, 512, 512, 1), (1, 1024, 2048, 2), (2, 512, 1024, 3)])
+@pytest.mark.parametrize("B,Sq,Skv,H", [(1, 512, 512, 1), (1, 1024, 2048, 2), (2, 512, 1024, 3), (1, 512, 128, 1),
+                                         (2, 512, 384, 48), (1, 2048, 1024, 16)])
 def test_cta_pair_kernel_matches_oracle(monkeypatch, B, Sq, Skv, H):
-    """The experimental cta_group::2 attention kernel (PK_ATTN_PAIR=1): four
-    query tiles per cluster, K and V halves split across the pair."""
+    """The cta_group::2 attention kernel (PK_ATTN_PAIR=1): four query tiles
+    per cluster, K and V halves split across the pair, persistent clusters
+    (96 items over 74 clusters: a second round; one key block; 16 heads)."""
     pk = _pk()
     monkeypatch.setenv("PK_ATTN_PAIR", "1")
     g = torch.Generator(device="cuda").manual_seed(Sq + Skv + H)
