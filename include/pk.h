@@ -219,8 +219,9 @@ PK_API int pk_all_reduce_ablate(pk_comm* comm, pk_tensor* x, uint32_t overheads,
  * compute CTAs work on the previous step (step-major units, log-sum-exp merge
  * in ascending step order). Communicators: NULL / mode intra_sm = a comm warp
  * in every compute CTA; mode inter_sm or num_comm_sms > 0 = dedicated CTAs
- * (num_comm_sms, 0 = sized to the link). k / v may be reused once the call
- * completes on `stream`. */
+ * (num_comm_sms, 0 = sized to the link). sched->stages = 2P stage slots:
+ * a work unit spans P ring steps (0 = default: 2 slots below n = 8, else 4).
+ * k / v may be reused once the call completes on `stream`. */
 PK_API int pk_ring_attn_fwd(pk_comm* comm, const pk_tensor* q, const pk_tensor* k,
                             const pk_tensor* v, pk_tensor* o, pk_tensor* lse, float softmax_scale,
                             const pk_sched* sched, void* stream);

@@ -23,17 +23,19 @@
 //                              lazy rescale of O in TMEM, exp2, P (bf16x2)
 //                              back into TMEM; final epilogue
 //   * ring (n > 1), the reference's schedule (workloads.py:644-685): work
-//     units are (step, item) in step-major order over the persistent compute
-//     CTAs. Step 0 reads the local shard; step s >= 1 reads slot s & 1 of a
-//     2-slot local stage. Communicator CTAs (the last CTAs of the grid, the
-//     inter-SM schedule) TMA-pull the shard of rank (r - s) mod n from its
-//     owner's symmetric K/V (peer VA -> smem -> slot, cp.async.bulk) as soon
-//     as every unit of step s - 2 has finished reading that slot, and publish
-//     the step (signal -> wait); a unit's loader waits for its step. Each
-//     unit leaves its (O, m, l) for the item in an fp32 state that the next
-//     step's unit of the same item merges in ascending step order
-//     (log-sum-exp); the last step writes o (bf16) and lse. Per rank: 2
-//     K/V slots, not n.
+//     units are (span, item) in span-major order over the persistent compute
+//     CTAs, a span being P consecutive ring steps (P = 1: the reference's
+//     per-step units). Step 0 reads the local shard; step s >= 1 reads slot
+//     s % 2P of a 2P-slot local stage (2 slots at P = 1). Communicators — a
+//     comm warp in every compute CTA (intra-SM, the default) or the last CTAs
+//     of the grid (inter-SM) — TMA-pull the shard of rank (r - s) mod n from
+//     its owner's symmetric K/V (peer VA -> smem -> slot, cp.async.bulk) as
+//     soon as every unit that read the slot's previous step has loaded it, and
+//     publish the step (signal -> wait); a unit's loader waits for each step.
+//     Each unit leaves its (O, m, l) for the item in an fp32 state that the
+//     next span's unit of the same item merges in ascending order
+//     (log-sum-exp); the last span writes o (bf16) and lse. Per rank: 2P K/V
+//     slots, not n.
 #include "pk_host.h"
 #include "pk_ptx.cuh"
 #include <algorithm>
@@ -111,6 +113,7 @@ struct AttnArgs {
   // device-staged ring (ring_steps > 1): see the header comment
   CUtensorMap tm_ks, tm_vs;      // the 2-slot stage, [2B, S, H, D] (slot = batch / B)
   int ring_steps;                // n
+  int ring_span;                 // P: ring steps per work unit (the stage holds 2P slots, step s in slot s % 2P)
   int ring_comm;                 // communicator CTAs (the last ones of the grid)
   int rank, world;
   const uint8_t* ring_src_k[8];  // every rank's K / V shard (peer VAs)
@@ -330,6 +333,12 @@ __global__ void __launch_bounds__(AT_THREADS, 1) attn_fwd_kernel(const __grid_co
   const bool is_comm = ring && (int)blockIdx.x >= ncompute;
   const RingCtr rc{a.ring_ctr, a.ring_steps};
   const int bps = a.blocks_per_step;
+  // ring: a unit covers a span of consecutive steps of one item — span 0 is
+  // step 0 (the local shard) alone, so the first pull hides behind a whole
+  // pass over the items; span k >= 1 is steps [(k-1)P + 1, kP]
+  const int nspans = ring ? 1 + (a.ring_steps - 1 + a.ring_span - 1) / a.ring_span : 1;
+  const int nslots = ring ? 2 * a.ring_span : 2;
+  auto span_of = [&](int step) { return step == 0 ? 0 : (step - 1) / a.ring_span + 1; };
   const int t0 = (me >= 0 && a.tail_items) ? (int)sp.tstart(me) : 0;
   const int t1 = (me >= 0 && a.tail_items) ? (int)sp.tstart(me + 1) : 0;
   // segment walk shared by every role: item, key blocks [j0, j1), pair shape
@@ -340,13 +349,14 @@ __global__ void __launch_bounds__(AT_THREADS, 1) attn_fwd_kernel(const __grid_co
   };
   auto seg_next = [&](SegIter& it, SegInfo& g) -> bool {
     if (ring) {                                      // it.k = next unit index
-      if (it.k >= a.ring_steps * items) return false;
+      if (it.k >= nspans * items) return false;
       const int u = it.k;
       it.k += ncompute;
       g.item = u % items;
       g.ti = -1;
-      g.j0 = (u / items) * bps;
-      g.j1 = g.j0 + bps;
+      const int k = u / items;                         // span: step 0 alone, then P steps each
+      g.j0 = (k == 0 ? 0 : (k - 1) * a.ring_span + 1) * bps;
+      g.j1 = (k == 0 ? 1 : min(a.ring_steps, k * a.ring_span + 1)) * bps;
     } else if (it.w < nfull) {
       g.item = it.w;
       g.ti = -1;
@@ -428,15 +438,17 @@ __global__ void __launch_bounds__(AT_THREADS, 1) attn_fwd_kernel(const __grid_co
 #ifdef AT_RING_PROF
       const long long tw = clock64();
 #endif
-      if (ok && s >= 3) ok = wait_geq(rc.units(s - 2), (uint32_t)items, a.err, a.timeout_ns);
+      // slot s % nslots last held step s - nslots (step 0 reads the local shard):
+      // every unit of that step's span must have loaded it
+      if (ok && s - nslots >= 1) ok = wait_geq(rc.units(span_of(s - nslots)), (uint32_t)items, a.err, a.timeout_ns);
       if (ok) ok = wait_geq(a.ready_local + src, ready_expect, a.err, a.timeout_ns);
 #ifdef AT_RING_PROF
       const long long tc0 = clock64();
       RP_ADD(5, tc0 - tw);
 #endif
       fence_async_global();
-      uint8_t* dk = a.stage_k + (long long)(s & 1) * a.shard_bytes;
-      uint8_t* dv = a.stage_v + (long long)(s & 1) * a.shard_bytes;
+      uint8_t* dk = a.stage_k + (long long)(s % nslots) * a.shard_bytes;
+      uint8_t* dv = a.stage_v + (long long)(s % nslots) * a.shard_bytes;
       auto piece = [&](long long k, const uint8_t** sp, uint8_t** dp, uint32_t* bytes) {
         const long long q = me_c + k * nc;
         const bool isv = q >= ppt;
@@ -510,7 +522,7 @@ __global__ void __launch_bounds__(AT_THREADS, 1) attn_fwd_kernel(const __grid_co
       auto kvmap = [&](const CUtensorMap* local, const CUtensorMap* stage, int step) {
         return (ring && step > 0) ? stage : local;
       };
-      auto kvb = [&](int step, int b) { return ring ? (step > 0 ? (step & 1) * a.B + b : b) : step * a.B + b; };
+      auto kvb = [&](int step, int b) { return ring ? (step > 0 ? (step % nslots) * a.B + b : b) : step * a.B + b; };
       auto step_ready = [&](int step) {
         if (ring) {
           if (step > 0 && step != ring_ok) {
@@ -631,7 +643,7 @@ __global__ void __launch_bounds__(AT_THREADS, 1) attn_fwd_kernel(const __grid_co
         if (ring && !more && lane == 0) {
           // every K/V block of this unit is in smem: its step's slot may be refilled
           fence_async_global();
-          asm volatile("red.release.gpu.global.add.u32 [%0], 1;" :: "l"(rc.units(sg.j0 / bps)) : "memory");
+          asm volatile("red.release.gpu.global.add.u32 [%0], 1;" :: "l"(rc.units(span_of(sg.j0 / bps))) : "memory");
         }
         if (more) mbar_wait(&k_full[(gg + 1) % AT_KSTAGES], ((gg + 1) / AT_KSTAGES) & 1);
         for (int x = 0; x < sg.ntile; ++x) {
@@ -826,7 +838,7 @@ __global__ void __launch_bounds__(AT_THREADS, 1) attn_fwd_kernel(const __grid_co
     // ring, step s > 0: the item's running state from steps < s is loaded
     // (all vectors in flight) while the unit's last PV finishes, then merged
     // chunk by chunk with O as it leaves TMEM (o[] holds the merge)
-    const int rstep = ring ? sg.j0 / bps : 0;
+    const int rstep = ring ? span_of(sg.j0 / bps) : 0;              // the unit's span
     const bool has_state = ring && rstep > 0;
     float* stt = ring ? a.ring_state + (long long)(2 * sg.item + x) * AT_STATE_FLOATS : nullptr;
     float4* st_o = reinterpret_cast<float4*>(stt) + (h * AT_OC / 4) * AT_BM + row;   // + c4 * AT_BM
@@ -899,7 +911,7 @@ __global__ void __launch_bounds__(AT_THREADS, 1) attn_fwd_kernel(const __grid_co
     const int sq_idx = (2 * sg.qp + x) * AT_BM + row;                      // query index within the local shard
     const long long srow = ((long long)(sg.b * a.H + sg.h) * a.S_q + sq_idx);   // [B, H, S_q] row
     bool write_final = true;
-    if (ring && rstep + 1 < a.ring_steps) {
+    if (ring && rstep + 1 < nspans) {
       // keep the merged state for step s + 1 (steps merge in ascending order);
       // the tile's threads sync, then one release publishes all their rows
 #pragma unroll
@@ -1505,7 +1517,19 @@ int ring_attn_fwd(Comm* c, const pk_tensor* q, const pk_tensor* k, const pk_tens
   // (O, m, l) state of every item, the ring counters (zeroed once here, then
   // re-armed by each launch's last CTA).
   const int items = (int)(B * H * ((S / AT_BM + 1) / 2));
-  const size_t stage_bytes = 4 * shard;
+  // Unit span P (ring steps per work unit): the stage holds 2P slots so the
+  // next span's shards land while the current one computes; a longer span
+  // means fewer state merges per item (n / P instead of n). sched->stages
+  // sets the slot count (2 = the reference's double buffer, P = 1).
+  // Default: P = 2 from n = 8 up (8 merges per item otherwise; measured ~3 % of
+  // the emulated n = 8 step at S = 32768, ~1.5 % at 131072,
+  // profiles/r2/s3/ring_span_ab.jsonl), else the reference's 2 slots.
+  int span = n >= 8 ? 2 : 1;
+  if (sched && sched->stages >= 2) span = sched->stages / 2;
+  if (const char* e = getenv("PK_RING_SPAN")) span = atoi(e);   // tuning hook
+  span = std::max(1, std::min(span, n));
+  const int slots = std::min(2 * span, n);                       // step s >= 1 in slot s % 2P
+  const size_t stage_bytes = (size_t)2 * slots * shard;
   const size_t state_bytes = (size_t)items * 2 * AT_STATE_FLOATS * sizeof(float);
   const size_t ctr_bytes = ring_ctr_words(n, items) * sizeof(uint32_t);
   const size_t need = stage_bytes + state_bytes + ctr_bytes;
@@ -1523,11 +1547,12 @@ int ring_attn_fwd(Comm* c, const pk_tensor* q, const pk_tensor* k, const pk_tens
     c->ring_ctr_bytes = c->ring_buf_bytes - stage_bytes - state_bytes;
   }
   a.stage_k = rb;
-  a.stage_v = rb + 2 * shard;
+  a.stage_v = rb + (size_t)slots * shard;
   a.ring_state = reinterpret_cast<float*>(rb + stage_bytes);
   a.ring_ctr = ctr;
   a.shard_bytes = (long long)shard;
   a.ring_steps = n;
+  a.ring_span = span;
   a.rank = c->rank;
   a.world = n;
   for (int r = 0; r < n; ++r) {
@@ -1544,8 +1569,8 @@ int ring_attn_fwd(Comm* c, const pk_tensor* q, const pk_tensor* k, const pk_tens
   // step 0 reads the local shard, step s >= 1 stage slot s & 1 ([2B, S, H, D])
   PK_TRY(tmap_bshd(&a.tm_k, kp[c->rank], B, S, H, AT_BN));
   PK_TRY(tmap_bshd(&a.tm_v, vp[c->rank], B, S, H, AT_BN));
-  PK_TRY(tmap_bshd(&a.tm_ks, a.stage_k, 2 * B, S, H, AT_BN));
-  PK_TRY(tmap_bshd(&a.tm_vs, a.stage_v, 2 * B, S, H, AT_BN));
+  PK_TRY(tmap_bshd(&a.tm_ks, a.stage_k, slots * B, S, H, AT_BN));
+  PK_TRY(tmap_bshd(&a.tm_vs, a.stage_v, slots * B, S, H, AT_BN));
   a.S_kv = (int)(n * S);
   a.blocks_per_step = (int)(S / AT_BN);
   // Communicators. Intra-SM (the default): warp 3 of every compute CTA pulls

@@ -269,7 +269,10 @@ def ring_attention(comm, q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, soft
     rank (r - s) mod n, which the kernel's communicators pull into a 2-slot
     local stage while step s - 1 computes: by default (or mode "intra_sm") a
     comm warp in every compute CTA, with mode "inter_sm" or
-    schedule={"num_comm_sms": k} dedicated communicator CTAs. Returns (o [B, S/n, H, D] bf16, lse [B, H, S/n] fp32,
+    schedule={"num_comm_sms": k} dedicated communicator CTAs.
+    schedule={"stages": 2P} sets the stage slots: a work unit then spans P ring
+    steps of an item (2 = the reference's double buffer, one state merge per
+    step; default 2 slots below n = 8, 4 from n = 8). Returns (o [B, S/n, H, D] bf16, lse [B, H, S/n] fp32,
     natural log)."""
     _require_cuda(q, k, v)
     B, S, H, D = q.shape

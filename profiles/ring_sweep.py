@@ -22,7 +22,8 @@ from ring_overlap import timed  # noqa: E402
 def main():
     B, H, D, S = 1, 16, 128, 32768
     inter = {"mode": "inter_sm"}
-    for n, comm_list in ((2, (None, inter, 2)), (4, (None, inter, 1)), (8, (None, inter, 1))):
+    spans = [{"stages": 2 * int(p)} for p in os.environ.get("SPANS", "").split(",") if p]
+    for n, comm_list in ((2, (None, inter, 2, *spans)), (4, (None, inter, 1, *spans)), (8, (None, inter, 1, *spans))):
         sl = S // n
         comms = pk.local_group(n)
         g = torch.Generator(device="cuda").manual_seed(0)
@@ -51,7 +52,9 @@ def main():
             t_ring = timed(ring, 3)
             for c in comms:
                 c.check()
-            print(json.dumps({"S": S, "world": n, "communicators": "comm warps" if nc is None else ("comm CTAs (auto)" if nc is inter else f"{nc} comm CTAs"), "ring_ms": t_ring,
+            print(json.dumps({"S": S, "world": n, "communicators": "comm warps" if nc is None or isinstance(nc, dict) and "stages" in nc else
+                              ("comm CTAs (auto)" if nc is inter else f"{nc} comm CTAs"),
+                              "span": nc["stages"] // 2 if isinstance(nc, dict) and "stages" in nc else 1, "ring_ms": t_ring,
                               "attention_only_ms": t_attn, "ratio": t_ring / t_attn,
                               "sms_per_rank": comms[0].num_sms}), flush=True)
         for c in comms:
