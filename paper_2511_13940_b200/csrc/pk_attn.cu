@@ -78,8 +78,11 @@ constexpr int AT_SMEM = 2 * AT_Q_BYTES + AT_KSTAGES * AT_K_BYTES + AT_VSTAGES * 
 // intra-SM ring communicator (warp 3 of each compute CTA): two pieces of smem
 // beside the Q / K / V stages (0: they do not fit this build's stages)
 constexpr int AT_RING_CBUF_OFF = 2 * AT_Q_BYTES + AT_KSTAGES * AT_K_BYTES + AT_VSTAGES * AT_V_BYTES + 512 + AT_RED_BYTES;
-constexpr int AT_RING_PIECE = (AT_SMEM + 2 * 16384 <= 232448 - 64) ? 16384 : 0;
-constexpr int AT_SMEM_RING = AT_SMEM + 2 * AT_RING_PIECE;
+#ifndef AT_RING_NBUF
+#define AT_RING_NBUF 2   // pieces of the intra-SM communicator's 32 KB of smem
+#endif
+constexpr int AT_RING_PIECE = (AT_SMEM + 32768 <= 232448 - 64) ? 32768 / AT_RING_NBUF : 0;
+constexpr int AT_SMEM_RING = AT_SMEM + AT_RING_NBUF * AT_RING_PIECE;
 constexpr int AT_TMEM_COLS = 512;                // per tile: S (128, P aliased in its first 64) + O (128)
 constexpr float AT_RESCALE_THRESHOLD = 8.0f;     // log2 units: P stays <= 2^8 between rescales
 #ifndef AT_POLY_DEG
@@ -466,7 +469,11 @@ __global__ void __launch_bounds__(AT_THREADS, 1) attn_fwd_kernel(const __grid_co
         mbar_arrive_expect_tx(&cbar[b], bytes);
         bulk_g2s(buf + (size_t)b * PIECE, sp, bytes, &cbar[b]);
       };
+#ifdef AT_RING_NOCOMM   // timing diagnostic only: steps are published without moving their shards (wrong results)
+      if (false) {
+#else
       if (ok) {
+#endif
         for (long long k = 0; k < mine && k < nbuf - 1; ++k) issue(k);
         for (long long k = 0; k < mine; ++k) {
           const int b = (int)((gp + k) % nbuf);
@@ -501,7 +508,7 @@ __global__ void __launch_bounds__(AT_THREADS, 1) attn_fwd_kernel(const __grid_co
       for (int d = 0; d < a.world; ++d) signal_add(a.done_peer[d] + a.rank, 1u);
     }
   };
-  __shared__ __align__(8) uint64_t ring_cbar[6];
+  __shared__ __align__(8) uint64_t ring_cbar[8];
 
   if (is_comm) {
     if (warp == 0 && lane == 0)                       // 192 KB: the Q / K / V buffers, unused here
@@ -688,7 +695,7 @@ __global__ void __launch_bounds__(AT_THREADS, 1) attn_fwd_kernel(const __grid_co
     // ------------------------------------------------------------ intra-SM ring communicator
     if constexpr (RING && AT_RING_PIECE > 0) {
       if (a.ring_comm == 0 && lane == 0)
-        ring_pull((int)blockIdx.x, ncompute, smem + AT_RING_CBUF_OFF, 2, AT_RING_PIECE, ring_cbar);
+        ring_pull((int)blockIdx.x, ncompute, smem + AT_RING_CBUF_OFF, AT_RING_NBUF, AT_RING_PIECE, ring_cbar);
     }
     __syncwarp();
   }
