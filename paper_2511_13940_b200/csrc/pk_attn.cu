@@ -88,6 +88,10 @@ constexpr float AT_RESCALE_THRESHOLD = 8.0f;     // log2 units: P stays <= 2^8 b
 #ifndef AT_POLY_DEG
 #define AT_POLY_DEG 3                            // degree of the FMA-pipe 2^f polynomial
 #endif
+#ifndef AT_QK_SPLIT
+#define AT_QK_SPLIT 0    // 1: next block's QK in two N = 64 halves, the high one ahead of PV — measured
+#endif                   // 25 % more cycles at the base clock (each half re-reads Q: QK then asks
+                         // 192 B/clk of smem), profiles/r2/s3/attn_qksplit_cycles.csv
 #ifndef AT_EXP_EMU
 #define AT_EXP_EMU 1                             // of every 4 key pairs, this many take 2^x on the FMA pipe (MUFU offload)
 #endif
@@ -308,7 +312,8 @@ __global__ void __launch_bounds__(AT_THREADS, 1) attn_fwd_kernel(const __grid_co
   uint64_t* p_full = s_full + 2;                // [2 tiles][2 halves]: P of keys [64h, 64h+64) in TMEM
   uint64_t* o_full = p_full + 4;                // [2] per tile
   uint64_t* o_empty = o_full + 2;               // [2] per tile: the epilogue has read O
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_empty + 2);
+  uint64_t* s_loaded = o_empty + 2;             // [2] per tile: S is in the softmax warps' registers
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(s_loaded + 2);
   __shared__ int merge_flag[2];
 
   const uint32_t warp = warp_id_sync();
@@ -396,6 +401,7 @@ __global__ void __launch_bounds__(AT_THREADS, 1) attn_fwd_kernel(const __grid_co
       mbar_init(&s_full[i], 1); mbar_init(&o_full[i], 1);
       mbar_init(&p_full[2 * i], 4); mbar_init(&p_full[2 * i + 1], 4);
       mbar_init(&o_empty[i], 4 * AT_CW);
+      mbar_init(&s_loaded[i], 4 * AT_CW);
     }
     fence_mbar_init();
   }
@@ -612,6 +618,21 @@ __global__ void __launch_bounds__(AT_THREADS, 1) attn_fwd_kernel(const __grid_co
       }
       umma_commit<1>(&s_full[x]);
     };
+    // S_x = Q_x K_g^T for keys [64 half, 64 half + 64) of the block (N = 64): the
+    // high half does not overlap P_x (packed into S_x's first 64 columns), so it
+    // is issued as soon as the softmax has S_x in registers, ahead of PV_x
+    constexpr uint32_t id_s64 = idesc_bf16(AT_BM, AT_BN / 2, 0);
+    auto issue_qk_half = [&](int x, int g, int half) {
+      const uint32_t q_addr = smem_u32(sq + x * AT_Q_BYTES);
+      const uint32_t k_addr = smem_u32(sk + (g % AT_KSTAGES) * AT_K_BYTES) + half * (AT_BN / 2) * 128;
+#pragma unroll
+      for (int kk = 0; kk < AT_D / 16; ++kk) {
+        const int atom = kk >> 2, sub = kk & 3;
+        const uint64_t ad = sdesc_kmajor_sw128(q_addr + atom * (AT_Q_BYTES / 2)) + (uint64_t)(sub * 2);
+        const uint64_t bd = sdesc_kmajor_sw128(k_addr + atom * (AT_K_BYTES / 2)) + (uint64_t)(sub * 2);
+        umma_f16<1>(tmem + 256 * x + half * (AT_BN / 2), ad, bd, id_s64, kk > 0 ? 1u : 0u);
+      }
+    };
     auto issue_pv = [&](int x, int g, int half, bool first) {   // O_x += P_x V_g over keys [64 half, 64 half + 64)
       const uint32_t v_addr = smem_u32(sv + (g & 1) * AT_V_BYTES);
 #pragma unroll
@@ -657,6 +678,14 @@ __global__ void __launch_bounds__(AT_THREADS, 1) attn_fwd_kernel(const __grid_co
           const int gxx = x ? gx1 : gx0, sgx = x ? segx1 : segx0;
           // O_x of the previous segment must have been read by its epilogue
           if (i == 0 && sgx > 0) mbar_wait(&o_empty[x], (sgx - 1) & 1);
+#if AT_QK_SPLIT
+          if (more) {
+            mbar_wait(&s_loaded[x], gxx & 1);
+            tc_fence_after();
+            if (elect_one()) issue_qk_half(x, gg + 1, 1);
+            __syncwarp();
+          }
+#endif
           // the first half of P is consumed while the softmax still works on the second
           mbar_wait(&p_full[2 * x], gxx & 1);
           tc_fence_after();
@@ -666,7 +695,14 @@ __global__ void __launch_bounds__(AT_THREADS, 1) attn_fwd_kernel(const __grid_co
           tc_fence_after();
           if (elect_one()) {
             issue_pv(x, gg, 1, i == 0);
+#if AT_QK_SPLIT
+            if (more) {
+              issue_qk_half(x, gg + 1, 0);
+              umma_commit<1>(&s_full[x]);
+            }
+#else
             if (more) issue_qk(x, gg + 1);
+#endif
             else umma_commit<1>(&o_full[x]);
           }
           __syncwarp();
@@ -736,8 +772,10 @@ __global__ void __launch_bounds__(AT_THREADS, 1) attn_fwd_kernel(const __grid_co
       tc_fence_after();
       AT_PROF_MARK(1);
 #ifdef AT_MMA_ONLY   // timing diagnostic only: the MMA pipeline without softmax (wrong results)
-      if (lane == 0)
+      if (lane == 0) {
+        mbar_arrive(&s_loaded[x]);
         for (int hh = h * (2 / AT_CW); hh < (h + 1) * (2 / AT_CW); ++hh) mbar_arrive(&p_full[2 * x + hh]);
+      }
       continue;
 #endif
       // my S columns into registers with one TMEM wait; the max and exp passes read registers
@@ -745,6 +783,10 @@ __global__ void __launch_bounds__(AT_THREADS, 1) attn_fwd_kernel(const __grid_co
 #pragma unroll
       for (int c = 0; c < AT_NC / 32; ++c) tmem_ld_32x32b_x32(t_my_s + c * 32, *reinterpret_cast<uint32_t(*)[32]>(r + c * 32));
       tmem_ld_wait();
+      // S_x's high 64 columns may now be overwritten by the next block's QK
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&s_loaded[x]);
       AT_PROF_MARK(2);
       // packed fp32 pairs: one FFMA2 computes s*scale - m for two keys, one FADD2
       // accumulates two probabilities (the softmax warps are issue-bound)
