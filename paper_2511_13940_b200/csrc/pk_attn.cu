@@ -88,6 +88,10 @@ constexpr float AT_RESCALE_THRESHOLD = 8.0f;     // log2 units: P stays <= 2^8 b
 #ifndef AT_POLY_DEG
 #define AT_POLY_DEG 3                            // degree of the FMA-pipe 2^f polynomial
 #endif
+#ifndef AT_PQ
+#define AT_PQ 2          // P published to the MMA warp in AT_PQ parts per 128-key block (2 or 4)
+#endif
+static_assert(AT_PQ == 2 || AT_PQ == 4, "P parts");
 #ifndef AT_QK_SPLIT
 #define AT_QK_SPLIT 0    // 1: next block's QK in two N = 64 halves, the high one ahead of PV — measured
 #endif                   // 25 % more cycles at the base clock (each half re-reads Q: QK then asks
@@ -309,8 +313,8 @@ __global__ void __launch_bounds__(AT_THREADS, 1) attn_fwd_kernel(const __grid_co
   uint64_t* v_full = k_empty + AT_KSTAGES;      // [2]
   uint64_t* v_empty = v_full + 2;               // [2]
   uint64_t* s_full = v_empty + 2;               // [2] per tile
-  uint64_t* p_full = s_full + 2;                // [2 tiles][2 halves]: P of keys [64h, 64h+64) in TMEM
-  uint64_t* o_full = p_full + 4;                // [2] per tile
+  uint64_t* p_full = s_full + 2;                // [2 tiles][AT_PQ parts]: P of keys [128q/PQ, 128(q+1)/PQ) in TMEM
+  uint64_t* o_full = p_full + 2 * AT_PQ;        // [2] per tile
   uint64_t* o_empty = o_full + 2;               // [2] per tile: the epilogue has read O
   uint64_t* s_loaded = o_empty + 2;             // [2] per tile: S is in the softmax warps' registers
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(s_loaded + 2);
@@ -399,7 +403,7 @@ __global__ void __launch_bounds__(AT_THREADS, 1) attn_fwd_kernel(const __grid_co
     for (int i = 0; i < 2; ++i) {
       mbar_init(&v_full[i], 1); mbar_init(&v_empty[i], 1);
       mbar_init(&s_full[i], 1); mbar_init(&o_full[i], 1);
-      mbar_init(&p_full[2 * i], 4); mbar_init(&p_full[2 * i + 1], 4);
+      for (int qq = 0; qq < AT_PQ; ++qq) mbar_init(&p_full[AT_PQ * i + qq], 4);
       mbar_init(&o_empty[i], 4 * AT_CW);
       mbar_init(&s_loaded[i], 4 * AT_CW);
     }
@@ -633,11 +637,11 @@ __global__ void __launch_bounds__(AT_THREADS, 1) attn_fwd_kernel(const __grid_co
         umma_f16<1>(tmem + 256 * x + half * (AT_BN / 2), ad, bd, id_s64, kk > 0 ? 1u : 0u);
       }
     };
-    auto issue_pv = [&](int x, int g, int half, bool first) {   // O_x += P_x V_g over keys [64 half, 64 half + 64)
+    auto issue_pv = [&](int x, int g, int part, bool first) {   // O_x += P_x V_g over keys of P part `part`
       const uint32_t v_addr = smem_u32(sv + (g & 1) * AT_V_BYTES);
 #pragma unroll
-      for (int k4 = 0; k4 < AT_BN / 32; ++k4) {
-        const int kk = half * (AT_BN / 32) + k4;
+      for (int k4 = 0; k4 < AT_BN / 16 / AT_PQ; ++k4) {
+        const int kk = part * (AT_BN / 16 / AT_PQ) + k4;
         const uint64_t bd = sdesc_mnmajor_sw128(v_addr + kk * 2048, AT_V_BYTES / 2, 1024);
         umma_f16_ts(tmem + 256 * x + 128, tmem + 256 * x + kk * 8, bd, id_o, (!first || kk > 0) ? 1u : 0u);
       }
@@ -686,15 +690,18 @@ __global__ void __launch_bounds__(AT_THREADS, 1) attn_fwd_kernel(const __grid_co
             __syncwarp();
           }
 #endif
-          // the first half of P is consumed while the softmax still works on the second
-          mbar_wait(&p_full[2 * x], gxx & 1);
-          tc_fence_after();
-          if (elect_one()) issue_pv(x, gg, 0, i == 0);
-          __syncwarp();
-          mbar_wait(&p_full[2 * x + 1], gxx & 1);
+          // the first parts of P are consumed while the softmax still works on the rest
+#pragma unroll
+          for (int qq = 0; qq + 1 < AT_PQ; ++qq) {
+            mbar_wait(&p_full[AT_PQ * x + qq], gxx & 1);
+            tc_fence_after();
+            if (elect_one()) issue_pv(x, gg, qq, i == 0);
+            __syncwarp();
+          }
+          mbar_wait(&p_full[AT_PQ * x + AT_PQ - 1], gxx & 1);
           tc_fence_after();
           if (elect_one()) {
-            issue_pv(x, gg, 1, i == 0);
+            issue_pv(x, gg, AT_PQ - 1, i == 0);
 #if AT_QK_SPLIT
             if (more) {
               issue_qk_half(x, gg + 1, 0);
@@ -773,8 +780,8 @@ __global__ void __launch_bounds__(AT_THREADS, 1) attn_fwd_kernel(const __grid_co
       AT_PROF_MARK(1);
 #ifdef AT_MMA_ONLY   // timing diagnostic only: the MMA pipeline without softmax (wrong results)
       if (lane == 0) {
-        mbar_arrive(&s_loaded[x]);
-        for (int hh = h * (2 / AT_CW); hh < (h + 1) * (2 / AT_CW); ++hh) mbar_arrive(&p_full[2 * x + hh]);
+        if (AT_QK_SPLIT) mbar_arrive(&s_loaded[x]);
+        for (int hh = h * (AT_PQ / AT_CW); hh < (h + 1) * (AT_PQ / AT_CW); ++hh) mbar_arrive(&p_full[AT_PQ * x + hh]);
       }
       continue;
 #endif
@@ -783,10 +790,12 @@ __global__ void __launch_bounds__(AT_THREADS, 1) attn_fwd_kernel(const __grid_co
 #pragma unroll
       for (int c = 0; c < AT_NC / 32; ++c) tmem_ld_32x32b_x32(t_my_s + c * 32, *reinterpret_cast<uint32_t(*)[32]>(r + c * 32));
       tmem_ld_wait();
+#if AT_QK_SPLIT
       // S_x's high 64 columns may now be overwritten by the next block's QK
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&s_loaded[x]);
+#endif
       AT_PROF_MARK(2);
       // packed fp32 pairs: one FFMA2 computes s*scale - m for two keys, one FADD2
       // accumulates two probabilities (the softmax warps are issue-bound)
@@ -807,11 +816,11 @@ __global__ void __launch_bounds__(AT_THREADS, 1) attn_fwd_kernel(const __grid_co
           pk[i2] = pack_bf16x2(p0, p1);
         }
       };
-      auto publish_half = [&](int hh) {                 // keys [64hh, 64hh+64) are in TMEM: release that half
+      auto publish_part = [&](int qq) {                 // P part qq is in TMEM: release it to the MMA warp
         tmem_st_wait();
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(&p_full[2 * x + hh]);
+        if (lane == 0) mbar_arrive(&p_full[AT_PQ * x + qq]);
       };
       auto rescale_o = [&](float alpha) {
 #pragma unroll 1
@@ -864,7 +873,8 @@ __global__ void __launch_bounds__(AT_THREADS, 1) attn_fwd_kernel(const __grid_co
         exp_chunk(c, nm2, pk, rs2);
         const int cg = h * (AT_NC / 32) + c;            // global 32-key chunk
         tmem_st_32x32b_x16(t_s + cg * 16, pk);          // packed P columns [16cg, 16cg+16)
-        if (cg & 1) publish_half(cg >> 1);
+        if constexpr (AT_PQ == 4) publish_part(cg);
+        else if (cg & 1) publish_part(cg >> 1);
       }
       float rs_lo, rs_hi;
       f2_unpack(f2_add(f2_add(rs2[0], rs2[1]), f2_add(rs2[2], rs2[3])), rs_lo, rs_hi);
@@ -1116,6 +1126,28 @@ PK_DEV void umma_f16_ts2(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc, uint3
       :: "r"(tmem_d), "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(accum) : "memory");
 }
 
+// Cross-CTA hand-offs of the pair kernel (P ready, O drained -> the leader's
+// MMA warp). AT2_RELAXED_ARRIVE=1: plain remote arrive (default .release.cta
+// semantics) and a plain wait, as CUTLASS's 2-SM pipelines do; 0: arrive
+// .release.cluster / wait .acquire.cluster.
+#ifndef AT2_RELAXED_ARRIVE
+#define AT2_RELAXED_ARRIVE 1
+#endif
+PK_DEV void mbar_arrive_remote_plain(uint64_t* bar, uint32_t cta) {
+  asm volatile(
+      "{\n\t.reg .b32 remAddr32;\n\t"
+      "mapa.shared::cluster.u32  remAddr32, %0, %1;\n\t"
+      "mbarrier.arrive.shared::cluster.b64  _, [remAddr32];\n\t}"
+      :: "r"(smem_u32(bar)), "r"(cta) : "memory");
+}
+#if AT2_RELAXED_ARRIVE
+#define AT2_ARRIVE_REMOTE mbar_arrive_remote_plain
+#define AT2_WAIT_REMOTE mbar_wait
+#else
+#define AT2_ARRIVE_REMOTE mbar_arrive_cluster
+#define AT2_WAIT_REMOTE mbar_wait_cluster
+#endif
+
 __global__ void __launch_bounds__(AT2_THREADS, 1) attn2_fwd_kernel(const __grid_constant__ AttnArgs a) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -1255,12 +1287,12 @@ __global__ void __launch_bounds__(AT2_THREADS, 1) attn2_fwd_kernel(const __grid_
         if (more) mbar_wait(&k_full[(gg + 1) % NS], ((gg + 1) / NS) & 1);
         for (int x = 0; x < 2; ++x) {
           // the previous item's O_x must have been drained in both CTAs
-          if (i == 0 && seg > 0) mbar_wait_cluster(&o_empty[x], (seg - 1) & 1);
-          mbar_wait_cluster(&p_full[2 * x], gg & 1);
+          if (i == 0 && seg > 0) AT2_WAIT_REMOTE(&o_empty[x], (seg - 1) & 1);
+          AT2_WAIT_REMOTE(&p_full[2 * x], gg & 1);
           tc_fence_after();
           if (elect_one()) issue_pv(x, gg, 0, i == 0);
           __syncwarp();
-          mbar_wait_cluster(&p_full[2 * x + 1], gg & 1);
+          AT2_WAIT_REMOTE(&p_full[2 * x + 1], gg & 1);
           tc_fence_after();
           if (elect_one()) {
             issue_pv(x, gg, 1, i == 0);
@@ -1299,7 +1331,7 @@ __global__ void __launch_bounds__(AT2_THREADS, 1) attn2_fwd_kernel(const __grid_
       mbar_wait(&s_full[x], gx & 1);
       tc_fence_after();
 #ifdef AT_MMA_ONLY   // timing diagnostic only: the MMA pipeline without softmax (wrong results)
-      if (lane == 0) { mbar_arrive_cluster(&p_full[2 * x], 0); mbar_arrive_cluster(&p_full[2 * x + 1], 0); }
+      if (lane == 0) { AT2_ARRIVE_REMOTE(&p_full[2 * x], 0); AT2_ARRIVE_REMOTE(&p_full[2 * x + 1], 0); }
       continue;
 #endif
       uint32_t r[AT_BN];
@@ -1355,7 +1387,7 @@ __global__ void __launch_bounds__(AT2_THREADS, 1) attn2_fwd_kernel(const __grid_
           tmem_st_wait();
           tc_fence_before();
           __syncwarp();
-          if (lane == 0) mbar_arrive_cluster(&p_full[2 * x + (c >> 1)], 0);
+          if (lane == 0) AT2_ARRIVE_REMOTE(&p_full[2 * x + (c >> 1)], 0);
         }
       }
       float rs_lo, rs_hi;
@@ -1376,7 +1408,7 @@ __global__ void __launch_bounds__(AT2_THREADS, 1) attn2_fwd_kernel(const __grid_
     }
     tc_fence_before();
     __syncwarp();
-    if (lane == 0) mbar_arrive_cluster(&o_empty[x], 0);   // the next item's PV may overwrite O_x
+    if (lane == 0) AT2_ARRIVE_REMOTE(&o_empty[x], 0);   // the next item's PV may overwrite O_x
     const int sq_idx = qt * AT_BM + row;
     const long long srow = ((long long)(b * a.H + h) * a.S_q + sq_idx);
     const float inv = (l > 0.f) ? 1.f / l : 0.f;
@@ -1437,12 +1469,21 @@ static int tmap_bshd(CUtensorMap* m, const void* p, int64_t B, int64_t S, int64_
 // Grid: one CTA per item when the items fill whole waves, else a persistent
 // stream-K grid of one CTA per SM sharing all key blocks evenly.
 static int launch_attn(AttnScratch& scr, int num_sms, AttnArgs& a, cudaStream_t st) {
-  // CTA-pair kernel (tuning hook for now): four query tiles per cluster
-  if (getenv("PK_ATTN_PAIR") && a.S_q % (4 * AT_BM) == 0) {
+  // CTA-pair kernel: four query tiles per cluster, each SM reads 25 % less
+  // smem per QK step and TMA-writes half the K/V, 2-5 % faster than the
+  // single-CTA kernel when its persistent clusters fill whole waves (it has no
+  // split tail); PK_ATTN_PAIR=1 / 0 forces it on / off (tuning and test hook)
+  const int items2 = a.S_q % (4 * AT_BM) == 0 ? a.B * a.H * (a.S_q / (4 * AT_BM)) : 0;
+  int sms = num_sms;
+  if (const char* e = getenv("PK_ATTN_SMS")) sms = std::max(2, atoi(e));   // tuning / test hook
+  const int clusters = sms / 2;
+  const double eff2 = items2 > 0 ? (double)items2 / ((double)((items2 + clusters - 1) / clusters) * clusters) : 0.0;
+  bool use_pair = items2 > 0 && eff2 >= 0.95 && !getenv("PK_ATTN_FORCE_SPLIT");
+  if (const char* e = getenv("PK_ATTN_PAIR")) use_pair = items2 > 0 && atoi(e) != 0;
+  if (use_pair) {
     PK_TRY(ensure_smem_attr((const void*)attn2_fwd_kernel, AT2_SMEM));
     cudaLaunchConfig_t cfg = {};
-    const int items2 = a.B * a.H * (a.S_q / (4 * AT_BM));
-    cfg.gridDim = dim3(2 * std::min(items2, num_sms / 2), 1, 1);     // persistent clusters
+    cfg.gridDim = dim3(2 * std::min(items2, clusters), 1, 1);     // persistent clusters
     cfg.blockDim = dim3(AT2_THREADS, 1, 1);
     cfg.dynamicSmemBytes = AT2_SMEM;
     cfg.stream = st;
@@ -1459,8 +1500,6 @@ static int launch_attn(AttnScratch& scr, int num_sms, AttnArgs& a, cudaStream_t 
   PK_TRY(ensure_smem_attr((const void*)attn_fwd_kernel<false>, AT_SMEM));
   const int items = a.B * a.H * ((a.S_q / AT_BM + 1) / 2);
   const int nblk = a.S_kv / AT_BN;
-  int sms = num_sms;
-  if (const char* e = getenv("PK_ATTN_SMS")) sms = std::max(1, atoi(e));   // tuning / test hook
   // split the partial last wave when the items are long enough for the
   // partial-state write and merge to pay (measured: not at 32 key blocks)
   int min_blocks = 64;

@@ -132,9 +132,10 @@ def test_stream_k_more_ctas_than_tail_blocks(monkeypatch):
 @pytest.mark.parametrize("B,Sq,Skv,H", [(1, 512, 512, 1), (1, 1024, 2048, 2), (2, 512, 1024, 3), (1, 512, 128, 1),
                                          (2, 512, 384, 48), (1, 2048, 1024, 16)])
 def test_cta_pair_kernel_matches_oracle(monkeypatch, B, Sq, Skv, H):
-    """The cta_group::2 attention kernel (PK_ATTN_PAIR=1): four query tiles
-    per cluster, K and V halves split across the pair, persistent clusters
-    (96 items over 74 clusters: a second round; one key block; 16 heads)."""
+    """The cta_group::2 attention kernel (forced with PK_ATTN_PAIR=1): four
+    query tiles per cluster, K and V halves split across the pair, persistent
+    clusters (96 items over 74 clusters: a second round; one key block; 16
+    heads)."""
     pk = _pk()
     monkeypatch.setenv("PK_ATTN_PAIR", "1")
     g = torch.Generator(device="cuda").manual_seed(Sq + Skv + H)
@@ -147,3 +148,25 @@ def test_cta_pair_kernel_matches_oracle(monkeypatch, B, Sq, Skv, H):
     ref_o, ref_l = oracle.attention_fwd(npy(q), npy(k), npy(v), 128 ** -0.5)
     assert np.abs(npy(o) - ref_o).max() <= 2e-2
     assert np.abs(lse.cpu().numpy() - ref_l).max() <= 1e-3 * max(1.0, np.abs(ref_l).max())
+
+
+@pytest.mark.parametrize("B,Sq,Skv,H", [(2, 512, 256, 37), (1, 1024, 384, 74)])
+def test_attention_auto_pair_matches_single_and_oracle(monkeypatch, B, Sq, Skv, H):
+    """Shapes whose four-tile items fill whole waves of 74 clusters take the
+    CTA-pair kernel by default; it matches the oracle and the single-CTA
+    kernel (PK_ATTN_PAIR=0) to within bf16 output rounding."""
+    pk = _pk()
+    g = torch.Generator(device="cuda").manual_seed(B * Sq + H)
+    q = torch.randn(B, Sq, H, 128, device="cuda", generator=g).bfloat16()
+    k = torch.randn(B, Skv, H, 128, device="cuda", generator=g).bfloat16()
+    v = torch.randn(B, Skv, H, 128, device="cuda", generator=g).bfloat16()
+    o, lse = pk.attention(q, k, v)
+    monkeypatch.setenv("PK_ATTN_PAIR", "0")
+    o1, lse1 = pk.attention(q, k, v)
+    torch.cuda.synchronize()
+    npy = lambda t: t.float().cpu().numpy()
+    ref_o, ref_l = oracle.attention_fwd(npy(q), npy(k), npy(v), 128 ** -0.5)
+    for oo, ll in ((o, lse), (o1, lse1)):
+        assert np.abs(npy(oo) - ref_o).max() <= 2e-2
+        assert np.abs(ll.cpu().numpy() - ref_l).max() <= 1e-3 * max(1.0, np.abs(ref_l).max())
+    assert np.abs(npy(o) - npy(o1)).max() <= 8e-3
