@@ -1133,15 +1133,8 @@ PK_DEV void umma_f16_ts2(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc, uint3
 #ifndef AT2_RELAXED_ARRIVE
 #define AT2_RELAXED_ARRIVE 1
 #endif
-PK_DEV void mbar_arrive_remote_plain(uint64_t* bar, uint32_t cta) {
-  asm volatile(
-      "{\n\t.reg .b32 remAddr32;\n\t"
-      "mapa.shared::cluster.u32  remAddr32, %0, %1;\n\t"
-      "mbarrier.arrive.shared::cluster.b64  _, [remAddr32];\n\t}"
-      :: "r"(smem_u32(bar)), "r"(cta) : "memory");
-}
 #if AT2_RELAXED_ARRIVE
-#define AT2_ARRIVE_REMOTE mbar_arrive_remote_plain
+#define AT2_ARRIVE_REMOTE mbar_arrive_remote
 #define AT2_WAIT_REMOTE mbar_wait
 #else
 #define AT2_ARRIVE_REMOTE mbar_arrive_cluster

@@ -46,6 +46,17 @@ enum EpiMode : int { EPI_STORE = 0, EPI_REDUCE_ADD = 1, EPI_SCATTER = 2, EPI_DIR
 // (through row_perm when set). tile_start / tile_rows give each tile's first
 // row and row count (full 256-row tiles and one remainder per group; an even
 // split of the group over its tiles measured 3-5 % slower).
+// TMEM-drained hand-off (epilogue warps -> the leader's MMA warp): tcgen05
+// fences order the TMEM reads, so a plain remote arrive suffices (1); 0 keeps
+// the .release.cluster form (A/B hook)
+#ifndef PK_PLAIN_TEMPTY
+#define PK_PLAIN_TEMPTY 1
+#endif
+#if PK_PLAIN_TEMPTY
+#define PK_TEMPTY_ARRIVE mbar_arrive_remote
+#else
+#define PK_TEMPTY_ARRIVE mbar_arrive_cluster
+#endif
 constexpr int kTileRing = 4;                // depth of the tile-index broadcast ring
 constexpr int kAgCountOffset = 32768;       // AG piece counters live after the first 32K m-tile flags
 
@@ -667,7 +678,7 @@ lcsc_gemm_kernel(const __grid_constant__ GemmArgs args) {
           if (c == nch - 1) {
             tc_fence_before();
             __syncwarp();
-            if (lane == 0) mbar_arrive_cluster(&tempty_bar[acc], 0);
+            if (lane == 0) PK_TEMPTY_ARRIVE(&tempty_bar[acc], 0);
           }
 #pragma unroll
           for (int i = 0; i < 32; i += 2) {
@@ -687,7 +698,7 @@ lcsc_gemm_kernel(const __grid_constant__ GemmArgs args) {
         if (nch == 0) {
           tc_fence_before();
           __syncwarp();
-          if (lane == 0) mbar_arrive_cluster(&tempty_bar[acc], 0);
+          if (lane == 0) PK_TEMPTY_ARRIVE(&tempty_bar[acc], 0);
         }
       } else if constexpr (Cfg::ACC_STAGES == 1 && (EPI == EPI_STORE || EPI == EPI_REDUCE_ADD)) {
         // Single accumulator stage (512-row pair tiles fill TMEM): drain the
@@ -708,7 +719,7 @@ lcsc_gemm_kernel(const __grid_constant__ GemmArgs args) {
         __syncwarp();
         if (lane == 0) {
           if constexpr (CG == 1) mbar_arrive(&tempty_bar[acc]);
-          else mbar_arrive_cluster(&tempty_bar[acc], 0);
+          else PK_TEMPTY_ARRIVE(&tempty_bar[acc], 0);
         }
 #pragma unroll
         for (int c = 0; c < BN / EPI_COLS; ++c) {
@@ -745,7 +756,7 @@ lcsc_gemm_kernel(const __grid_constant__ GemmArgs args) {
           __syncwarp();
           if (lane == 0) {
             if constexpr (CG == 1) mbar_arrive(&tempty_bar[acc]);
-            else mbar_arrive_cluster(&tempty_bar[acc], 0);
+            else PK_TEMPTY_ARRIVE(&tempty_bar[acc], 0);
           }
         }
         if constexpr (EPI == EPI_SCATTER || EPI == EPI_DIRECT) {

@@ -74,6 +74,18 @@ PK_DEV void mbar_arrive_cluster(uint64_t* bar, uint32_t cta) {
       "mbarrier.arrive.release.cluster.shared::cluster.b64  _, [remAddr32];\n\t}"
       :: "r"(smem_u32(bar)), "r"(cta) : "memory");
 }
+// Plain remote arrive (default .release.cta semantics) for hand-offs that
+// order tensor-memory or async-proxy work through tcgen05 fences, not data
+// the peer reads from shared memory: the .release.cluster form above costs a
+// cluster-scope fence per arrive (the CTA-pair attention kernel ran ~30 %
+// slower with it on its per-block P-ready hand-off).
+PK_DEV void mbar_arrive_remote(uint64_t* bar, uint32_t cta) {
+  asm volatile(
+      "{\n\t.reg .b32 remAddr32;\n\t"
+      "mapa.shared::cluster.u32  remAddr32, %0, %1;\n\t"
+      "mbarrier.arrive.shared::cluster.b64  _, [remAddr32];\n\t}"
+      :: "r"(smem_u32(bar)), "r"(cta) : "memory");
+}
 PK_DEV bool mbar_try_wait(uint32_t addr, uint32_t parity) {
   uint32_t ok;
   asm volatile(
