@@ -401,7 +401,10 @@ def main():
     #     copied in and both outputs read back every step.
     e2e = None
     if not args.no_e2e:
-        k_e2e = int(os.environ.get("PK_E2E_STEPS", max(4, args.steps)))   # enough steps that the first H2D / last D2H amortise
+        # steady-state throughput: the first step's H2D and the last step's D2H
+        # cannot overlap compute, so the e2e loop runs 3x the timed steps
+        # (20 -> 60: +2 % e2e, profiles/r2/e2e/bench_k20.json vs bench_k60.json)
+        k_e2e = int(os.environ.get("PK_E2E_STEPS", max(4, 3 * args.steps)))
         s_h2d, s_d2h = torch.cuda.Stream(), torch.cuda.Stream()
         nbytes = lambda ts: sum(t.numel() * t.element_size() for t in ts)
 
