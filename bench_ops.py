@@ -250,7 +250,7 @@ def local(args, out):
         for t_ in ash:
             t_.copy_(torch.randn_like(t_, dtype=torch.float32).bfloat16())
         ms = timeit(ranks(comms, lambda r, c, s: pk.all_gather_gemm(c, ash[r], bsh[r], out=cs[r], stream=s)), iters=5)
-        emit(out, **tensor_line(f"ag_gemm_local{world}", 2 * S ** 3, ms, shape=[S, S, S], mode="inter_sm"))
+        emit(out, **tensor_line(f"ag_gemm_local{world}", 2 * S ** 3, ms, shape=[S, S, S], mode="auto"))
         ars = [torch.randn(S, S // world, device=dev).bfloat16() for _ in comms]
         brs = [torch.randn(S, S // world, device=dev).bfloat16() for _ in comms]
         ors = [c.empty((S // world, S)) for c in comms]

@@ -181,9 +181,10 @@ PK_API int pk_gemm(const pk_tensor* a, const pk_tensor* b, pk_tensor* c,
 
 /* AG-GEMM: C_r[M, N/n] = AllGather_rows(A_r[M/n, K]) . B_r[N/n, K]^T.
  * a_gathered (nullable): if given, receives the rank-major gathered A[M,K]
- * (the reference's `ag` layout, workloads.py:603-609); the communicator CTAs
- * write it inside the kernel, so a call with a_gathered always runs the
- * inter-SM schedule. */
+ * (the reference's `ag` layout, workloads.py:603-609); the communicators
+ * write it inside the kernel, so a call with a_gathered runs a staged schedule
+ * (PK_INTER_SM: communicator CTAs; PK_HYBRID: communicator warps in every
+ * compute CTA; an intra-SM request becomes inter-SM). */
 PK_API int pk_ag_gemm(pk_comm* comm, const pk_tensor* a_shard, const pk_tensor* b,
                       pk_tensor* c, pk_tensor* a_gathered, const pk_sched* sched, void* stream);
 

@@ -108,6 +108,8 @@ struct GemmArgs {
   uint8_t* comm_dst;                      // local gathered buffer [M, K]
   long long comm_shard_bytes;             // bytes per shard (= rows_per_src * K * 2)
   int comm_copy_local;                    // also copy the local shard into the gathered buffer
+  int comm_warps;                         // 1: warps 2 and 3 of every compute CTA are the communicators
+                                          //    (hybrid schedule: no dedicated SMs, 16 B register copies)
   // fused GEMM + all-reduce (GemmArPlan inter-SM, workloads.py:517-542)
   int ar_mode;                            // 1: signal each finished tile's owner; comm CTAs all-reduce owned tiles
   uint32_t* ar_tile_local;                // [tiles] partial-tile arrivals at this rank (as owner)
@@ -583,6 +585,64 @@ lcsc_gemm_kernel(const __grid_constant__ GemmArgs args) {
         }
         __syncwarp();
         if (++stage == Cfg::STAGES) { stage = 0; phase ^= 1; }
+      }
+    }
+    } else if (args.comm_warps && warp >= 2) {
+    // ========================================================= communicator warps (hybrid)
+    // Warps 2 and 3 of every compute CTA gather the peer shards into the local
+    // buffer beside the GEMM: the chunk / piece order and per-m-tile flags of
+    // the communicator CTAs below, but 16 B register copies (8 vectors in
+    // flight per lane) through the LSU instead of bulk copies through smem —
+    // the GEMM's stages fill the smem — so no SM is set aside.
+    const int ncomm = args.num_compute_clusters * CG * 2;
+    const int me = (cluster * CG + (int)cta_rank) * 2 + ((int)warp - 2);
+    const long long chunk_bytes = (long long)Cfg::TILE_M * args.K * 2;
+    const int chunks_per_shard = args.a_rows_per_src / Cfg::TILE_M;
+    const int nvis = (args.comm_copy_local ? args.world : args.world - 1) * chunks_per_shard;
+    constexpr int PIECE = 32768;
+    constexpr int kCommVec = 6;                        // 16 B vectors in flight per lane (the warpgroup holds 56 registers)
+    const int ppc = (int)((chunk_bytes + PIECE - 1) / PIECE);
+    const long long gtotal = (long long)nvis * ppc;
+    const int parts = ppc < ncomm ? ppc : ncomm;
+    uint32_t* piece_count = args.sync.flags + kAgCountOffset;
+    uint32_t ready_mask = 0;
+    bool failed = false;
+    for (long long g = me; g < gtotal && !failed; g += ncomm) {
+      const int vi = (int)(g / ppc);
+      const int src = (args.rank + 1 + vi / chunks_per_shard) % args.world;
+      const int mt = (src * args.a_rows_per_src) / Cfg::TILE_M + vi % chunks_per_shard;
+      const long long off = (g % ppc) * (long long)PIECE;
+      const long long bytes = min((long long)PIECE, chunk_bytes - off);
+      if (src != args.rank && args.sync.ready_local != nullptr && !((ready_mask >> src) & 1)) {
+        int ok = 1;
+        if (lane == 0) ok = wait_geq(args.sync.ready_local + src, s_call[1], args.sync.err, args.sync.timeout_ns) ? 1 : 0;
+        ok = __shfl_sync(0xffffffffu, ok, 0);
+        if (!ok) { failed = true; break; }
+        ready_mask |= 1u << src;
+      }
+      const uint8_t* sp = args.comm_src[src] + (long long)(vi % chunks_per_shard) * chunk_bytes + off;
+      uint8_t* dp = args.comm_dst + (long long)mt * chunk_bytes + off;
+      for (int v0 = (int)lane * 16; v0 < (int)bytes; v0 += 32 * 16 * kCommVec) {
+        uint4 x[kCommVec];
+#pragma unroll
+        for (int u = 0; u < kCommVec; ++u)
+          if (v0 + u * 512 < (int)bytes) x[u] = ld_v4_cg(sp + v0 + u * 512);
+#pragma unroll
+        for (int u = 0; u < kCommVec; ++u)
+          if (v0 + u * 512 < (int)bytes) st_v4(dp + v0 + u * 512, x[u]);
+      }
+      // my last piece of chunk vi is in: count it; the chunk's last share publishes the m-tile
+      if (g + ncomm >= gtotal || (g + ncomm) / ppc != vi) {
+        __syncwarp();
+        if (lane == 0) {
+          __threadfence();
+          if (atomicAdd(piece_count + mt, 1u) == (uint32_t)parts - 1) {
+            piece_count[mt] = 0;
+            __threadfence();
+            asm volatile("st.release.gpu.global.u32 [%0], %1;" :: "l"(args.sync.flags + mt), "r"(s_call[0]) : "memory");
+          }
+        }
+        __syncwarp();
       }
     }
     } else if (warp == 1) {

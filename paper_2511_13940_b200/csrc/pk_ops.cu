@@ -303,15 +303,26 @@ int ag_gemm(Comm* c, const pk_tensor* A, const pk_tensor* B, pk_tensor* C, pk_te
   }
   const int def_comm = ag_default_comm_sms(M, n_loc, K, n, c->num_sms);
   // compute pairs: all of this rank's SMs less the communicator share (as below)
+  const bool hybrid = (sched && sched->mode == PK_HYBRID) ||
+                      ((!sched || sched->mode == PK_SCHED_AUTO) && c->local_group && !(n_loc <= 256 && !AG));
   const int64_t ag_pairs = std::max(1, (sched && sched->num_sms > 0 ? std::min(sched->num_sms, c->num_sms) : c->num_sms) / 2 -
-                                           ((sched && sched->num_comm_sms > 0) ? sched->num_comm_sms : def_comm) / 2);
+                                           (hybrid ? 0 : ((sched && sched->num_comm_sms > 0) ? sched->num_comm_sms : def_comm) / 2));
   const Variant v = pick_variant(m_loc, K, sched, false, M, n_loc, ag_pairs, true);
   const int cg = v.cg;
   const int tile_m = 128 * v.am * cg;
   const int num_n = (int)(n_loc / v.bn);
   int mode = sched ? sched->mode : PK_SCHED_AUTO;
-  if (mode == PK_SCHED_AUTO) mode = (n_loc <= 256 && !AG) ? PK_INTRA_SM : PK_INTER_SM;
-  if (mode == PK_HYBRID) mode = PK_INTER_SM;   // HYBRID behaves like INTER_SM
+  // auto: intra-SM for thin B slabs; otherwise staged — communicator CTAs sized
+  // to the link on a real rank (the paper's TMA placement), communicator warps
+  // on an emulated rank, whose 148/n SMs cannot spare whole communicator SMs
+  // (emulated n = 4 at 8192^3: 1.16x vs 1.78x the GEMM alone,
+  // profiles/r2/s3/ag_modes.jsonl); a tuned table (tune.py) overrides both
+  if (mode == PK_SCHED_AUTO) mode = (n_loc <= 256 && !AG) ? PK_INTRA_SM : (c->local_group ? PK_HYBRID : PK_INTER_SM);
+  // HYBRID: the inter-SM gather (staged into a local buffer, per-m-tile flags)
+  // done by communicator warps inside the compute CTAs instead of dedicated
+  // ones — the paper's intra-SM placement of the communicator role
+  const bool comm_warps = mode == PK_HYBRID;
+  if (mode == PK_HYBRID) mode = PK_INTER_SM;
   // The gathered rows are materialised by the communicator CTAs, inside the
   // kernel and before this rank's done signal; an intra-SM launch would have to
   // copy peer shards after it (racing the peers' next writes into them).
@@ -345,7 +356,7 @@ int ag_gemm(Comm* c, const pk_tensor* A, const pk_tensor* B, pk_tensor* C, pk_te
     args.sync_ready_before_load = 1;
   } else {
     const int comm_sms = (sched && sched->num_comm_sms > 0) ? sched->num_comm_sms : def_comm;
-    comm_clusters = std::max(1, comm_sms / cg);
+    comm_clusters = comm_warps ? 0 : std::max(1, comm_sms / cg);
     // An emulated rank owns only num_sms/world SMs: scale the communicator
     // share down with it instead of starving the GEMM.
     if (c->local_group) comm_clusters = std::min(comm_clusters, std::max(1, clusters_total / 4));
@@ -373,6 +384,7 @@ int ag_gemm(Comm* c, const pk_tensor* A, const pk_tensor* B, pk_tensor* C, pk_te
     args.comm_dst = static_cast<uint8_t*>(gathered);
     args.comm_shard_bytes = (long long)shard_bytes;
     args.comm_copy_local = AG ? 1 : 0;
+    args.comm_warps = comm_warps ? 1 : 0;
   }
   int compute_clusters = std::min(tiles, clusters_total - comm_clusters);
   args.num_compute_clusters = compute_clusters;

@@ -67,7 +67,10 @@ def all_gather_gemm(comm, a_shard: torch.Tensor, b: torch.Tensor, out: torch.Ten
 
     a_shard is this rank's rows [M/n, K]; rows are gathered rank-major
     (workloads.py:603-609). If `a_gathered` [M, K] is given it receives the
-    gathered rows (the reference's `ag` layout).
+    gathered rows (the reference's `ag` layout). schedule mode: "intra_sm"
+    (the loader reads peer rows directly), "inter_sm" (communicator CTAs stage
+    the shards, `num_comm_sms` of them), "hybrid" (communicator warps inside
+    every compute CTA stage them; no SM set aside).
     """
     _require_cuda(a_shard, b)
     m = a_shard.shape[0] * comm.world

@@ -96,7 +96,7 @@ def test_gemm_strided_inputs_and_errors():
 
 
 @pytest.mark.parametrize("world", [1, 2, 4, 8])
-@pytest.mark.parametrize("mode", ["intra_sm", "inter_sm"])
+@pytest.mark.parametrize("mode", ["intra_sm", "inter_sm", "hybrid"])
 def test_ag_gemm_matches_oracle(world, mode):
     pk = _pk()
     rng = np.random.default_rng(world)
@@ -135,6 +135,33 @@ def test_ag_gemm_symmetric_input_and_repeat(world):
         exp = oracle.ag_gemm(a, b)
         for r in range(world):
             assert np.array_equal(outs[r].float().cpu().numpy(), bf16_round(exp[r])), (it, r)
+    for c in comms:
+        c.destroy()
+
+
+@pytest.mark.parametrize("world", [2, 4, 8])
+@pytest.mark.parametrize("with_gathered", [False, True])
+def test_ag_gemm_comm_warps_larger(world, with_gathered):
+    """Hybrid schedule (communicator warps in every compute CTA): several
+    512-row pair-tile chunks per shard, 32 KB pieces striped over all the
+    communicator warps, three back-to-back calls (flags and piece counters
+    re-arm); with and without the gathered-A output."""
+    pk = _pk()
+    rng = np.random.default_rng(40 + world)
+    m_loc, n_loc, K = 1024, 512, 640
+    comms = pk.local_group(world)
+    for it in range(3):
+        a = [ints(rng, (m_loc, K)) for _ in range(world)]
+        b = [ints(rng, (n_loc, K)) for _ in range(world)]
+        gathered = [torch.empty(m_loc * world, K, device="cuda", dtype=torch.bfloat16) for _ in range(world)] \
+            if with_gathered else [None] * world
+        outs = run_ranks(comms, lambda r, c, s: pk.all_gather_gemm(c, to_dev(a[r]), to_dev(b[r]), a_gathered=gathered[r],
+                                                                   schedule={"mode": "hybrid"}, stream=s))
+        exp = oracle.ag_gemm(a, b)
+        for r in range(world):
+            assert np.array_equal(outs[r].float().cpu().numpy(), bf16_round(exp[r])), (it, r)
+            if with_gathered:
+                assert np.array_equal(gathered[r].float().cpu().numpy(), oracle.gather_rows(a))
     for c in comms:
         c.destroy()
 

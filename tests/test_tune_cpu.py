@@ -23,8 +23,9 @@ def test_pick_best_ties_toward_fewer_comm_sms():
 
 def test_candidates_respect_sm_budget():
     c = tune.candidates("ag_gemm", 2, [2, 16, 80], sms_per_rank=74)
-    assert c[0] == {"mode": "intra_sm"}
-    assert [x["num_comm_sms"] for x in c[1:]] == [2, 16]
+    assert c[0] == {"mode": "intra_sm"} and c[1] == {"mode": "hybrid"}   # AG-GEMM: communicator warps too
+    assert [x["num_comm_sms"] for x in c[2:]] == [2, 16]
+    assert {"mode": "hybrid"} not in tune.candidates("gemm_rs", 2, [2])
     assert all(x["mode"] == "inter_sm" for x in tune.candidates("gemm_ar", 4))   # GEMM-AR is inter-SM only
 
 
