@@ -301,19 +301,19 @@ lcsc_gemm_kernel(const __grid_constant__ GemmArgs args) {
     return t;
   };
 
-  if (is_comm && args.ar_mode) {
-    // ========================================================= communicator: all-reduce
-    // Tiles owned by this rank (tile % world == rank) are split across the
-    // comm CTAs; each waits until every rank's partial of the tile landed, then
-    // reduces it in place on every rank: NVLS multimem.ld_reduce + multimem.st
-    // on the multicast VA, or P2P 16 B loads / fp32 fold in ascending rank
-    // order / 16 B stores (primitives.py:187-195, 237-261).
-    const int ncomm = (int)(gridDim.x / CG) - args.num_compute_clusters;
-    const int me = (cluster - args.num_compute_clusters) * CG + (int)cta_rank;
-    const int comm_ctas = ncomm * CG;
+  // ---------------------------------------------------------- all-reduce communicator
+  // Tiles owned by this rank (tile % world == rank; GEMM-RS: the tiles of this
+  // rank's row block) are split across the communicator units; a unit waits
+  // until every rank's partial of the tile landed, then reduces it in place on
+  // every rank: NVLS multimem.ld_reduce + multimem.st on the multicast VA, or
+  // P2P 16 B loads / fp32 fold in ascending rank order / 16 B stores
+  // (primitives.py:187-195, 237-261). A unit is a communicator CTA (inter-SM:
+  // `nthr` = its threads) or a communicator warp of a compute CTA (hybrid: 32
+  // lanes); `unit_sync` syncs the unit, `lead_ok` broadcasts its leader's wait
+  // result.
+  auto ar_reduce = [&](int me, int units, int tid, int nthr, auto&& unit_sync, auto&& lead_ok) {
     const int vec_per_row = BN * 2 / 16;                       // 16 B vectors per tile row
     const int vecs = Cfg::TILE_M * vec_per_row;
-    __shared__ int ok_s;
     const bool rs = args.ar_mode == 2;
     // AR: tiles t = rank, rank + world, ...; RS: the tiles of this rank's row block
     const int t_first = rs ? (args.rank * args.ar_owner_rows / Cfg::TILE_M) * num_n : args.rank;
@@ -321,16 +321,16 @@ lcsc_gemm_kernel(const __grid_constant__ GemmArgs args) {
     const int t_step = rs ? 1 : args.world;
     int j = 0;
     for (int t = t_first; t < t_end; t += t_step, ++j) {
-      if (j % comm_ctas != me) continue;
-      if (threadIdx.x == 0) {
-        ok_s = wait_geq(args.ar_tile_local + t, args.ar_expect, args.sync.err, args.sync.timeout_ns) ? 1 : 0;
+      if (j % units != me) continue;
+      int ok = 1;
+      if (tid == 0) {
+        ok = wait_geq(args.ar_tile_local + t, args.ar_expect, args.sync.err, args.sync.timeout_ns) ? 1 : 0;
         // all arrivals of this call are in: re-arm the counter for the next call
         // (no rank can start its next call before our done signal, sent later)
-        if (ok_s) args.ar_tile_local[t] = 0;
+        if (ok) args.ar_tile_local[t] = 0;
         fence_async_global();
       }
-      __syncthreads();
-      if (!ok_s) break;
+      if (!lead_ok(ok)) break;
       const long long base = (long long)(t / num_n) * Cfg::TILE_M * args.ar_ld + (long long)(t % num_n) * BN * 2;
       // RS: destination row inside the owner's [M / world, N] output
       const long long rs_base = rs ? ((long long)(t / num_n) * Cfg::TILE_M - (long long)args.rank * args.ar_owner_rows) *
@@ -341,27 +341,27 @@ lcsc_gemm_kernel(const __grid_constant__ GemmArgs args) {
       // reduced load per vector), P2P 4 (world loads per vector).
       constexpr int CU = 8;
       const int cu = args.ar_mc != nullptr ? CU : CU / 2;
-      for (int v0 = threadIdx.x; v0 < vecs; v0 += blockDim.x * cu) {
+      for (int v0 = tid; v0 < vecs; v0 += nthr * cu) {
         long long off[CU];
-        bool ok[CU];
+        bool okv[CU];
 #pragma unroll
         for (int u = 0; u < CU; ++u) {
-          const int v = v0 + u * (int)blockDim.x;
-          ok[u] = u < cu && v < vecs;
+          const int v = v0 + u * nthr;
+          okv[u] = u < cu && v < vecs;
           off[u] = base + (long long)(v / vec_per_row) * args.ar_ld + (v % vec_per_row) * 16;
         }
         auto rs_dst = [&](int u) {
-          const int v = v0 + u * (int)blockDim.x;
+          const int v = v0 + u * nthr;
           return args.rs_out + rs_base + (long long)(v / vec_per_row) * args.rs_ld + (v % vec_per_row) * 16;
         };
         if (args.ar_mc != nullptr) {
           uint32_t r[CU][4];
 #pragma unroll
           for (int u = 0; u < CU; ++u)
-            if (ok[u]) mm_ld_reduce_bf16x8(args.ar_mc + off[u], r[u]);      // reduce(): in-fabric reduction loads
+            if (okv[u]) mm_ld_reduce_bf16x8(args.ar_mc + off[u], r[u]);      // reduce(): in-fabric reduction loads
 #pragma unroll
           for (int u = 0; u < CU; ++u) {
-            if (!ok[u]) continue;
+            if (!okv[u]) continue;
             if (rs) st_v4(rs_dst(u), make_uint4(r[u][0], r[u][1], r[u][2], r[u][3]));
             else mm_st_v4(args.ar_mc + off[u], r[u]);                       // all_reduce(): + multicast write-back
           }
@@ -376,7 +376,7 @@ lcsc_gemm_kernel(const __grid_constant__ GemmArgs args) {
             uint4 x[CP];
 #pragma unroll
             for (int u = 0; u < CP; ++u)
-              if (ok[u]) x[u] = __ldcg(reinterpret_cast<const uint4*>(args.ar_buf_peer[d] + off[u]));
+              if (okv[u]) x[u] = __ldcg(reinterpret_cast<const uint4*>(args.ar_buf_peer[d] + off[u]));
 #pragma unroll
             for (int u = 0; u < CP; ++u) {
               const uint32_t w[4] = {x[u].x, x[u].y, x[u].z, x[u].w};
@@ -389,7 +389,7 @@ lcsc_gemm_kernel(const __grid_constant__ GemmArgs args) {
           }
 #pragma unroll
           for (int u = 0; u < CP; ++u) {
-            if (!ok[u]) continue;
+            if (!okv[u]) continue;
             const uint4 o = make_uint4(pack_bf16x2(acc[u][0], acc[u][1]), pack_bf16x2(acc[u][2], acc[u][3]),
                                        pack_bf16x2(acc[u][4], acc[u][5]), pack_bf16x2(acc[u][6], acc[u][7]));
             if (rs) st_v4(rs_dst(u), o);
@@ -397,13 +397,22 @@ lcsc_gemm_kernel(const __grid_constant__ GemmArgs args) {
           }
         }
       }
-      __syncthreads();
+      unit_sync();
     }
-    __syncthreads();
-    if (threadIdx.x == 0) {
+    unit_sync();
+    if (tid == 0) {
       fence_sys();
       for (int d = 0; d < args.world; ++d) signal_add(args.sync.done_peer[d] + args.rank, 1u);
     }
+  };
+
+  if (is_comm && args.ar_mode) {
+    // ========================================================= communicator CTAs: all-reduce
+    __shared__ int ok_s;
+    const int ncomm = (int)(gridDim.x / CG) - args.num_compute_clusters;
+    ar_reduce((cluster - args.num_compute_clusters) * CG + (int)cta_rank, ncomm * CG, (int)threadIdx.x,
+              (int)blockDim.x, [&]() { __syncthreads(); },
+              [&](int ok) { if (threadIdx.x == 0) ok_s = ok; __syncthreads(); return ok_s != 0; });
   } else if (is_comm) {
     // ========================================================= communicator
     // Inter-SM all-gather: copy every shard (peer VA -> smem ring -> local
@@ -586,6 +595,14 @@ lcsc_gemm_kernel(const __grid_constant__ GemmArgs args) {
         __syncwarp();
         if (++stage == Cfg::STAGES) { stage = 0; phase ^= 1; }
       }
+    }
+    } else if (args.comm_warps && warp >= 2 && args.ar_mode) {
+    // ========================================================= communicator warps (hybrid): all-reduce
+    // the fused GEMM + all-reduce with its owner-side reduction done by warps 2
+    // and 3 of every compute CTA instead of dedicated communicator CTAs
+    if constexpr (AM == 1) {
+      ar_reduce((cluster * CG + (int)cta_rank) * 2 + ((int)warp - 2), args.num_compute_clusters * CG * 2, (int)lane, 32,
+                [&]() { __syncwarp(); }, [&](int ok) { return __shfl_sync(0xffffffffu, ok, 0) != 0; });
     }
     } else if (args.comm_warps && warp >= 2) {
     // ========================================================= communicator warps (hybrid)

@@ -583,8 +583,13 @@ int gemm_ar(Comm* c, const pk_tensor* A, const pk_tensor* B, pk_tensor* O, const
   PK_TRY(tmap_c(&args.tmap_c[0], dst[c->rank], M, N, N));
   const int clusters_total = std::max(2, (sched && sched->num_sms > 0 ? std::min(sched->num_sms, c->num_sms) : c->num_sms) / 2);
   const int comm_sms = (sched && sched->num_comm_sms > 0) ? sched->num_comm_sms : 16;   // GemmArPlan default (workloads.py:425-426)
-  int comm_clusters = std::max(1, comm_sms / 2);
-  if (c->local_group) comm_clusters = std::min(comm_clusters, std::max(1, clusters_total / 4));
+  // HYBRID (and auto on an emulated rank, whose 148/n SMs cannot spare
+  // communicator SMs): the owner-side reduction runs in communicator warps of
+  // the compute CTAs
+  const bool comm_warps = (sched && sched->mode == PK_HYBRID) ||
+                          ((!sched || sched->mode == PK_SCHED_AUTO) && c->local_group && !(sched && sched->num_comm_sms > 0));
+  int comm_clusters = comm_warps ? 0 : std::max(1, comm_sms / 2);
+  if (c->local_group && !comm_warps) comm_clusters = std::min(comm_clusters, std::max(1, clusters_total / 4));
   if (comm_clusters >= clusters_total) return fail(PK_ERR_INVALID, "gemm_ar: num_comm_sms leaves no compute SMs");
   const int compute_clusters = std::min(tiles, clusters_total - comm_clusters);
   args.num_compute_clusters = compute_clusters;
@@ -598,9 +603,10 @@ int gemm_ar(Comm* c, const pk_tensor* A, const pk_tensor* B, pk_tensor* O, const
   args.ar_mc = static_cast<uint8_t*>(mc);
   args.ar_ld = N * 2;
   args.ar_expect = (uint32_t)(n * 4 * 2);                          // every rank's 4 epilogue warps x 2 CTAs per tile
-  args.sync_done_wait = 1;                                         // block 0 waits for every rank's comm CTAs
+  args.sync_done_wait = 1;                                         // block 0 waits for every rank's communicators
+  args.comm_warps = comm_warps ? 1 : 0;
   CallRef call;
-  PK_TRY(begin_call(c, 1, 0, (uint32_t)(comm_clusters * 2), st, &call));
+  PK_TRY(begin_call(c, 1, 0, (uint32_t)(comm_warps ? compute_clusters * 2 * 2 : comm_clusters * 2), st, &call));
   fill_sync(c, args.sync, call);
   args.sync.ready_local = nullptr;                                 // no ready handshake: tiles are flagged
   PK_TRY(launch_gemm_variant(v, EPI_STORE, args, (compute_clusters + comm_clusters) * 2, st));

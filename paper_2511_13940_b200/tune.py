@@ -110,11 +110,11 @@ def pick_best(rows: Iterable[tuple]) -> tuple:
 
 def candidates(op: str, world: int, comm_sms: Iterable[int] = DEFAULT_COMM_SMS,
                sms_per_rank: int = 148) -> list[dict]:
-    """Intra-SM (where the op has one), the AG-GEMM's hybrid schedule
-    (communicator warps inside the compute CTAs), plus an inter-SM sweep of
-    comm SM counts."""
+    """Intra-SM (where the op has one), the hybrid schedule of AG-GEMM and
+    GEMM-AR (communicator warps inside the compute CTAs), plus an inter-SM
+    sweep of comm SM counts."""
     out = [] if op == "gemm_ar" else [{"mode": "intra_sm"}]
-    if op == "ag_gemm":
+    if op in ("ag_gemm", "gemm_ar"):
         out.append({"mode": "hybrid"})
     for k in comm_sms:
         if 1 <= k < sms_per_rank:

@@ -30,7 +30,11 @@ def run_ranks(comms, fn):
 
 
 @pytest.mark.parametrize("world", [2, 3, 4, 8])
-def test_gemm_ar_exact(world):
+@pytest.mark.parametrize("schedule", [None, {"mode": "inter_sm", "num_comm_sms": 4}, {"mode": "hybrid"}],
+                         ids=["auto", "comm-ctas", "comm-warps"])
+def test_gemm_ar_exact(world, schedule):
+    """Auto (communicator warps on emulated ranks), dedicated communicator CTAs
+    and the hybrid schedule all reduce every tile exactly."""
     pk = _pk()
     rng = np.random.default_rng(world)
     M, N, K = 512, 512, 128
@@ -41,7 +45,7 @@ def test_gemm_ar_exact(world):
     da = [torch.from_numpy(x).cuda().bfloat16() for x in a]
     db = [torch.from_numpy(x).cuda().bfloat16() for x in b]
     torch.cuda.synchronize()
-    run_ranks(comms, lambda r, c, s: pk.gemm_all_reduce(c, da[r], db[r], out=outs[r], stream=s))
+    run_ranks(comms, lambda r, c, s: pk.gemm_all_reduce(c, da[r], db[r], out=outs[r], schedule=schedule, stream=s))
     exp = oracle.fold([x.astype(np.float64) @ y.T.astype(np.float64) for x, y in zip(a, b)])
     assert np.abs(exp).max() <= 256
     for r in range(world):

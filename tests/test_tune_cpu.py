@@ -26,7 +26,8 @@ def test_candidates_respect_sm_budget():
     assert c[0] == {"mode": "intra_sm"} and c[1] == {"mode": "hybrid"}   # AG-GEMM: communicator warps too
     assert [x["num_comm_sms"] for x in c[2:]] == [2, 16]
     assert {"mode": "hybrid"} not in tune.candidates("gemm_rs", 2, [2])
-    assert all(x["mode"] == "inter_sm" for x in tune.candidates("gemm_ar", 4))   # GEMM-AR is inter-SM only
+    ar = tune.candidates("gemm_ar", 4)                         # GEMM-AR: no intra-SM schedule
+    assert ar[0] == {"mode": "hybrid"} and all(x["mode"] == "inter_sm" for x in ar[1:])
 
 
 def test_table_lookup_nearest_shape(tmp_path):
