@@ -49,6 +49,9 @@ enum EpiMode : int { EPI_STORE = 0, EPI_REDUCE_ADD = 1, EPI_SCATTER = 2, EPI_DIR
 // TMEM-drained hand-off (epilogue warps -> the leader's MMA warp): tcgen05
 // fences order the TMEM reads, so a plain remote arrive suffices (1); 0 keeps
 // the .release.cluster form (A/B hook)
+#ifndef PK_EPI_SLEEP
+#define PK_EPI_SLEEP 0   // 1: epilogue warps sleep in the accumulator-full wait: +0.2 % at 16384^3
+#endif           // under the power cap, -0.9 % cycles at K = 2048 (profiles/r2/s3/gemm_sleep_*)
 #ifndef PK_PLAIN_TEMPTY
 #define PK_PLAIN_TEMPTY 1
 #endif
@@ -735,7 +738,11 @@ lcsc_gemm_kernel(const __grid_constant__ GemmArgs args) {
         __syncwarp();
         owners_ready |= 1u << dst;
       }
+#if PK_EPI_SLEEP
+      mbar_wait_sleep(&tfull_bar[acc], acc_phase);     // idle for the tile's whole main loop
+#else
       mbar_wait(&tfull_bar[acc], acc_phase);
+#endif
       tc_fence_after();
       const uint32_t t_lane = (uint32_t)(q * 32) << 16;
       if constexpr (EPI == EPI_TOKENS_T) {

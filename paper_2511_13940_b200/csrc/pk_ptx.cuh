@@ -99,6 +99,20 @@ PK_DEV void mbar_wait(uint64_t* bar, uint32_t parity) {
   const uint32_t a = smem_u32(bar);
   while (!mbar_try_wait(a, parity)) {}
 }
+// Long waits (a role idle for a whole tile's main loop): try_wait with a
+// suspend-time hint, so the waiting warps sleep in the barrier instead of
+// re-issuing the probe (hint in ns; the hardware may wake earlier).
+PK_DEV void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
+  const uint32_t a = smem_u32(bar);
+  uint32_t ok = 0;
+  while (!ok) {
+    asm volatile(
+        "{\n\t.reg .pred P1;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2, %3;\n\t"
+        "selp.b32 %0, 1, 0, P1;\n\t}"
+        : "=r"(ok) : "r"(a), "r"(parity), "r"(1000000u) : "memory");
+  }
+}
 // Wait with cluster-scope acquire: pairs with a peer CTA's
 // mbarrier.arrive.release.cluster that publishes data it stored into this
 // CTA's shared memory (st.shared::cluster) before arriving.
