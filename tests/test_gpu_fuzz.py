@@ -68,7 +68,7 @@ def test_fuzz_ag_rs_ar_one_group_many_calls():
             m_loc, n_loc, K = 128 * int(rng.integers(1, 5)), 256 * int(rng.integers(1, 3)), 64 * int(rng.integers(1, 4))
             A = [rng.integers(-4, 5, size=(m_loc, K)).astype(np.float32) for _ in range(world)]
             B = [rng.integers(-1, 2, size=(n_loc, K)).astype(np.float32) for _ in range(world)]
-            mode = ["intra_sm", "inter_sm"][int(rng.integers(0, 2))]
+            mode = ["intra_sm", "inter_sm", "hybrid"][int(rng.integers(0, 3))]
             da, db = [bf(x) for x in A], [bf(x) for x in B]
             outs = run_ranks(comms, lambda r, c, s: pk.all_gather_gemm(c, da[r], db[r], schedule={"mode": mode},
                                                                      stream=s))
@@ -86,7 +86,8 @@ def test_fuzz_ag_rs_ar_one_group_many_calls():
                 outs = run_ranks(comms, lambda r, c, s: pk.gemm_reduce_scatter(c, da[r], db[r], stream=s))
                 exp = oracle.gemm_rs(A, B)
             else:
-                outs = run_ranks(comms, lambda r, c, s: pk.gemm_all_reduce(c, da[r], db[r], stream=s))
+                sched = [None, {"mode": "inter_sm", "num_comm_sms": 2}, {"mode": "hybrid"}][int(rng.integers(0, 3))]
+                outs = run_ranks(comms, lambda r, c, s: pk.gemm_all_reduce(c, da[r], db[r], schedule=sched, stream=s))
                 tot = oracle.fold([x.astype(np.float64) @ y.T for x, y in zip(A, B)])
                 exp = [tot] * world
             for r in range(world):
@@ -133,9 +134,10 @@ def test_fuzz_ring_attention_shapes():
     pk = _pk()
     rng = np.random.default_rng(5 + SEED)
     for _ in range(4 * SCALE):
-        world = int(rng.integers(1, 5))
+        world = int(rng.integers(1, 9))
         B, H = int(rng.integers(1, 3)), int(rng.integers(1, 4))
         S_loc = 128 * int(rng.integers(1, 4))
+        sched = [None, {"mode": "inter_sm"}, {"stages": 2 * int(rng.integers(1, 5))}][int(rng.integers(0, 3))]
         comms = pk.local_group(world)
         g = torch.Generator(device="cuda").manual_seed(int(rng.integers(0, 1 << 30)))
         qs = [torch.randn(B, S_loc, H, 128, device="cuda", generator=g).bfloat16() for _ in range(world)]
@@ -144,7 +146,7 @@ def test_fuzz_ring_attention_shapes():
         outs = [(torch.empty_like(q), torch.empty(B, H, S_loc, device="cuda")) for q in qs]
         torch.cuda.synchronize()
         run_ranks(comms, lambda r, c, s: pk.ring_attention(c, qs[r], ks[r], vs[r], out=outs[r][0], lse=outs[r][1],
-                                                           stream=s))
+                                                           schedule=sched, stream=s))
         npy = lambda t: t.float().cpu().numpy()
         ro, rl = oracle.ring_attention([npy(x) for x in qs], [npy(x) for x in ks], [npy(x) for x in vs], 128 ** -0.5)
         for r in range(world):
@@ -152,3 +154,24 @@ def test_fuzz_ring_attention_shapes():
             assert np.abs(outs[r][1].cpu().numpy() - rl[r]).max() <= 1e-3 * max(1.0, np.abs(rl[r]).max())
         for c in comms:
             c.destroy()
+
+
+def test_fuzz_attention_kernels(monkeypatch):
+    """Single-GPU attention on random shapes through the CTA-pair kernel and the
+    single-CTA kernel (forced either way) against the oracle."""
+    pk = _pk()
+    rng = np.random.default_rng(17 + SEED)
+    for it in range(6 * SCALE):
+        B, H = int(rng.integers(1, 3)), int(rng.integers(1, 5))
+        Sq, Skv = 512 * int(rng.integers(1, 3)), 128 * int(rng.integers(1, 9))
+        monkeypatch.setenv("PK_ATTN_PAIR", str(it % 2))
+        g = torch.Generator(device="cuda").manual_seed(int(rng.integers(0, 1 << 30)))
+        q = torch.randn(B, Sq, H, 128, device="cuda", generator=g).bfloat16()
+        k = torch.randn(B, Skv, H, 128, device="cuda", generator=g).bfloat16()
+        v = torch.randn(B, Skv, H, 128, device="cuda", generator=g).bfloat16()
+        o, lse = pk.attention(q, k, v)
+        torch.cuda.synchronize()
+        npy = lambda t: t.float().cpu().numpy()
+        ro, rl = oracle.attention_fwd(npy(q), npy(k), npy(v), 128 ** -0.5)
+        assert np.abs(npy(o) - ro).max() <= 2e-2, (it, B, H, Sq, Skv)
+        assert np.abs(lse.cpu().numpy() - rl).max() <= 1e-3 * max(1.0, np.abs(rl).max()), (it, B, H, Sq, Skv)
