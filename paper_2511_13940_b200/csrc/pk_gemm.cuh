@@ -196,7 +196,7 @@ __global__ void __launch_bounds__(GemmCfg<CG, BN, AM>::NUM_THREADS, 1)
 lcsc_gemm_kernel(const __grid_constant__ GemmArgs args) {
   using Cfg = GemmCfg<CG, BN, AM>;
   static_assert(EPI != EPI_REDUCE_ADD_F32 || Cfg::EPI_NBUF == 2, "fp32 partials need the double-buffered epilogue");
-  static_assert(EPI != EPI_TOKENS_T || (CG == 2 && AM == 1 && BN == 256), "token tiles: 256-feature pair tiles");
+  static_assert(EPI != EPI_TOKENS_T || (CG == 2 && BN == 256), "token tiles: 256 (AM 1) or 512 (AM 2) features per pair tile");
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* smem_a = smem;
@@ -221,7 +221,7 @@ lcsc_gemm_kernel(const __grid_constant__ GemmArgs args) {
   const bool is_comm = cluster >= args.num_compute_clusters;
 
   const int num_m = args.num_m_tiles_dev ? *args.num_m_tiles_dev : args.M / Cfg::TILE_M;
-  const int num_n = args.N / BN;
+  const int num_n = args.N / (EPI == EPI_TOKENS_T ? BN * AM : BN);   // token tiles: AM x 256 features per tile
   const int num_tiles = num_m * num_n;
   const int num_kb = args.K / BLOCK_K;
 
@@ -554,7 +554,7 @@ lcsc_gemm_kernel(const __grid_constant__ GemmArgs args) {
       if constexpr (EPI == EPI_TOKENS_T) {
         // A operand: this CTA's 128 weight rows (features); B operand: its half
         // of the tile's tokens (the pair splits the MMA's N)
-        a_row = args.tile_group[mt] * args.N + nt * BN + (int)cta_rank * Cfg::BM;
+        a_row = args.tile_group[mt] * args.N + nt * BN * AM + (int)cta_rank * Cfg::BM;
         b_row = (args.tile_start ? args.tile_start[mt] : mt * Cfg::TILE_M) + (int)cta_rank * (tokens_n(args, mt) / CG);
       }
       if (args.a_wait_flag[src]) {
@@ -752,12 +752,12 @@ lcsc_gemm_kernel(const __grid_constant__ GemmArgs args) {
         // bytes of a token row)
         const int valid = args.tile_rows[mt];
         const int row0 = args.tile_start ? args.tile_start[mt] : mt * Cfg::TILE_M;
-        const int f0 = nt * BN + (int)cta_rank * Cfg::BM + q * 32;       // feature of lane 0
+        const int f0 = nt * BN * AM + (int)cta_rank * Cfg::BM + am * 128 + q * 32;   // feature of lane 0
         const int nch = (valid + 31) / 32;
         const bool odd = lane & 1;
         for (int c = 0; c < nch; ++c) {
           uint32_t v[32];
-          tmem_ld_32x32b_x32(tmem_base + t_lane + (uint32_t)(acc * Cfg::ACC_COLS + c * 32), v);
+          tmem_ld_32x32b_x32(tmem_base + t_lane + (uint32_t)(acc * Cfg::ACC_COLS + am * BN + c * 32), v);
           tmem_ld_wait();
           if (c == nch - 1) {
             tc_fence_before();

@@ -22,11 +22,22 @@
 namespace pk {
 
 int launch_gemm_grouped(const GemmArgs& args, int grid_ctas, cudaStream_t st);   // pk_ops.cu
-int launch_gemm_tokens(const GemmArgs& args, int grid_ctas, cudaStream_t st);    // pk_ops.cu
+int launch_gemm_tokens(const GemmArgs& args, int grid_ctas, cudaStream_t st, int am);   // pk_ops.cu
 
 // Token tiles (EPI_TOKENS_T) unless PK_GROUPED_PADDED is set (A/B hook: the
 // 256-row padded tiles with the weights as the B operand)
 static bool use_token_tiles() { return getenv("PK_GROUPED_PADDED") == nullptr; }
+// Feature rows per CTA of a token tile: 128 (default) or, with PK_TOKENS_AM=2,
+// 256 (two 128-row accumulators, a 512-feature pair tile: every token row is
+// loaded once per 512 features instead of per 256). Measured at the MoE GEMM1
+// shape (profiles/r2/s3/tokens_*): AM 2 moves 22 % fewer bytes L2 -> SM
+// (6.7 vs 8.6 GB) but takes 4-14 % more cycles (its single accumulator stage
+// leaves the epilogue unhidden and half as many tiles fill the waves worse),
+// so the kernel is not bandwidth-bound there and AM 1 stays.
+static int tokens_am(int64_t N) {
+  if (const char* e = getenv("PK_TOKENS_AM")) return atoi(e) == 2 && N % 512 == 0 ? 2 : 1;
+  return 1;
+}
 
 constexpr int kGrpTile = 256;          // pair tile rows (CG = 2, AM = 1)
 constexpr int kMaxGroups = 1024;
@@ -187,8 +198,9 @@ int grouped_gemm(const pk_tensor* A, const pk_tensor* group, const pk_tensor* W,
   if (use_token_tiles()) {
     // weights as the A operand (256 features per pair tile), the sorted rows
     // as the B operand, outputs scattered back through row_perm
-    PK_TRY(make_tmap_2d(&args.tmap_a[0], W->ptr, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, (int64_t)G * N, K, K, 128, BLOCK_K,
-                        CU_TENSOR_MAP_SWIZZLE_128B));
+    const int am = tokens_am(N);
+    PK_TRY(make_tmap_2d(&args.tmap_a[0], W->ptr, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, (int64_t)G * N, K, K, 128 * am,
+                        BLOCK_K, CU_TENSOR_MAP_SWIZZLE_128B));
     PK_TRY(make_tmap_2d(&args.tmap_b, p.a_sorted, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, R_pad, K, K, 128, BLOCK_K,
                         CU_TENSOR_MAP_SWIZZLE_128B));
     PK_TRY(make_tmap_2d(&args.tmap_b16, p.a_sorted, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, R_pad, K, K, 16, BLOCK_K,
@@ -205,7 +217,7 @@ int grouped_gemm(const pk_tensor* A, const pk_tensor* group, const pk_tensor* W,
     args.raster_group = 1;                 // the feature tiles of one token tile back to back
     args.y = static_cast<uint8_t*>(Y->ptr);
     args.y_ld = ldY * 2;
-    return launch_gemm_tokens(args, clusters * 2, st);
+    return launch_gemm_tokens(args, clusters * 2, st, am);
   }
   PK_TRY(make_tmap_2d(&args.tmap_a[0], p.a_sorted, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, R_pad, K, K, 128, BLOCK_K,
                       CU_TENSOR_MAP_SWIZZLE_128B));
@@ -259,8 +271,9 @@ int grouped_gemm_planned(const pk_tensor* A, const pk_tensor* plan, const pk_ten
   if (plan->shape[0] >= 2 + 3 * max_tiles && use_token_tiles()) {
     // the plan carries every tile's rows and first row (pk_moe_dispatch_ex
     // with a plan of >= 2 + 3 * rows/256 entries): token tiles, no padded work
-    PK_TRY(make_tmap_2d(&args.tmap_a[0], W->ptr, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, W->shape[0] * N, K, K, 128, BLOCK_K,
-                        CU_TENSOR_MAP_SWIZZLE_128B));
+    const int am = tokens_am(N);
+    PK_TRY(make_tmap_2d(&args.tmap_a[0], W->ptr, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, W->shape[0] * N, K, K, 128 * am,
+                        BLOCK_K, CU_TENSOR_MAP_SWIZZLE_128B));
     PK_TRY(make_tmap_2d(&args.tmap_b, A->ptr, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, R, K, ldA, 128, BLOCK_K,
                         CU_TENSOR_MAP_SWIZZLE_128B));
     PK_TRY(make_tmap_2d(&args.tmap_b16, A->ptr, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, R, K, ldA, 16, BLOCK_K,
@@ -276,7 +289,7 @@ int grouped_gemm_planned(const pk_tensor* A, const pk_tensor* plan, const pk_ten
     args.raster_group = 1;
     args.y = static_cast<uint8_t*>(Y->ptr);
     args.y_ld = ldY * 2;
-    return launch_gemm_tokens(args, clusters * 2, st);
+    return launch_gemm_tokens(args, clusters * 2, st, am);
   }
   PK_TRY(make_tmap_2d(&args.tmap_a[0], A->ptr, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, R, K, ldA, 128, BLOCK_K,
                       CU_TENSOR_MAP_SWIZZLE_128B));

@@ -80,7 +80,8 @@ int launch_gemm_grouped(const GemmArgs& args, int grid_ctas, cudaStream_t st) {
   return launch_lcsc<2, 256, 1, EPI_SCATTER>(args, grid_ctas, st);
 }
 
-int launch_gemm_tokens(const GemmArgs& args, int grid_ctas, cudaStream_t st) {
+int launch_gemm_tokens(const GemmArgs& args, int grid_ctas, cudaStream_t st, int am) {
+  if (am == 2) return launch_lcsc<2, 256, 2, EPI_TOKENS_T>(args, grid_ctas, st);
   return launch_lcsc<2, 256, 1, EPI_TOKENS_T>(args, grid_ctas, st);
 }
 
@@ -93,7 +94,7 @@ int preload_gemm() {
 #define PK_L(CG, AM, E) PK_CUDA(cudaFuncGetAttributes(&fa, lcsc_gemm_kernel<CG, 256, AM, E>));
   PK_L(2, 2, EPI_STORE) PK_L(2, 2, EPI_REDUCE_ADD) PK_L(2, 1, EPI_DIRECT) PK_L(2, 1, EPI_STORE) PK_L(2, 1, EPI_REDUCE_ADD)
   PK_L(1, 1, EPI_STORE) PK_L(1, 1, EPI_REDUCE_ADD) PK_L(2, 1, EPI_SCATTER) PK_L(2, 1, EPI_REDUCE_ADD_F32)
-  PK_L(2, 1, EPI_TOKENS_T)
+  PK_L(2, 1, EPI_TOKENS_T) PK_L(2, 2, EPI_TOKENS_T)
 #undef PK_L
   PK_CUDA(cudaFuncGetAttributes(&fa, lcsc_gemm_kernel<1, 128, 1, EPI_STORE>));
   PK_CUDA(cudaFuncGetAttributes(&fa, lcsc_gemm_kernel<2, 128, 1, EPI_STORE>));

@@ -19,7 +19,8 @@ def bf16_round(x):
     return torch.from_numpy(np.asarray(x, dtype=np.float32)).to(torch.bfloat16).float().numpy()
 
 
-@pytest.mark.parametrize("R,G,N,K", [(1, 1, 256, 64), (300, 3, 256, 128), (2048, 8, 512, 256), (5000, 16, 256, 192)])
+@pytest.mark.parametrize("R,G,N,K", [(1, 1, 256, 64), (300, 3, 256, 128), (2048, 8, 512, 256), (5000, 16, 256, 192),
+                                     (3000, 5, 1536, 128)])
 def test_grouped_gemm_exact(R, G, N, K):
     pk = _pk()
     rng = np.random.default_rng(R + G)
@@ -110,12 +111,15 @@ def test_moe_dispatch_gemm_combine_pipeline(world):
 _EDGE_COUNTS = [1, 15, 16, 17, 31, 32, 33, 47, 63, 64, 65, 127, 128, 129, 200, 255, 256, 257, 300, 511, 512, 513]
 
 
-@pytest.mark.parametrize("padded", [False, True])
-def test_grouped_gemm_token_tile_boundaries(monkeypatch, padded):
-    """Every group size around the token-tile edges, exact; the 256-row padded
-    tiles (PK_GROUPED_PADDED) must agree bit for bit."""
-    if padded:
+@pytest.mark.parametrize("variant", ["tokens_256_features", "tokens_512_features", "padded"])
+def test_grouped_gemm_token_tile_boundaries(monkeypatch, variant):
+    """Every group size around the token-tile edges, exact: token tiles of 256
+    features per pair tile (the default), of 512 (PK_TOKENS_AM=2), and the
+    256-row padded tiles (PK_GROUPED_PADDED)."""
+    if variant == "padded":
         monkeypatch.setenv("PK_GROUPED_PADDED", "1")
+    if variant == "tokens_512_features":
+        monkeypatch.setenv("PK_TOKENS_AM", "2")
     pk = _pk()
     rng = np.random.default_rng(11)
     G, N, K = len(_EDGE_COUNTS), 512, 128
