@@ -139,7 +139,7 @@ def test_ag_gemm_symmetric_input_and_repeat(world):
         c.destroy()
 
 
-@pytest.mark.parametrize("world", [2, 4, 8])
+@pytest.mark.parametrize("world", [2, 3, 4, 8])
 @pytest.mark.parametrize("with_gathered", [False, True])
 def test_ag_gemm_comm_warps_larger(world, with_gathered):
     """Hybrid schedule (communicator warps in every compute CTA): several

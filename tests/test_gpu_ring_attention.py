@@ -67,7 +67,7 @@ def test_ring_attention_communicator_modes(world, schedule):
     run(world, 1, 512, 2, seed=11 + world, schedule=schedule)
 
 
-@pytest.mark.parametrize("world,stages", [(2, 4), (4, 4), (8, 4), (8, 6), (4, 16), (8, 2)])
+@pytest.mark.parametrize("world,stages", [(2, 4), (4, 4), (8, 4), (8, 6), (4, 16), (8, 2), (3, 4), (5, 4), (6, 6), (7, 0)])
 def test_ring_attention_unit_span(world, stages):
     """A work unit spans stages / 2 ring steps of an item (2P stage slots):
     fewer state merges; spans that do not divide n, and one span over the
