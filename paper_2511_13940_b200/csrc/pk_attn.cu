@@ -78,11 +78,15 @@ constexpr int AT_SMEM = 2 * AT_Q_BYTES + AT_KSTAGES * AT_K_BYTES + AT_VSTAGES * 
 // intra-SM ring communicator (warp 3 of each compute CTA): two pieces of smem
 // beside the Q / K / V stages (0: they do not fit this build's stages)
 constexpr int AT_RING_CBUF_OFF = 2 * AT_Q_BYTES + AT_KSTAGES * AT_K_BYTES + AT_VSTAGES * AT_V_BYTES + 512 + AT_RED_BYTES;
+#ifndef AT_RING_REGCOPY
+#define AT_RING_REGCOPY 0  // intra-SM communicators: bulk copies by warp 3 (0) or register copies by warps 2-3
+#endif                     // (1: measured alike in emulation, profiles/r2/s3/ring_regcopy.jsonl; bulk
+                           // copies keep more in flight per SM against NVLink latency on a real rank)
 #ifndef AT_RING_NBUF
 #define AT_RING_NBUF 2   // pieces of the intra-SM communicator's 32 KB of smem
 #endif
 constexpr int AT_RING_PIECE = (AT_SMEM + 32768 <= 232448 - 64) ? 32768 / AT_RING_NBUF : 0;
-constexpr int AT_SMEM_RING = AT_SMEM + AT_RING_NBUF * AT_RING_PIECE;
+constexpr int AT_SMEM_RING = AT_SMEM + (AT_RING_REGCOPY ? 0 : AT_RING_NBUF * AT_RING_PIECE);
 constexpr int AT_TMEM_COLS = 512;                // per tile: S (128, P aliased in its first 64) + O (128)
 constexpr float AT_RESCALE_THRESHOLD = 8.0f;     // log2 units: P stays <= 2^8 between rescales
 #ifndef AT_POLY_DEG
@@ -519,6 +523,66 @@ __global__ void __launch_bounds__(AT_THREADS, 1) attn_fwd_kernel(const __grid_co
     }
   };
   __shared__ __align__(8) uint64_t ring_cbar[8];
+  // The same pull with register copies (AT_RING_REGCOPY): warps 2 and 3 of
+  // every compute CTA move 16 B vectors through the LSU (4 in flight per lane)
+  // instead of bulk copies through smem, so the K/V TMA loads of the same SM
+  // never queue behind a communicator piece. `me` / `nc` count warps.
+  auto ring_pull_regs = [&](int me, int nc) {
+    constexpr long long PIECE = 16384;
+    constexpr int V = 4;
+    const int n = a.ring_steps;
+    const long long ppt = (a.shard_bytes + PIECE - 1) / PIECE;
+    const long long per_step = 2 * ppt;
+    const uint32_t ready_expect = call_get(a.call, 1);
+    bool ok = true;
+    for (int s = 1; s < n; ++s) {
+      const int src = (a.rank - s + n) % n;
+      int okl = 1;
+      if (lane == 0) {
+        if (s - nslots >= 1) okl = wait_geq(rc.units(span_of(s - nslots)), (uint32_t)items, a.err, a.timeout_ns) ? 1 : 0;
+        if (okl) okl = wait_geq(a.ready_local + src, ready_expect, a.err, a.timeout_ns) ? 1 : 0;
+      }
+      ok = ok && __shfl_sync(0xffffffffu, okl, 0) != 0;
+      uint8_t* dk = a.stage_k + (long long)(s % nslots) * a.shard_bytes;
+      uint8_t* dv = a.stage_v + (long long)(s % nslots) * a.shard_bytes;
+#ifndef AT_RING_NOCOMM
+      for (long long q = me; ok && q < per_step; q += nc) {
+        const bool isv = q >= ppt;
+        const long long off = (isv ? q - ppt : q) * PIECE;
+        const uint8_t* sp = (isv ? a.ring_src_v[src] : a.ring_src_k[src]) + off;
+        uint8_t* dp = (isv ? dv : dk) + off;
+        const int bytes = (int)min(PIECE, a.shard_bytes - off);
+        for (int v0 = (int)lane * 16; v0 < bytes; v0 += 32 * 16 * V) {
+          uint4 x[V];
+#pragma unroll
+          for (int u = 0; u < V; ++u)
+            if (v0 + u * 512 < bytes) x[u] = ld_v4_cg(sp + v0 + u * 512);
+#pragma unroll
+          for (int u = 0; u < V; ++u)
+            if (v0 + u * 512 < bytes) st_v4(dp + v0 + u * 512, x[u]);
+        }
+      }
+#endif
+      __syncwarp();
+      if (lane == 0) {
+        // my share of step s is written (generic stores): make it visible to
+        // the loaders' TMA reads before counting it
+        __threadfence();
+        fence_async_global();
+        if (atomicAdd(rc.pieces(s), 1u) == (uint32_t)nc - 1)
+          asm volatile("st.release.gpu.global.u32 [%0], %1;" :: "l"(rc.ready(s)), "r"(1u) : "memory");
+      }
+      __syncwarp();
+    }
+    if (lane == 0) {
+      __threadfence();
+      if (atomicAdd(rc.comm_done(), 1u) == (uint32_t)nc - 1) {
+        fence_sys();
+        for (int d = 0; d < a.world; ++d) signal_add(a.done_peer[d] + a.rank, 1u);
+      }
+    }
+    __syncwarp();
+  };
 
   if (is_comm) {
     if (warp == 0 && lane == 0)                       // 192 KB: the Q / K / V buffers, unused here
@@ -734,10 +798,12 @@ __global__ void __launch_bounds__(AT_THREADS, 1) attn_fwd_kernel(const __grid_co
       segx1 += sg.ntile > 1;
       g += len;
     }
-  } else if (warp == 3) {
+  } else if (warp >= 2) {
     // ------------------------------------------------------------ intra-SM ring communicator
-    if constexpr (RING && AT_RING_PIECE > 0) {
-      if (a.ring_comm == 0 && lane == 0)
+    if constexpr (RING && AT_RING_REGCOPY) {
+      if (a.ring_comm == 0) ring_pull_regs((int)blockIdx.x * 2 + ((int)warp - 2), ncompute * 2);
+    } else if constexpr (RING && AT_RING_PIECE > 0) {
+      if (warp == 3 && a.ring_comm == 0 && lane == 0)
         ring_pull((int)blockIdx.x, ncompute, smem + AT_RING_CBUF_OFF, AT_RING_NBUF, AT_RING_PIECE, ring_cbar);
     }
     __syncwarp();
@@ -1663,7 +1729,8 @@ int ring_attn_fwd(Comm* c, const pk_tensor* q, const pk_tensor* k, const pk_tens
   // (669 GB/s saturating at 15 SMs) and ~1.2 PF/s of attention
   // over this rank's SMs. Emulated ranks keep a quarter of their SMs at most.
   int ncomm = 0;
-  const bool inter = (sched && (sched->num_comm_sms > 0 || sched->mode == 1 || sched->mode == 2)) || AT_RING_PIECE == 0;
+  const bool inter = (sched && (sched->num_comm_sms > 0 || sched->mode == 1 || sched->mode == 2)) ||
+                     (!AT_RING_REGCOPY && AT_RING_PIECE == 0);
   if (inter) {
     if (sched && sched->num_comm_sms > 0) {
       ncomm = sched->num_comm_sms;
