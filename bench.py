@@ -735,7 +735,8 @@ def decomposition_leg(pk, comm, dev, n, S, a_ag, b_ag, c_ag, a_rs, b_rs, o_rs, a
 
 def schedule_leg(pk, comm, n, S, a_ag, b_ag, c_ag, a_rs, b_rs, o_rs, barrier, max_over_ranks) -> dict:
     """The reference's autotune_partition (lcsc.py:164-191) on the real ranks:
-    intra-SM vs inter-SM with several communicator-SM counts for AG-GEMM, and
+    intra-SM, hybrid (communicator warps) and inter-SM with several
+    communicator-SM counts for AG-GEMM, and
     intra-SM (bf16 / fp32 partials) vs inter-SM for GEMM-RS, at the timed
     size; device time max over ranks; ties toward fewer communicator SMs. The
     `table` entry is a measured schedule table (tune.ScheduleTable format)."""
@@ -755,7 +756,7 @@ def schedule_leg(pk, comm, n, S, a_ag, b_ag, c_ag, a_rs, b_rs, o_rs, barrier, ma
         return max_over_ranks(e0.elapsed_time(e1) / iters)
     out = {"size": S, "world": n}
     table = tune.ScheduleTable()
-    ag_c = [{"mode": "intra_sm"}] + [{"mode": "inter_sm", "num_comm_sms": k} for k in (4, 8, 16, 24)]
+    ag_c = [{"mode": "intra_sm"}, {"mode": "hybrid"}] + [{"mode": "inter_sm", "num_comm_sms": k} for k in (4, 8, 16, 24)]
     rows = [(sc, timed(lambda: pk.all_gather_gemm(comm, a_ag, b_ag, out=c_ag, schedule=sc))) for sc in ag_c]
     best, t = tune.pick_best(rows)
     table.put("ag_gemm", n, S, S, S, best, ms=round(t, 4), emulated=False, sms_per_rank=comm.num_sms)
