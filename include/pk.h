@@ -218,8 +218,8 @@ PK_API int pk_all_reduce_ablate(pk_comm* comm, pk_tensor* x, uint32_t overheads,
  * rank (r - s) mod n (workloads.py:666-681): one launch whose communicators
  * pull each step's shard into a 2-slot local stage over peer memory while the
  * compute CTAs work on the previous step (step-major units, log-sum-exp merge
- * in ascending step order). Communicators: NULL / mode intra_sm = a comm warp
- * in every compute CTA; mode inter_sm or num_comm_sms > 0 = dedicated CTAs
+ * in ascending step order). Communicators: NULL / mode intra_sm / hybrid = a
+ * comm warp in every compute CTA; mode inter_sm or num_comm_sms > 0 = dedicated CTAs
  * (num_comm_sms, 0 = sized to the link). sched->stages = 2P stage slots:
  * a work unit spans P ring steps (0 = default: 2 slots below n = 8, else 4).
  * k / v may be reused once the call completes on `stream`. */

@@ -1729,8 +1729,9 @@ int ring_attn_fwd(Comm* c, const pk_tensor* q, const pk_tensor* k, const pk_tens
   // (669 GB/s saturating at 15 SMs) and ~1.2 PF/s of attention
   // over this rank's SMs. Emulated ranks keep a quarter of their SMs at most.
   int ncomm = 0;
-  const bool inter = (sched && (sched->num_comm_sms > 0 || sched->mode == 1 || sched->mode == 2)) ||
-                     (!AT_RING_REGCOPY && AT_RING_PIECE == 0);
+  // (intra_sm and hybrid both name the communicator warps here: the ring has
+  // no communicator-free schedule)
+  const bool inter = (sched && (sched->num_comm_sms > 0 || sched->mode == 1)) || (!AT_RING_REGCOPY && AT_RING_PIECE == 0);
   if (inter) {
     if (sched && sched->num_comm_sms > 0) {
       ncomm = sched->num_comm_sms;

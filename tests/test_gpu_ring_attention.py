@@ -58,8 +58,8 @@ def test_ring_attention_matches_oracle(world):
 
 
 @pytest.mark.parametrize("world", [2, 4, 8])
-@pytest.mark.parametrize("schedule", [{"mode": "intra_sm"}, {"mode": "inter_sm"}, {"num_comm_sms": 1}],
-                         ids=["comm-warps", "comm-ctas", "one-comm-cta"])
+@pytest.mark.parametrize("schedule", [{"mode": "intra_sm"}, {"mode": "hybrid"}, {"mode": "inter_sm"}, {"num_comm_sms": 1}],
+                         ids=["comm-warps", "comm-warps-hybrid", "comm-ctas", "one-comm-cta"])
 def test_ring_attention_communicator_modes(world, schedule):
     """Intra-SM (a comm warp in every compute CTA, the default) and inter-SM
     (dedicated communicator CTAs) pulls give the same result; several steps
