@@ -183,6 +183,30 @@ def test_ring_attention_emulated_world8(S_tot):
         c.destroy()
 
 
+@pytest.mark.parametrize("Sq,Skv", [(16384, 16384), (32768, 32768), (16384, 131072), (4096, 32768)])
+def test_single_gpu_attention_full_shape(Sq, Skv):
+    """pk.attention at the BASELINE config-4 shapes (B1 H16 D128): the CTA-pair
+    kernel where its items fill the waves (S_q >= 16384), the single-CTA kernel
+    with its split tail on the rank step; sampled query rows against an fp64
+    reference over all keys."""
+    pk = _pk()
+    B, H, D = 1, 16, 128
+    g = torch.Generator(device="cuda").manual_seed(Sq + Skv)
+    q = torch.randn(B, Sq, H, D, device="cuda", generator=g).bfloat16()
+    k = torch.randn(B, Skv, H, D, device="cuda", generator=g).bfloat16()
+    v = torch.randn(B, Skv, H, D, device="cuda", generator=g).bfloat16()
+    o_got, lse_got = pk.attention(q, k, v)
+    torch.cuda.synchronize()
+    k_all, v_all = k[0].double(), v[0].double()
+    rows = torch.randint(0, Sq, (16,), device="cuda", generator=g)
+    qq = q[0, rows].double()
+    s_ = torch.einsum("qhd,khd->hqk", qq, k_all) * D ** -0.5
+    lse = torch.logsumexp(s_, -1)
+    o = torch.einsum("hqk,khd->qhd", torch.softmax(s_, -1), v_all)
+    assert (o_got[0, rows].double() - o).abs().max().item() <= 2e-2
+    assert (lse_got[0][:, rows].double() - lse).abs().max().item() <= 1e-3 * max(1.0, lse.abs().max().item())
+
+
 @pytest.mark.parametrize("T", [1024, 4096, 16384])
 def test_moe_dispatch_combine_full_shape(T):
     """cfg5 (T 4096, E 64, k 8, H 7168) over an emulated n = 2: every received
